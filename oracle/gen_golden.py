@@ -1,0 +1,176 @@
+"""TEST INFRASTRUCTURE — regenerate tests/golden/*.npz from the UNMODIFIED reference.
+
+Run in the build container (needs /root/reference mounted so that oracle/Makefile can
+compile oracle/_ref/libtemo_ref.so):
+
+    python -m oracle.gen_golden
+
+Every array stored here is an input to, or an output of, the reference's own functions
+(called through oracle/ref_wrap.cpp). The instance generators mirror the reference's
+verification suites (verify.hpp:41-47,53-76,83-103: master seed + instance number, all
+randomness from RngStream) so a fixture can be re-derived from (seed, instance) alone.
+The fixtures are what pins the C restatement (and the CUDA path) on machines where the
+reference is not mounted.
+"""
+from __future__ import annotations
+
+import os
+
+import numpy as np
+
+from .pyoracle import Ref
+
+OUT = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden")
+
+
+class Stream:
+    """RngStream (rng.hpp:34-52) driven through the reference's value_at."""
+
+    def __init__(self, ref, seed, counter=0):
+        self.ref, self.seed, self.counter = ref, seed, counter
+
+    def next(self):
+        v = self.ref.value_at(self.seed, self.counter)
+        self.counter += 1
+        return v
+
+    def pick(self, lo, hi):  # verify.hpp:33-35
+        return lo + int(self.next() * float(hi - lo + 1))
+
+    def tensor(self, rows, cols):
+        out = self.ref.uniform(self.seed, self.counter, rows * cols).reshape(rows, cols)
+        self.counter += rows * cols
+        return out
+
+
+def operator_instance(ref, g, n_min, n_max, d_max):
+    """verify.hpp:83-103 random_operator_instance."""
+    n = g.pick(n_min, n_max)
+    d = g.pick(1, d_max)
+    lower, upper = np.empty(d), np.empty(d)
+    for j in range(d):
+        lower[j] = -1.0 - g.next()
+        upper[j] = lower[j] + 0.5 + 2.0 * g.next()
+    x = g.tensor(n, d)
+    x = lower + x * (upper - lower)
+    return n, d, lower, upper, x
+
+
+def main():
+    ref = Ref()
+    os.makedirs(OUT, exist_ok=True)
+
+    # ---- rng -----------------------------------------------------------------------
+    seeds = np.array([0, 7, 42, 99, 2**63 + 12345], dtype=np.uint64)
+    draws = np.array([[ref.value_at(int(s), k) for k in range(24)] for s in seeds])
+    far = np.array([ref.value_at(42, k) for k in (10**6, 2**32 + 5, 2**40 + 17, 2**63)])
+    perm20, c20 = ref.shuffle_indices(42, 0, 20)
+    perm257, c257 = ref.shuffle_indices(5, 1000, 257)
+    pool, cpool = ref.parent_pool_indices(77, 105, 42, 5000)
+    np.savez(os.path.join(OUT, "rng.npz"), seeds=seeds, draws=draws, far=far,
+             far_k=np.array([10**6, 2**32 + 5, 2**40 + 17, 2**63], dtype=np.uint64),
+             perm20=perm20, c20=c20, perm257=perm257, c257=c257, pool=pool, cpool=cpool)
+
+    # ---- operators (verify.hpp:117-182 instance recipe; test_operators.cpp:63-114 seeds)
+    ops = {}
+    for tag, seed, nmin, nmax, dmax in (("a", 37, 8, 8, 5), ("b", 7002, 2, 16, 8), ("c", 7003, 2, 16, 8),
+                                        ("odd", 8101, 9, 9, 7), ("wide", 8102, 12, 12, 40)):
+        g = Stream(ref, seed)
+        n, d, lower, upper, x = operator_instance(ref, g, nmin, nmax, dmax)
+        sseed = seed ^ 0x5EED
+        sbx, c1 = ref.sbx(x, sseed, 0, lower, upper)
+        pm, c2 = ref.polynomial_mutation(x, sseed, 0, lower, upper)
+        ga, c3 = ref.ga_reproduce(x, sseed, 0, lower, upper)
+        # a high mutation rate instance so the pow branch of PM is exercised on many genes
+        pm_hot, _ = ref.polynomial_mutation(x, sseed, 11, lower, upper, ga=(1.0, 20.0, float(d) * 0.6, 20.0))
+        ga_pc, _ = ref.ga_reproduce(x, sseed, 3, lower, upper, ga=(0.5, 15.0, 2.0, 10.0))
+        for k, v in dict(x=x, lower=lower, upper=upper, sbx=sbx, pm=pm, ga=ga, pm_hot=pm_hot, ga_pc=ga_pc,
+                         counters=np.array([c1, c2, c3], dtype=np.uint64),
+                         seed=np.array([sseed], dtype=np.uint64)).items():
+            ops[f"{tag}_{k}"] = v
+    rr, crr = ref.random_reproduce(5, 7, 42, 3, np.linspace(-1, 0, 7), np.linspace(1, 3, 7))
+    ops["rr"] = rr
+    ops["rr_counter"] = np.array([crr], dtype=np.uint64)
+    np.savez(os.path.join(OUT, "operators.npz"), **ops)
+
+    # ---- problems ------------------------------------------------------------------
+    pr = {}
+    g = Stream(ref, 9100)
+    for m, d in ((3, 12), (2, 7), (5, 30), (10, 25)):
+        x = g.tensor(9, d)
+        x[0, :] = 0.5          # test_problems.cpp:8-33 slices
+        x[1, :] = 0.0
+        x[2, :] = 1.0
+        pr[f"x_m{m}"] = x
+        for pid in (1, 2, 3, 4):
+            pr[f"f{pid}_m{m}"] = ref.evaluate(f"dtlz{pid}", x, m)
+    np.savez(os.path.join(OUT, "problems.npz"), **pr)
+
+    # ---- refvec --------------------------------------------------------------------
+    rv = {}
+    for m, H in ((3, 4), (2, 9), (3, 13), (5, 4), (10, 2)):
+        v0, gamma = ref.make_ref_set(m, H)
+        g = Stream(ref, 9200 + m * 100 + H)
+        zmin = g.tensor(1, m)[0]
+        zmax = zmin + 0.1 + 5.0 * g.tensor(1, m)[0]
+        v1, g1 = ref.adapt(v0, v0, gamma, zmin, zmax)
+        zbad = zmax.copy()
+        zbad[m - 1] = zmin[m - 1]
+        v2, g2 = ref.adapt(v0, v1, g1, zmin, zbad)  # degenerate range: untouched
+        rv.update({f"v0_{m}_{H}": v0, f"gamma_{m}_{H}": gamma, f"zmin_{m}_{H}": zmin, f"zmax_{m}_{H}": zmax,
+                   f"v1_{m}_{H}": v1, f"g1_{m}_{H}": g1, f"v2_{m}_{H}": v2, f"g2_{m}_{H}": g2})
+    rv["density"] = np.array([[m, n, ref.lattice_density_for(m, n)] for m, n in
+                              ((3, 105), (3, 10000), (3, 16384), (3, 131072), (3, 1048576), (10, 65536), (2, 50), (5, 1000))],
+                             dtype=np.uint64)
+    np.savez(os.path.join(OUT, "refvec.npz"), **rv)
+
+    # ---- selection (verify.hpp:53-76 recipe, master seed 7001) ------------------------
+    se = {}
+    count = 0
+    for k in range(40):
+        g = Stream(ref, 7001 + k)
+        n = g.pick(1, 64)
+        m = g.pick(2, 3)
+        H = g.pick(1, 14) if m == 2 else g.pick(1, 4)
+        t_max = g.pick(1, 200)
+        t = g.pick(0, t_max)
+        v0, gamma = ref.make_ref_set(m, H)
+        f = g.tensor(n, m) * 10.0
+        s = ref.rv_select(f, v0, gamma, t, t_max, 2.0)
+        s2 = ref.rv_select(f, v0, gamma, t, t_max, 2.0, set_form=True)
+        assert np.array_equal(s.elite, s2.elite) and np.array_equal(s.validity, s2.validity)
+        se.update({f"f_{k}": f, f"mh_{k}": np.array([m, H, t, t_max], dtype=np.uint64), f"elite_{k}": s.elite,
+                   f"valid_{k}": s.validity, f"assoc_{k}": s.assoc, f"theta_{k}": s.theta, f"apd_{k}": s.apd})
+        count += 1
+    se["count"] = np.array([count])
+    # crafted: duplicates (exact APD ties -> lowest row), a row at the ideal point, adapted vectors
+    v0, gamma = ref.make_ref_set(3, 5)
+    g = Stream(ref, 9300)
+    f = g.tensor(30, 3)
+    f[7] = f[3]
+    f[21] = f[3]
+    f[12] = f.min(axis=0)  # exactly at the ideal point -> nf == 0 -> vector 0, apd 0
+    v1, g1 = ref.adapt(v0, v0, gamma, np.array([0.0, 0.1, 0.2]), np.array([3.0, 1.0, 0.7]))
+    s = ref.rv_select(f, v1, g1, 37, 100, 2.0)
+    se.update(dict(crafted_f=f, crafted_v=v1, crafted_gamma=g1, crafted_elite=s.elite, crafted_valid=s.validity,
+                   crafted_assoc=s.assoc, crafted_apd=s.apd))
+    np.savez(os.path.join(OUT, "selection.npz"), **se)
+
+    # ---- whole pipeline (SURVEY.md §8c goldens; test_algorithms.cpp:198-210 seed 77) ----
+    c1 = ref.rvea_run("dtlz1", 105, 12, 3, 100, seed=42, lattice_h=13)
+    s77 = ref.rvea_run("dtlz2", 12, 8, 3, 10, seed=77, lattice_h=3)
+    s77o = ref.rvea_run("dtlz2", 12, 8, 3, 10, seed=77, lattice_h=3, scalar=True)
+    assert np.array_equal(s77["f"], s77o["f"]) and np.array_equal(s77["x"], s77o["x"])
+    d3 = ref.rvea_run("dtlz3", 64, 20, 4, 30, seed=5)
+    d4 = ref.rvea_run("dtlz4", 50, 10, 2, 25, seed=11)
+    np.savez(os.path.join(OUT, "pipeline.npz"),
+             c1_x=c1["x"], c1_f=c1["f"], c1_pop=c1["pop_size"],
+             s77_x=s77["x"], s77_f=s77["f"], s77_pop=s77["pop_size"],
+             d3_x=d3["x"], d3_f=d3["f"], d3_pop=d3["pop_size"],
+             d4_x=d4["x"], d4_f=d4["f"], d4_pop=d4["pop_size"])
+    total = sum(os.path.getsize(os.path.join(OUT, f)) for f in os.listdir(OUT))
+    print(f"wrote {OUT}: {total/1024:.1f} KiB")
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,481 @@
+"""TEST INFRASTRUCTURE — ctypes front-ends for the two CPU checkers.
+
+``Oracle``  : oracle/libtemo_oracle.so, our plain-C restatement (temo_oracle.c).
+``Ref``     : oracle/_ref/libtemo_ref.so, the UNMODIFIED reference headers compiled by
+              oracle/Makefile through ref_wrap.cpp (present only if it was built in the
+              container that has /root/reference; it travels to the GPU box prebuilt).
+
+Both expose the same numpy-level methods so a parity test can be parametrised over them.
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference legs
+may import this module; the product package never does.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from dataclasses import dataclass
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(HERE, "libtemo_oracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libtemo_ref.so")
+
+u64 = C.c_uint64
+f64p = C.POINTER(C.c_double)
+u64p = C.POINTER(C.c_uint64)
+u8p = C.POINTER(C.c_ubyte)
+
+PROBLEM_IDS = {"dtlz1": 1, "dtlz2": 2, "dtlz3": 3, "dtlz4": 4, "lsmop1": 101}
+GA_DEFAULT = (1.0, 20.0, 1.0, 20.0)  # pc, eta, pm, xi — operators.hpp:22-27
+
+
+def build(force: bool = False) -> None:
+    """Compile the C restatement (always) and the reference shim (when mounted)."""
+    if force or not os.path.exists(ORACLE_SO) or (
+        os.path.getmtime(ORACLE_SO) < os.path.getmtime(os.path.join(HERE, "temo_oracle.c"))
+    ):
+        subprocess.check_call(["make", "-s", "-C", HERE, "libtemo_oracle.so"])
+    ref_src = os.path.join(HERE, "ref_wrap.cpp")
+    if os.path.isdir("/root/reference/proj/include") and (
+        force or not os.path.exists(REF_SO) or os.path.getmtime(REF_SO) < os.path.getmtime(ref_src)
+    ):
+        subprocess.check_call(["make", "-s", "-C", HERE, "_ref/libtemo_ref.so"])
+
+
+def _f(a, dtype=np.float64):
+    return np.ascontiguousarray(a, dtype=dtype)
+
+
+def _p(a, typ=f64p):
+    return None if a is None else a.ctypes.data_as(typ)
+
+
+@dataclass
+class Selection:
+    elite: np.ndarray      # merged-row index per valid vector, ascending vector index
+    validity: np.ndarray   # uint8[r]
+    assoc: np.ndarray | None = None
+    theta: np.ndarray | None = None
+    apd: np.ndarray | None = None
+
+
+class _Base:
+    name = "base"
+
+    # ---- shared numpy-level helpers -------------------------------------------------
+    def take_generation(self, *a, **k):  # pragma: no cover - overridden
+        raise NotImplementedError
+
+
+class Oracle(_Base):
+    """Plain-C restatement (oracle/temo_oracle.c)."""
+
+    name = "oracle"
+
+    def __init__(self):
+        build()
+        self.lib = C.CDLL(ORACLE_SO)
+        L = self.lib
+        L.to_value_at.restype = C.c_double
+        L.to_value_at.argtypes = [u64, u64]
+        L.to_polynomial_delta.restype = C.c_double
+        L.to_polynomial_delta.argtypes = [C.c_double] * 5
+        L.to_apd_penalty.restype = C.c_double
+        L.to_apd_penalty.argtypes = [u64, u64, u64, C.c_double]
+        L.to_lattice_count.restype = u64
+        L.to_lattice_count.argtypes = [u64, u64]
+        L.to_lattice_density_for.restype = u64
+        L.to_lattice_density_for.argtypes = [u64, u64]
+
+    # rng
+    def value_at(self, seed, k):
+        return self.lib.to_value_at(seed, k)
+
+    def uniform(self, seed, counter, count):
+        out = np.empty(count)
+        self.lib.to_uniform_fill(u64(seed), u64(counter), _p(out), u64(count))
+        return out
+
+    def shuffle_indices(self, seed, counter, n):
+        out = np.empty(n, dtype=np.uint64)
+        c = u64(counter)
+        self.lib.to_shuffle_indices(u64(seed), C.byref(c), u64(n), _p(out, u64p))
+        return out, c.value
+
+    def parent_pool_indices(self, current, n, seed, counter):
+        out = np.empty(n, dtype=np.uint64)
+        c = u64(counter)
+        self.lib.to_parent_pool_indices(u64(current), u64(n), u64(seed), C.byref(c), _p(out, u64p))
+        return out, c.value
+
+    # operators
+    def _op(self, fn, x, seed, counter, ga, lower, upper):
+        x = _f(x)
+        n, d = x.shape
+        out = np.empty_like(x)
+        c = u64(counter)
+        g = _f(ga)
+        rc = fn(_p(x), u64(n), u64(d), u64(seed), C.byref(c), _p(g), _p(_f(lower)), _p(_f(upper)), _p(out))
+        if rc not in (0, None):
+            raise RuntimeError(f"oracle operator failed rc={rc}")
+        return out, c.value
+
+    def sbx(self, x, seed, counter, lower, upper, ga=GA_DEFAULT):
+        self.lib.to_sbx.restype = None
+        return self._op(self.lib.to_sbx, x, seed, counter, ga, lower, upper)
+
+    def polynomial_mutation(self, x, seed, counter, lower, upper, ga=GA_DEFAULT):
+        self.lib.to_polynomial_mutation.restype = None
+        return self._op(self.lib.to_polynomial_mutation, x, seed, counter, ga, lower, upper)
+
+    def ga_reproduce(self, x, seed, counter, lower, upper, ga=GA_DEFAULT):
+        self.lib.to_ga_reproduce.restype = C.c_int
+        return self._op(self.lib.to_ga_reproduce, x, seed, counter, ga, lower, upper)
+
+    def random_reproduce(self, n, d, seed, counter, lower, upper):
+        out = np.empty((n, d))
+        c = u64(counter)
+        self.lib.to_random_reproduce(u64(n), u64(d), u64(seed), C.byref(c), _p(_f(lower)), _p(_f(upper)), _p(out))
+        return out, c.value
+
+    def polynomial_delta(self, u, x, lo, hi, xi):
+        return self.lib.to_polynomial_delta(u, x, lo, hi, xi)
+
+    # problems
+    def evaluate(self, problem, x, m):
+        x = _f(x)
+        n, d = x.shape
+        f = np.empty((n, m))
+        pid = PROBLEM_IDS[problem]
+        if pid == 101:
+            rc = self.lib.to_lsmop1_eval(_p(x), u64(n), u64(d), u64(m), _p(f))
+        else:
+            rc = self.lib.to_dtlz_eval(C.c_int(pid), _p(x), u64(n), u64(d), u64(m), _p(f))
+        if rc:
+            raise ValueError(f"evaluate({problem}) rejected its arguments rc={rc}")
+        return f
+
+    def problem_bounds(self, problem, d, m):
+        lo, hi = np.empty(d), np.empty(d)
+        self.lib.to_problem_bounds(C.c_int(PROBLEM_IDS[problem]), u64(d), u64(m), _p(lo), _p(hi))
+        return lo, hi
+
+    # refvec
+    def lattice_count(self, m, H):
+        return self.lib.to_lattice_count(m, H)
+
+    def lattice_density_for(self, m, target):
+        return self.lib.to_lattice_density_for(m, target)
+
+    def simplex_lattice(self, m, H):
+        out = np.empty((self.lattice_count(m, H), m))
+        self.lib.to_simplex_lattice(u64(m), u64(H), _p(out))
+        return out
+
+    def normalize_to_unit(self, v):
+        v = _f(v)
+        out = np.empty_like(v)
+        if self.lib.to_normalize_to_unit(_p(v), u64(v.shape[0]), u64(v.shape[1]), _p(out)):
+            raise ValueError("normalize_to_unit: zero row")
+        return out
+
+    def min_vector_angles(self, v):
+        v = _f(v)
+        g = np.empty(v.shape[0])
+        rc = self.lib.to_min_vector_angles(_p(v), u64(v.shape[0]), u64(v.shape[1]), _p(g))
+        if rc:
+            raise ValueError(f"min_vector_angles rc={rc}")
+        return g
+
+    def make_ref_set(self, m, H):
+        r = self.lattice_count(m, H)
+        v0, g = np.empty((r, m)), np.empty(r)
+        rc = self.lib.to_make_ref_set(u64(m), u64(H), _p(v0), _p(g))
+        if rc:
+            raise ValueError(f"make_ref_set rc={rc}")
+        return v0, g
+
+    def adapt(self, v0, v, gamma, zmin, zmax):
+        v0 = _f(v0)
+        v, gamma = _f(v).copy(), _f(gamma).copy()
+        rc = self.lib.to_adapt(_p(v0), _p(v), _p(gamma), u64(v0.shape[0]), u64(v0.shape[1]), _p(_f(zmin)), _p(_f(zmax)))
+        if rc:
+            raise ValueError(f"adapt rc={rc}")
+        return v, gamma
+
+    # selection
+    def apd_penalty(self, m, t, t_max, alpha):
+        return self.lib.to_apd_penalty(m, t, t_max, alpha)
+
+    def rv_select(self, f, v, gamma, t, t_max, alpha=2.0):
+        f, v, gamma = _f(f), _f(v), _f(gamma)
+        n, m = f.shape
+        r = v.shape[0]
+        elite = np.empty(max(r, 1), dtype=np.uint64)
+        valid = np.empty(r, dtype=np.uint8)
+        assoc = np.empty(n, dtype=np.uint64)
+        theta, apd = np.empty(n), np.empty(n)
+        ne = u64(0)
+        rc = self.lib.to_rv_select(_p(f), u64(n), u64(m), _p(v), _p(gamma), u64(r), u64(t), u64(t_max),
+                                   C.c_double(alpha), _p(elite, u64p), C.byref(ne), _p(valid, u8p),
+                                   _p(assoc, u64p), _p(theta), _p(apd))
+        if rc:
+            raise ValueError(f"rv_select contract violation rc={rc}")
+        return Selection(elite[: ne.value].copy(), valid, assoc, theta, apd)
+
+    # algorithms
+    def generation(self, problem, n, m, seed, counter, lower, upper, t, t_max, alpha, adapt_every,
+                   v0, v, gamma, x, f, ga=GA_DEFAULT):
+        """One generation on explicit state. Returns dict with new x, f, v, gamma, counter,
+        offspring, f_off, elite (merged indices)."""
+        x, f = _f(x), _f(f)
+        P, d = x.shape
+        v0, v, gamma = _f(v0), _f(v).copy(), _f(gamma).copy()
+        r = v0.shape[0]
+        cap = max(P, r, n)
+        xb = np.zeros((cap, d)); xb[:P] = x
+        fb = np.zeros((cap, m)); fb[:P] = f
+        rows = u64(P)
+        c = u64(counter)
+        off, f_off = np.empty((n, d)), np.empty((n, m))
+        elite = np.empty(max(r, P + n), dtype=np.uint64)
+        ne = u64(0)
+        g = _f(ga)
+        rc = self.lib.to_generation(C.c_int(PROBLEM_IDS[problem]), u64(n), u64(d), u64(m), u64(seed), C.byref(c),
+                                    _p(g), _p(_f(lower)), _p(_f(upper)), u64(t), u64(t_max), C.c_double(alpha),
+                                    u64(adapt_every), _p(v0), _p(v), _p(gamma), u64(r), _p(xb), _p(fb),
+                                    C.byref(rows), _p(off), _p(f_off), _p(elite, u64p), C.byref(ne))
+        if rc:
+            raise RuntimeError(f"generation rc={rc}")
+        k = rows.value
+        return dict(x=xb[:k].copy(), f=fb[:k].copy(), v=v, gamma=gamma, counter=c.value,
+                    offspring=off, f_off=f_off, elite=elite[: ne.value].copy())
+
+    def rvea_run(self, problem, n, d, m, generations, seed=42, lattice_h=0, alpha=2.0, fr=0.1, ga=GA_DEFAULT):
+        H = lattice_h or self.lattice_density_for(m, n)
+        r = self.lattice_count(m, H)
+        cap = max(n, r)
+        x, f = np.empty((cap, d)), np.empty((cap, m))
+        rows = u64(0)
+        pops = np.zeros(generations, dtype=np.uint64)
+        v, gamma = np.empty((r, m)), np.empty(r)
+        c = u64(0)
+        g = _f(ga)
+        rc = self.lib.to_rvea_run(C.c_int(PROBLEM_IDS[problem]), u64(n), u64(d), u64(m), u64(lattice_h),
+                                  u64(generations), C.c_double(alpha), C.c_double(fr), u64(seed), _p(g),
+                                  _p(x), _p(f), C.byref(rows), _p(pops, u64p), _p(v), _p(gamma), C.byref(c))
+        if rc:
+            raise RuntimeError(f"rvea_run rc={rc}")
+        k = rows.value
+        return dict(x=x[:k].copy(), f=f[:k].copy(), pop_size=pops, v=v, gamma=gamma, counter=c.value)
+
+
+class Ref(_Base):
+    """The unmodified reference (oracle/_ref/libtemo_ref.so)."""
+
+    name = "reference"
+
+    @staticmethod
+    def available() -> bool:
+        try:
+            build()
+        except Exception:
+            pass
+        return os.path.exists(REF_SO)
+
+    def __init__(self):
+        if not Ref.available():
+            raise FileNotFoundError(REF_SO)
+        self.lib = C.CDLL(REF_SO)
+        L = self.lib
+        L.ref_last_error.restype = C.c_char_p
+        L.ref_value_at.restype = C.c_double
+        L.ref_value_at.argtypes = [u64, u64]
+        L.ref_polynomial_delta.restype = C.c_double
+        L.ref_polynomial_delta.argtypes = [C.c_double] * 5
+        L.ref_apd_penalty.restype = C.c_double
+        L.ref_apd_penalty.argtypes = [u64, u64, u64, C.c_double]
+        for fn in (L.ref_lattice_count, L.ref_lattice_density_for):
+            fn.restype = u64
+            fn.argtypes = [u64, u64]
+        L.ref_num_threads.restype = u64
+
+    def _chk(self, rc):
+        if rc:
+            msg = self.lib.ref_last_error().decode()
+            if rc == -2:
+                raise MemoryError(msg)
+            raise ValueError(msg)
+
+    def num_threads(self):
+        return int(self.lib.ref_num_threads())
+
+    def set_num_threads(self, n):
+        self.lib.ref_set_num_threads(u64(n))
+
+    def value_at(self, seed, k):
+        return self.lib.ref_value_at(seed, k)
+
+    def uniform(self, seed, counter, count):
+        out = np.empty(count)
+        self._chk(self.lib.ref_uniform_fill(u64(seed), u64(counter), _p(out), u64(count), u64(1)))
+        return out
+
+    def shuffle_indices(self, seed, counter, n):
+        out = np.empty(n, dtype=np.uint64)
+        c = u64(counter)
+        self._chk(self.lib.ref_shuffle_indices(u64(seed), C.byref(c), u64(n), _p(out, u64p)))
+        return out, c.value
+
+    def parent_pool_indices(self, current, n, seed, counter):
+        out = np.empty(n, dtype=np.uint64)
+        c = u64(counter)
+        self._chk(self.lib.ref_parent_pool_indices(u64(current), u64(n), u64(seed), C.byref(c), _p(out, u64p)))
+        return out, c.value
+
+    def _op(self, which, x, seed, counter, ga, lower, upper):
+        x = _f(x)
+        n, d = x.shape
+        out = np.empty_like(x)
+        c = u64(counter)
+        g = _f(ga)
+        self._chk(self.lib.ref_operator(C.c_int(which), _p(x), u64(n), u64(d), u64(seed), C.byref(c), _p(g),
+                                        _p(_f(lower)), _p(_f(upper)), _p(out)))
+        return out, c.value
+
+    def sbx(self, x, seed, counter, lower, upper, ga=GA_DEFAULT, scalar=False):
+        return self._op(3 if scalar else 0, x, seed, counter, ga, lower, upper)
+
+    def polynomial_mutation(self, x, seed, counter, lower, upper, ga=GA_DEFAULT, scalar=False):
+        return self._op(4 if scalar else 1, x, seed, counter, ga, lower, upper)
+
+    def ga_reproduce(self, x, seed, counter, lower, upper, ga=GA_DEFAULT, scalar=False):
+        return self._op(5 if scalar else 2, x, seed, counter, ga, lower, upper)
+
+    def random_reproduce(self, n, d, seed, counter, lower, upper):
+        out = np.empty((n, d))
+        c = u64(counter)
+        self._chk(self.lib.ref_random_reproduce(u64(n), u64(d), u64(seed), C.byref(c), _p(_f(lower)), _p(_f(upper)), _p(out)))
+        return out, c.value
+
+    def polynomial_delta(self, u, x, lo, hi, xi):
+        return self.lib.ref_polynomial_delta(u, x, lo, hi, xi)
+
+    def evaluate(self, problem, x, m):
+        pid = PROBLEM_IDS[problem]
+        if pid > 4:
+            raise NotImplementedError("the reference has no LSMOP1")
+        x = _f(x)
+        n, d = x.shape
+        f = np.empty((n, m))
+        self._chk(self.lib.ref_dtlz_eval(C.c_int(pid), _p(x), u64(n), u64(d), u64(m), _p(f)))
+        return f
+
+    def problem_bounds(self, problem, d, m):
+        return np.zeros(d), np.ones(d)  # problems.hpp:271-272
+
+    def dtlz_pf_reference(self, pid, m, H):
+        out = np.empty((self.lattice_count(m, H), m))
+        self._chk(self.lib.ref_dtlz_pf_reference(C.c_int(pid), u64(m), u64(H), _p(out)))
+        return out
+
+    def lattice_count(self, m, H):
+        return self.lib.ref_lattice_count(m, H)
+
+    def lattice_density_for(self, m, target):
+        return self.lib.ref_lattice_density_for(m, target)
+
+    def simplex_lattice(self, m, H):
+        out = np.empty((self.lattice_count(m, H), m))
+        self._chk(self.lib.ref_simplex_lattice(u64(m), u64(H), _p(out)))
+        return out
+
+    def normalize_to_unit(self, v):
+        v = _f(v)
+        out = np.empty_like(v)
+        self._chk(self.lib.ref_normalize_to_unit(_p(v), u64(v.shape[0]), u64(v.shape[1]), _p(out)))
+        return out
+
+    def min_vector_angles(self, v):
+        v = _f(v)
+        g = np.empty(v.shape[0])
+        self._chk(self.lib.ref_min_vector_angles(_p(v), u64(v.shape[0]), u64(v.shape[1]), _p(g)))
+        return g
+
+    def make_ref_set(self, m, H):
+        r = self.lattice_count(m, H)
+        v0, g = np.empty((r, m)), np.empty(r)
+        self._chk(self.lib.ref_make_ref_set(u64(m), u64(H), _p(v0), _p(g)))
+        return v0, g
+
+    def adapt(self, v0, v, gamma, zmin, zmax):
+        v0 = _f(v0)
+        v, gamma = _f(v).copy(), _f(gamma).copy()
+        self._chk(self.lib.ref_adapt(_p(v0), _p(v), _p(gamma), u64(v0.shape[0]), u64(v0.shape[1]), _p(_f(zmin)), _p(_f(zmax))))
+        return v, gamma
+
+    def apd_penalty(self, m, t, t_max, alpha):
+        return self.lib.ref_apd_penalty(m, t, t_max, alpha)
+
+    def rv_select(self, f, v, gamma, t, t_max, alpha=2.0, set_form=False):
+        f, v, gamma = _f(f), _f(v), _f(gamma)
+        n, m = f.shape
+        r = v.shape[0]
+        elite = np.empty(max(r, 1), dtype=np.uint64)
+        valid = np.empty(r, dtype=np.uint8)
+        assoc = np.empty(n, dtype=np.uint64)
+        theta, apd = np.empty(n), np.empty(n)
+        ne = u64(0)
+        self._chk(self.lib.ref_rv_select(C.c_int(1 if set_form else 0), _p(f), u64(n), u64(m), _p(v), _p(gamma),
+                                         u64(r), u64(t), u64(t_max), C.c_double(alpha), _p(elite, u64p),
+                                         C.byref(ne), _p(valid, u8p), _p(assoc, u64p), _p(theta), _p(apd), None))
+        if set_form:
+            return Selection(elite[: ne.value].copy(), valid)
+        return Selection(elite[: ne.value].copy(), valid, assoc, theta, apd)
+
+    def igd(self, f, pf):
+        f, pf = _f(f), _f(pf)
+        out = C.c_double(0)
+        self._chk(self.lib.ref_igd(_p(f), u64(f.shape[0]), u64(f.shape[1]), _p(pf), u64(pf.shape[0]), C.byref(out)))
+        return out.value
+
+    def generation(self, problem, n, m, seed, counter, lower, upper, t, t_max, alpha, adapt_every,
+                   v0, v, gamma, x, f, ga=GA_DEFAULT):
+        """algorithms.hpp:246-281 composed from the reference's own stage functions."""
+        x, f = _f(x), _f(f)
+        P = x.shape[0]
+        pool_idx, c = self.parent_pool_indices(P, n, seed, counter)
+        pool = x[pool_idx.astype(np.int64)]
+        off, c = self.ga_reproduce(pool, seed, c, lower, upper, ga)
+        f_off = self.evaluate(problem, off, m)
+        mx, mf = np.vstack([x, off]), np.vstack([f, f_off])
+        sel = self.rv_select(mf, v, gamma, t, t_max, alpha)
+        e = sel.elite.astype(np.int64)
+        nx, nf = mx[e], mf[e]
+        v, gamma = _f(v).copy(), _f(gamma).copy()
+        if (t + 1) % adapt_every == 0:
+            v, gamma = self.adapt(v0, v, gamma, nf.min(axis=0), nf.max(axis=0))
+        return dict(x=nx, f=nf, v=v, gamma=gamma, counter=c, offspring=off, f_off=f_off, elite=sel.elite)
+
+    def rvea_run(self, problem, n, d, m, generations, seed=42, lattice_h=0, alpha=2.0, fr=0.1, ga=GA_DEFAULT,
+                 scalar=False, time_budget_s=0.0, igd_H=0, want_x=True):
+        H = lattice_h or self.lattice_density_for(m, n)
+        r = self.lattice_count(m, H)
+        cap = max(n, r)
+        x = np.empty((cap, d)) if want_x else None
+        f = np.empty((cap, m))
+        cfg_u = np.array([n, lattice_h, generations, seed, d, m], dtype=np.uint64)
+        cfg_d = np.array([alpha, fr, time_budget_s])
+        rows, done = u64(0), u64(0)
+        pops = np.zeros(generations, dtype=np.uint64)
+        ms = np.zeros(generations)
+        igd = np.full(generations, np.nan)
+        g = _f(ga)
+        self._chk(self.lib.ref_rvea_run(C.c_int(1 if scalar else 0), problem.encode(), _p(cfg_u, u64p), _p(cfg_d),
+                                        _p(g), u64(igd_H), _p(x), _p(f), C.byref(rows), C.byref(done),
+                                        _p(pops, u64p), _p(ms), _p(igd)))
+        k, g_done = rows.value, done.value
+        return dict(x=None if x is None else x[:k].copy(), f=f[:k].copy(), pop_size=pops[:g_done],
+                    elapsed_ms=ms[:g_done], igd=igd[:g_done])

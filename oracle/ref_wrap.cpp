@@ -1,0 +1,297 @@
+// TEST INFRASTRUCTURE — not product code.
+//
+// Thin extern "C" shim that compiles the UNMODIFIED reference headers where
+// they lie (/root/reference/proj/include, passed with -I by oracle/Makefile)
+// into oracle/_ref/libtemo_ref.so. Nothing from the reference is copied into
+// this repository: this file only forwards flat C arrays to the reference's
+// own inline functions and copies their results back out.
+//
+// Users: tests/ (validating the C restatement in temo_oracle.c and checking the
+// CUDA path directly against the real reference), oracle/gen_golden.py (golden
+// fixtures) and bench.py's cpu_baseline / --impl reference legs.
+//
+// Every entry point returns 0 on success, a negative value on a C++ exception
+// (message retrievable with ref_last_error()).
+
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <string>
+#include <vector>
+
+#include "temo/algorithms.hpp"
+#include "temo/metrics.hpp"
+#include "temo/operators.hpp"
+#include "temo/oracle.hpp"
+#include "temo/problems.hpp"
+#include "temo/refvec.hpp"
+#include "temo/rng.hpp"
+#include "temo/selection.hpp"
+
+namespace {
+
+thread_local std::string g_err;
+
+temo::Tensor2D wrap(const double* p, std::size_t r, std::size_t c) {
+    temo::Tensor2D t(r, c);
+    if (r * c) std::memcpy(t.data.data(), p, r * c * sizeof(double));
+    return t;
+}
+
+void unwrap(const temo::Tensor2D& t, double* out) {
+    if (t.size()) std::memcpy(out, t.data.data(), t.size() * sizeof(double));
+}
+
+temo::GaParams ga_of(const double* g) {
+    temo::GaParams p;
+    p.pc = g[0];
+    p.eta = g[1];
+    p.pm = g[2];
+    p.xi = g[3];
+    return p;
+}
+
+template <class F>
+int guarded(F&& body) {
+    try {
+        body();
+        return 0;
+    } catch (const std::bad_alloc&) {
+        g_err = "bad_alloc";
+        return -2;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
+temo::RefVectorSet refs_of(const double* v, const double* gamma, std::size_t r, std::size_t m) {
+    temo::RefVectorSet refs;
+    refs.v0 = wrap(v, r, m);
+    refs.v = refs.v0;
+    refs.gamma = wrap(gamma, r, 1);
+    return refs;
+}
+
+} // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+std::uint64_t ref_num_threads() { return temo::num_threads(); }
+void ref_set_num_threads(std::uint64_t n) { temo::set_num_threads(n); }
+
+// ---- rng.hpp ---------------------------------------------------------------
+double ref_value_at(std::uint64_t seed, std::uint64_t counter) {
+    return temo::RngStream::value_at(seed, counter);
+}
+
+int ref_uniform_fill(std::uint64_t seed, std::uint64_t counter, double* out,
+                     std::uint64_t rows, std::uint64_t cols) {
+    return guarded([&] {
+        temo::RngStream s{seed, counter};
+        unwrap(temo::uniform_tensor(s, rows, cols), out);
+    });
+}
+
+int ref_shuffle_indices(std::uint64_t seed, std::uint64_t* counter, std::uint64_t n,
+                        std::uint64_t* out) {
+    return guarded([&] {
+        temo::RngStream s{seed, *counter};
+        const auto perm = temo::shuffle_indices(s, n);
+        for (std::size_t i = 0; i < n; ++i) out[i] = perm[i];
+        *counter = s.counter;
+    });
+}
+
+int ref_parent_pool_indices(std::uint64_t current, std::uint64_t n, std::uint64_t seed,
+                            std::uint64_t* counter, std::uint64_t* out) {
+    return guarded([&] {
+        temo::RngStream s{seed, *counter};
+        const auto idx = temo::parent_pool_indices(current, n, s);
+        for (std::size_t i = 0; i < n; ++i) out[i] = idx[i];
+        *counter = s.counter;
+    });
+}
+
+// ---- operators.hpp ---------------------------------------------------------
+// which: 0 sbx, 1 polynomial_mutation, 2 ga_reproduce, 3 oracle_sbx, 4 oracle_pm, 5 oracle_ga
+int ref_operator(int which, const double* x, std::uint64_t n, std::uint64_t d,
+                 std::uint64_t seed, std::uint64_t* counter, const double* ga,
+                 const double* lower, const double* upper, double* out) {
+    return guarded([&] {
+        temo::RngStream s{seed, *counter};
+        const temo::Tensor2D xt = wrap(x, n, d);
+        const temo::Tensor2D lo = wrap(lower, 1, d), hi = wrap(upper, 1, d);
+        const temo::GaParams p = ga_of(ga);
+        temo::Tensor2D res;
+        namespace orc = temo::oracle;
+        switch (which) {
+        case 0: res = temo::sbx(xt, s, p, lo, hi); break;
+        case 1: res = temo::polynomial_mutation(xt, s, p, lo, hi); break;
+        case 2: res = temo::ga_reproduce(xt, s, p, lo, hi); break;
+        case 3: res = orc::to_tensor(orc::oracle_sbx(orc::to_matrix(xt), s, p, lo.data, hi.data)); break;
+        case 4: res = orc::to_tensor(orc::oracle_pm(orc::to_matrix(xt), s, p, lo.data, hi.data)); break;
+        case 5: res = orc::to_tensor(orc::oracle_ga(orc::to_matrix(xt), s, p, lo.data, hi.data)); break;
+        default: throw std::invalid_argument("ref_operator: unknown operator id");
+        }
+        unwrap(res, out);
+        *counter = s.counter;
+    });
+}
+
+int ref_random_reproduce(std::uint64_t n, std::uint64_t d, std::uint64_t seed,
+                         std::uint64_t* counter, const double* lower, const double* upper,
+                         double* out) {
+    return guarded([&] {
+        temo::RngStream s{seed, *counter};
+        unwrap(temo::random_reproduce(n, d, s, wrap(lower, 1, d), wrap(upper, 1, d)), out);
+        *counter = s.counter;
+    });
+}
+
+double ref_polynomial_delta(double u, double x, double lo, double hi, double xi) {
+    return temo::polynomial_delta(u, x, lo, hi, xi);
+}
+
+// ---- problems.hpp ----------------------------------------------------------
+int ref_dtlz_eval(int id, const double* x, std::uint64_t n, std::uint64_t d, std::uint64_t m,
+                  double* f) {
+    return guarded([&] { unwrap(temo::dtlz_eval(id, wrap(x, n, d), m), f); });
+}
+
+int ref_dtlz_pf_reference(int id, std::uint64_t m, std::uint64_t H, double* out) {
+    return guarded([&] { unwrap(temo::dtlz_pf_reference(id, m, H), out); });
+}
+
+// ---- refvec.hpp ------------------------------------------------------------
+std::uint64_t ref_lattice_count(std::uint64_t m, std::uint64_t H) {
+    return temo::lattice_count(m, H);
+}
+std::uint64_t ref_lattice_density_for(std::uint64_t m, std::uint64_t target) {
+    return temo::lattice_density_for(m, target);
+}
+
+int ref_simplex_lattice(std::uint64_t m, std::uint64_t H, double* out) {
+    return guarded([&] { unwrap(temo::simplex_lattice(m, H), out); });
+}
+
+int ref_normalize_to_unit(const double* v, std::uint64_t r, std::uint64_t m, double* out) {
+    return guarded([&] { unwrap(temo::normalize_to_unit(wrap(v, r, m)), out); });
+}
+
+int ref_make_ref_set(std::uint64_t m, std::uint64_t H, double* v0, double* gamma) {
+    return guarded([&] {
+        const temo::RefVectorSet refs = temo::make_ref_set(m, H);
+        unwrap(refs.v0, v0);
+        unwrap(refs.gamma, gamma);
+    });
+}
+
+int ref_min_vector_angles(const double* v, std::uint64_t r, std::uint64_t m, double* gamma) {
+    return guarded([&] { unwrap(temo::min_vector_angles(wrap(v, r, m)), gamma); });
+}
+
+// v and gamma are in/out (the reference mutates RefVectorSet in place).
+int ref_adapt(const double* v0, double* v, double* gamma, std::uint64_t r, std::uint64_t m,
+              const double* zmin, const double* zmax) {
+    return guarded([&] {
+        temo::RefVectorSet refs;
+        refs.v0 = wrap(v0, r, m);
+        refs.v = wrap(v, r, m);
+        refs.gamma = wrap(gamma, r, 1);
+        temo::adapt(refs, wrap(zmin, 1, m), wrap(zmax, 1, m));
+        unwrap(refs.v, v);
+        unwrap(refs.gamma, gamma);
+    });
+}
+
+// ---- selection.hpp ---------------------------------------------------------
+// which: 0 rv_select (production, rv_core), 1 oracle_rv_select (argmin-angle set form).
+// Optional outputs (may be NULL): assoc[n], theta[n], apd[n] (rv_core only), table[n*r].
+int ref_rv_select(int which, const double* f, std::uint64_t n, std::uint64_t m, const double* v,
+                  const double* gamma, std::uint64_t r, std::uint64_t t, std::uint64_t t_max,
+                  double alpha, std::uint64_t* elite, std::uint64_t* n_elite,
+                  unsigned char* validity, std::uint64_t* assoc, double* theta, double* apd,
+                  double* table) {
+    return guarded([&] {
+        const temo::Tensor2D ft = wrap(f, n, m);
+        const temo::RefVectorSet refs = refs_of(v, gamma, r, m);
+        const temo::SelectionOutcome out =
+            which == 0 ? temo::rv_select(ft, refs, t, t_max, alpha, table != nullptr)
+                       : temo::oracle::oracle_rv_select(ft, refs, t, t_max, alpha);
+        *n_elite = out.elite_indices.size();
+        for (std::size_t i = 0; i < out.elite_indices.size(); ++i) elite[i] = out.elite_indices[i];
+        for (std::size_t j = 0; j < r; ++j) validity[j] = out.validity[j] ? 1 : 0;
+        if (table && out.apd_table.size()) unwrap(out.apd_table, table);
+        if (which == 0 && (assoc || theta || apd)) {
+            const temo::detail::RvCore core = temo::detail::rv_core(ft, refs, t, t_max, alpha);
+            for (std::size_t i = 0; i < n; ++i) {
+                if (assoc) assoc[i] = core.assoc[i];
+                if (theta) theta[i] = core.theta[i];
+                if (apd) apd[i] = core.apd[i];
+            }
+        }
+    });
+}
+
+double ref_apd_penalty(std::uint64_t m, std::uint64_t t, std::uint64_t t_max, double alpha) {
+    return temo::detail::apd_penalty(m, t, t_max, alpha);
+}
+
+// ---- metrics.hpp -----------------------------------------------------------
+int ref_igd(const double* f, std::uint64_t n, std::uint64_t m, const double* pf,
+            std::uint64_t n_ref, double* out) {
+    return guarded([&] { *out = temo::igd(wrap(f, n, m), wrap(pf, n_ref, m)); });
+}
+
+int ref_hv_mc(const double* f, std::uint64_t n, std::uint64_t m, const double* ref_point,
+              std::uint64_t samples, std::uint64_t seed, double* out) {
+    return guarded([&] {
+        *out = temo::hv_mc(wrap(f, n, m), wrap(ref_point, 1, m), samples, seed).value;
+    });
+}
+
+// ---- algorithms.hpp --------------------------------------------------------
+// which: 0 rvea_run (batched, all lanes), 1 oracle_rvea_run (scalar loops).
+// cfg_u: {pop, lattice_h, generations, seed, dim, obj}; cfg_d: {alpha, fr, time_budget_s};
+// final_x/final_f must hold max(pop, R) rows. rows_* arrays hold `generations` entries.
+// igd_H > 0 -> per-generation IGD against dtlz_pf_reference(id, m, igd_H) of the population.
+int ref_rvea_run(int which, const char* problem, const std::uint64_t* cfg_u, const double* cfg_d,
+                 const double* ga, std::uint64_t igd_H, double* final_x, double* final_f,
+                 std::uint64_t* final_rows, std::uint64_t* rows_done, std::uint64_t* pop_size,
+                 double* elapsed_ms, double* igd_out) {
+    return guarded([&] {
+        temo::RunConfig cfg;
+        cfg.problem = problem;
+        cfg.op = "ga";
+        cfg.pop = cfg_u[0];
+        cfg.lattice_h = cfg_u[1];
+        cfg.generations = cfg_u[2];
+        cfg.seed = cfg_u[3];
+        cfg.dim = cfg_u[4];
+        cfg.obj = cfg_u[5];
+        cfg.alpha = cfg_d[0];
+        cfg.fr = cfg_d[1];
+        cfg.time_budget_s = cfg_d[2];
+        cfg.track_archive = false;
+        cfg.ga = ga_of(ga);
+        const temo::ProblemInstance prob = temo::make_problem(cfg.problem, cfg.dim, cfg.obj);
+        temo::MetricContext mc;
+        if (igd_H > 0) mc.pf_ref = temo::dtlz_pf_reference(prob.dtlz_id, prob.num_obj, igd_H);
+        const temo::RunRecord rec = which == 0 ? temo::rvea_run(prob, cfg, mc)
+                                               : temo::oracle::oracle_rvea_run(prob, cfg, mc);
+        *final_rows = rec.final_x.rows;
+        if (final_x) unwrap(rec.final_x, final_x);
+        if (final_f) unwrap(rec.final_f, final_f);
+        *rows_done = rec.rows.size();
+        for (std::size_t i = 0; i < rec.rows.size(); ++i) {
+            if (pop_size) pop_size[i] = rec.rows[i].pop_size;
+            if (elapsed_ms) elapsed_ms[i] = rec.rows[i].elapsed_ms;
+            if (igd_out) igd_out[i] = rec.rows[i].igd_value;
+        }
+    });
+}
+
+} // extern "C"

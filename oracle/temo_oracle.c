@@ -1,0 +1,581 @@
+/* TEST INFRASTRUCTURE — CPU restatement of the TensorRVEA generation loop.
+ *
+ * This file is the parity ORACLE for the CUDA path in paper_2404_01159_b200/csrc.
+ * It is never linked into, imported by, or called from the product: only tests/,
+ * __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference legs may
+ * load it. It restates, in plain C over flat row-major fp64 arrays, the arithmetic
+ * of the reference (paths relative to /root/reference/proj/include/temo):
+ *
+ *   rng.hpp:23-78            SplitMix64 counter stream, uniform fill, Fisher-Yates
+ *   operators.hpp:65-161     SBX, polynomial mutation, GA reproduction
+ *   operators.hpp:287-296    random_reproduce (initial population)
+ *   problems.hpp:24-92       DTLZ1-4
+ *   refvec.hpp:15-140        lattice, unit vectors, gamma, adaptation
+ *   selection.hpp:82-224     rv_core / rv_select (max-cosine association, APD, elites)
+ *   algorithms.hpp:211-296   parent_pool_indices, rvea_run loop
+ *
+ * Pinning: tests/test_oracle_vs_ref.py checks every function here bit-for-bit
+ * against oracle/_ref/libtemo_ref.so (the unmodified reference compiled by
+ * oracle/Makefile) and tests/test_oracle_golden.py checks it against the committed
+ * fixtures in tests/golden/ (generated from the reference by oracle/gen_golden.py)
+ * and against the known answers in the reference's own tests.
+ * LSMOP1 (to_lsmop1_*) has NO counterpart in the reference: parity unpinned.
+ *
+ * Bit-exactness rules followed throughout (reference: CMakeLists.txt:19-21
+ * -ffp-contract=off; tensor.hpp:143-182 ascending-index accumulation from 0.0):
+ * compile with -ffp-contract=off, accumulate in ascending index order, one
+ * rounding per operation, libm pow/cos/sin/acos exactly where the reference calls them.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define TO_PI 3.141592653589793238462643383279502884 /* std::numbers::pi rounds to the same double */
+
+/* ------------------------------------------------------------------ rng.hpp */
+
+/* rng.hpp:23-30 (Stafford variant 13 finalizer). */
+static uint64_t to_mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+
+/* rng.hpp:39-43: draw k of stream `seed`, top 53 bits scaled into [0,1). */
+double to_value_at(uint64_t seed, uint64_t k) {
+    const uint64_t word = to_mix64(to_mix64(seed) + k * 0x9e3779b97f4a7c15ULL);
+    return (double)(word >> 11) * 0x1.0p-53;
+}
+
+/* rng.hpp:55-66: element e of a block starting at `counter` uses counter+e. */
+void to_uniform_fill(uint64_t seed, uint64_t counter, double* out, uint64_t count) {
+    for (uint64_t e = 0; e < count; ++e) out[e] = to_value_at(seed, counter + e);
+}
+
+/* rng.hpp:69-78: Fisher-Yates from the top index down, n-1 draws. */
+void to_shuffle_indices(uint64_t seed, uint64_t* counter, uint64_t n, uint64_t* perm) {
+    for (uint64_t i = 0; i < n; ++i) perm[i] = i;
+    uint64_t c = *counter;
+    for (uint64_t i = n; i-- > 1;) {
+        const uint64_t j = (uint64_t)(to_value_at(seed, c++) * (double)(i + 1));
+        const uint64_t tmp = perm[i];
+        perm[i] = perm[j];
+        perm[j] = tmp;
+    }
+    *counter = c;
+}
+
+/* algorithms.hpp:211-221: identity when the population already has n rows
+ * (no draws), else n draws sampling with replacement. */
+void to_parent_pool_indices(uint64_t current, uint64_t n, uint64_t seed, uint64_t* counter,
+                            uint64_t* idx) {
+    if (current == n) {
+        for (uint64_t i = 0; i < n; ++i) idx[i] = i;
+        return;
+    }
+    uint64_t c = *counter;
+    for (uint64_t i = 0; i < n; ++i) idx[i] = (uint64_t)(to_value_at(seed, c++) * (double)current);
+    *counter = c;
+}
+
+/* ------------------------------------------------------------- tensor.hpp */
+
+static double to_step(double x) { return x >= 0.0 ? 1.0 : 0.0; }   /* tensor.hpp:76 */
+static double to_sign(double x) { return x >= 0.0 ? 1.0 : -1.0; }  /* tensor.hpp:73 */
+static double to_clip(double x, double lo, double hi) {            /* tensor.hpp:85-87 */
+    return x < lo ? lo : (x > hi ? hi : x);
+}
+static double to_acos_clamped(double c) {                          /* tensor.hpp:79-83 */
+    if (c > 1.0) c = 1.0;
+    if (c < -1.0) c = -1.0;
+    return acos(c);
+}
+
+/* ---------------------------------------------------------- operators.hpp */
+
+/* ga = {pc, eta, pm, xi} (operators.hpp:22-27). */
+
+/* operators.hpp:65-102. Draw blocks in order: Mc, R1, R2 (half x d each), R3 (half). */
+void to_sbx(const double* x, uint64_t n, uint64_t d, uint64_t seed, uint64_t* counter,
+            const double* ga, const double* lower, const double* upper, double* out) {
+    const uint64_t half = n / 2;
+    const uint64_t c_mc = *counter, c_r1 = c_mc + half * d, c_r2 = c_r1 + half * d,
+                   c_r3 = c_r2 + half * d;
+    const double pc = ga[0], eta = ga[1];
+    const double inv_exp = 1.0 / (eta + 1.0);
+    for (uint64_t p = 0; p < half; ++p) {
+        const double* pa = x + p * d;
+        const double* pb = x + (half + p) * d;
+        double* ca = out + p * d;
+        double* cb = out + (half + p) * d;
+        const double hc = to_step(to_value_at(seed, c_r3 + p) - pc);
+        for (uint64_t j = 0; j < d; ++j) {
+            const uint64_t e = p * d + j;
+            const double mc = to_value_at(seed, c_mc + e);
+            const double low = pow(2.0 * mc, inv_exp);
+            const double high = pow(2.0 - 2.0 * mc, -inv_exp);
+            const double hm = to_step(0.5 - mc);
+            double beta = to_sign(to_value_at(seed, c_r1 + e) - 0.5) * (hm * low + (1.0 - hm) * high);
+            const double hr = to_step(to_value_at(seed, c_r2 + e) - 0.5);
+            beta = (1.0 - hc) * ((1.0 - hr) * beta + hr) + hc;
+            ca[j] = to_clip(((1.0 + beta) * pa[j] + (1.0 - beta) * pb[j]) / 2.0, lower[j], upper[j]);
+            cb[j] = to_clip(((1.0 - beta) * pa[j] + (1.0 + beta) * pb[j]) / 2.0, lower[j], upper[j]);
+        }
+    }
+    if (n & 1) memcpy(out + (n - 1) * d, x + (n - 1) * d, d * sizeof(double)); /* :98-100 */
+    *counter = c_r3 + half;
+}
+
+/* operators.hpp:106-121: both branches are always evaluated and blended by steps. */
+double to_polynomial_delta(double u, double x, double lo, double hi, double xi) {
+    const double range = hi - lo;
+    const double e = xi + 1.0, inv_e = 1.0 / e;
+    const double near_lo = 1.0 - (x - lo) / range;
+    const double d_lo = range * (pow(2.0 * u + (1.0 - 2.0 * u) * pow(near_lo, e), inv_e) - 1.0);
+    const double near_hi = 1.0 - (hi - x) / range;
+    const double d_hi =
+        range * (1.0 - pow(2.0 * (1.0 - u) + 2.0 * (u - 0.5) * pow(near_hi, e), inv_e));
+    return d_lo * to_step(0.5 - u) + d_hi * to_step(u - 0.5);
+}
+
+/* operators.hpp:126-149. Draw blocks: R4 (mask), Mmut, n x d each. */
+void to_polynomial_mutation(const double* x, uint64_t n, uint64_t d, uint64_t seed,
+                            uint64_t* counter, const double* ga, const double* lower,
+                            const double* upper, double* out) {
+    const uint64_t c_mask = *counter, c_mut = c_mask + n * d;
+    const double rate = ga[2] / (double)d, xi = ga[3];
+    for (uint64_t e = 0; e < n * d; ++e) {
+        const uint64_t j = e % d;
+        const double xv = x[e];
+        if (to_step(rate - to_value_at(seed, c_mask + e)) == 0.0 || upper[j] - lower[j] <= 0.0) {
+            out[e] = xv;
+            continue;
+        }
+        const double delta = to_polynomial_delta(to_value_at(seed, c_mut + e), xv, lower[j], upper[j], xi);
+        out[e] = to_clip(xv + delta, lower[j], upper[j]);
+    }
+    *counter = c_mut + n * d;
+}
+
+/* operators.hpp:153-161: shuffle -> gather -> sbx -> pm. */
+int to_ga_reproduce(const double* x, uint64_t n, uint64_t d, uint64_t seed, uint64_t* counter,
+                    const double* ga, const double* lower, const double* upper, double* out) {
+    uint64_t* perm = (uint64_t*)malloc(n * sizeof(uint64_t));
+    double* mates = (double*)malloc(n * d * sizeof(double));
+    double* crossed = (double*)malloc(n * d * sizeof(double));
+    if (!perm || !mates || !crossed) { free(perm); free(mates); free(crossed); return -2; }
+    to_shuffle_indices(seed, counter, n, perm);
+    for (uint64_t i = 0; i < n; ++i) memcpy(mates + i * d, x + perm[i] * d, d * sizeof(double));
+    to_sbx(mates, n, d, seed, counter, ga, lower, upper, crossed);
+    to_polynomial_mutation(crossed, n, d, seed, counter, ga, lower, upper, out);
+    free(perm); free(mates); free(crossed);
+    return 0;
+}
+
+/* operators.hpp:287-296. */
+void to_random_reproduce(uint64_t n, uint64_t d, uint64_t seed, uint64_t* counter,
+                         const double* lower, const double* upper, double* out) {
+    const uint64_t c = *counter;
+    for (uint64_t i = 0; i < n; ++i)
+        for (uint64_t j = 0; j < d; ++j)
+            out[i * d + j] = lower[j] + to_value_at(seed, c + i * d + j) * (upper[j] - lower[j]);
+    *counter = c + n * d;
+}
+
+/* ----------------------------------------------------------- problems.hpp */
+
+/* problems.hpp:69-92 with the g and shape helpers of :24-64 folded in. */
+int to_dtlz_eval(int id, const double* x, uint64_t n, uint64_t d, uint64_t m, double* f) {
+    if (id < 1 || id > 4 || m < 2 || d < m) return -1;
+    const double half_pi = TO_PI / 2.0;
+    double* pos = (double*)malloc((m - 1) * sizeof(double));
+    if (!pos) return -2;
+    for (uint64_t r = 0; r < n; ++r) {
+        const double* row = x + r * d;
+        double* fr = f + r * m;
+        for (uint64_t j = 0; j + 1 < m; ++j) pos[j] = id == 4 ? pow(row[j], 100.0) : row[j];
+        double g;
+        if (id == 1 || id == 3) { /* :24-32 */
+            g = (double)(d - m + 1);
+            for (uint64_t i = m - 1; i < d; ++i) {
+                const double t = row[i] - 0.5;
+                g += t * t - cos(20.0 * TO_PI * t);
+            }
+            g = 100.0 * g;
+        } else { /* :34-41 */
+            g = 0.0;
+            for (uint64_t i = m - 1; i < d; ++i) {
+                const double t = row[i] - 0.5;
+                g += t * t;
+            }
+        }
+        for (uint64_t j = 0; j < m; ++j) {
+            double v;
+            if (id == 1) { /* :44-52 linear front */
+                v = 0.5 * (1.0 + g);
+                for (uint64_t i = 0; i + j + 1 < m; ++i) v *= pos[i];
+                if (j > 0) v *= 1.0 - pos[m - 1 - j];
+            } else { /* :55-64 spherical front */
+                v = 1.0 + g;
+                for (uint64_t i = 0; i + j + 1 < m; ++i) v *= cos(pos[i] * half_pi);
+                if (j > 0) v *= sin(pos[m - 1 - j] * half_pi);
+            }
+            fr[j] = v;
+        }
+    }
+    free(pos);
+    return 0;
+}
+
+/* LSMOP1 — NOT in the reference: PARITY UNPINNED.
+ * Definition restated from the LSMOP suite (Cheng, Jin, Olhofer, Sendhoff 2017,
+ * "Test problems for large-scale multiobjective and many-objective optimization"),
+ * as popularised by PlatEMO: nk = 5 sub-components per group; group sizes from the
+ * logistic map c_1 = 3.8*0.1*0.9, c_i = 3.8 c_{i-1}(1-c_{i-1}); linear linkage
+ * x'_j = (1 + j/d) x_j - 10 x_1 for the tail genes (1-based j = m..d); every group
+ * uses the sphere basic function; linear front f_i = (1+g_i) prod x_k (1 - x_{m-i+1}).
+ * Tail bounds are [0,10], position bounds [0,1]. */
+void to_lsmop1_layout(uint64_t d, uint64_t m, uint64_t* sublen /* m */, uint64_t* start /* m+1 */) {
+    double c[64];
+    double sum = 0.0;
+    c[0] = 3.8 * 0.1 * (1.0 - 0.1);
+    for (uint64_t i = 1; i < m; ++i) c[i] = 3.8 * c[i - 1] * (1.0 - c[i - 1]);
+    for (uint64_t i = 0; i < m; ++i) sum += c[i];
+    start[0] = 0;
+    for (uint64_t i = 0; i < m; ++i) {
+        sublen[i] = (uint64_t)floor(c[i] / sum * (double)(d - m + 1) / 5.0);
+        start[i + 1] = start[i] + sublen[i] * 5;
+    }
+}
+
+void to_lsmop1_bounds(uint64_t d, uint64_t m, double* lower, double* upper) {
+    for (uint64_t j = 0; j < d; ++j) {
+        lower[j] = 0.0;
+        upper[j] = j + 1 < m ? 1.0 : 10.0;
+    }
+}
+
+int to_lsmop1_eval(const double* x, uint64_t n, uint64_t d, uint64_t m, double* f) {
+    if (m < 2 || m > 64 || d < m) return -1;
+    uint64_t sublen[64], start[65];
+    to_lsmop1_layout(d, m, sublen, start);
+    for (uint64_t r = 0; r < n; ++r) {
+        const double* row = x + r * d;
+        double* fr = f + r * m;
+        for (uint64_t i = 0; i < m; ++i) {
+            /* group i covers tail genes (0-based) m-1+start[i] .. m-1+start[i+1]-1; the nk
+             * sub-blocks are contiguous so their spheres add up in ascending gene order. */
+            double g = 0.0;
+            for (uint64_t q = start[i]; q < start[i + 1]; ++q) {
+                const uint64_t j = m - 1 + q; /* 0-based gene; 1-based index j+1 */
+                const double y = (1.0 + (double)(j + 1) / (double)d) * row[j] - 10.0 * row[0];
+                g += y * y;
+            }
+            g = sublen[i] ? g / (double)sublen[i] / 5.0 : 0.0;
+            double v = 1.0 + g;
+            for (uint64_t k = 0; k + i + 1 < m; ++k) v *= row[k];
+            if (i > 0) v *= 1.0 - row[m - 1 - i];
+            fr[i] = v;
+        }
+    }
+    return 0;
+}
+
+/* ------------------------------------------------------------- refvec.hpp */
+
+/* refvec.hpp:15-19: C(H+m-1, m-1) by the incremental product. */
+uint64_t to_lattice_count(uint64_t m, uint64_t H) {
+    uint64_t c = 1;
+    for (uint64_t i = 1; i < m; ++i) c = c * (H + i) / i;
+    return c;
+}
+
+/* refvec.hpp:22-35: closest lattice size, ties -> smaller H, stop once size >= target. */
+uint64_t to_lattice_density_for(uint64_t m, uint64_t target) {
+    uint64_t best_h = 1, best_gap = UINT64_MAX;
+    for (uint64_t h = 1; h < 100000; ++h) {
+        const uint64_t c = to_lattice_count(m, h);
+        const uint64_t gap = c > target ? c - target : target - c;
+        if (gap < best_gap) { best_gap = gap; best_h = h; }
+        if (c >= target) break;
+    }
+    return best_h;
+}
+
+/* refvec.hpp:40-62: compositions of H into m parts, lexicographic with every
+ * part descending from what is left; emitted iteratively instead of recursively. */
+void to_simplex_lattice(uint64_t m, uint64_t H, double* out) {
+    uint64_t* part = (uint64_t*)calloc(m, sizeof(uint64_t));
+    part[0] = H; /* first row (H,0,...,0) */
+    uint64_t row = 0;
+    for (;;) {
+        for (uint64_t j = 0; j < m; ++j) out[row * m + j] = (double)part[j] / (double)H;
+        ++row;
+        /* next composition: find the right-most position before the last that is
+         * still positive, decrement it, and dump the remainder right after it. */
+        uint64_t tail = part[m - 1];
+        part[m - 1] = 0;
+        uint64_t k = m - 1;
+        while (k > 0 && part[k - 1] == 0) --k;
+        if (k == 0) break;
+        part[k - 1] -= 1;
+        part[k] = tail + 1; /* the whole remainder goes to position k, later ones stay 0 */
+    }
+    free(part);
+}
+
+/* refvec.hpp:65-75. Returns -1 on a zero row. */
+int to_normalize_to_unit(const double* v, uint64_t r, uint64_t m, double* out) {
+    for (uint64_t i = 0; i < r; ++i) {
+        double s = 0.0;
+        for (uint64_t k = 0; k < m; ++k) s += v[i * m + k] * v[i * m + k];
+        const double norm = sqrt(s);
+        if (!(norm > 0.0)) return -1;
+        for (uint64_t k = 0; k < m; ++k) out[i * m + k] = v[i * m + k] / norm;
+    }
+    return 0;
+}
+
+static void to_row_norms(const double* a, uint64_t r, uint64_t m, double* out) { /* tensor.hpp:171-182 */
+    for (uint64_t i = 0; i < r; ++i) {
+        double s = 0.0;
+        for (uint64_t k = 0; k < m; ++k) s += a[i * m + k] * a[i * m + k];
+        out[i] = sqrt(s);
+    }
+}
+
+/* refvec.hpp:81-100, streamed: the reference materialises cos = V V^T (tensor.hpp:145-161,
+ * ascending k from 0.0) and then scans it; scanning pair by pair performs the same
+ * operations in the same order without the R x R matrix. Returns -1 if any gamma <= 0. */
+int to_min_vector_angles(const double* v, uint64_t r, uint64_t m, double* gamma) {
+    if (r < 2) return -3;
+    double* norms = (double*)malloc(r * sizeof(double));
+    if (!norms) return -2;
+    to_row_norms(v, r, m, norms);
+    int bad = 0;
+    for (uint64_t i = 0; i < r; ++i) {
+        double best = -INFINITY;
+        for (uint64_t j = 0; j < r; ++j) {
+            if (j == i) continue;
+            double dot = 0.0;
+            for (uint64_t k = 0; k < m; ++k) dot += v[i * m + k] * v[j * m + k];
+            const double c = dot / (norms[i] * norms[j]);
+            if (c > best) best = c;
+        }
+        gamma[i] = to_acos_clamped(best);
+        if (!(gamma[i] > 0.0)) bad = 1;
+    }
+    free(norms);
+    return bad ? -1 : 0;
+}
+
+/* refvec.hpp:108-114. v0 and v start identical. */
+int to_make_ref_set(uint64_t m, uint64_t H, double* v0, double* gamma) {
+    const uint64_t r = to_lattice_count(m, H);
+    double* lat = (double*)malloc(r * m * sizeof(double));
+    if (!lat) return -2;
+    to_simplex_lattice(m, H, lat);
+    int rc = to_normalize_to_unit(lat, r, m, v0);
+    free(lat);
+    if (rc) return rc;
+    return to_min_vector_angles(v0, r, m, gamma);
+}
+
+/* refvec.hpp:119-140: skipped (v, gamma untouched) unless every range is > 0. */
+int to_adapt(const double* v0, double* v, double* gamma, uint64_t r, uint64_t m,
+             const double* zmin, const double* zmax) {
+    for (uint64_t k = 0; k < m; ++k)
+        if (!(zmax[k] > zmin[k])) return 0;
+    double* scaled = (double*)malloc(r * m * sizeof(double));
+    if (!scaled) return -2;
+    for (uint64_t i = 0; i < r; ++i)
+        for (uint64_t k = 0; k < m; ++k) scaled[i * m + k] = v0[i * m + k] * (zmax[k] - zmin[k]);
+    int rc = to_normalize_to_unit(scaled, r, m, v);
+    free(scaled);
+    if (rc) return rc;
+    return to_min_vector_angles(v, r, m, gamma);
+}
+
+/* ---------------------------------------------------------- selection.hpp */
+
+/* selection.hpp:86-89. */
+double to_apd_penalty(uint64_t m, uint64_t t, uint64_t t_max, double alpha) {
+    return (double)m * pow((double)t / (double)t_max, alpha);
+}
+
+/* selection.hpp:148-224 (rv_core + rv_select, want_table = false).
+ * Outputs assoc/theta/apd are optional (NULL to skip). Returns -1 on a contract
+ * violation (non-positive gamma, t_max == 0), like detail::require. */
+int to_rv_select(const double* f, uint64_t n, uint64_t m, const double* v, const double* gamma,
+                 uint64_t r, uint64_t t, uint64_t t_max, double alpha, uint64_t* elite,
+                 uint64_t* n_elite, unsigned char* validity, uint64_t* assoc_out,
+                 double* theta_out, double* apd_out) {
+    if (t_max < 1 || n < 1) return -1;
+    for (uint64_t j = 0; j < r; ++j)
+        if (!(gamma[j] > 0.0)) return -1;
+    double* z = (double*)malloc(m * sizeof(double));
+    double* fp = (double*)malloc(m * sizeof(double));
+    double* vn = (double*)malloc(r * sizeof(double));
+    double* apd = (double*)malloc(n * sizeof(double));
+    uint64_t* assoc = (uint64_t*)malloc(n * sizeof(uint64_t));
+    uint64_t* best = (uint64_t*)calloc(r, sizeof(uint64_t));
+    if (!z || !fp || !vn || !apd || !assoc || !best) return -2;
+    /* ideal point: tensor.hpp:211-219 */
+    for (uint64_t k = 0; k < m; ++k) z[k] = f[k];
+    for (uint64_t i = 1; i < n; ++i)
+        for (uint64_t k = 0; k < m; ++k)
+            if (f[i * m + k] < z[k]) z[k] = f[i * m + k];
+    to_row_norms(v, r, m, vn);
+    const double penalty = to_apd_penalty(m, t, t_max, alpha);
+    for (uint64_t i = 0; i < n; ++i) {
+        double s = 0.0;
+        for (uint64_t k = 0; k < m; ++k) {
+            fp[k] = f[i * m + k] - z[k];
+            s += fp[k] * fp[k];
+        }
+        const double nf = sqrt(s);
+        uint64_t arg = 0;
+        double theta = 0.0; /* a row at the ideal point: angle 0, vector 0 (:167-169) */
+        if (nf != 0.0) {
+            double top = -INFINITY;
+            for (uint64_t j = 0; j < r; ++j) {
+                double dot = 0.0;
+                for (uint64_t k = 0; k < m; ++k) dot += fp[k] * v[j * m + k];
+                const double c = dot / (nf * vn[j]);
+                if (c > top) { top = c; arg = j; } /* first strict maximum wins */
+            }
+            theta = to_acos_clamped(top);
+        }
+        assoc[i] = arg;
+        apd[i] = (1.0 + penalty * (theta / gamma[arg])) * nf; /* :82-84 */
+        if (assoc_out) assoc_out[i] = arg;
+        if (theta_out) theta_out[i] = theta;
+        if (apd_out) apd_out[i] = apd[i];
+    }
+    /* :206-217: lowest row index among the minimal APD of each vector. */
+    memset(validity, 0, r);
+    for (uint64_t i = 0; i < n; ++i) {
+        const uint64_t j = assoc[i];
+        if (!validity[j] || apd[i] < apd[best[j]]) { best[j] = i; validity[j] = 1; }
+    }
+    uint64_t cnt = 0;
+    for (uint64_t j = 0; j < r; ++j)
+        if (validity[j]) elite[cnt++] = best[j];
+    *n_elite = cnt;
+    free(z); free(fp); free(vn); free(apd); free(assoc); free(best);
+    return 0;
+}
+
+/* --------------------------------------------------------- algorithms.hpp */
+
+/* Problem ids: 1..4 DTLZ1-4 (problems.hpp:261-278), 101 LSMOP1 (unpinned). */
+static int to_evaluate(int problem, const double* x, uint64_t n, uint64_t d, uint64_t m, double* f) {
+    if (problem >= 1 && problem <= 4) return to_dtlz_eval(problem, x, n, d, m, f);
+    if (problem == 101) return to_lsmop1_eval(x, n, d, m, f);
+    return -1;
+}
+
+void to_problem_bounds(int problem, uint64_t d, uint64_t m, double* lower, double* upper) {
+    if (problem == 101) { to_lsmop1_bounds(d, m, lower, upper); return; }
+    for (uint64_t j = 0; j < d; ++j) { lower[j] = 0.0; upper[j] = 1.0; }
+}
+
+/* One generation of algorithms.hpp:246-281 on explicit state, used by the lock-step
+ * parity tests. In/out: x (rows_cap x d), f (rows_cap x m), *rows, v, gamma, *counter.
+ * Optional outputs: offspring (n x d), f_off (n x m), elite (merged indices, <= r). */
+int to_generation(int problem, uint64_t n, uint64_t d, uint64_t m, uint64_t seed, uint64_t* counter,
+                  const double* ga, const double* lower, const double* upper, uint64_t t,
+                  uint64_t t_max, double alpha, uint64_t adapt_every, const double* v0, double* v,
+                  double* gamma, uint64_t r, double* x, double* f, uint64_t* rows,
+                  double* offspring_out, double* f_off_out, uint64_t* elite_out,
+                  uint64_t* n_elite_out) {
+    const uint64_t P = *rows;
+    uint64_t* pool_idx = (uint64_t*)malloc(n * sizeof(uint64_t));
+    double* pool = (double*)malloc(n * d * sizeof(double));
+    double* merged_x = (double*)malloc((P + n) * d * sizeof(double));
+    double* merged_f = (double*)malloc((P + n) * m * sizeof(double));
+    uint64_t* elite = (uint64_t*)malloc((r > P + n ? r : P + n) * sizeof(uint64_t));
+    unsigned char* valid = (unsigned char*)malloc(r);
+    if (!pool_idx || !pool || !merged_x || !merged_f || !elite || !valid) return -2;
+    int rc = 0;
+    to_parent_pool_indices(P, n, seed, counter, pool_idx);                       /* :247 */
+    for (uint64_t i = 0; i < n; ++i) memcpy(pool + i * d, x + pool_idx[i] * d, d * sizeof(double)); /* :248 */
+    memcpy(merged_x, x, P * d * sizeof(double));                                  /* :274 parents first */
+    memcpy(merged_f, f, P * m * sizeof(double));
+    double* off = merged_x + P * d;
+    double* f_off = merged_f + P * m;
+    rc = to_ga_reproduce(pool, n, d, seed, counter, ga, lower, upper, off);      /* :252 */
+    if (!rc) rc = to_evaluate(problem, off, n, d, m, f_off);                      /* :273 */
+    uint64_t cnt = 0;
+    if (!rc) rc = to_rv_select(merged_f, P + n, m, v, gamma, r, t, t_max, alpha, elite, &cnt, valid,
+                               NULL, NULL, NULL);                                 /* :276-277 */
+    if (!rc) {
+        if (offspring_out) memcpy(offspring_out, off, n * d * sizeof(double));
+        if (f_off_out) memcpy(f_off_out, f_off, n * m * sizeof(double));
+        for (uint64_t k = 0; k < cnt; ++k) {                                      /* :278-279 */
+            memcpy(x + k * d, merged_x + elite[k] * d, d * sizeof(double));
+            memcpy(f + k * m, merged_f + elite[k] * m, m * sizeof(double));
+            if (elite_out) elite_out[k] = elite[k];
+        }
+        *rows = cnt;
+        if (n_elite_out) *n_elite_out = cnt;
+        if ((t + 1) % adapt_every == 0) {                                         /* :281 */
+            double zmin[64], zmax[64];
+            for (uint64_t k = 0; k < m; ++k) zmin[k] = zmax[k] = f[k];
+            for (uint64_t i = 1; i < cnt; ++i)
+                for (uint64_t k = 0; k < m; ++k) {
+                    if (f[i * m + k] < zmin[k]) zmin[k] = f[i * m + k];
+                    if (f[i * m + k] > zmax[k]) zmax[k] = f[i * m + k];
+                }
+            rc = to_adapt(v0, v, gamma, r, m, zmin, zmax);
+        }
+    }
+    free(pool_idx); free(pool); free(merged_x); free(merged_f); free(elite); free(valid);
+    return rc;
+}
+
+/* algorithms.hpp:227-296 with track_archive = false and the GA operator.
+ * x_out/f_out need max(n, r) rows. pop_size[generations] receives the survivor counts. */
+int to_rvea_run(int problem, uint64_t n, uint64_t d, uint64_t m, uint64_t lattice_h,
+                uint64_t generations, double alpha, double fr, uint64_t seed, const double* ga,
+                double* x_out, double* f_out, uint64_t* rows_out, uint64_t* pop_size,
+                double* v_out, double* gamma_out, uint64_t* counter_out) {
+    if (n < 2 || generations < 1 || m > 64) return -1;
+    const uint64_t H = lattice_h ? lattice_h : to_lattice_density_for(m, n); /* :233-235 */
+    const uint64_t r = to_lattice_count(m, H);
+    const uint64_t cap = n > r ? n : r;
+    double* v0 = (double*)malloc(r * m * sizeof(double));
+    double* v = (double*)malloc(r * m * sizeof(double));
+    double* gamma = (double*)malloc(r * sizeof(double));
+    double* lower = (double*)malloc(d * sizeof(double));
+    double* upper = (double*)malloc(d * sizeof(double));
+    double* x = (double*)malloc(cap * d * sizeof(double));
+    double* f = (double*)malloc(cap * m * sizeof(double));
+    if (!v0 || !v || !gamma || !lower || !upper || !x || !f) return -2;
+    int rc = to_make_ref_set(m, H, v0, gamma); /* :236 */
+    memcpy(v, v0, r * m * sizeof(double));
+    double ae = ceil(fr * (double)generations); /* :237-239 */
+    uint64_t adapt_every = ae < 1.0 ? 1 : (uint64_t)ae;
+    to_problem_bounds(problem, d, m, lower, upper);
+    uint64_t counter = 0, rows = n;
+    if (!rc) {
+        to_random_reproduce(n, d, seed, &counter, lower, upper, x); /* :241 */
+        rc = to_evaluate(problem, x, n, d, m, f);                   /* :242 */
+    }
+    for (uint64_t t = 0; !rc && t < generations; ++t) {
+        rc = to_generation(problem, n, d, m, seed, &counter, ga, lower, upper, t, generations, alpha,
+                           adapt_every, v0, v, gamma, r, x, f, &rows, NULL, NULL, NULL, NULL);
+        if (pop_size) pop_size[t] = rows;
+    }
+    if (!rc) {
+        memcpy(x_out, x, rows * d * sizeof(double));
+        memcpy(f_out, f, rows * m * sizeof(double));
+        *rows_out = rows;
+        if (v_out) memcpy(v_out, v, r * m * sizeof(double));
+        if (gamma_out) memcpy(gamma_out, gamma, r * sizeof(double));
+        if (counter_out) *counter_out = counter;
+    }
+    free(v0); free(v); free(gamma); free(lower); free(upper); free(x); free(f);
+    return rc;
+}

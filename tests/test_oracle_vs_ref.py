@@ -1,0 +1,103 @@
+"""CPU: the C restatement against the UNMODIFIED reference compiled into
+oracle/_ref/libtemo_ref.so, on the reference's own randomized suites (verify.hpp master
+seeds 7001/7002). Everything is compared bit-for-bit. Skipped when _ref is not built."""
+import numpy as np
+import pytest
+
+from conftest import Stream, operator_instance
+
+
+def test_rng_stream(oracle, ref):
+    for seed in (0, 1, 7, 42, 2**64 - 1):
+        assert np.array_equal(oracle.uniform(seed, 123456789, 4096), ref.uniform(seed, 123456789, 4096))
+    for n in (1, 2, 3, 64, 1000):
+        a, ca = oracle.shuffle_indices(11, 17, n)
+        b, cb = ref.shuffle_indices(11, 17, n)
+        assert np.array_equal(a, b) and ca == cb == 17 + n - 1
+
+
+def test_rv_select_suite_7001(oracle, ref):
+    """verify.hpp:53-76 instance generator, 200 instances; also the set-form oracle of the reference."""
+    for k in range(200):
+        g = Stream(ref, 7001 + k)
+        n, m = g.pick(1, 64), g.pick(2, 3)
+        H = g.pick(1, 14) if m == 2 else g.pick(1, 4)
+        t_max = g.pick(1, 200)
+        t = g.pick(0, t_max)
+        v0, gamma = ref.make_ref_set(m, H)
+        f = g.tensor(n, m) * 10.0
+        a = oracle.rv_select(f, v0, gamma, t, t_max, 2.0)
+        b = ref.rv_select(f, v0, gamma, t, t_max, 2.0)
+        c = ref.rv_select(f, v0, gamma, t, t_max, 2.0, set_form=True)
+        assert np.array_equal(a.elite, b.elite) and np.array_equal(a.validity, b.validity), k
+        assert np.array_equal(a.elite, c.elite) and np.array_equal(a.validity, c.validity), k
+        assert np.array_equal(a.assoc, b.assoc) and np.array_equal(a.theta, b.theta) and np.array_equal(a.apd, b.apd), k
+
+
+@pytest.mark.parametrize("op", [0, 1])
+def test_operator_suite_7002(oracle, ref, op):
+    """verify.hpp:117-182: seed 7002 + op*1000003 + k, n<=16, d<=8, random per-gene bounds."""
+    for k in range(100):
+        seed = 7002 + op * 1000003 + k
+        g = Stream(ref, seed)
+        n, d, lo, hi, x = operator_instance(g, 2, 16, 8)
+        s = seed ^ 0x5EED
+        if op == 0:
+            a, ca = oracle.sbx(x, s, 0, lo, hi)
+            b, cb = ref.sbx(x, s, 0, lo, hi)
+            c, _ = ref.sbx(x, s, 0, lo, hi, scalar=True)
+        else:
+            a, ca = oracle.polynomial_mutation(x, s, 0, lo, hi)
+            b, cb = ref.polynomial_mutation(x, s, 0, lo, hi)
+            c, _ = ref.polynomial_mutation(x, s, 0, lo, hi, scalar=True)
+        assert np.array_equal(a, b) and np.array_equal(a, c) and ca == cb, (op, k)
+        a, ca = oracle.ga_reproduce(x, s, 5, lo, hi)
+        b, cb = ref.ga_reproduce(x, s, 5, lo, hi)
+        assert np.array_equal(a, b) and ca == cb, (op, k)
+
+
+def test_dtlz_random(oracle, ref):
+    g = Stream(ref, 9400)
+    for m, d in ((2, 2), (3, 7), (3, 500), (6, 41), (10, 1000)):
+        x = g.tensor(13, d)
+        for pid in (1, 2, 3, 4):
+            assert np.array_equal(oracle.evaluate(f"dtlz{pid}", x, m), ref.evaluate(f"dtlz{pid}", x, m)), (pid, m, d)
+
+
+def test_refvec_streaming_gamma_matches_dense(oracle, ref):
+    """the streamed gamma equals the reference's dense R x R form, also after
+    an anisotropic adaptation."""
+    for m, H in ((3, 40), (10, 4), (2, 50), (4, 9)):
+        v0, g0 = oracle.make_ref_set(m, H)
+        rv0, rg0 = ref.make_ref_set(m, H)
+        assert np.array_equal(v0, rv0) and np.array_equal(g0, rg0), (m, H)
+        zmin = np.linspace(0.0, 0.3, m)
+        zmax = zmin + np.linspace(0.2, 7.0, m)
+        a = oracle.adapt(v0, v0, g0, zmin, zmax)
+        b = ref.adapt(v0, v0, g0, zmin, zmax)
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]), (m, H)
+
+
+@pytest.mark.parametrize("cfg", [("dtlz2", 40, 9, 3, 0, 12, 3), ("dtlz1", 33, 15, 2, 0, 20, 8), ("dtlz4", 105, 12, 3, 13, 25, 1)])
+def test_pipeline_and_lockstep(oracle, ref, cfg):
+    """Free-running runs agree bit-for-bit, and so does a generation stepped on explicit state."""
+    problem, n, d, m, H, gens, seed = cfg
+    a = oracle.rvea_run(problem, n, d, m, gens, seed=seed, lattice_h=H)
+    b = ref.rvea_run(problem, n, d, m, gens, seed=seed, lattice_h=H)
+    assert np.array_equal(a["x"], b["x"]) and np.array_equal(a["f"], b["f"]) and np.array_equal(a["pop_size"], b["pop_size"])
+    # lock-step
+    Hh = H or oracle.lattice_density_for(m, n)
+    v0, gamma = oracle.make_ref_set(m, Hh)
+    lo, hi = oracle.problem_bounds(problem, d, m)
+    x, c = oracle.random_reproduce(n, d, seed, 0, lo, hi)
+    f = oracle.evaluate(problem, x, m)
+    adapt_every = max(1, int(np.ceil(0.1 * gens)))
+    so = dict(x=x, f=f, v=v0, gamma=gamma, counter=c)
+    sr = dict(so)
+    for t in range(gens):
+        so = oracle.generation(problem, n, m, seed, so["counter"], lo, hi, t, gens, 2.0, adapt_every, v0, so["v"], so["gamma"], so["x"], so["f"])
+        sr = ref.generation(problem, n, m, seed, sr["counter"], lo, hi, t, gens, 2.0, adapt_every, v0, sr["v"], sr["gamma"], sr["x"], sr["f"])
+        for key in ("x", "f", "v", "gamma", "offspring", "f_off", "elite"):
+            assert np.array_equal(so[key], sr[key]), (t, key)
+        assert so["counter"] == sr["counter"]
+    assert np.array_equal(so["x"], a["x"]) and np.array_equal(so["f"], a["f"])
