@@ -1,0 +1,199 @@
+/* temo_b200.h — C ABI of the B200-native TensorRVEA generation loop.
+ *
+ * Drop-in boundary for ONE path of the reference (arxiv 2404.01159 "temo" artifact):
+ * the per-generation loop of rvea_run with the GA operator on DTLZ/LSMOP problems
+ * (reference: proj/include/temo/algorithms.hpp:246-292). Every entry point below names
+ * the reference interface it replaces. All matrices are dense row-major fp64 exactly
+ * like temo::Tensor2D (tensor.hpp:22-59); index outputs are uint64 like std::size_t.
+ *
+ * Conventions
+ *   - every function returns 0 on success; non-zero = failure, message via
+ *     temo_b200_last_error(). TEMO_B200_EINVAL mirrors the reference's
+ *     detail::require -> std::invalid_argument (tensor.hpp:63-65).
+ *   - `counter` arguments are in/out and advance by exactly the reference's documented
+ *     draw count (operators.hpp:3-13, rng.hpp:64), so a caller can interleave GPU and
+ *     CPU operators on one RngStream.
+ *   - host-pointer functions ("drop-ins") copy in, run the CUDA kernels, copy out.
+ *     There is NO CPU fallback: without a CUDA device they fail with TEMO_B200_ENODEV.
+ *   - the device-resident loop (temo_b200_run_*) keeps X, F, V, gamma in HBM for the
+ *     whole run; per generation the host only ships the mating permutation (4 B/row)
+ *     and reads back the survivor count.
+ */
+#ifndef TEMO_B200_H
+#define TEMO_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TEMO_B200_OK 0
+#define TEMO_B200_EINVAL 1   /* contract violation (reference: std::invalid_argument) */
+#define TEMO_B200_ECUDA 2    /* CUDA runtime error */
+#define TEMO_B200_ENODEV 3   /* no usable CUDA device: the product has no CPU path */
+#define TEMO_B200_ENOMEM 4
+#define TEMO_B200_ERUNTIME 5 /* reference: std::runtime_error (algorithms.hpp:182-191) */
+
+/* Problem ids (reference: make_problem, problems.hpp:261-296). LSMOP1 is an extension
+ * required by BASELINE.json config #3; the reference has no LSMOP (parity unpinned). */
+#define TEMO_B200_DTLZ1 1
+#define TEMO_B200_DTLZ2 2
+#define TEMO_B200_DTLZ3 3
+#define TEMO_B200_DTLZ4 4
+#define TEMO_B200_LSMOP1 101
+
+/* RNG policy. SPLITMIX64 reproduces RngStream::value_at bit for bit (rng.hpp:23-43) and is
+ * the only mode with draw-for-draw parity; PHILOX is the north star's Philox4x32-10
+ * throughput mode (not in the reference: parity unpinned, invariants only). */
+#define TEMO_B200_RNG_SPLITMIX64 0
+#define TEMO_B200_RNG_PHILOX 1
+
+/* reference: GaParams, operators.hpp:22-27 */
+typedef struct temo_b200_ga_params {
+    double pc;  /* crossover probability per pair */
+    double eta; /* SBX distribution index */
+    double pm;  /* mutation numerator; per-gene rate pm/d */
+    double xi;  /* mutation distribution index */
+} temo_b200_ga_params;
+
+/* reference: RunConfig, algorithms.hpp:21-41 (GA operator, track_archive = false) */
+typedef struct temo_b200_run_config {
+    int32_t problem;      /* TEMO_B200_DTLZ1.. */
+    int32_t rng_mode;     /* TEMO_B200_RNG_* */
+    uint64_t pop;         /* n */
+    uint64_t lattice_h;   /* 0 -> lattice_density_for(obj, pop) */
+    uint64_t generations; /* t_max */
+    uint64_t seed;
+    uint64_t dim;         /* d (0 -> problem default: DTLZ1 7, DTLZ2-4 12, LSMOP1 100*obj) */
+    uint64_t obj;         /* m */
+    double alpha;         /* APD penalty exponent */
+    double fr;            /* adaptation frequency: every ceil(fr * generations) generations */
+    double time_budget_s; /* 0 -> run all generations */
+    temo_b200_ga_params ga;
+    int32_t fuse_eval;    /* 1: evaluate offspring inside the reproduction kernel (default) */
+    int32_t reserved;
+} temo_b200_run_config;
+
+/* ---- library / device ------------------------------------------------------------- */
+const char* temo_b200_last_error(void);
+const char* temo_b200_version(void);
+int temo_b200_device_count(void);
+/* Selects the device for this process (one process per GPU) and creates the library's
+ * stream. Implicitly called with device 0 by the first compute entry point. */
+int temo_b200_init(int device);
+void temo_b200_default_run_config(temo_b200_run_config* cfg);
+void temo_b200_default_ga_params(temo_b200_ga_params* ga);
+
+/* ---- rng.hpp ---------------------------------------------------------------------- */
+/* uniform_tensor (rng.hpp:55-66): rows*cols draws, element e at counter+e. */
+int temo_b200_uniform_tensor(uint64_t seed, uint64_t* counter, uint64_t rows, uint64_t cols,
+                             int rng_mode, double* out);
+/* shuffle_indices (rng.hpp:69-78): host-side Fisher-Yates, n-1 draws. */
+int temo_b200_shuffle_indices(uint64_t seed, uint64_t* counter, uint64_t n, uint64_t* perm);
+/* parent_pool_indices (algorithms.hpp:211-221). */
+int temo_b200_parent_pool_indices(uint64_t current, uint64_t n, uint64_t seed, uint64_t* counter,
+                                  uint64_t* idx);
+
+/* ---- operators.hpp ---------------------------------------------------------------- */
+/* sbx (operators.hpp:65-102): x n x d -> out n x d; 3*(n/2)*d + n/2 draws. */
+int temo_b200_sbx(const double* x, uint64_t n, uint64_t d, uint64_t seed, uint64_t* counter,
+                  const temo_b200_ga_params* ga, const double* lower, const double* upper,
+                  int rng_mode, double* out);
+/* polynomial_mutation (operators.hpp:126-149): 2*n*d draws. */
+int temo_b200_polynomial_mutation(const double* x, uint64_t n, uint64_t d, uint64_t seed,
+                                  uint64_t* counter, const temo_b200_ga_params* ga,
+                                  const double* lower, const double* upper, int rng_mode,
+                                  double* out);
+/* ga_reproduce (operators.hpp:153-161): shuffle + SBX + PM fused into one kernel pass. */
+int temo_b200_ga_reproduce(const double* x, uint64_t n, uint64_t d, uint64_t seed,
+                           uint64_t* counter, const temo_b200_ga_params* ga, const double* lower,
+                           const double* upper, int rng_mode, double* out);
+/* random_reproduce (operators.hpp:287-296): n*d draws. */
+int temo_b200_random_reproduce(uint64_t n, uint64_t d, uint64_t seed, uint64_t* counter,
+                               const double* lower, const double* upper, int rng_mode, double* out);
+
+/* ---- problems.hpp ----------------------------------------------------------------- */
+/* dtlz_eval (problems.hpp:69-92) and ProblemInstance::evaluate (problems.hpp:252); also LSMOP1. */
+int temo_b200_evaluate(int problem, const double* x, uint64_t n, uint64_t d, uint64_t m, double* f);
+/* make_problem bounds (problems.hpp:271-272): lower/upper 1 x d. */
+int temo_b200_problem_bounds(int problem, uint64_t d, uint64_t m, double* lower, double* upper);
+uint64_t temo_b200_problem_default_dim(int problem, uint64_t m);
+
+/* ---- refvec.hpp ------------------------------------------------------------------- */
+uint64_t temo_b200_lattice_count(uint64_t m, uint64_t H);            /* refvec.hpp:15-19 */
+uint64_t temo_b200_lattice_density_for(uint64_t m, uint64_t target); /* refvec.hpp:22-35 */
+int temo_b200_simplex_lattice(uint64_t m, uint64_t H, double* out);  /* refvec.hpp:40-62 */
+/* make_ref_set (refvec.hpp:108-114): v0 (= v) r x m and gamma r. */
+int temo_b200_make_ref_set(uint64_t m, uint64_t H, double* v0, double* gamma);
+/* min_vector_angles (refvec.hpp:81-100), tiled on the device: no R x R matrix. */
+int temo_b200_min_vector_angles(const double* v, uint64_t r, uint64_t m, double* gamma);
+/* adapt (refvec.hpp:135-140): v, gamma in/out; untouched unless every range is > 0. */
+int temo_b200_adapt(const double* v0, double* v, double* gamma, uint64_t r, uint64_t m,
+                    const double* z_min, const double* z_max);
+
+/* ---- selection.hpp ---------------------------------------------------------------- */
+/* rv_select (selection.hpp:200-224, want_table = false) = rv_core (:148-192) + elites.
+ * elite: capacity r; validity: r bytes. Optional per-row outputs (NULL to skip):
+ * assoc[n], theta[n], apd[n] (RvCore, selection.hpp:139-143). */
+int temo_b200_rv_select(const double* f, uint64_t n, uint64_t m, const double* v,
+                        const double* gamma, uint64_t r, uint64_t t, uint64_t t_max, double alpha,
+                        uint64_t* elite, uint64_t* n_elite, unsigned char* validity,
+                        uint64_t* assoc, double* theta, double* apd);
+/* detail::apd_penalty (selection.hpp:86-89), host scalar (glibc pow). */
+double temo_b200_apd_penalty(uint64_t m, uint64_t t, uint64_t t_max, double alpha);
+
+/* ---- algorithms.hpp: device-resident generation loop ------------------------------- */
+typedef struct temo_b200_run temo_b200_run; /* opaque */
+
+/* Initialisation of rvea_run (algorithms.hpp:229-243): reference set, initial population
+ * (n*d draws), first evaluation. */
+int temo_b200_run_create(const temo_b200_run_config* cfg, temo_b200_run** out);
+/* One generation (algorithms.hpp:246-292). Returns the survivor count in *pop_size.
+ * survivors_f (optional, capacity r*m doubles, host) receives the survivors' objectives
+ * (the per-generation result the reference hands to fill_metrics, algorithms.hpp:287). */
+int temo_b200_run_step(temo_b200_run* run, uint64_t* pop_size, double* survivors_f);
+/* Lock-step testing hooks: overwrite / read the loop state with host data.
+ * x: rows x d, f: rows x m, v: r x m, gamma: r (any may be NULL = keep). */
+int temo_b200_run_inject(temo_b200_run* run, uint64_t rows, const double* x, const double* f,
+                         const double* v, const double* gamma, uint64_t counter, uint64_t t);
+int temo_b200_run_state(temo_b200_run* run, uint64_t* rows, uint64_t* counter, uint64_t* t,
+                        uint64_t* r, uint64_t* d, uint64_t* m);
+/* Copies out x (rows x d), f (rows x m), v (r x m), gamma (r); any may be NULL. */
+int temo_b200_run_download(temo_b200_run* run, double* x, double* f, double* v, double* gamma);
+/* Last generation's offspring (n x d), their objectives (n x m) and the elite merged-row
+ * indices (survivor k came from merged row elite[k]; parents first, algorithms.hpp:274-279). */
+int temo_b200_run_last_generation(temo_b200_run* run, double* offspring, double* f_off,
+                                  uint64_t* elite);
+/* Device-side timings of the last step in ms (CUDA events on the library stream):
+ * [0] whole generation, [1] reproduction(+fused eval), [2] evaluation, [3] selection,
+ * [4] adaptation, [5] host mating-permutation time (wall), [6..7] reserved. */
+int temo_b200_run_timings(temo_b200_run* run, double* ms8);
+int temo_b200_run_destroy(temo_b200_run* run);
+
+/* rvea_run (algorithms.hpp:227-296), whole run, RunRecord fields flattened:
+ * final_x (cap x d, cap = max(pop, r)), final_f, rows per generation. */
+int temo_b200_rvea_run(const temo_b200_run_config* cfg, double* final_x, double* final_f,
+                       uint64_t* final_rows, uint64_t* rows_done, uint64_t* pop_size,
+                       double* elapsed_ms);
+
+/* ---- device-pointer stage API (used by bench.py kernel timings and the multi-GPU host
+ * orchestration in paper_2404_01159_b200/dist.py). Pointers are CUDA device pointers of
+ * this process; all launches go to the library stream. ------------------------------ */
+void* temo_b200_dev_alloc(size_t bytes);
+int temo_b200_dev_free(void* p);
+int temo_b200_dev_upload(void* dst, const void* src, size_t bytes);
+int temo_b200_dev_download(void* dst, const void* src, size_t bytes);
+int temo_b200_dev_sync(void);
+/* Times `reps` back-to-back launches of a stage with CUDA events on the library stream,
+ * returns the mean ms per launch. stage: 1 reproduction (ga, unfused), 2 evaluation,
+ * 3 reproduction with fused evaluation, 4 selection, 5 gamma. Used for the roofline. */
+int temo_b200_run_time_stage(temo_b200_run* run, int stage, int reps, double* mean_ms);
+/* Overwrites >= bytes of scratch HBM (L2 flush between timed iterations). */
+int temo_b200_flush_l2(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TEMO_B200_H */

@@ -1,0 +1,433 @@
+"""Host-side mirror of the reference's operator / problem / selection / algorithm interface
+for the TensorRVEA generation loop, bound to the CUDA implementation through the C ABI.
+
+Names, argument meaning, draw-counter behaviour and error behaviour follow the reference's
+free functions (reference paths under proj/include/temo/):
+
+    RngStream, uniform_tensor, shuffle_indices           rng.hpp:34-78
+    GaParams, sbx, polynomial_mutation, ga_reproduce,
+    random_reproduce                                     operators.hpp:22-27,65-161,287-296
+    dtlz_eval, ProblemInstance, make_problem             problems.hpp:69-92,246-296
+    lattice_count, lattice_density_for, simplex_lattice,
+    RefVectorSet, make_ref_set, min_vector_angles, adapt refvec.hpp:15-140
+    SelectionOutcome, rv_select                          selection.hpp:131-135,200-224
+    RunConfig, RunRecord, GenerationRow, rvea_run        algorithms.hpp:21-63,144-150,227-296
+
+A ``Tensor2D`` is a C-contiguous float64 numpy array of shape (rows, cols). Contract
+violations raise ValueError where the reference throws std::invalid_argument. Everything
+numeric runs in the sm_100a kernels; nothing here computes on the CPU except the pieces the
+design keeps on the host (lattice enumeration, Fisher-Yates permutation, scalar APD penalty),
+which live in the shared library too.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from ._lib import GaParamsC, RunConfigC, TemoB200Error, f64p, u64, u64p, u8p
+
+PROBLEM_IDS = {"dtlz1": 1, "dtlz2": 2, "dtlz3": 3, "dtlz4": 4, "lsmop1": 101}
+RNG_SPLITMIX64, RNG_PHILOX = 0, 1
+
+
+def _call(fn, *args):
+    rc = fn(*args)
+    if rc != 0:
+        msg = _lib.load().temo_b200_last_error().decode(errors="replace")
+        if rc == 1:
+            raise ValueError(msg)  # reference: std::invalid_argument
+        if rc == 4:
+            raise MemoryError(msg)
+        raise TemoB200Error(rc, msg)
+
+
+def _t(a):
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    return a
+
+
+def _p(a, typ=f64p):
+    return None if a is None else a.ctypes.data_as(typ)
+
+
+def device_count() -> int:
+    return int(_lib.load().temo_b200_device_count())
+
+
+def init(device: int = 0) -> None:
+    _call(_lib.load().temo_b200_init, device)
+
+
+# ------------------------------------------------------------------------------- rng.hpp
+@dataclass
+class RngStream:
+    """reference: RngStream (rng.hpp:34-52); `counter` advances exactly as in the reference."""
+    seed: int = 0
+    counter: int = 0
+    mode: int = RNG_SPLITMIX64
+
+    def at(self, c: int) -> "RngStream":
+        return RngStream(self.seed, c, self.mode)
+
+
+def uniform_tensor(stream: RngStream, rows: int, cols: int) -> np.ndarray:
+    out = np.empty((rows, cols))
+    c = u64(stream.counter)
+    _call(_lib.load().temo_b200_uniform_tensor, u64(stream.seed), C.byref(c), u64(rows), u64(cols), stream.mode, _p(out))
+    stream.counter = c.value
+    return out
+
+
+def shuffle_indices(stream: RngStream, n: int) -> np.ndarray:
+    out = np.empty(n, dtype=np.uint64)
+    c = u64(stream.counter)
+    _call(_lib.load().temo_b200_shuffle_indices, u64(stream.seed), C.byref(c), u64(n), _p(out, u64p))
+    stream.counter = c.value
+    return out
+
+
+def parent_pool_indices(current: int, n: int, stream: RngStream) -> np.ndarray:
+    """reference: algorithms.hpp:211-221."""
+    out = np.empty(n, dtype=np.uint64)
+    c = u64(stream.counter)
+    _call(_lib.load().temo_b200_parent_pool_indices, u64(current), u64(n), u64(stream.seed), C.byref(c), _p(out, u64p))
+    stream.counter = c.value
+    return out
+
+
+# ------------------------------------------------------------------------- operators.hpp
+@dataclass
+class GaParams:
+    pc: float = 1.0
+    eta: float = 20.0
+    pm: float = 1.0
+    xi: float = 20.0
+
+    def c(self) -> GaParamsC:
+        return GaParamsC(self.pc, self.eta, self.pm, self.xi)
+
+
+def _operator(fn, x, stream, p, lower, upper):
+    x = _t(x)
+    if x.ndim != 2:
+        raise ValueError("operator: x must be a 2-D tensor")
+    n, d = x.shape
+    lower, upper = _t(lower).reshape(-1), _t(upper).reshape(-1)
+    if lower.size != d or upper.size != d:
+        raise ValueError("operator: bounds shape mismatch")
+    out = np.empty_like(x)
+    c = u64(stream.counter)
+    g = (p or GaParams()).c()
+    _call(fn, _p(x), u64(n), u64(d), u64(stream.seed), C.byref(c), C.byref(g), _p(lower), _p(upper), stream.mode, _p(out))
+    stream.counter = c.value
+    return out
+
+
+def sbx(x, stream: RngStream, p: GaParams, lower, upper) -> np.ndarray:
+    return _operator(_lib.load().temo_b200_sbx, x, stream, p, lower, upper)
+
+
+def polynomial_mutation(x, stream: RngStream, p: GaParams, lower, upper) -> np.ndarray:
+    return _operator(_lib.load().temo_b200_polynomial_mutation, x, stream, p, lower, upper)
+
+
+def ga_reproduce(x, stream: RngStream, p: GaParams, lower, upper) -> np.ndarray:
+    return _operator(_lib.load().temo_b200_ga_reproduce, x, stream, p, lower, upper)
+
+
+def random_reproduce(n: int, d: int, stream: RngStream, lower, upper) -> np.ndarray:
+    lower, upper = _t(lower).reshape(-1), _t(upper).reshape(-1)
+    out = np.empty((n, d))
+    c = u64(stream.counter)
+    _call(_lib.load().temo_b200_random_reproduce, u64(n), u64(d), u64(stream.seed), C.byref(c), _p(lower), _p(upper),
+          stream.mode, _p(out))
+    stream.counter = c.value
+    return out
+
+
+# -------------------------------------------------------------------------- problems.hpp
+def evaluate(problem: str | int, x, m: int) -> np.ndarray:
+    pid = PROBLEM_IDS[problem] if isinstance(problem, str) else int(problem)
+    x = _t(x)
+    if x.ndim != 2:
+        raise ValueError("evaluate: x must be a 2-D tensor")
+    n, d = x.shape
+    f = np.empty((n, m))
+    _call(_lib.load().temo_b200_evaluate, pid, _p(x), u64(n), u64(d), u64(m), _p(f))
+    return f
+
+
+def dtlz_eval(id: int, x, m: int) -> np.ndarray:
+    """reference: dtlz_eval (problems.hpp:69-92)."""
+    if not 1 <= id <= 4:
+        raise ValueError("dtlz_eval: id must be in 1..4")
+    return evaluate(id, x, m)
+
+
+@dataclass
+class ProblemInstance:
+    """reference: ProblemInstance (problems.hpp:246-257)."""
+    name: str
+    dim: int
+    num_obj: int
+    lower: np.ndarray
+    upper: np.ndarray
+    dtlz_id: int = 0
+    pf_extent: float = 1.0
+    maximization: bool = False
+    problem_id: int = 0
+
+    def evaluate(self, x) -> np.ndarray:
+        return evaluate(self.problem_id, x, self.num_obj)
+
+
+def make_problem(name: str, dim: int = 0, m: int = 3) -> ProblemInstance:
+    """reference: make_problem (problems.hpp:261-296) for the DTLZ family, plus 'lsmop1'."""
+    if name not in PROBLEM_IDS:
+        raise ValueError(f"make_problem: unknown problem '{name}'")
+    pid = PROBLEM_IDS[name]
+    L = _lib.load()
+    d = dim or int(L.temo_b200_problem_default_dim(pid, u64(m)))
+    if d < m:
+        raise ValueError("make_problem: DTLZ needs d >= m")
+    lo, hi = np.empty(d), np.empty(d)
+    _call(L.temo_b200_problem_bounds, pid, u64(d), u64(m), _p(lo), _p(hi))
+    return ProblemInstance(name, d, m, lo, hi, dtlz_id=pid if pid <= 4 else 0,
+                           pf_extent=0.5 if pid == 1 else 1.0, problem_id=pid)
+
+
+# ---------------------------------------------------------------------------- refvec.hpp
+def lattice_count(m: int, H: int) -> int:
+    return int(_lib.load().temo_b200_lattice_count(u64(m), u64(H)))
+
+
+def lattice_density_for(m: int, target: int) -> int:
+    return int(_lib.load().temo_b200_lattice_density_for(u64(m), u64(target)))
+
+
+def simplex_lattice(m: int, H: int) -> np.ndarray:
+    if m < 2:
+        raise ValueError("simplex_lattice: m must be at least 2")
+    if H < 1:
+        raise ValueError("simplex_lattice: H must be at least 1")
+    out = np.empty((lattice_count(m, H), m))
+    _call(_lib.load().temo_b200_simplex_lattice, u64(m), u64(H), _p(out))
+    return out
+
+
+@dataclass
+class RefVectorSet:
+    """reference: RefVectorSet (refvec.hpp:102-106)."""
+    v0: np.ndarray
+    v: np.ndarray
+    gamma: np.ndarray
+
+
+def min_vector_angles(v) -> np.ndarray:
+    v = _t(v)
+    gamma = np.empty(v.shape[0])
+    _call(_lib.load().temo_b200_min_vector_angles, _p(v), u64(v.shape[0]), u64(v.shape[1]), _p(gamma))
+    return gamma
+
+
+def make_ref_set(m: int, H: int) -> RefVectorSet:
+    if m < 2:
+        raise ValueError("simplex_lattice: m must be at least 2")
+    if H < 1:
+        raise ValueError("simplex_lattice: H must be at least 1")
+    r = lattice_count(m, H)
+    v0, gamma = np.empty((r, m)), np.empty(r)
+    _call(_lib.load().temo_b200_make_ref_set, u64(m), u64(H), _p(v0), _p(gamma))
+    return RefVectorSet(v0, v0.copy(), gamma)
+
+
+def adapt(refs: RefVectorSet, z_min, z_max) -> None:
+    """reference: adapt (refvec.hpp:135-140): in place; untouched unless every range is > 0."""
+    z_min, z_max = _t(z_min).reshape(-1), _t(z_max).reshape(-1)
+    v0 = _t(refs.v0)
+    r, m = v0.shape
+    if z_min.size != m or z_max.size != m:
+        raise ValueError("adapt_vectors: range shape mismatch")
+    v, gamma = _t(refs.v).copy(), _t(refs.gamma).reshape(-1).copy()
+    _call(_lib.load().temo_b200_adapt, _p(v0), _p(v), _p(gamma), u64(r), u64(m), _p(z_min), _p(z_max))
+    refs.v, refs.gamma = v, gamma
+
+
+# ------------------------------------------------------------------------- selection.hpp
+@dataclass
+class SelectionOutcome:
+    """reference: SelectionOutcome (selection.hpp:131-135) + RvCore (selection.hpp:139-143)."""
+    elite_indices: np.ndarray
+    validity: np.ndarray
+    assoc: np.ndarray
+    theta: np.ndarray
+    apd: np.ndarray
+
+
+def apd_penalty(m: int, t: int, t_max: int, alpha: float) -> float:
+    return float(_lib.load().temo_b200_apd_penalty(u64(m), u64(t), u64(t_max), alpha))
+
+
+def rv_select(f, refs: RefVectorSet, t: int, t_max: int, alpha: float = 2.0) -> SelectionOutcome:
+    f, v, gamma = _t(f), _t(refs.v), _t(refs.gamma).reshape(-1)
+    if f.ndim != 2 or f.shape[1] != v.shape[1]:
+        raise ValueError("rv_select: objective count mismatch")  # selection.hpp:150
+    n, m = f.shape
+    r = v.shape[0]
+    elite = np.empty(max(r, 1), dtype=np.uint64)
+    valid = np.empty(r, dtype=np.uint8)
+    assoc = np.empty(n, dtype=np.uint64)
+    theta, apd = np.empty(n), np.empty(n)
+    ne = u64(0)
+    _call(_lib.load().temo_b200_rv_select, _p(f), u64(n), u64(m), _p(v), _p(gamma), u64(r), u64(t), u64(t_max),
+          C.c_double(alpha), _p(elite, u64p), C.byref(ne), _p(valid, u8p), _p(assoc, u64p), _p(theta), _p(apd))
+    return SelectionOutcome(elite[: ne.value].copy(), valid, assoc, theta, apd)
+
+
+# ------------------------------------------------------------------------ algorithms.hpp
+@dataclass
+class RunConfig:
+    """reference: RunConfig (algorithms.hpp:21-41), GA operator, track_archive = false."""
+    problem: str = "dtlz2"
+    op: str = "ga"
+    pop: int = 105
+    lattice_h: int = 0
+    generations: int = 100
+    alpha: float = 2.0
+    fr: float = 0.1
+    seed: int = 42
+    time_budget_s: float = 0.0
+    dim: int = 0
+    obj: int = 3
+    ga: GaParams = field(default_factory=GaParams)
+    rng_mode: int = RNG_SPLITMIX64
+    fuse_eval: bool = True
+
+    def c(self) -> RunConfigC:
+        if self.op != "ga":
+            raise ValueError(f"rvea_run: unknown operator '{self.op}'")  # only the GA path is in scope
+        if self.problem not in PROBLEM_IDS:
+            raise ValueError(f"make_problem: unknown problem '{self.problem}'")
+        cfg = RunConfigC()
+        _lib.load().temo_b200_default_run_config(C.byref(cfg))
+        cfg.problem = PROBLEM_IDS[self.problem]
+        cfg.rng_mode = self.rng_mode
+        cfg.pop, cfg.lattice_h, cfg.generations, cfg.seed = self.pop, self.lattice_h, self.generations, self.seed
+        cfg.dim, cfg.obj = self.dim, self.obj
+        cfg.alpha, cfg.fr, cfg.time_budget_s = self.alpha, self.fr, self.time_budget_s
+        cfg.ga = self.ga.c()
+        cfg.fuse_eval = 1 if self.fuse_eval else 0
+        return cfg
+
+
+@dataclass
+class GenerationRow:
+    t: int
+    elapsed_ms: float
+    pop_size: int
+
+
+@dataclass
+class RunRecord:
+    rows: list
+    final_x: np.ndarray
+    final_f: np.ndarray
+
+
+class RveaRun:
+    """Device-resident generation loop (session form of rvea_run): create -> step()* -> download()."""
+
+    def __init__(self, cfg: RunConfig):
+        self._L = _lib.load()
+        self._h = C.c_void_p()
+        ccfg = cfg.c()
+        _call(self._L.temo_b200_run_create, C.byref(ccfg), C.byref(self._h))
+        self.cfg = cfg
+        st = self.state()
+        self.r, self.d, self.m, self.n = st["r"], st["d"], st["m"], cfg.pop
+        self._fbuf = np.empty((max(self.r, self.n), self.m))
+
+    def close(self):
+        if self._h:
+            _call(self._L.temo_b200_run_destroy, self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def step(self, want_f: bool = False):
+        """One generation; returns the survivor count (and the survivors' objectives if asked)."""
+        p = u64(0)
+        _call(self._L.temo_b200_run_step, self._h, C.byref(p), _p(self._fbuf) if want_f else None)
+        if want_f:
+            return p.value, self._fbuf[: p.value]
+        return p.value
+
+    def state(self) -> dict:
+        vals = [u64(0) for _ in range(6)]
+        _call(self._L.temo_b200_run_state, self._h, *[C.byref(v) for v in vals])
+        return dict(zip(("rows", "counter", "t", "r", "d", "m"), (v.value for v in vals)))
+
+    def inject(self, x=None, f=None, v=None, gamma=None, counter=0, t=0, rows=None):
+        x = None if x is None else _t(x)
+        f = None if f is None else _t(f)
+        v = None if v is None else _t(v)
+        gamma = None if gamma is None else _t(gamma).reshape(-1)
+        if rows is None:
+            rows = x.shape[0] if x is not None else (f.shape[0] if f is not None else self.state()["rows"])
+        _call(self._L.temo_b200_run_inject, self._h, u64(rows), _p(x), _p(f), _p(v), _p(gamma), u64(counter), u64(t))
+
+    def download(self, want_x=True):
+        rows = self.state()["rows"]
+        x = np.empty((rows, self.d)) if want_x else None
+        f = np.empty((rows, self.m))
+        v, gamma = np.empty((self.r, self.m)), np.empty(self.r)
+        _call(self._L.temo_b200_run_download, self._h, _p(x), _p(f), _p(v), _p(gamma))
+        return dict(x=x, f=f, v=v, gamma=gamma)
+
+    def last_generation(self):
+        rows = self.state()["rows"]
+        off, f_off = np.empty((self.n, self.d)), np.empty((self.n, self.m))
+        elite = np.empty(rows, dtype=np.uint64)
+        _call(self._L.temo_b200_run_last_generation, self._h, _p(off), _p(f_off), _p(elite, u64p))
+        return dict(offspring=off, f_off=f_off, elite=elite)
+
+    def timings(self) -> dict:
+        ms = np.zeros(8)
+        _call(self._L.temo_b200_run_timings, self._h, _p(ms))
+        return dict(generation=ms[0], reproduce=ms[1], evaluate=ms[2], select=ms[3], adapt=ms[4], host_perm=ms[5])
+
+    def time_stage(self, stage: int, reps: int = 5) -> float:
+        out = C.c_double(0)
+        _call(self._L.temo_b200_run_time_stage, self._h, stage, reps, C.byref(out))
+        return out.value
+
+
+def rvea_run(prob: ProblemInstance, cfg: RunConfig) -> RunRecord:
+    """reference: rvea_run (algorithms.hpp:227-296). `prob` supplies name/dim/num_obj like the
+    reference's ProblemInstance; the evaluator itself runs on the device."""
+    cfg = RunConfig(**{**cfg.__dict__, "problem": prob.name, "dim": prob.dim, "obj": prob.num_obj})
+    ccfg = cfg.c()
+    L = _lib.load()
+    H = cfg.lattice_h or lattice_density_for(prob.num_obj, cfg.pop)
+    cap = max(cfg.pop, lattice_count(prob.num_obj, H))
+    x, f = np.empty((cap, prob.dim)), np.empty((cap, prob.num_obj))
+    rows, done = u64(0), u64(0)
+    pops = np.zeros(cfg.generations, dtype=np.uint64)
+    ms = np.zeros(cfg.generations)
+    _call(L.temo_b200_rvea_run, C.byref(ccfg), _p(x), _p(f), C.byref(rows), C.byref(done), _p(pops, u64p), _p(ms))
+    rec_rows = [GenerationRow(t, float(ms[t]), int(pops[t])) for t in range(done.value)]
+    return RunRecord(rec_rows, x[: rows.value].copy(), f[: rows.value].copy())

@@ -1,0 +1,523 @@
+// C ABI of libtemo_b200.so — see include/temo_b200.h for the contract and the reference
+// interface each entry point replaces. No torch types, no C++ types cross this boundary.
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <vector>
+
+#include "../../include/temo_b200.h"
+#include "internal.h"
+#include "run.h"
+
+using namespace temo_b200;
+
+namespace {
+
+thread_local std::string g_error;
+
+template <class F>
+int guarded(F&& body) {
+    try {
+        body();
+        return TEMO_B200_OK;
+    } catch (const Error& e) {
+        g_error = e.what();
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_error = "host allocation failed";
+        return TEMO_B200_ENOMEM;
+    } catch (const std::exception& e) {
+        g_error = e.what();
+        return TEMO_B200_ERUNTIME;
+    }
+}
+
+// RAII device buffer for the host-pointer drop-ins.
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t count = 0;
+    explicit DevBuf(size_t n) : p(dev_alloc<T>(n)), count(n) {}
+    DevBuf(const T* host, size_t n, cudaStream_t s) : DevBuf(n) {
+        if (n) TEMO_CUDA(cudaMemcpyAsync(p, host, n * sizeof(T), cudaMemcpyHostToDevice, s));
+    }
+    ~DevBuf() { cudaFree(p); }
+    void to_host(T* host, cudaStream_t s, size_t n = (size_t)-1) const {
+        if (n == (size_t)-1) n = count;
+        if (n) TEMO_CUDA(cudaMemcpyAsync(host, p, n * sizeof(T), cudaMemcpyDeviceToHost, s));
+    }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+};
+
+GaParams ga_of(const temo_b200_ga_params* g) {
+    GaParams p;
+    if (g) {
+        p.pc = g->pc;
+        p.eta = g->eta;
+        p.pm = g->pm;
+        p.xi = g->xi;
+    }
+    return p;
+}
+
+RunConfig cfg_of(const temo_b200_run_config* c) {
+    require(c != nullptr, "run config is null");
+    RunConfig r;
+    r.problem = c->problem;
+    r.rng_mode = c->rng_mode;
+    r.pop = c->pop;
+    r.lattice_h = c->lattice_h;
+    r.generations = c->generations;
+    r.seed = c->seed;
+    r.dim = c->dim;
+    r.obj = c->obj;
+    r.alpha = c->alpha;
+    r.fr = c->fr;
+    r.time_budget_s = c->time_budget_s;
+    r.ga = ga_of(&c->ga);
+    r.fuse_eval = c->fuse_eval;
+    require(r.rng_mode == 0 || r.rng_mode == 1, "unknown rng mode");
+    return r;
+}
+
+void check_mode(int rng_mode) { require(rng_mode == 0 || rng_mode == 1, "unknown rng mode"); }
+
+// Shared body of sbx / polynomial_mutation / ga_reproduce on host buffers.
+void host_operator(bool do_shuffle, bool do_sbx, bool do_pm, const double* x, uint64_t n, uint64_t d,
+                   uint64_t seed, uint64_t* counter, const temo_b200_ga_params* ga, const double* lower,
+                   const double* upper, int rng_mode, double* out) {
+    require(x && counter && lower && upper && out, "operator: null argument");
+    require(n >= 1 && d >= 1, "operator: empty population");
+    if (do_sbx) require(n >= 2, "sbx: needs at least two rows");
+    check_mode(rng_mode);
+    Context& cx = ctx();
+    cudaStream_t s = cx.stream;
+    DevBuf<double> dx(x, n * d, s), dlo(lower, d, s), dhi(upper, d, s), dout(n * d);
+    uint64_t c = *counter;
+    std::unique_ptr<DevBuf<uint32_t>> dperm;
+    std::vector<uint32_t> perm;
+    if (do_shuffle) {
+        perm.resize(n);
+        shuffle_indices(seed, c, n, perm.data());
+        dperm.reset(new DevBuf<uint32_t>(perm.data(), n, s));
+    }
+    ReproArgs a;
+    a.pool = dx.p;
+    a.src = dperm ? dperm->p : nullptr;
+    a.out = dout.p;
+    a.n = n;
+    a.d = d;
+    a.rng = make_rng(seed, rng_mode);
+    a.ga = ga_of(ga);
+    a.lower = dlo.p;
+    a.upper = dhi.p;
+    a.do_sbx = do_sbx;
+    a.do_pm = do_pm;
+    if (do_sbx) {
+        a.c_sbx = c;
+        c += 3 * (n / 2) * d + n / 2;
+    }
+    if (do_pm) {
+        a.c_pm = c;
+        c += 2 * n * d;
+    }
+    launch_reproduce(a, s);
+    dout.to_host(out, s);
+    TEMO_CUDA(cudaStreamSynchronize(s));
+    *counter = c;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* temo_b200_last_error(void) { return g_error.c_str(); }
+const char* temo_b200_version(void) { return "temo_b200 0.1 (sm_100a)"; }
+
+int temo_b200_device_count(void) {
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return count;
+}
+
+int temo_b200_init(int device) {
+    return guarded([&] { init_context(device); });
+}
+
+void temo_b200_default_ga_params(temo_b200_ga_params* ga) {
+    if (!ga) return;
+    ga->pc = 1.0;
+    ga->eta = 20.0;
+    ga->pm = 1.0;
+    ga->xi = 20.0;
+}
+
+void temo_b200_default_run_config(temo_b200_run_config* cfg) {
+    if (!cfg) return;
+    std::memset(cfg, 0, sizeof(*cfg));
+    cfg->problem = TEMO_B200_DTLZ2;
+    cfg->rng_mode = TEMO_B200_RNG_SPLITMIX64;
+    cfg->pop = 105;
+    cfg->lattice_h = 0;
+    cfg->generations = 100;
+    cfg->seed = 42;
+    cfg->dim = 0;
+    cfg->obj = 3;
+    cfg->alpha = 2.0;
+    cfg->fr = 0.1;
+    cfg->time_budget_s = 0.0;
+    temo_b200_default_ga_params(&cfg->ga);
+    cfg->fuse_eval = 1;
+}
+
+// ---- rng.hpp ------------------------------------------------------------------------------
+int temo_b200_uniform_tensor(uint64_t seed, uint64_t* counter, uint64_t rows, uint64_t cols, int rng_mode,
+                             double* out) {
+    return guarded([&] {
+        require(counter && out, "uniform_tensor: null argument");
+        require(rows >= 1 && cols >= 1, "uniform_tensor: empty shape");  // rng.hpp:56
+        check_mode(rng_mode);
+        Context& cx = ctx();
+        DevBuf<double> d(rows * cols);
+        launch_uniform_fill(d.p, rows * cols, make_rng(seed, rng_mode), *counter, cx.stream);
+        d.to_host(out, cx.stream);
+        TEMO_CUDA(cudaStreamSynchronize(cx.stream));
+        *counter += rows * cols;
+    });
+}
+
+int temo_b200_shuffle_indices(uint64_t seed, uint64_t* counter, uint64_t n, uint64_t* perm) {
+    return guarded([&] {
+        require(counter && perm, "shuffle_indices: null argument");
+        require(n >= 1 && n < 0xffffffffULL, "shuffle_indices: n must be positive");
+        std::vector<uint32_t> p(n);
+        shuffle_indices(seed, *counter, n, p.data());
+        for (uint64_t i = 0; i < n; ++i) perm[i] = p[i];
+    });
+}
+
+int temo_b200_parent_pool_indices(uint64_t current, uint64_t n, uint64_t seed, uint64_t* counter,
+                                  uint64_t* idx) {
+    return guarded([&] {
+        require(counter && idx, "parent_pool_indices: null argument");
+        if (current == n) {  // algorithms.hpp:214-217: no draws
+            for (uint64_t i = 0; i < n; ++i) idx[i] = i;
+            return;
+        }
+        const uint64_t base = mix64(seed);
+        for (uint64_t i = 0; i < n; ++i) {
+            const double u = (double)(mix64(base + (*counter + i) * kGolden) >> 11) * 0x1.0p-53;
+            idx[i] = (uint64_t)(u * (double)current);
+        }
+        *counter += n;
+    });
+}
+
+// ---- operators.hpp --------------------------------------------------------------------------
+int temo_b200_sbx(const double* x, uint64_t n, uint64_t d, uint64_t seed, uint64_t* counter,
+                  const temo_b200_ga_params* ga, const double* lower, const double* upper, int rng_mode,
+                  double* out) {
+    return guarded([&] { host_operator(false, true, false, x, n, d, seed, counter, ga, lower, upper, rng_mode, out); });
+}
+
+int temo_b200_polynomial_mutation(const double* x, uint64_t n, uint64_t d, uint64_t seed, uint64_t* counter,
+                                  const temo_b200_ga_params* ga, const double* lower, const double* upper,
+                                  int rng_mode, double* out) {
+    return guarded([&] { host_operator(false, false, true, x, n, d, seed, counter, ga, lower, upper, rng_mode, out); });
+}
+
+int temo_b200_ga_reproduce(const double* x, uint64_t n, uint64_t d, uint64_t seed, uint64_t* counter,
+                           const temo_b200_ga_params* ga, const double* lower, const double* upper,
+                           int rng_mode, double* out) {
+    return guarded([&] { host_operator(true, true, true, x, n, d, seed, counter, ga, lower, upper, rng_mode, out); });
+}
+
+int temo_b200_random_reproduce(uint64_t n, uint64_t d, uint64_t seed, uint64_t* counter, const double* lower,
+                               const double* upper, int rng_mode, double* out) {
+    return guarded([&] {
+        require(counter && lower && upper && out, "random_reproduce: null argument");
+        require(n >= 1 && d >= 1, "uniform_tensor: empty shape");
+        check_mode(rng_mode);
+        Context& cx = ctx();
+        cudaStream_t s = cx.stream;
+        DevBuf<double> dlo(lower, d, s), dhi(upper, d, s), dout(n * d);
+        launch_random_reproduce(dout.p, nullptr, n, d, make_rng(seed, rng_mode), *counter, dlo.p, dhi.p, s);
+        dout.to_host(out, s);
+        TEMO_CUDA(cudaStreamSynchronize(s));
+        *counter += n * d;
+    });
+}
+
+// ---- problems.hpp -----------------------------------------------------------------------------
+int temo_b200_evaluate(int problem, const double* x, uint64_t n, uint64_t d, uint64_t m, double* f) {
+    return guarded([&] {
+        require(x && f, "evaluate: null argument");
+        Context& cx = ctx();
+        cudaStream_t s = cx.stream;
+        DevBuf<double> dx(x, n * d, s), df(n * m);
+        EvalArgs a;
+        a.problem = problem;
+        a.x = dx.p;
+        a.n = n;
+        a.d = d;
+        a.m = m;
+        a.f = df.p;
+        launch_evaluate(a, s);
+        df.to_host(f, s);
+        TEMO_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int temo_b200_problem_bounds(int problem, uint64_t d, uint64_t m, double* lower, double* upper) {
+    return guarded([&] {
+        require(lower && upper, "problem_bounds: null argument");
+        problem_bounds(problem, d, m, lower, upper);
+    });
+}
+
+uint64_t temo_b200_problem_default_dim(int problem, uint64_t m) { return problem_default_dim(problem, m); }
+
+// ---- refvec.hpp ---------------------------------------------------------------------------------
+uint64_t temo_b200_lattice_count(uint64_t m, uint64_t H) { return lattice_count(m, H); }
+uint64_t temo_b200_lattice_density_for(uint64_t m, uint64_t target) { return lattice_density_for(m, target); }
+
+int temo_b200_simplex_lattice(uint64_t m, uint64_t H, double* out) {
+    return guarded([&] {
+        require(out != nullptr, "simplex_lattice: null argument");
+        const std::vector<double> lat = simplex_lattice(m, H);
+        std::memcpy(out, lat.data(), lat.size() * sizeof(double));
+    });
+}
+
+int temo_b200_min_vector_angles(const double* v, uint64_t r, uint64_t m, double* gamma) {
+    return guarded([&] {
+        require(v && gamma, "min_vector_angles: null argument");
+        require(r >= 2, "min_vector_angles: needs at least two vectors");
+        Context& cx = ctx();
+        cudaStream_t s = cx.stream;
+        DevBuf<double> dv(v, r * m, s), dvn(r), dg(r);
+        DevBuf<uint32_t> err(1);
+        TEMO_CUDA(cudaMemsetAsync(err.p, 0, sizeof(uint32_t), s));
+        launch_row_norms(dv.p, r, m, dvn.p, s);
+        launch_gamma(dv.p, dvn.p, r, m, dg.p, err.p, nullptr, s);
+        uint32_t flag = 0;
+        err.to_host(&flag, s);
+        dg.to_host(gamma, s);
+        TEMO_CUDA(cudaStreamSynchronize(s));
+        require(!(flag & 1u), "min_vector_angles: duplicate reference vectors");
+    });
+}
+
+int temo_b200_make_ref_set(uint64_t m, uint64_t H, double* v0, double* gamma) {
+    return guarded([&] {
+        require(v0 && gamma, "make_ref_set: null argument");
+        const uint64_t r = lattice_count(m, H);
+        const std::vector<double> unit = normalize_to_unit(simplex_lattice(m, H), r, m);
+        std::memcpy(v0, unit.data(), unit.size() * sizeof(double));
+        const int rc = temo_b200_min_vector_angles(v0, r, m, gamma);
+        if (rc) fail(rc, g_error);
+    });
+}
+
+int temo_b200_adapt(const double* v0, double* v, double* gamma, uint64_t r, uint64_t m, const double* z_min,
+                    const double* z_max) {
+    return guarded([&] {
+        require(v0 && v && gamma && z_min && z_max, "adapt: null argument");
+        require(r >= 2, "min_vector_angles: needs at least two vectors");
+        for (uint64_t k = 0; k < m; ++k)
+            if (!(z_max[k] > z_min[k])) return;  // refvec.hpp:136-137: nothing changes
+        Context& cx = ctx();
+        cudaStream_t s = cx.stream;
+        DevBuf<double> dv0(v0, r * m, s), dv(v, r * m, s), dvn(r), dg(r), dzmin(z_min, m, s), dzmax(z_max, m, s);
+        DevBuf<uint32_t> flags(2);
+        TEMO_CUDA(cudaMemsetAsync(flags.p, 0, 2 * sizeof(uint32_t), s));
+        launch_adapt_vectors(dv0.p, dv.p, dvn.p, r, m, dzmin.p, dzmax.p, flags.p + 1, flags.p, s);
+        launch_gamma(dv.p, dvn.p, r, m, dg.p, flags.p, flags.p + 1, s);
+        uint32_t h[2] = {0, 0};
+        flags.to_host(h, s);
+        std::vector<double> nv(r * m), ng(r);
+        dv.to_host(nv.data(), s);
+        dg.to_host(ng.data(), s);
+        TEMO_CUDA(cudaStreamSynchronize(s));
+        require(!(h[0] & 2u), "normalize_to_unit: zero row");
+        require(!(h[0] & 1u), "min_vector_angles: duplicate reference vectors");
+        std::memcpy(v, nv.data(), nv.size() * sizeof(double));
+        std::memcpy(gamma, ng.data(), ng.size() * sizeof(double));
+    });
+}
+
+// ---- selection.hpp --------------------------------------------------------------------------------
+double temo_b200_apd_penalty(uint64_t m, uint64_t t, uint64_t t_max, double alpha) {
+    return apd_penalty(m, t, t_max, alpha);
+}
+
+int temo_b200_rv_select(const double* f, uint64_t n, uint64_t m, const double* v, const double* gamma, uint64_t r,
+                        uint64_t t, uint64_t t_max, double alpha, uint64_t* elite, uint64_t* n_elite,
+                        unsigned char* validity, uint64_t* assoc, double* theta, double* apd) {
+    return guarded([&] {
+        require(f && v && gamma && elite && n_elite && validity, "rv_select: null argument");
+        require(t_max >= 1, "rv_select: t_max must be positive");  // selection.hpp:151
+        require(n >= 1, "translate: empty objective tensor");
+        require(r >= 1, "rv_select: no reference vectors");
+        Context& cx = ctx();
+        cudaStream_t s = cx.stream;
+        DevBuf<double> df(f, n * m, s), dv(v, r * m, s), dg(gamma, r, s);
+        SelectWorkspace ws;
+        ws.alloc(n, r, m);
+        struct Guard {
+            SelectWorkspace& w;
+            ~Guard() { w.release(); }
+        } guard{ws};
+        launch_row_norms(dv.p, r, m, ws.vn, s);
+        launch_select(df.p, n, nullptr, m, dv.p, dg.p, r, apd_penalty(m, t, t_max, alpha), ws, s);
+        uint32_t cnt = 0, flag = 0;
+        std::vector<uint32_t> h_elite(r), h_assoc(assoc ? n : 0);
+        TEMO_CUDA(cudaMemcpyAsync(&cnt, ws.n_elite, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+        TEMO_CUDA(cudaMemcpyAsync(&flag, ws.err_flag, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+        TEMO_CUDA(cudaMemcpyAsync(h_elite.data(), ws.elite, r * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+        TEMO_CUDA(cudaMemcpyAsync(validity, ws.valid, r, cudaMemcpyDeviceToHost, s));
+        if (assoc) TEMO_CUDA(cudaMemcpyAsync(h_assoc.data(), ws.assoc, n * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+        if (theta) TEMO_CUDA(cudaMemcpyAsync(theta, ws.theta, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+        if (apd) TEMO_CUDA(cudaMemcpyAsync(apd, ws.apd, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+        TEMO_CUDA(cudaStreamSynchronize(s));
+        require(!(flag & 1u), "rv_select: gamma must be positive");  // selection.hpp:152
+        *n_elite = cnt;
+        for (uint32_t k = 0; k < cnt; ++k) elite[k] = h_elite[k];
+        if (assoc)
+            for (uint64_t i = 0; i < n; ++i) assoc[i] = h_assoc[i];
+    });
+}
+
+// ---- algorithms.hpp ----------------------------------------------------------------------------------
+struct temo_b200_run {
+    std::unique_ptr<Run> impl;
+};
+
+int temo_b200_run_create(const temo_b200_run_config* cfg, temo_b200_run** out) {
+    return guarded([&] {
+        require(out != nullptr, "run_create: null output");
+        *out = nullptr;
+        std::unique_ptr<temo_b200_run> h(new temo_b200_run);
+        h->impl.reset(new Run(cfg_of(cfg)));
+        *out = h.release();
+    });
+}
+
+int temo_b200_run_step(temo_b200_run* run, uint64_t* pop_size, double* survivors_f) {
+    return guarded([&] {
+        require(run && run->impl, "run_step: null run");
+        const uint64_t p = run->impl->step(survivors_f);
+        if (pop_size) *pop_size = p;
+    });
+}
+
+int temo_b200_run_inject(temo_b200_run* run, uint64_t rows, const double* x, const double* f, const double* v,
+                         const double* gamma, uint64_t counter, uint64_t t) {
+    return guarded([&] {
+        require(run && run->impl, "run_inject: null run");
+        run->impl->inject(rows, x, f, v, gamma, counter, t);
+    });
+}
+
+int temo_b200_run_state(temo_b200_run* run, uint64_t* rows, uint64_t* counter, uint64_t* t, uint64_t* r,
+                        uint64_t* d, uint64_t* m) {
+    return guarded([&] {
+        require(run && run->impl, "run_state: null run");
+        const Run& R = *run->impl;
+        if (rows) *rows = R.P;
+        if (counter) *counter = R.counter;
+        if (t) *t = R.t;
+        if (r) *r = R.r;
+        if (d) *d = R.d;
+        if (m) *m = R.m;
+    });
+}
+
+int temo_b200_run_download(temo_b200_run* run, double* x, double* f, double* v, double* gamma) {
+    return guarded([&] {
+        require(run && run->impl, "run_download: null run");
+        run->impl->download(x, f, v, gamma);
+    });
+}
+
+int temo_b200_run_last_generation(temo_b200_run* run, double* offspring, double* f_off, uint64_t* elite) {
+    return guarded([&] {
+        require(run && run->impl, "run_last_generation: null run");
+        run->impl->last_generation(offspring, f_off, elite);
+    });
+}
+
+int temo_b200_run_timings(temo_b200_run* run, double* ms8) {
+    return guarded([&] {
+        require(run && run->impl && ms8, "run_timings: null argument");
+        std::memcpy(ms8, run->impl->timings, 8 * sizeof(double));
+    });
+}
+
+int temo_b200_run_time_stage(temo_b200_run* run, int stage, int reps, double* mean_ms) {
+    return guarded([&] {
+        require(run && run->impl && mean_ms, "run_time_stage: null argument");
+        *mean_ms = run->impl->time_stage(stage, reps);
+    });
+}
+
+int temo_b200_run_destroy(temo_b200_run* run) {
+    return guarded([&] { delete run; });
+}
+
+int temo_b200_rvea_run(const temo_b200_run_config* cfg, double* final_x, double* final_f, uint64_t* final_rows,
+                       uint64_t* rows_done, uint64_t* pop_size, double* elapsed_ms) {
+    return guarded([&] {
+        const auto t0 = std::chrono::steady_clock::now();  // GenerationTimer, algorithms.hpp:193-204
+        Run run(cfg_of(cfg));
+        uint64_t done = 0;
+        for (uint64_t t = 0; t < run.cfg.generations; ++t) {
+            const uint64_t p = run.step(nullptr);
+            const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+            if (pop_size) pop_size[t] = p;
+            if (elapsed_ms) elapsed_ms[t] = ms;
+            ++done;
+            if (run.cfg.time_budget_s > 0.0 && ms >= run.cfg.time_budget_s * 1e3) break;  // algorithms.hpp:291
+        }
+        run.download(final_x, final_f, nullptr, nullptr);
+        if (final_rows) *final_rows = run.P;
+        if (rows_done) *rows_done = done;
+    });
+}
+
+// ---- device-pointer helpers -------------------------------------------------------------------------------
+void* temo_b200_dev_alloc(size_t bytes) {
+    void* p = nullptr;
+    const int rc = guarded([&] {
+        ctx();
+        p = dev_alloc<unsigned char>(bytes);
+    });
+    return rc ? nullptr : p;
+}
+
+int temo_b200_dev_free(void* p) {
+    return guarded([&] { TEMO_CUDA(cudaFree(p)); });
+}
+
+int temo_b200_dev_upload(void* dst, const void* src, size_t bytes) {
+    return guarded([&] { TEMO_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice)); });
+}
+
+int temo_b200_dev_download(void* dst, const void* src, size_t bytes) {
+    return guarded([&] { TEMO_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost)); });
+}
+
+int temo_b200_dev_sync(void) {
+    return guarded([&] { TEMO_CUDA(cudaStreamSynchronize(ctx().stream)); });
+}
+
+int temo_b200_flush_l2(void) {
+    return guarded([&] { flush_l2(); });
+}
+
+}  // extern "C"

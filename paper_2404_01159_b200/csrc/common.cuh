@@ -1,0 +1,118 @@
+// Shared device/host helpers for the temo_b200 kernels (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+
+namespace temo_b200 {
+
+constexpr int kSMs = 148;  // B200: 2 dies x 74 SMs
+constexpr double kPi = 3.141592653589793238462643383279502884;
+
+// ---- errors ---------------------------------------------------------------------------
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] inline void fail(int code, const std::string& msg) { throw Error(code, msg); }
+
+// reference: detail::require (tensor.hpp:63-65)
+inline void require(bool cond, const char* msg) {
+    if (!cond) fail(1 /*EINVAL*/, msg);
+}
+
+#define TEMO_CUDA(expr)                                                                      \
+    do {                                                                                     \
+        cudaError_t err__ = (expr);                                                          \
+        if (err__ != cudaSuccess)                                                            \
+            ::temo_b200::fail(2, std::string(#expr) + ": " + cudaGetErrorString(err__));     \
+    } while (0)
+
+// ---- counter-based randomness -----------------------------------------------------------
+// reference: rng.hpp:23-43. word(seed,k) = mix64(mix64(seed) + k*GOLDEN); uniform = top 53 bits.
+constexpr uint64_t kGolden = 0x9e3779b97f4a7c15ULL;
+
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+
+// Philox4x32-10 (Salmon et al. 2011), counter = (k >> 1, stream tag), key = seed; one call
+// yields two 64-bit words, word (k & 1) is draw k. Not in the reference: parity unpinned.
+__host__ __device__ __forceinline__ uint64_t philox_word(uint64_t seed, uint64_t k) {
+    uint32_t c0 = (uint32_t)(k >> 1), c1 = (uint32_t)(k >> 33), c2 = 0x74656d6fu, c3 = 0x62323030u;
+    uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint64_t p0 = (uint64_t)0xD2511F53u * c0;
+        const uint64_t p1 = (uint64_t)0xCD9E8D57u * c2;
+        const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1 ^ k0;
+        const uint32_t n2 = (uint32_t)(p0 >> 32) ^ c3 ^ k1;
+        c1 = (uint32_t)p1;
+        c3 = (uint32_t)p0;
+        c0 = n0;
+        c2 = n2;
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+    return (k & 1) ? (((uint64_t)c3 << 32) | c2) : (((uint64_t)c1 << 32) | c0);
+}
+
+// RNG policy object passed by value into kernels. `base` is mix64(seed) for SplitMix64.
+struct Rng {
+    uint64_t seed;
+    uint64_t base;
+    int mode;  // 0 SplitMix64 (reference), 1 Philox4x32-10
+};
+
+inline Rng make_rng(uint64_t seed, int mode) { return Rng{seed, mix64(seed), mode}; }
+
+template <int MODE>
+__host__ __device__ __forceinline__ uint64_t draw_word(const Rng& g, uint64_t k) {
+    if (MODE == 0) return mix64(g.base + k * kGolden);
+    return philox_word(g.seed, k);
+}
+
+// Exact (double)(w >> 11) * 2^-53 without an integer->double conversion: the low 32 and the
+// high 21 bits of the 53-bit integer are planted into the mantissas of 0.5 and 2^31 (whose
+// ulps are 2^-53 and 2^-21); removing the offsets leaves lo*2^-53 and hi*2^-21, and their
+// sum has at most 53 significant bits, so every step is exact.
+__host__ __device__ __forceinline__ double word_to_unit(uint64_t w) {
+    const uint64_t u = w >> 11;
+#ifdef __CUDA_ARCH__
+    const double lo = __longlong_as_double(0x3FE0000000000000LL | (long long)(u & 0xffffffffULL)) - 0.5;
+    const double hi = __longlong_as_double(0x41E0000000000000LL | (long long)(u >> 32)) - 2147483648.0;
+    return hi + lo;
+#else
+    return (double)u * 0x1.0p-53;
+#endif
+}
+
+// ---- scalar conventions (tensor.hpp:73-87) ------------------------------------------------
+__host__ __device__ __forceinline__ double clampd(double x, double lo, double hi) {
+    return x < lo ? lo : (x > hi ? hi : x);
+}
+
+// ---- block reductions with a fixed (launch-shape independent of the GPU count) order -------
+// Sum over the block in a canonical tree: xor-shuffle butterfly inside each warp, then the
+// warp totals are added in ascending warp order by every thread (all threads get the result).
+template <int MAXW>
+__device__ __forceinline__ double block_sum(double v, double* smem /* MAXW doubles */) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    const int warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) smem[warp] = v;
+    __syncthreads();
+    double s = smem[0];
+    for (int w = 1; w < nw; ++w) s += smem[w];
+    return s;
+}
+
+}  // namespace temo_b200

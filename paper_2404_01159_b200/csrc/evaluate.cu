@@ -1,0 +1,250 @@
+// K2 — objective evaluation as bandwidth-bound row reductions.
+//
+// reference: dtlz_eval (problems.hpp:69-92) behind ProblemInstance::evaluate
+// (problems.hpp:252); LSMOP1 is an extension (not in the reference: parity unpinned).
+// Algorithmic traffic: 8*n*d bytes read + 8*n*m written.
+//
+// Two DTLZ paths with bit-identical results (same thread->gene mapping, same reduction tree
+// as the epilogue fused into reproduce.cu):
+//   eval_tma_kernel  persistent CTAs; an elected thread streams row chunks into a shared-
+//                    memory ring with cp.async.bulk (TMA, SASS UBLKCP) + mbarrier
+//                    complete_tx; needs 16-byte aligned rows (d even).
+//   eval_ldg_kernel  one CTA per row with plain (128-bit when d is even) loads; any shape.
+#include "internal.h"
+#include "problems.cuh"
+
+namespace temo_b200 {
+
+namespace {
+
+struct EvalK {
+    const double* x;
+    const uint32_t* rows;
+    uint64_t n, d, m;
+    double* f;
+    uint64_t f_row0;
+    const uint32_t* f_row0_dev;
+};
+
+template <int PID, int VEC>
+__global__ void __launch_bounds__(256) eval_ldg_kernel(const EvalK a) {
+    __shared__ double s_red[8];
+    __shared__ double s_pos[kMaxObj];
+    const uint64_t i = blockIdx.x;
+    const uint64_t row = a.rows ? a.rows[i] : i;
+    const double* p = a.x + row * a.d;
+    double acc = 0.0;
+    const uint64_t nvec = a.d / VEC;
+    for (uint64_t q = threadIdx.x; q < nvec; q += blockDim.x) {
+        const uint64_t j0 = q * VEC;
+        double xv[VEC];
+        if (VEC == 2) {
+            const double2 t = *reinterpret_cast<const double2*>(p + j0);
+            xv[0] = t.x;
+            xv[VEC - 1] = t.y;
+        } else {
+            xv[0] = p[j0];
+        }
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) {
+            const uint64_t j = j0 + v;
+            if (j + 1 >= a.m)
+                acc += dtlz_term<PID>(xv[v]);
+            else
+                s_pos[j] = xv[v];
+        }
+    }
+    const double sum = block_sum<8>(acc, s_red);
+    const uint64_t f0 = a.f_row0 + (a.f_row0_dev ? (uint64_t)*a.f_row0_dev : 0);
+    dtlz_finish<PID>(sum, s_pos, a.m, a.d, a.f + (f0 + i) * a.m);
+}
+
+// ---- TMA path ---------------------------------------------------------------------------------
+constexpr int kChunkGenes = 4096;  // 32 KB per stage; multiple of B*VEC = 512 keeps the canonical order
+constexpr int kStages = 3;         // 96 KB ring -> two CTAs per SM
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_LOOP:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@p bra DONE;\n"
+        "bra WAIT_LOOP;\n"
+        "DONE:\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// 1-D bulk async copy global -> shared, completion signalled on the mbarrier (TMA unit).
+__device__ __forceinline__ void tma_load_1d(void* dst_smem, const void* src_gmem, uint32_t bytes,
+                                            uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst_smem)),
+        "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// Persistent: CTA c handles rows c, c+grid, ... ; every row is ceil(d/kChunkGenes) chunks that
+// flow through a kStages-deep ring. Thread 0 is the producer (issues the next bulk copy as soon
+// as a stage has been drained), all 256 threads consume. d must be even (16-byte rows).
+template <int PID>
+__global__ void __launch_bounds__(256) eval_tma_kernel(const EvalK a) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    double* ring = reinterpret_cast<double*>(smem_raw);  // kStages x kChunkGenes
+    __shared__ __align__(8) uint64_t full_bar[kStages];
+    __shared__ double s_red[8];
+    __shared__ double s_pos[kMaxObj];
+
+    const uint64_t chunks_per_row = (a.d + kChunkGenes - 1) / kChunkGenes;
+    const uint64_t my_rows = a.n > blockIdx.x ? (a.n - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    const uint64_t total = my_rows * chunks_per_row;  // chunks this CTA will consume
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) mbar_init(&full_bar[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    auto issue = [&](uint64_t c) {  // producer: start the copy of this CTA's c-th chunk
+        const uint64_t local_row = c / chunks_per_row, ch = c - local_row * chunks_per_row;
+        const uint64_t i = blockIdx.x + local_row * gridDim.x;
+        const uint64_t row = a.rows ? a.rows[i] : i;
+        const uint64_t g0 = ch * kChunkGenes;
+        const uint32_t genes = (uint32_t)((a.d - g0) < (uint64_t)kChunkGenes ? (a.d - g0) : kChunkGenes);
+        const int st = (int)(c % kStages);
+        mbar_expect_tx(&full_bar[st], genes * 8u);
+        tma_load_1d(ring + (size_t)st * kChunkGenes, a.x + row * a.d + g0, genes * 8u, &full_bar[st]);
+    };
+
+    if (threadIdx.x == 0)
+        for (uint64_t c = 0; c < total && c < (uint64_t)kStages; ++c) issue(c);
+
+    const uint64_t f0 = a.f_row0 + (a.f_row0_dev ? (uint64_t)*a.f_row0_dev : 0);
+    double acc = 0.0;
+    for (uint64_t c = 0; c < total; ++c) {
+        const uint64_t local_row = c / chunks_per_row, ch = c - local_row * chunks_per_row;
+        const int st = (int)(c % kStages);
+        mbar_wait(&full_bar[st], (uint32_t)((c / kStages) & 1));
+        const uint64_t g0 = ch * kChunkGenes;
+        const uint32_t genes = (uint32_t)((a.d - g0) < (uint64_t)kChunkGenes ? (a.d - g0) : kChunkGenes);
+        const double2* tile = reinterpret_cast<const double2*>(ring + (size_t)st * kChunkGenes);
+        // canonical order: global vector index q = g0/2 + t, t = tid, tid+256, ...
+        for (uint32_t t = threadIdx.x; t < genes / 2; t += 256) {
+            const double2 v = tile[t];
+            const uint64_t j = g0 + 2ull * t;
+            if (j + 1 >= a.m) acc += dtlz_term<PID>(v.x); else s_pos[j] = v.x;
+            if (j + 2 >= a.m) acc += dtlz_term<PID>(v.y); else s_pos[j + 1] = v.y;
+        }
+        __syncthreads();  // stage drained by everyone
+        if (threadIdx.x == 0 && c + kStages < total) issue(c + kStages);
+        if (ch + 1 == chunks_per_row) {  // row complete
+            const double sum = block_sum<8>(acc, s_red);
+            const uint64_t i = blockIdx.x + local_row * gridDim.x;
+            dtlz_finish<PID>(sum, s_pos, a.m, a.d, a.f + (f0 + i) * a.m);
+            acc = 0.0;
+            __syncthreads();  // s_pos / s_red free for the next row
+        }
+    }
+}
+
+// ---- LSMOP1 --------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) eval_lsmop1_kernel(const EvalK a, const LsmopLayout lay) {
+    __shared__ double s_red[8];
+    __shared__ double s_g[kMaxObj];
+    const uint64_t i = blockIdx.x;
+    const uint64_t row = a.rows ? a.rows[i] : i;
+    const double* p = a.x + row * a.d;
+    const double x0 = p[0];
+    const double dd = (double)a.d;
+    for (uint64_t grp = 0; grp < a.m; ++grp) {
+        double acc = 0.0;
+        for (uint64_t q = lay.start[grp] + threadIdx.x; q < lay.start[grp + 1]; q += blockDim.x) {
+            const uint64_t j = a.m - 1 + q;
+            const double y = (1.0 + (double)(j + 1) / dd) * p[j] - 10.0 * x0;
+            acc += y * y;
+        }
+        const double sum = block_sum<8>(acc, s_red);
+        if (threadIdx.x == 0) s_g[grp] = lay.sublen[grp] ? sum / (double)lay.sublen[grp] / (double)kLsmopNk : 0.0;
+    }
+    __syncthreads();
+    const uint64_t f0 = a.f_row0 + (a.f_row0_dev ? (uint64_t)*a.f_row0_dev : 0);
+    double* frow = a.f + (f0 + i) * a.m;
+    for (uint64_t o = threadIdx.x; o < a.m; o += blockDim.x) {
+        double v = 1.0 + s_g[o];
+        for (uint64_t k = 0; k + o + 1 < a.m; ++k) v *= p[k];
+        if (o > 0) v *= 1.0 - p[a.m - 1 - o];
+        frow[o] = v;
+    }
+}
+
+template <int PID>
+void launch_dtlz(const EvalK& k, bool tma, cudaStream_t s) {
+    const int vec = row_vec(k.d), block = row_block(k.d);
+    if (tma && vec == 2 && block == 256) {
+        const size_t smem = (size_t)kStages * kChunkGenes * sizeof(double);
+        static bool configured = false;
+        if (!configured) {
+            TEMO_CUDA(cudaFuncSetAttribute(eval_tma_kernel<PID>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            configured = true;
+        }
+        uint64_t grid = (uint64_t)kSMs * 2;
+        if (grid > k.n) grid = k.n;
+        eval_tma_kernel<PID><<<(unsigned)grid, 256, smem, s>>>(k);
+    } else if (vec == 2) {
+        eval_ldg_kernel<PID, 2><<<(unsigned)k.n, block, 0, s>>>(k);
+    } else {
+        eval_ldg_kernel<PID, 1><<<(unsigned)k.n, block, 0, s>>>(k);
+    }
+}
+
+}  // namespace
+
+LsmopLayout lsmop1_layout(uint64_t d, uint64_t m) {
+    // LSMOP suite (Cheng et al. 2017): logistic-map group sizes, nk = 5 sub-components.
+    LsmopLayout lay{};
+    double c[kMaxObj];
+    double sum = 0.0;
+    c[0] = 3.8 * 0.1 * (1.0 - 0.1);
+    for (uint64_t i = 1; i < m; ++i) c[i] = 3.8 * c[i - 1] * (1.0 - c[i - 1]);
+    for (uint64_t i = 0; i < m; ++i) sum += c[i];
+    lay.start[0] = 0;
+    for (uint64_t i = 0; i < m; ++i) {
+        lay.sublen[i] = (uint32_t)std::floor(c[i] / sum * (double)(d - m + 1) / (double)kLsmopNk);
+        lay.start[i + 1] = lay.start[i] + lay.sublen[i] * kLsmopNk;
+    }
+    return lay;
+}
+
+void launch_evaluate(const EvalArgs& a, cudaStream_t s) {
+    require(problem_known(a.problem), "evaluate: unknown problem");
+    if (a.problem <= kDtlz4) require(a.problem >= 1, "dtlz_eval: id must be in 1..4");  // problems.hpp:70
+    require(a.m >= 2, "dtlz_eval: m must be at least 2");                                // problems.hpp:71
+    require(a.d >= a.m, "dtlz_eval: d must be at least m");                              // problems.hpp:72
+    require(a.m <= (uint64_t)kMaxObj, "evaluate: more than 32 objectives are not supported");
+    if (a.n == 0) return;
+    EvalK k{a.x, a.rows, a.n, a.d, a.m, a.f, a.f_row0, a.f_row0_dev};
+    switch (a.problem) {
+    case kDtlz1: launch_dtlz<kDtlz1>(k, a.allow_tma, s); break;
+    case kDtlz2: launch_dtlz<kDtlz2>(k, a.allow_tma, s); break;
+    case kDtlz3: launch_dtlz<kDtlz3>(k, a.allow_tma, s); break;
+    case kDtlz4: launch_dtlz<kDtlz4>(k, a.allow_tma, s); break;
+    case kLsmop1:
+        eval_lsmop1_kernel<<<(unsigned)a.n, row_block(a.d), 0, s>>>(k, lsmop1_layout(a.d, a.m));
+        break;
+    }
+    TEMO_CUDA(cudaGetLastError());
+}
+
+}  // namespace temo_b200

@@ -1,0 +1,152 @@
+// Internal launch interface between the kernel translation units, the run driver and the
+// C ABI (capi.cu). Everything lives in namespace temo_b200; nothing here is exported.
+#pragma once
+
+#include <cstdint>
+#include <vector>
+
+#include "common.cuh"
+
+namespace temo_b200 {
+
+// Problem ids (mirrors include/temo_b200.h).
+constexpr int kDtlz1 = 1, kDtlz2 = 2, kDtlz3 = 3, kDtlz4 = 4, kLsmop1 = 101;
+constexpr int kMaxObj = 32;   // objectives supported by the on-device evaluators/selection
+constexpr int kLsmopNk = 5;
+
+// Canonical row mapping shared by the evaluation kernels (fused and standalone) so that
+// their reductions associate identically: VEC genes per load, B threads per row.
+inline int row_vec(uint64_t d) { return (d % 2 == 0) ? 2 : 1; }
+inline int row_block(uint64_t d) {
+    const uint64_t nvec = d / row_vec(d);
+    uint64_t b = ((nvec + 31) / 32) * 32;
+    if (b < 32) b = 32;
+    if (b > 256) b = 256;
+    return (int)b;
+}
+
+// LSMOP1 group layout (host-computed, passed by value to kernels).
+struct LsmopLayout {
+    uint32_t start[kMaxObj + 1];  // tail-relative first gene of each group
+    uint32_t sublen[kMaxObj];
+};
+LsmopLayout lsmop1_layout(uint64_t d, uint64_t m);
+
+struct GaParams {
+    double pc = 1.0, eta = 20.0, pm = 1.0, xi = 20.0;  // operators.hpp:22-27
+};
+
+// ---- K1: reproduction ---------------------------------------------------------------------
+struct ReproArgs {
+    const double* pool = nullptr;   // parent storage, row stride d
+    const uint32_t* src = nullptr;  // [n] storage row of mating row i (nullptr: i)
+    double* out = nullptr;          // child storage, row stride d
+    const uint32_t* dst = nullptr;  // [n] storage row of child i (nullptr: i)
+    uint64_t n = 0, d = 0;
+    Rng rng{};
+    uint64_t c_sbx = 0;   // counter of the first SBX block (Mc); R1, R2, R3 follow (operators.hpp:70-73)
+    uint64_t c_pm = 0;    // counter of the mask block R4; Mmut follows (operators.hpp:130-131)
+    GaParams ga;
+    const double* lower = nullptr;
+    const double* upper = nullptr;
+    bool do_sbx = true, do_pm = true;
+    // fused evaluation of the children (0 = off): problem id, m, output rows f_out[(f_row0+i)*m..]
+    int eval_problem = 0;
+    uint64_t m = 0;
+    double* f_out = nullptr;
+    uint64_t f_row0 = 0;
+    const uint32_t* f_row0_dev = nullptr;  // optional device-side row offset (survivor count)
+};
+void launch_reproduce(const ReproArgs& a, cudaStream_t s);
+
+// random_reproduce (operators.hpp:287-296) and uniform_tensor (rng.hpp:55-66).
+void launch_random_reproduce(double* out, const uint32_t* dst, uint64_t n, uint64_t d, Rng rng,
+                             uint64_t counter, const double* lower, const double* upper,
+                             cudaStream_t s);
+void launch_uniform_fill(double* out, uint64_t count, Rng rng, uint64_t counter, cudaStream_t s);
+
+// ---- K2: evaluation -------------------------------------------------------------------------
+struct EvalArgs {
+    int problem = 0;
+    const double* x = nullptr;      // storage base, row stride d
+    const uint32_t* rows = nullptr; // [n] storage row of logical row i (nullptr: i)
+    uint64_t n = 0, d = 0, m = 0;
+    double* f = nullptr;            // f[(f_row0 + i) * m + j]
+    uint64_t f_row0 = 0;
+    const uint32_t* f_row0_dev = nullptr;
+    bool allow_tma = true;
+};
+void launch_evaluate(const EvalArgs& a, cudaStream_t s);
+
+// ---- K3: selection ----------------------------------------------------------------------------
+struct SelectWorkspace {
+    // sized for rows_cap merged rows and r vectors
+    uint64_t rows_cap = 0, r = 0, m = 0;
+    double* z = nullptr;              // [m] ideal point
+    unsigned long long* zkey = nullptr;  // [m] ordered-int min keys
+    double* vn = nullptr;             // [r] ||v_j||
+    uint32_t* assoc = nullptr;        // [rows_cap]
+    double* theta = nullptr;          // [rows_cap]
+    double* apd = nullptr;            // [rows_cap]
+    unsigned long long* best_key = nullptr;  // [r]
+    uint32_t* best_row = nullptr;     // [r]
+    uint32_t* first_row = nullptr;    // [r]
+    uint32_t* elite = nullptr;        // [r] merged-row index per valid vector (compacted)
+    unsigned char* valid = nullptr;   // [r]
+    uint32_t* n_elite = nullptr;      // [1]
+    uint32_t* err_flag = nullptr;     // [1] bit0: gamma <= 0
+    void alloc(uint64_t rows_cap_, uint64_t r_, uint64_t m_);
+    void release();
+};
+// n_rows_dev (optional): device-side row count overriding n_rows (<= n_rows, which then only
+// sizes the grid).
+void launch_select(const double* f, uint64_t n_rows, const uint32_t* n_rows_dev, uint64_t m,
+                   const double* v, const double* gamma, uint64_t r, double penalty,
+                   SelectWorkspace& ws, cudaStream_t s);
+void launch_row_norms(const double* v, uint64_t r, uint64_t m, double* vn, cudaStream_t s);
+
+// ---- K4: reference vectors ----------------------------------------------------------------------
+// gamma_i = acos(max_{j != i} cos(v_i, v_j)) (refvec.hpp:81-100); err_flag bit0 set if any <= 0.
+void launch_gamma(const double* v, const double* vn, uint64_t r, uint64_t m, double* gamma,
+                  uint32_t* err_flag, const uint32_t* skip_flag, cudaStream_t s);
+// zmin/zmax over rows [0, n_rows) of f (tensor.hpp:211-229).
+void launch_col_minmax(const double* f, uint64_t n_rows, const uint32_t* n_rows_dev, uint64_t m,
+                       double* zmin, double* zmax, unsigned long long* scratch2m, cudaStream_t s);
+// adapt_vectors (refvec.hpp:119-131): v = unit(v0 * (zmax - zmin)); skip_flag[0] is set to 1
+// (and v left untouched) unless every range is > 0; err bit1 on a zero row.
+void launch_adapt_vectors(const double* v0, double* v, double* vn, uint64_t r, uint64_t m,
+                          const double* zmin, const double* zmax, uint32_t* skip_flag,
+                          uint32_t* err_flag, cudaStream_t s);
+
+// ---- host-side pieces (host_ops.cu) ---------------------------------------------------------------
+uint64_t lattice_count(uint64_t m, uint64_t H);
+uint64_t lattice_density_for(uint64_t m, uint64_t target);
+std::vector<double> simplex_lattice(uint64_t m, uint64_t H);
+std::vector<double> normalize_to_unit(const std::vector<double>& v, uint64_t r, uint64_t m);
+void shuffle_indices(uint64_t seed, uint64_t& counter, uint64_t n, uint32_t* perm);
+double apd_penalty(uint64_t m, uint64_t t, uint64_t t_max, double alpha);
+void problem_bounds(int problem, uint64_t d, uint64_t m, double* lower, double* upper);
+uint64_t problem_default_dim(int problem, uint64_t m);
+bool problem_known(int problem);
+
+// ---- device context -----------------------------------------------------------------------------------
+struct Context {
+    int device = -1;
+    cudaStream_t stream = nullptr;
+    cudaStream_t copy_stream = nullptr;
+    void* flush_buf = nullptr;
+    size_t flush_bytes = 0;
+};
+void init_context(int device);
+Context& ctx();  // initialises device 0 on first use; throws ENODEV without a GPU
+
+template <class T>
+T* dev_alloc(size_t count) {
+    T* p = nullptr;
+    if (count == 0) count = 1;
+    cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+    if (e != cudaSuccess) fail(4, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    return p;
+}
+
+}  // namespace temo_b200

@@ -1,0 +1,311 @@
+// K1 — fused GA reproduction: mating gather + SBX crossover + polynomial mutation
+// (+ optional objective evaluation of the children) in ONE pass over the population.
+//
+// reference: ga_reproduce (operators.hpp:153-161) = shuffle_indices -> row gather -> sbx
+// (operators.hpp:65-102) -> polynomial_mutation (operators.hpp:126-149), which on the CPU is
+// six full N x d passes plus five materialised N x d random tensors. Here every random
+// number is re-derived in registers from its (seed, counter) address (rng.hpp:39-43; SURVEY.md
+// Appendix A gives the counter map), the shuffled/pooled parent matrix is never built (the
+// kernel reads parent rows through the `src` indirection) and children are written straight
+// into free rows of the population pool (`dst`): algorithmic traffic = 16*N*d bytes.
+//
+// Mapping: one CTA per mating pair (rows p and half+p of the shuffled order); thread t owns
+// gene vectors t, t+B, ... (VEC = 2 doubles = one 128-bit load/store when d is even), which
+// is the canonical order the evaluation reductions share with evaluate.cu.
+//
+// Exactness (compiled with --fmad=false): all blends, clamps and copies are the reference's
+// IEEE operations in the reference's order. Dead branches the reference multiplies by an
+// exact 0.0 are skipped (verified bit-identical); the only inexact pieces are
+// CUDA's pow (<= 2 ulp) on crossed/mutated genes.
+#include "internal.h"
+#include "problems.cuh"
+
+namespace temo_b200 {
+
+namespace {
+
+struct ReproK {
+    const double* pool;
+    const uint32_t* src;
+    double* out;
+    const uint32_t* dst;
+    uint64_t n, d, half;
+    Rng rng;
+    uint64_t c_mc, c_r1, c_r2, c_r3, c_mask, c_mut;
+    double pc, inv_exp, xi;
+    uint64_t mask_thresh;  // mutate iff (word >> 11) <= mask_thresh
+    int mask_never;
+    const double* lower;
+    const double* upper;
+    uint64_t m;
+    double* f_out;
+    uint64_t f_row0;
+    const uint32_t* f_row0_dev;
+};
+
+// polynomial_delta (operators.hpp:106-121): both branches evaluated, blended by steps.
+__device__ __noinline__ double polynomial_delta_dev(double u, double x, double lo, double hi, double xi) {
+    const double range = hi - lo;
+    const double e = xi + 1.0, inv_e = 1.0 / e;
+    const double near_lo = 1.0 - (x - lo) / range;
+    const double d_lo = range * (pow(2.0 * u + (1.0 - 2.0 * u) * pow(near_lo, e), inv_e) - 1.0);
+    const double near_hi = 1.0 - (hi - x) / range;
+    const double d_hi = range * (1.0 - pow(2.0 * (1.0 - u) + 2.0 * (u - 0.5) * pow(near_hi, e), inv_e));
+    const double h_lo = (0.5 - u) >= 0.0 ? 1.0 : 0.0;
+    const double h_hi = (u - 0.5) >= 0.0 ? 1.0 : 0.0;
+    return d_lo * h_lo + d_hi * h_hi;
+}
+
+template <int MODE, bool SBX, bool PM, int EVAL, int VEC>
+__global__ void __launch_bounds__(256) reproduce_kernel(const ReproK a) {
+    __shared__ double s_red[8];
+    __shared__ double s_pos[2][kMaxObj];
+
+    const uint64_t unit = blockIdx.x;
+    const bool paired = SBX && unit < a.half;
+    // shuffled-order rows handled by this CTA
+    const uint64_t row_a = SBX ? (paired ? unit : a.n - 1) : unit;
+    const uint64_t row_b = a.half + unit;  // only meaningful when paired
+
+    const uint64_t src_a = a.src ? a.src[row_a] : row_a;
+    const uint64_t dst_a = a.dst ? a.dst[row_a] : row_a;
+    const double* pa = a.pool + src_a * a.d;
+    double* oa = a.out + dst_a * a.d;
+    const double* pb = nullptr;
+    double* ob = nullptr;
+    if (paired) {
+        const uint64_t src_b = a.src ? a.src[row_b] : row_b;
+        const uint64_t dst_b = a.dst ? a.dst[row_b] : row_b;
+        pb = a.pool + src_b * a.d;
+        ob = a.out + dst_b * a.d;
+    }
+
+    // pair-level crossover switch: hc = H(r3 - pc) (operators.hpp:82)
+    bool pair_cross = false;
+    if (paired) {
+        const double r3 = word_to_unit(draw_word<MODE>(a.rng, a.c_r3 + unit));
+        pair_cross = !(r3 - a.pc >= 0.0);
+    }
+
+    double acc_a = 0.0, acc_b = 0.0;
+    const uint64_t nvec = a.d / VEC;
+    const uint64_t e_pair = unit * a.d;   // element offset inside the half x d SBX blocks
+    const uint64_t e_a = row_a * a.d;     // element offsets inside the n x d PM blocks
+    const uint64_t e_b = row_b * a.d;
+
+    for (uint64_t q = threadIdx.x; q < nvec; q += blockDim.x) {
+        const uint64_t j0 = q * VEC;
+        double xa[VEC], xb[VEC];
+        if (VEC == 2) {
+            const double2 t = *reinterpret_cast<const double2*>(pa + j0);
+            xa[0] = t.x;
+            xa[VEC - 1] = t.y;
+            if (paired) {
+                const double2 w = *reinterpret_cast<const double2*>(pb + j0);
+                xb[0] = w.x;
+                xb[VEC - 1] = w.y;
+            }
+        } else {
+            xa[0] = pa[j0];
+            if (paired) xb[0] = pb[j0];
+        }
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) {
+            const uint64_t j = j0 + v;
+            const double lo = a.lower[j], hi = a.upper[j];
+            double ca = xa[v], cb = paired ? xb[v] : 0.0;
+            if (SBX && paired) {
+                const uint64_t e = e_pair + j;
+                const uint64_t w2 = draw_word<MODE>(a.rng, a.c_r2 + e);
+                const bool keep = (w2 >> 63) != 0;  // hr = H(r2 - 0.5): top bit of the word
+                if (pair_cross && !keep) {
+                    const double mc = word_to_unit(draw_word<MODE>(a.rng, a.c_mc + e));
+                    const uint64_t w1 = draw_word<MODE>(a.rng, a.c_r1 + e);
+                    // live spread branch only (hm = H(0.5 - mc)); the other is multiplied by 0.0
+                    double spread;
+                    if (0.5 - mc >= 0.0)
+                        spread = pow(2.0 * mc, a.inv_exp);
+                    else
+                        spread = pow(2.0 - 2.0 * mc, -a.inv_exp);
+                    const double b = (w1 >> 63) ? spread : -spread;  // sgn(r1 - 0.5) * spread
+                    ca = ((1.0 + b) * xa[v] + (1.0 - b) * xb[v]) / 2.0;
+                    cb = ((1.0 - b) * xa[v] + (1.0 + b) * xb[v]) / 2.0;
+                }
+                ca = clampd(ca, lo, hi);
+                cb = clampd(cb, lo, hi);
+            }
+            if (PM && !a.mask_never) {
+                const bool live = !(hi - lo <= 0.0);
+                const uint64_t w4a = draw_word<MODE>(a.rng, a.c_mask + e_a + j);
+                if (live && (w4a >> 11) <= a.mask_thresh) {
+                    const double u = word_to_unit(draw_word<MODE>(a.rng, a.c_mut + e_a + j));
+                    ca = clampd(ca + polynomial_delta_dev(u, ca, lo, hi, a.xi), lo, hi);
+                }
+                if (paired) {
+                    const uint64_t w4b = draw_word<MODE>(a.rng, a.c_mask + e_b + j);
+                    if (live && (w4b >> 11) <= a.mask_thresh) {
+                        const double u = word_to_unit(draw_word<MODE>(a.rng, a.c_mut + e_b + j));
+                        cb = clampd(cb + polynomial_delta_dev(u, cb, lo, hi, a.xi), lo, hi);
+                    }
+                }
+            }
+            if (EVAL != 0) {
+                if (j + 1 >= a.m) {
+                    acc_a += dtlz_term<EVAL>(ca);
+                    if (paired) acc_b += dtlz_term<EVAL>(cb);
+                } else {
+                    s_pos[0][j] = ca;
+                    if (paired) s_pos[1][j] = cb;
+                }
+            }
+            xa[v] = ca;
+            xb[v] = cb;
+        }
+        if (VEC == 2) {
+            *reinterpret_cast<double2*>(oa + j0) = make_double2(xa[0], xa[VEC - 1]);
+            if (paired) *reinterpret_cast<double2*>(ob + j0) = make_double2(xb[0], xb[VEC - 1]);
+        } else {
+            oa[j0] = xa[0];
+            if (paired) ob[j0] = xb[0];
+        }
+    }
+
+    if (EVAL != 0) {
+        const uint64_t f0 = a.f_row0 + (a.f_row0_dev ? (uint64_t)*a.f_row0_dev : 0);
+        const double ga = block_sum<8>(acc_a, s_red);
+        dtlz_finish<EVAL>(ga, s_pos[0], a.m, a.d, a.f_out + (f0 + row_a) * a.m);
+        if (paired) {
+            const double gb = block_sum<8>(acc_b, s_red);
+            dtlz_finish<EVAL>(gb, s_pos[1], a.m, a.d, a.f_out + (f0 + row_b) * a.m);
+        }
+    }
+}
+
+template <int MODE, bool SBX, bool PM, int EVAL>
+void launch_vec(const ReproK& k, uint64_t units, int block, int vec, cudaStream_t s) {
+    if (units == 0) return;
+    if (vec == 2)
+        reproduce_kernel<MODE, SBX, PM, EVAL, 2><<<(unsigned)units, block, 0, s>>>(k);
+    else
+        reproduce_kernel<MODE, SBX, PM, EVAL, 1><<<(unsigned)units, block, 0, s>>>(k);
+}
+
+template <int MODE, bool SBX, bool PM>
+void launch_eval(const ReproK& k, uint64_t units, int block, int vec, int eval, cudaStream_t s) {
+    switch (eval) {
+    case 0: launch_vec<MODE, SBX, PM, 0>(k, units, block, vec, s); break;
+    case kDtlz1: launch_vec<MODE, SBX, PM, kDtlz1>(k, units, block, vec, s); break;
+    case kDtlz2: launch_vec<MODE, SBX, PM, kDtlz2>(k, units, block, vec, s); break;
+    case kDtlz3: launch_vec<MODE, SBX, PM, kDtlz3>(k, units, block, vec, s); break;
+    case kDtlz4: launch_vec<MODE, SBX, PM, kDtlz4>(k, units, block, vec, s); break;
+    default: fail(1, "reproduce: fused evaluation supports DTLZ1-4 only");
+    }
+}
+
+template <int MODE>
+void launch_mode(const ReproK& k, bool sbx, bool pm, uint64_t units, int block, int vec, int eval,
+                 cudaStream_t s) {
+    if (sbx && pm) launch_eval<MODE, true, true>(k, units, block, vec, eval, s);
+    else if (sbx) launch_eval<MODE, true, false>(k, units, block, vec, eval, s);
+    else if (pm) launch_eval<MODE, false, true>(k, units, block, vec, eval, s);
+    else fail(1, "reproduce: nothing to do");
+}
+
+template <int MODE>
+__global__ void random_reproduce_kernel(double* out, const uint32_t* dst, uint64_t n, uint64_t d,
+                                        Rng rng, uint64_t counter, const double* lower,
+                                        const double* upper) {
+    const uint64_t total = n * d;
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t i = e / d, j = e - i * d;
+        const double u = word_to_unit(draw_word<MODE>(rng, counter + e));
+        const uint64_t row = dst ? dst[i] : i;
+        out[row * d + j] = lower[j] + u * (upper[j] - lower[j]);  // operators.hpp:293
+    }
+}
+
+template <int MODE>
+__global__ void uniform_fill_kernel(double* out, uint64_t count, Rng rng, uint64_t counter) {
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < count;
+         e += (uint64_t)gridDim.x * blockDim.x)
+        out[e] = word_to_unit(draw_word<MODE>(rng, counter + e));
+}
+
+inline unsigned stream_grid(uint64_t total, int block) {
+    uint64_t g = (total + block - 1) / block;
+    const uint64_t cap = (uint64_t)kSMs * 16;
+    if (g > cap) g = cap;
+    if (g < 1) g = 1;
+    return (unsigned)g;
+}
+
+}  // namespace
+
+void launch_reproduce(const ReproArgs& a, cudaStream_t s) {
+    require(a.n >= 1 && a.d >= 1, "reproduce: empty population");
+    if (a.do_sbx) require(a.n >= 2, "sbx: needs at least two rows");  // operators.hpp:67
+    require(a.eval_problem == 0 || (a.m >= 2 && a.m <= (uint64_t)kMaxObj && a.d >= a.m),
+            "reproduce: bad objective count for fused evaluation");
+    ReproK k{};
+    k.pool = a.pool;
+    k.src = a.src;
+    k.out = a.out;
+    k.dst = a.dst;
+    k.n = a.n;
+    k.d = a.d;
+    k.half = a.n / 2;
+    k.rng = a.rng;
+    const uint64_t hd = k.half * a.d;
+    k.c_mc = a.c_sbx;
+    k.c_r1 = a.c_sbx + hd;
+    k.c_r2 = a.c_sbx + 2 * hd;
+    k.c_r3 = a.c_sbx + 3 * hd;
+    k.c_mask = a.c_pm;
+    k.c_mut = a.c_pm + a.n * a.d;
+    k.pc = a.ga.pc;
+    k.inv_exp = 1.0 / (a.ga.eta + 1.0);  // operators.hpp:75
+    k.xi = a.ga.xi;
+    // H(rate - r4) == 1  <=>  r4 <= rate  <=>  (word >> 11) <= floor(rate * 2^53)   (r4 = k * 2^-53)
+    const double rate = a.ga.pm / (double)a.d;  // operators.hpp:133
+    k.mask_never = !(rate >= 0.0);
+    if (!k.mask_never) {
+        const double scaled = rate * 0x1.0p53;
+        k.mask_thresh = scaled >= 0x1.0p53 ? ((1ULL << 53) - 1) : (uint64_t)scaled;
+    }
+    k.lower = a.lower;
+    k.upper = a.upper;
+    k.m = a.m;
+    k.f_out = a.f_out;
+    k.f_row0 = a.f_row0;
+    k.f_row0_dev = a.f_row0_dev;
+    const uint64_t units = a.do_sbx ? k.half + (a.n & 1) : a.n;
+    const int vec = row_vec(a.d), block = row_block(a.d);
+    if (a.rng.mode == 0)
+        launch_mode<0>(k, a.do_sbx, a.do_pm, units, block, vec, a.eval_problem, s);
+    else
+        launch_mode<1>(k, a.do_sbx, a.do_pm, units, block, vec, a.eval_problem, s);
+    TEMO_CUDA(cudaGetLastError());
+}
+
+void launch_random_reproduce(double* out, const uint32_t* dst, uint64_t n, uint64_t d, Rng rng,
+                             uint64_t counter, const double* lower, const double* upper,
+                             cudaStream_t s) {
+    const unsigned g = stream_grid(n * d, 256);
+    if (rng.mode == 0)
+        random_reproduce_kernel<0><<<g, 256, 0, s>>>(out, dst, n, d, rng, counter, lower, upper);
+    else
+        random_reproduce_kernel<1><<<g, 256, 0, s>>>(out, dst, n, d, rng, counter, lower, upper);
+    TEMO_CUDA(cudaGetLastError());
+}
+
+void launch_uniform_fill(double* out, uint64_t count, Rng rng, uint64_t counter, cudaStream_t s) {
+    const unsigned g = stream_grid(count, 256);
+    if (rng.mode == 0)
+        uniform_fill_kernel<0><<<g, 256, 0, s>>>(out, count, rng, counter);
+    else
+        uniform_fill_kernel<1><<<g, 256, 0, s>>>(out, count, rng, counter);
+    TEMO_CUDA(cudaGetLastError());
+}
+
+}  // namespace temo_b200

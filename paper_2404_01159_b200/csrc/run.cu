@@ -1,0 +1,466 @@
+// Device-resident generation loop.
+//
+// reference: rvea_run (algorithms.hpp:227-296) with op = "ga", track_archive = false.
+// The CPU loop copies the whole population four times per generation (take_rows x3, vconcat,
+// plus the shuffle gather); here X never moves: the population lives in a pool of
+// max(n,R)+n rows in HBM, survivors are addressed through a slot table, children are written
+// into free slots, and the merged objective matrix (parents first, algorithms.hpp:274-275) is
+// the only thing that is compacted (it is (|P|+n) x m, a few MB).
+//
+// Host work per generation: the sequential Fisher-Yates permutation (rng.hpp:69-78), computed
+// speculatively for generation t+1 while the GPU runs generation t (the draw counters depend on
+// the survivor count only through "|P| == n ? 0 : n" extra draws, algorithms.hpp:211-221 — the
+// speculation assumes |P| != n and is redone in the rare other case), one 4*n-byte H2D of the
+// permutation, and one 8-byte D2H of the survivor count + error flags.
+#include <chrono>
+#include <cmath>
+#include <cstring>
+
+#include "internal.h"
+#include "run.h"
+
+namespace temo_b200 {
+
+namespace {
+
+// src[i] = storage slot of the i-th row of the shuffled mating pool:
+// pool_idx = identity when |P| == n, else floor(u * |P|) with u the draw at c_pool + q
+// (algorithms.hpp:211-221); mating row i is pool row perm[i] (operators.hpp:155-158).
+template <int MODE>
+__global__ void build_src_kernel(const uint32_t* perm, const uint32_t* parent_slot, uint64_t n, uint64_t P,
+                                 Rng rng, uint64_t c_pool, uint32_t* src) {
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint64_t q = perm[i];
+    uint64_t k = q;
+    if (P != n) k = (uint64_t)(word_to_unit(draw_word<MODE>(rng, c_pool + q)) * (double)P);
+    src[i] = parent_slot[k];
+}
+
+// Survivor k takes over the storage slot and the objective row of merged row elite[k]
+// (detail::take_rows on merged_x / merged_f, algorithms.hpp:278-279).
+__global__ void commit_survivors_kernel(const uint32_t* elite, const uint32_t* n_elite, uint64_t P, uint64_t m,
+                                        const uint32_t* parent_slot, const uint32_t* free_slot,
+                                        uint32_t* parent_slot_next, const double* f_merged, double* f_next,
+                                        unsigned char* used, uint32_t* d_P) {
+    const uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint32_t cnt = *n_elite;
+    if (k == 0) *d_P = cnt;
+    if (k >= cnt) return;
+    const uint32_t e = elite[k];
+    const uint32_t slot = e < P ? parent_slot[e] : free_slot[e - P];
+    parent_slot_next[k] = slot;
+    used[slot] = 1;
+    for (uint64_t j = 0; j < m; ++j) f_next[k * m + j] = f_merged[(uint64_t)e * m + j];
+}
+
+// One CTA: the first `want` unused slots in ascending order become the next free list.
+__global__ void __launch_bounds__(1024) free_list_kernel(const unsigned char* used, uint64_t cap, uint64_t want,
+                                                        uint32_t* free_slot) {
+    __shared__ uint32_t s_warp[32];
+    const uint64_t chunk = (cap + blockDim.x - 1) / blockDim.x;
+    const uint64_t lo = threadIdx.x * chunk;
+    const uint64_t hi = lo + chunk < cap ? lo + chunk : cap;
+    uint32_t cnt = 0;
+    for (uint64_t s = lo; s < hi; ++s) cnt += used[s] == 0;
+    uint32_t incl = cnt;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t o = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += o;
+    }
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t w = s_warp[lane];
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const uint32_t o = __shfl_up_sync(0xffffffffu, w, off);
+            if (lane >= off) w += o;
+        }
+        s_warp[lane] = w;
+    }
+    __syncthreads();
+    uint64_t pos = incl - cnt + (warp ? s_warp[warp - 1] : 0);
+    for (uint64_t s = lo; s < hi && pos < want; ++s)
+        if (used[s] == 0) free_slot[pos++] = (uint32_t)s;
+}
+
+__global__ void iota_kernel(uint32_t* p, uint64_t n, uint32_t first) {
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i < n) p[i] = first + (uint32_t)i;
+}
+
+__global__ void gather_rows_kernel(const double* pool, const uint32_t* slot, uint64_t rows, uint64_t d, double* out) {
+    const uint64_t i = blockIdx.x;
+    if (i >= rows) return;
+    const double* p = pool + (uint64_t)slot[i] * d;
+    for (uint64_t j = threadIdx.x; j < d; j += blockDim.x) out[i * d + j] = p[j];
+}
+
+__global__ void scatter_rows_kernel(const double* in, const uint32_t* slot, uint64_t rows, uint64_t d, double* pool) {
+    const uint64_t i = blockIdx.x;
+    if (i >= rows) return;
+    double* p = pool + (uint64_t)slot[i] * d;
+    for (uint64_t j = threadIdx.x; j < d; j += blockDim.x) p[j] = in[i * d + j];
+}
+
+double now_ms() {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+}  // namespace
+
+Run::Run(const RunConfig& c) : cfg(c) {
+    require(cfg.pop >= 2 && cfg.generations >= 1, "rvea_run: bad config");  // algorithms.hpp:229
+    require(problem_known(cfg.problem), "make_problem: unknown problem");
+    require(cfg.obj >= 2 && cfg.obj <= (uint64_t)kMaxObj, "rvea_run: objective count out of range");
+    n = cfg.pop;
+    m = cfg.obj;
+    d = cfg.dim ? cfg.dim : problem_default_dim(cfg.problem, m);
+    require(d >= m, "make_problem: DTLZ needs d >= m");  // problems.hpp:269
+    H = cfg.lattice_h ? cfg.lattice_h : lattice_density_for(m, n);  // algorithms.hpp:233-235
+    r = lattice_count(m, H);
+    require(r >= 2, "min_vector_angles: needs at least two vectors");
+    const double ae = std::ceil(cfg.fr * (double)cfg.generations);  // algorithms.hpp:237-239
+    adapt_every = ae < 1.0 ? 1 : (uint64_t)ae;
+    rng = make_rng(cfg.seed, cfg.rng_mode);
+    pcap = n > r ? n : r;
+    cap = pcap + n;
+    require(cap < 0xffffffffULL, "rvea_run: population too large for 32-bit slots");
+    Context& cx = ctx();
+    stream = cx.stream;
+
+    pool = dev_alloc<double>(cap * d);
+    for (int b = 0; b < 2; ++b) {
+        fm[b] = dev_alloc<double>(cap * m);
+        parent_slot[b] = dev_alloc<uint32_t>(pcap);
+        free_slot[b] = dev_alloc<uint32_t>(n);
+        TEMO_CUDA(cudaMallocHost(&h_perm[b], n * sizeof(uint32_t)));
+    }
+    src = dev_alloc<uint32_t>(n);
+    perm_dev = dev_alloc<uint32_t>(n);
+    used = dev_alloc<unsigned char>(cap);
+    d_P = dev_alloc<uint32_t>(1);
+    v0 = dev_alloc<double>(r * m);
+    v = dev_alloc<double>(r * m);
+    gamma = dev_alloc<double>(r);
+    lower = dev_alloc<double>(d);
+    upper = dev_alloc<double>(d);
+    zmin = dev_alloc<double>(m);
+    zmax = dev_alloc<double>(m);
+    zscratch = dev_alloc<unsigned long long>(2 * m);
+    skip_flag = dev_alloc<uint32_t>(1);
+    TEMO_CUDA(cudaMallocHost(&h_status, 4 * sizeof(uint32_t)));
+    ws.alloc(cap, r, m);
+    for (int e = 0; e < kNumEvents; ++e) TEMO_CUDA(cudaEventCreate(&ev[e]));
+
+    // reference set (algorithms.hpp:236): lattice + unit vectors on the host (once), gamma on device
+    const std::vector<double> unit = normalize_to_unit(simplex_lattice(m, H), r, m);
+    TEMO_CUDA(cudaMemcpyAsync(v0, unit.data(), r * m * sizeof(double), cudaMemcpyHostToDevice, stream));
+    TEMO_CUDA(cudaMemcpyAsync(v, v0, r * m * sizeof(double), cudaMemcpyDeviceToDevice, stream));
+    launch_row_norms(v, r, m, ws.vn, stream);
+    launch_gamma(v, ws.vn, r, m, gamma, ws.err_flag, nullptr, stream);
+
+    std::vector<double> lo(d), hi(d);
+    problem_bounds(cfg.problem, d, m, lo.data(), hi.data());
+    TEMO_CUDA(cudaMemcpyAsync(lower, lo.data(), d * sizeof(double), cudaMemcpyHostToDevice, stream));
+    TEMO_CUDA(cudaMemcpyAsync(upper, hi.data(), d * sizeof(double), cudaMemcpyHostToDevice, stream));
+    TEMO_CUDA(cudaStreamSynchronize(stream));  // host vectors go out of scope
+
+    // initial population (algorithms.hpp:241-242): slots 0..n-1, n*d draws
+    iota_kernel<<<(unsigned)((pcap + 255) / 256), 256, 0, stream>>>(parent_slot[0], pcap, 0);
+    iota_kernel<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(free_slot[0], n, (uint32_t)n);
+    launch_random_reproduce(pool, nullptr, n, d, rng, 0, lower, upper, stream);
+    counter = n * d;
+    EvalArgs ea;
+    ea.problem = cfg.problem;
+    ea.x = pool;
+    ea.n = n;
+    ea.d = d;
+    ea.m = m;
+    ea.f = fm[0];
+    launch_evaluate(ea, stream);
+    P = n;
+    const uint32_t p32 = (uint32_t)P;
+    TEMO_CUDA(cudaMemcpyAsync(d_P, &p32, sizeof(uint32_t), cudaMemcpyHostToDevice, stream));
+    check_status();
+    t = 0;
+    cur = 0;
+    spec_valid = false;
+}
+
+Run::~Run() {
+    cudaStreamSynchronize(stream);
+    cudaFree(pool);
+    for (int b = 0; b < 2; ++b) {
+        cudaFree(fm[b]);
+        cudaFree(parent_slot[b]);
+        cudaFree(free_slot[b]);
+        cudaFreeHost(h_perm[b]);
+    }
+    cudaFree(src); cudaFree(perm_dev); cudaFree(used); cudaFree(d_P);
+    cudaFree(v0); cudaFree(v); cudaFree(gamma); cudaFree(lower); cudaFree(upper);
+    cudaFree(zmin); cudaFree(zmax); cudaFree(zscratch); cudaFree(skip_flag);
+    cudaFreeHost(h_status);
+    ws.release();
+    for (int e = 0; e < kNumEvents; ++e) cudaEventDestroy(ev[e]);
+}
+
+// Reads n_elite / error flags back (one small D2H) and turns device-side contract violations
+// into the reference's exceptions.
+void Run::check_status() {
+    TEMO_CUDA(cudaMemcpyAsync(h_status, ws.err_flag, sizeof(uint32_t), cudaMemcpyDeviceToHost, stream));
+    TEMO_CUDA(cudaMemcpyAsync(h_status + 1, d_P, sizeof(uint32_t), cudaMemcpyDeviceToHost, stream));
+    TEMO_CUDA(cudaStreamSynchronize(stream));
+    if (h_status[0] & 1u) fail(1, "min_vector_angles: duplicate reference vectors");  // refvec.hpp:97-98
+    if (h_status[0] & 2u) fail(1, "normalize_to_unit: zero row");                      // refvec.hpp:72
+}
+
+// Draw-counter plan of one generation.
+Run::Plan Run::plan_for(uint64_t P_now, uint64_t c) const {
+    Plan p;
+    p.c_pool = c;
+    if (P_now != n) c += n;
+    p.c_shuffle = c;
+    c += n - 1;
+    p.c_sbx = c;
+    const uint64_t h = n / 2;
+    c += 3 * h * d + h;
+    p.c_pm = c;
+    c += 2 * n * d;
+    p.c_end = c;
+    return p;
+}
+
+void Run::ensure_permutation(const Plan& p) {
+    if (spec_valid && spec_c_shuffle == p.c_shuffle) return;  // speculation hit
+    uint64_t c = p.c_shuffle;
+    shuffle_indices(cfg.seed, c, n, h_perm[hp]);
+    spec_c_shuffle = p.c_shuffle;
+    spec_valid = true;
+}
+
+void Run::launch_reproduction(const Plan& p, bool fused) {
+    const unsigned g = (unsigned)((n + 255) / 256);
+    if (rng.mode == 0)
+        build_src_kernel<0><<<g, 256, 0, stream>>>(perm_dev, parent_slot[cur], n, P, rng, p.c_pool, src);
+    else
+        build_src_kernel<1><<<g, 256, 0, stream>>>(perm_dev, parent_slot[cur], n, P, rng, p.c_pool, src);
+    ReproArgs ra;
+    ra.pool = pool;
+    ra.src = src;
+    ra.out = pool;
+    ra.dst = free_slot[cur];
+    ra.n = n;
+    ra.d = d;
+    ra.rng = rng;
+    ra.c_sbx = p.c_sbx;
+    ra.c_pm = p.c_pm;
+    ra.ga = cfg.ga;
+    ra.lower = lower;
+    ra.upper = upper;
+    if (fused) {
+        ra.eval_problem = cfg.problem;
+        ra.m = m;
+        ra.f_out = fm[cur];
+        ra.f_row0 = P;
+    }
+    launch_reproduce(ra, stream);
+}
+
+void Run::launch_offspring_eval() {
+    EvalArgs ea;
+    ea.problem = cfg.problem;
+    ea.x = pool;
+    ea.rows = free_slot[cur];
+    ea.n = n;
+    ea.d = d;
+    ea.m = m;
+    ea.f = fm[cur];
+    ea.f_row0 = P;
+    launch_evaluate(ea, stream);
+}
+
+bool Run::fusable() const { return cfg.fuse_eval && cfg.problem >= kDtlz1 && cfg.problem <= kDtlz4; }
+
+uint64_t Run::step(double* survivors_f_host) {
+    require(t < cfg.generations, "rvea_run: all generations already done");
+    const double host0 = now_ms();
+    P_before = P;
+    const Plan p = plan_for(P, counter);
+    ensure_permutation(p);
+    const double host1 = now_ms();
+
+    TEMO_CUDA(cudaEventRecord(ev[0], stream));
+    TEMO_CUDA(cudaMemcpyAsync(perm_dev, h_perm[hp], n * sizeof(uint32_t), cudaMemcpyHostToDevice, stream));
+    const bool fused = fusable();
+    launch_reproduction(p, fused);
+    TEMO_CUDA(cudaEventRecord(ev[1], stream));
+    if (!fused) launch_offspring_eval();
+    TEMO_CUDA(cudaEventRecord(ev[2], stream));
+
+    // environmental selection over the merged population (algorithms.hpp:274-279)
+    const double penalty = apd_penalty(m, t, cfg.generations, cfg.alpha);
+    launch_select(fm[cur], P + n, nullptr, m, v, gamma, r, penalty, ws, stream);
+    TEMO_CUDA(cudaMemsetAsync(used, 0, cap, stream));
+    const uint64_t kmax = r < P + n ? r : P + n;
+    commit_survivors_kernel<<<(unsigned)((kmax + 255) / 256), 256, 0, stream>>>(
+        ws.elite, ws.n_elite, P, m, parent_slot[cur], free_slot[cur], parent_slot[cur ^ 1], fm[cur], fm[cur ^ 1],
+        used, d_P);
+    free_list_kernel<<<1, 1024, 0, stream>>>(used, cap, n, free_slot[cur ^ 1]);
+    TEMO_CUDA(cudaEventRecord(ev[3], stream));
+
+    // reference-vector adaptation (algorithms.hpp:281)
+    if ((t + 1) % adapt_every == 0) {
+        launch_col_minmax(fm[cur ^ 1], pcap, d_P, m, zmin, zmax, zscratch, stream);
+        launch_adapt_vectors(v0, v, ws.vn, r, m, zmin, zmax, skip_flag, ws.err_flag, stream);
+        launch_gamma(v, ws.vn, r, m, gamma, ws.err_flag, skip_flag, stream);
+    }
+    TEMO_CUDA(cudaEventRecord(ev[4], stream));
+    TEMO_CUDA(cudaMemcpyAsync(h_status, ws.err_flag, sizeof(uint32_t), cudaMemcpyDeviceToHost, stream));
+    TEMO_CUDA(cudaMemcpyAsync(h_status + 1, d_P, sizeof(uint32_t), cudaMemcpyDeviceToHost, stream));
+    TEMO_CUDA(cudaGetLastError());
+
+    // while the GPU works: speculative permutation of the next generation (|P'| != n assumed)
+    const double host2 = now_ms();
+    counter = p.c_end;
+    hp ^= 1;
+    spec_valid = false;
+    if (t + 1 < cfg.generations) {
+        const Plan next = plan_for(n + 1 /* any value != n */, counter);
+        ensure_permutation(next);
+    }
+    const double host3 = now_ms();
+
+    TEMO_CUDA(cudaStreamSynchronize(stream));
+    if (h_status[0] & 1u) fail(1, "rv_select: gamma must be positive");
+    if (h_status[0] & 2u) fail(1, "normalize_to_unit: zero row");
+    P = h_status[1];
+    cur ^= 1;
+    ++t;
+    if (survivors_f_host)
+        TEMO_CUDA(cudaMemcpy(survivors_f_host, fm[cur], P * m * sizeof(double), cudaMemcpyDeviceToHost));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ev[0], ev[4]); timings[0] = ms;
+    cudaEventElapsedTime(&ms, ev[0], ev[1]); timings[1] = ms;
+    cudaEventElapsedTime(&ms, ev[1], ev[2]); timings[2] = ms;
+    cudaEventElapsedTime(&ms, ev[2], ev[3]); timings[3] = ms;
+    cudaEventElapsedTime(&ms, ev[3], ev[4]); timings[4] = ms;
+    timings[5] = (host1 - host0) + (host3 - host2);
+    return P;
+}
+
+void Run::inject(uint64_t rows, const double* x, const double* f, const double* v_in, const double* gamma_in,
+                 uint64_t counter_in, uint64_t t_in) {
+    require(rows >= 1 && rows <= pcap, "inject: row count out of range");
+    TEMO_CUDA(cudaStreamSynchronize(stream));
+    if (x) {
+        TEMO_CUDA(cudaMemcpy(pool, x, rows * d * sizeof(double), cudaMemcpyHostToDevice));
+        iota_kernel<<<(unsigned)((pcap + 255) / 256), 256, 0, stream>>>(parent_slot[cur], pcap, 0);
+        iota_kernel<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(free_slot[cur], n, (uint32_t)rows);
+    } else {
+        require(rows == P, "inject: row count must match when x is kept");
+    }
+    if (f) TEMO_CUDA(cudaMemcpy(fm[cur], f, rows * m * sizeof(double), cudaMemcpyHostToDevice));
+    if (v_in) {
+        TEMO_CUDA(cudaMemcpy(v, v_in, r * m * sizeof(double), cudaMemcpyHostToDevice));
+        launch_row_norms(v, r, m, ws.vn, stream);
+    }
+    if (gamma_in) TEMO_CUDA(cudaMemcpy(gamma, gamma_in, r * sizeof(double), cudaMemcpyHostToDevice));
+    P = rows;
+    const uint32_t p32 = (uint32_t)P;
+    TEMO_CUDA(cudaMemcpy(d_P, &p32, sizeof(uint32_t), cudaMemcpyHostToDevice));
+    counter = counter_in;
+    t = t_in;
+    spec_valid = false;
+    TEMO_CUDA(cudaStreamSynchronize(stream));
+}
+
+void Run::download(double* x, double* f, double* v_out, double* gamma_out) {
+    TEMO_CUDA(cudaStreamSynchronize(stream));
+    if (x) {
+        double* tmp = dev_alloc<double>(P * d);
+        gather_rows_kernel<<<(unsigned)P, 256, 0, stream>>>(pool, parent_slot[cur], P, d, tmp);
+        const cudaError_t e = cudaMemcpyAsync(x, tmp, P * d * sizeof(double), cudaMemcpyDeviceToHost, stream);
+        cudaStreamSynchronize(stream);
+        cudaFree(tmp);
+        TEMO_CUDA(e);
+    }
+    if (f) TEMO_CUDA(cudaMemcpy(f, fm[cur], P * m * sizeof(double), cudaMemcpyDeviceToHost));
+    if (v_out) TEMO_CUDA(cudaMemcpy(v_out, v, r * m * sizeof(double), cudaMemcpyDeviceToHost));
+    if (gamma_out) TEMO_CUDA(cudaMemcpy(gamma_out, gamma, r * sizeof(double), cudaMemcpyDeviceToHost));
+}
+
+// Offspring of the last generation still sit in the slots of the previous free list, their
+// objectives in the previous merged matrix after the previous parents.
+void Run::last_generation(double* offspring, double* f_off, uint64_t* elite_out) {
+    require(t >= 1, "last_generation: no generation has run");
+    TEMO_CUDA(cudaStreamSynchronize(stream));
+    if (offspring) {
+        double* tmp = dev_alloc<double>(n * d);
+        gather_rows_kernel<<<(unsigned)n, 256, 0, stream>>>(pool, free_slot[cur ^ 1], n, d, tmp);
+        const cudaError_t e = cudaMemcpyAsync(offspring, tmp, n * d * sizeof(double), cudaMemcpyDeviceToHost, stream);
+        cudaStreamSynchronize(stream);
+        cudaFree(tmp);
+        TEMO_CUDA(e);
+    }
+    if (f_off)
+        TEMO_CUDA(cudaMemcpy(f_off, fm[cur ^ 1] + P_prev() * m, n * m * sizeof(double), cudaMemcpyDeviceToHost));
+    if (elite_out) {
+        std::vector<uint32_t> tmp(P);
+        TEMO_CUDA(cudaMemcpy(tmp.data(), ws.elite, P * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+        for (uint64_t k = 0; k < P; ++k) elite_out[k] = tmp[k];
+    }
+}
+
+double Run::time_stage(int stage, int reps) {
+    require(reps >= 1, "time_stage: reps must be positive");
+    const Plan p = plan_for(P, counter);
+    ensure_permutation(p);
+    TEMO_CUDA(cudaMemcpyAsync(perm_dev, h_perm[hp], n * sizeof(uint32_t), cudaMemcpyHostToDevice, stream));
+    // make sure the offspring rows / merged objectives of this generation exist for stages 2 and 4
+    launch_reproduction(p, false);
+    launch_offspring_eval();
+    const double penalty = apd_penalty(m, t < cfg.generations ? t : cfg.generations, cfg.generations, cfg.alpha);
+    cudaEvent_t a, b;
+    TEMO_CUDA(cudaEventCreate(&a));
+    TEMO_CUDA(cudaEventCreate(&b));
+    double total = 0.0;
+    for (int it = 0; it < reps; ++it) {
+        flush_l2();
+        TEMO_CUDA(cudaEventRecord(a, stream));
+        switch (stage) {
+        case 1: launch_reproduction(p, false); break;
+        case 2: launch_offspring_eval(); break;
+        case 3:
+            require(cfg.problem >= kDtlz1 && cfg.problem <= kDtlz4, "time_stage: fused evaluation is DTLZ-only");
+            launch_reproduction(p, true);
+            break;
+        case 4: launch_select(fm[cur], P + n, nullptr, m, v, gamma, r, penalty, ws, stream); break;
+        case 5: launch_gamma(v, ws.vn, r, m, gamma, ws.err_flag, nullptr, stream); break;
+        default: fail(1, "time_stage: unknown stage");
+        }
+        TEMO_CUDA(cudaEventRecord(b, stream));
+        TEMO_CUDA(cudaEventSynchronize(b));
+        float ms = 0.f;
+        TEMO_CUDA(cudaEventElapsedTime(&ms, a, b));
+        total += ms;
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    return total / reps;
+}
+
+void flush_l2() {
+    Context& cx = ctx();
+    const size_t bytes = 256u << 20;  // > 126 MB L2
+    if (!cx.flush_buf) {
+        cx.flush_buf = dev_alloc<unsigned char>(bytes);
+        cx.flush_bytes = bytes;
+    }
+    TEMO_CUDA(cudaMemsetAsync(cx.flush_buf, 0x5a, cx.flush_bytes, cx.stream));
+}
+
+}  // namespace temo_b200

@@ -1,0 +1,80 @@
+// Device-resident RVEA run state (see run.cu). reference: rvea_run, algorithms.hpp:227-296.
+#pragma once
+
+#include "internal.h"
+
+namespace temo_b200 {
+
+struct RunConfig {  // reference: RunConfig, algorithms.hpp:21-41
+    int problem = kDtlz2;
+    int rng_mode = 0;
+    uint64_t pop = 105, lattice_h = 0, generations = 100, seed = 42, dim = 0, obj = 3;
+    double alpha = 2.0, fr = 0.1, time_budget_s = 0.0;
+    GaParams ga;
+    int fuse_eval = 1;
+};
+
+void flush_l2();
+
+struct Run {
+    static constexpr int kNumEvents = 5;
+    struct Plan {
+        uint64_t c_pool, c_shuffle, c_sbx, c_pm, c_end;
+    };
+
+    explicit Run(const RunConfig& c);
+    ~Run();
+    Run(const Run&) = delete;
+    Run& operator=(const Run&) = delete;
+
+    uint64_t step(double* survivors_f_host);
+    void inject(uint64_t rows, const double* x, const double* f, const double* v_in, const double* gamma_in,
+                uint64_t counter_in, uint64_t t_in);
+    void download(double* x, double* f, double* v_out, double* gamma_out);
+    void last_generation(double* offspring, double* f_off, uint64_t* elite_out);
+    double time_stage(int stage, int reps);
+
+    RunConfig cfg;
+    uint64_t n = 0, d = 0, m = 0, r = 0, H = 0, adapt_every = 1;
+    uint64_t pcap = 0;  // max(n, r): most parents a generation can have
+    uint64_t cap = 0;   // pool rows: pcap + n
+    uint64_t P = 0;     // current survivor count (host copy)
+    uint64_t P_before = 0;  // survivor count at the start of the last step
+    uint64_t counter = 0, t = 0;
+    Rng rng{};
+    cudaStream_t stream = nullptr;
+
+    double* pool = nullptr;          // cap x d
+    double* fm[2] = {nullptr, nullptr};       // merged objectives, cap x m (double buffered)
+    uint32_t* parent_slot[2] = {nullptr, nullptr};
+    uint32_t* free_slot[2] = {nullptr, nullptr};
+    int cur = 0;
+    uint32_t* src = nullptr;
+    uint32_t* perm_dev = nullptr;
+    unsigned char* used = nullptr;
+    uint32_t* d_P = nullptr;
+    double *v0 = nullptr, *v = nullptr, *gamma = nullptr, *lower = nullptr, *upper = nullptr;
+    double *zmin = nullptr, *zmax = nullptr;
+    unsigned long long* zscratch = nullptr;
+    uint32_t* skip_flag = nullptr;
+    SelectWorkspace ws;
+
+    uint32_t* h_perm[2] = {nullptr, nullptr};  // pinned
+    int hp = 0;
+    bool spec_valid = false;
+    uint64_t spec_c_shuffle = 0;
+    uint32_t* h_status = nullptr;  // pinned: [0] error flags, [1] survivor count
+    cudaEvent_t ev[kNumEvents]{};
+    double timings[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+
+private:
+    void check_status();
+    Plan plan_for(uint64_t P_now, uint64_t c) const;
+    void ensure_permutation(const Plan& p);
+    void launch_reproduction(const Plan& p, bool fused);
+    void launch_offspring_eval();
+    bool fusable() const;
+    uint64_t P_prev() const { return P_before; }
+};
+
+}  // namespace temo_b200

@@ -1,0 +1,309 @@
+// K3 — APD environmental selection.
+//
+// reference: rv_select (selection.hpp:200-224) = detail::rv_core (selection.hpp:148-192:
+// ideal-point translation, row norms, first-max-cosine association over the R reference
+// vectors, one acos per row, angle-penalised distance) followed by the serial per-vector
+// argmin with lowest-row tie-break (selection.hpp:206-217).
+//
+// Bit-exactness (compiled with --fmad=false): dot products
+// accumulate in ascending k, the cosine is dot / (nf * vn[j]) with IEEE divide, strict `>`
+// keeps the lowest j among equal cosines, and the elite of each vector is the lexicographic
+// minimum of (apd, row) — implemented order-independently with two rounds of 64-bit/32-bit
+// atomicMin, plus the reference's NaN rule (a NaN APD is never an improvement, but the first
+// row of a subpopulation is taken unconditionally).
+#include "internal.h"
+
+namespace temo_b200 {
+
+namespace {
+
+// Total-order key of a double: monotone for all non-NaN values.
+__device__ __forceinline__ unsigned long long order_key(double x) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(x);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ULL);
+}
+__device__ __forceinline__ double key_value(unsigned long long k) {
+    const unsigned long long b = (k >> 63) ? (k & 0x7fffffffffffffffULL) : ~k;
+    return __longlong_as_double((long long)b);
+}
+constexpr unsigned long long kKeyMax = 0xffffffffffffffffULL;
+
+// ---- ideal point: column minima (tensor.hpp:211-219) --------------------------------------------
+// grid (blocks, m): block-strided rows of one column; NaNs never win (strict <).
+__global__ void colmin_kernel(const double* f, uint64_t n_rows, const uint32_t* n_rows_dev, uint64_t m,
+                              unsigned long long* zkey_min, unsigned long long* zkey_max) {
+    const uint64_t n = n_rows_dev ? (uint64_t)*n_rows_dev : n_rows;
+    const uint64_t j = blockIdx.y;
+    unsigned long long kmin = kKeyMax, kmax = 0ULL;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const double v = f[i * m + j];
+        if (v == v) {
+            const unsigned long long k = order_key(v);
+            kmin = k < kmin ? k : kmin;
+            kmax = k > kmax ? k : kmax;
+        }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        const unsigned long long o1 = __shfl_xor_sync(0xffffffffu, kmin, off);
+        const unsigned long long o2 = __shfl_xor_sync(0xffffffffu, kmax, off);
+        kmin = o1 < kmin ? o1 : kmin;
+        kmax = o2 > kmax ? o2 : kmax;
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (kmin != kKeyMax) atomicMin(&zkey_min[j], kmin);
+        if (zkey_max && kmax != 0ULL) atomicMax(&zkey_max[j], kmax);
+    }
+}
+
+// Decodes the keys; a NaN in row 0 sticks (the reference seeds the scan with row 0 and a NaN
+// never compares smaller/greater).
+__global__ void colmin_finish_kernel(const double* f, uint64_t m, const unsigned long long* zkey_min,
+                                     const unsigned long long* zkey_max, double* zmin, double* zmax) {
+    const uint64_t j = threadIdx.x;
+    if (j >= m) return;
+    const double first = f[j];
+    if (zmin) zmin[j] = (first != first) ? first : key_value(zkey_min[j]);
+    if (zmax) zmax[j] = (first != first) ? first : key_value(zkey_max[j]);
+}
+
+__global__ void row_norms_kernel(const double* v, uint64_t r, uint64_t m, double* vn) {
+    const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (j >= r) return;
+    double s = 0.0;
+    for (uint64_t k = 0; k < m; ++k) s += v[j * m + k] * v[j * m + k];  // tensor.hpp:171-182
+    vn[j] = sqrt(s);
+}
+
+__global__ void gamma_check_kernel(const double* gamma, uint64_t r, uint32_t* err_flag) {
+    const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (j < r && !(gamma[j] > 0.0)) atomicOr(err_flag, 1u);  // selection.hpp:152
+}
+
+// ---- association + APD ------------------------------------------------------------------------------
+constexpr int kAssocThreads = 128;
+constexpr int kTileVecs = 512;
+
+template <int M>
+__global__ void __launch_bounds__(kAssocThreads) assoc_kernel(
+    const double* __restrict__ f, uint64_t n_rows, const uint32_t* n_rows_dev, uint64_t m_rt,
+    const double* __restrict__ z, const double* __restrict__ v, const double* __restrict__ vn,
+    const double* __restrict__ gamma, uint64_t r, double penalty, uint32_t* __restrict__ assoc,
+    double* __restrict__ theta_out, double* __restrict__ apd_out,
+    unsigned long long* __restrict__ best_key, uint32_t* __restrict__ first_row) {
+    constexpr int MM = M > 0 ? M : kMaxObj;
+    const int m = M > 0 ? M : (int)m_rt;
+    extern __shared__ double s_tile[];  // kTileVecs x (m + 1): v_j[0..m-1], vn_j
+    const uint64_t n = n_rows_dev ? (uint64_t)*n_rows_dev : n_rows;
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const bool live = i < n;
+
+    double fp[MM];
+    double nf = 0.0;
+    if (live) {
+        double s = 0.0;
+#pragma unroll
+        for (int k = 0; k < MM; ++k) {
+            if (k < m) {
+                fp[k] = f[i * m + k] - z[k];  // selection.hpp:155-157
+                s += fp[k] * fp[k];
+            }
+        }
+        nf = sqrt(s);
+    }
+    double best_cos = -INFINITY;
+    uint32_t arg = 0;
+    const int stride = m + 1;
+    for (uint64_t j0 = 0; j0 < r; j0 += kTileVecs) {
+        const int tile = (int)((r - j0) < (uint64_t)kTileVecs ? (r - j0) : kTileVecs);
+        __syncthreads();
+        for (int e = threadIdx.x; e < tile * stride; e += blockDim.x) {
+            const int jj = e / stride, k = e - jj * stride;
+            s_tile[e] = k < m ? v[(j0 + jj) * m + k] : vn[j0 + jj];
+        }
+        __syncthreads();
+        if (live && nf != 0.0) {
+            for (int jj = 0; jj < tile; ++jj) {
+                const double* vr = s_tile + jj * stride;
+                double dot = 0.0;
+#pragma unroll
+                for (int k = 0; k < MM; ++k)
+                    if (k < m) dot += fp[k] * vr[k];
+                const double c = dot / (nf * vr[m]);  // selection.hpp:178
+                if (c > best_cos) {
+                    best_cos = c;
+                    arg = (uint32_t)(j0 + jj);
+                }
+            }
+        }
+    }
+    if (!live) return;
+    double theta = 0.0;  // a row at the ideal point: angle 0 to vector 0 (selection.hpp:167-169)
+    if (nf != 0.0) {
+        double c = best_cos;
+        if (c > 1.0) c = 1.0;
+        if (c < -1.0) c = -1.0;
+        theta = acos(c);  // tensor.hpp:79-83
+    }
+    const double apd = (1.0 + penalty * (theta / gamma[arg])) * nf;  // selection.hpp:82-84
+    assoc[i] = arg;
+    theta_out[i] = theta;
+    apd_out[i] = apd;
+    const unsigned long long key = (apd != apd) ? kKeyMax : order_key(apd);
+    atomicMin(&best_key[arg], key);
+    atomicMin(&first_row[arg], (uint32_t)i);
+}
+
+// lowest row among those that attain the minimal APD of their vector
+__global__ void elite_rows_kernel(uint64_t n_rows, const uint32_t* n_rows_dev, const uint32_t* assoc,
+                                  const double* apd, const unsigned long long* best_key,
+                                  uint32_t* best_row) {
+    const uint64_t n = n_rows_dev ? (uint64_t)*n_rows_dev : n_rows;
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double a = apd[i];
+    const unsigned long long key = (a != a) ? kKeyMax : order_key(a);
+    const uint32_t j = assoc[i];
+    if (key == best_key[j]) atomicMin(&best_row[j], (uint32_t)i);
+}
+
+// One CTA: validity + compaction of the elites in ascending vector index (selection.hpp:216-217).
+__global__ void __launch_bounds__(1024) elite_compact_kernel(uint64_t r, const double* apd,
+                                                            const uint32_t* first_row,
+                                                            const uint32_t* best_row, uint32_t* elite,
+                                                            unsigned char* valid, uint32_t* n_elite) {
+    __shared__ uint32_t s_warp[32];
+    __shared__ uint32_t s_total;
+    const uint64_t chunk = (r + blockDim.x - 1) / blockDim.x;
+    const uint64_t lo = threadIdx.x * chunk;
+    const uint64_t hi = lo + chunk < r ? lo + chunk : r;
+    uint32_t cnt = 0;
+    for (uint64_t j = lo; j < hi; ++j) cnt += first_row[j] != 0xffffffffu;
+    // block exclusive scan of cnt
+    uint32_t incl = cnt;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t o = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += o;
+    }
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t w = s_warp[lane];
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const uint32_t o = __shfl_up_sync(0xffffffffu, w, off);
+            if (lane >= off) w += o;
+        }
+        s_warp[lane] = w;
+        if (lane == 31) s_total = w;
+    }
+    __syncthreads();
+    uint32_t pos = incl - cnt + (warp ? s_warp[warp - 1] : 0);
+    for (uint64_t j = lo; j < hi; ++j) {
+        const uint32_t fr = first_row[j];
+        const bool ok = fr != 0xffffffffu;
+        valid[j] = ok ? 1 : 0;
+        if (ok) {
+            const double a0 = apd[fr];
+            elite[pos++] = (a0 != a0) ? fr : best_row[j];
+        }
+    }
+    if (threadIdx.x == 0) *n_elite = s_total;
+}
+
+template <int M>
+void launch_assoc(const double* f, uint64_t n_rows, const uint32_t* n_rows_dev, uint64_t m,
+                  const double* v, const double* gamma, uint64_t r, double penalty, SelectWorkspace& ws,
+                  cudaStream_t s) {
+    const unsigned grid = (unsigned)((n_rows + kAssocThreads - 1) / kAssocThreads);
+    const size_t smem = (size_t)kTileVecs * (m + 1) * sizeof(double);
+    if (smem > 48 * 1024) {
+        static bool configured = false;
+        if (!configured) {
+            TEMO_CUDA(cudaFuncSetAttribute(assoc_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+            configured = true;
+        }
+    }
+    assoc_kernel<M><<<grid, kAssocThreads, smem, s>>>(f, n_rows, n_rows_dev, m, ws.z, v, ws.vn, gamma, r,
+                                                     penalty, ws.assoc, ws.theta, ws.apd, ws.best_key,
+                                                     ws.first_row);
+}
+
+}  // namespace
+
+void SelectWorkspace::alloc(uint64_t rows_cap_, uint64_t r_, uint64_t m_) {
+    rows_cap = rows_cap_;
+    r = r_;
+    m = m_;
+    z = dev_alloc<double>(m);
+    zkey = dev_alloc<unsigned long long>(2 * m);
+    vn = dev_alloc<double>(r);
+    assoc = dev_alloc<uint32_t>(rows_cap);
+    theta = dev_alloc<double>(rows_cap);
+    apd = dev_alloc<double>(rows_cap);
+    best_key = dev_alloc<unsigned long long>(r);
+    best_row = dev_alloc<uint32_t>(r);
+    first_row = dev_alloc<uint32_t>(r);
+    elite = dev_alloc<uint32_t>(r);
+    valid = dev_alloc<unsigned char>(r);
+    n_elite = dev_alloc<uint32_t>(1);
+    err_flag = dev_alloc<uint32_t>(1);
+    TEMO_CUDA(cudaMemset(err_flag, 0, sizeof(uint32_t)));
+}
+
+void SelectWorkspace::release() {
+    cudaFree(z); cudaFree(zkey); cudaFree(vn); cudaFree(assoc); cudaFree(theta); cudaFree(apd);
+    cudaFree(best_key); cudaFree(best_row); cudaFree(first_row); cudaFree(elite); cudaFree(valid);
+    cudaFree(n_elite); cudaFree(err_flag);
+    *this = SelectWorkspace{};
+}
+
+void launch_row_norms(const double* v, uint64_t r, uint64_t m, double* vn, cudaStream_t s) {
+    row_norms_kernel<<<(unsigned)((r + 255) / 256), 256, 0, s>>>(v, r, m, vn);
+    TEMO_CUDA(cudaGetLastError());
+}
+
+void launch_col_minmax(const double* f, uint64_t n_rows, const uint32_t* n_rows_dev, uint64_t m,
+                       double* zmin, double* zmax, unsigned long long* scratch2m, cudaStream_t s) {
+    TEMO_CUDA(cudaMemsetAsync(scratch2m, 0xff, m * sizeof(unsigned long long), s));
+    TEMO_CUDA(cudaMemsetAsync(scratch2m + m, 0x00, m * sizeof(unsigned long long), s));
+    uint64_t blocks = (n_rows + 255) / 256;
+    if (blocks > (uint64_t)kSMs * 4) blocks = (uint64_t)kSMs * 4;
+    if (blocks < 1) blocks = 1;
+    colmin_kernel<<<dim3((unsigned)blocks, (unsigned)m), 256, 0, s>>>(f, n_rows, n_rows_dev, m, scratch2m,
+                                                                     zmax ? scratch2m + m : nullptr);
+    colmin_finish_kernel<<<1, 32, 0, s>>>(f, m, scratch2m, scratch2m + m, zmin, zmax);
+    TEMO_CUDA(cudaGetLastError());
+}
+
+void launch_select(const double* f, uint64_t n_rows, const uint32_t* n_rows_dev, uint64_t m,
+                   const double* v, const double* gamma, uint64_t r, double penalty,
+                   SelectWorkspace& ws, cudaStream_t s) {
+    require(n_rows >= 1, "translate: empty objective tensor");
+    require(m >= 1 && m <= (uint64_t)kMaxObj, "rv_select: unsupported objective count");
+    require(n_rows <= ws.rows_cap && r <= ws.r, "rv_select: workspace too small");
+    require(n_rows < 0xffffffffULL && r < 0xffffffffULL, "rv_select: index range");
+    gamma_check_kernel<<<(unsigned)((r + 255) / 256), 256, 0, s>>>(gamma, r, ws.err_flag);
+    launch_col_minmax(f, n_rows, n_rows_dev, m, ws.z, nullptr, ws.zkey, s);
+    TEMO_CUDA(cudaMemsetAsync(ws.best_key, 0xff, r * sizeof(unsigned long long), s));
+    TEMO_CUDA(cudaMemsetAsync(ws.best_row, 0xff, r * sizeof(uint32_t), s));
+    TEMO_CUDA(cudaMemsetAsync(ws.first_row, 0xff, r * sizeof(uint32_t), s));
+    switch (m) {
+    case 2: launch_assoc<2>(f, n_rows, n_rows_dev, m, v, gamma, r, penalty, ws, s); break;
+    case 3: launch_assoc<3>(f, n_rows, n_rows_dev, m, v, gamma, r, penalty, ws, s); break;
+    case 4: launch_assoc<4>(f, n_rows, n_rows_dev, m, v, gamma, r, penalty, ws, s); break;
+    case 5: launch_assoc<5>(f, n_rows, n_rows_dev, m, v, gamma, r, penalty, ws, s); break;
+    case 10: launch_assoc<10>(f, n_rows, n_rows_dev, m, v, gamma, r, penalty, ws, s); break;
+    default: launch_assoc<0>(f, n_rows, n_rows_dev, m, v, gamma, r, penalty, ws, s); break;
+    }
+    elite_rows_kernel<<<(unsigned)((n_rows + 255) / 256), 256, 0, s>>>(n_rows, n_rows_dev, ws.assoc, ws.apd,
+                                                                     ws.best_key, ws.best_row);
+    elite_compact_kernel<<<1, 1024, 0, s>>>(r, ws.apd, ws.first_row, ws.best_row, ws.elite, ws.valid,
+                                            ws.n_elite);
+    TEMO_CUDA(cudaGetLastError());
+}
+
+}  // namespace temo_b200
