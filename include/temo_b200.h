@@ -154,8 +154,14 @@ int temo_b200_run_create(const temo_b200_run_config* cfg, temo_b200_run** out);
  * survivors_f (optional, capacity r*m doubles, host) receives the survivors' objectives
  * (the per-generation result the reference hands to fill_metrics, algorithms.hpp:287). */
 int temo_b200_run_step(temo_b200_run* run, uint64_t* pop_size, double* survivors_f);
+/* Lock-step testing hook: one generation whose environmental selection runs on the caller's
+ * offspring objectives f_off (n x m, host) instead of the device-computed ones (those stay
+ * readable through temo_b200_run_last_generation). With parents injected too, the selection
+ * input is bit-identical to the CPU's, so the survivor set must be as well. */
+int temo_b200_run_step_injected(temo_b200_run* run, const double* f_off, uint64_t* pop_size);
 /* Lock-step testing hooks: overwrite / read the loop state with host data.
- * x: rows x d, f: rows x m, v: r x m, gamma: r (any may be NULL = keep). */
+ * x: rows x d, f: rows x m, v: r x m, gamma: r (any may be NULL = keep; x without f
+ * re-evaluates the injected rows on the device). */
 int temo_b200_run_inject(temo_b200_run* run, uint64_t rows, const double* x, const double* f,
                          const double* v, const double* gamma, uint64_t counter, uint64_t t);
 int temo_b200_run_state(temo_b200_run* run, uint64_t* rows, uint64_t* counter, uint64_t* t,
@@ -190,6 +196,11 @@ int temo_b200_dev_sync(void);
  * returns the mean ms per launch. stage: 1 reproduction (ga, unfused), 2 evaluation,
  * 3 reproduction with fused evaluation, 4 selection, 5 gamma. Used for the roofline. */
 int temo_b200_run_time_stage(temo_b200_run* run, int stage, int reps, double* mean_ms);
+/* Self-test hook for the libm-exact pow used by SBX / polynomial mutation / DTLZ4
+ * (reference call sites: operators.hpp:85-86,115-118; problems.hpp:79): out[e] = pow(x[e], y[e])
+ * evaluated by the device kernel (on_device = 1) or by its host twin (on_device = 0, no GPU
+ * needed). Must equal the host C library's pow bit for bit on the main path. */
+int temo_b200_pow(const double* x, const double* y, uint64_t n, double* out, int on_device);
 /* Overwrites >= bytes of scratch HBM (L2 flush between timed iterations). */
 int temo_b200_flush_l2(void);
 

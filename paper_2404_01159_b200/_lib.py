@@ -70,6 +70,7 @@ SIGNATURES = {
     "temo_b200_apd_penalty": (C.c_double, [u64, u64, u64, C.c_double]),
     "temo_b200_run_create": (C.c_int, [_CFG, C.POINTER(_RUN)]),
     "temo_b200_run_step": (C.c_int, [_RUN, u64p, f64p]),
+    "temo_b200_run_step_injected": (C.c_int, [_RUN, f64p, u64p]),
     "temo_b200_run_inject": (C.c_int, [_RUN, u64, f64p, f64p, f64p, f64p, u64, u64]),
     "temo_b200_run_state": (C.c_int, [_RUN, u64p, u64p, u64p, u64p, u64p, u64p]),
     "temo_b200_run_download": (C.c_int, [_RUN, f64p, f64p, f64p, f64p]),
@@ -83,6 +84,7 @@ SIGNATURES = {
     "temo_b200_dev_download": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t]),
     "temo_b200_dev_sync": (C.c_int, []),
     "temo_b200_run_time_stage": (C.c_int, [_RUN, C.c_int, C.c_int, f64p]),
+    "temo_b200_pow": (C.c_int, [f64p, f64p, u64, f64p, C.c_int]),
     "temo_b200_flush_l2": (C.c_int, []),
 }
 

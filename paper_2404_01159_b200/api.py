@@ -62,6 +62,14 @@ def init(device: int = 0) -> None:
     _call(_lib.load().temo_b200_init, device)
 
 
+def pow_like_host(x, y, on_device: bool = True) -> np.ndarray:
+    """Self-test hook: elementwise pow through the libm-exact implementation (device or host twin)."""
+    x, y = _t(x).reshape(-1), _t(y).reshape(-1)
+    out = np.empty_like(x)
+    _call(_lib.load().temo_b200_pow, _p(x), _p(y), u64(x.size), _p(out), 1 if on_device else 0)
+    return out
+
+
 # ------------------------------------------------------------------------------- rng.hpp
 @dataclass
 class RngStream:
@@ -374,6 +382,15 @@ class RveaRun:
         _call(self._L.temo_b200_run_step, self._h, C.byref(p), _p(self._fbuf) if want_f else None)
         if want_f:
             return p.value, self._fbuf[: p.value]
+        return p.value
+
+    def step_injected(self, f_off) -> int:
+        """Lock-step testing: selection runs on the given offspring objectives (n x m)."""
+        f_off = _t(f_off)
+        if f_off.shape != (self.n, self.m):
+            raise ValueError("step_injected: f_off must be n x m")
+        p = u64(0)
+        _call(self._L.temo_b200_run_step_injected, self._h, _p(f_off), C.byref(p))
         return p.value
 
     def state(self) -> dict:

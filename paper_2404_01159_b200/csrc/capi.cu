@@ -7,6 +7,7 @@
 #include <vector>
 
 #include "../../include/temo_b200.h"
+#include "glibc_pow.cuh"
 #include "internal.h"
 #include "run.h"
 
@@ -416,6 +417,14 @@ int temo_b200_run_step(temo_b200_run* run, uint64_t* pop_size, double* survivors
     });
 }
 
+int temo_b200_run_step_injected(temo_b200_run* run, const double* f_off, uint64_t* pop_size) {
+    return guarded([&] {
+        require(run && run->impl && f_off, "run_step_injected: null argument");
+        const uint64_t p = run->impl->step(nullptr, f_off);
+        if (pop_size) *pop_size = p;
+    });
+}
+
 int temo_b200_run_inject(temo_b200_run* run, uint64_t rows, const double* x, const double* f, const double* v,
                          const double* gamma, uint64_t counter, uint64_t t) {
     return guarded([&] {
@@ -514,6 +523,22 @@ int temo_b200_dev_download(void* dst, const void* src, size_t bytes) {
 
 int temo_b200_dev_sync(void) {
     return guarded([&] { TEMO_CUDA(cudaStreamSynchronize(ctx().stream)); });
+}
+
+int temo_b200_pow(const double* x, const double* y, uint64_t n, double* out, int on_device) {
+    return guarded([&] {
+        require(x && y && out, "pow: null argument");
+        if (!on_device) {
+            for (uint64_t e = 0; e < n; ++e) out[e] = glibc_pow_host(x[e], y[e]);
+            return;
+        }
+        Context& cx = ctx();
+        cudaStream_t s = cx.stream;
+        DevBuf<double> dx(x, n, s), dy(y, n, s), dout(n);
+        launch_pow_batch(dx.p, dy.p, n, dout.p, s);
+        dout.to_host(out, s);
+        TEMO_CUDA(cudaStreamSynchronize(s));
+    });
 }
 
 int temo_b200_flush_l2(void) {

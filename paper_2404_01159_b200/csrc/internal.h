@@ -64,6 +64,8 @@ void launch_random_reproduce(double* out, const uint32_t* dst, uint64_t n, uint6
                              uint64_t counter, const double* lower, const double* upper,
                              cudaStream_t s);
 void launch_uniform_fill(double* out, uint64_t count, Rng rng, uint64_t counter, cudaStream_t s);
+// pow with the host libm's bits (glibc_pow.cuh), elementwise; diagnostic/self-test entry.
+void launch_pow_batch(const double* x, const double* y, uint64_t n, double* out, cudaStream_t s);
 
 // ---- K2: evaluation -------------------------------------------------------------------------
 struct EvalArgs {

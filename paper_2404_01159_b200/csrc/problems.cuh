@@ -3,6 +3,7 @@
 // reference: problems.hpp:24-92 (DTLZ1-4). LSMOP1 is an extension (parity unpinned).
 #pragma once
 
+#include "glibc_pow_dev.cuh"
 #include "internal.h"
 
 namespace temo_b200 {
@@ -40,11 +41,11 @@ __device__ __forceinline__ void dtlz_finish(double sum, const double* pos, uint6
         } else {
             v = 1.0 + g;
             for (uint64_t i = 0; i + j + 1 < m; ++i) {
-                const double p = PID == kDtlz4 ? pow(pos[i], 100.0) : pos[i];
+                const double p = PID == kDtlz4 ? pow_like_host(pos[i], 100.0, pow_tables_global()) : pos[i];
                 v *= cos(p * half_pi);
             }
             if (j > 0) {
-                const double p = PID == kDtlz4 ? pow(pos[m - 1 - j], 100.0) : pos[m - 1 - j];
+                const double p = PID == kDtlz4 ? pow_like_host(pos[m - 1 - j], 100.0, pow_tables_global()) : pos[m - 1 - j];
                 v *= sin(p * half_pi);
             }
         }

@@ -17,6 +17,7 @@
 // IEEE operations in the reference's order. Dead branches the reference multiplies by an
 // exact 0.0 are skipped (verified bit-identical); the only inexact pieces are
 // CUDA's pow (<= 2 ulp) on crossed/mutated genes.
+#include "glibc_pow_dev.cuh"
 #include "internal.h"
 #include "problems.cuh"
 
@@ -44,13 +45,17 @@ struct ReproK {
 };
 
 // polynomial_delta (operators.hpp:106-121): both branches evaluated, blended by steps.
-__device__ __noinline__ double polynomial_delta_dev(double u, double x, double lo, double hi, double xi) {
+__device__ __noinline__ double polynomial_delta_dev(double u, double x, double lo, double hi, double xi,
+                                                    const PowSmem* tab) {
+    const PowTables T = pow_tables(*tab);
     const double range = hi - lo;
     const double e = xi + 1.0, inv_e = 1.0 / e;
     const double near_lo = 1.0 - (x - lo) / range;
-    const double d_lo = range * (pow(2.0 * u + (1.0 - 2.0 * u) * pow(near_lo, e), inv_e) - 1.0);
+    const double d_lo =
+        range * (pow_like_host(2.0 * u + (1.0 - 2.0 * u) * pow_like_host(near_lo, e, T), inv_e, T) - 1.0);
     const double near_hi = 1.0 - (hi - x) / range;
-    const double d_hi = range * (1.0 - pow(2.0 * (1.0 - u) + 2.0 * (u - 0.5) * pow(near_hi, e), inv_e));
+    const double d_hi =
+        range * (1.0 - pow_like_host(2.0 * (1.0 - u) + 2.0 * (u - 0.5) * pow_like_host(near_hi, e, T), inv_e, T));
     const double h_lo = (0.5 - u) >= 0.0 ? 1.0 : 0.0;
     const double h_hi = (u - 0.5) >= 0.0 ? 1.0 : 0.0;
     return d_lo * h_lo + d_hi * h_hi;
@@ -60,6 +65,10 @@ template <int MODE, bool SBX, bool PM, int EVAL, int VEC>
 __global__ void __launch_bounds__(256) reproduce_kernel(const ReproK a) {
     __shared__ double s_red[8];
     __shared__ double s_pos[2][kMaxObj];
+    __shared__ PowSmem s_pow;
+    pow_smem_load(s_pow);
+    __syncthreads();
+    const PowTables T = pow_tables(s_pow);
 
     const uint64_t unit = blockIdx.x;
     const bool paired = SBX && unit < a.half;
@@ -124,9 +133,9 @@ __global__ void __launch_bounds__(256) reproduce_kernel(const ReproK a) {
                     // live spread branch only (hm = H(0.5 - mc)); the other is multiplied by 0.0
                     double spread;
                     if (0.5 - mc >= 0.0)
-                        spread = pow(2.0 * mc, a.inv_exp);
+                        spread = pow_like_host(2.0 * mc, a.inv_exp, T);
                     else
-                        spread = pow(2.0 - 2.0 * mc, -a.inv_exp);
+                        spread = pow_like_host(2.0 - 2.0 * mc, -a.inv_exp, T);
                     const double b = (w1 >> 63) ? spread : -spread;  // sgn(r1 - 0.5) * spread
                     ca = ((1.0 + b) * xa[v] + (1.0 - b) * xb[v]) / 2.0;
                     cb = ((1.0 - b) * xa[v] + (1.0 + b) * xb[v]) / 2.0;
@@ -139,13 +148,13 @@ __global__ void __launch_bounds__(256) reproduce_kernel(const ReproK a) {
                 const uint64_t w4a = draw_word<MODE>(a.rng, a.c_mask + e_a + j);
                 if (live && (w4a >> 11) <= a.mask_thresh) {
                     const double u = word_to_unit(draw_word<MODE>(a.rng, a.c_mut + e_a + j));
-                    ca = clampd(ca + polynomial_delta_dev(u, ca, lo, hi, a.xi), lo, hi);
+                    ca = clampd(ca + polynomial_delta_dev(u, ca, lo, hi, a.xi, &s_pow), lo, hi);
                 }
                 if (paired) {
                     const uint64_t w4b = draw_word<MODE>(a.rng, a.c_mask + e_b + j);
                     if (live && (w4b >> 11) <= a.mask_thresh) {
                         const double u = word_to_unit(draw_word<MODE>(a.rng, a.c_mut + e_b + j));
-                        cb = clampd(cb + polynomial_delta_dev(u, cb, lo, hi, a.xi), lo, hi);
+                        cb = clampd(cb + polynomial_delta_dev(u, cb, lo, hi, a.xi, &s_pow), lo, hi);
                     }
                 }
             }
@@ -232,6 +241,15 @@ __global__ void uniform_fill_kernel(double* out, uint64_t count, Rng rng, uint64
         out[e] = word_to_unit(draw_word<MODE>(rng, counter + e));
 }
 
+__global__ void pow_batch_kernel(const double* x, const double* y, uint64_t n, double* out) {
+    __shared__ PowSmem s_pow;
+    pow_smem_load(s_pow);
+    __syncthreads();
+    const PowTables T = pow_tables(s_pow);
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < n; e += (uint64_t)gridDim.x * blockDim.x)
+        out[e] = pow_like_host(x[e], y[e], T);
+}
+
 inline unsigned stream_grid(uint64_t total, int block) {
     uint64_t g = (total + block - 1) / block;
     const uint64_t cap = (uint64_t)kSMs * 16;
@@ -285,6 +303,11 @@ void launch_reproduce(const ReproArgs& a, cudaStream_t s) {
         launch_mode<0>(k, a.do_sbx, a.do_pm, units, block, vec, a.eval_problem, s);
     else
         launch_mode<1>(k, a.do_sbx, a.do_pm, units, block, vec, a.eval_problem, s);
+    TEMO_CUDA(cudaGetLastError());
+}
+
+void launch_pow_batch(const double* x, const double* y, uint64_t n, double* out, cudaStream_t s) {
+    pow_batch_kernel<<<stream_grid(n, 256), 256, 0, s>>>(x, y, n, out);
     TEMO_CUDA(cudaGetLastError());
 }
 

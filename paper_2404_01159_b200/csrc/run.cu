@@ -202,7 +202,7 @@ Run::~Run() {
     }
     cudaFree(src); cudaFree(perm_dev); cudaFree(used); cudaFree(d_P);
     cudaFree(v0); cudaFree(v); cudaFree(gamma); cudaFree(lower); cudaFree(upper);
-    cudaFree(zmin); cudaFree(zmax); cudaFree(zscratch); cudaFree(skip_flag);
+    cudaFree(zmin); cudaFree(zmax); cudaFree(zscratch); cudaFree(skip_flag); cudaFree(f_off_saved);
     cudaFreeHost(h_status);
     ws.release();
     for (int e = 0; e < kNumEvents; ++e) cudaEventDestroy(ev[e]);
@@ -285,7 +285,7 @@ void Run::launch_offspring_eval() {
 
 bool Run::fusable() const { return cfg.fuse_eval && cfg.problem >= kDtlz1 && cfg.problem <= kDtlz4; }
 
-uint64_t Run::step(double* survivors_f_host) {
+uint64_t Run::step(double* survivors_f_host, const double* f_off_inject) {
     require(t < cfg.generations, "rvea_run: all generations already done");
     const double host0 = now_ms();
     P_before = P;
@@ -300,6 +300,12 @@ uint64_t Run::step(double* survivors_f_host) {
     TEMO_CUDA(cudaEventRecord(ev[1], stream));
     if (!fused) launch_offspring_eval();
     TEMO_CUDA(cudaEventRecord(ev[2], stream));
+    if (f_off_inject) {  // lock-step testing: keep the device's objectives aside, select on the given ones
+        if (!f_off_saved) f_off_saved = dev_alloc<double>(n * m);
+        TEMO_CUDA(cudaMemcpyAsync(f_off_saved, fm[cur] + P * m, n * m * sizeof(double), cudaMemcpyDeviceToDevice, stream));
+        TEMO_CUDA(cudaMemcpyAsync(fm[cur] + P * m, f_off_inject, n * m * sizeof(double), cudaMemcpyHostToDevice, stream));
+    }
+    f_off_was_injected = f_off_inject != nullptr;
 
     // environmental selection over the merged population (algorithms.hpp:274-279)
     const double penalty = apd_penalty(m, t, cfg.generations, cfg.alpha);
@@ -363,7 +369,18 @@ void Run::inject(uint64_t rows, const double* x, const double* f, const double* 
     } else {
         require(rows == P, "inject: row count must match when x is kept");
     }
-    if (f) TEMO_CUDA(cudaMemcpy(fm[cur], f, rows * m * sizeof(double), cudaMemcpyHostToDevice));
+    if (f) {
+        TEMO_CUDA(cudaMemcpy(fm[cur], f, rows * m * sizeof(double), cudaMemcpyHostToDevice));
+    } else if (x) {  // objectives of the injected rows come from the device evaluator
+        EvalArgs ea;
+        ea.problem = cfg.problem;
+        ea.x = pool;
+        ea.n = rows;
+        ea.d = d;
+        ea.m = m;
+        ea.f = fm[cur];
+        launch_evaluate(ea, stream);
+    }
     if (v_in) {
         TEMO_CUDA(cudaMemcpy(v, v_in, r * m * sizeof(double), cudaMemcpyHostToDevice));
         launch_row_norms(v, r, m, ws.vn, stream);
@@ -407,7 +424,8 @@ void Run::last_generation(double* offspring, double* f_off, uint64_t* elite_out)
         TEMO_CUDA(e);
     }
     if (f_off)
-        TEMO_CUDA(cudaMemcpy(f_off, fm[cur ^ 1] + P_prev() * m, n * m * sizeof(double), cudaMemcpyDeviceToHost));
+        TEMO_CUDA(cudaMemcpy(f_off, f_off_was_injected ? f_off_saved : fm[cur ^ 1] + P_prev() * m,
+                             n * m * sizeof(double), cudaMemcpyDeviceToHost));
     if (elite_out) {
         std::vector<uint32_t> tmp(P);
         TEMO_CUDA(cudaMemcpy(tmp.data(), ws.elite, P * sizeof(uint32_t), cudaMemcpyDeviceToHost));

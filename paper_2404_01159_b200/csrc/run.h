@@ -27,7 +27,7 @@ struct Run {
     Run(const Run&) = delete;
     Run& operator=(const Run&) = delete;
 
-    uint64_t step(double* survivors_f_host);
+    uint64_t step(double* survivors_f_host, const double* f_off_inject = nullptr);
     void inject(uint64_t rows, const double* x, const double* f, const double* v_in, const double* gamma_in,
                 uint64_t counter_in, uint64_t t_in);
     void download(double* x, double* f, double* v_out, double* gamma_out);
@@ -57,6 +57,8 @@ struct Run {
     double *zmin = nullptr, *zmax = nullptr;
     unsigned long long* zscratch = nullptr;
     uint32_t* skip_flag = nullptr;
+    double* f_off_saved = nullptr;  // device objectives of the last offspring when selection ran on injected ones
+    bool f_off_was_injected = false;
     SelectWorkspace ws;
 
     uint32_t* h_perm[2] = {nullptr, nullptr};  // pinned
