@@ -173,8 +173,9 @@ int temo_b200_run_download(temo_b200_run* run, double* x, double* f, double* v, 
 int temo_b200_run_last_generation(temo_b200_run* run, double* offspring, double* f_off,
                                   uint64_t* elite);
 /* Device-side timings of the last step in ms (CUDA events on the library stream):
- * [0] whole generation, [1] reproduction(+fused eval), [2] evaluation, [3] selection,
- * [4] adaptation, [5] host mating-permutation time (wall), [6..7] reserved. */
+ * [0] whole generation, [1] reproduction kernel (+fused evaluation), [2] standalone evaluation,
+ * [3] selection (+survivor commit), [4] adaptation, [5] host mating-permutation time (wall),
+ * [6] number of kernels launched in the step, [7] permutation upload + mating table. */
 int temo_b200_run_timings(temo_b200_run* run, double* ms8);
 int temo_b200_run_destroy(temo_b200_run* run);
 

@@ -425,7 +425,8 @@ class RveaRun:
     def timings(self) -> dict:
         ms = np.zeros(8)
         _call(self._L.temo_b200_run_timings, self._h, _p(ms))
-        return dict(generation=ms[0], reproduce=ms[1], evaluate=ms[2], select=ms[3], adapt=ms[4], host_perm=ms[5])
+        return dict(generation=ms[0], reproduce=ms[1], evaluate=ms[2], select=ms[3], adapt=ms[4], host_perm=ms[5],
+                    launches=int(ms[6]), prep=ms[7])
 
     def time_stage(self, stage: int, reps: int = 5) -> float:
         out = C.c_double(0)

@@ -242,12 +242,15 @@ void Run::ensure_permutation(const Plan& p) {
     spec_valid = true;
 }
 
-void Run::launch_reproduction(const Plan& p, bool fused) {
+void Run::launch_mating_table(const Plan& p) {
     const unsigned g = (unsigned)((n + 255) / 256);
     if (rng.mode == 0)
         build_src_kernel<0><<<g, 256, 0, stream>>>(perm_dev, parent_slot[cur], n, P, rng, p.c_pool, src);
     else
         build_src_kernel<1><<<g, 256, 0, stream>>>(perm_dev, parent_slot[cur], n, P, rng, p.c_pool, src);
+}
+
+void Run::launch_reproduction(const Plan& p, bool fused) {
     ReproArgs ra;
     ra.pool = pool;
     ra.src = src;
@@ -296,10 +299,13 @@ uint64_t Run::step(double* survivors_f_host, const double* f_off_inject) {
     TEMO_CUDA(cudaEventRecord(ev[0], stream));
     TEMO_CUDA(cudaMemcpyAsync(perm_dev, h_perm[hp], n * sizeof(uint32_t), cudaMemcpyHostToDevice, stream));
     const bool fused = fusable();
-    launch_reproduction(p, fused);
+    launch_mating_table(p);
     TEMO_CUDA(cudaEventRecord(ev[1], stream));
-    if (!fused) launch_offspring_eval();
+    launch_reproduction(p, fused);
     TEMO_CUDA(cudaEventRecord(ev[2], stream));
+    if (!fused) launch_offspring_eval();
+    TEMO_CUDA(cudaEventRecord(ev[3], stream));
+    uint64_t launches = 2 + (fused ? 0 : 1) + 6 + 2;
     if (f_off_inject) {  // lock-step testing: keep the device's objectives aside, select on the given ones
         if (!f_off_saved) f_off_saved = dev_alloc<double>(n * m);
         TEMO_CUDA(cudaMemcpyAsync(f_off_saved, fm[cur] + P * m, n * m * sizeof(double), cudaMemcpyDeviceToDevice, stream));
@@ -316,15 +322,16 @@ uint64_t Run::step(double* survivors_f_host, const double* f_off_inject) {
         ws.elite, ws.n_elite, P, m, parent_slot[cur], free_slot[cur], parent_slot[cur ^ 1], fm[cur], fm[cur ^ 1],
         used, d_P);
     free_list_kernel<<<1, 1024, 0, stream>>>(used, cap, n, free_slot[cur ^ 1]);
-    TEMO_CUDA(cudaEventRecord(ev[3], stream));
+    TEMO_CUDA(cudaEventRecord(ev[4], stream));
 
     // reference-vector adaptation (algorithms.hpp:281)
     if ((t + 1) % adapt_every == 0) {
         launch_col_minmax(fm[cur ^ 1], pcap, d_P, m, zmin, zmax, zscratch, stream);
         launch_adapt_vectors(v0, v, ws.vn, r, m, zmin, zmax, skip_flag, ws.err_flag, stream);
         launch_gamma(v, ws.vn, r, m, gamma, ws.err_flag, skip_flag, stream);
+        launches += 5;
     }
-    TEMO_CUDA(cudaEventRecord(ev[4], stream));
+    TEMO_CUDA(cudaEventRecord(ev[5], stream));
     TEMO_CUDA(cudaMemcpyAsync(h_status, ws.err_flag, sizeof(uint32_t), cudaMemcpyDeviceToHost, stream));
     TEMO_CUDA(cudaMemcpyAsync(h_status + 1, d_P, sizeof(uint32_t), cudaMemcpyDeviceToHost, stream));
     TEMO_CUDA(cudaGetLastError());
@@ -349,12 +356,14 @@ uint64_t Run::step(double* survivors_f_host, const double* f_off_inject) {
     if (survivors_f_host)
         TEMO_CUDA(cudaMemcpy(survivors_f_host, fm[cur], P * m * sizeof(double), cudaMemcpyDeviceToHost));
     float ms = 0.f;
-    cudaEventElapsedTime(&ms, ev[0], ev[4]); timings[0] = ms;
-    cudaEventElapsedTime(&ms, ev[0], ev[1]); timings[1] = ms;
-    cudaEventElapsedTime(&ms, ev[1], ev[2]); timings[2] = ms;
-    cudaEventElapsedTime(&ms, ev[2], ev[3]); timings[3] = ms;
-    cudaEventElapsedTime(&ms, ev[3], ev[4]); timings[4] = ms;
+    cudaEventElapsedTime(&ms, ev[0], ev[5]); timings[0] = ms;
+    cudaEventElapsedTime(&ms, ev[1], ev[2]); timings[1] = ms;
+    cudaEventElapsedTime(&ms, ev[2], ev[3]); timings[2] = ms;
+    cudaEventElapsedTime(&ms, ev[3], ev[4]); timings[3] = ms;
+    cudaEventElapsedTime(&ms, ev[4], ev[5]); timings[4] = ms;
     timings[5] = (host1 - host0) + (host3 - host2);
+    timings[6] = (double)launches;
+    cudaEventElapsedTime(&ms, ev[0], ev[1]); timings[7] = ms;
     return P;
 }
 
@@ -439,6 +448,7 @@ double Run::time_stage(int stage, int reps) {
     ensure_permutation(p);
     TEMO_CUDA(cudaMemcpyAsync(perm_dev, h_perm[hp], n * sizeof(uint32_t), cudaMemcpyHostToDevice, stream));
     // make sure the offspring rows / merged objectives of this generation exist for stages 2 and 4
+    launch_mating_table(p);
     launch_reproduction(p, false);
     launch_offspring_eval();
     const double penalty = apd_penalty(m, t < cfg.generations ? t : cfg.generations, cfg.generations, cfg.alpha);

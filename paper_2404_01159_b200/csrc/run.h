@@ -17,7 +17,7 @@ struct RunConfig {  // reference: RunConfig, algorithms.hpp:21-41
 void flush_l2();
 
 struct Run {
-    static constexpr int kNumEvents = 5;
+    static constexpr int kNumEvents = 6;
     struct Plan {
         uint64_t c_pool, c_shuffle, c_sbx, c_pm, c_end;
     };
@@ -73,6 +73,7 @@ private:
     void check_status();
     Plan plan_for(uint64_t P_now, uint64_t c) const;
     void ensure_permutation(const Plan& p);
+    void launch_mating_table(const Plan& p);
     void launch_reproduction(const Plan& p, bool fused);
     void launch_offspring_eval();
     bool fusable() const;
