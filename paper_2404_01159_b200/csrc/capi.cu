@@ -10,6 +10,7 @@
 #include "glibc_pow.cuh"
 #include "internal.h"
 #include "run.h"
+#include "vecindex.h"
 
 using namespace temo_b200;
 
@@ -82,6 +83,9 @@ RunConfig cfg_of(const temo_b200_run_config* c) {
     require(r.rng_mode == 0 || r.rng_mode == 1, "unknown rng mode");
     return r;
 }
+
+// below this many reference vectors the exhaustive scan is cheaper than building the index
+constexpr uint64_t kIndexMinVectors = 1024;
 
 void check_mode(int rng_mode) { require(rng_mode == 0 || rng_mode == 1, "unknown rng mode"); }
 
@@ -305,7 +309,17 @@ int temo_b200_min_vector_angles(const double* v, uint64_t r, uint64_t m, double*
         DevBuf<uint32_t> err(1);
         TEMO_CUDA(cudaMemsetAsync(err.p, 0, sizeof(uint32_t), s));
         launch_row_norms(dv.p, r, m, dvn.p, s);
-        launch_gamma(dv.p, dvn.p, r, m, dg.p, err.p, nullptr, s);
+        if (r >= kIndexMinVectors) {
+            VecIndex index;
+            index.alloc(r, m);
+            struct Guard { VecIndex& x; ~Guard() { x.release(); } } guard{index};
+            index.set_order(v, s);
+            index.build(dv.p, dvn.p, s);
+            launch_gamma_indexed(dv.p, dvn.p, r, m, index, dg.p, err.p, nullptr, s);
+            TEMO_CUDA(cudaStreamSynchronize(s));
+        } else {
+            launch_gamma(dv.p, dvn.p, r, m, dg.p, err.p, nullptr, s);
+        }
         uint32_t flag = 0;
         err.to_host(&flag, s);
         dg.to_host(gamma, s);
@@ -338,7 +352,17 @@ int temo_b200_adapt(const double* v0, double* v, double* gamma, uint64_t r, uint
         DevBuf<uint32_t> flags(2);
         TEMO_CUDA(cudaMemsetAsync(flags.p, 0, 2 * sizeof(uint32_t), s));
         launch_adapt_vectors(dv0.p, dv.p, dvn.p, r, m, dzmin.p, dzmax.p, flags.p + 1, flags.p, s);
-        launch_gamma(dv.p, dvn.p, r, m, dg.p, flags.p, flags.p + 1, s);
+        if (r >= kIndexMinVectors) {
+            VecIndex index;
+            index.alloc(r, m);
+            struct Guard { VecIndex& x; ~Guard() { x.release(); } } guard{index};
+            index.set_order(v0, s);
+            index.build(dv.p, dvn.p, s);
+            launch_gamma_indexed(dv.p, dvn.p, r, m, index, dg.p, flags.p, flags.p + 1, s);
+            TEMO_CUDA(cudaStreamSynchronize(s));
+        } else {
+            launch_gamma(dv.p, dvn.p, r, m, dg.p, flags.p, flags.p + 1, s);
+        }
         uint32_t h[2] = {0, 0};
         flags.to_host(h, s);
         std::vector<double> nv(r * m), ng(r);
@@ -375,7 +399,15 @@ int temo_b200_rv_select(const double* f, uint64_t n, uint64_t m, const double* v
             ~Guard() { w.release(); }
         } guard{ws};
         launch_row_norms(dv.p, r, m, ws.vn, s);
-        launch_select(df.p, n, nullptr, m, dv.p, dg.p, r, apd_penalty(m, t, t_max, alpha), ws, s);
+        VecIndex index;
+        struct IndexGuard { VecIndex& x; ~IndexGuard() { x.release(); } } index_guard{index};
+        const bool indexed = r >= kIndexMinVectors;
+        if (indexed) {
+            index.alloc(r, m);
+            index.set_order(v, s);
+            index.build(dv.p, ws.vn, s);
+        }
+        launch_select(df.p, n, nullptr, m, dv.p, dg.p, r, apd_penalty(m, t, t_max, alpha), ws, s, indexed ? &index : nullptr);
         uint32_t cnt = 0, flag = 0;
         std::vector<uint32_t> h_elite(r), h_assoc(assoc ? n : 0);
         TEMO_CUDA(cudaMemcpyAsync(&cnt, ws.n_elite, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));

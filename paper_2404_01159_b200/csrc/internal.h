@@ -102,9 +102,11 @@ struct SelectWorkspace {
 };
 // n_rows_dev (optional): device-side row count overriding n_rows (<= n_rows, which then only
 // sizes the grid).
+struct VecIndex;
+// index (optional): hierarchical direction index over v (vecindex.h); nullptr = exhaustive scan.
 void launch_select(const double* f, uint64_t n_rows, const uint32_t* n_rows_dev, uint64_t m,
                    const double* v, const double* gamma, uint64_t r, double penalty,
-                   SelectWorkspace& ws, cudaStream_t s);
+                   SelectWorkspace& ws, cudaStream_t s, VecIndex* index = nullptr);
 void launch_row_norms(const double* v, uint64_t r, uint64_t m, double* vn, cudaStream_t s);
 
 // ---- K4: reference vectors ----------------------------------------------------------------------

@@ -161,7 +161,10 @@ Run::Run(const RunConfig& c) : cfg(c) {
     TEMO_CUDA(cudaMemcpyAsync(v0, unit.data(), r * m * sizeof(double), cudaMemcpyHostToDevice, stream));
     TEMO_CUDA(cudaMemcpyAsync(v, v0, r * m * sizeof(double), cudaMemcpyDeviceToDevice, stream));
     launch_row_norms(v, r, m, ws.vn, stream);
-    launch_gamma(v, ws.vn, r, m, gamma, ws.err_flag, nullptr, stream);
+    vindex.alloc(r, m);
+    vindex.set_order(unit.data(), stream);
+    vindex.build(v, ws.vn, stream);
+    launch_gamma_indexed(v, ws.vn, r, m, vindex, gamma, ws.err_flag, nullptr, stream);
 
     std::vector<double> lo(d), hi(d);
     problem_bounds(cfg.problem, d, m, lo.data(), hi.data());
@@ -205,6 +208,7 @@ Run::~Run() {
     cudaFree(zmin); cudaFree(zmax); cudaFree(zscratch); cudaFree(skip_flag); cudaFree(f_off_saved);
     cudaFreeHost(h_status);
     ws.release();
+    vindex.release();
     for (int e = 0; e < kNumEvents; ++e) cudaEventDestroy(ev[e]);
 }
 
@@ -315,7 +319,7 @@ uint64_t Run::step(double* survivors_f_host, const double* f_off_inject) {
 
     // environmental selection over the merged population (algorithms.hpp:274-279)
     const double penalty = apd_penalty(m, t, cfg.generations, cfg.alpha);
-    launch_select(fm[cur], P + n, nullptr, m, v, gamma, r, penalty, ws, stream);
+    launch_select(fm[cur], P + n, nullptr, m, v, gamma, r, penalty, ws, stream, &vindex);
     TEMO_CUDA(cudaMemsetAsync(used, 0, cap, stream));
     const uint64_t kmax = r < P + n ? r : P + n;
     commit_survivors_kernel<<<(unsigned)((kmax + 255) / 256), 256, 0, stream>>>(
@@ -328,8 +332,9 @@ uint64_t Run::step(double* survivors_f_host, const double* f_off_inject) {
     if ((t + 1) % adapt_every == 0) {
         launch_col_minmax(fm[cur ^ 1], pcap, d_P, m, zmin, zmax, zscratch, stream);
         launch_adapt_vectors(v0, v, ws.vn, r, m, zmin, zmax, skip_flag, ws.err_flag, stream);
-        launch_gamma(v, ws.vn, r, m, gamma, ws.err_flag, skip_flag, stream);
-        launches += 5;
+        vindex.build(v, ws.vn, stream);
+        launch_gamma_indexed(v, ws.vn, r, m, vindex, gamma, ws.err_flag, skip_flag, stream);
+        launches += 6 + vindex.levels;
     }
     TEMO_CUDA(cudaEventRecord(ev[5], stream));
     TEMO_CUDA(cudaMemcpyAsync(h_status, ws.err_flag, sizeof(uint32_t), cudaMemcpyDeviceToHost, stream));
@@ -393,6 +398,7 @@ void Run::inject(uint64_t rows, const double* x, const double* f, const double* 
     if (v_in) {
         TEMO_CUDA(cudaMemcpy(v, v_in, r * m * sizeof(double), cudaMemcpyHostToDevice));
         launch_row_norms(v, r, m, ws.vn, stream);
+        vindex.build(v, ws.vn, stream);
     }
     if (gamma_in) TEMO_CUDA(cudaMemcpy(gamma, gamma_in, r * sizeof(double), cudaMemcpyHostToDevice));
     P = rows;
@@ -466,8 +472,10 @@ double Run::time_stage(int stage, int reps) {
             require(cfg.problem >= kDtlz1 && cfg.problem <= kDtlz4, "time_stage: fused evaluation is DTLZ-only");
             launch_reproduction(p, true);
             break;
-        case 4: launch_select(fm[cur], P + n, nullptr, m, v, gamma, r, penalty, ws, stream); break;
-        case 5: launch_gamma(v, ws.vn, r, m, gamma, ws.err_flag, nullptr, stream); break;
+        case 4: launch_select(fm[cur], P + n, nullptr, m, v, gamma, r, penalty, ws, stream, &vindex); break;
+        case 5: launch_gamma_indexed(v, ws.vn, r, m, vindex, gamma, ws.err_flag, nullptr, stream); break;
+        case 6: launch_select(fm[cur], P + n, nullptr, m, v, gamma, r, penalty, ws, stream, nullptr); break;
+        case 7: launch_gamma(v, ws.vn, r, m, gamma, ws.err_flag, nullptr, stream); break;
         default: fail(1, "time_stage: unknown stage");
         }
         TEMO_CUDA(cudaEventRecord(b, stream));

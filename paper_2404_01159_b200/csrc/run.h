@@ -2,6 +2,7 @@
 #pragma once
 
 #include "internal.h"
+#include "vecindex.h"
 
 namespace temo_b200 {
 
@@ -60,6 +61,7 @@ struct Run {
     double* f_off_saved = nullptr;  // device objectives of the last offspring when selection ran on injected ones
     bool f_off_was_injected = false;
     SelectWorkspace ws;
+    VecIndex vindex;  // hierarchical direction index over v (rebuilt after every adaptation)
 
     uint32_t* h_perm[2] = {nullptr, nullptr};  // pinned
     int hp = 0;

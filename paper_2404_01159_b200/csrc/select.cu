@@ -12,6 +12,7 @@
 // atomicMin, plus the reference's NaN rule (a NaN APD is never an improvement, but the first
 // row of a subpopulation is taken unconditionally).
 #include "internal.h"
+#include "vecindex.h"
 
 namespace temo_b200 {
 
@@ -281,7 +282,7 @@ void launch_col_minmax(const double* f, uint64_t n_rows, const uint32_t* n_rows_
 
 void launch_select(const double* f, uint64_t n_rows, const uint32_t* n_rows_dev, uint64_t m,
                    const double* v, const double* gamma, uint64_t r, double penalty,
-                   SelectWorkspace& ws, cudaStream_t s) {
+                   SelectWorkspace& ws, cudaStream_t s, VecIndex* index) {
     require(n_rows >= 1, "translate: empty objective tensor");
     require(m >= 1 && m <= (uint64_t)kMaxObj, "rv_select: unsupported objective count");
     require(n_rows <= ws.rows_cap && r <= ws.r, "rv_select: workspace too small");
@@ -291,6 +292,10 @@ void launch_select(const double* f, uint64_t n_rows, const uint32_t* n_rows_dev,
     TEMO_CUDA(cudaMemsetAsync(ws.best_key, 0xff, r * sizeof(unsigned long long), s));
     TEMO_CUDA(cudaMemsetAsync(ws.best_row, 0xff, r * sizeof(uint32_t), s));
     TEMO_CUDA(cudaMemsetAsync(ws.first_row, 0xff, r * sizeof(uint32_t), s));
+    if (index && index->built) {
+        launch_assoc_indexed(f, n_rows, n_rows_dev, m, ws.z, *index, gamma, penalty, ws.assoc, ws.theta, ws.apd,
+                             ws.best_key, ws.first_row, s);
+    } else
     switch (m) {
     case 2: launch_assoc<2>(f, n_rows, n_rows_dev, m, v, gamma, r, penalty, ws, s); break;
     case 3: launch_assoc<3>(f, n_rows, n_rows_dev, m, v, gamma, r, penalty, ws, s); break;
