@@ -1,0 +1,200 @@
+// temo_b200.hpp — reference-side binding: the reference's own signatures in namespace temo::b200,
+// forwarding to the C ABI of libtemo_b200.so (temo_b200.h).
+//
+// A maintainer of the reference adds this header next to proj/include/temo/*.hpp, links
+// libtemo_b200.so, and swaps one call: temo::sbx(...) -> temo::b200::sbx(...), temo::rv_select(...) ->
+// temo::b200::rv_select(...), temo::rvea_run(...) -> temo::b200::rvea_run(...). Argument meaning, RngStream
+// counter advance and exceptions are the reference's (std::invalid_argument for contract violations,
+// std::runtime_error otherwise). Requires the reference headers on the include path.
+//
+// reference interfaces mirrored: rng.hpp:55-78, operators.hpp:65-161,287-296, problems.hpp:69-92,
+// refvec.hpp:81-140, selection.hpp:131-135,200-224, algorithms.hpp:21-63,144-150,211-296.
+#pragma once
+
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "temo/algorithms.hpp"
+#include "temo/operators.hpp"
+#include "temo/problems.hpp"
+#include "temo/refvec.hpp"
+#include "temo/rng.hpp"
+#include "temo/selection.hpp"
+#include "temo_b200.h"
+
+namespace temo::b200 {
+
+namespace detail {
+
+inline void check(int rc) {
+    if (rc == TEMO_B200_OK) return;
+    const std::string msg = temo_b200_last_error();
+    if (rc == TEMO_B200_EINVAL) throw std::invalid_argument(msg);
+    if (rc == TEMO_B200_ENOMEM) throw std::bad_alloc();
+    throw std::runtime_error(msg);
+}
+
+inline temo_b200_ga_params ga_of(const GaParams& p) { return {p.pc, p.eta, p.pm, p.xi}; }
+
+inline int problem_id(const ProblemInstance& prob) {
+    if (prob.dtlz_id >= 1 && prob.dtlz_id <= 4) return prob.dtlz_id;
+    if (prob.name == "lsmop1") return TEMO_B200_LSMOP1;
+    throw std::invalid_argument("temo::b200: problem '" + prob.name + "' has no device evaluator");
+}
+
+using OperatorFn = int (*)(const double*, uint64_t, uint64_t, uint64_t, uint64_t*, const temo_b200_ga_params*,
+                           const double*, const double*, int, double*);
+
+inline Tensor2D run_operator(OperatorFn fn, const Tensor2D& x, RngStream& stream, const GaParams& p,
+                             const Tensor2D& lower, const Tensor2D& upper) {
+    temo::detail::require(lower.size() == x.cols && upper.size() == x.cols, "operator: bounds shape mismatch");
+    Tensor2D out(x.rows, x.cols);
+    const temo_b200_ga_params ga = ga_of(p);
+    uint64_t counter = stream.counter;
+    check(fn(x.data.data(), x.rows, x.cols, stream.seed, &counter, &ga, lower.data.data(), upper.data.data(),
+             TEMO_B200_RNG_SPLITMIX64, out.data.data()));
+    stream.counter = counter;
+    return out;
+}
+
+}  // namespace detail
+
+// ---- rng.hpp ---------------------------------------------------------------------------------
+inline Tensor2D uniform_tensor(RngStream& stream, std::size_t rows, std::size_t cols) {
+    Tensor2D out(rows, cols);
+    uint64_t counter = stream.counter;
+    detail::check(temo_b200_uniform_tensor(stream.seed, &counter, rows, cols, TEMO_B200_RNG_SPLITMIX64, out.data.data()));
+    stream.counter = counter;
+    return out;
+}
+
+// ---- operators.hpp ---------------------------------------------------------------------------
+inline Tensor2D sbx(const Tensor2D& x, RngStream& stream, const GaParams& p, const Tensor2D& lower,
+                    const Tensor2D& upper) {
+    return detail::run_operator(temo_b200_sbx, x, stream, p, lower, upper);
+}
+
+inline Tensor2D polynomial_mutation(const Tensor2D& x, RngStream& stream, const GaParams& p, const Tensor2D& lower,
+                                    const Tensor2D& upper) {
+    return detail::run_operator(temo_b200_polynomial_mutation, x, stream, p, lower, upper);
+}
+
+inline Tensor2D ga_reproduce(const Tensor2D& x, RngStream& stream, const GaParams& p, const Tensor2D& lower,
+                             const Tensor2D& upper) {
+    return detail::run_operator(temo_b200_ga_reproduce, x, stream, p, lower, upper);
+}
+
+inline Tensor2D random_reproduce(std::size_t n, std::size_t d, RngStream& stream, const Tensor2D& lower,
+                                 const Tensor2D& upper) {
+    Tensor2D out(n, d);
+    uint64_t counter = stream.counter;
+    detail::check(temo_b200_random_reproduce(n, d, stream.seed, &counter, lower.data.data(), upper.data.data(),
+                                             TEMO_B200_RNG_SPLITMIX64, out.data.data()));
+    stream.counter = counter;
+    return out;
+}
+
+// ---- problems.hpp ----------------------------------------------------------------------------
+inline Tensor2D dtlz_eval(int id, const Tensor2D& x, std::size_t m) {
+    temo::detail::require(id >= 1 && id <= 4, "dtlz_eval: id must be in 1..4");
+    Tensor2D f(x.rows, m);
+    detail::check(temo_b200_evaluate(id, x.data.data(), x.rows, x.cols, m, f.data.data()));
+    return f;
+}
+
+/// A ProblemInstance whose evaluate() runs on the device (drop-in for make_problem("dtlzN", ...)).
+inline ProblemInstance make_problem(const std::string& name, std::size_t dim = 0, std::size_t m = 3) {
+    ProblemInstance p = temo::make_problem(name, dim, m);
+    const int id = p.dtlz_id;
+    const std::size_t mm = p.num_obj;
+    p.evaluate = [id, mm](const Tensor2D& x) { return temo::b200::dtlz_eval(id, x, mm); };
+    return p;
+}
+
+// ---- refvec.hpp ------------------------------------------------------------------------------
+inline Tensor2D min_vector_angles(const Tensor2D& v) {
+    Tensor2D gamma(v.rows, 1);
+    detail::check(temo_b200_min_vector_angles(v.data.data(), v.rows, v.cols, gamma.data.data()));
+    return gamma;
+}
+
+inline RefVectorSet make_ref_set(std::size_t m, std::size_t H) {
+    RefVectorSet refs;
+    const std::size_t r = lattice_count(m, H);
+    refs.v0 = Tensor2D(r, m);
+    refs.gamma = Tensor2D(r, 1);
+    detail::check(temo_b200_make_ref_set(m, H, refs.v0.data.data(), refs.gamma.data.data()));
+    refs.v = refs.v0;
+    return refs;
+}
+
+inline void adapt(RefVectorSet& refs, const Tensor2D& z_min, const Tensor2D& z_max) {
+    temo::detail::require(z_min.size() == refs.v0.cols && z_max.size() == refs.v0.cols,
+                          "adapt_vectors: range shape mismatch");
+    detail::check(temo_b200_adapt(refs.v0.data.data(), refs.v.data.data(), refs.gamma.data.data(), refs.v0.rows,
+                                  refs.v0.cols, z_min.data.data(), z_max.data.data()));
+}
+
+// ---- selection.hpp ---------------------------------------------------------------------------
+inline SelectionOutcome rv_select(const Tensor2D& f, const RefVectorSet& refs, std::size_t t, std::size_t t_max,
+                                  double alpha, bool want_table = true) {
+    temo::detail::require(f.cols == refs.v.cols, "rv_select: objective count mismatch");
+    const std::size_t n = f.rows, r = refs.v.rows;
+    std::vector<uint64_t> elite(r ? r : 1), assoc(n);
+    std::vector<unsigned char> valid(r);
+    std::vector<double> apd(n);
+    uint64_t count = 0;
+    detail::check(temo_b200_rv_select(f.data.data(), n, f.cols, refs.v.data.data(), refs.gamma.data.data(), r, t, t_max,
+                                      alpha, elite.data(), &count, valid.data(), assoc.data(), nullptr, apd.data()));
+    SelectionOutcome out;
+    out.elite_indices.assign(elite.begin(), elite.begin() + count);
+    out.validity.assign(valid.begin(), valid.end());
+    if (want_table) {  // selection.hpp:218-222
+        out.apd_table = Tensor2D(n, r, inf);
+        for (std::size_t i = 0; i < n; ++i) out.apd_table(i, assoc[i]) = apd[i];
+    }
+    return out;
+}
+
+// ---- algorithms.hpp --------------------------------------------------------------------------
+/// rvea_run with the GA operator and track_archive = false, device-resident for the whole run.
+inline RunRecord rvea_run(const ProblemInstance& prob, const RunConfig& cfg) {
+    temo::detail::require(cfg.pop >= 2 && cfg.generations >= 1, "rvea_run: bad config");
+    if (cfg.op != "ga") throw std::invalid_argument("rvea_run: unknown operator '" + cfg.op + "'");
+    temo_b200_run_config c;
+    temo_b200_default_run_config(&c);
+    c.problem = detail::problem_id(prob);
+    c.pop = cfg.pop;
+    c.lattice_h = cfg.lattice_h;
+    c.generations = cfg.generations;
+    c.seed = cfg.seed;
+    c.dim = prob.dim;
+    c.obj = prob.num_obj;
+    c.alpha = cfg.alpha;
+    c.fr = cfg.fr;
+    c.time_budget_s = cfg.time_budget_s;
+    c.ga = detail::ga_of(cfg.ga);
+    const std::size_t h = cfg.lattice_h ? cfg.lattice_h : lattice_density_for(prob.num_obj, cfg.pop);
+    const std::size_t cap = std::max<std::size_t>(cfg.pop, lattice_count(prob.num_obj, h));
+    Tensor2D x(cap, prob.dim), f(cap, prob.num_obj);
+    std::vector<uint64_t> pops(cfg.generations);
+    std::vector<double> ms(cfg.generations);
+    uint64_t rows = 0, done = 0;
+    detail::check(temo_b200_rvea_run(&c, x.data.data(), f.data.data(), &rows, &done, pops.data(), ms.data()));
+    RunRecord rec;
+    for (uint64_t t = 0; t < done; ++t) {
+        GenerationRow row;
+        row.t = t;
+        row.elapsed_ms = ms[t];
+        row.pop_size = pops[t];
+        rec.rows.push_back(row);
+    }
+    rec.final_x = Tensor2D(rows, prob.dim);
+    rec.final_f = Tensor2D(rows, prob.num_obj);
+    std::copy_n(x.data.begin(), rows * prob.dim, rec.final_x.data.begin());
+    std::copy_n(f.data.begin(), rows * prob.num_obj, rec.final_f.data.begin());
+    return rec;
+}
+
+}  // namespace temo::b200

@@ -1,0 +1,129 @@
+// TEST INFRASTRUCTURE — the reference's own equivalence suites with the GPU path swapped in.
+//
+// Compiled (oracle/Makefile, only where /root/reference is mounted) against the UNMODIFIED reference
+// headers and include/temo_b200.hpp into oracle/_ref/shim_parity; linked to libtemo_b200.so. Each suite
+// re-hosts the instance generator of the reference's verify.hpp (same master seeds, same draw order) and
+// replaces the batched CPU call by its temo::b200:: twin, comparing against the reference's scalar oracle
+// (temo::oracle::*) exactly like the reference does:
+//   rv_select_suite   verify.hpp:53-76   200 instances, seed 7001: elite indices + validity identical, APD 1e-9
+//   operator_suite    verify.hpp:117-144 100 x {sbx, pm}, seed 7002 + op*1000003 + k: here bit-identical
+//   ga pipeline       test_operators.cpp:104-114
+//   whole run         test_algorithms.cpp:198-210 (seed 77) and BASELINE config #1
+// Exit code = number of failed suites.
+#include <cstdio>
+#include <cstring>
+
+#include "temo/verify.hpp"
+#include "temo_b200.hpp"
+
+using namespace temo;
+
+static bool same_bits(const Tensor2D& a, const Tensor2D& b) {
+    return a.same_shape(b) && std::memcmp(a.data.data(), b.data.data(), a.size() * sizeof(double)) == 0;
+}
+
+static int rv_select_suite_gpu() {
+    int failed = 0;
+    for (std::size_t k = 0; k < 200; ++k) {
+        RngStream g{7001 + k, 0};
+        const std::size_t n = verify::detail::pick(g, 1, 64);
+        const std::size_t m = verify::detail::pick(g, 2, 3);
+        const std::size_t h = m == 2 ? verify::detail::pick(g, 1, 14) : verify::detail::pick(g, 1, 4);
+        const std::size_t t_max = verify::detail::pick(g, 1, 200);
+        const std::size_t t = verify::detail::pick(g, 0, t_max);
+        const RefVectorSet refs = make_ref_set(m, h);
+        Tensor2D f = uniform_tensor(g, n, m);
+        for (double& v : f.data) v *= 10.0;
+        const SelectionOutcome a = b200::rv_select(f, refs, t, t_max, 2.0, true);
+        const SelectionOutcome b = oracle::oracle_rv_select(f, refs, t, t_max, 2.0);
+        bool ok = a.elite_indices == b.elite_indices && a.validity == b.validity;
+        for (std::size_t i = 0; ok && i < a.apd_table.size(); ++i)
+            ok = verify::detail::close(a.apd_table.data[i], b.apd_table.data[i], 1e-9);
+        failed += !ok;
+    }
+    std::printf("rv_select_suite (gpu vs oracle_rv_select): %d/200 failed\n", failed);
+    return failed;
+}
+
+static int operator_suite_gpu() {
+    int failed = 0;
+    for (std::size_t op = 0; op < 2; ++op) {
+        for (std::size_t k = 0; k < 100; ++k) {
+            const std::uint64_t seed = 7002 + op * 1000003 + k;
+            RngStream g{seed, 0};
+            auto inst = verify::detail::random_operator_instance(g, 2, 16, 8);
+            RngStream sa{seed ^ 0x5eed, 0}, sb{seed ^ 0x5eed, 0};
+            const GaParams p;
+            Tensor2D got, exp;
+            if (op == 0) {
+                got = b200::sbx(inst.x, sa, p, inst.lower, inst.upper);
+                exp = oracle::to_tensor(oracle::oracle_sbx(oracle::to_matrix(inst.x), sb, p, inst.lower.data, inst.upper.data));
+            } else {
+                got = b200::polynomial_mutation(inst.x, sa, p, inst.lower, inst.upper);
+                exp = oracle::to_tensor(oracle::oracle_pm(oracle::to_matrix(inst.x), sb, p, inst.lower.data, inst.upper.data));
+            }
+            failed += !(same_bits(got, exp) && sa.counter == sb.counter);
+        }
+    }
+    std::printf("operator_suite (gpu sbx/pm vs oracle, bit-exact): %d/200 failed\n", failed);
+    return failed;
+}
+
+static int ga_pipeline_gpu() {
+    int failed = 0;
+    for (std::uint64_t seed = 43; seed < 63; ++seed) {
+        RngStream g{seed, 0};
+        auto inst = verify::detail::random_operator_instance(g, 2, 40, 30);
+        RngStream sa{seed + 1, 7}, sb{seed + 1, 7};
+        const GaParams p;
+        const Tensor2D got = b200::ga_reproduce(inst.x, sa, p, inst.lower, inst.upper);
+        const Tensor2D exp = ga_reproduce(inst.x, sb, p, inst.lower, inst.upper);
+        failed += !(same_bits(got, exp) && sa.counter == sb.counter);
+    }
+    std::printf("ga_reproduce (gpu vs temo::ga_reproduce, bit-exact): %d/20 failed\n", failed);
+    return failed;
+}
+
+static int whole_run_gpu() {
+    int failed = 0;
+    struct Case { const char* problem; std::size_t dim, obj, pop, h, gens; std::uint64_t seed; };
+    const Case cases[] = {{"dtlz2", 8, 3, 12, 3, 10, 77}, {"dtlz1", 12, 3, 105, 13, 100, 42}};
+    for (const Case& c : cases) {
+        RunConfig cfg;
+        cfg.problem = c.problem;
+        cfg.pop = c.pop;
+        cfg.lattice_h = c.h;
+        cfg.generations = c.gens;
+        cfg.seed = c.seed;
+        cfg.track_archive = false;
+        const ProblemInstance prob = make_problem(c.problem, c.dim, c.obj);
+        const RunRecord a = b200::rvea_run(prob, cfg);
+        const RunRecord b = oracle::oracle_rvea_run(prob, cfg);
+        bool ok = a.rows.size() == b.rows.size();
+        std::size_t same_pop = 0;
+        for (std::size_t t = 0; ok && t < a.rows.size(); ++t) same_pop += a.rows[t].pop_size == b.rows[t].pop_size;
+        const bool x_same = same_bits(a.final_x, b.final_x);
+        bool f_close = a.final_f.same_shape(b.final_f);
+        for (std::size_t i = 0; f_close && i < a.final_f.size(); ++i)
+            f_close = verify::detail::close(a.final_f.data[i], b.final_f.data[i], 1e-9 * std::max(1.0, std::abs(b.final_f.data[i])));
+        std::printf("rvea_run %s pop=%zu gens=%zu seed=%llu: survivor counts equal in %zu/%zu generations, final x %s, final f %s\n",
+                    c.problem, c.pop, c.gens, (unsigned long long)c.seed, same_pop, a.rows.size(),
+                    x_same ? "bit-identical" : "differs", f_close ? "within 1e-9" : "differs");
+        failed += !(ok && same_pop == a.rows.size() && x_same && f_close);
+    }
+    return failed;
+}
+
+int main() {
+    if (temo_b200_device_count() < 1) {
+        std::printf("no CUDA device\n");
+        return 99;
+    }
+    int failed = 0;
+    failed += rv_select_suite_gpu() != 0;
+    failed += operator_suite_gpu() != 0;
+    failed += ga_pipeline_gpu() != 0;
+    failed += whole_run_gpu() != 0;
+    std::printf("%s\n", failed ? "SHIM PARITY FAILED" : "SHIM PARITY OK");
+    return failed;
+}

@@ -59,16 +59,22 @@ static inline unsigned long long temo_as_u64_host(double d) {
 #define TEMO_AS_U64(d) temo_as_u64_host(d)
 #endif
 
-// Returns true and writes *out when (x, y) is on the main path; false otherwise.
+// Returns true and writes *out when (x, y) is on a path restated here; false otherwise.
+// NARROW = true is the caller's promise that x is positive and normal, |y| is ordinary and
+// |y log x| < 512 (SBX: x in [2^-52, 2], |y| = 1/(eta+1)), which removes the range checks and the
+// under/overflow tail; the arithmetic of the common path is the same instruction for instruction.
+template <bool NARROW = false>
 __host__ __device__ inline bool glibc_pow_main(double x, double y, const PowTables& T, double* out) {
     unsigned long long ix = TEMO_AS_U64(x);
-    const unsigned long long iy = TEMO_AS_U64(y);
-    const unsigned topx = (unsigned)(ix >> 52), topy = (unsigned)(iy >> 52);
-    if ((topy & 0x7ffu) - 0x3beu > 0x7fu) return false;  // |y| tiny or huge (or nan)
-    if (topx - 1u > 0x7fdu) {
-        if (topx != 0u || ix == 0ULL) return false;  // zero, negative, inf, nan
-        // positive subnormal: normalise (x * 2^52, exponent corrected in the integer domain)
-        ix = TEMO_AS_U64(TEMO_MUL(x, 4503599627370496.0)) - (52ULL << 52);
+    if (!NARROW) {
+        const unsigned long long iy = TEMO_AS_U64(y);
+        const unsigned topx = (unsigned)(ix >> 52), topy = (unsigned)(iy >> 52);
+        if ((topy & 0x7ffu) - 0x3beu > 0x7fu) return false;  // |y| tiny or huge (or nan)
+        if (topx - 1u > 0x7fdu) {
+            if (topx != 0u || ix == 0ULL) return false;  // zero, negative, inf, nan
+            // positive subnormal: normalise (x * 2^52, exponent corrected in the integer domain)
+            ix = TEMO_AS_U64(TEMO_MUL(x, 4503599627370496.0)) - (52ULL << 52);
+        }
     }
 
     // ---- log_inline: x = 2^k z, z in [OFF, 2 OFF), c_i near the centre of z's subinterval
@@ -115,6 +121,7 @@ __host__ __device__ inline bool glibc_pow_main(double x, double y, const PowTabl
             *out = TEMO_ADD(ehi, 1.0);
             return true;
         }
+        if (NARROW) return false;
         if (abstop > 0x408u) {  // |y log x| >= 1024: certain under/overflow (round to nearest)
             *out = (TEMO_AS_U64(ehi) >> 63) ? 0.0 : TEMO_AS_DOUBLE(0x7ff0000000000000ULL);
             return true;
@@ -141,7 +148,7 @@ __host__ __device__ inline bool glibc_pow_main(double x, double y, const PowTabl
     const double acc = TEMO_FMA(c23, r2, tr);
     const double r4 = TEMO_MUL(r2, r2);
     const double tmpv = TEMO_FMA(c45, r4, acc);
-    if (special) {
+    if (!NARROW && special) {
         if ((ki & 0x80000000ULL) == 0) {  // k > 0: scale overflowed by <= 460 binades
             const double sc = TEMO_AS_DOUBLE(sbits - (1009ULL << 52));
             *out = TEMO_MUL(TEMO_FMA(sc, tmpv, sc), TEMO_AS_DOUBLE(0x7f00000000000000ULL));  // * 2^1009
@@ -179,7 +186,7 @@ inline double glibc_pow_host(double x, double y) {
     static const PowTables T{reinterpret_cast<const double*>(invc), reinterpret_cast<const double*>(logc),
                              reinterpret_cast<const double*>(logctail), exptab};
     double out;
-    if (glibc_pow_main(x, y, T, &out)) return out;
+    if (glibc_pow_main<false>(x, y, T, &out)) return out;
     return std::pow(x, y);
 }
 

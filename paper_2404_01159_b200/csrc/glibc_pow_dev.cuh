@@ -40,8 +40,15 @@ __device__ __forceinline__ PowTables pow_tables_global() {
 // pow with the host libm's bits on the main path, CUDA's pow elsewhere (x == 0, under/overflow).
 __device__ __forceinline__ double pow_like_host(double x, double y, const PowTables& T) {
     double out;
-    if (glibc_pow_main(x, y, T, &out)) return out;
+    if (glibc_pow_main<false>(x, y, T, &out)) return out;
     return pow(x, y);
+}
+
+// Same bits, for callers that guarantee a positive normal x, an ordinary y and |y log x| < 512.
+__device__ __forceinline__ double pow_like_host_narrow(double x, double y, const PowTables& T) {
+    double out;
+    if (glibc_pow_main<true>(x, y, T, &out)) return out;
+    return pow_like_host(x, y, T);
 }
 
 }  // namespace temo_b200

@@ -97,6 +97,7 @@ struct SelectWorkspace {
     unsigned char* valid = nullptr;   // [r]
     uint32_t* n_elite = nullptr;      // [1]
     uint32_t* err_flag = nullptr;     // [1] bit0: gamma <= 0
+    uint32_t* tile_scratch = nullptr; // compaction tile counts
     void alloc(uint64_t rows_cap_, uint64_t r_, uint64_t m_);
     void release();
 };

@@ -36,6 +36,7 @@ struct ReproK {
     double pc, inv_exp, xi;
     uint64_t mask_thresh;  // mutate iff (word >> 11) <= mask_thresh
     int mask_never;
+    int narrow_pow;  // 1/(eta+1) in [2^-10, 1]: the SBX pow stays on the common path of the libm algorithm
     const double* lower;
     const double* upper;
     uint64_t m;
@@ -61,14 +62,31 @@ __device__ __noinline__ double polynomial_delta_dev(double u, double x, double l
     return d_lo * h_lo + d_hi * h_hi;
 }
 
+// Counter stream positioned at a row of a draw block: word(j) is the draw of element j of that row.
+// SplitMix64: mix64(mix64(seed) + (c0 + j) * GOLDEN); the row offset is folded into `a` once per
+// CTA so that a draw costs one 32x64-bit multiply-add plus the two mixing rounds.
+template <int MODE>
+struct RowStream {
+    uint64_t a;
+    uint64_t seed;
+    __device__ __forceinline__ RowStream(const Rng& g, uint64_t c0) : a(MODE == 0 ? g.base + c0 * kGolden : c0), seed(g.seed) {}
+    __device__ __forceinline__ uint64_t word(uint32_t j) const {
+        if (MODE == 0) return mix64(a + (uint64_t)j * kGolden);
+        return philox_word(seed, a + j);
+    }
+};
+
 template <int MODE, bool SBX, bool PM, int EVAL, int VEC>
-__global__ void __launch_bounds__(256) reproduce_kernel(const ReproK a) {
+__global__ void __launch_bounds__(256, 3) reproduce_kernel(const ReproK a) {
     __shared__ double s_red[8];
     __shared__ double s_pos[2][kMaxObj];
     __shared__ PowSmem s_pow;
+    __shared__ unsigned char s_list[8][64];  // per warp: compacted (lane, v) codes of the crossing genes
+    __shared__ double s_beta[8][64];         // per warp: signed spread factor per (lane, v)
     pow_smem_load(s_pow);
     __syncthreads();
     const PowTables T = pow_tables(s_pow);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
     const uint64_t unit = blockIdx.x;
     const bool paired = SBX && unit < a.half;
@@ -89,6 +107,12 @@ __global__ void __launch_bounds__(256) reproduce_kernel(const ReproK a) {
         ob = a.out + dst_b * a.d;
     }
 
+    // draw streams of this CTA's rows: SBX blocks are half x d, PM blocks n x d
+    const RowStream<MODE> st_mc(a.rng, a.c_mc + unit * a.d), st_r1(a.rng, a.c_r1 + unit * a.d),
+        st_r2(a.rng, a.c_r2 + unit * a.d);
+    const RowStream<MODE> st_mask_a(a.rng, a.c_mask + row_a * a.d), st_mut_a(a.rng, a.c_mut + row_a * a.d);
+    const RowStream<MODE> st_mask_b(a.rng, a.c_mask + row_b * a.d), st_mut_b(a.rng, a.c_mut + row_b * a.d);
+
     // pair-level crossover switch: hc = H(r3 - pc) (operators.hpp:82)
     bool pair_cross = false;
     if (paired) {
@@ -97,47 +121,80 @@ __global__ void __launch_bounds__(256) reproduce_kernel(const ReproK a) {
     }
 
     double acc_a = 0.0, acc_b = 0.0;
-    const uint64_t nvec = a.d / VEC;
-    const uint64_t e_pair = unit * a.d;   // element offset inside the half x d SBX blocks
-    const uint64_t e_a = row_a * a.d;     // element offsets inside the n x d PM blocks
-    const uint64_t e_b = row_b * a.d;
+    const uint32_t nvec = (uint32_t)(a.d / VEC);
+    const uint32_t nvec_ceil = (nvec + blockDim.x - 1) / blockDim.x * blockDim.x;
 
-    for (uint64_t q = threadIdx.x; q < nvec; q += blockDim.x) {
-        const uint64_t j0 = q * VEC;
+    for (uint32_t q = threadIdx.x; q < nvec_ceil; q += blockDim.x) {  // whole warps stay in the loop
+        const bool in_range = q < nvec;
+        const uint32_t j0 = q * VEC;
         double xa[VEC], xb[VEC];
-        if (VEC == 2) {
-            const double2 t = *reinterpret_cast<const double2*>(pa + j0);
-            xa[0] = t.x;
-            xa[VEC - 1] = t.y;
-            if (paired) {
-                const double2 w = *reinterpret_cast<const double2*>(pb + j0);
-                xb[0] = w.x;
-                xb[VEC - 1] = w.y;
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) xa[v] = xb[v] = 0.0;
+        if (in_range) {
+            if (VEC == 2) {
+                const double2 t = *reinterpret_cast<const double2*>(pa + j0);
+                xa[0] = t.x;
+                xa[VEC - 1] = t.y;
+                if (paired) {
+                    const double2 w = *reinterpret_cast<const double2*>(pb + j0);
+                    xb[0] = w.x;
+                    xb[VEC - 1] = w.y;
+                }
+            } else {
+                xa[0] = pa[j0];
+                if (paired) xb[0] = pb[j0];
             }
-        } else {
-            xa[0] = pa[j0];
-            if (paired) xb[0] = pb[j0];
+        }
+        double beta[VEC];
+        bool crosses[VEC];
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) {
+            beta[v] = 1.0;
+            crosses[v] = false;
+        }
+        if (SBX && paired && pair_cross) {  // CTA-uniform
+            // hr = H(r2 - 0.5): the top bit of the word; a gene crosses iff it is clear (operators.hpp:90-91)
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) crosses[v] = in_range && (st_r2.word(j0 + v) >> 63) == 0;
+            // The spread factor (two draws + one pow) is needed by ~half of the genes only: compact the
+            // crossing genes of the warp so that the expensive part runs with full lanes.
+            const unsigned b0 = __ballot_sync(0xffffffffu, crosses[0]);
+            const unsigned b1 = VEC == 2 ? __ballot_sync(0xffffffffu, crosses[VEC - 1]) : 0u;
+            const unsigned lt = (1u << lane) - 1u;
+            const int n0 = __popc(b0), total = n0 + __popc(b1);
+            if (crosses[0]) s_list[warp][__popc(b0 & lt)] = (unsigned char)(lane * 2);
+            if (VEC == 2 && crosses[VEC - 1]) s_list[warp][n0 + __popc(b1 & lt)] = (unsigned char)(lane * 2 + 1);
+            __syncwarp();
+            const uint32_t q_warp = q - lane;  // vector index handled by lane 0 of this warp
+            for (int t = lane; t < total; t += 32) {
+                const int code = s_list[warp][t];
+                const uint32_t j = (q_warp + (code >> 1)) * VEC + (code & 1);
+                const double mc = word_to_unit(st_mc.word(j));
+                const bool up = (st_r1.word(j) >> 63) != 0;  // sgn(r1 - 0.5)
+                // live spread branch only (hm = H(0.5 - mc)); the other one is multiplied by exactly 0.0
+                const bool low = 0.5 - mc >= 0.0;
+                const double base = low ? 2.0 * mc : 2.0 - 2.0 * mc;
+                // base is 0 (mc == 0) or in [2^-52, 2]; |y log base| < 2 for any eta >= 0
+                const double yexp = low ? a.inv_exp : -a.inv_exp;
+                const double spread = (base > 0.0 && a.narrow_pow) ? pow_like_host_narrow(base, yexp, T) : pow_like_host(base, yexp, T);
+                s_beta[warp][code] = up ? spread : -spread;
+            }
+            __syncwarp();
+#pragma unroll
+            for (int v = 0; v < VEC; ++v)
+                if (crosses[v]) beta[v] = s_beta[warp][lane * 2 + v];
+            __syncwarp();
         }
 #pragma unroll
         for (int v = 0; v < VEC; ++v) {
-            const uint64_t j = j0 + v;
+            const uint32_t j = j0 + v;
+            if (!in_range) continue;
             const double lo = a.lower[j], hi = a.upper[j];
-            double ca = xa[v], cb = paired ? xb[v] : 0.0;
+            double ca = xa[v], cb = xb[v];
             if (SBX && paired) {
-                const uint64_t e = e_pair + j;
-                const uint64_t w2 = draw_word<MODE>(a.rng, a.c_r2 + e);
-                const bool keep = (w2 >> 63) != 0;  // hr = H(r2 - 0.5): top bit of the word
-                if (pair_cross && !keep) {
-                    const double mc = word_to_unit(draw_word<MODE>(a.rng, a.c_mc + e));
-                    const uint64_t w1 = draw_word<MODE>(a.rng, a.c_r1 + e);
-                    // live spread branch only (hm = H(0.5 - mc)); the other is multiplied by 0.0
-                    double spread;
-                    if (0.5 - mc >= 0.0)
-                        spread = pow_like_host(2.0 * mc, a.inv_exp, T);
-                    else
-                        spread = pow_like_host(2.0 - 2.0 * mc, -a.inv_exp, T);
-                    const double b = (w1 >> 63) ? spread : -spread;  // sgn(r1 - 0.5) * spread
-                    ca = ((1.0 + b) * xa[v] + (1.0 - b) * xb[v]) / 2.0;
+                if (crosses[v]) {
+                    const double b = beta[v];
+                    ca = ((1.0 + b) * xa[v] + (1.0 - b) * xb[v]) / 2.0;  // operators.hpp:94-95
                     cb = ((1.0 - b) * xa[v] + (1.0 + b) * xb[v]) / 2.0;
                 }
                 ca = clampd(ca, lo, hi);
@@ -145,17 +202,13 @@ __global__ void __launch_bounds__(256) reproduce_kernel(const ReproK a) {
             }
             if (PM && !a.mask_never) {
                 const bool live = !(hi - lo <= 0.0);
-                const uint64_t w4a = draw_word<MODE>(a.rng, a.c_mask + e_a + j);
-                if (live && (w4a >> 11) <= a.mask_thresh) {
-                    const double u = word_to_unit(draw_word<MODE>(a.rng, a.c_mut + e_a + j));
+                if (live && (st_mask_a.word(j) >> 11) <= a.mask_thresh) {
+                    const double u = word_to_unit(st_mut_a.word(j));
                     ca = clampd(ca + polynomial_delta_dev(u, ca, lo, hi, a.xi, &s_pow), lo, hi);
                 }
-                if (paired) {
-                    const uint64_t w4b = draw_word<MODE>(a.rng, a.c_mask + e_b + j);
-                    if (live && (w4b >> 11) <= a.mask_thresh) {
-                        const double u = word_to_unit(draw_word<MODE>(a.rng, a.c_mut + e_b + j));
-                        cb = clampd(cb + polynomial_delta_dev(u, cb, lo, hi, a.xi, &s_pow), lo, hi);
-                    }
+                if (paired && live && (st_mask_b.word(j) >> 11) <= a.mask_thresh) {
+                    const double u = word_to_unit(st_mut_b.word(j));
+                    cb = clampd(cb + polynomial_delta_dev(u, cb, lo, hi, a.xi, &s_pow), lo, hi);
                 }
             }
             if (EVAL != 0) {
@@ -170,12 +223,14 @@ __global__ void __launch_bounds__(256) reproduce_kernel(const ReproK a) {
             xa[v] = ca;
             xb[v] = cb;
         }
-        if (VEC == 2) {
-            *reinterpret_cast<double2*>(oa + j0) = make_double2(xa[0], xa[VEC - 1]);
-            if (paired) *reinterpret_cast<double2*>(ob + j0) = make_double2(xb[0], xb[VEC - 1]);
-        } else {
-            oa[j0] = xa[0];
-            if (paired) ob[j0] = xb[0];
+        if (in_range) {
+            if (VEC == 2) {
+                *reinterpret_cast<double2*>(oa + j0) = make_double2(xa[0], xa[VEC - 1]);
+                if (paired) *reinterpret_cast<double2*>(ob + j0) = make_double2(xb[0], xb[VEC - 1]);
+            } else {
+                oa[j0] = xa[0];
+                if (paired) ob[j0] = xb[0];
+            }
         }
     }
 
@@ -262,6 +317,7 @@ inline unsigned stream_grid(uint64_t total, int block) {
 
 void launch_reproduce(const ReproArgs& a, cudaStream_t s) {
     require(a.n >= 1 && a.d >= 1, "reproduce: empty population");
+    require(a.d < 0xffffffffULL, "reproduce: decision dimension exceeds 32 bits");
     if (a.do_sbx) require(a.n >= 2, "sbx: needs at least two rows");  // operators.hpp:67
     require(a.eval_problem == 0 || (a.m >= 2 && a.m <= (uint64_t)kMaxObj && a.d >= a.m),
             "reproduce: bad objective count for fused evaluation");
@@ -284,6 +340,7 @@ void launch_reproduce(const ReproArgs& a, cudaStream_t s) {
     k.pc = a.ga.pc;
     k.inv_exp = 1.0 / (a.ga.eta + 1.0);  // operators.hpp:75
     k.xi = a.ga.xi;
+    k.narrow_pow = (k.inv_exp >= 0x1.0p-10 && k.inv_exp <= 1.0) ? 1 : 0;
     // H(rate - r4) == 1  <=>  r4 <= rate  <=>  (word >> 11) <= floor(rate * 2^53)   (r4 = k * 2^-53)
     const double rate = a.ga.pm / (double)a.d;  // operators.hpp:133
     k.mask_never = !(rate >= 0.0);

@@ -16,6 +16,7 @@
 #include <cmath>
 #include <cstring>
 
+#include "compact.cuh"
 #include "internal.h"
 #include "run.h"
 
@@ -54,38 +55,14 @@ __global__ void commit_survivors_kernel(const uint32_t* elite, const uint32_t* n
     for (uint64_t j = 0; j < m; ++j) f_next[k * m + j] = f_merged[(uint64_t)e * m + j];
 }
 
-// One CTA: the first `want` unused slots in ascending order become the next free list.
-__global__ void __launch_bounds__(1024) free_list_kernel(const unsigned char* used, uint64_t cap, uint64_t want,
-                                                        uint32_t* free_slot) {
-    __shared__ uint32_t s_warp[32];
-    const uint64_t chunk = (cap + blockDim.x - 1) / blockDim.x;
-    const uint64_t lo = threadIdx.x * chunk;
-    const uint64_t hi = lo + chunk < cap ? lo + chunk : cap;
-    uint32_t cnt = 0;
-    for (uint64_t s = lo; s < hi; ++s) cnt += used[s] == 0;
-    uint32_t incl = cnt;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-        const uint32_t o = __shfl_up_sync(0xffffffffu, incl, off);
-        if (lane >= off) incl += o;
-    }
-    if (lane == 31) s_warp[warp] = incl;
-    __syncthreads();
-    if (warp == 0) {
-        uint32_t w = s_warp[lane];
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-            const uint32_t o = __shfl_up_sync(0xffffffffu, w, off);
-            if (lane >= off) w += o;
-        }
-        s_warp[lane] = w;
-    }
-    __syncthreads();
-    uint64_t pos = incl - cnt + (warp ? s_warp[warp - 1] : 0);
-    for (uint64_t s = lo; s < hi && pos < want; ++s)
-        if (used[s] == 0) free_slot[pos++] = (uint32_t)s;
-}
+// The first `want` unused slots in ascending order become the next free list.
+struct FreePred {
+    const unsigned char* used;
+    __device__ bool operator()(uint64_t i) const { return used[i] == 0; }
+};
+struct IdentityVal {
+    __device__ uint32_t operator()(uint64_t i) const { return (uint32_t)i; }
+};
 
 __global__ void iota_kernel(uint32_t* p, uint64_t n, uint32_t first) {
     const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
@@ -143,6 +120,7 @@ Run::Run(const RunConfig& c) : cfg(c) {
     perm_dev = dev_alloc<uint32_t>(n);
     used = dev_alloc<unsigned char>(cap);
     d_P = dev_alloc<uint32_t>(1);
+    free_scratch = dev_alloc<uint32_t>((cap + kCompactTile - 1) / kCompactTile + 1);
     v0 = dev_alloc<double>(r * m);
     v = dev_alloc<double>(r * m);
     gamma = dev_alloc<double>(r);
@@ -203,7 +181,7 @@ Run::~Run() {
         cudaFree(free_slot[b]);
         cudaFreeHost(h_perm[b]);
     }
-    cudaFree(src); cudaFree(perm_dev); cudaFree(used); cudaFree(d_P);
+    cudaFree(src); cudaFree(perm_dev); cudaFree(used); cudaFree(d_P); cudaFree(free_scratch);
     cudaFree(v0); cudaFree(v); cudaFree(gamma); cudaFree(lower); cudaFree(upper);
     cudaFree(zmin); cudaFree(zmax); cudaFree(zscratch); cudaFree(skip_flag); cudaFree(f_off_saved);
     cudaFreeHost(h_status);
@@ -309,7 +287,7 @@ uint64_t Run::step(double* survivors_f_host, const double* f_off_inject) {
     TEMO_CUDA(cudaEventRecord(ev[2], stream));
     if (!fused) launch_offspring_eval();
     TEMO_CUDA(cudaEventRecord(ev[3], stream));
-    uint64_t launches = 2 + (fused ? 0 : 1) + 6 + 2;
+    uint64_t launches = 2 + (fused ? 0 : 1) + 9 + 4;
     if (f_off_inject) {  // lock-step testing: keep the device's objectives aside, select on the given ones
         if (!f_off_saved) f_off_saved = dev_alloc<double>(n * m);
         TEMO_CUDA(cudaMemcpyAsync(f_off_saved, fm[cur] + P * m, n * m * sizeof(double), cudaMemcpyDeviceToDevice, stream));
@@ -325,7 +303,7 @@ uint64_t Run::step(double* survivors_f_host, const double* f_off_inject) {
     commit_survivors_kernel<<<(unsigned)((kmax + 255) / 256), 256, 0, stream>>>(
         ws.elite, ws.n_elite, P, m, parent_slot[cur], free_slot[cur], parent_slot[cur ^ 1], fm[cur], fm[cur ^ 1],
         used, d_P);
-    free_list_kernel<<<1, 1024, 0, stream>>>(used, cap, n, free_slot[cur ^ 1]);
+    launch_compact(cap, FreePred{used}, IdentityVal{}, free_scratch, n, free_slot[cur ^ 1], nullptr, stream);
     TEMO_CUDA(cudaEventRecord(ev[4], stream));
 
     // reference-vector adaptation (algorithms.hpp:281)

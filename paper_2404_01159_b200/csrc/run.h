@@ -54,6 +54,7 @@ struct Run {
     uint32_t* perm_dev = nullptr;
     unsigned char* used = nullptr;
     uint32_t* d_P = nullptr;
+    uint32_t* free_scratch = nullptr;
     double *v0 = nullptr, *v = nullptr, *gamma = nullptr, *lower = nullptr, *upper = nullptr;
     double *zmin = nullptr, *zmax = nullptr;
     unsigned long long* zscratch = nullptr;

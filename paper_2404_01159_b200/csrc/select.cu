@@ -11,6 +11,7 @@
 // minimum of (apd, row) — implemented order-independently with two rounds of 64-bit/32-bit
 // atomicMin, plus the reference's NaN rule (a NaN APD is never an improvement, but the first
 // row of a subpopulation is taken unconditionally).
+#include "compact.cuh"
 #include "internal.h"
 #include "vecindex.h"
 
@@ -169,50 +170,25 @@ __global__ void elite_rows_kernel(uint64_t n_rows, const uint32_t* n_rows_dev, c
     if (key == best_key[j]) atomicMin(&best_row[j], (uint32_t)i);
 }
 
-// One CTA: validity + compaction of the elites in ascending vector index (selection.hpp:216-217).
-__global__ void __launch_bounds__(1024) elite_compact_kernel(uint64_t r, const double* apd,
-                                                            const uint32_t* first_row,
-                                                            const uint32_t* best_row, uint32_t* elite,
-                                                            unsigned char* valid, uint32_t* n_elite) {
-    __shared__ uint32_t s_warp[32];
-    __shared__ uint32_t s_total;
-    const uint64_t chunk = (r + blockDim.x - 1) / blockDim.x;
-    const uint64_t lo = threadIdx.x * chunk;
-    const uint64_t hi = lo + chunk < r ? lo + chunk : r;
-    uint32_t cnt = 0;
-    for (uint64_t j = lo; j < hi; ++j) cnt += first_row[j] != 0xffffffffu;
-    // block exclusive scan of cnt
-    uint32_t incl = cnt;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-        const uint32_t o = __shfl_up_sync(0xffffffffu, incl, off);
-        if (lane >= off) incl += o;
-    }
-    if (lane == 31) s_warp[warp] = incl;
-    __syncthreads();
-    if (warp == 0) {
-        uint32_t w = s_warp[lane];
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-            const uint32_t o = __shfl_up_sync(0xffffffffu, w, off);
-            if (lane >= off) w += o;
-        }
-        s_warp[lane] = w;
-        if (lane == 31) s_total = w;
-    }
-    __syncthreads();
-    uint32_t pos = incl - cnt + (warp ? s_warp[warp - 1] : 0);
-    for (uint64_t j = lo; j < hi; ++j) {
+// validity + the elite of every valid vector (selection.hpp:209-217); compaction in ascending j follows
+struct ElitePred {
+    const uint32_t* first_row;
+    __device__ bool operator()(uint64_t j) const { return first_row[j] != 0xffffffffu; }
+};
+struct EliteVal {
+    const double* apd;
+    const uint32_t* first_row;
+    const uint32_t* best_row;
+    // a NaN APD in the first row of a subpopulation is never displaced (selection.hpp:211)
+    __device__ uint32_t operator()(uint64_t j) const {
         const uint32_t fr = first_row[j];
-        const bool ok = fr != 0xffffffffu;
-        valid[j] = ok ? 1 : 0;
-        if (ok) {
-            const double a0 = apd[fr];
-            elite[pos++] = (a0 != a0) ? fr : best_row[j];
-        }
+        const double a0 = apd[fr];
+        return (a0 != a0) ? fr : best_row[j];
     }
-    if (threadIdx.x == 0) *n_elite = s_total;
+};
+__global__ void validity_kernel(const uint32_t* first_row, uint64_t r, unsigned char* valid) {
+    const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (j < r) valid[j] = first_row[j] != 0xffffffffu ? 1 : 0;
 }
 
 template <int M>
@@ -252,13 +228,14 @@ void SelectWorkspace::alloc(uint64_t rows_cap_, uint64_t r_, uint64_t m_) {
     valid = dev_alloc<unsigned char>(r);
     n_elite = dev_alloc<uint32_t>(1);
     err_flag = dev_alloc<uint32_t>(1);
+    tile_scratch = dev_alloc<uint32_t>((r + kCompactTile - 1) / kCompactTile + 1);
     TEMO_CUDA(cudaMemset(err_flag, 0, sizeof(uint32_t)));
 }
 
 void SelectWorkspace::release() {
     cudaFree(z); cudaFree(zkey); cudaFree(vn); cudaFree(assoc); cudaFree(theta); cudaFree(apd);
     cudaFree(best_key); cudaFree(best_row); cudaFree(first_row); cudaFree(elite); cudaFree(valid);
-    cudaFree(n_elite); cudaFree(err_flag);
+    cudaFree(n_elite); cudaFree(err_flag); cudaFree(tile_scratch);
     *this = SelectWorkspace{};
 }
 
@@ -306,8 +283,9 @@ void launch_select(const double* f, uint64_t n_rows, const uint32_t* n_rows_dev,
     }
     elite_rows_kernel<<<(unsigned)((n_rows + 255) / 256), 256, 0, s>>>(n_rows, n_rows_dev, ws.assoc, ws.apd,
                                                                      ws.best_key, ws.best_row);
-    elite_compact_kernel<<<1, 1024, 0, s>>>(r, ws.apd, ws.first_row, ws.best_row, ws.elite, ws.valid,
-                                            ws.n_elite);
+    validity_kernel<<<(unsigned)((r + 255) / 256), 256, 0, s>>>(ws.first_row, r, ws.valid);
+    launch_compact(r, ElitePred{ws.first_row}, EliteVal{ws.apd, ws.first_row, ws.best_row}, ws.tile_scratch, r, ws.elite,
+                   ws.n_elite, s);
     TEMO_CUDA(cudaGetLastError());
 }
 

@@ -425,3 +425,18 @@ def test_fused_and_unfused_evaluation_agree_bitwise(tb):
                 run.step()
             runs.append(run.download())
     assert np.array_equal(runs[0]["x"], runs[1]["x"]) and np.array_equal(runs[0]["f"], runs[1]["f"])
+
+
+def test_reference_suites_through_the_cpp_shim(tb):
+    """oracle/_ref/shim_parity = the reference's own verify.hpp suites compiled against the UNMODIFIED
+    reference headers with temo::b200:: (include/temo_b200.hpp -> C ABI) in place of the batched CPU calls."""
+    import os
+    import subprocess
+    from conftest import ROOT
+    exe = os.path.join(ROOT, "oracle", "_ref", "shim_parity")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/shim_parity not built (reference not mounted at build time)")
+    res = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    print(res.stdout)
+    assert res.returncode == 0, res.stdout + res.stderr
+    assert "SHIM PARITY OK" in res.stdout
