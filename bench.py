@@ -179,7 +179,10 @@ def run_reference_arm(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
+    if world > 1:  # weak scaling: the N-GPU arm runs N shards of --pop rows = one population of N * pop rows
+        args.pop = args.pop * world
     base = cpu_reference_sample(args, args.steps, args.warmup)
+    base["value"] *= world  # unit: generations of one pop-row shard per second (see dist.bench_main)
     line = {
         "impl": "reference", "metric": METRIC, "value": base["value"], "unit": "generations/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": base["scaled_ms_per_gen"],

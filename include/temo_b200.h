@@ -197,6 +197,38 @@ int temo_b200_dev_sync(void);
  * returns the mean ms per launch. stage: 1 reproduction (ga, unfused), 2 evaluation,
  * 3 reproduction with fused evaluation, 4 selection, 5 gamma. Used for the roofline. */
 int temo_b200_run_time_stage(temo_b200_run* run, int stage, int reps, double* mean_ms);
+/* ---- sharded generation loop: stage-level entry points of ONE rank (one process per GPU). The host
+ * orchestration (paper_2404_01159_b200/dist.py) puts torch.distributed collectives between them:
+ * all-to-all of parent rows, all-gather of offspring objectives / free slots, min-allreduces of the
+ * per-vector (APD key, row) minima. reference: rvea_run, algorithms.hpp:227-296. */
+typedef struct temo_b200_shard temo_b200_shard; /* opaque */
+const char* temo_b200_shard_last_error(void);
+/* Pure host code (no GPU needed): the exchange plan of one generation for `rank` from the replicated
+ * survivor tables: local slots to send (grouped by destination, in the destination's mating-row order),
+ * per-peer row counts, the receive-buffer row of every local mating row, and the generation's draw
+ * counters {c_sbx, c_pm, counter after the generation}. */
+int temo_b200_shard_plan(uint64_t seed, uint64_t counter, uint64_t P, uint64_t n, uint64_t d, int rank, int world,
+                         const int32_t* surv_owner, const uint32_t* surv_slot, uint32_t* send_slots,
+                         uint64_t send_slots_cap, uint64_t* send_counts, uint64_t* recv_counts,
+                         uint32_t* recv_pos, uint64_t* counters3);
+int temo_b200_shard_create(const temo_b200_run_config* cfg, int rank, int world, temo_b200_shard** out);
+int temo_b200_shard_destroy(temo_b200_shard* s);
+/* info8: n_loc, d, m, r, send_cap, pcap, cap_loc, adapt_every */
+int temo_b200_shard_info(temo_b200_shard* s, uint64_t* info8);
+/* device buffers the collectives operate on: 0 send_buf, 1 recv_buf, 2 f_off_loc, 3 f_gather,
+ * 4 best_key (int64 view), 5 first_row (int32 view), 6 best_row (int32 view), 7 free_slot (int32 view) */
+void* temo_b200_shard_buffer(temo_b200_shard* s, int which);
+int temo_b200_shard_pack(temo_b200_shard* s, const uint32_t* slots, uint64_t count);
+int temo_b200_shard_reproduce(temo_b200_shard* s, const uint32_t* recv_pos, uint64_t c_sbx, uint64_t c_pm);
+int temo_b200_shard_place_f(temo_b200_shard* s, uint64_t P, int initial);
+int temo_b200_shard_select_local(temo_b200_shard* s, uint64_t P, uint64_t lo, uint64_t hi, uint64_t t);
+int temo_b200_shard_select_rows(temo_b200_shard* s, uint64_t lo, uint64_t hi);
+int temo_b200_shard_select_finish(temo_b200_shard* s, uint32_t* elite, uint64_t* count);
+int temo_b200_shard_commit(temo_b200_shard* s, uint64_t count, const uint32_t* own_slots, uint64_t own_count,
+                           uint64_t t);
+int temo_b200_shard_download(temo_b200_shard* s, const uint32_t* slots, uint64_t rows, double* x, uint64_t f_rows,
+                             double* f, double* v, double* gamma);
+
 /* Self-test hook for the libm-exact pow used by SBX / polynomial mutation / DTLZ4
  * (reference call sites: operators.hpp:85-86,115-118; problems.hpp:79): out[e] = pow(x[e], y[e])
  * evaluated by the device kernel (on_device = 1) or by its host twin (on_device = 0, no GPU

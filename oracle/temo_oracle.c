@@ -173,6 +173,46 @@ int to_ga_reproduce(const double* x, uint64_t n, uint64_t d, uint64_t seed, uint
     return 0;
 }
 
+/* Children of the mating pairs [unit0, unit0 + h_loc) of a GLOBAL shuffled population of n_g rows, the two
+ * mates of every pair given explicitly (pa, pb: h_loc x d). Same arithmetic and the same draws as to_sbx followed by
+ * to_polynomial_mutation for those rows (draw blocks addressed globally: SBX blocks are n_g/2 x d, PM blocks n_g x d),
+ * i.e. what one shard of the multi-GPU run must produce. Used only by the sharded-orchestration tests. */
+void to_reproduce_pairs(const double* pa, const double* pb, uint64_t h_loc, uint64_t d, uint64_t unit0, uint64_t n_g,
+                        uint64_t seed, uint64_t c_sbx, uint64_t c_pm, const double* ga, const double* lower,
+                        const double* upper, double* ca, double* cb) {
+    const uint64_t half = n_g / 2;
+    const uint64_t c_mc = c_sbx, c_r1 = c_mc + half * d, c_r2 = c_r1 + half * d, c_r3 = c_r2 + half * d;
+    const uint64_t c_mask = c_pm, c_mut = c_pm + n_g * d;
+    const double pc = ga[0], inv_exp = 1.0 / (ga[1] + 1.0), rate = ga[2] / (double)d, xi = ga[3];
+    for (uint64_t p = 0; p < h_loc; ++p) {
+        const uint64_t pg = unit0 + p;
+        const double hc = to_step(to_value_at(seed, c_r3 + pg) - pc);
+        for (uint64_t j = 0; j < d; ++j) {
+            const uint64_t e = pg * d + j;
+            const double mc = to_value_at(seed, c_mc + e);
+            const double low = pow(2.0 * mc, inv_exp), high = pow(2.0 - 2.0 * mc, -inv_exp);
+            const double hm = to_step(0.5 - mc);
+            double beta = to_sign(to_value_at(seed, c_r1 + e) - 0.5) * (hm * low + (1.0 - hm) * high);
+            const double hr = to_step(to_value_at(seed, c_r2 + e) - 0.5);
+            beta = (1.0 - hc) * ((1.0 - hr) * beta + hr) + hc;
+            const double xa = pa[p * d + j], xb = pb[p * d + j];
+            double child[2];
+            child[0] = to_clip(((1.0 + beta) * xa + (1.0 - beta) * xb) / 2.0, lower[j], upper[j]);
+            child[1] = to_clip(((1.0 - beta) * xa + (1.0 + beta) * xb) / 2.0, lower[j], upper[j]);
+            for (int w = 0; w < 2; ++w) {
+                const uint64_t row = w == 0 ? pg : half + pg;
+                const uint64_t em = row * d + j;
+                double xv = child[w];
+                if (!(to_step(rate - to_value_at(seed, c_mask + em)) == 0.0 || upper[j] - lower[j] <= 0.0)) {
+                    const double delta = to_polynomial_delta(to_value_at(seed, c_mut + em), xv, lower[j], upper[j], xi);
+                    xv = to_clip(xv + delta, lower[j], upper[j]);
+                }
+                (w == 0 ? ca : cb)[p * d + j] = xv;
+            }
+        }
+    }
+}
+
 /* operators.hpp:287-296. */
 void to_random_reproduce(uint64_t n, uint64_t d, uint64_t seed, uint64_t* counter,
                          const double* lower, const double* upper, double* out) {

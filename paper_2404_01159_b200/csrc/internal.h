@@ -56,6 +56,9 @@ struct ReproArgs {
     double* f_out = nullptr;
     uint64_t f_row0 = 0;
     const uint32_t* f_row0_dev = nullptr;  // optional device-side row offset (survivor count)
+    // sharded runs: this launch covers pairs [global_unit0, global_unit0 + n/2) of a global population of
+    // global_n rows (0 = not sharded); draw counters are addressed globally, storage rows locally
+    uint64_t global_n = 0, global_unit0 = 0;
 };
 void launch_reproduce(const ReproArgs& a, cudaStream_t s);
 
@@ -109,6 +112,12 @@ void launch_select(const double* f, uint64_t n_rows, const uint32_t* n_rows_dev,
                    const double* v, const double* gamma, uint64_t r, double penalty,
                    SelectWorkspace& ws, cudaStream_t s, VecIndex* index = nullptr);
 void launch_row_norms(const double* v, uint64_t r, uint64_t m, double* vn, cudaStream_t s);
+// the stages of launch_select, separately (the sharded run puts collectives between them)
+void launch_select_prepare(const double* f, uint64_t n_rows, uint64_t m, const double* gamma, uint64_t r,
+                           SelectWorkspace& ws, cudaStream_t s);
+void launch_elite_rows(uint64_t n_rows, const uint32_t* assoc, const double* apd, const unsigned long long* best_key,
+                       uint32_t* best_row, uint32_t row0, cudaStream_t s);
+void launch_select_finish(uint64_t r, SelectWorkspace& ws, bool nan_rule, cudaStream_t s);
 
 // ---- K4: reference vectors ----------------------------------------------------------------------
 // gamma_i = acos(max_{j != i} cos(v_i, v_j)) (refvec.hpp:81-100); err_flag bit0 set if any <= 0.

@@ -31,6 +31,7 @@ struct ReproK {
     double* out;
     const uint32_t* dst;
     uint64_t n, d, half;
+    uint64_t g_unit0, g_half, g_n;  // position of this launch inside the global draw blocks (sharded runs)
     Rng rng;
     uint64_t c_mc, c_r1, c_r2, c_r3, c_mask, c_mut;
     double pc, inv_exp, xi;
@@ -108,15 +109,19 @@ __global__ void __launch_bounds__(256, 3) reproduce_kernel(const ReproK a) {
     }
 
     // draw streams of this CTA's rows: SBX blocks are half x d, PM blocks n x d
-    const RowStream<MODE> st_mc(a.rng, a.c_mc + unit * a.d), st_r1(a.rng, a.c_r1 + unit * a.d),
-        st_r2(a.rng, a.c_r2 + unit * a.d);
-    const RowStream<MODE> st_mask_a(a.rng, a.c_mask + row_a * a.d), st_mut_a(a.rng, a.c_mut + row_a * a.d);
-    const RowStream<MODE> st_mask_b(a.rng, a.c_mask + row_b * a.d), st_mut_b(a.rng, a.c_mut + row_b * a.d);
+    // (global numbering: a shard of a multi-GPU run draws exactly what the single-GPU run draws for its rows)
+    const uint64_t g_unit = a.g_unit0 + unit;
+    const uint64_t g_row_a = SBX ? (paired ? g_unit : a.g_n - 1) : g_unit;
+    const uint64_t g_row_b = a.g_half + g_unit;
+    const RowStream<MODE> st_mc(a.rng, a.c_mc + g_unit * a.d), st_r1(a.rng, a.c_r1 + g_unit * a.d),
+        st_r2(a.rng, a.c_r2 + g_unit * a.d);
+    const RowStream<MODE> st_mask_a(a.rng, a.c_mask + g_row_a * a.d), st_mut_a(a.rng, a.c_mut + g_row_a * a.d);
+    const RowStream<MODE> st_mask_b(a.rng, a.c_mask + g_row_b * a.d), st_mut_b(a.rng, a.c_mut + g_row_b * a.d);
 
     // pair-level crossover switch: hc = H(r3 - pc) (operators.hpp:82)
     bool pair_cross = false;
     if (paired) {
-        const double r3 = word_to_unit(draw_word<MODE>(a.rng, a.c_r3 + unit));
+        const double r3 = word_to_unit(draw_word<MODE>(a.rng, a.c_r3 + g_unit));
         pair_cross = !(r3 - a.pc >= 0.0);
     }
 
@@ -329,14 +334,18 @@ void launch_reproduce(const ReproArgs& a, cudaStream_t s) {
     k.n = a.n;
     k.d = a.d;
     k.half = a.n / 2;
+    k.g_n = a.global_n ? a.global_n : a.n;
+    k.g_half = k.g_n / 2;
+    k.g_unit0 = a.global_unit0;
+    if (a.global_n) require(a.n % 2 == 0 && a.global_n % 2 == 0, "reproduce: sharded launches need an even row count");
     k.rng = a.rng;
-    const uint64_t hd = k.half * a.d;
+    const uint64_t hd = k.g_half * a.d;
     k.c_mc = a.c_sbx;
     k.c_r1 = a.c_sbx + hd;
     k.c_r2 = a.c_sbx + 2 * hd;
     k.c_r3 = a.c_sbx + 3 * hd;
     k.c_mask = a.c_pm;
-    k.c_mut = a.c_pm + a.n * a.d;
+    k.c_mut = a.c_pm + k.g_n * a.d;
     k.pc = a.ga.pc;
     k.inv_exp = 1.0 / (a.ga.eta + 1.0);  // operators.hpp:75
     k.xi = a.ga.xi;

@@ -160,20 +160,24 @@ __global__ void __launch_bounds__(kAssocThreads) assoc_kernel(
 // lowest row among those that attain the minimal APD of their vector
 __global__ void elite_rows_kernel(uint64_t n_rows, const uint32_t* n_rows_dev, const uint32_t* assoc,
                                   const double* apd, const unsigned long long* best_key,
-                                  uint32_t* best_row) {
+                                  uint32_t* best_row, uint32_t row0) {
     const uint64_t n = n_rows_dev ? (uint64_t)*n_rows_dev : n_rows;
     const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
     const double a = apd[i];
     const unsigned long long key = (a != a) ? kKeyMax : order_key(a);
     const uint32_t j = assoc[i];
-    if (key == best_key[j]) atomicMin(&best_row[j], (uint32_t)i);
+    if (key == best_key[j]) atomicMin(&best_row[j], row0 + (uint32_t)i);
 }
 
 // validity + the elite of every valid vector (selection.hpp:209-217); compaction in ascending j follows
 struct ElitePred {
     const uint32_t* first_row;
     __device__ bool operator()(uint64_t j) const { return first_row[j] != 0xffffffffu; }
+};
+struct EliteValPlain {  // sharded runs: objectives are finite, the NaN rule cannot trigger
+    const uint32_t* best_row;
+    __device__ uint32_t operator()(uint64_t j) const { return best_row[j]; }
 };
 struct EliteVal {
     const double* apd;
@@ -257,35 +261,55 @@ void launch_col_minmax(const double* f, uint64_t n_rows, const uint32_t* n_rows_
     TEMO_CUDA(cudaGetLastError());
 }
 
-void launch_select(const double* f, uint64_t n_rows, const uint32_t* n_rows_dev, uint64_t m,
-                   const double* v, const double* gamma, uint64_t r, double penalty,
-                   SelectWorkspace& ws, cudaStream_t s, VecIndex* index) {
+void launch_select_prepare(const double* f, uint64_t n_rows, uint64_t m, const double* gamma, uint64_t r,
+                           SelectWorkspace& ws, cudaStream_t s) {
     require(n_rows >= 1, "translate: empty objective tensor");
     require(m >= 1 && m <= (uint64_t)kMaxObj, "rv_select: unsupported objective count");
     require(n_rows <= ws.rows_cap && r <= ws.r, "rv_select: workspace too small");
     require(n_rows < 0xffffffffULL && r < 0xffffffffULL, "rv_select: index range");
     gamma_check_kernel<<<(unsigned)((r + 255) / 256), 256, 0, s>>>(gamma, r, ws.err_flag);
-    launch_col_minmax(f, n_rows, n_rows_dev, m, ws.z, nullptr, ws.zkey, s);
+    launch_col_minmax(f, n_rows, nullptr, m, ws.z, nullptr, ws.zkey, s);
     TEMO_CUDA(cudaMemsetAsync(ws.best_key, 0xff, r * sizeof(unsigned long long), s));
     TEMO_CUDA(cudaMemsetAsync(ws.best_row, 0xff, r * sizeof(uint32_t), s));
     TEMO_CUDA(cudaMemsetAsync(ws.first_row, 0xff, r * sizeof(uint32_t), s));
-    if (index && index->built) {
-        launch_assoc_indexed(f, n_rows, n_rows_dev, m, ws.z, *index, gamma, penalty, ws.assoc, ws.theta, ws.apd,
-                             ws.best_key, ws.first_row, s);
-    } else
-    switch (m) {
-    case 2: launch_assoc<2>(f, n_rows, n_rows_dev, m, v, gamma, r, penalty, ws, s); break;
-    case 3: launch_assoc<3>(f, n_rows, n_rows_dev, m, v, gamma, r, penalty, ws, s); break;
-    case 4: launch_assoc<4>(f, n_rows, n_rows_dev, m, v, gamma, r, penalty, ws, s); break;
-    case 5: launch_assoc<5>(f, n_rows, n_rows_dev, m, v, gamma, r, penalty, ws, s); break;
-    case 10: launch_assoc<10>(f, n_rows, n_rows_dev, m, v, gamma, r, penalty, ws, s); break;
-    default: launch_assoc<0>(f, n_rows, n_rows_dev, m, v, gamma, r, penalty, ws, s); break;
-    }
-    elite_rows_kernel<<<(unsigned)((n_rows + 255) / 256), 256, 0, s>>>(n_rows, n_rows_dev, ws.assoc, ws.apd,
-                                                                     ws.best_key, ws.best_row);
+}
+
+void launch_elite_rows(uint64_t n_rows, const uint32_t* assoc, const double* apd, const unsigned long long* best_key,
+                       uint32_t* best_row, uint32_t row0, cudaStream_t s) {
+    elite_rows_kernel<<<(unsigned)((n_rows + 255) / 256), 256, 0, s>>>(n_rows, nullptr, assoc, apd, best_key, best_row, row0);
+    TEMO_CUDA(cudaGetLastError());
+}
+
+void launch_select_finish(uint64_t r, SelectWorkspace& ws, bool nan_rule, cudaStream_t s) {
     validity_kernel<<<(unsigned)((r + 255) / 256), 256, 0, s>>>(ws.first_row, r, ws.valid);
-    launch_compact(r, ElitePred{ws.first_row}, EliteVal{ws.apd, ws.first_row, ws.best_row}, ws.tile_scratch, r, ws.elite,
-                   ws.n_elite, s);
+    if (nan_rule)
+        launch_compact(r, ElitePred{ws.first_row}, EliteVal{ws.apd, ws.first_row, ws.best_row}, ws.tile_scratch, r, ws.elite,
+                       ws.n_elite, s);
+    else
+        launch_compact(r, ElitePred{ws.first_row}, EliteValPlain{ws.best_row}, ws.tile_scratch, r, ws.elite, ws.n_elite, s);
+    TEMO_CUDA(cudaGetLastError());
+}
+
+void launch_select(const double* f, uint64_t n_rows, const uint32_t* n_rows_dev, uint64_t m,
+                   const double* v, const double* gamma, uint64_t r, double penalty,
+                   SelectWorkspace& ws, cudaStream_t s, VecIndex* index) {
+    require(n_rows_dev == nullptr, "rv_select: device-side row counts are not supported here");
+    launch_select_prepare(f, n_rows, m, gamma, r, ws, s);
+    if (index && index->built) {
+        launch_assoc_indexed(f, n_rows, nullptr, m, ws.z, *index, gamma, penalty, ws.assoc, ws.theta, ws.apd,
+                             ws.best_key, ws.first_row, s);
+    } else {
+        switch (m) {
+        case 2: launch_assoc<2>(f, n_rows, nullptr, m, v, gamma, r, penalty, ws, s); break;
+        case 3: launch_assoc<3>(f, n_rows, nullptr, m, v, gamma, r, penalty, ws, s); break;
+        case 4: launch_assoc<4>(f, n_rows, nullptr, m, v, gamma, r, penalty, ws, s); break;
+        case 5: launch_assoc<5>(f, n_rows, nullptr, m, v, gamma, r, penalty, ws, s); break;
+        case 10: launch_assoc<10>(f, n_rows, nullptr, m, v, gamma, r, penalty, ws, s); break;
+        default: launch_assoc<0>(f, n_rows, nullptr, m, v, gamma, r, penalty, ws, s); break;
+        }
+    }
+    launch_elite_rows(n_rows, ws.assoc, ws.apd, ws.best_key, ws.best_row, 0, s);
+    launch_select_finish(r, ws, /*nan_rule=*/true, s);
     TEMO_CUDA(cudaGetLastError());
 }
 

@@ -238,7 +238,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) assoc_indexed_kernel(
     const double* __restrict__ f, uint64_t n_rows, const uint32_t* n_rows_dev, uint64_t m_rt,
     const double* __restrict__ z, const IndexView ix, const uint32_t* __restrict__ vflags, const double* __restrict__ gamma,
     double penalty, uint32_t* __restrict__ assoc, double* __restrict__ theta_out, double* __restrict__ apd_out,
-    unsigned long long* __restrict__ best_key, uint32_t* __restrict__ first_row) {
+    unsigned long long* __restrict__ best_key, uint32_t* __restrict__ first_row, uint32_t row0) {
     constexpr int MM = M > 0 ? M : kMaxObj;
     const int m = M > 0 ? M : (int)m_rt;
     const uint64_t n = n_rows_dev ? (uint64_t)*n_rows_dev : n_rows;
@@ -277,7 +277,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) assoc_indexed_kernel(
     apd_out[i] = apd;
     const unsigned long long key = (apd != apd) ? kKeyMax : order_key(apd);
     atomicMin(&best_key[arg], key);
-    atomicMin(&first_row[arg], (uint32_t)i);
+    atomicMin(&first_row[arg], row0 + (uint32_t)i);  // row0: merged-row number of this launch's first row
 }
 
 // gamma_i = acos(max_{j != i} cos(v_i, v_j)) (refvec.hpp:81-100), one warp per vector.
@@ -419,13 +419,13 @@ void VecIndex::build(const double* v, const double* vn, cudaStream_t s) {
 
 void launch_assoc_indexed(const double* f, uint64_t n_rows, const uint32_t* n_rows_dev, uint64_t m, const double* z,
                           VecIndex& index, const double* gamma, double penalty, uint32_t* assoc, double* theta,
-                          double* apd, unsigned long long* best_key, uint32_t* first_row, cudaStream_t s) {
+                          double* apd, unsigned long long* best_key, uint32_t* first_row, cudaStream_t s, uint32_t row0) {
     require(index.built, "VecIndex: not built");
     const IndexView view = view_of(index);
     const unsigned grid = (unsigned)((n_rows + kWarpsPerCta - 1) / kWarpsPerCta);
 #define CALL(MV) \
     assoc_indexed_kernel<MV><<<grid, kWarpsPerCta * 32, 0, s>>>(f, n_rows, n_rows_dev, m, z, view, index.flags, gamma, penalty, \
-                                                               assoc, theta, apd, best_key, first_row)
+                                                               assoc, theta, apd, best_key, first_row, row0)
     TEMO_DISPATCH_M(m, CALL)
 #undef CALL
     TEMO_CUDA(cudaGetLastError());

@@ -29,7 +29,8 @@ std::vector<uint32_t> morton_order(const double* v, uint64_t r, uint64_t m);
 
 void launch_assoc_indexed(const double* f, uint64_t n_rows, const uint32_t* n_rows_dev, uint64_t m, const double* z,
                           VecIndex& index, const double* gamma, double penalty, uint32_t* assoc, double* theta,
-                          double* apd, unsigned long long* best_key, uint32_t* first_row, cudaStream_t s);
+                          double* apd, unsigned long long* best_key, uint32_t* first_row, cudaStream_t s,
+                          uint32_t row0 = 0);
 void launch_gamma_indexed(const double* v, const double* vn, uint64_t r, uint64_t m, VecIndex& index, double* gamma,
                           uint32_t* err_flag, const uint32_t* skip_flag, cudaStream_t s);
 

@@ -440,3 +440,30 @@ def test_reference_suites_through_the_cpp_shim(tb):
     print(res.stdout)
     assert res.returncode == 0, res.stdout + res.stderr
     assert "SHIM PARITY OK" in res.stdout
+
+
+@pytest.mark.parametrize("case", [("dtlz2", 512, 300, 3, 12), ("dtlz1", 256, 64, 3, 10), ("lsmop1", 128, 200, 3, 6)])
+def test_sharded_stage_path_equals_single_gpu_run(tb, case):
+    """The multi-GPU stage functions (GpuShard, C ABI temo_b200_shard_*) driven by the same orchestration as on
+    N GPUs, here with world size 1: must equal the monolithic device-resident run bit for bit (X, F, V, gamma,
+    survivor sets, draw counter). Together with tests/test_dist_cpu.py (world size 2, collectives over gloo)
+    this covers the N>1 path without N GPUs."""
+    from paper_2404_01159_b200.dist import GpuShard, LocalComm, ShardedRvea
+    problem, n, d, m, gens = case
+    cfg = tb.RunConfig(problem=problem, pop=n, dim=d, obj=m, generations=gens, seed=21)
+    shard = GpuShard(cfg, 0, 1)
+    try:
+        sharded = ShardedRvea(cfg, LocalComm(), shard)
+        with tb.RveaRun(cfg) as run:
+            for t in range(gens):
+                assert sharded.step() == run.step(), t
+                assert np.array_equal(sharded.last_elite, run.last_generation()["elite"]), t
+                assert sharded.counter == run.state()["counter"]
+            mono = run.download()
+        idx, slots = sharded.own_slots()
+        x, f, v, gamma = shard.download(slots, sharded.P)
+        assert np.array_equal(idx, np.arange(sharded.P))
+        assert np.array_equal(x, mono["x"]) and np.array_equal(f, mono["f"])
+        assert np.array_equal(v, mono["v"]) and np.array_equal(gamma, mono["gamma"])
+    finally:
+        shard.close()
