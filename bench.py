@@ -210,7 +210,7 @@ def run_ours(args):
     rank, world, local = dist_env()
     import paper_2404_01159_b200 as tb
 
-    if world > 1:
+    if world > 1 or os.environ.get("TEMO_FORCE_DIST") == "1":  # the env switch exercises the N-GPU path on one GPU
         from paper_2404_01159_b200 import dist as tdist
         return tdist.bench_main(args, METRIC, workload_config, measured_peaks, ClockSampler)
 

@@ -43,6 +43,20 @@ __host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
     return z ^ (z >> 31);
 }
 
+// High 32 bits of mix64(z) before the final xor-shift. Enough for every test that only looks at the top
+// bits of the word — w = y ^ (y >> 31) leaves the top 31 bits of y untouched — and one multiply-add
+// shorter than the full mix: the sign tests H(r - 0.5) (bit 63) and the quick reject of the mutation mask.
+__host__ __device__ __forceinline__ uint32_t mix64_top32(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z ^= z >> 27;
+    const uint32_t lo = (uint32_t)z, hi = (uint32_t)(z >> 32);
+#ifdef __CUDA_ARCH__
+    return __umulhi(lo, 0x133111ebu) + lo * 0x94d049bbu + hi * 0x133111ebu;
+#else
+    return (uint32_t)((z * 0x94d049bb133111ebULL) >> 32);
+#endif
+}
+
 // Philox4x32-10 (Salmon et al. 2011), counter = (k >> 1, stream tag), key = seed; one call
 // yields two 64-bit words, word (k & 1) is draw k. Not in the reference: parity unpinned.
 __host__ __device__ __forceinline__ uint64_t philox_word(uint64_t seed, uint64_t k) {

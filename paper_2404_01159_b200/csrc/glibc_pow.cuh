@@ -35,6 +35,23 @@ struct PowTables {
     const unsigned long long* exptab;  // [256] {tail, scale bits}
 };
 
+// The 17 scalar constants as one table: on the device it lives in constant memory, which lets the FP64
+// instructions take them as c[bank][offset] operands (no register / uniform-register traffic).
+#define TEMO_POW_SCALARS_INIT {TEMO_POW_LN2HI, TEMO_POW_LN2LO, TEMO_POW_A0, TEMO_POW_A1, TEMO_POW_A2, TEMO_POW_A3, \
+                               TEMO_POW_A4, TEMO_POW_A5, TEMO_POW_A6, TEMO_POW_INVLN2N, TEMO_POW_SHIFT,           \
+                               TEMO_POW_NEGLN2HIN, TEMO_POW_NEGLN2LON, TEMO_POW_C2, TEMO_POW_C3, TEMO_POW_C4,     \
+                               TEMO_POW_C5}
+#ifdef __CUDACC__
+static __constant__ unsigned long long d_pow_scalars[17] = TEMO_POW_SCALARS_INIT;
+#endif
+static const unsigned long long h_pow_scalars[17] = TEMO_POW_SCALARS_INIT;
+
+#ifdef __CUDA_ARCH__
+#define TEMO_POW_K(i) __longlong_as_double((long long)d_pow_scalars[i])
+#else
+#define TEMO_POW_K(i) temo_as_double_host(h_pow_scalars[i])
+#endif
+
 #ifdef __CUDA_ARCH__
 #define TEMO_FMA(a, b, c) __fma_rn((a), (b), (c))
 #define TEMO_MUL(a, b) __dmul_rn((a), (b))
@@ -83,10 +100,9 @@ __host__ __device__ inline bool glibc_pow_main(double x, double y, const PowTabl
     const int k = (int)((long long)tmp >> 52);
     const double z = TEMO_AS_DOUBLE(ix - (tmp & 0xfff0000000000000ULL));
     const double kd = (double)k;
-    const double ln2hi = TEMO_AS_DOUBLE(TEMO_POW_LN2HI), ln2lo = TEMO_AS_DOUBLE(TEMO_POW_LN2LO);
-    const double A0 = TEMO_AS_DOUBLE(TEMO_POW_A0), A1 = TEMO_AS_DOUBLE(TEMO_POW_A1), A2 = TEMO_AS_DOUBLE(TEMO_POW_A2),
-                 A3 = TEMO_AS_DOUBLE(TEMO_POW_A3), A4 = TEMO_AS_DOUBLE(TEMO_POW_A4), A5 = TEMO_AS_DOUBLE(TEMO_POW_A5),
-                 A6 = TEMO_AS_DOUBLE(TEMO_POW_A6);
+    const double ln2hi = TEMO_POW_K(0), ln2lo = TEMO_POW_K(1);
+    const double A0 = TEMO_POW_K(2), A1 = TEMO_POW_K(3), A2 = TEMO_POW_K(4), A3 = TEMO_POW_K(5), A4 = TEMO_POW_K(6),
+                 A5 = TEMO_POW_K(7), A6 = TEMO_POW_K(8);
     const double t1 = TEMO_FMA(kd, ln2hi, T.logc[i]);
     const double lo1 = TEMO_FMA(kd, ln2lo, T.logctail[i]);
     const double r = TEMO_FMA(z, T.invc[i], -1.0);
@@ -128,10 +144,9 @@ __host__ __device__ inline bool glibc_pow_main(double x, double y, const PowTabl
         }
         special = true;  // 512 <= |y log x| < 1024: the scale may leave the normal range
     }
-    const double invln2N = TEMO_AS_DOUBLE(TEMO_POW_INVLN2N), shift = TEMO_AS_DOUBLE(TEMO_POW_SHIFT),
-                 negln2hiN = TEMO_AS_DOUBLE(TEMO_POW_NEGLN2HIN), negln2loN = TEMO_AS_DOUBLE(TEMO_POW_NEGLN2LON),
-                 C2 = TEMO_AS_DOUBLE(TEMO_POW_C2), C3 = TEMO_AS_DOUBLE(TEMO_POW_C3), C4 = TEMO_AS_DOUBLE(TEMO_POW_C4),
-                 C5 = TEMO_AS_DOUBLE(TEMO_POW_C5);
+    const double invln2N = TEMO_POW_K(9), shift = TEMO_POW_K(10), negln2hiN = TEMO_POW_K(11),
+                 negln2loN = TEMO_POW_K(12), C2 = TEMO_POW_K(13), C3 = TEMO_POW_K(14), C4 = TEMO_POW_K(15),
+                 C5 = TEMO_POW_K(16);
     const double kds = TEMO_FMA(ehi, invln2N, shift);
     const unsigned long long ki = TEMO_AS_U64(kds);
     const double kdd = TEMO_ADD(kds, -shift);

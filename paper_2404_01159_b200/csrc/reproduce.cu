@@ -36,6 +36,7 @@ struct ReproK {
     uint64_t c_mc, c_r1, c_r2, c_r3, c_mask, c_mut;
     double pc, inv_exp, xi;
     uint64_t mask_thresh;  // mutate iff (word >> 11) <= mask_thresh
+    uint32_t mask_top;     // = mask_thresh >> 32: necessary condition on the top 21 bits
     int mask_never;
     int narrow_pow;  // 1/(eta+1) in [2^-10, 1]: the SBX pow stays on the common path of the libm algorithm
     const double* lower;
@@ -75,10 +76,18 @@ struct RowStream {
         if (MODE == 0) return mix64(a + (uint64_t)j * kGolden);
         return philox_word(seed, a + j);
     }
+    // top 31 bits of word(j) (bit 0 of the result is not meaningful)
+    __device__ __forceinline__ uint32_t top(uint32_t j) const {
+        if (MODE == 0) return mix64_top32(a + (uint64_t)j * kGolden);
+        return (uint32_t)(philox_word(seed, a + j) >> 32);
+    }
 };
 
+#ifndef TEMO_REPRO_MIN_BLOCKS
+#define TEMO_REPRO_MIN_BLOCKS 4
+#endif
 template <int MODE, bool SBX, bool PM, int EVAL, int VEC>
-__global__ void __launch_bounds__(256, 3) reproduce_kernel(const ReproK a) {
+__global__ void __launch_bounds__(256, TEMO_REPRO_MIN_BLOCKS) reproduce_kernel(const ReproK a) {
     __shared__ double s_red[8];
     __shared__ double s_pos[2][kMaxObj];
     __shared__ PowSmem s_pow;
@@ -160,7 +169,7 @@ __global__ void __launch_bounds__(256, 3) reproduce_kernel(const ReproK a) {
         if (SBX && paired && pair_cross) {  // CTA-uniform
             // hr = H(r2 - 0.5): the top bit of the word; a gene crosses iff it is clear (operators.hpp:90-91)
 #pragma unroll
-            for (int v = 0; v < VEC; ++v) crosses[v] = in_range && (st_r2.word(j0 + v) >> 63) == 0;
+            for (int v = 0; v < VEC; ++v) crosses[v] = in_range && (st_r2.top(j0 + v) >> 31) == 0;
             // The spread factor (two draws + one pow) is needed by ~half of the genes only: compact the
             // crossing genes of the warp so that the expensive part runs with full lanes.
             const unsigned b0 = __ballot_sync(0xffffffffu, crosses[0]);
@@ -175,7 +184,7 @@ __global__ void __launch_bounds__(256, 3) reproduce_kernel(const ReproK a) {
                 const int code = s_list[warp][t];
                 const uint32_t j = (q_warp + (code >> 1)) * VEC + (code & 1);
                 const double mc = word_to_unit(st_mc.word(j));
-                const bool up = (st_r1.word(j) >> 63) != 0;  // sgn(r1 - 0.5)
+                const bool up = (st_r1.top(j) >> 31) != 0;  // sgn(r1 - 0.5)
                 // live spread branch only (hm = H(0.5 - mc)); the other one is multiplied by exactly 0.0
                 const bool low = 0.5 - mc >= 0.0;
                 const double base = low ? 2.0 * mc : 2.0 - 2.0 * mc;
@@ -197,21 +206,20 @@ __global__ void __launch_bounds__(256, 3) reproduce_kernel(const ReproK a) {
             const double lo = a.lower[j], hi = a.upper[j];
             double ca = xa[v], cb = xb[v];
             if (SBX && paired) {
-                if (crosses[v]) {
-                    const double b = beta[v];
-                    ca = ((1.0 + b) * xa[v] + (1.0 - b) * xb[v]) / 2.0;  // operators.hpp:94-95
-                    cb = ((1.0 - b) * xa[v] + (1.0 + b) * xb[v]) / 2.0;
-                }
-                ca = clampd(ca, lo, hi);
-                cb = clampd(cb, lo, hi);
+                // operators.hpp:92-95 as written: a gene that does not cross has beta = 1 exactly (hr = 1 or hc = 1),
+                // and the blend then returns the parents through the same arithmetic as on the CPU
+                const double b = beta[v];
+                ca = clampd(((1.0 + b) * xa[v] + (1.0 - b) * xb[v]) / 2.0, lo, hi);
+                cb = clampd(((1.0 - b) * xa[v] + (1.0 + b) * xb[v]) / 2.0, lo, hi);
             }
             if (PM && !a.mask_never) {
                 const bool live = !(hi - lo <= 0.0);
-                if (live && (st_mask_a.word(j) >> 11) <= a.mask_thresh) {
+                // (word >> 11) <= T  can only hold if the top 21 bits do not exceed T's: decided from the top word
+                if (live && (st_mask_a.top(j) >> 11) <= a.mask_top && (st_mask_a.word(j) >> 11) <= a.mask_thresh) {
                     const double u = word_to_unit(st_mut_a.word(j));
                     ca = clampd(ca + polynomial_delta_dev(u, ca, lo, hi, a.xi, &s_pow), lo, hi);
                 }
-                if (paired && live && (st_mask_b.word(j) >> 11) <= a.mask_thresh) {
+                if (paired && live && (st_mask_b.top(j) >> 11) <= a.mask_top && (st_mask_b.word(j) >> 11) <= a.mask_thresh) {
                     const double u = word_to_unit(st_mut_b.word(j));
                     cb = clampd(cb + polynomial_delta_dev(u, cb, lo, hi, a.xi, &s_pow), lo, hi);
                 }
@@ -356,6 +364,7 @@ void launch_reproduce(const ReproArgs& a, cudaStream_t s) {
     if (!k.mask_never) {
         const double scaled = rate * 0x1.0p53;
         k.mask_thresh = scaled >= 0x1.0p53 ? ((1ULL << 53) - 1) : (uint64_t)scaled;
+        k.mask_top = (uint32_t)(k.mask_thresh >> 32);
     }
     k.lower = a.lower;
     k.upper = a.upper;
