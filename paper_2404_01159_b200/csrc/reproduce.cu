@@ -47,10 +47,10 @@ struct ReproK {
     const uint32_t* f_row0_dev;
 };
 
-// polynomial_delta (operators.hpp:106-121): both branches evaluated, blended by steps.
-__device__ __noinline__ double polynomial_delta_dev(double u, double x, double lo, double hi, double xi,
-                                                    const PowSmem* tab) {
-    const PowTables T = pow_tables(*tab);
+// polynomial_delta (operators.hpp:106-121): both branches evaluated, blended by steps. Rare path (about one
+// gene per row): tables are read from global memory so that no pointer into shared memory escapes the kernel.
+__device__ __noinline__ double polynomial_delta_dev(double u, double x, double lo, double hi, double xi) {
+    const PowTables T = pow_tables_global();
     const double range = hi - lo;
     const double e = xi + 1.0, inv_e = 1.0 / e;
     const double near_lo = 1.0 - (x - lo) / range;
@@ -62,6 +62,16 @@ __device__ __noinline__ double polynomial_delta_dev(double u, double x, double l
     const double h_lo = (0.5 - u) >= 0.0 ? 1.0 : 0.0;
     const double h_hi = (u - 0.5) >= 0.0 ? 1.0 : 0.0;
     return d_lo * h_lo + d_hi * h_hi;
+}
+
+// Slow half of the mutation test (operators.hpp:136-145), entered only when the top 21 bits of the mask draw
+// do not already exceed the threshold's (probability ~ pm/d): the full 53-bit comparison and, if the gene is
+// really selected, the mutation itself. Kept out of line so that the hot loop carries only the top-word hash.
+__device__ __noinline__ double mutate_if_selected(double x, uint64_t mask_word, uint64_t mut_word, uint64_t thresh,
+                                                  double lo, double hi, double xi) {
+    if ((mask_word >> 11) > thresh) return x;
+    const double u = word_to_unit(mut_word);
+    return clampd(x + polynomial_delta_dev(u, x, lo, hi, xi), lo, hi);
 }
 
 // Counter stream positioned at a row of a draw block: word(j) is the draw of element j of that row.
@@ -214,15 +224,11 @@ __global__ void __launch_bounds__(256, TEMO_REPRO_MIN_BLOCKS) reproduce_kernel(c
             }
             if (PM && !a.mask_never) {
                 const bool live = !(hi - lo <= 0.0);
-                // (word >> 11) <= T  can only hold if the top 21 bits do not exceed T's: decided from the top word
-                if (live && (st_mask_a.top(j) >> 11) <= a.mask_top && (st_mask_a.word(j) >> 11) <= a.mask_thresh) {
-                    const double u = word_to_unit(st_mut_a.word(j));
-                    ca = clampd(ca + polynomial_delta_dev(u, ca, lo, hi, a.xi, &s_pow), lo, hi);
-                }
-                if (paired && live && (st_mask_b.top(j) >> 11) <= a.mask_top && (st_mask_b.word(j) >> 11) <= a.mask_thresh) {
-                    const double u = word_to_unit(st_mut_b.word(j));
-                    cb = clampd(cb + polynomial_delta_dev(u, cb, lo, hi, a.xi, &s_pow), lo, hi);
-                }
+                // (word >> 11) <= T can only hold if the top 21 bits do not exceed T's: decided from the top word
+                if (live && (st_mask_a.top(j) >> 11) <= a.mask_top)
+                    ca = mutate_if_selected(ca, st_mask_a.word(j), st_mut_a.word(j), a.mask_thresh, lo, hi, a.xi);
+                if (paired && live && (st_mask_b.top(j) >> 11) <= a.mask_top)
+                    cb = mutate_if_selected(cb, st_mask_b.word(j), st_mut_b.word(j), a.mask_thresh, lo, hi, a.xi);
             }
             if (EVAL != 0) {
                 if (j + 1 >= a.m) {
