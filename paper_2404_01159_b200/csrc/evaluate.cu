@@ -24,6 +24,7 @@ struct EvalK {
     double* f;
     uint64_t f_row0;
     const uint32_t* f_row0_dev;
+    uint32_t chunk;  // genes per TMA stage: a multiple of 512 (canonical order), <= kChunkGenes, rows split evenly
 };
 
 template <int PID, int VEC>
@@ -107,7 +108,8 @@ __global__ void __launch_bounds__(256) eval_tma_kernel(const EvalK a) {
     __shared__ double s_red[8];
     __shared__ double s_pos[kMaxObj];
 
-    const uint64_t chunks_per_row = (a.d + kChunkGenes - 1) / kChunkGenes;
+    const uint64_t chunk = a.chunk;
+    const uint64_t chunks_per_row = (a.d + chunk - 1) / chunk;
     const uint64_t my_rows = a.n > blockIdx.x ? (a.n - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
     const uint64_t total = my_rows * chunks_per_row;  // chunks this CTA will consume
 
@@ -121,8 +123,8 @@ __global__ void __launch_bounds__(256) eval_tma_kernel(const EvalK a) {
         const uint64_t local_row = c / chunks_per_row, ch = c - local_row * chunks_per_row;
         const uint64_t i = blockIdx.x + local_row * gridDim.x;
         const uint64_t row = a.rows ? a.rows[i] : i;
-        const uint64_t g0 = ch * kChunkGenes;
-        const uint32_t genes = (uint32_t)((a.d - g0) < (uint64_t)kChunkGenes ? (a.d - g0) : kChunkGenes);
+        const uint64_t g0 = ch * chunk;
+        const uint32_t genes = (uint32_t)((a.d - g0) < chunk ? (a.d - g0) : chunk);
         const int st = (int)(c % kStages);
         mbar_expect_tx(&full_bar[st], genes * 8u);
         tma_load_1d(ring + (size_t)st * kChunkGenes, a.x + row * a.d + g0, genes * 8u, &full_bar[st]);
@@ -137,8 +139,8 @@ __global__ void __launch_bounds__(256) eval_tma_kernel(const EvalK a) {
         const uint64_t local_row = c / chunks_per_row, ch = c - local_row * chunks_per_row;
         const int st = (int)(c % kStages);
         mbar_wait(&full_bar[st], (uint32_t)((c / kStages) & 1));
-        const uint64_t g0 = ch * kChunkGenes;
-        const uint32_t genes = (uint32_t)((a.d - g0) < (uint64_t)kChunkGenes ? (a.d - g0) : kChunkGenes);
+        const uint64_t g0 = ch * chunk;
+        const uint32_t genes = (uint32_t)((a.d - g0) < chunk ? (a.d - g0) : chunk);
         const double2* tile = reinterpret_cast<const double2*>(ring + (size_t)st * kChunkGenes);
         // canonical order: global vector index q = g0/2 + t, t = tid, tid+256, ...
         for (uint32_t t = threadIdx.x; t < genes / 2; t += 256) {
@@ -149,10 +151,12 @@ __global__ void __launch_bounds__(256) eval_tma_kernel(const EvalK a) {
         }
         __syncthreads();  // stage drained by everyone
         if (threadIdx.x == 0 && c + kStages < total) issue(c + kStages);
-        if (ch + 1 == chunks_per_row) {  // row complete
+        if (ch + 1 == chunks_per_row) {  // row complete: leave {sum, position genes} for eval_finish_kernel
             const double sum = block_sum<8>(acc, s_red);
             const uint64_t i = blockIdx.x + local_row * gridDim.x;
-            dtlz_finish<PID>(sum, s_pos, a.m, a.d, a.f + (f0 + i) * a.m);
+            double* frow = a.f + (f0 + i) * a.m;
+            if (threadIdx.x == 0) frow[0] = sum;
+            if (threadIdx.x >= 1 && threadIdx.x < a.m) frow[threadIdx.x] = s_pos[threadIdx.x - 1];
             acc = 0.0;
             __syncthreads();  // s_pos / s_red free for the next row
         }
@@ -189,6 +193,47 @@ __global__ void __launch_bounds__(256) eval_lsmop1_kernel(const EvalK a, const L
     }
 }
 
+// Second half of the TMA path: the streaming kernel leaves {tail sum, position genes} in each objective
+// row; one thread per row turns them into objectives. Keeping the cos/sin/pow latency chain out of the
+// streaming CTAs is what lets them run at HBM speed.
+template <int PID>
+__global__ void eval_finish_kernel(double* f, uint64_t n, uint64_t m, uint64_t d, uint64_t f_row0,
+                                   const uint32_t* f_row0_dev) {
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint64_t f0 = f_row0 + (f_row0_dev ? (uint64_t)*f_row0_dev : 0);
+    double* frow = f + (f0 + i) * m;
+    double pos[kMaxObj];
+    const double sum = frow[0];
+    for (uint64_t k = 0; k + 1 < m; ++k) pos[k] = frow[1 + k];
+    double g;
+    if (PID == kDtlz1 || PID == kDtlz3)
+        g = 100.0 * ((double)(d - m + 1) + sum);
+    else
+        g = sum;
+    const double half_pi = kPi / 2.0;
+    const PowTables T = pow_tables_global();
+    for (uint64_t j = 0; j < m; ++j) {  // same arithmetic as dtlz_finish (problems.cuh)
+        double v;
+        if (PID == kDtlz1) {
+            v = 0.5 * (1.0 + g);
+            for (uint64_t q = 0; q + j + 1 < m; ++q) v *= pos[q];
+            if (j > 0) v *= 1.0 - pos[m - 1 - j];
+        } else {
+            v = 1.0 + g;
+            for (uint64_t q = 0; q + j + 1 < m; ++q) {
+                const double p = PID == kDtlz4 ? pow_like_host(pos[q], 100.0, T) : pos[q];
+                v *= cos(p * half_pi);
+            }
+            if (j > 0) {
+                const double p = PID == kDtlz4 ? pow_like_host(pos[m - 1 - j], 100.0, T) : pos[m - 1 - j];
+                v *= sin(p * half_pi);
+            }
+        }
+        frow[j] = v;
+    }
+}
+
 template <int PID>
 void launch_dtlz(const EvalK& k, bool tma, cudaStream_t s) {
     const int vec = row_vec(k.d), block = row_block(k.d);
@@ -202,6 +247,7 @@ void launch_dtlz(const EvalK& k, bool tma, cudaStream_t s) {
         uint64_t grid = (uint64_t)kSMs * 2;
         if (grid > k.n) grid = k.n;
         eval_tma_kernel<PID><<<(unsigned)grid, 256, smem, s>>>(k);
+        eval_finish_kernel<PID><<<(unsigned)((k.n + 127) / 128), 128, 0, s>>>(k.f, k.n, k.m, k.d, k.f_row0, k.f_row0_dev);
     } else if (vec == 2) {
         eval_ldg_kernel<PID, 2><<<(unsigned)k.n, block, 0, s>>>(k);
     } else {
@@ -234,7 +280,11 @@ void launch_evaluate(const EvalArgs& a, cudaStream_t s) {
     require(a.d >= a.m, "dtlz_eval: d must be at least m");                              // problems.hpp:72
     require(a.m <= (uint64_t)kMaxObj, "evaluate: more than 32 objectives are not supported");
     if (a.n == 0) return;
-    EvalK k{a.x, a.rows, a.n, a.d, a.m, a.f, a.f_row0, a.f_row0_dev};
+    // split a row into equal stages: ceil(d / 4096) chunks, each rounded up to a multiple of 512 genes
+    const uint64_t nchunks = (a.d + kChunkGenes - 1) / kChunkGenes;
+    uint64_t chunk = ((a.d + nchunks - 1) / nchunks + 511) / 512 * 512;
+    if (chunk > (uint64_t)kChunkGenes) chunk = kChunkGenes;
+    EvalK k{a.x, a.rows, a.n, a.d, a.m, a.f, a.f_row0, a.f_row0_dev, (uint32_t)chunk};
     switch (a.problem) {
     case kDtlz1: launch_dtlz<kDtlz1>(k, a.allow_tma, s); break;
     case kDtlz2: launch_dtlz<kDtlz2>(k, a.allow_tma, s); break;
