@@ -98,13 +98,15 @@ __host__ __device__ __forceinline__ uint64_t draw_word(const Rng& g, uint64_t k)
 // ulps are 2^-53 and 2^-21); removing the offsets leaves lo*2^-53 and hi*2^-21, and their
 // sum has at most 53 significant bits, so every step is exact.
 __host__ __device__ __forceinline__ double word_to_unit(uint64_t w) {
-    const uint64_t u = w >> 11;
 #ifdef __CUDA_ARCH__
-    const double lo = __longlong_as_double(0x3FE0000000000000LL | (long long)(u & 0xffffffffULL)) - 0.5;
-    const double hi = __longlong_as_double(0x41E0000000000000LL | (long long)(u >> 32)) - 2147483648.0;
+    const uint32_t w_hi = (uint32_t)(w >> 32), w_lo = (uint32_t)w;
+    const uint32_t u_hi = w_hi >> 11;                     // top 21 of the 53 bits
+    const uint32_t u_lo = (w_hi << 21) | (w_lo >> 11);    // low 32 of the 53 bits
+    const double lo = __hiloint2double(0x3FE00000, (int)u_lo) - 0.5;
+    const double hi = __hiloint2double(0x41E00000, (int)u_hi) - 2147483648.0;
     return hi + lo;
 #else
-    return (double)u * 0x1.0p-53;
+    return (double)(w >> 11) * 0x1.0p-53;
 #endif
 }
 
