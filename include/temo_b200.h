@@ -211,6 +211,12 @@ int temo_b200_shard_plan(uint64_t seed, uint64_t counter, uint64_t P, uint64_t n
                          const int32_t* surv_owner, const uint32_t* surv_slot, uint32_t* send_slots,
                          uint64_t send_slots_cap, uint64_t* send_counts, uint64_t* recv_counts,
                          uint32_t* recv_pos, uint64_t* counters3);
+/* Host thread computing the Fisher-Yates shuffle of a future generation ahead of time (rng.hpp:69-78). */
+int temo_b200_shard_perm_prefetch(uint64_t seed, uint64_t c_shuffle, uint64_t n);
+/* Pure host code: replicated survivor tables after selection (algorithms.hpp:278-279 in sharded form). */
+int temo_b200_shard_update_tables(const uint32_t* elite, uint64_t count, uint64_t P, uint64_t n, int rank, int world,
+                                  const uint32_t* free_all, int32_t* surv_owner, uint32_t* surv_slot,
+                                  uint32_t* own_slots, uint64_t* own_count);
 int temo_b200_shard_create(const temo_b200_run_config* cfg, int rank, int world, temo_b200_shard** out);
 int temo_b200_shard_destroy(temo_b200_shard* s);
 /* info8: n_loc, d, m, r, send_cap, pcap, cap_loc, adapt_every */

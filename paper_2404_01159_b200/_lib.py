@@ -87,6 +87,9 @@ SIGNATURES = {
     "temo_b200_shard_last_error": (C.c_char_p, []),
     "temo_b200_shard_plan": (C.c_int, [u64, u64, u64, u64, u64, C.c_int, C.c_int, C.POINTER(C.c_int32), C.POINTER(C.c_uint32),
                                        C.POINTER(C.c_uint32), u64, u64p, u64p, C.POINTER(C.c_uint32), u64p]),
+    "temo_b200_shard_perm_prefetch": (C.c_int, [u64, u64, u64]),
+    "temo_b200_shard_update_tables": (C.c_int, [C.POINTER(C.c_uint32), u64, u64, u64, C.c_int, C.c_int, C.POINTER(C.c_uint32),
+                                                C.POINTER(C.c_int32), C.POINTER(C.c_uint32), C.POINTER(C.c_uint32), u64p]),
     "temo_b200_shard_create": (C.c_int, [_CFG, C.c_int, C.c_int, C.POINTER(_RUN)]),
     "temo_b200_shard_destroy": (C.c_int, [_RUN]),
     "temo_b200_shard_info": (C.c_int, [_RUN, u64p]),

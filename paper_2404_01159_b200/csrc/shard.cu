@@ -11,6 +11,7 @@
 // draws/evaluates/selects exactly what the single-GPU run does for the same rows (global draw addressing).
 #include <cstring>
 #include <numeric>
+#include <thread>
 
 #include "../../include/temo_b200.h"
 #include "compact.cuh"
@@ -79,6 +80,39 @@ struct IdentityValS {
 
 }  // namespace
 
+// Speculative mating permutation: the Fisher-Yates shuffle of generation t+1 only depends on the draw
+// counter, so a host thread computes it while the GPU is busy with generation t (rng.hpp:69-78).
+struct PermCache {
+    std::thread worker;
+    std::vector<uint32_t> perm;
+    uint64_t seed = 0, c_shuffle = 0, n = 0;
+    bool valid = false;
+    void start(uint64_t seed_, uint64_t c_shuffle_, uint64_t n_) {
+        join();
+        seed = seed_;
+        c_shuffle = c_shuffle_;
+        n = n_;
+        valid = true;
+        worker = std::thread([this] {
+            perm.resize(n);
+            uint64_t c = c_shuffle;
+            shuffle_indices(seed, c, n, perm.data());
+        });
+    }
+    void join() {
+        if (worker.joinable()) worker.join();
+    }
+    bool take(uint64_t seed_, uint64_t c_shuffle_, uint64_t n_, std::vector<uint32_t>& out) {
+        join();
+        if (!valid || seed != seed_ || c_shuffle != c_shuffle_ || n != n_) return false;
+        out.swap(perm);
+        valid = false;
+        return true;
+    }
+    ~PermCache() { join(); }
+};
+static PermCache g_perm_cache;
+
 // Host-side exchange plan of one generation (pure host code; exercised on CPU by the gloo tests).
 // Inputs: the replicated survivor tables and the draw counter at the top of the generation.
 // Outputs (for `rank`): the local slots to send, grouped by destination rank and ordered by the
@@ -93,8 +127,13 @@ void shard_plan(uint64_t seed, uint64_t counter, uint64_t P, uint64_t n, int ran
     uint64_t c = counter;
     const uint64_t c_pool = c;
     if (P != n) c += n;  // algorithms.hpp:211-221
-    std::vector<uint32_t> perm(n);
-    shuffle_indices(seed, c, n, perm.data());  // advances c by n - 1
+    std::vector<uint32_t> perm;
+    if (g_perm_cache.take(seed, c, n, perm)) {
+        c += n - 1;  // computed ahead of time by the speculation thread
+    } else {
+        perm.resize(n);
+        shuffle_indices(seed, c, n, perm.data());  // advances c by n - 1
+    }
     counters_out[0] = c;                       // c_sbx: first draw after the shuffle
     const uint64_t base = mix64(seed);
     auto pool_idx = [&](uint64_t q) -> uint64_t {
@@ -419,6 +458,47 @@ int temo_b200_shard_plan(uint64_t seed, uint64_t counter, uint64_t P, uint64_t n
         counters3[0] = cs[0];                              // c_sbx
         counters3[1] = cs[0] + 3 * half * d + half;        // c_pm
         counters3[2] = counters3[1] + 2 * n * d;           // counter after the generation
+    });
+}
+
+// Starts the Fisher-Yates shuffle of a future generation on a host thread (consumed by the next
+// temo_b200_shard_plan with the same seed / shuffle counter / n; ignored otherwise).
+int temo_b200_shard_perm_prefetch(uint64_t seed, uint64_t c_shuffle, uint64_t n) {
+    return guarded_shard([&] {
+        require(n >= 1 && n < 0xffffffffULL, "shuffle_indices: n must be positive");
+        g_perm_cache.start(seed, c_shuffle, n);
+    });
+}
+
+// Pure host code: survivor tables after selection. Survivor k takes over merged row elite[k]: a parent keeps
+// its (owner, slot); child i = elite[k] - P lives on the rank that produced it, in that rank's free slot
+// (free_all[rank * n_loc + local child index]). Also lists the slots owned by `rank`.
+int temo_b200_shard_update_tables(const uint32_t* elite, uint64_t count, uint64_t P, uint64_t n, int rank, int world,
+                                  const uint32_t* free_all, int32_t* surv_owner, uint32_t* surv_slot,
+                                  uint32_t* own_slots, uint64_t* own_count) {
+    return guarded_shard([&] {
+        require(elite && free_all && surv_owner && surv_slot && own_slots && own_count, "update_tables: null argument");
+        const uint64_t half = n / 2, h_loc = half / world, n_loc = 2 * h_loc;
+        std::vector<int32_t> no(count);
+        std::vector<uint32_t> ns(count);
+        uint64_t mine = 0;
+        for (uint64_t k = 0; k < count; ++k) {
+            const uint64_t e = elite[k];
+            if (e < P) {
+                no[k] = surv_owner[e];
+                ns[k] = surv_slot[e];
+            } else {
+                const uint64_t i = e - P, p = i < half ? i : i - half;
+                const uint64_t rk = p / h_loc;
+                const uint64_t j = i < half ? p - rk * h_loc : h_loc + p - rk * h_loc;
+                no[k] = (int32_t)rk;
+                ns[k] = free_all[rk * n_loc + j];
+            }
+            if (no[k] == rank) own_slots[mine++] = ns[k];
+        }
+        std::memcpy(surv_owner, no.data(), count * sizeof(int32_t));
+        std::memcpy(surv_slot, ns.data(), count * sizeof(uint32_t));
+        *own_count = mine;
     });
 }
 

@@ -244,6 +244,9 @@ class ShardedRvea:
         n, world, rank, P = self.n, self.world, self.rank, self.P
         t0 = time.perf_counter()
         plan = shard_plan(cfg.seed, self.counter, P, n, self.d, rank, world, self.surv_owner[:P], self.surv_slot[:P])
+        # while the GPU works on this generation, a host thread shuffles for the next one (its counters only
+        # depend on this generation's, assuming the survivor count will differ from n: algorithms.hpp:211-221)
+        _lib.load().temo_b200_shard_perm_prefetch(u64(cfg.seed), u64(plan["c_end"] + n), u64(n))
         self._tick("plan", t0)
         t0 = time.perf_counter()
         sh.pack(plan["send_slots"])
@@ -271,17 +274,18 @@ class ShardedRvea:
         self._tick("select", t0)
         t0 = time.perf_counter()
         # survivor k <- merged row elite[k]: a parent keeps its (owner, slot); a child lives where it was born
-        is_parent = elite < P
-        child = np.where(is_parent, 0, elite - P)
-        c_rank, c_local = child_location(child, n, world)
-        free_all = sh.free_slots_host().astype(np.uint32)
-        c_slot = free_all[c_rank.astype(np.int64) * self.n_loc + c_local]
-        pe = np.where(is_parent, elite, 0)
-        new_owner = np.where(is_parent, self.surv_owner[pe], c_rank).astype(np.int32)
-        new_slot = np.where(is_parent, self.surv_slot[pe], c_slot).astype(np.uint32)
         cnt = len(elite)
-        self.surv_owner[:cnt], self.surv_slot[:cnt] = new_owner, new_slot
-        sh.commit(cnt, new_slot[new_owner == rank], self.t)
+        elite32 = np.ascontiguousarray(elite, dtype=np.uint32)
+        free_all = np.ascontiguousarray(sh.free_slots_host()).view(np.uint32)
+        own = np.empty(max(cnt, 1), dtype=np.uint32)
+        own_count = u64(0)
+        L = _lib.load()
+        rc = L.temo_b200_shard_update_tables(elite32.ctypes.data_as(u32p), u64(cnt), u64(P), u64(n), rank, world,
+                                             free_all.ctypes.data_as(u32p), self.surv_owner.ctypes.data_as(i32p),
+                                             self.surv_slot.ctypes.data_as(u32p), own.ctypes.data_as(u32p), C.byref(own_count))
+        if rc:
+            raise ValueError(L.temo_b200_shard_last_error().decode())
+        sh.commit(cnt, own[: own_count.value], self.t)
         self._tick("commit", t0)
         self.last_elite = elite
         self.P, self.counter, self.t = cnt, plan["c_end"], self.t + 1
