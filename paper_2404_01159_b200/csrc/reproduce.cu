@@ -34,6 +34,10 @@ struct ReproK {
     uint64_t g_unit0, g_half, g_n;  // position of this launch inside the global draw blocks (sharded runs)
     Rng rng;
     uint64_t c_mc, c_r1, c_r2, c_r3, c_mask, c_mut;
+    // Draw addressing in stream units (SplitMix64: counter * GOLDEN added to mix64(seed); Philox: the counter
+    // itself): element j of row u of a draw block sits at s_base + u * s_row + j * s_gene + (block delta). All
+    // block deltas are launch constants, so one 64-bit value per CTA positions every stream.
+    uint64_t s_base, s_row, s_gene, dl_r1, dl_r2, dl_mask_a, dl_mask_b, dl_mut_a, dl_mut_b;
     double pc, inv_exp, xi;
     uint64_t mask_thresh;  // mutate iff (word >> 11) <= mask_thresh
     uint32_t mask_top;     // = mask_thresh >> 32: necessary condition on the top 21 bits
@@ -74,22 +78,19 @@ __device__ __noinline__ double mutate_if_selected(double x, uint64_t mask_word, 
     return clampd(x + polynomial_delta_dev(u, x, lo, hi, xi), lo, hi);
 }
 
-// Counter stream positioned at a row of a draw block: word(j) is the draw of element j of that row.
-// SplitMix64: mix64(mix64(seed) + (c0 + j) * GOLDEN); the row offset is folded into `a` once per
-// CTA so that a draw costs one 32x64-bit multiply-add plus the two mixing rounds.
+// Draw words of this CTA's rows. pos = s_base + row * s_row is computed once per CTA; a gene's stream
+// positions are pos + j * s_gene + (launch-constant block delta), so a draw costs one 32x64-bit multiply-add
+// per gene (shared by all of its streams), one 64-bit add per stream and the two mixing rounds.
 template <int MODE>
-struct RowStream {
-    uint64_t a;
+struct Draws {
     uint64_t seed;
-    __device__ __forceinline__ RowStream(const Rng& g, uint64_t c0) : a(MODE == 0 ? g.base + c0 * kGolden : c0), seed(g.seed) {}
-    __device__ __forceinline__ uint64_t word(uint32_t j) const {
-        if (MODE == 0) return mix64(a + (uint64_t)j * kGolden);
-        return philox_word(seed, a + j);
+    __device__ __forceinline__ uint64_t gene(uint64_t pos, uint32_t j, uint64_t s_gene) const {
+        return pos + (uint64_t)j * s_gene;
     }
-    // top 31 bits of word(j) (bit 0 of the result is not meaningful)
-    __device__ __forceinline__ uint32_t top(uint32_t j) const {
-        if (MODE == 0) return mix64_top32(a + (uint64_t)j * kGolden);
-        return (uint32_t)(philox_word(seed, a + j) >> 32);
+    __device__ __forceinline__ uint64_t word(uint64_t at) const { return MODE == 0 ? mix64(at) : philox_word(seed, at); }
+    // top 31 bits of word(at) (bit 0 of the result is not meaningful)
+    __device__ __forceinline__ uint32_t top(uint64_t at) const {
+        return MODE == 0 ? mix64_top32(at) : (uint32_t)(philox_word(seed, at) >> 32);
     }
 };
 
@@ -131,11 +132,8 @@ __global__ void __launch_bounds__(256, TEMO_REPRO_MIN_BLOCKS) reproduce_kernel(c
     // (global numbering: a shard of a multi-GPU run draws exactly what the single-GPU run draws for its rows)
     const uint64_t g_unit = a.g_unit0 + unit;
     const uint64_t g_row_a = SBX ? (paired ? g_unit : a.g_n - 1) : g_unit;
-    const uint64_t g_row_b = a.g_half + g_unit;
-    const RowStream<MODE> st_mc(a.rng, a.c_mc + g_unit * a.d), st_r1(a.rng, a.c_r1 + g_unit * a.d),
-        st_r2(a.rng, a.c_r2 + g_unit * a.d);
-    const RowStream<MODE> st_mask_a(a.rng, a.c_mask + g_row_a * a.d), st_mut_a(a.rng, a.c_mut + g_row_a * a.d);
-    const RowStream<MODE> st_mask_b(a.rng, a.c_mask + g_row_b * a.d), st_mut_b(a.rng, a.c_mut + g_row_b * a.d);
+    const Draws<MODE> rnd{a.rng.seed};
+    const uint64_t pos = a.s_base + g_row_a * a.s_row;  // Mc block position of row g_row_a; the others are offsets
 
     // pair-level crossover switch: hc = H(r3 - pc) (operators.hpp:82)
     bool pair_cross = false;
@@ -179,7 +177,8 @@ __global__ void __launch_bounds__(256, TEMO_REPRO_MIN_BLOCKS) reproduce_kernel(c
         if (SBX && paired && pair_cross) {  // CTA-uniform
             // hr = H(r2 - 0.5): the top bit of the word; a gene crosses iff it is clear (operators.hpp:90-91)
 #pragma unroll
-            for (int v = 0; v < VEC; ++v) crosses[v] = in_range && (st_r2.top(j0 + v) >> 31) == 0;
+            for (int v = 0; v < VEC; ++v)
+                crosses[v] = in_range && (rnd.top(rnd.gene(pos, j0 + v, a.s_gene) + a.dl_r2) >> 31) == 0;
             // The spread factor (two draws + one pow) is needed by ~half of the genes only: compact the
             // crossing genes of the warp so that the expensive part runs with full lanes.
             const unsigned b0 = __ballot_sync(0xffffffffu, crosses[0]);
@@ -193,8 +192,9 @@ __global__ void __launch_bounds__(256, TEMO_REPRO_MIN_BLOCKS) reproduce_kernel(c
             for (int t = lane; t < total; t += 32) {
                 const int code = s_list[warp][t];
                 const uint32_t j = (q_warp + (code >> 1)) * VEC + (code & 1);
-                const double mc = word_to_unit(st_mc.word(j));
-                const bool up = (st_r1.top(j) >> 31) != 0;  // sgn(r1 - 0.5)
+                const uint64_t at = rnd.gene(pos, j, a.s_gene);
+                const double mc = word_to_unit(rnd.word(at));
+                const bool up = (rnd.top(at + a.dl_r1) >> 31) != 0;  // sgn(r1 - 0.5)
                 // live spread branch only (hm = H(0.5 - mc)); the other one is multiplied by exactly 0.0
                 const bool low = 0.5 - mc >= 0.0;
                 const double base = low ? 2.0 * mc : 2.0 - 2.0 * mc;
@@ -225,10 +225,11 @@ __global__ void __launch_bounds__(256, TEMO_REPRO_MIN_BLOCKS) reproduce_kernel(c
             if (PM && !a.mask_never) {
                 const bool live = !(hi - lo <= 0.0);
                 // (word >> 11) <= T can only hold if the top 21 bits do not exceed T's: decided from the top word
-                if (live && (st_mask_a.top(j) >> 11) <= a.mask_top)
-                    ca = mutate_if_selected(ca, st_mask_a.word(j), st_mut_a.word(j), a.mask_thresh, lo, hi, a.xi);
-                if (paired && live && (st_mask_b.top(j) >> 11) <= a.mask_top)
-                    cb = mutate_if_selected(cb, st_mask_b.word(j), st_mut_b.word(j), a.mask_thresh, lo, hi, a.xi);
+                const uint64_t at = rnd.gene(pos, j, a.s_gene);
+                if (live && (rnd.top(at + a.dl_mask_a) >> 11) <= a.mask_top)
+                    ca = mutate_if_selected(ca, rnd.word(at + a.dl_mask_a), rnd.word(at + a.dl_mut_a), a.mask_thresh, lo, hi, a.xi);
+                if (paired && live && (rnd.top(at + a.dl_mask_b) >> 11) <= a.mask_top)
+                    cb = mutate_if_selected(cb, rnd.word(at + a.dl_mask_b), rnd.word(at + a.dl_mut_b), a.mask_thresh, lo, hi, a.xi);
             }
             if (EVAL != 0) {
                 if (j + 1 >= a.m) {
@@ -360,6 +361,20 @@ void launch_reproduce(const ReproArgs& a, cudaStream_t s) {
     k.c_r3 = a.c_sbx + 3 * hd;
     k.c_mask = a.c_pm;
     k.c_mut = a.c_pm + k.g_n * a.d;
+    {
+        // stream units: SplitMix64 positions are (counter * GOLDEN) added to mix64(seed); Philox uses the counter
+        const uint64_t u = a.rng.mode == 0 ? kGolden : 1ULL;
+        const uint64_t c_ref = a.do_sbx ? k.c_mc : k.c_mask;  // block the CTA position refers to
+        k.s_base = (a.rng.mode == 0 ? a.rng.base : 0ULL) + c_ref * u;
+        k.s_row = a.d * u;
+        k.s_gene = u;
+        k.dl_r1 = (k.c_r1 - c_ref) * u;
+        k.dl_r2 = (k.c_r2 - c_ref) * u;
+        k.dl_mask_a = (k.c_mask - c_ref) * u;
+        k.dl_mask_b = k.dl_mask_a + k.g_half * a.d * u;  // row half + p of the mask block
+        k.dl_mut_a = (k.c_mut - c_ref) * u;
+        k.dl_mut_b = k.dl_mut_a + k.g_half * a.d * u;
+    }
     k.pc = a.ga.pc;
     k.inv_exp = 1.0 / (a.ga.eta + 1.0);  // operators.hpp:75
     k.xi = a.ga.xi;
