@@ -273,6 +273,20 @@ LsmopLayout lsmop1_layout(uint64_t d, uint64_t m) {
     return lay;
 }
 
+// {tail sum, position genes} left in the objective rows by a streaming kernel -> objectives (DTLZ1-4)
+void launch_dtlz_finish(int problem, double* f, uint64_t n, uint64_t m, uint64_t d, uint64_t f_row0, cudaStream_t s) {
+    if (n == 0) return;
+    const unsigned grid = (unsigned)((n + 127) / 128);
+    switch (problem) {
+    case kDtlz1: eval_finish_kernel<kDtlz1><<<grid, 128, 0, s>>>(f, n, m, d, f_row0, nullptr); break;
+    case kDtlz2: eval_finish_kernel<kDtlz2><<<grid, 128, 0, s>>>(f, n, m, d, f_row0, nullptr); break;
+    case kDtlz3: eval_finish_kernel<kDtlz3><<<grid, 128, 0, s>>>(f, n, m, d, f_row0, nullptr); break;
+    case kDtlz4: eval_finish_kernel<kDtlz4><<<grid, 128, 0, s>>>(f, n, m, d, f_row0, nullptr); break;
+    default: fail(1, "dtlz finish: not a DTLZ problem");
+    }
+    TEMO_CUDA(cudaGetLastError());
+}
+
 void launch_evaluate(const EvalArgs& a, cudaStream_t s) {
     require(problem_known(a.problem), "evaluate: unknown problem");
     if (a.problem <= kDtlz4) require(a.problem >= 1, "dtlz_eval: id must be in 1..4");  // problems.hpp:70

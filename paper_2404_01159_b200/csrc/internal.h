@@ -82,6 +82,8 @@ struct EvalArgs {
     bool allow_tma = true;
 };
 void launch_evaluate(const EvalArgs& a, cudaStream_t s);
+// second half of the streaming evaluators: rows holding {tail sum, position genes} -> objectives
+void launch_dtlz_finish(int problem, double* f, uint64_t n, uint64_t m, uint64_t d, uint64_t f_row0, cudaStream_t s);
 
 // ---- K3: selection ----------------------------------------------------------------------------
 struct SelectWorkspace {

@@ -256,11 +256,17 @@ __global__ void __launch_bounds__(256, TEMO_REPRO_MIN_BLOCKS) reproduce_kernel(c
 
     if (EVAL != 0) {
         const uint64_t f0 = a.f_row0 + (a.f_row0_dev ? (uint64_t)*a.f_row0_dev : 0);
+        // leave {tail sum, position genes} in the objective rows; launch_dtlz_finish turns them into objectives
+        // (keeps the cos/sin/pow latency chain out of the tail of every CTA)
         const double ga = block_sum<8>(acc_a, s_red);
-        dtlz_finish<EVAL>(ga, s_pos[0], a.m, a.d, a.f_out + (f0 + row_a) * a.m);
+        double* fa = a.f_out + (f0 + row_a) * a.m;
+        if (threadIdx.x == 0) fa[0] = ga;
+        if (threadIdx.x >= 1 && threadIdx.x < a.m) fa[threadIdx.x] = s_pos[0][threadIdx.x - 1];
         if (paired) {
             const double gb = block_sum<8>(acc_b, s_red);
-            dtlz_finish<EVAL>(gb, s_pos[1], a.m, a.d, a.f_out + (f0 + row_b) * a.m);
+            double* fb = a.f_out + (f0 + row_b) * a.m;
+            if (threadIdx.x == 0) fb[0] = gb;
+            if (threadIdx.x >= 1 && threadIdx.x < a.m) fb[threadIdx.x] = s_pos[1][threadIdx.x - 1];
         }
     }
 }
@@ -400,6 +406,10 @@ void launch_reproduce(const ReproArgs& a, cudaStream_t s) {
     else
         launch_mode<1>(k, a.do_sbx, a.do_pm, units, block, vec, a.eval_problem, s);
     TEMO_CUDA(cudaGetLastError());
+    if (a.eval_problem != 0) {
+        require(a.f_row0_dev == nullptr, "reproduce: device-side row offsets are not supported with fused evaluation");
+        launch_dtlz_finish(a.eval_problem, a.f_out, a.n, a.m, a.d, a.f_row0, s);
+    }
 }
 
 void launch_pow_batch(const double* x, const double* y, uint64_t n, double* out, cudaStream_t s) {
