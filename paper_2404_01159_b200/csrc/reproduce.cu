@@ -17,6 +17,9 @@
 // IEEE operations in the reference's order. Dead branches the reference multiplies by an
 // exact 0.0 are skipped (verified bit-identical); the only inexact pieces are
 // CUDA's pow (<= 2 ulp) on crossed/mutated genes.
+#include <algorithm>
+#include <cstdlib>
+
 #include "glibc_pow_dev.cuh"
 #include "internal.h"
 #include "problems.cuh"
@@ -31,6 +34,7 @@ struct ReproK {
     double* out;
     const uint32_t* dst;
     uint64_t n, d, half;
+    uint64_t unit0;  // first mating unit of this launch (grid block 0)
     uint64_t g_unit0, g_half, g_n;  // position of this launch inside the global draw blocks (sharded runs)
     Rng rng;
     uint64_t c_mc, c_r1, c_r2, c_r3, c_mask, c_mut;
@@ -42,6 +46,7 @@ struct ReproK {
     uint64_t mask_thresh;  // mutate iff (word >> 11) <= mask_thresh
     uint32_t mask_top;     // = mask_thresh >> 32: necessary condition on the top 21 bits
     int mask_never;
+    int cand_cap;    // pair kernel: mutation-candidate slots per warp and tile (<= kPairCand)
     int narrow_pow;  // 1/(eta+1) in [2^-10, 1]: the SBX pow stays on the common path of the libm algorithm
     const double* lower;
     const double* upper;
@@ -94,22 +99,27 @@ struct Draws {
     }
 };
 
-#ifndef TEMO_REPRO_MIN_BLOCKS
-#define TEMO_REPRO_MIN_BLOCKS 4
-#endif
+// Shared memory of the generic unit (also carved out of the pair kernel's tile for its redo path).
+struct GenericSmem {
+    double red[8];
+    double pos[2][kMaxObj];
+    PowSmem pow;
+    unsigned char list[8][64];  // per warp: compacted (lane, v) codes of the crossing genes
+    double beta[8][64];         // per warp: signed spread factor per (lane, v)
+};
+
+// One mating unit (a pair, or the unpaired last row of an odd population) by the whole CTA.
 template <int MODE, bool SBX, bool PM, int EVAL, int VEC>
-__global__ void __launch_bounds__(256, TEMO_REPRO_MIN_BLOCKS) reproduce_kernel(const ReproK a) {
-    __shared__ double s_red[8];
-    __shared__ double s_pos[2][kMaxObj];
-    __shared__ PowSmem s_pow;
-    __shared__ unsigned char s_list[8][64];  // per warp: compacted (lane, v) codes of the crossing genes
-    __shared__ double s_beta[8][64];         // per warp: signed spread factor per (lane, v)
-    pow_smem_load(s_pow);
+__device__ __forceinline__ void reproduce_unit(const ReproK& a, const uint64_t unit, GenericSmem& G) {
+    double* const s_red = G.red;
+    double (*const s_pos)[kMaxObj] = G.pos;
+    unsigned char (*const s_list)[64] = G.list;
+    double (*const s_beta)[64] = G.beta;
+    pow_smem_load(G.pow);
     __syncthreads();
-    const PowTables T = pow_tables(s_pow);
+    const PowTables T = pow_tables(G.pow);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
-    const uint64_t unit = blockIdx.x;
     const bool paired = SBX && unit < a.half;
     // shuffled-order rows handled by this CTA
     const uint64_t row_a = SBX ? (paired ? unit : a.n - 1) : unit;
@@ -271,6 +281,402 @@ __global__ void __launch_bounds__(256, TEMO_REPRO_MIN_BLOCKS) reproduce_kernel(c
     }
 }
 
+#ifndef TEMO_REPRO_MIN_BLOCKS
+#define TEMO_REPRO_MIN_BLOCKS 4
+#endif
+template <int MODE, bool SBX, bool PM, int EVAL, int VEC>
+__global__ void __launch_bounds__(256, TEMO_REPRO_MIN_BLOCKS) reproduce_kernel(const ReproK a) {
+    __shared__ GenericSmem G;
+    reproduce_unit<MODE, SBX, PM, EVAL, VEC>(a, a.unit0 + blockIdx.x, G);
+}
+
+
+// ------------------------------------------------------------------------------------------------
+// Fast path: SBX + PM over full mating pairs, 128-bit vectors (d even), 256 threads per pair.
+//
+// Same arithmetic, same draws, same thread->gene map (warp w owns the 64-gene blocks w, w+8, ... of the
+// row; lane l the vector l of a block) as reproduce_unit above, reorganised so that the expensive parts
+// run dense and branch-free. Every warp walks its blocks of a row tile in four passes of its own (no CTA
+// barrier between them, so the warps of an SM drift apart and their passes overlap):
+//   A  hashes only. hr = H(r2 - 0.5) for every gene (operators.hpp:90-91): the crossing genes (about half)
+//      are appended to the warp's list in shared memory and beta = 1 is planted for everybody. The quick
+//      reject of the mutation mask H(pm/d - r4) (operators.hpp:136) for both children: the few genes that
+//      survive it (about one per row) go to the warp's candidate list.
+//   B  the crossing list is consumed 32 genes at a time with all lanes busy: Mc, sgn(R1 - 0.5) and the
+//      libm-exact pow give the signed spread factor, stored by gene into the beta tile (operators.hpp:85-89).
+//   M  the candidate list (rare): exact 53-bit mask test, SBX children of that gene, polynomial mutation
+//      (operators.hpp:106-145); the final pair of children is parked in shared memory and the gene's beta is
+//      replaced by a tagged NaN pointing at it.
+//   C  the streaming pass: 128-bit loads of both parents, blend + clamp (operators.hpp:92-95), a tagged beta
+//      swaps in the parked children, fused objective partial sums, 128-bit stores of both children.
+// The parent rows are pulled into L2 by the bulk-copy engine (cp.async.bulk.prefetch.L2, SASS UBLKPF) when
+// the CTA starts, so HBM streams while passes A and B compute and pass C reads L2 hits.
+// A warp with more than kPairCand mutation candidates in one tile (probability ~1e-15 at pm = 1) raises a
+// flag and the CTA redoes the pair through reproduce_unit: the result is exact in every case.
+constexpr int kPairWarps = 8;
+constexpr int kPairBlocks = 10;                              // 64-gene blocks per warp and tile
+constexpr int kPairTile = kPairWarps * kPairBlocks * 64;     // genes per tile (5120)
+constexpr int kPairCand = 16;                                // mutation candidates per warp and tile
+constexpr uint32_t kBetaTagHi = 0x7ff80000u;                 // high word of the tagged NaN
+
+struct PairSmem {
+    PowSmem pow;
+    double beta[kPairTile];
+    unsigned short list[kPairTile];
+    double2 side[kPairWarps][kPairCand];  // final children {a, b} of a candidate gene
+    unsigned short cand[kPairWarps][kPairCand];
+    uint32_t ncand[kPairWarps];
+    uint32_t overflow;
+    double red[8];
+    double pos[2][kMaxObj];
+};
+static_assert(sizeof(GenericSmem) <= sizeof(double) * kPairTile, "redo path aliases the beta tile");
+
+__device__ __forceinline__ void l2_prefetch_bulk(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+// mix64 (rng.hpp:23-30) on 32-bit halves; a 64-bit product costs one wide multiply and two multiply-adds.
+struct Hash64 {
+    uint32_t lo, hi;
+};
+__device__ __forceinline__ Hash64 mix_round1(uint64_t z) {
+    const uint32_t zl = (uint32_t)z, zh = (uint32_t)(z >> 32);
+    const uint32_t xl = zl ^ __funnelshift_r(zl, zh, 30), xh = zh ^ (zh >> 30);
+    uint32_t pl, ph;
+    asm("{\n\t.reg .u64 p;\n\tmul.wide.u32 p, %2, 0x1ce4e5b9;\n\tmov.b64 {%0, %1}, p;\n\t"
+        "mad.lo.u32 %1, %3, 0x1ce4e5b9, %1;\n\tmad.lo.u32 %1, %2, 0xbf58476d, %1;\n\t}"
+        : "=r"(pl), "=&r"(ph)
+        : "r"(xl), "r"(xh));
+    Hash64 y;
+    y.lo = pl ^ __funnelshift_r(pl, ph, 27);
+    y.hi = ph ^ (ph >> 27);
+    return y;
+}
+// top 32 bits of mix64(z) before the last xor-shift (bits 31..1 are those of the word: w = y ^ (y >> 31))
+__device__ __forceinline__ uint32_t mix_top(uint64_t z) {
+    const Hash64 y = mix_round1(z);
+    uint32_t t;
+    asm("{\n\tmul.hi.u32 %0, %1, 0x133111eb;\n\tmad.lo.u32 %0, %1, 0x94d049bb, %0;\n\tmad.lo.u32 %0, %2, 0x133111eb, %0;\n\t}"
+        : "=&r"(t)
+        : "r"(y.lo), "r"(y.hi));
+    return t;
+}
+__device__ __forceinline__ uint64_t mix_full(uint64_t z) {
+    const Hash64 y = mix_round1(z);
+    uint32_t pl, ph;
+    asm("{\n\t.reg .u64 p;\n\tmul.wide.u32 p, %2, 0x133111eb;\n\tmov.b64 {%0, %1}, p;\n\t"
+        "mad.lo.u32 %1, %3, 0x133111eb, %1;\n\tmad.lo.u32 %1, %2, 0x94d049bb, %1;\n\t}"
+        : "=r"(pl), "=&r"(ph)
+        : "r"(y.lo), "r"(y.hi));
+    const uint32_t wl = pl ^ __funnelshift_r(pl, ph, 31), wh = ph ^ (ph >> 31);
+    return ((uint64_t)wh << 32) | wl;
+}
+template <int MODE>
+__device__ __forceinline__ uint32_t draw_top(uint64_t seed, uint64_t at) {
+    return MODE == 0 ? mix_top(at) : (uint32_t)(philox_word(seed, at) >> 32);
+}
+template <int MODE>
+__device__ __forceinline__ uint64_t draw_full(uint64_t seed, uint64_t at) {
+    return MODE == 0 ? mix_full(at) : philox_word(seed, at);
+}
+
+// SBX blend of one gene (operators.hpp:92-95 as written); beta = 1 returns the parents through the same
+// arithmetic as on the CPU. Shared by passes M and C so that both produce the same bits.
+__device__ __forceinline__ void sbx_children(double xa, double xb, double beta, double lo, double hi, double& ca,
+                                             double& cb) {
+    const double p = 1.0 + beta, m = 1.0 - beta;
+    ca = clampd((p * xa + m * xb) / 2.0, lo, hi);
+    cb = clampd((m * xa + p * xb) / 2.0, lo, hi);
+}
+
+// pow for the spread factor outside the narrow fast path (never taken for ordinary eta)
+__device__ __noinline__ double pow_spread_slow(double x, double y) { return pow_like_host(x, y, pow_tables_global()); }
+
+// Pass M for one candidate gene (rare, out of line): exact mask tests, live range, mutation of either child.
+template <int MODE>
+__device__ __noinline__ void mutate_candidate(uint64_t seed, uint64_t pos_ma, uint64_t pos_mb, uint64_t d_mut, uint64_t thresh,
+                                              double xi, uint32_t entry, uint32_t j, double xa, double xb, double lo, double hi,
+                                              double* beta_slot, double2* side_slot, uint32_t slot) {
+    constexpr uint64_t SG = MODE == 0 ? kGolden : 1ULL;
+    double ca, cb;
+    sbx_children(xa, xb, *beta_slot, lo, hi, ca, cb);
+    if (!(hi - lo <= 0.0)) {  // operators.hpp:137
+        if (entry & 0x2000u) {
+            const uint64_t at = pos_ma + (uint64_t)j * SG;
+            ca = mutate_if_selected(ca, draw_full<MODE>(seed, at), draw_full<MODE>(seed, at + d_mut), thresh, lo, hi, xi);
+        }
+        if (entry & 0x4000u) {
+            const uint64_t at = pos_mb + (uint64_t)j * SG;
+            cb = mutate_if_selected(cb, draw_full<MODE>(seed, at), draw_full<MODE>(seed, at + d_mut), thresh, lo, hi, xi);
+        }
+    }
+    *side_slot = make_double2(ca, cb);
+    *beta_slot = __hiloint2double((int)kBetaTagHi, (int)slot);
+}
+
+template <int MODE, int EVAL>
+__device__ __noinline__ void redo_pair(const ReproK a, uint64_t unit, GenericSmem& G) {
+    reproduce_unit<MODE, true, true, EVAL, 2>(a, unit, G);
+}
+
+#ifndef TEMO_PAIR_MIN_BLOCKS
+#define TEMO_PAIR_MIN_BLOCKS 3
+#endif
+// Shared-memory accesses of the pair kernel go through explicit 32-bit shared addresses, and the per-thread
+// constants are made opaque to the compiler once: both keep ptxas from re-deriving them (special-register reads,
+// window-base arithmetic, 64-bit multiplies) inside the hot loops.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint32_t opaque(uint32_t v) {
+    asm volatile("" : "+r"(v));
+    return v;
+}
+template <class P>
+__device__ __forceinline__ P* opaque_ptr(P* p) {
+    asm volatile("" : "+l"(p));
+    return p;
+}
+__device__ __forceinline__ void sts_f64x2(uint32_t addr, double a, double b) {
+    asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(addr), "d"(a), "d"(b) : "memory");
+}
+__device__ __forceinline__ void sts_f64(uint32_t addr, double a) {
+    asm volatile("st.shared.f64 [%0], %1;" ::"r"(addr), "d"(a) : "memory");
+}
+__device__ __forceinline__ void sts_u16(uint32_t addr, uint32_t v) {
+    asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"((unsigned short)v) : "memory");
+}
+__device__ __forceinline__ double2 lds_f64x2(uint32_t addr) {
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ uint32_t lds_u16(uint32_t addr) {
+    unsigned short v;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr));
+    return v;
+}
+
+template <int MODE, int EVAL>
+__global__ void __launch_bounds__(256, TEMO_PAIR_MIN_BLOCKS) reproduce_pairs_kernel(const ReproK a) {
+    extern __shared__ __align__(16) unsigned char pair_smem_raw[];
+    PairSmem& S = *reinterpret_cast<PairSmem*>(pair_smem_raw);
+    constexpr uint64_t SG = MODE == 0 ? kGolden : 1ULL;  // stream distance of neighbouring genes
+    constexpr uint64_t STEP = SG * (uint64_t)(kPairWarps * 64);  // ... of a lane's consecutive blocks
+    constexpr uint32_t kBlockBytes = kPairWarps * 64 * 8;  // beta-tile distance of a lane's consecutive blocks
+    const uint32_t lane = opaque(threadIdx.x & 31), warp = opaque(threadIdx.x >> 5);
+
+    const uint64_t unit = a.unit0 + blockIdx.x;  // < a.half: always a full pair
+    const uint64_t row_a = unit, row_b = a.half + unit;
+    const double* pa = a.pool + (a.src ? (uint64_t)a.src[row_a] : row_a) * a.d;
+    const double* pb = a.pool + (a.src ? (uint64_t)a.src[row_b] : row_b) * a.d;
+    double* oa = a.out + (a.dst ? (uint64_t)a.dst[row_a] : row_a) * a.d;
+    double* ob = a.out + (a.dst ? (uint64_t)a.dst[row_b] : row_b) * a.d;
+    if (threadIdx.x == 0) {
+        l2_prefetch_bulk(pa, (uint32_t)(a.d * 8));
+        l2_prefetch_bulk(pb, (uint32_t)(a.d * 8));
+        S.overflow = 0;
+    }
+    pow_smem_load(S.pow);
+    __syncthreads();
+    const PowTables T = pow_tables(S.pow);
+
+    const uint64_t g_unit = a.g_unit0 + unit;
+    const uint64_t seed = a.rng.seed;
+    const uint64_t pos = a.s_base + g_unit * a.s_row;  // Mc block position of gene 0 of this pair
+    const bool pair_cross = !(word_to_unit(draw_word<MODE>(a.rng, a.c_r3 + g_unit)) - a.pc >= 0.0);  // operators.hpp:82
+
+    const uint32_t nvec = (uint32_t)(a.d >> 1);
+    const uint32_t nblk = (nvec + 31) >> 5;  // 64-gene blocks in a row
+    const uint32_t lt = opaque((1u << lane) - 1u);
+    const uint32_t top_thr = a.mask_never ? 0u : ((a.mask_top << 11) | 0x7ffu);  // (top >> 11) <= mask_top
+    // this thread's slots: its vector of the warp's first block in the beta tile, the warp's crossing list
+    const uint32_t sm_beta0 = opaque(smem_u32(S.beta) + (warp * 64 + lane * 2) * 8);
+    const uint32_t sm_beta_tile = opaque(smem_u32(S.beta));
+    const uint32_t sm_list = opaque(smem_u32(S.list) + warp * (kPairBlocks * 64 * 2));
+    double acc_a = 0.0, acc_b = 0.0;
+
+    for (uint32_t blk0 = 0; blk0 < nblk; blk0 += kPairWarps * kPairBlocks) {
+        const uint32_t q_first = (blk0 + warp) * 32 + lane;  // this lane's vector in the warp's first block
+        // blocks of this warp in this tile (warp-uniform)
+        const uint32_t left = nblk - blk0 > warp ? (nblk - blk0 - warp + kPairWarps - 1) / kPairWarps : 0u;
+        const uint32_t kmax = opaque(min(left, (uint32_t)kPairBlocks));
+        // ---- pass A: crossing genes and mutation candidates (hashes only)
+        uint32_t total = 0;
+        {
+            if (lane == 0) S.ncand[warp] = 0;
+            __syncwarp();
+            const uint64_t first = pos + (uint64_t)(2 * q_first) * SG;
+            uint64_t p_r2 = first + a.dl_r2, p_ma = first + a.dl_mask_a, p_mb = first + a.dl_mask_b;
+            uint32_t q = q_first, goff = (warp * 64 + lane * 2), sm_b = sm_beta0;
+            for (uint32_t k = 0; k < kmax; ++k, p_r2 += STEP, p_ma += STEP, p_mb += STEP, q += kPairWarps * 32,
+                          goff += kPairWarps * 64, sm_b += kBlockBytes) {
+                const bool valid = q < nvec;
+                const bool vc = valid && pair_cross;
+                // hr = H(r2 - 0.5) = 0 <=> top bit clear
+                const bool c0 = vc & ((int)draw_top<MODE>(seed, p_r2) >= 0);
+                const bool c1 = vc & ((int)draw_top<MODE>(seed, p_r2 + SG) >= 0);
+                const unsigned b0 = __ballot_sync(0xffffffffu, c0), b1 = __ballot_sync(0xffffffffu, c1);
+                sts_f64x2(sm_b, 1.0, 1.0);
+                const uint32_t n0 = __popc(b0);
+                const uint32_t i0 = total + __popc(b0 & lt), i1 = total + n0 + __popc(b1 & lt);
+                if (c0) sts_u16(sm_list + 2 * i0, goff);
+                if (c1) sts_u16(sm_list + 2 * i1, goff + 1);
+                total += n0 + __popc(b1);
+                if (!a.mask_never) {
+                    const uint32_t ta0 = draw_top<MODE>(seed, p_ma), ta1 = draw_top<MODE>(seed, p_ma + SG);
+                    const uint32_t tb0 = draw_top<MODE>(seed, p_mb), tb1 = draw_top<MODE>(seed, p_mb + SG);
+                    if (valid && min(min(ta0, ta1), min(tb0, tb1)) <= top_thr) {  // ~ 4 pm/d of the vectors
+                        if (min(ta0, tb0) <= top_thr) {
+                            const uint32_t slot = atomicAdd(&S.ncand[warp], 1u);
+                            if (slot < (uint32_t)a.cand_cap)
+                                S.cand[warp][slot] = (unsigned short)(goff | (ta0 <= top_thr ? 0x2000u : 0u) | (tb0 <= top_thr ? 0x4000u : 0u));
+                            else
+                                S.overflow = 1;
+                        }
+                        if (min(ta1, tb1) <= top_thr) {
+                            const uint32_t slot = atomicAdd(&S.ncand[warp], 1u);
+                            if (slot < (uint32_t)a.cand_cap)
+                                S.cand[warp][slot] = (unsigned short)((goff + 1) | (ta1 <= top_thr ? 0x2000u : 0u) | (tb1 <= top_thr ? 0x4000u : 0u));
+                            else
+                                S.overflow = 1;
+                        }
+                    }
+                }
+            }
+        }
+        __syncwarp();
+        // ---- pass B: signed spread factor of the crossing genes, 32 at a time
+        {
+            const uint64_t pos_tile = pos + (uint64_t)(blk0 * 64) * SG;
+            for (uint32_t t = lane; t < total; t += 32) {
+                const uint32_t goff = lds_u16(sm_list + 2 * t);
+                const uint64_t at = pos_tile + (uint64_t)goff * SG;
+                const double mc = word_to_unit(draw_full<MODE>(seed, at));
+                const bool up = (int)draw_top<MODE>(seed, at + a.dl_r1) < 0;  // sgn(r1 - 0.5)
+                // live spread branch only (hm = H(0.5 - mc)); the other one is multiplied by exactly 0.0
+                const bool low = 0.5 - mc >= 0.0;
+                const double base = low ? 2.0 * mc : 2.0 - 2.0 * mc;
+                const double yexp = low ? a.inv_exp : -a.inv_exp;
+                // base is 0 (mc == 0) or in [2^-52, 2]; |y log base| < 2 for any eta >= 0
+                double spread;
+                if (!(base > 0.0 && a.narrow_pow) || !glibc_pow_main<true>(base, yexp, T, &spread))
+                    spread = pow_spread_slow(base, yexp);
+                sts_f64(sm_beta_tile + 8 * goff, up ? spread : -spread);
+            }
+        }
+        __syncwarp();
+        // ---- pass M: the mutation candidates of this warp (usually none)
+        {
+            const uint32_t nc = min(S.ncand[warp], (uint32_t)a.cand_cap);
+#pragma unroll 1
+            for (uint32_t t = lane; t < nc; t += 32) {
+                const uint32_t entry = S.cand[warp][t], goff = entry & 0x1fffu, j = blk0 * 64 + goff;
+                mutate_candidate<MODE>(seed, pos + a.dl_mask_a, pos + a.dl_mask_b, a.dl_mut_a - a.dl_mask_a, a.mask_thresh, a.xi,
+                                       entry, j, pa[j], pb[j], a.lower[j], a.upper[j], &S.beta[goff], &S.side[warp][t], t);
+            }
+        }
+        __syncwarp();
+        // ---- pass C: stream the rows
+        {
+            const uint32_t m1 = (uint32_t)a.m - 1;  // first tail gene (fused evaluation)
+            const double2* __restrict__ pa2 = opaque_ptr(reinterpret_cast<const double2*>(pa));
+            const double2* __restrict__ pb2 = opaque_ptr(reinterpret_cast<const double2*>(pb));
+            double2* __restrict__ oa2 = opaque_ptr(reinterpret_cast<double2*>(oa));
+            double2* __restrict__ ob2 = opaque_ptr(reinterpret_cast<double2*>(ob));
+            const double2* __restrict__ lo2 = reinterpret_cast<const double2*>(a.lower);
+            const double2* __restrict__ hi2 = reinterpret_cast<const double2*>(a.upper);
+            const uint32_t sm_side = smem_u32(S.side[warp]);
+            uint32_t q = q_first, sm_b = sm_beta0;
+#pragma unroll 2
+            for (uint32_t k = 0; k < kmax; ++k, q += kPairWarps * 32, sm_b += kBlockBytes) {
+                if (q >= nvec) break;  // only in the last block of the row
+                const double2 va = pa2[q];
+                const double2 vb = pb2[q];
+                const double2 vlo = __ldg(lo2 + q);
+                const double2 vhi = __ldg(hi2 + q);
+                const double2 vbeta = lds_f64x2(sm_b);
+                double ca0, cb0, ca1, cb1;
+                sbx_children(va.x, vb.x, vbeta.x, vlo.x, vhi.x, ca0, cb0);
+                sbx_children(va.y, vb.y, vbeta.y, vlo.y, vhi.y, ca1, cb1);
+                if (max(__double2hiint(vbeta.x), __double2hiint(vbeta.y)) >= (int)kBetaTagHi) {  // rare: parked children
+                    if (__double2hiint(vbeta.x) >= (int)kBetaTagHi) {
+                        const double2 e = lds_f64x2(sm_side + 16 * __double2loint(vbeta.x));
+                        ca0 = e.x;
+                        cb0 = e.y;
+                    }
+                    if (__double2hiint(vbeta.y) >= (int)kBetaTagHi) {
+                        const double2 e = lds_f64x2(sm_side + 16 * __double2loint(vbeta.y));
+                        ca1 = e.x;
+                        cb1 = e.y;
+                    }
+                }
+                if (EVAL != 0) {
+                    const uint32_t j0 = 2 * q;
+                    if (j0 >= m1) {
+                        acc_a += dtlz_term<EVAL>(ca0);
+                        acc_b += dtlz_term<EVAL>(cb0);
+                        acc_a += dtlz_term<EVAL>(ca1);
+                        acc_b += dtlz_term<EVAL>(cb1);
+                    } else {  // the vector holds a position gene (first block of the row only)
+                        S.pos[0][j0] = ca0;
+                        S.pos[1][j0] = cb0;
+                        if (j0 + 1 >= m1) {
+                            acc_a += dtlz_term<EVAL>(ca1);
+                            acc_b += dtlz_term<EVAL>(cb1);
+                        } else {
+                            S.pos[0][j0 + 1] = ca1;
+                            S.pos[1][j0 + 1] = cb1;
+                        }
+                    }
+                }
+                oa2[q] = make_double2(ca0, ca1);
+                ob2[q] = make_double2(cb0, cb1);
+            }
+        }
+        __syncwarp();
+    }
+
+    __syncthreads();
+    if (S.overflow) {  // a warp ran out of candidate slots: redo the pair the plain way (exact, practically never)
+        __syncthreads();
+        redo_pair<MODE, EVAL>(a, unit, *reinterpret_cast<GenericSmem*>(S.beta));
+        return;
+    }
+    if (EVAL != 0) {
+        const uint64_t f0 = a.f_row0 + (a.f_row0_dev ? (uint64_t)*a.f_row0_dev : 0);
+        const double ga = block_sum<8>(acc_a, S.red);
+        double* fa = a.f_out + (f0 + row_a) * a.m;
+        if (threadIdx.x == 0) fa[0] = ga;
+        if (threadIdx.x >= 1 && threadIdx.x < a.m) fa[threadIdx.x] = S.pos[0][threadIdx.x - 1];
+        const double gb = block_sum<8>(acc_b, S.red);
+        double* fb = a.f_out + (f0 + row_b) * a.m;
+        if (threadIdx.x == 0) fb[0] = gb;
+        if (threadIdx.x >= 1 && threadIdx.x < a.m) fb[threadIdx.x] = S.pos[1][threadIdx.x - 1];
+    }
+}
+
+template <int MODE, int EVAL>
+void launch_pairs_eval(const ReproK& k, uint64_t units, cudaStream_t s) {
+    static bool configured = false;  // per instantiation
+    if (!configured) {
+        TEMO_CUDA(cudaFuncSetAttribute(reproduce_pairs_kernel<MODE, EVAL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)sizeof(PairSmem)));
+        configured = true;
+    }
+    reproduce_pairs_kernel<MODE, EVAL><<<(unsigned)units, 256, sizeof(PairSmem), s>>>(k);
+}
+
+template <int MODE>
+void launch_pairs(const ReproK& k, uint64_t units, int eval, cudaStream_t s) {
+    switch (eval) {
+    case 0: launch_pairs_eval<MODE, 0>(k, units, s); break;
+    case kDtlz1: launch_pairs_eval<MODE, kDtlz1>(k, units, s); break;
+    case kDtlz2: launch_pairs_eval<MODE, kDtlz2>(k, units, s); break;
+    case kDtlz3: launch_pairs_eval<MODE, kDtlz3>(k, units, s); break;
+    case kDtlz4: launch_pairs_eval<MODE, kDtlz4>(k, units, s); break;
+    default: fail(1, "reproduce: fused evaluation supports DTLZ1-4 only");
+    }
+}
 template <int MODE, bool SBX, bool PM, int EVAL>
 void launch_vec(const ReproK& k, uint64_t units, int block, int vec, cudaStream_t s) {
     if (units == 0) return;
@@ -329,6 +735,22 @@ __global__ void pow_batch_kernel(const double* x, const double* y, uint64_t n, d
     const PowTables T = pow_tables(s_pow);
     for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < n; e += (uint64_t)gridDim.x * blockDim.x)
         out[e] = pow_like_host(x[e], y[e], T);
+}
+
+// TEMO_B200_GENERIC_K1=1 routes everything through the generic kernel (A/B checks of the two K1 paths)
+inline bool force_generic_kernel() {
+    static const bool v = [] { const char* e = getenv("TEMO_B200_GENERIC_K1"); return e && e[0] == '1'; }();
+    return v;
+}
+
+// TEMO_B200_K1_CAND_CAP=<n> shrinks the candidate slots of the pair kernel (0 forces its redo path; tests)
+inline int pair_cand_cap() {
+    static const int v = [] {
+        const char* e = getenv("TEMO_B200_K1_CAND_CAP");
+        const int c = e ? atoi(e) : kPairCand;
+        return c < 0 ? 0 : (c > kPairCand ? kPairCand : c);
+    }();
+    return v;
 }
 
 inline unsigned stream_grid(uint64_t total, int block) {
@@ -399,12 +821,30 @@ void launch_reproduce(const ReproArgs& a, cudaStream_t s) {
     k.f_out = a.f_out;
     k.f_row0 = a.f_row0;
     k.f_row0_dev = a.f_row0_dev;
-    const uint64_t units = a.do_sbx ? k.half + (a.n & 1) : a.n;
+    uint64_t units = a.do_sbx ? k.half + (a.n & 1) : a.n;
     const int vec = row_vec(a.d), block = row_block(a.d);
-    if (a.rng.mode == 0)
-        launch_mode<0>(k, a.do_sbx, a.do_pm, units, block, vec, a.eval_problem, s);
-    else
-        launch_mode<1>(k, a.do_sbx, a.do_pm, units, block, vec, a.eval_problem, s);
+    const auto aligned16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
+    // Full pairs of wide even rows go through the phased pair kernel when mutation candidates are rare (expected
+    // number per warp and tile <= 1); what is left (an odd last row) and every other shape through the generic one.
+    const double cand_rate = k.mask_never ? 0.0 : ((double)k.mask_top + 1.0) * 0x1.0p-21;  // P(quick reject passes)
+    const double cand_per_warp = 2.0 * (double)std::min<uint64_t>(a.d, kPairTile) / kPairWarps * cand_rate;
+    k.cand_cap = pair_cand_cap();
+    if (a.do_sbx && a.do_pm && vec == 2 && block == 256 && k.half > 0 && a.d * 8 < (1ULL << 32) && cand_per_warp <= 1.0 &&
+        aligned16(a.pool) && aligned16(a.out) && aligned16(a.lower) && aligned16(a.upper) && !force_generic_kernel()) {
+        if (a.rng.mode == 0)
+            launch_pairs<0>(k, k.half, a.eval_problem, s);
+        else
+            launch_pairs<1>(k, k.half, a.eval_problem, s);
+        TEMO_CUDA(cudaGetLastError());
+        k.unit0 = k.half;
+        units -= k.half;
+    }
+    if (units > 0) {
+        if (a.rng.mode == 0)
+            launch_mode<0>(k, a.do_sbx, a.do_pm, units, block, vec, a.eval_problem, s);
+        else
+            launch_mode<1>(k, a.do_sbx, a.do_pm, units, block, vec, a.eval_problem, s);
+    }
     TEMO_CUDA(cudaGetLastError());
     if (a.eval_problem != 0) {
         require(a.f_row0_dev == nullptr, "reproduce: device-side row offsets are not supported with fused evaluation");
