@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libtemo_b200.so")
+# TEMO_B200_LIB: developer override used to A/B differently compiled builds of the same library
+LIB_PATH = os.environ.get("TEMO_B200_LIB") or os.path.join(HERE, "libtemo_b200.so")
 
 u64 = C.c_uint64
 f64p = C.POINTER(C.c_double)
@@ -104,6 +105,7 @@ SIGNATURES = {
     "temo_b200_shard_download": (C.c_int, [_RUN, C.POINTER(C.c_uint32), u64, f64p, u64, f64p, f64p, f64p]),
     "temo_b200_pow": (C.c_int, [f64p, f64p, u64, f64p, C.c_int]),
     "temo_b200_flush_l2": (C.c_int, []),
+    "temo_b200_set_option": (C.c_int, [C.c_char_p, C.c_long]),
 }
 
 _lib = None

@@ -62,6 +62,12 @@ def init(device: int = 0) -> None:
     _call(_lib.load().temo_b200_init, device)
 
 
+def set_option(name: str, value: int) -> None:
+    """Path-selection knobs for tests / A-B runs (results are identical on every path): "k1_generic",
+    "k1_bound_arrays", "k1_cand_cap" (see include/temo_b200.h)."""
+    _call(_lib.load().temo_b200_set_option, name.encode(), int(value))
+
+
 def pow_like_host(x, y, on_device: bool = True) -> np.ndarray:
     """Self-test hook: elementwise pow through the libm-exact implementation (device or host twin)."""
     x, y = _t(x).reshape(-1), _t(y).reshape(-1)

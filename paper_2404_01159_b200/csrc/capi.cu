@@ -118,6 +118,7 @@ void host_operator(bool do_shuffle, bool do_sbx, bool do_pm, const double* x, ui
     a.ga = ga_of(ga);
     a.lower = dlo.p;
     a.upper = dhi.p;
+    a.seg = find_bound_segments(lower, upper, d);
     a.do_sbx = do_sbx;
     a.do_pm = do_pm;
     if (do_sbx) {
@@ -571,6 +572,10 @@ int temo_b200_pow(const double* x, const double* y, uint64_t n, double* out, int
         dout.to_host(out, s);
         TEMO_CUDA(cudaStreamSynchronize(s));
     });
+}
+
+int temo_b200_set_option(const char* name, long value) {
+    return guarded([&] { require(set_k1_option(name, value), "set_option: unknown option"); });
 }
 
 int temo_b200_flush_l2(void) {

@@ -192,6 +192,71 @@ __host__ __device__ inline bool glibc_pow_main(double x, double y, const PowTabl
     return true;
 }
 
+// Branch-free form of the NARROW path for callers that evaluate several independent powers at once (the
+// instruction streams interleave). Same operations, same bits; returns false when the result is not valid
+// (|y log x| >= 512: never for the SBX spread factor) and the caller must fall back to the general routine.
+// x must be positive and normal.
+__host__ __device__ __forceinline__ bool glibc_pow_narrow_flat(double x, double y, const PowTables& T, double* out) {
+    const unsigned long long ix = TEMO_AS_U64(x);
+    const unsigned long long tmp = ix - 0x3fe6955500000000ULL;
+    const int i = (int)((tmp >> 45) & 127);
+    const int k = (int)((long long)tmp >> 52);
+    const double z = TEMO_AS_DOUBLE(ix - (tmp & 0xfff0000000000000ULL));
+    const double kd = (double)k;
+    const double ln2hi = TEMO_POW_K(0), ln2lo = TEMO_POW_K(1);
+    const double A0 = TEMO_POW_K(2), A1 = TEMO_POW_K(3), A2 = TEMO_POW_K(4), A3 = TEMO_POW_K(5), A4 = TEMO_POW_K(6),
+                 A5 = TEMO_POW_K(7), A6 = TEMO_POW_K(8);
+    const double t1 = TEMO_FMA(kd, ln2hi, T.logc[i]);
+    const double lo1 = TEMO_FMA(kd, ln2lo, T.logctail[i]);
+    const double r = TEMO_FMA(z, T.invc[i], -1.0);
+    const double ar = TEMO_MUL(r, A0);
+    const double p12 = TEMO_FMA(r, A2, A1);
+    const double p34 = TEMO_FMA(r, A4, A3);
+    const double t2 = TEMO_ADD(r, t1);
+    const double lo2 = TEMO_ADD(TEMO_ADD(t1, -t2), r);
+    const double ar2 = TEMO_MUL(r, ar);
+    const double ar3 = TEMO_MUL(r, ar2);
+    const double lo3 = TEMO_FMA(ar, r, -ar2);
+    const double hi = TEMO_ADD(t2, ar2);
+    const double p56 = TEMO_FMA(r, A6, A5);
+    const double lo4 = TEMO_ADD(TEMO_ADD(t2, -hi), ar2);
+    const double q = TEMO_FMA(ar2, TEMO_FMA(p56, ar2, p34), p12);
+    double lo = TEMO_ADD(lo1, lo2);
+    lo = TEMO_ADD(lo, lo3);
+    lo = TEMO_ADD(lo, lo4);
+    lo = TEMO_FMA(ar3, q, lo);
+    const double lg = TEMO_ADD(hi, lo);
+    const double lgtail = TEMO_ADD(TEMO_ADD(hi, -lg), lo);
+    const double ehi = TEMO_MUL(y, lg);
+    const double elo = TEMO_FMA(y, lgtail, TEMO_FMA(lg, y, -ehi));
+    const unsigned abstop = (unsigned)(TEMO_AS_U64(ehi) >> 52) & 0x7ffu;
+    const bool tiny = abstop < 0x3c9u;              // |y log x| < 2^-54: the result rounds from 1 + ehi
+    const bool valid = tiny || abstop - 0x3c9u <= 0x3eu;
+    const double invln2N = TEMO_POW_K(9), shift = TEMO_POW_K(10), negln2hiN = TEMO_POW_K(11),
+                 negln2loN = TEMO_POW_K(12), C2 = TEMO_POW_K(13), C3 = TEMO_POW_K(14), C4 = TEMO_POW_K(15),
+                 C5 = TEMO_POW_K(16);
+    const double kds = TEMO_FMA(ehi, invln2N, shift);
+    const unsigned long long ki = TEMO_AS_U64(kds);
+    const double kdd = TEMO_ADD(kds, -shift);
+    double rr = TEMO_FMA(kdd, negln2hiN, ehi);
+    rr = TEMO_FMA(kdd, negln2loN, rr);
+    rr = TEMO_ADD(elo, rr);
+    const unsigned idx = 2u * (unsigned)(ki & 127);
+    const unsigned long long sbits = T.exptab[idx + 1] + (ki << 45);
+    const double tail = TEMO_AS_DOUBLE(T.exptab[idx]);
+    const double c23 = TEMO_FMA(rr, C3, C2);
+    const double tr = TEMO_ADD(rr, tail);
+    const double r2 = TEMO_MUL(rr, rr);
+    const double c45 = TEMO_FMA(rr, C5, C4);
+    const double acc = TEMO_FMA(c23, r2, tr);
+    const double r4 = TEMO_MUL(r2, r2);
+    const double tmpv = TEMO_FMA(c45, r4, acc);
+    const double scale = TEMO_AS_DOUBLE(sbits);
+    const double res = TEMO_FMA(tmpv, scale, scale);
+    *out = tiny ? TEMO_ADD(ehi, 1.0) : res;
+    return valid;
+}
+
 // Host twin (used by the C-ABI self-test hook): tables straight from the generated header.
 inline double glibc_pow_host(double x, double y) {
     static const unsigned long long invc[128] = TEMO_POW_INVC_INIT;

@@ -139,4 +139,27 @@ Context& ctx() {
     return g_ctx;
 }
 
+// Bounds that are constant on [0, split) and on [split, d) (bit patterns compared, so -0.0 != 0.0 and NaNs
+// never match: anything unusual simply stays on the array path).
+BoundSegments find_bound_segments(const double* lower, const double* upper, uint64_t d) {
+    BoundSegments g;
+    if (!lower || !upper || d == 0) return g;
+    const auto same = [](double x, double y) { return std::memcmp(&x, &y, sizeof(double)) == 0; };
+    uint64_t split = d;
+    for (uint64_t j = 1; j < d; ++j)
+        if (!same(lower[j], lower[0]) || !same(upper[j], upper[0])) {
+            split = j;
+            break;
+        }
+    for (uint64_t j = split; j < d; ++j)
+        if (!same(lower[j], lower[split]) || !same(upper[j], upper[split])) return g;
+    g.valid = true;
+    g.split = split;
+    g.lo[0] = lower[0];
+    g.hi[0] = upper[0];
+    g.lo[1] = split < d ? lower[split] : lower[0];
+    g.hi[1] = split < d ? upper[split] : upper[0];
+    return g;
+}
+
 }  // namespace temo_b200

@@ -36,6 +36,16 @@ struct GaParams {
     double pc = 1.0, eta = 20.0, pm = 1.0, xi = 20.0;  // operators.hpp:22-27
 };
 
+// Optional piecewise-constant description of the box bounds: genes [0, split) have (lo[0], hi[0]), genes
+// [split, d) have (lo[1], hi[1]) (DTLZ: one segment; LSMOP: two). Lets K1 keep the bounds in registers instead
+// of loading two arrays per gene; the arrays stay authoritative (valid == false: arrays only).
+struct BoundSegments {
+    bool valid = false;
+    uint64_t split = 0;
+    double lo[2] = {0.0, 0.0}, hi[2] = {0.0, 0.0};
+};
+BoundSegments find_bound_segments(const double* lower, const double* upper, uint64_t d);  // host arrays
+
 // ---- K1: reproduction ---------------------------------------------------------------------
 struct ReproArgs {
     const double* pool = nullptr;   // parent storage, row stride d
@@ -49,6 +59,7 @@ struct ReproArgs {
     GaParams ga;
     const double* lower = nullptr;
     const double* upper = nullptr;
+    BoundSegments seg;  // optional: same bounds as the arrays, piecewise constant
     bool do_sbx = true, do_pm = true;
     // fused evaluation of the children (0 = off): problem id, m, output rows f_out[(f_row0+i)*m..]
     int eval_problem = 0;
@@ -61,6 +72,8 @@ struct ReproArgs {
     uint64_t global_n = 0, global_unit0 = 0;
 };
 void launch_reproduce(const ReproArgs& a, cudaStream_t s);
+// K1 path-selection knobs ("k1_generic", "k1_bound_arrays", "k1_cand_cap"); false for an unknown name.
+bool set_k1_option(const char* name, long value);
 
 // random_reproduce (operators.hpp:287-296) and uniform_tensor (rng.hpp:55-66).
 void launch_random_reproduce(double* out, const uint32_t* dst, uint64_t n, uint64_t d, Rng rng,

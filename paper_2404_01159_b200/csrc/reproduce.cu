@@ -18,6 +18,7 @@
 // exact 0.0 are skipped (verified bit-identical); the only inexact pieces are
 // CUDA's pow (<= 2 ulp) on crossed/mutated genes.
 #include <algorithm>
+#include <cstddef>
 #include <cstdlib>
 
 #include "glibc_pow_dev.cuh"
@@ -50,6 +51,8 @@ struct ReproK {
     int narrow_pow;  // 1/(eta+1) in [2^-10, 1]: the SBX pow stays on the common path of the libm algorithm
     const double* lower;
     const double* upper;
+    uint32_t seg_split;          // pair kernel, SEG variant: genes < seg_split have bounds [0], the others [1]
+    double seg_lo[2], seg_hi[2];
     uint64_t m;
     double* f_out;
     uint64_t f_row0;
@@ -292,12 +295,13 @@ __global__ void __launch_bounds__(256, TEMO_REPRO_MIN_BLOCKS) reproduce_kernel(c
 
 
 // ------------------------------------------------------------------------------------------------
-// Fast path: SBX + PM over full mating pairs, 128-bit vectors (d even), 256 threads per pair.
+// Fast path: SBX + PM over full mating pairs of wide even rows — persistent teams of eight warps.
 //
-// Same arithmetic, same draws, same thread->gene map (warp w owns the 64-gene blocks w, w+8, ... of the
-// row; lane l the vector l of a block) as reproduce_unit above, reorganised so that the expensive parts
-// run dense and branch-free. Every warp walks its blocks of a row tile in four passes of its own (no CTA
-// barrier between them, so the warps of an SM drift apart and their passes overlap):
+// Same arithmetic, same draws, same thread->gene map (warp w owns the 64-gene blocks w, w+8, ... of the row,
+// lane l the vector l of a block) and the same reduction order as reproduce_unit above, reorganised so that
+// the expensive parts run dense and branch-free and no warp ever waits for another one:
+// a CTA (team) loops over pairs; inside a pair each warp works through its own blocks, one row tile of
+// 80 blocks (10 per warp) at a time, in four passes:
 //   A  hashes only. hr = H(r2 - 0.5) for every gene (operators.hpp:90-91): the crossing genes (about half)
 //      are appended to the warp's list in shared memory and beta = 1 is planted for everybody. The quick
 //      reject of the mutation mask H(pm/d - r4) (operators.hpp:136) for both children: the few genes that
@@ -309,32 +313,56 @@ __global__ void __launch_bounds__(256, TEMO_REPRO_MIN_BLOCKS) reproduce_kernel(c
 //      replaced by a tagged NaN pointing at it.
 //   C  the streaming pass: 128-bit loads of both parents, blend + clamp (operators.hpp:92-95), a tagged beta
 //      swaps in the parked children, fused objective partial sums, 128-bit stores of both children.
-// The parent rows are pulled into L2 by the bulk-copy engine (cp.async.bulk.prefetch.L2, SASS UBLKPF) when
-// the CTA starts, so HBM streams while passes A and B compute and pass C reads L2 hits.
-// A warp with more than kPairCand mutation candidates in one tile (probability ~1e-15 at pm = 1) raises a
-// flag and the CTA redoes the pair through reproduce_unit: the result is exact in every case.
-constexpr int kPairWarps = 8;
-constexpr int kPairBlocks = 10;                              // 64-gene blocks per warp and tile
-constexpr int kPairTile = kPairWarps * kPairBlocks * 64;     // genes per tile (5120)
-constexpr int kPairCand = 16;                                // mutation candidates per warp and tile
+// There is no CTA barrier after start-up. A warp that finishes its share of a pair leaves its partial sums in
+// one of kPairSlots per-pair slots and moves on to the next pair; the last warp to arrive adds the eight
+// partials in ascending warp order (the order of block_sum) and writes the objective rows. The warps of an SM
+// therefore drift apart and their compute and memory passes overlap. At the start of a tile every warp asks for
+// its own parent blocks to be pulled into L2 (prefetch.global.L2; about half of those hints are honoured under
+// load), and pass C keeps the parents of the next two blocks in flight in registers.
+// A tile with more than kPairCand mutation candidates (probability ~1e-15 at pm = 1) is recomputed by
+// tile_plain(), the literal per-gene formulation: the result is exact in every case.
+constexpr int kVirtWarps = 8;                                // warps of the canonical row mapping = warps of a team
+#ifndef TEMO_PAIR_BLOCKS
+#define TEMO_PAIR_BLOCKS 10
+#endif
+constexpr int kPairBlocks = TEMO_PAIR_BLOCKS;                // 64-gene blocks per warp and tile
+constexpr int kTileGenes = kPairBlocks * 64;                 // genes of one warp tile
+constexpr int kPairCand = 8;                                 // mutation candidates per warp tile
+constexpr int kPairSlots = 4;                                // pairs a team can have in flight
 constexpr uint32_t kBetaTagHi = 0x7ff80000u;                 // high word of the tagged NaN
+#ifndef TEMO_PAIR_MIN_BLOCKS
+#define TEMO_PAIR_MIN_BLOCKS 3                               // teams per SM
+#endif
 
+
+// Everything a warp needs to know about its current pair (kept in shared memory, not in registers).
+struct PairCtx {
+    const double* pa;
+    const double* pb;
+    double* oa;
+    double* ob;
+    uint64_t pos;    // stream position of (Mc block, gene 0) of this pair
+    uint32_t cross;  // pair-level crossover switch hc = H(r3 - pc) == 0 (operators.hpp:82)
+    uint32_t pad;
+};
+struct WarpSmem {
+    double beta[kTileGenes];
+    unsigned short list[kTileGenes];
+    double2 side[kPairCand];  // final children {a, b} of a candidate gene
+    PairCtx ctx;
+    unsigned short cand[kPairCand];
+};
+struct PairSlot {
+    double part[2][kVirtWarps];  // per-warp totals of the two children
+    double pos[2][kMaxObj];      // position genes of the two children
+    uint32_t arrived;            // warps that have delivered their partials
+    uint32_t done;               // pairs completed through this slot
+};
 struct PairSmem {
     PowSmem pow;
-    double beta[kPairTile];
-    unsigned short list[kPairTile];
-    double2 side[kPairWarps][kPairCand];  // final children {a, b} of a candidate gene
-    unsigned short cand[kPairWarps][kPairCand];
-    uint32_t ncand[kPairWarps];
-    uint32_t overflow;
-    double red[8];
-    double pos[2][kMaxObj];
+    WarpSmem w[kVirtWarps];
+    PairSlot slot[kPairSlots];
 };
-static_assert(sizeof(GenericSmem) <= sizeof(double) * kPairTile, "redo path aliases the beta tile");
-
-__device__ __forceinline__ void l2_prefetch_bulk(const void* p, uint32_t bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
 
 // mix64 (rng.hpp:23-30) on 32-bit halves; a 64-bit product costs one wide multiply and two multiply-adds.
 struct Hash64 {
@@ -382,7 +410,7 @@ __device__ __forceinline__ uint64_t draw_full(uint64_t seed, uint64_t at) {
 }
 
 // SBX blend of one gene (operators.hpp:92-95 as written); beta = 1 returns the parents through the same
-// arithmetic as on the CPU. Shared by passes M and C so that both produce the same bits.
+// arithmetic as on the CPU. Shared by every pass so that all of them produce the same bits.
 __device__ __forceinline__ void sbx_children(double xa, double xb, double beta, double lo, double hi, double& ca,
                                              double& cb) {
     const double p = 1.0 + beta, m = 1.0 - beta;
@@ -393,36 +421,48 @@ __device__ __forceinline__ void sbx_children(double xa, double xb, double beta, 
 // pow for the spread factor outside the narrow fast path (never taken for ordinary eta)
 __device__ __noinline__ double pow_spread_slow(double x, double y) { return pow_like_host(x, y, pow_tables_global()); }
 
-// Pass M for one candidate gene (rare, out of line): exact mask tests, live range, mutation of either child.
+// Signed SBX spread factor of a crossing gene: Mc at stream position `at`, R1 at `at + dl_r1` (operators.hpp:85-89).
+// Branch-free on the common path so that several genes can be evaluated side by side.
+struct SpreadIn {
+    double base, yexp;
+    bool up;
+};
 template <int MODE>
-__device__ __noinline__ void mutate_candidate(uint64_t seed, uint64_t pos_ma, uint64_t pos_mb, uint64_t d_mut, uint64_t thresh,
-                                              double xi, uint32_t entry, uint32_t j, double xa, double xb, double lo, double hi,
-                                              double* beta_slot, double2* side_slot, uint32_t slot) {
-    constexpr uint64_t SG = MODE == 0 ? kGolden : 1ULL;
+__device__ __forceinline__ SpreadIn spread_inputs(uint64_t seed, uint64_t at, uint64_t dl_r1, double inv_exp) {
+    SpreadIn s;
+    const double mc = word_to_unit(draw_full<MODE>(seed, at));
+    s.up = (int)draw_top<MODE>(seed, at + dl_r1) < 0;  // sgn(r1 - 0.5)
+    // live spread branch only (hm = H(0.5 - mc)); the other one is multiplied by exactly 0.0
+    const bool low = 0.5 - mc >= 0.0;
+    s.base = low ? 2.0 * mc : 2.0 - 2.0 * mc;  // 0 (mc == 0) or in [2^-52, 2]; |y log base| < 2 for any eta >= 0
+    s.yexp = low ? inv_exp : -inv_exp;
+    return s;
+}
+template <int MODE>
+__device__ __forceinline__ double signed_spread(uint64_t seed, uint64_t at, uint64_t dl_r1, double inv_exp, int narrow,
+                                                const PowTables& T) {
+    const SpreadIn s = spread_inputs<MODE>(seed, at, dl_r1, inv_exp);
+    double spread;
+    const bool fast = s.base > 0.0 && narrow;
+    if (!glibc_pow_narrow_flat(fast ? s.base : 1.0, s.yexp, T, &spread) || !fast) spread = pow_spread_slow(s.base, s.yexp);
+    return s.up ? spread : -spread;
+}
+
+// Both children of one gene with the mutation applied where the full 53-bit mask test selects it
+// (operators.hpp:133-145). hit_a / hit_b: the quick reject let that child through.
+template <int MODE>
+__device__ __noinline__ double2 mutated_children(uint64_t seed, uint64_t at_ma, uint64_t at_mb, uint64_t d_mut, uint64_t thresh,
+                                                 double xi, bool hit_a, bool hit_b, double xa, double xb, double beta,
+                                                 double lo, double hi) {
     double ca, cb;
-    sbx_children(xa, xb, *beta_slot, lo, hi, ca, cb);
+    sbx_children(xa, xb, beta, lo, hi, ca, cb);
     if (!(hi - lo <= 0.0)) {  // operators.hpp:137
-        if (entry & 0x2000u) {
-            const uint64_t at = pos_ma + (uint64_t)j * SG;
-            ca = mutate_if_selected(ca, draw_full<MODE>(seed, at), draw_full<MODE>(seed, at + d_mut), thresh, lo, hi, xi);
-        }
-        if (entry & 0x4000u) {
-            const uint64_t at = pos_mb + (uint64_t)j * SG;
-            cb = mutate_if_selected(cb, draw_full<MODE>(seed, at), draw_full<MODE>(seed, at + d_mut), thresh, lo, hi, xi);
-        }
+        if (hit_a) ca = mutate_if_selected(ca, draw_full<MODE>(seed, at_ma), draw_full<MODE>(seed, at_ma + d_mut), thresh, lo, hi, xi);
+        if (hit_b) cb = mutate_if_selected(cb, draw_full<MODE>(seed, at_mb), draw_full<MODE>(seed, at_mb + d_mut), thresh, lo, hi, xi);
     }
-    *side_slot = make_double2(ca, cb);
-    *beta_slot = __hiloint2double((int)kBetaTagHi, (int)slot);
+    return make_double2(ca, cb);
 }
 
-template <int MODE, int EVAL>
-__device__ __noinline__ void redo_pair(const ReproK a, uint64_t unit, GenericSmem& G) {
-    reproduce_unit<MODE, true, true, EVAL, 2>(a, unit, G);
-}
-
-#ifndef TEMO_PAIR_MIN_BLOCKS
-#define TEMO_PAIR_MIN_BLOCKS 3
-#endif
 // Shared-memory accesses of the pair kernel go through explicit 32-bit shared addresses, and the per-thread
 // constants are made opaque to the compiler once: both keep ptxas from re-deriving them (special-register reads,
 // window-base arithmetic, 64-bit multiplies) inside the hot loops.
@@ -450,233 +490,367 @@ __device__ __forceinline__ double2 lds_f64x2(uint32_t addr) {
     asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
     return v;
 }
+__device__ __forceinline__ double lds_f64(uint32_t addr) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+    return v;
+}
 __device__ __forceinline__ uint32_t lds_u16(uint32_t addr) {
     unsigned short v;
     asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr));
     return v;
 }
+__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 
+template <int EVAL>
+__device__ __forceinline__ void accumulate_vector(uint32_t j0, uint32_t m1, double ca0, double cb0, double ca1, double cb1,
+                                                  double& acc_a, double& acc_b, double (*pos)[kMaxObj]) {
+    if (EVAL == 0) return;
+    if (j0 >= m1) {
+        acc_a += dtlz_term<EVAL>(ca0);
+        acc_b += dtlz_term<EVAL>(cb0);
+        acc_a += dtlz_term<EVAL>(ca1);
+        acc_b += dtlz_term<EVAL>(cb1);
+    } else {  // the vector holds a position gene (first block of the row only)
+        pos[0][j0] = ca0;
+        pos[1][j0] = cb0;
+        if (j0 + 1 >= m1) {
+            acc_a += dtlz_term<EVAL>(ca1);
+            acc_b += dtlz_term<EVAL>(cb1);
+        } else {
+            pos[0][j0 + 1] = ca1;
+            pos[1][j0 + 1] = cb1;
+        }
+    }
+}
+
+// The literal per-gene formulation of one warp tile (blocks v + 8k of the row tile starting at blk0): used when
+// the candidate slots of the phased passes overflow. Same bits, same accumulation order.
 template <int MODE, int EVAL>
-__global__ void __launch_bounds__(256, TEMO_PAIR_MIN_BLOCKS) reproduce_pairs_kernel(const ReproK a) {
+__device__ __noinline__ void tile_plain(const ReproK& a, uint32_t blk0, uint32_t v, uint32_t kmax, double* acc, WarpSmem& W,
+                                        double (*pos)[kMaxObj]) {
+    const PairCtx c = W.ctx;
+    constexpr uint64_t SG = MODE == 0 ? kGolden : 1ULL;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t nvec = (uint32_t)(a.d >> 1), m1 = (uint32_t)a.m - 1;
+    const uint32_t top_thr = a.mask_never ? 0u : ((a.mask_top << 11) | 0x7ffu);
+    const PowTables T = pow_tables_global();
+    double acc_a = acc[0], acc_b = acc[1];
+    for (uint32_t k = 0; k < kmax; ++k) {
+        const uint32_t q = (blk0 + v + k * kVirtWarps) * 32 + lane;
+        if (q >= nvec) break;
+        double xa[2], xb[2], lo[2], hi[2], ca[2], cb[2];
+        const double2 va = reinterpret_cast<const double2*>(c.pa)[q], vb = reinterpret_cast<const double2*>(c.pb)[q];
+        const double2 vlo = reinterpret_cast<const double2*>(a.lower)[q], vhi = reinterpret_cast<const double2*>(a.upper)[q];
+        xa[0] = va.x, xa[1] = va.y, xb[0] = vb.x, xb[1] = vb.y, lo[0] = vlo.x, lo[1] = vlo.y, hi[0] = vhi.x, hi[1] = vhi.y;
+        for (int g = 0; g < 2; ++g) {
+            const uint64_t at = c.pos + (uint64_t)(2 * q + g) * SG;
+            double beta = 1.0;
+            if (c.cross && (int)draw_top<MODE>(a.rng.seed, at + a.dl_r2) >= 0)
+                beta = signed_spread<MODE>(a.rng.seed, at, a.dl_r1, a.inv_exp, a.narrow_pow, T);
+            const bool hit_a = !a.mask_never && draw_top<MODE>(a.rng.seed, at + a.dl_mask_a) <= top_thr;
+            const bool hit_b = !a.mask_never && draw_top<MODE>(a.rng.seed, at + a.dl_mask_b) <= top_thr;
+            const double2 ch = mutated_children<MODE>(a.rng.seed, at + a.dl_mask_a, at + a.dl_mask_b, a.dl_mut_a - a.dl_mask_a,
+                                                      a.mask_thresh, a.xi, hit_a, hit_b, xa[g], xb[g], beta, lo[g], hi[g]);
+            ca[g] = ch.x, cb[g] = ch.y;
+        }
+        accumulate_vector<EVAL>(2 * q, m1, ca[0], cb[0], ca[1], cb[1], acc_a, acc_b, pos);
+        reinterpret_cast<double2*>(c.oa)[q] = make_double2(ca[0], ca[1]);
+        reinterpret_cast<double2*>(c.ob)[q] = make_double2(cb[0], cb[1]);
+    }
+    acc[0] = acc_a, acc[1] = acc_b;
+}
+
+template <int MODE, int EVAL, bool SEG>
+__global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reproduce_pairs_kernel(const __grid_constant__ ReproK a) {
     extern __shared__ __align__(16) unsigned char pair_smem_raw[];
     PairSmem& S = *reinterpret_cast<PairSmem*>(pair_smem_raw);
-    constexpr uint64_t SG = MODE == 0 ? kGolden : 1ULL;  // stream distance of neighbouring genes
-    constexpr uint64_t STEP = SG * (uint64_t)(kPairWarps * 64);  // ... of a lane's consecutive blocks
-    constexpr uint32_t kBlockBytes = kPairWarps * 64 * 8;  // beta-tile distance of a lane's consecutive blocks
-    const uint32_t lane = opaque(threadIdx.x & 31), warp = opaque(threadIdx.x >> 5);
+    constexpr uint64_t SG = MODE == 0 ? kGolden : 1ULL;            // stream distance of neighbouring genes
+    constexpr uint64_t STEP = SG * (uint64_t)(kVirtWarps * 64);    // ... of a lane's consecutive blocks
+    constexpr uint32_t kOffList = offsetof(WarpSmem, list), kOffSide = offsetof(WarpSmem, side);
+    const uint32_t lane = opaque(threadIdx.x & 31), v = opaque(threadIdx.x >> 5);
+    WarpSmem& W = S.w[v];
 
-    const uint64_t unit = a.unit0 + blockIdx.x;  // < a.half: always a full pair
-    const uint64_t row_a = unit, row_b = a.half + unit;
-    const double* pa = a.pool + (a.src ? (uint64_t)a.src[row_a] : row_a) * a.d;
-    const double* pb = a.pool + (a.src ? (uint64_t)a.src[row_b] : row_b) * a.d;
-    double* oa = a.out + (a.dst ? (uint64_t)a.dst[row_a] : row_a) * a.d;
-    double* ob = a.out + (a.dst ? (uint64_t)a.dst[row_b] : row_b) * a.d;
-    if (threadIdx.x == 0) {
-        l2_prefetch_bulk(pa, (uint32_t)(a.d * 8));
-        l2_prefetch_bulk(pb, (uint32_t)(a.d * 8));
-        S.overflow = 0;
-    }
     pow_smem_load(S.pow);
-    __syncthreads();
+    if (threadIdx.x < kPairSlots) {
+        S.slot[threadIdx.x].arrived = 0;
+        S.slot[threadIdx.x].done = 0;
+    }
+    __syncthreads();  // the only CTA barrier: from here on every warp is on its own
     const PowTables T = pow_tables(S.pow);
 
-    const uint64_t g_unit = a.g_unit0 + unit;
     const uint64_t seed = a.rng.seed;
-    const uint64_t pos = a.s_base + g_unit * a.s_row;  // Mc block position of gene 0 of this pair
-    const bool pair_cross = !(word_to_unit(draw_word<MODE>(a.rng, a.c_r3 + g_unit)) - a.pc >= 0.0);  // operators.hpp:82
-
     const uint32_t nvec = (uint32_t)(a.d >> 1);
     const uint32_t nblk = (nvec + 31) >> 5;  // 64-gene blocks in a row
     const uint32_t lt = opaque((1u << lane) - 1u);
     const uint32_t top_thr = a.mask_never ? 0u : ((a.mask_top << 11) | 0x7ffu);  // (top >> 11) <= mask_top
-    // this thread's slots: its vector of the warp's first block in the beta tile, the warp's crossing list
-    const uint32_t sm_beta0 = opaque(smem_u32(S.beta) + (warp * 64 + lane * 2) * 8);
-    const uint32_t sm_beta_tile = opaque(smem_u32(S.beta));
-    const uint32_t sm_list = opaque(smem_u32(S.list) + warp * (kPairBlocks * 64 * 2));
-    double acc_a = 0.0, acc_b = 0.0;
+    const uint32_t sm_w = opaque(smem_u32(&W)), sm_lane = opaque(smem_u32(&W) + lane * 16);  // beta tile is first in WarpSmem
 
-    for (uint32_t blk0 = 0; blk0 < nblk; blk0 += kPairWarps * kPairBlocks) {
-        const uint32_t q_first = (blk0 + warp) * 32 + lane;  // this lane's vector in the warp's first block
-        // blocks of this warp in this tile (warp-uniform)
-        const uint32_t left = nblk - blk0 > warp ? (nblk - blk0 - warp + kPairWarps - 1) / kPairWarps : 0u;
-        const uint32_t kmax = opaque(min(left, (uint32_t)kPairBlocks));
-        // ---- pass A: crossing genes and mutation candidates (hashes only)
-        uint32_t total = 0;
-        {
-            if (lane == 0) S.ncand[warp] = 0;
+    uint32_t turn = 0;   // pairs this team has started
+    for (uint64_t unit = a.unit0 + blockIdx.x; unit < a.half; unit += gridDim.x, ++turn) {
+        PairSlot& slot = S.slot[turn % kPairSlots];
+        if (lane == 0) {
+            const uint64_t row_a = unit, row_b = a.half + unit, g_unit = a.g_unit0 + unit;
+            W.ctx.pa = a.pool + (a.src ? (uint64_t)a.src[row_a] : row_a) * a.d;
+            W.ctx.pb = a.pool + (a.src ? (uint64_t)a.src[row_b] : row_b) * a.d;
+            W.ctx.oa = a.out + (a.dst ? (uint64_t)a.dst[row_a] : row_a) * a.d;
+            W.ctx.ob = a.out + (a.dst ? (uint64_t)a.dst[row_b] : row_b) * a.d;
+            W.ctx.pos = a.s_base + g_unit * a.s_row;
+            W.ctx.cross = !(word_to_unit(draw_word<MODE>(a.rng, a.c_r3 + g_unit)) - a.pc >= 0.0) ? 1u : 0u;
+            // the slot is free once the pair that used it kPairSlots turns ago has been written out
+            if (EVAL != 0) {
+                while (*reinterpret_cast<volatile uint32_t*>(&slot.done) < turn / kPairSlots) __nanosleep(200);
+            }
+        }
+        __syncwarp();
+
+        double acc_a = 0.0, acc_b = 0.0;
+        for (uint32_t blk0 = 0; blk0 < nblk; blk0 += kVirtWarps * kPairBlocks) {
+            // blocks v, v + 8, ... of this row tile (warp-uniform count)
+            const uint32_t left = nblk - blk0 > v ? (nblk - blk0 - v + kVirtWarps - 1) / kVirtWarps : 0u;
+            const uint32_t kmax = opaque(min(left, (uint32_t)kPairBlocks));
+            if (kmax == 0) break;
+            const uint32_t q_first = (blk0 + v) * 32 + lane;  // this lane's vector in the tile's first block
+            const uint64_t pos = W.ctx.pos;
+            {   // this warp's parent blocks of this tile into L2 (they are read in pass C)
+                const uint32_t kk = lane & 15, blk = blk0 + v + kk * kVirtWarps;
+                if (kk < kmax && blk < nblk) {
+                    const char* p = reinterpret_cast<const char*>(lane < 16 ? W.ctx.pa : W.ctx.pb) + (uint64_t)blk * 512;
+#pragma unroll
+                    for (int o = 0; o < 512; o += 128) prefetch_l2(p + o);
+                }
+            }
+            // ---- pass A: crossing genes and mutation candidates (hashes only)
+            uint32_t total = 0, ncand = 0;
+            {
+                const bool cross = W.ctx.cross != 0;
+                const uint64_t first = pos + (uint64_t)(2 * q_first) * SG;
+                uint64_t p_r2 = first + a.dl_r2, p_ma = first + a.dl_mask_a, p_mb = first + a.dl_mask_b;
+                uint32_t q = q_first, e = lane * 2, sm_b = sm_lane;
+                for (uint32_t k = 0; k < kmax; ++k, p_r2 += STEP, p_ma += STEP, p_mb += STEP, q += kVirtWarps * 32, e += 64, sm_b += 512) {
+                    const bool valid = q < nvec;
+                    const bool vc = valid && cross;
+                    // hr = H(r2 - 0.5) = 0 <=> top bit clear
+                    const bool c0 = vc & ((int)draw_top<MODE>(seed, p_r2) >= 0);
+                    const bool c1 = vc & ((int)draw_top<MODE>(seed, p_r2 + SG) >= 0);
+                    const unsigned b0 = __ballot_sync(0xffffffffu, c0), b1 = __ballot_sync(0xffffffffu, c1);
+                    sts_f64x2(sm_b, 1.0, 1.0);
+                    const uint32_t n0 = __popc(b0);
+                    const uint32_t i0 = total + __popc(b0 & lt), i1 = total + n0 + __popc(b1 & lt);
+                    if (c0) sts_u16(sm_w + kOffList + 2 * i0, e);
+                    if (c1) sts_u16(sm_w + kOffList + 2 * i1, e + 1);
+                    total += n0 + __popc(b1);
+                    if (!a.mask_never) {
+                        const uint32_t ta0 = draw_top<MODE>(seed, p_ma), ta1 = draw_top<MODE>(seed, p_ma + SG);
+                        const uint32_t tb0 = draw_top<MODE>(seed, p_mb), tb1 = draw_top<MODE>(seed, p_mb + SG);
+                        const bool hit = valid && min(min(ta0, ta1), min(tb0, tb1)) <= top_thr;
+                        if (__any_sync(0xffffffffu, hit)) {  // ~ 128 pm/d of the blocks
+                            const bool h0 = hit && min(ta0, tb0) <= top_thr, h1 = hit && min(ta1, tb1) <= top_thr;
+                            const unsigned m0 = __ballot_sync(0xffffffffu, h0), mm1 = __ballot_sync(0xffffffffu, h1);
+                            const uint32_t s0 = ncand + __popc(m0 & lt), s1 = ncand + __popc(m0) + __popc(mm1 & lt);
+                            if (h0 && s0 < (uint32_t)a.cand_cap)
+                                W.cand[s0] = (unsigned short)(e | (ta0 <= top_thr ? 0x2000u : 0u) | (tb0 <= top_thr ? 0x4000u : 0u));
+                            if (h1 && s1 < (uint32_t)a.cand_cap)
+                                W.cand[s1] = (unsigned short)((e + 1) | (ta1 <= top_thr ? 0x2000u : 0u) | (tb1 <= top_thr ? 0x4000u : 0u));
+                            ncand += __popc(m0) + __popc(mm1);
+                        }
+                    }
+                }
+            }
             __syncwarp();
-            const uint64_t first = pos + (uint64_t)(2 * q_first) * SG;
-            uint64_t p_r2 = first + a.dl_r2, p_ma = first + a.dl_mask_a, p_mb = first + a.dl_mask_b;
-            uint32_t q = q_first, goff = (warp * 64 + lane * 2), sm_b = sm_beta0;
-            for (uint32_t k = 0; k < kmax; ++k, p_r2 += STEP, p_ma += STEP, p_mb += STEP, q += kPairWarps * 32,
-                          goff += kPairWarps * 64, sm_b += kBlockBytes) {
-                const bool valid = q < nvec;
-                const bool vc = valid && pair_cross;
-                // hr = H(r2 - 0.5) = 0 <=> top bit clear
-                const bool c0 = vc & ((int)draw_top<MODE>(seed, p_r2) >= 0);
-                const bool c1 = vc & ((int)draw_top<MODE>(seed, p_r2 + SG) >= 0);
-                const unsigned b0 = __ballot_sync(0xffffffffu, c0), b1 = __ballot_sync(0xffffffffu, c1);
-                sts_f64x2(sm_b, 1.0, 1.0);
-                const uint32_t n0 = __popc(b0);
-                const uint32_t i0 = total + __popc(b0 & lt), i1 = total + n0 + __popc(b1 & lt);
-                if (c0) sts_u16(sm_list + 2 * i0, goff);
-                if (c1) sts_u16(sm_list + 2 * i1, goff + 1);
-                total += n0 + __popc(b1);
-                if (!a.mask_never) {
-                    const uint32_t ta0 = draw_top<MODE>(seed, p_ma), ta1 = draw_top<MODE>(seed, p_ma + SG);
-                    const uint32_t tb0 = draw_top<MODE>(seed, p_mb), tb1 = draw_top<MODE>(seed, p_mb + SG);
-                    if (valid && min(min(ta0, ta1), min(tb0, tb1)) <= top_thr) {  // ~ 4 pm/d of the vectors
-                        if (min(ta0, tb0) <= top_thr) {
-                            const uint32_t slot = atomicAdd(&S.ncand[warp], 1u);
-                            if (slot < (uint32_t)a.cand_cap)
-                                S.cand[warp][slot] = (unsigned short)(goff | (ta0 <= top_thr ? 0x2000u : 0u) | (tb0 <= top_thr ? 0x4000u : 0u));
-                            else
-                                S.overflow = 1;
-                        }
-                        if (min(ta1, tb1) <= top_thr) {
-                            const uint32_t slot = atomicAdd(&S.ncand[warp], 1u);
-                            if (slot < (uint32_t)a.cand_cap)
-                                S.cand[warp][slot] = (unsigned short)((goff + 1) | (ta1 <= top_thr ? 0x2000u : 0u) | (tb1 <= top_thr ? 0x4000u : 0u));
-                            else
-                                S.overflow = 1;
-                        }
+            if (ncand > (uint32_t)a.cand_cap) {  // practically never: the literal formulation of this tile
+                double acc[2] = {acc_a, acc_b};
+                tile_plain<MODE, EVAL>(a, blk0, v, kmax, acc, W, slot.pos);
+                acc_a = acc[0], acc_b = acc[1];
+                __syncwarp();
+                continue;
+            }
+            // ---- pass B: signed spread factor of the crossing genes, 32 at a time
+            {
+                const uint64_t pos_tile = pos + (uint64_t)((blk0 + v) * 64) * SG;  // gene (blk0 + v) * 64
+                for (uint32_t t = lane; t < total; t += 64) {  // two genes per lane: their pow chains interleave
+                    const bool two = t + 32 < total;
+                    const uint32_t e0 = lds_u16(sm_w + kOffList + 2 * t), e1 = two ? lds_u16(sm_w + kOffList + 2 * t + 64) : e0;
+                    // gene index relative to the tile's first gene
+                    const uint32_t j0 = e0 + (e0 >> 6) * (kVirtWarps * 64 - 64), j1 = e1 + (e1 >> 6) * (kVirtWarps * 64 - 64);
+                    const SpreadIn s0 = spread_inputs<MODE>(seed, pos_tile + (uint64_t)j0 * SG, a.dl_r1, a.inv_exp);
+                    const SpreadIn s1 = spread_inputs<MODE>(seed, pos_tile + (uint64_t)j1 * SG, a.dl_r1, a.inv_exp);
+                    const bool f0 = s0.base > 0.0 && a.narrow_pow, f1 = s1.base > 0.0 && a.narrow_pow;
+                    double p0, p1;
+                    const bool ok0 = glibc_pow_narrow_flat(f0 ? s0.base : 1.0, s0.yexp, T, &p0) && f0;
+                    const bool ok1 = glibc_pow_narrow_flat(f1 ? s1.base : 1.0, s1.yexp, T, &p1) && f1;
+                    if (!(ok0 && ok1)) {  // never for ordinary eta
+                        if (!ok0) p0 = pow_spread_slow(s0.base, s0.yexp);
+                        if (!ok1) p1 = pow_spread_slow(s1.base, s1.yexp);
                     }
+                    sts_f64(sm_w + 8 * e0, s0.up ? p0 : -p0);
+                    if (two) sts_f64(sm_w + 8 * e1, s1.up ? p1 : -p1);
                 }
             }
-        }
-        __syncwarp();
-        // ---- pass B: signed spread factor of the crossing genes, 32 at a time
-        {
-            const uint64_t pos_tile = pos + (uint64_t)(blk0 * 64) * SG;
-            for (uint32_t t = lane; t < total; t += 32) {
-                const uint32_t goff = lds_u16(sm_list + 2 * t);
-                const uint64_t at = pos_tile + (uint64_t)goff * SG;
-                const double mc = word_to_unit(draw_full<MODE>(seed, at));
-                const bool up = (int)draw_top<MODE>(seed, at + a.dl_r1) < 0;  // sgn(r1 - 0.5)
-                // live spread branch only (hm = H(0.5 - mc)); the other one is multiplied by exactly 0.0
-                const bool low = 0.5 - mc >= 0.0;
-                const double base = low ? 2.0 * mc : 2.0 - 2.0 * mc;
-                const double yexp = low ? a.inv_exp : -a.inv_exp;
-                // base is 0 (mc == 0) or in [2^-52, 2]; |y log base| < 2 for any eta >= 0
-                double spread;
-                if (!(base > 0.0 && a.narrow_pow) || !glibc_pow_main<true>(base, yexp, T, &spread))
-                    spread = pow_spread_slow(base, yexp);
-                sts_f64(sm_beta_tile + 8 * goff, up ? spread : -spread);
-            }
-        }
-        __syncwarp();
-        // ---- pass M: the mutation candidates of this warp (usually none)
-        {
-            const uint32_t nc = min(S.ncand[warp], (uint32_t)a.cand_cap);
+            __syncwarp();
+            // ---- pass M: the mutation candidates of this tile (usually none)
 #pragma unroll 1
-            for (uint32_t t = lane; t < nc; t += 32) {
-                const uint32_t entry = S.cand[warp][t], goff = entry & 0x1fffu, j = blk0 * 64 + goff;
-                mutate_candidate<MODE>(seed, pos + a.dl_mask_a, pos + a.dl_mask_b, a.dl_mut_a - a.dl_mask_a, a.mask_thresh, a.xi,
-                                       entry, j, pa[j], pb[j], a.lower[j], a.upper[j], &S.beta[goff], &S.side[warp][t], t);
+            for (uint32_t t = lane; t < ncand; t += 32) {
+                const uint32_t entry = W.cand[t], e = entry & 0x1fffu;
+                const uint32_t j = (blk0 + v) * 64 + e + (e >> 6) * (kVirtWarps * 64 - 64);
+                const uint64_t at = pos + (uint64_t)j * SG;
+                const double2 ch = mutated_children<MODE>(seed, at + a.dl_mask_a, at + a.dl_mask_b, a.dl_mut_a - a.dl_mask_a,
+                                                          a.mask_thresh, a.xi, (entry & 0x2000u) != 0, (entry & 0x4000u) != 0,
+                                                          W.ctx.pa[j], W.ctx.pb[j], W.beta[e], a.lower[j], a.upper[j]);
+                W.side[t] = ch;
+                W.beta[e] = __hiloint2double((int)kBetaTagHi, (int)t);
             }
-        }
-        __syncwarp();
-        // ---- pass C: stream the rows
-        {
-            const uint32_t m1 = (uint32_t)a.m - 1;  // first tail gene (fused evaluation)
-            const double2* __restrict__ pa2 = opaque_ptr(reinterpret_cast<const double2*>(pa));
-            const double2* __restrict__ pb2 = opaque_ptr(reinterpret_cast<const double2*>(pb));
-            double2* __restrict__ oa2 = opaque_ptr(reinterpret_cast<double2*>(oa));
-            double2* __restrict__ ob2 = opaque_ptr(reinterpret_cast<double2*>(ob));
-            const double2* __restrict__ lo2 = reinterpret_cast<const double2*>(a.lower);
-            const double2* __restrict__ hi2 = reinterpret_cast<const double2*>(a.upper);
-            const uint32_t sm_side = smem_u32(S.side[warp]);
-            uint32_t q = q_first, sm_b = sm_beta0;
-#pragma unroll 2
-            for (uint32_t k = 0; k < kmax; ++k, q += kPairWarps * 32, sm_b += kBlockBytes) {
-                if (q >= nvec) break;  // only in the last block of the row
-                const double2 va = pa2[q];
-                const double2 vb = pb2[q];
-                const double2 vlo = __ldg(lo2 + q);
-                const double2 vhi = __ldg(hi2 + q);
-                const double2 vbeta = lds_f64x2(sm_b);
-                double ca0, cb0, ca1, cb1;
-                sbx_children(va.x, vb.x, vbeta.x, vlo.x, vhi.x, ca0, cb0);
-                sbx_children(va.y, vb.y, vbeta.y, vlo.y, vhi.y, ca1, cb1);
-                if (max(__double2hiint(vbeta.x), __double2hiint(vbeta.y)) >= (int)kBetaTagHi) {  // rare: parked children
-                    if (__double2hiint(vbeta.x) >= (int)kBetaTagHi) {
-                        const double2 e = lds_f64x2(sm_side + 16 * __double2loint(vbeta.x));
-                        ca0 = e.x;
-                        cb0 = e.y;
-                    }
-                    if (__double2hiint(vbeta.y) >= (int)kBetaTagHi) {
-                        const double2 e = lds_f64x2(sm_side + 16 * __double2loint(vbeta.y));
-                        ca1 = e.x;
-                        cb1 = e.y;
-                    }
+            __syncwarp();
+            // ---- pass C: stream the rows
+            {
+                const uint32_t m1 = (uint32_t)a.m - 1;  // first tail gene (fused evaluation)
+                double2* __restrict__ oa2 = reinterpret_cast<double2*>(W.ctx.oa);
+                double2* __restrict__ ob2 = reinterpret_cast<double2*>(W.ctx.ob);
+                const double2* __restrict__ lo2 = reinterpret_cast<const double2*>(a.lower);
+                const double2* __restrict__ hi2 = reinterpret_cast<const double2*>(a.upper);
+                // piecewise-constant bounds from the launch constants (SEG): one side of the split for the whole tile,
+                // unless the tile's blocks straddle it
+                const uint32_t tile_g0 = (blk0 + v) * 64, tile_g1 = (blk0 + v + (kmax - 1) * kVirtWarps) * 64 + 64;
+                const bool seg_hi_side = tile_g0 >= a.seg_split, seg_mixed = SEG && !seg_hi_side && tile_g1 > a.seg_split;
+                const double seg_lo = a.seg_lo[seg_hi_side ? 1 : 0], seg_hi = a.seg_hi[seg_hi_side ? 1 : 0];
+                const double2* __restrict__ pa2 = reinterpret_cast<const double2*>(W.ctx.pa);
+                const double2* __restrict__ pb2 = reinterpret_cast<const double2*>(W.ctx.pb);
+                uint32_t q = q_first, sm_b = sm_lane;
+                const double2 zero2 = make_double2(0.0, 0.0);
+                // the parents of the next two blocks are always in flight (register double buffer)
+                double2 na = q < nvec ? __ldcs(pa2 + q) : zero2, nb = q < nvec ? __ldcs(pb2 + q) : zero2;
+                double2 fa = zero2, fb = zero2;
+                if (kmax > 1 && q + kVirtWarps * 32 < nvec) {
+                    fa = __ldcs(pa2 + q + kVirtWarps * 32);
+                    fb = __ldcs(pb2 + q + kVirtWarps * 32);
                 }
-                if (EVAL != 0) {
-                    const uint32_t j0 = 2 * q;
-                    if (j0 >= m1) {
-                        acc_a += dtlz_term<EVAL>(ca0);
-                        acc_b += dtlz_term<EVAL>(cb0);
-                        acc_a += dtlz_term<EVAL>(ca1);
-                        acc_b += dtlz_term<EVAL>(cb1);
-                    } else {  // the vector holds a position gene (first block of the row only)
-                        S.pos[0][j0] = ca0;
-                        S.pos[1][j0] = cb0;
-                        if (j0 + 1 >= m1) {
-                            acc_a += dtlz_term<EVAL>(ca1);
-                            acc_b += dtlz_term<EVAL>(cb1);
-                        } else {
-                            S.pos[0][j0 + 1] = ca1;
-                            S.pos[1][j0 + 1] = cb1;
+                for (uint32_t k = 0; k < kmax; ++k, q += kVirtWarps * 32, sm_b += 512) {
+                    if (q >= nvec) break;  // only in the last block of the row
+                    const double2 va = na, vb = nb;
+                    na = fa;
+                    nb = fb;
+                    {
+                        const uint32_t qf = q + 2 * kVirtWarps * 32;
+                        if (k + 2 < kmax && qf < nvec) {
+                            fa = __ldcs(pa2 + qf);
+                            fb = __ldcs(pb2 + qf);
                         }
                     }
+                    double2 vlo, vhi;
+                    if (SEG) {
+                        if (seg_mixed) {  // this tile holds the split: per gene
+                            const int sx = 2 * q >= a.seg_split, sy = 2 * q + 1 >= a.seg_split;
+                            vlo = make_double2(a.seg_lo[sx], a.seg_lo[sy]);
+                            vhi = make_double2(a.seg_hi[sx], a.seg_hi[sy]);
+                        } else {
+                            vlo = make_double2(seg_lo, seg_lo);
+                            vhi = make_double2(seg_hi, seg_hi);
+                        }
+                    } else {
+                        vlo = __ldg(lo2 + q);
+                        vhi = __ldg(hi2 + q);
+                    }
+                    const double2 vbeta = lds_f64x2(sm_b);
+                    double ca0, cb0, ca1, cb1;
+                    sbx_children(va.x, vb.x, vbeta.x, vlo.x, vhi.x, ca0, cb0);
+                    sbx_children(va.y, vb.y, vbeta.y, vlo.y, vhi.y, ca1, cb1);
+                    if (max(__double2hiint(vbeta.x), __double2hiint(vbeta.y)) >= (int)kBetaTagHi) {  // rare: parked children
+                        if (__double2hiint(vbeta.x) >= (int)kBetaTagHi) {
+                            const double2 ch = lds_f64x2(sm_w + kOffSide + 16 * __double2loint(vbeta.x));
+                            ca0 = ch.x;
+                            cb0 = ch.y;
+                        }
+                        if (__double2hiint(vbeta.y) >= (int)kBetaTagHi) {
+                            const double2 ch = lds_f64x2(sm_w + kOffSide + 16 * __double2loint(vbeta.y));
+                            ca1 = ch.x;
+                            cb1 = ch.y;
+                        }
+                    }
+                    accumulate_vector<EVAL>(2 * q, m1, ca0, cb0, ca1, cb1, acc_a, acc_b, slot.pos);
+                    __stcs(oa2 + q, make_double2(ca0, ca1));
+                    __stcs(ob2 + q, make_double2(cb0, cb1));
                 }
-                oa2[q] = make_double2(ca0, ca1);
-                ob2[q] = make_double2(cb0, cb1);
+            }
+            __syncwarp();
+        }
+        if (EVAL != 0) {
+            // this warp's totals (the xor butterfly of block_sum) go into the pair's slot; the last warp to arrive adds
+            // the eight totals in ascending warp order and writes the two objective rows
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                acc_a += __shfl_xor_sync(0xffffffffu, acc_a, off);
+                acc_b += __shfl_xor_sync(0xffffffffu, acc_b, off);
+            }
+            uint32_t before = 0;
+            if (lane == 0) {
+                slot.part[0][v] = acc_a;
+                slot.part[1][v] = acc_b;
+                __threadfence_block();
+                before = atomicAdd(&slot.arrived, 1u);
+            }
+            before = __shfl_sync(0xffffffffu, before, 0);
+            if (before == kVirtWarps - 1) {
+                __threadfence_block();
+                const uint64_t f0 = a.f_row0 + (a.f_row0_dev ? (uint64_t)*a.f_row0_dev : 0);
+                double* fa = a.f_out + (f0 + unit) * a.m;
+                double* fb = a.f_out + (f0 + a.half + unit) * a.m;
+                if (lane < 2) {
+                    const volatile double* part = slot.part[lane];
+                    double g = part[0];
+#pragma unroll
+                    for (int w = 1; w < kVirtWarps; ++w) g += part[w];
+                    (lane == 0 ? fa : fb)[0] = g;
+                }
+                for (uint32_t i = lane + 1; i < a.m; i += 32) {
+                    fa[i] = *reinterpret_cast<volatile double*>(&slot.pos[0][i - 1]);
+                    fb[i] = *reinterpret_cast<volatile double*>(&slot.pos[1][i - 1]);
+                }
+                __syncwarp();
+                if (lane == 0) {
+                    slot.arrived = 0;
+                    __threadfence_block();
+                    *reinterpret_cast<volatile uint32_t*>(&slot.done) = turn / kPairSlots + 1;
+                }
             }
         }
         __syncwarp();
     }
+}
 
-    __syncthreads();
-    if (S.overflow) {  // a warp ran out of candidate slots: redo the pair the plain way (exact, practically never)
-        __syncthreads();
-        redo_pair<MODE, EVAL>(a, unit, *reinterpret_cast<GenericSmem*>(S.beta));
-        return;
+template <int MODE, int EVAL, bool SEG>
+void launch_pairs_seg(const ReproK& k, uint64_t units, cudaStream_t s) {
+    static int grid = 0;  // per instantiation
+    if (grid == 0) {
+        TEMO_CUDA(cudaFuncSetAttribute(reproduce_pairs_kernel<MODE, EVAL, SEG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)sizeof(PairSmem)));
+        int dev = 0, sms = 0;
+        TEMO_CUDA(cudaGetDevice(&dev));
+        TEMO_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        grid = (sms > 0 ? sms : kSMs) * TEMO_PAIR_MIN_BLOCKS;
     }
-    if (EVAL != 0) {
-        const uint64_t f0 = a.f_row0 + (a.f_row0_dev ? (uint64_t)*a.f_row0_dev : 0);
-        const double ga = block_sum<8>(acc_a, S.red);
-        double* fa = a.f_out + (f0 + row_a) * a.m;
-        if (threadIdx.x == 0) fa[0] = ga;
-        if (threadIdx.x >= 1 && threadIdx.x < a.m) fa[threadIdx.x] = S.pos[0][threadIdx.x - 1];
-        const double gb = block_sum<8>(acc_b, S.red);
-        double* fb = a.f_out + (f0 + row_b) * a.m;
-        if (threadIdx.x == 0) fb[0] = gb;
-        if (threadIdx.x >= 1 && threadIdx.x < a.m) fb[threadIdx.x] = S.pos[1][threadIdx.x - 1];
-    }
+    reproduce_pairs_kernel<MODE, EVAL, SEG><<<(unsigned)std::min<uint64_t>(units, (uint64_t)grid), kVirtWarps * 32, sizeof(PairSmem), s>>>(k);
 }
 
 template <int MODE, int EVAL>
-void launch_pairs_eval(const ReproK& k, uint64_t units, cudaStream_t s) {
-    static bool configured = false;  // per instantiation
-    if (!configured) {
-        TEMO_CUDA(cudaFuncSetAttribute(reproduce_pairs_kernel<MODE, EVAL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)sizeof(PairSmem)));
-        configured = true;
-    }
-    reproduce_pairs_kernel<MODE, EVAL><<<(unsigned)units, 256, sizeof(PairSmem), s>>>(k);
+void launch_pairs_eval(const ReproK& k, uint64_t units, bool seg, cudaStream_t s) {
+    if (seg)
+        launch_pairs_seg<MODE, EVAL, true>(k, units, s);
+    else
+        launch_pairs_seg<MODE, EVAL, false>(k, units, s);
 }
 
 template <int MODE>
-void launch_pairs(const ReproK& k, uint64_t units, int eval, cudaStream_t s) {
+void launch_pairs(const ReproK& k, uint64_t units, int eval, bool seg, cudaStream_t s) {
     switch (eval) {
-    case 0: launch_pairs_eval<MODE, 0>(k, units, s); break;
-    case kDtlz1: launch_pairs_eval<MODE, kDtlz1>(k, units, s); break;
-    case kDtlz2: launch_pairs_eval<MODE, kDtlz2>(k, units, s); break;
-    case kDtlz3: launch_pairs_eval<MODE, kDtlz3>(k, units, s); break;
-    case kDtlz4: launch_pairs_eval<MODE, kDtlz4>(k, units, s); break;
+    case 0: launch_pairs_eval<MODE, 0>(k, units, seg, s); break;
+    case kDtlz1: launch_pairs_eval<MODE, kDtlz1>(k, units, seg, s); break;
+    case kDtlz2: launch_pairs_eval<MODE, kDtlz2>(k, units, seg, s); break;
+    case kDtlz3: launch_pairs_eval<MODE, kDtlz3>(k, units, seg, s); break;
+    case kDtlz4: launch_pairs_eval<MODE, kDtlz4>(k, units, seg, s); break;
     default: fail(1, "reproduce: fused evaluation supports DTLZ1-4 only");
     }
 }
+
 template <int MODE, bool SBX, bool PM, int EVAL>
 void launch_vec(const ReproK& k, uint64_t units, int block, int vec, cudaStream_t s) {
     if (units == 0) return;
@@ -737,21 +911,27 @@ __global__ void pow_batch_kernel(const double* x, const double* y, uint64_t n, d
         out[e] = pow_like_host(x[e], y[e], T);
 }
 
-// TEMO_B200_GENERIC_K1=1 routes everything through the generic kernel (A/B checks of the two K1 paths)
-inline bool force_generic_kernel() {
-    static const bool v = [] { const char* e = getenv("TEMO_B200_GENERIC_K1"); return e && e[0] == '1'; }();
-    return v;
+// Path-selection knobs of K1 (tests and A/B measurements; temo_b200_set_option, or the environment at start-up):
+//   k1_generic       1: everything goes through the generic kernel        TEMO_B200_GENERIC_K1
+//   k1_bound_arrays  1: the pair kernel reads the bound arrays even when
+//                       they are piecewise constant                       TEMO_B200_K1_BOUND_ARRAYS
+//   k1_cand_cap      mutation-candidate slots per warp tile of the pair
+//                    kernel, 0..kPairCand (0 forces its plain-tile path)  TEMO_B200_K1_CAND_CAP
+struct K1Options {
+    int generic, bound_arrays, cand_cap;
+};
+inline int env_int(const char* name, int dflt) {
+    const char* e = getenv(name);
+    return e ? atoi(e) : dflt;
 }
-
-// TEMO_B200_K1_CAND_CAP=<n> shrinks the candidate slots of the pair kernel (0 forces its redo path; tests)
-inline int pair_cand_cap() {
-    static const int v = [] {
-        const char* e = getenv("TEMO_B200_K1_CAND_CAP");
-        const int c = e ? atoi(e) : kPairCand;
-        return c < 0 ? 0 : (c > kPairCand ? kPairCand : c);
-    }();
-    return v;
+inline K1Options& k1_options() {
+    static K1Options o{env_int("TEMO_B200_GENERIC_K1", 0), env_int("TEMO_B200_K1_BOUND_ARRAYS", 0),
+                       std::max(0, std::min(kPairCand, env_int("TEMO_B200_K1_CAND_CAP", kPairCand)))};
+    return o;
 }
+inline bool force_generic_kernel() { return k1_options().generic != 0; }
+inline bool no_bound_segments() { return k1_options().bound_arrays != 0; }
+inline int pair_cand_cap() { return k1_options().cand_cap; }
 
 inline unsigned stream_grid(uint64_t total, int block) {
     uint64_t g = (total + block - 1) / block;
@@ -827,14 +1007,19 @@ void launch_reproduce(const ReproArgs& a, cudaStream_t s) {
     // Full pairs of wide even rows go through the phased pair kernel when mutation candidates are rare (expected
     // number per warp and tile <= 1); what is left (an odd last row) and every other shape through the generic one.
     const double cand_rate = k.mask_never ? 0.0 : ((double)k.mask_top + 1.0) * 0x1.0p-21;  // P(quick reject passes)
-    const double cand_per_warp = 2.0 * (double)std::min<uint64_t>(a.d, kPairTile) / kPairWarps * cand_rate;
+    const double cand_per_warp = 2.0 * (double)std::min<uint64_t>(a.d / kVirtWarps, kTileGenes) * cand_rate;
     k.cand_cap = pair_cand_cap();
     if (a.do_sbx && a.do_pm && vec == 2 && block == 256 && k.half > 0 && a.d * 8 < (1ULL << 32) && cand_per_warp <= 1.0 &&
         aligned16(a.pool) && aligned16(a.out) && aligned16(a.lower) && aligned16(a.upper) && !force_generic_kernel()) {
+        const bool seg = a.seg.valid && a.seg.split <= a.d && !no_bound_segments();
+        if (seg) {
+            k.seg_split = (uint32_t)a.seg.split;
+            for (int i = 0; i < 2; ++i) k.seg_lo[i] = a.seg.lo[i], k.seg_hi[i] = a.seg.hi[i];
+        }
         if (a.rng.mode == 0)
-            launch_pairs<0>(k, k.half, a.eval_problem, s);
+            launch_pairs<0>(k, k.half, a.eval_problem, seg, s);
         else
-            launch_pairs<1>(k, k.half, a.eval_problem, s);
+            launch_pairs<1>(k, k.half, a.eval_problem, seg, s);
         TEMO_CUDA(cudaGetLastError());
         k.unit0 = k.half;
         units -= k.half;
@@ -850,6 +1035,16 @@ void launch_reproduce(const ReproArgs& a, cudaStream_t s) {
         require(a.f_row0_dev == nullptr, "reproduce: device-side row offsets are not supported with fused evaluation");
         launch_dtlz_finish(a.eval_problem, a.f_out, a.n, a.m, a.d, a.f_row0, s);
     }
+}
+
+bool set_k1_option(const char* name, long value) {
+    const std::string key(name ? name : "");
+    K1Options& o = k1_options();
+    if (key == "k1_generic") o.generic = value != 0;
+    else if (key == "k1_bound_arrays") o.bound_arrays = value != 0;
+    else if (key == "k1_cand_cap") o.cand_cap = (int)std::max(0L, std::min((long)kPairCand, value));
+    else return false;
+    return true;
 }
 
 void launch_pow_batch(const double* x, const double* y, uint64_t n, double* out, cudaStream_t s) {

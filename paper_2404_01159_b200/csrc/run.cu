@@ -146,6 +146,7 @@ Run::Run(const RunConfig& c) : cfg(c) {
 
     std::vector<double> lo(d), hi(d);
     problem_bounds(cfg.problem, d, m, lo.data(), hi.data());
+    bound_seg = find_bound_segments(lo.data(), hi.data(), d);
     TEMO_CUDA(cudaMemcpyAsync(lower, lo.data(), d * sizeof(double), cudaMemcpyHostToDevice, stream));
     TEMO_CUDA(cudaMemcpyAsync(upper, hi.data(), d * sizeof(double), cudaMemcpyHostToDevice, stream));
     TEMO_CUDA(cudaStreamSynchronize(stream));  // host vectors go out of scope
@@ -246,6 +247,7 @@ void Run::launch_reproduction(const Plan& p, bool fused) {
     ra.ga = cfg.ga;
     ra.lower = lower;
     ra.upper = upper;
+    ra.seg = bound_seg;
     if (fused) {
         ra.eval_problem = cfg.problem;
         ra.m = m;

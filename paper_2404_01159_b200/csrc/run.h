@@ -56,6 +56,7 @@ struct Run {
     uint32_t* d_P = nullptr;
     uint32_t* free_scratch = nullptr;
     double *v0 = nullptr, *v = nullptr, *gamma = nullptr, *lower = nullptr, *upper = nullptr;
+    BoundSegments bound_seg;  // the same bounds, piecewise constant (K1 keeps them in registers)
     double *zmin = nullptr, *zmax = nullptr;
     unsigned long long* zscratch = nullptr;
     uint32_t* skip_flag = nullptr;

@@ -191,6 +191,7 @@ struct Shard {
     double* f_off_loc = nullptr;  // n_loc x m
     double* f_gather = nullptr;   // world x n_loc x m
     double *v0 = nullptr, *v = nullptr, *gamma = nullptr, *lower = nullptr, *upper = nullptr;
+    BoundSegments bound_seg;
     double *zmin = nullptr, *zmax = nullptr;
     unsigned long long* zscratch = nullptr;
     uint32_t* skip_flag = nullptr;
@@ -250,6 +251,7 @@ struct Shard {
         launch_gamma_indexed(v, ws.vn, r, m, vindex, gamma, ws.err_flag, nullptr, stream);
         std::vector<double> lo(d), hi(d);
         problem_bounds(cfg.problem, d, m, lo.data(), hi.data());
+        bound_seg = find_bound_segments(lo.data(), hi.data(), d);
         TEMO_CUDA(cudaMemcpyAsync(lower, lo.data(), d * sizeof(double), cudaMemcpyHostToDevice, stream));
         TEMO_CUDA(cudaMemcpyAsync(upper, hi.data(), d * sizeof(double), cudaMemcpyHostToDevice, stream));
         // initial population (algorithms.hpp:241-242): global rows [rank*n/world, (rank+1)*n/world) in local
@@ -318,6 +320,7 @@ struct Shard {
         ra.ga = cfg.ga;
         ra.lower = lower;
         ra.upper = upper;
+        ra.seg = bound_seg;
         ra.global_n = n;
         ra.global_unit0 = (uint64_t)rank * h_loc;
         const bool fused = cfg.fuse_eval && cfg.problem >= kDtlz1 && cfg.problem <= kDtlz4;

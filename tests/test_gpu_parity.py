@@ -162,6 +162,91 @@ def test_ga_reproduce_larger_shapes(tb, oracle, shape):
     assert np.array_equal(gm, em)
 
 
+# ---- the phased pair kernel (wide even rows) against the oracle and against the generic kernel
+
+
+@pytest.fixture
+def k1_options(tb):
+    """Restores the K1 path-selection knobs after a test that flips them."""
+    yield tb.set_option
+    tb.set_option("k1_generic", 0)
+    tb.set_option("k1_bound_arrays", 0)
+    tb.set_option("k1_cand_cap", 8)
+
+
+@pytest.mark.parametrize("shape", [(16, 512), (12, 5120), (6, 5122), (6, 10240), (5, 20000), (9, 2002)])
+@pytest.mark.parametrize("ga", [(1.0, 20.0, 1.0, 20.0), (0.6, 5.0, 3.0, 7.0)])
+def test_pair_kernel_vs_oracle(tb, oracle, shape, ga):
+    """Rows wide enough for the pair kernel (d even, >= 512): one and several row tiles, a partial last block, an odd
+    population (the last row goes through the generic kernel), pairs that do not cross (pc < 1), several mutations per row."""
+    n, d = shape
+    lo, hi = np.zeros(d), np.ones(d)
+    x, _ = oracle.random_reproduce(n, d, 23, 0, lo, hi)
+    st = tb.RngStream(77, 12345)
+    got = tb.ga_reproduce(x, st, tb.GaParams(*ga), lo, hi)
+    exp, c = oracle.ga_reproduce(x, 77, 12345, lo, hi, ga=ga)
+    assert st.counter == c
+    assert np.array_equal(got, exp), ulp_diff(got, exp).max()
+
+
+@pytest.mark.parametrize("split", [0, 1, 3, 64, 1001, 2500, 4999])
+def test_pair_kernel_bound_segments(tb, oracle, k1_options, split):
+    """Piecewise-constant bounds kept in registers (the LSMOP shape: [0,1] then [0,10]) give the same bits as the bound
+    arrays, wherever the split falls (first block, odd gene, inside a later block)."""
+    n, d = 8, 5000
+    lo, hi = np.zeros(d), np.ones(d)
+    lo[split:], hi[split:] = -2.0, 10.0
+    x, _ = oracle.random_reproduce(n, d, 5, 0, lo, hi)
+    exp, _ = oracle.ga_reproduce(x, 9, 0, lo, hi)
+    got = {}
+    for arrays in (0, 1):
+        k1_options("k1_bound_arrays", arrays)
+        got[arrays] = tb.ga_reproduce(x, tb.RngStream(9, 0), tb.GaParams(), lo, hi)
+        assert np.array_equal(got[arrays], exp), (arrays, ulp_diff(got[arrays], exp).max())
+    # three segments: not representable, must silently stay on the arrays
+    lo[d // 3:d // 2] = -5.0
+    x3, _ = oracle.random_reproduce(n, d, 6, 0, lo, hi)
+    k1_options("k1_bound_arrays", 0)
+    e3, _ = oracle.ga_reproduce(x3, 9, 0, lo, hi)
+    assert np.array_equal(tb.ga_reproduce(x3, tb.RngStream(9, 0), tb.GaParams(), lo, hi), e3)
+
+
+@pytest.mark.parametrize("cap", [0, 1, 8])
+def test_pair_kernel_candidate_overflow_path(tb, oracle, k1_options, cap):
+    """With the mutation-candidate slots of a warp tile exhausted the tile is recomputed by the plain per-gene
+    formulation: same offspring, and (fused evaluation) the same objectives as the generic kernel."""
+    n, d = 24, 5000
+    lo, hi = np.zeros(d), np.ones(d)
+    x, _ = oracle.random_reproduce(n, d, 31, 0, lo, hi)
+    k1_options("k1_cand_cap", cap)
+    for pm in (1.0, 3.0):
+        got = tb.ga_reproduce(x, tb.RngStream(3, 7), tb.GaParams(pm=pm), lo, hi)
+        exp, _ = oracle.ga_reproduce(x, 3, 7, lo, hi, ga=(1.0, 20.0, pm, 20.0))
+        assert np.array_equal(got, exp), (pm, ulp_diff(got, exp).max())
+
+
+@pytest.mark.parametrize("problem", ["dtlz1", "dtlz2", "dtlz4"])
+def test_pair_kernel_runs_equal_generic_kernel_runs(tb, k1_options, problem):
+    """Whole generations (fused evaluation, last-arriver objective sums, survivors) through the pair kernel, through
+    its plain-tile path and through the generic kernel: bit-identical populations and objectives."""
+    outs = []
+    for opts in ({"k1_generic": 0, "k1_cand_cap": 8}, {"k1_generic": 0, "k1_cand_cap": 0}, {"k1_generic": 1}):
+        for k, v in opts.items():
+            k1_options(k, v)
+        with tb.RveaRun(tb.RunConfig(problem=problem, pop=600, dim=1400, obj=3, generations=4, seed=11)) as run:
+            pops = [run.step() for _ in range(4)]
+            out = run.download()
+        outs.append((pops, out["x"], out["f"]))
+    for pops, x, f in outs[1:]:
+        assert pops == outs[0][0]
+        assert np.array_equal(x, outs[0][1]) and np.array_equal(f, outs[0][2])
+
+
+def test_lockstep_wide_rows(tb, oracle):
+    """Lock-step generations at a row width that runs the pair kernel (d = 1000, the shape of config #4)."""
+    _lockstep(tb, oracle, "dtlz3", 128, 1000, 3, 5, 21)
+
+
 # -------------------------------------------------------------------------- problems
 @pytest.mark.parametrize("m", [3, 2, 5, 10])
 def test_problems_golden(tb, m):

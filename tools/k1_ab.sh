@@ -8,3 +8,4 @@ TEMO_B200_K1_CAND_CAP=1 python tools/k1_check.py --pop 4096 --dim 5000 --gens 4 
 python tools/k1_check.py --pop 4097 --dim 5000 --gens 3 --reps 2 --rng philox
 TEMO_B200_GENERIC_K1=1 python tools/k1_check.py --pop 4097 --dim 5000 --gens 3 --reps 2 --rng philox
 python tools/k1_check.py --no-hash --gens 3 --reps 5
+TEMO_B200_K1_BOUND_ARRAYS=1 python tools/k1_check.py --pop 4096 --dim 5000 --gens 4 --reps 2
