@@ -212,10 +212,17 @@ struct Searcher {
             const bool is_self = valid && row.self != 0xffffffffu && ix.orig[ix.centre[LVL][id]] == row.self;
             Lf = warp_max_lower((valid && !is_self && q <= 1.5) ? q : -1.0, Lf);
             unsigned done = 0;
+            // best-first: the passing child whose centre is closest to the row is opened first, which raises L to
+            // (nearly) its final value at once and prunes most siblings; the order of visits does not change the
+            // result (lexicographic reduction over everything visited, conservative pruning)
+            const unsigned qkey = __float_as_uint(fminf(fmaxf(__double2float_rn(q), 0.0f), 4.0f));  // q in [0, 2]: bits are monotone
             for (;;) {
-                const unsigned mask = __ballot_sync(0xffffffffu, valid && passes(q, cr, sr)) & ~done;
+                const bool open = valid && !((done >> lane) & 1u) && passes(q, cr, sr);
+                const unsigned mask = __ballot_sync(0xffffffffu, open);
                 if (!mask) break;
-                const int bsel = __ffs(mask) - 1;
+                const unsigned top = __reduce_max_sync(0xffffffffu, open ? qkey : 0u);
+                const unsigned pick = __ballot_sync(0xffffffffu, open && qkey == top);
+                const int bsel = __ffs(pick ? pick : mask) - 1;
                 done |= 1u << bsel;
                 const uint64_t child = base + bsel;
                 if (LVL == 1) {
