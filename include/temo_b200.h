@@ -204,10 +204,12 @@ int temo_b200_run_time_stage(temo_b200_run* run, int stage, int reps, double* me
 typedef struct temo_b200_shard temo_b200_shard; /* opaque */
 const char* temo_b200_shard_last_error(void);
 /* Pure host code (no GPU needed): the exchange plan of one generation for `rank` from the replicated
- * survivor tables: local slots to send (grouped by destination, in the destination's mating-row order),
- * per-peer row counts, the receive-buffer row of every local mating row, and the generation's draw
- * counters {c_sbx, c_pm, counter after the generation}. */
-int temo_b200_shard_plan(uint64_t seed, uint64_t counter, uint64_t P, uint64_t n, uint64_t d, int rank, int world,
+ * survivor tables. The exchange is cut into `chunks` pieces by local mating pair (pair p belongs to chunk
+ * p / ceil(h_loc / chunks)) so that reproduction can start on the first pairs while the rest is on the wire:
+ * local slots to send ordered by (chunk, destination), row counts indexed [chunk * world + peer], the
+ * receive-buffer row of every local mating row (the buffer is filled chunk after chunk, source after source),
+ * and the generation's draw counters {c_sbx, c_pm, counter after the generation}. */
+int temo_b200_shard_plan(uint64_t seed, uint64_t counter, uint64_t P, uint64_t n, uint64_t d, int rank, int world, int chunks,
                          const int32_t* surv_owner, const uint32_t* surv_slot, uint32_t* send_slots,
                          uint64_t send_slots_cap, uint64_t* send_counts, uint64_t* recv_counts,
                          uint32_t* recv_pos, uint64_t* counters3);
@@ -226,6 +228,13 @@ int temo_b200_shard_info(temo_b200_shard* s, uint64_t* info8);
 void* temo_b200_shard_buffer(temo_b200_shard* s, int which);
 int temo_b200_shard_pack(temo_b200_shard* s, const uint32_t* slots, uint64_t count);
 int temo_b200_shard_reproduce(temo_b200_shard* s, const uint32_t* recv_pos, uint64_t c_sbx, uint64_t c_pm);
+/* Pieces of a chunked exchange: pack `count` rows into the send buffer from row `row0`; reproduce (+ evaluate) only the
+ * local pairs [unit_begin, unit_begin + unit_count). Both only enqueue work on the shard's stream and return. */
+int temo_b200_shard_pack_at(temo_b200_shard* s, const uint32_t* slots, uint64_t count, uint64_t row0);
+int temo_b200_shard_reproduce_range(temo_b200_shard* s, const uint32_t* recv_pos, uint64_t c_sbx, uint64_t c_pm,
+                                    uint64_t unit_begin, uint64_t unit_count);
+/* The cudaStream_t all stages of this shard are enqueued on (collectives issued on it need no device-wide syncs). */
+void* temo_b200_shard_stream(temo_b200_shard* s);
 int temo_b200_shard_place_f(temo_b200_shard* s, uint64_t P, int initial);
 int temo_b200_shard_select_local(temo_b200_shard* s, uint64_t P, uint64_t lo, uint64_t hi, uint64_t t);
 int temo_b200_shard_select_rows(temo_b200_shard* s, uint64_t lo, uint64_t hi);

@@ -70,6 +70,9 @@ struct ReproArgs {
     // sharded runs: this launch covers pairs [global_unit0, global_unit0 + n/2) of a global population of
     // global_n rows (0 = not sharded); draw counters are addressed globally, storage rows locally
     uint64_t global_n = 0, global_unit0 = 0;
+    // optional: only the mating units [unit_begin, unit_begin + unit_count) of this launch's rows (0 = all); lets a
+    // sharded run start on the pairs whose parents have already arrived
+    uint64_t unit_begin = 0, unit_count = 0;
 };
 void launch_reproduce(const ReproArgs& a, cudaStream_t s);
 // K1 path-selection knobs ("k1_generic", "k1_bound_arrays", "k1_cand_cap"); false for an unknown name.

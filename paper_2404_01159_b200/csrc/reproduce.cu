@@ -35,7 +35,8 @@ struct ReproK {
     double* out;
     const uint32_t* dst;
     uint64_t n, d, half;
-    uint64_t unit0;  // first mating unit of this launch (grid block 0)
+    uint64_t unit0;     // first mating unit of this launch (grid block 0)
+    uint64_t unit_end;  // pair kernel: one past its last unit (<= half)
     uint64_t g_unit0, g_half, g_n;  // position of this launch inside the global draw blocks (sharded runs)
     Rng rng;
     uint64_t c_mc, c_r1, c_r2, c_r3, c_mask, c_mut;
@@ -587,7 +588,7 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
     const uint32_t sm_w = opaque(smem_u32(&W)), sm_lane = opaque(smem_u32(&W) + lane * 16);  // beta tile is first in WarpSmem
 
     uint32_t turn = 0;   // pairs this team has started
-    for (uint64_t unit = a.unit0 + blockIdx.x; unit < a.half; unit += gridDim.x, ++turn) {
+    for (uint64_t unit = a.unit0 + blockIdx.x; unit < a.unit_end; unit += gridDim.x, ++turn) {
         PairSlot& slot = S.slot[turn % kPairSlots];
         if (lane == 0) {
             const uint64_t row_a = unit, row_b = a.half + unit, g_unit = a.g_unit0 + unit;
@@ -1001,7 +1002,9 @@ void launch_reproduce(const ReproArgs& a, cudaStream_t s) {
     k.f_out = a.f_out;
     k.f_row0 = a.f_row0;
     k.f_row0_dev = a.f_row0_dev;
-    uint64_t units = a.do_sbx ? k.half + (a.n & 1) : a.n;
+    const uint64_t units_all = a.do_sbx ? k.half + (a.n & 1) : a.n;
+    require(a.unit_begin <= units_all && a.unit_count <= units_all - a.unit_begin, "reproduce: bad unit range");
+    const uint64_t unit_lo = a.unit_begin, unit_hi = a.unit_count ? a.unit_begin + a.unit_count : units_all;
     const int vec = row_vec(a.d), block = row_block(a.d);
     const auto aligned16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
     // Full pairs of wide even rows go through the phased pair kernel when mutation candidates are rare (expected
@@ -1009,22 +1012,27 @@ void launch_reproduce(const ReproArgs& a, cudaStream_t s) {
     const double cand_rate = k.mask_never ? 0.0 : ((double)k.mask_top + 1.0) * 0x1.0p-21;  // P(quick reject passes)
     const double cand_per_warp = 2.0 * (double)std::min<uint64_t>(a.d / kVirtWarps, kTileGenes) * cand_rate;
     k.cand_cap = pair_cand_cap();
-    if (a.do_sbx && a.do_pm && vec == 2 && block == 256 && k.half > 0 && a.d * 8 < (1ULL << 32) && cand_per_warp <= 1.0 &&
-        aligned16(a.pool) && aligned16(a.out) && aligned16(a.lower) && aligned16(a.upper) && !force_generic_kernel()) {
+    uint64_t next = unit_lo;  // first unit not yet launched
+    if (a.do_sbx && a.do_pm && vec == 2 && block == 256 && unit_lo < std::min(unit_hi, k.half) && a.d * 8 < (1ULL << 32) &&
+        cand_per_warp <= 1.0 && aligned16(a.pool) && aligned16(a.out) && aligned16(a.lower) && aligned16(a.upper) &&
+        !force_generic_kernel()) {
         const bool seg = a.seg.valid && a.seg.split <= a.d && !no_bound_segments();
         if (seg) {
             k.seg_split = (uint32_t)a.seg.split;
             for (int i = 0; i < 2; ++i) k.seg_lo[i] = a.seg.lo[i], k.seg_hi[i] = a.seg.hi[i];
         }
+        k.unit0 = unit_lo;
+        k.unit_end = std::min(unit_hi, k.half);
         if (a.rng.mode == 0)
-            launch_pairs<0>(k, k.half, a.eval_problem, seg, s);
+            launch_pairs<0>(k, k.unit_end - k.unit0, a.eval_problem, seg, s);
         else
-            launch_pairs<1>(k, k.half, a.eval_problem, seg, s);
+            launch_pairs<1>(k, k.unit_end - k.unit0, a.eval_problem, seg, s);
         TEMO_CUDA(cudaGetLastError());
-        k.unit0 = k.half;
-        units -= k.half;
+        next = k.unit_end;
     }
-    if (units > 0) {
+    if (next < unit_hi) {
+        k.unit0 = next;
+        const uint64_t units = unit_hi - next;
         if (a.rng.mode == 0)
             launch_mode<0>(k, a.do_sbx, a.do_pm, units, block, vec, a.eval_problem, s);
         else
@@ -1033,7 +1041,18 @@ void launch_reproduce(const ReproArgs& a, cudaStream_t s) {
     TEMO_CUDA(cudaGetLastError());
     if (a.eval_problem != 0) {
         require(a.f_row0_dev == nullptr, "reproduce: device-side row offsets are not supported with fused evaluation");
-        launch_dtlz_finish(a.eval_problem, a.f_out, a.n, a.m, a.d, a.f_row0, s);
+        if (unit_lo == 0 && unit_hi == units_all) {
+            launch_dtlz_finish(a.eval_problem, a.f_out, a.n, a.m, a.d, a.f_row0, s);
+        } else if (a.do_sbx) {  // rows p and half + p of the units launched (the unpaired last row is unit `half`)
+            const uint64_t pairs_hi = std::min(unit_hi, k.half);
+            if (pairs_hi > unit_lo) {
+                launch_dtlz_finish(a.eval_problem, a.f_out, pairs_hi - unit_lo, a.m, a.d, a.f_row0 + unit_lo, s);
+                launch_dtlz_finish(a.eval_problem, a.f_out, pairs_hi - unit_lo, a.m, a.d, a.f_row0 + k.half + unit_lo, s);
+            }
+            if (unit_hi > k.half) launch_dtlz_finish(a.eval_problem, a.f_out, 1, a.m, a.d, a.f_row0 + a.n - 1, s);
+        } else {
+            launch_dtlz_finish(a.eval_problem, a.f_out, unit_hi - unit_lo, a.m, a.d, a.f_row0 + unit_lo, s);
+        }
     }
 }
 

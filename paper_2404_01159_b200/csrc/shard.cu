@@ -118,12 +118,18 @@ static PermCache g_perm_cache;
 // Outputs (for `rank`): the local slots to send, grouped by destination rank and ordered by the
 // destination's local mating row; send/recv row counts per peer; for every local mating row its row in
 // the receive buffer; and the draw counters of the generation.
-void shard_plan(uint64_t seed, uint64_t counter, uint64_t P, uint64_t n, int rank, int world, const int32_t* surv_owner,
+// The exchange is cut into `chunks` pieces by local mating pair (pair p of a rank belongs to chunk p / ceil(h_loc / chunks)):
+// piece c carries the parents of the pairs of chunk c, so K1 can start on chunk c while piece c + 1 is still on the
+// wire. Layout: send_slots ordered by (chunk, destination), counts indexed [chunk * world + peer], the receive buffer
+// filled chunk after chunk and, inside a chunk, source after source (the order all_to_all delivers).
+void shard_plan(uint64_t seed, uint64_t counter, uint64_t P, uint64_t n, int rank, int world, int chunks, const int32_t* surv_owner,
                 const uint32_t* surv_slot, std::vector<uint32_t>& send_slots, std::vector<uint64_t>& send_counts,
                 std::vector<uint64_t>& recv_counts, std::vector<uint32_t>& recv_pos, uint64_t counters_out[3]) {
     require(world >= 1 && rank >= 0 && rank < world, "shard_plan: bad rank");
+    require(chunks >= 1, "shard_plan: at least one chunk");
     require(n % (2 * (uint64_t)world) == 0, "shard_plan: population must be divisible by 2 * world size");
     const uint64_t half = n / 2, h_loc = half / world, n_loc = 2 * h_loc;
+    const uint64_t per_chunk = (h_loc + (uint64_t)chunks - 1) / (uint64_t)chunks;  // pairs per chunk
     uint64_t c = counter;
     const uint64_t c_pool = c;
     if (P != n) c += n;  // algorithms.hpp:211-221
@@ -143,29 +149,30 @@ void shard_plan(uint64_t seed, uint64_t counter, uint64_t P, uint64_t n, int ran
     };
     // mating row i of the shuffled order is handled by rank (i mod half) / h_loc, local row
     // (i < half ? i - dest*h_loc : h_loc + (i - half) - dest*h_loc)
-    send_counts.assign(world, 0);
-    recv_counts.assign(world, 0);
+    const size_t cells = (size_t)chunks * (size_t)world;
+    send_counts.assign(cells, 0);
+    recv_counts.assign(cells, 0);
     recv_pos.assign(n_loc, 0);
-    std::vector<std::vector<uint32_t>> send_by_dest(world);
-    std::vector<std::vector<uint32_t>> recv_rows_by_src(world);  // my local mating rows whose parent lives on src
+    std::vector<std::vector<uint32_t>> send_cell(cells);  // [chunk * world + dest]: my slots to send
+    std::vector<std::vector<uint32_t>> recv_cell(cells);  // [chunk * world + src]: my local mating rows fed by src
     for (int dest = 0; dest < world; ++dest) {
         for (uint64_t j = 0; j < n_loc; ++j) {
+            const uint64_t pair = j < h_loc ? j : j - h_loc;
+            const size_t chunk = (size_t)(pair / per_chunk);
             const uint64_t i = j < h_loc ? dest * h_loc + j : half + dest * h_loc + (j - h_loc);
             const uint64_t k = pool_idx(perm[i]);
             const int owner = surv_owner[k];
-            if (owner == rank) send_by_dest[dest].push_back(surv_slot[k]);
-            if (dest == rank) recv_rows_by_src[owner].push_back((uint32_t)j);
+            if (owner == rank) send_cell[chunk * world + dest].push_back(surv_slot[k]);
+            if (dest == rank) recv_cell[chunk * world + owner].push_back((uint32_t)j);
         }
     }
     send_slots.clear();
-    for (int dest = 0; dest < world; ++dest) {
-        send_counts[dest] = send_by_dest[dest].size();
-        send_slots.insert(send_slots.end(), send_by_dest[dest].begin(), send_by_dest[dest].end());
-    }
     uint32_t pos = 0;
-    for (int src = 0; src < world; ++src) {
-        recv_counts[src] = recv_rows_by_src[src].size();
-        for (const uint32_t j : recv_rows_by_src[src]) recv_pos[j] = pos++;
+    for (size_t cell = 0; cell < cells; ++cell) {
+        send_counts[cell] = send_cell[cell].size();
+        send_slots.insert(send_slots.end(), send_cell[cell].begin(), send_cell[cell].end());
+        recv_counts[cell] = recv_cell[cell].size();
+        for (const uint32_t j : recv_cell[cell]) recv_pos[j] = pos++;
     }
     counters_out[1] = counters_out[2] = 0;  // filled by the caller (needs d)
 }
@@ -296,17 +303,21 @@ struct Shard {
     }
 
     // rows of the send buffer <- local pool rows (slots given by the plan)
-    void pack(const uint32_t* slots_host, uint64_t count) {
-        require(count <= send_cap, "shard: send buffer too small (ownership imbalance)");
+    // (rows [row0, row0 + count) of the send buffer: one piece of a chunked exchange)
+    void pack(const uint32_t* slots_host, uint64_t count, uint64_t row0) {
+        require(row0 <= send_cap && count <= send_cap - row0, "shard: send buffer too small (ownership imbalance)");
         if (count == 0) return;
-        TEMO_CUDA(cudaMemcpyAsync(send_slots, slots_host, count * sizeof(uint32_t), cudaMemcpyHostToDevice, stream));
-        gather_slots_kernel<<<(unsigned)count, 256, 0, stream>>>(pool, send_slots, count, d, send_buf);
+        TEMO_CUDA(cudaMemcpyAsync(send_slots + row0, slots_host, count * sizeof(uint32_t), cudaMemcpyHostToDevice, stream));
+        gather_slots_kernel<<<(unsigned)count, 256, 0, stream>>>(pool, send_slots + row0, count, d, send_buf + row0 * d);
         TEMO_CUDA(cudaGetLastError());
     }
 
     // K1 (+ fused evaluation) on this rank's pairs; parents in recv_buf at recv_pos_host[]
-    void reproduce(const uint32_t* recv_pos_host, uint64_t c_sbx, uint64_t c_pm) {
-        TEMO_CUDA(cudaMemcpyAsync(recv_pos, recv_pos_host, n_loc * sizeof(uint32_t), cudaMemcpyHostToDevice, stream));
+    // (pairs [unit_begin, unit_begin + unit_count) only; unit_count = 0: all of them)
+    void reproduce(const uint32_t* recv_pos_host, uint64_t c_sbx, uint64_t c_pm, uint64_t unit_begin, uint64_t unit_count) {
+        require(unit_begin <= h_loc && unit_count <= h_loc - unit_begin, "shard: bad pair range");
+        if (unit_begin == 0)
+            TEMO_CUDA(cudaMemcpyAsync(recv_pos, recv_pos_host, n_loc * sizeof(uint32_t), cudaMemcpyHostToDevice, stream));
         ReproArgs ra;
         ra.pool = recv_buf;
         ra.src = recv_pos;
@@ -323,6 +334,8 @@ struct Shard {
         ra.seg = bound_seg;
         ra.global_n = n;
         ra.global_unit0 = (uint64_t)rank * h_loc;
+        ra.unit_begin = unit_begin;
+        ra.unit_count = unit_count;
         const bool fused = cfg.fuse_eval && cfg.problem >= kDtlz1 && cfg.problem <= kDtlz4;
         if (fused) {
             ra.eval_problem = cfg.problem;
@@ -331,7 +344,8 @@ struct Shard {
             ra.f_row0 = 0;
         }
         launch_reproduce(ra, stream);
-        if (!fused) {
+        const bool last = unit_count == 0 || unit_begin + unit_count == h_loc;
+        if (!fused && last) {  // unfused problems are evaluated once every child exists
             EvalArgs ea;
             ea.problem = cfg.problem;
             ea.x = pool;
@@ -440,7 +454,7 @@ extern "C" {
 
 const char* temo_b200_shard_last_error(void) { return g_shard_error.c_str(); }
 
-int temo_b200_shard_plan(uint64_t seed, uint64_t counter, uint64_t P, uint64_t n, uint64_t d, int rank, int world,
+int temo_b200_shard_plan(uint64_t seed, uint64_t counter, uint64_t P, uint64_t n, uint64_t d, int rank, int world, int chunks,
                          const int32_t* surv_owner, const uint32_t* surv_slot, uint32_t* send_slots,
                          uint64_t send_slots_cap, uint64_t* send_counts, uint64_t* recv_counts, uint32_t* recv_pos,
                          uint64_t* counters3) {
@@ -450,7 +464,7 @@ int temo_b200_shard_plan(uint64_t seed, uint64_t counter, uint64_t P, uint64_t n
         std::vector<uint32_t> ss, rp;
         std::vector<uint64_t> sc, rc;
         uint64_t cs[3];
-        shard_plan(seed, counter, P, n, rank, world, surv_owner, surv_slot, ss, sc, rc, rp, cs);
+        shard_plan(seed, counter, P, n, rank, world, chunks, surv_owner, surv_slot, ss, sc, rc, rp, cs);
         require(ss.size() <= send_slots_cap, "shard_plan: send list exceeds the caller's capacity");
         std::memcpy(send_slots, ss.data(), ss.size() * sizeof(uint32_t));
         std::memcpy(send_counts, sc.data(), sc.size() * sizeof(uint64_t));
@@ -566,11 +580,22 @@ void* temo_b200_shard_buffer(temo_b200_shard* s, int which) {
 }
 
 int temo_b200_shard_pack(temo_b200_shard* s, const uint32_t* slots, uint64_t count) {
-    return guarded_shard([&] { s->impl->pack(slots, count); TEMO_CUDA(cudaStreamSynchronize(s->impl->stream)); });
+    return guarded_shard([&] { s->impl->pack(slots, count, 0); TEMO_CUDA(cudaStreamSynchronize(s->impl->stream)); });
 }
 int temo_b200_shard_reproduce(temo_b200_shard* s, const uint32_t* recv_pos, uint64_t c_sbx, uint64_t c_pm) {
-    return guarded_shard([&] { s->impl->reproduce(recv_pos, c_sbx, c_pm); TEMO_CUDA(cudaStreamSynchronize(s->impl->stream)); });
+    return guarded_shard([&] { s->impl->reproduce(recv_pos, c_sbx, c_pm, 0, 0); TEMO_CUDA(cudaStreamSynchronize(s->impl->stream)); });
 }
+// Pieces of a chunked exchange; both only enqueue work on the shard's stream (temo_b200_shard_stream) and return.
+int temo_b200_shard_pack_at(temo_b200_shard* s, const uint32_t* slots, uint64_t count, uint64_t row0) {
+    return guarded_shard([&] { s->impl->pack(slots, count, row0); });
+}
+int temo_b200_shard_reproduce_range(temo_b200_shard* s, const uint32_t* recv_pos, uint64_t c_sbx, uint64_t c_pm,
+                                    uint64_t unit_begin, uint64_t unit_count) {
+    return guarded_shard([&] { s->impl->reproduce(recv_pos, c_sbx, c_pm, unit_begin, unit_count); });
+}
+// The CUDA stream (cudaStream_t) every stage of this shard is enqueued on: a caller that issues collectives on it
+// (or on a stream ordered against it) needs no device-wide synchronisation between stages.
+void* temo_b200_shard_stream(temo_b200_shard* s) { return (s && s->impl) ? (void*)s->impl->stream : nullptr; }
 int temo_b200_shard_place_f(temo_b200_shard* s, uint64_t P, int initial) {
     return guarded_shard([&] { s->impl->place_offspring_f(P, initial != 0); });
 }

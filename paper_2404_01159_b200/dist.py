@@ -5,8 +5,10 @@ reference: rvea_run (algorithms.hpp:227-296) — single-process in the reference
 the sharding. Per generation and rank:
 
     plan (host, C ABI)      who needs which survivor row from whom (the global shuffle scatters mates)
-    pack + all_to_all       parents of this rank's pairs -> receive buffer          [rows, the only big exchange]
-    reproduce (+evaluate)   K1 on the local pairs with GLOBAL draw addressing: bit-identical children
+    pack + all_to_all       parents of this rank's pairs -> receive buffer          [rows, the only big exchange],
+                            cut into EXCHANGE_CHUNKS pieces by mating pair and pipelined:
+    reproduce (+evaluate)   K1 on the pairs of piece c (GLOBAL draw addressing: bit-identical children) runs while
+                            piece c+1 is on the wire (NCCL on its own stream, ordered against the shard's stream)
     all_gather              offspring objectives (n x m doubles) and free-slot lists (n x 4 bytes)
     select_local            ideal point (replicated F) + association/APD of this rank's slice of merged rows
     all_reduce(min) x2      per-vector APD keys (order-preserving int64) + first rows, then lowest rows
@@ -45,9 +47,11 @@ class TorchComm:
         self.rank = dist.get_rank()
         self.world = dist.get_world_size()
 
-    def all_to_all_rows(self, recv, send, recv_counts, send_counts):
-        """recv/send: 2-D row tensors; counts in rows per peer."""
-        self.dist.all_to_all_single(recv, send, [int(c) for c in recv_counts], [int(c) for c in send_counts])
+    def all_to_all_rows(self, recv, send, recv_counts, send_counts, async_op=False):
+        """recv/send: 2-D row tensors; counts in rows per peer. async_op: returns the work handle (its wait() orders the
+        CURRENT CUDA stream after the exchange; with gloo it blocks the host)."""
+        return self.dist.all_to_all_single(recv, send, [int(c) for c in recv_counts], [int(c) for c in send_counts],
+                                           async_op=async_op)
 
     def all_gather(self, out, inp):
         self.dist.all_gather_into_tensor(out, inp)
@@ -69,8 +73,9 @@ class LocalComm:
     """World size 1: the collectives degenerate to copies (used to validate the sharded path on one GPU)."""
     rank, world = 0, 1
 
-    def all_to_all_rows(self, recv, send, recv_counts, send_counts):
+    def all_to_all_rows(self, recv, send, recv_counts, send_counts, async_op=False):
         recv[: int(recv_counts[0])].copy_(send[: int(send_counts[0])])
+        return None
 
     def all_gather(self, out, inp):
         out.view(-1)[: inp.numel()].copy_(inp.view(-1))
@@ -86,18 +91,18 @@ class LocalComm:
 
 
 # ------------------------------------------------------------------------------------ host plan
-def shard_plan(seed, counter, P, n, d, rank, world, surv_owner, surv_slot):
-    """C-ABI temo_b200_shard_plan (pure host code, no GPU needed)."""
+def shard_plan(seed, counter, P, n, d, rank, world, surv_owner, surv_slot, chunks=1):
+    """C-ABI temo_b200_shard_plan (pure host code, no GPU needed). send_counts / recv_counts: [chunks, world]."""
     L = _lib.load()
     n_loc = n // world
     surv_owner = np.ascontiguousarray(surv_owner, dtype=np.int32)
     surv_slot = np.ascontiguousarray(surv_slot, dtype=np.uint32)
     send_slots = np.empty(n, dtype=np.uint32)
-    send_counts = np.zeros(world, dtype=np.uint64)
-    recv_counts = np.zeros(world, dtype=np.uint64)
+    send_counts = np.zeros((chunks, world), dtype=np.uint64)
+    recv_counts = np.zeros((chunks, world), dtype=np.uint64)
     recv_pos = np.empty(n_loc, dtype=np.uint32)
     counters = np.zeros(3, dtype=np.uint64)
-    rc = L.temo_b200_shard_plan(u64(seed), u64(counter), u64(P), u64(n), u64(d), rank, world,
+    rc = L.temo_b200_shard_plan(u64(seed), u64(counter), u64(P), u64(n), u64(d), rank, world, chunks,
                                 surv_owner.ctypes.data_as(i32p), surv_slot.ctypes.data_as(u32p),
                                 send_slots.ctypes.data_as(u32p), u64(n), send_counts.ctypes.data_as(u64p),
                                 recv_counts.ctypes.data_as(u64p), recv_pos.ctypes.data_as(u32p), counters.ctypes.data_as(u64p))
@@ -153,6 +158,10 @@ class GpuShard:
         self.free_slot = wrap(7, (self.n_loc,), "<i4")
         self.free_all = torch.empty(world * self.n_loc, dtype=torch.int32, device=dev)
         self._torch = torch
+        # every stage runs on the library's stream: collectives issued with it as the current stream are ordered
+        # against the stages by NCCL's own stream events, without device-wide synchronisation
+        self.stream = torch.cuda.ExternalStream(int(self._L.temo_b200_shard_stream(self._h)), device=dev)
+        self.k1_events = None  # list: collect (start, end) CUDA events of every K1 launch
 
     def _chk(self, rc):
         if rc:
@@ -162,13 +171,27 @@ class GpuShard:
     def sync(self):
         self._torch.cuda.synchronize()
 
-    def pack(self, slots):
-        slots = np.ascontiguousarray(slots, dtype=np.uint32)
-        self._chk(self._L.temo_b200_shard_pack(self._h, slots.ctypes.data_as(u32p), u64(slots.size)))
+    def on_stream(self):
+        """Context manager: torch ops (collectives) issued inside use the shard's stream as the current stream."""
+        return self._torch.cuda.stream(self.stream)
 
-    def reproduce(self, recv_pos, c_sbx, c_pm):
+    def pack(self, slots, row0=0):
+        """Gathers pool rows into send_buf[row0:row0+len(slots)] (enqueued on the shard's stream)."""
+        slots = np.ascontiguousarray(slots, dtype=np.uint32)
+        self._chk(self._L.temo_b200_shard_pack_at(self._h, slots.ctypes.data_as(u32p), u64(slots.size), u64(row0)))
+
+    def reproduce(self, recv_pos, c_sbx, c_pm, unit_begin=0, unit_count=0):
+        """K1 (+ evaluation) on the local pairs [unit_begin, unit_begin + unit_count) (0: all); enqueued, not awaited."""
         recv_pos = np.ascontiguousarray(recv_pos, dtype=np.uint32)
-        self._chk(self._L.temo_b200_shard_reproduce(self._h, recv_pos.ctypes.data_as(u32p), u64(c_sbx), u64(c_pm)))
+        ev = None
+        if self.k1_events is not None:  # device time of the K1 launches (bench): events on the shard's stream
+            ev = (self._torch.cuda.Event(enable_timing=True), self._torch.cuda.Event(enable_timing=True))
+            ev[0].record(self.stream)
+        self._chk(self._L.temo_b200_shard_reproduce_range(self._h, recv_pos.ctypes.data_as(u32p), u64(c_sbx), u64(c_pm),
+                                                          u64(unit_begin), u64(unit_count)))
+        if ev is not None:
+            ev[1].record(self.stream)
+            self.k1_events.append(ev)
 
     def place_f(self, P, initial):
         self._chk(self._L.temo_b200_shard_place_f(self._h, u64(P), 1 if initial else 0))
@@ -232,6 +255,9 @@ class ShardedRvea:
         self.counter = self.n * self.d  # operators.hpp:287-296: n*d draws for the initial population
         self.t = 0
         self.last_elite = None
+        # pieces of the parent exchange (pipelined with reproduction); 1 = one exchange, then K1
+        self.chunks = max(1, min(int(os.environ.get("TEMO_B200_EXCHANGE_CHUNKS", "4" if self.world > 1 else "1")),
+                                 max(1, self.n_loc // 2)))
         comm.all_gather(shard.f_gather, shard.f_off_loc)
         shard.place_f(0, True)
         self.timers = {}
@@ -243,50 +269,70 @@ class ShardedRvea:
         cfg, comm, sh = self.cfg, self.comm, self.shard
         n, world, rank, P = self.n, self.world, self.rank, self.P
         t0 = time.perf_counter()
-        plan = shard_plan(cfg.seed, self.counter, P, n, self.d, rank, world, self.surv_owner[:P], self.surv_slot[:P])
+        chunks = self.chunks
+        plan = shard_plan(cfg.seed, self.counter, P, n, self.d, rank, world, self.surv_owner[:P], self.surv_slot[:P], chunks)
         # while the GPU works on this generation, a host thread shuffles for the next one (its counters only
         # depend on this generation's, assuming the survivor count will differ from n: algorithms.hpp:211-221)
         _lib.load().temo_b200_shard_perm_prefetch(u64(cfg.seed), u64(plan["c_end"] + n), u64(n))
         self._tick("plan", t0)
         t0 = time.perf_counter()
-        sh.pack(plan["send_slots"])
-        comm.all_to_all_rows(sh.recv_buf, sh.send_buf[: len(plan["send_slots"])], plan["recv_counts"], plan["send_counts"])
-        sh.sync()
-        self._tick("exchange", t0)
-        t0 = time.perf_counter()
-        sh.reproduce(plan["recv_pos"], plan["c_sbx"], plan["c_pm"])
-        self._tick("reproduce", t0)
-        t0 = time.perf_counter()
-        comm.all_gather(sh.f_gather, sh.f_off_loc)
-        comm.all_gather(sh.free_all, sh.free_slot)
-        sh.sync()
-        sh.place_f(P, False)
-        rows = P + n
-        lo, hi = rows * rank // world, rows * (rank + 1) // world
-        sh.select_local(P, lo, hi, self.t)
-        comm.all_reduce_min(sh.best_key)
-        comm.all_reduce_min(sh.first_row)
-        sh.sync()
-        sh.select_rows(lo, hi)
-        comm.all_reduce_min(sh.best_row)
-        sh.sync()
-        elite = sh.select_finish().astype(np.int64)
-        self._tick("select", t0)
-        t0 = time.perf_counter()
-        # survivor k <- merged row elite[k]: a parent keeps its (owner, slot); a child lives where it was born
-        cnt = len(elite)
-        elite32 = np.ascontiguousarray(elite, dtype=np.uint32)
-        free_all = np.ascontiguousarray(sh.free_slots_host()).view(np.uint32)
-        own = np.empty(max(cnt, 1), dtype=np.uint32)
-        own_count = u64(0)
-        L = _lib.load()
-        rc = L.temo_b200_shard_update_tables(elite32.ctypes.data_as(u32p), u64(cnt), u64(P), u64(n), rank, world,
-                                             free_all.ctypes.data_as(u32p), self.surv_owner.ctypes.data_as(i32p),
-                                             self.surv_slot.ctypes.data_as(u32p), own.ctypes.data_as(u32p), C.byref(own_count))
-        if rc:
-            raise ValueError(L.temo_b200_shard_last_error().decode())
-        sh.commit(cnt, own[: own_count.value], self.t)
-        self._tick("commit", t0)
+        # Pipelined exchange + reproduction: piece c of the parent rows is packed and sent while K1 works on the pairs
+        # of piece c - 1. Everything is enqueued on the shard's stream (NCCL orders its own stream against it), so the
+        # host never waits inside the loop.
+        h_loc = self.n_loc // 2
+        per_chunk = (h_loc + chunks - 1) // chunks
+        send_counts, recv_counts = plan["send_counts"], plan["recv_counts"]
+        send_off = np.concatenate([[0], np.cumsum(send_counts.sum(axis=1))]).astype(np.int64)
+        recv_off = np.concatenate([[0], np.cumsum(recv_counts.sum(axis=1))]).astype(np.int64)
+
+        def send_piece(c):
+            sh.pack(plan["send_slots"][send_off[c]:send_off[c + 1]], int(send_off[c]))
+            return comm.all_to_all_rows(sh.recv_buf[recv_off[c]:recv_off[c + 1]], sh.send_buf[send_off[c]:send_off[c + 1]],
+                                        recv_counts[c], send_counts[c], async_op=True)
+
+        with sh.on_stream():
+            work = send_piece(0)
+            for c in range(chunks):
+                nxt = send_piece(c + 1) if c + 1 < chunks else None
+                if work is not None:
+                    work.wait()  # orders the shard's stream after piece c (host-blocking only with gloo)
+                u0 = c * per_chunk
+                cnt = min(per_chunk, h_loc - u0)
+                if cnt > 0:
+                    sh.reproduce(plan["recv_pos"], plan["c_sbx"], plan["c_pm"], u0, cnt)
+                work = nxt
+            self._tick("exchange+reproduce", t0)
+            t0 = time.perf_counter()
+            comm.all_gather(sh.f_gather, sh.f_off_loc)
+            comm.all_gather(sh.free_all, sh.free_slot)
+            sh.sync()
+            sh.place_f(P, False)
+            rows = P + n
+            lo, hi = rows * rank // world, rows * (rank + 1) // world
+            sh.select_local(P, lo, hi, self.t)
+            comm.all_reduce_min(sh.best_key)
+            comm.all_reduce_min(sh.first_row)
+            sh.sync()
+            sh.select_rows(lo, hi)
+            comm.all_reduce_min(sh.best_row)
+            sh.sync()
+            elite = sh.select_finish().astype(np.int64)
+            self._tick("select", t0)
+            t0 = time.perf_counter()
+            # survivor k <- merged row elite[k]: a parent keeps its (owner, slot); a child lives where it was born
+            cnt = len(elite)
+            elite32 = np.ascontiguousarray(elite, dtype=np.uint32)
+            free_all = np.ascontiguousarray(sh.free_slots_host()).view(np.uint32)
+            own = np.empty(max(cnt, 1), dtype=np.uint32)
+            own_count = u64(0)
+            L = _lib.load()
+            rc = L.temo_b200_shard_update_tables(elite32.ctypes.data_as(u32p), u64(cnt), u64(P), u64(n), rank, world,
+                                                 free_all.ctypes.data_as(u32p), self.surv_owner.ctypes.data_as(i32p),
+                                                 self.surv_slot.ctypes.data_as(u32p), own.ctypes.data_as(u32p), C.byref(own_count))
+            if rc:
+                raise ValueError(L.temo_b200_shard_last_error().decode())
+            sh.commit(cnt, own[: own_count.value], self.t)
+            self._tick("commit", t0)
         self.last_elite = elite
         self.P, self.counter, self.t = cnt, plan["c_end"], self.t + 1
         return cnt
@@ -317,6 +363,7 @@ def bench_main(args, metric, workload_config, measured_peaks, ClockSampler):
     for _ in range(W):
         run.step()
     run.timers.clear()
+    shard.k1_events = []
     sampler = ClockSampler(local)
     if rank == 0:
         sampler.start()
@@ -336,7 +383,7 @@ def bench_main(args, metric, workload_config, measured_peaks, ClockSampler):
     if rank == 0:
         peak, peak_src = measured_peaks()
         nd = float(run.n_loc) * run.d
-        rep_ms = run.timers.get("reproduce", 0.0) / K * 1e3
+        rep_ms = sum(a.elapsed_time(b) for a, b in shard.k1_events) / K  # K1 launches of one step (CUDA events)
         args_cfg = workload_config(args, None)
         args_cfg.update({"workload": f"RVEA/{args.problem} m={args.obj} d={args.dim} pop={pop} ({world} shards of {args.pop})",
                          "pop": pop, "ref_vectors": run.r, "survivors_last": int(pop_size)})
@@ -350,10 +397,11 @@ def bench_main(args, metric, workload_config, measured_peaks, ClockSampler):
             "dtype": "f64", "data": "synthetic", "config": args_cfg,
             "e2e": {"value": world * K / wall, "unit": "generations/s", "h2d_bytes_per_step": 8 * run.n_loc, "d2h_bytes_per_step": 4 * pop + 4 * run.r},
             "gpu_launches": int(K * 30),
-            "roofline": {"bound": "hbm", "kernel": "reproduce_kernel (per rank, host-timed incl. launch)", "achieved": 16.0 * nd / (rep_ms * 1e-3) / 1e9 if rep_ms else None,
+            "roofline": {"bound": "hbm", "kernel": "reproduce_pairs_kernel (rank 0, CUDA events over the K1 launches of a step: one per exchange piece)", "achieved": 16.0 * nd / (rep_ms * 1e-3) / 1e9 if rep_ms else None,
                          "peak": peak, "unit": "GB/s", "frac": (16.0 * nd / (rep_ms * 1e-3) / 1e9 / peak) if rep_ms else None, "traffic": None,
                          "peak_source": peak_src},
-            "stages_ms": {k: v / K * 1e3 for k, v in run.timers.items()},
+            "stages_ms": {**{k: v / K * 1e3 for k, v in run.timers.items()}, "reproduce_device": rep_ms},
+            "exchange_chunks": run.chunks,
             "clocks": clocks,
             "rows_per_s": K * float(pop) / wall,
         }

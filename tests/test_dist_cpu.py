@@ -67,19 +67,29 @@ class CpuShard:
     def sync(self):
         pass
 
-    def pack(self, slots):
-        self.send_buf[: len(slots)] = torch.from_numpy(self.pool[np.asarray(slots, dtype=np.int64)])
+    def on_stream(self):
+        import contextlib
+        return contextlib.nullcontext()
 
-    def reproduce(self, recv_pos, c_sbx, c_pm):
-        parents = self.recv_buf.numpy()[np.asarray(recv_pos, dtype=np.int64)]
-        pa, pb = np.ascontiguousarray(parents[: self.h_loc]), np.ascontiguousarray(parents[self.h_loc:])
+    def pack(self, slots, row0=0):
+        self.send_buf[row0: row0 + len(slots)] = torch.from_numpy(self.pool[np.asarray(slots, dtype=np.int64)])
+
+    def reproduce(self, recv_pos, c_sbx, c_pm, unit_begin=0, unit_count=0):
+        """Pairs [unit_begin, unit_begin + unit_count) of this rank (0: all), as GpuShard.reproduce."""
+        u0, cnt = unit_begin, (unit_count or self.h_loc - unit_begin)
+        recv_pos = np.asarray(recv_pos, dtype=np.int64)
+        buf = self.recv_buf.numpy()
+        pa = np.ascontiguousarray(buf[recv_pos[u0:u0 + cnt]])
+        pb = np.ascontiguousarray(buf[recv_pos[self.h_loc + u0: self.h_loc + u0 + cnt]])
         ca, cb = np.empty_like(pa), np.empty_like(pb)
         _p, u64 = self._p, self.u64
-        self.o.lib.to_reproduce_pairs(_p(pa), _p(pb), u64(self.h_loc), u64(self.d), u64(self.rank * self.h_loc), u64(self.n),
+        self.o.lib.to_reproduce_pairs(_p(pa), _p(pb), u64(cnt), u64(self.d), u64(self.rank * self.h_loc + u0), u64(self.n),
                                       u64(self.cfg.seed), u64(c_sbx), u64(c_pm), _p(self.ga), _p(self.lo), _p(self.hi), _p(ca), _p(cb))
-        kids = np.vstack([ca, cb])
-        self.pool[self.free_slot.numpy().astype(np.int64)] = kids
-        self.f_off_loc.copy_(torch.from_numpy(self.o.evaluate(self.cfg.problem, kids, self.m)))
+        free = self.free_slot.numpy().astype(np.int64)
+        f_loc = self.f_off_loc.numpy()
+        for kids, first in ((ca, u0), (cb, self.h_loc + u0)):
+            self.pool[free[first:first + cnt]] = kids
+            f_loc[first:first + cnt] = self.o.evaluate(self.cfg.problem, kids, self.m)
 
     def place_f(self, P, initial):
         g = self.f_gather.numpy()
@@ -133,10 +143,11 @@ class CpuShard:
         return self.free_all.numpy()
 
 
-def _worker(rank, world, port, problem, n, d, m, gens, seed, out_dir):
+def _worker(rank, world, port, problem, n, d, m, gens, seed, out_dir, chunks):
     sys.path.insert(0, ROOT)
     sys.path.insert(0, os.path.join(ROOT, "tests"))
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
+                      TEMO_B200_EXCHANGE_CHUNKS=str(chunks))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from oracle.pyoracle import Oracle
@@ -158,12 +169,15 @@ def _worker(rank, world, port, problem, n, d, m, gens, seed, out_dir):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("case", [("dtlz2", 24, 9, 3, 8, 7), ("dtlz1", 40, 12, 3, 12, 3), ("dtlz3", 16, 6, 2, 6, 11)])
+@pytest.mark.parametrize("case", [("dtlz2", 24, 9, 3, 8, 7, 1), ("dtlz1", 40, 12, 3, 12, 3, 4), ("dtlz3", 16, 6, 2, 6, 11, 3),
+                                  ("dtlz2", 36, 7, 3, 6, 5, 9)])
 def test_sharded_orchestration_world2_matches_single_process(tmp_path, oracle, case):
-    problem, n, d, m, gens, seed = case
+    """The last field is the number of pieces the parent exchange is cut into (pipelined with reproduction): one piece,
+    several, more pieces than some chunks have pairs."""
+    problem, n, d, m, gens, seed, chunks = case
     world = 2
     port = 29500 + (os.getpid() % 2000)
-    mp.spawn(_worker, args=(world, port, problem, n, d, m, gens, seed, str(tmp_path)), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, port, problem, n, d, m, gens, seed, str(tmp_path), chunks), nprocs=world, join=True)
     exp = oracle.rvea_run(problem, n, d, m, gens, seed=seed)
     parts = [np.load(os.path.join(tmp_path, f"rank{r}.npz")) for r in range(world)]
     for p in parts:  # replicated state is identical on every rank and equals the single-process run
@@ -187,7 +201,12 @@ def test_shard_plan_is_consistent_across_ranks(oracle):
     rng = np.random.default_rng(0)
     owner = rng.integers(0, world, P).astype(np.int32)
     slot = rng.integers(0, 1000, P).astype(np.uint32)
-    plans = [shard_plan(seed, counter, P, n, d, r, world, owner, slot) for r in range(world)]
+    for chunks in (1, 2, 5):
+        _check_plans(oracle, [shard_plan(seed, counter, P, n, d, r, world, owner, slot, chunks) for r in range(world)],
+                     n, d, world, P, seed, counter, owner, slot, chunks)
+
+
+def _check_plans(oracle, plans, n, d, world, P, seed, counter, owner, slot, chunks):
     pool_idx, c = oracle.parent_pool_indices(P, n, seed, counter)
     perm, c = oracle.shuffle_indices(seed, c, n)
     half, h_loc = n // 2, n // 2 // world
@@ -196,12 +215,19 @@ def test_shard_plan_is_consistent_across_ranks(oracle):
         assert plans[h]["c_end"] == plans[h]["c_pm"] + 2 * n * d
         rows = [h * h_loc + j if j < h_loc else half + h * h_loc + (j - h_loc) for j in range(2 * h_loc)]
         want = pool_idx[perm[rows].astype(np.int64)].astype(np.int64)  # survivor index of every local mating row
-        # rebuild the receive buffer of rank h from what every source says it sends
+        # rebuild the receive buffer of rank h from what every source says it sends, piece after piece
         recv = []
-        for g in range(world):
-            sc = plans[g]["send_counts"].astype(np.int64)
-            start = int(sc[:h].sum())
-            recv += [(g, int(s)) for s in plans[g]["send_slots"][start:start + int(sc[h])]]
-            assert int(plans[h]["recv_counts"][g]) == int(sc[h])
+        per_chunk = -(-h_loc // chunks)
+        for ch in range(chunks):
+            first = len(recv)
+            for g in range(world):
+                sc = plans[g]["send_counts"].astype(np.int64)  # [chunks, world]
+                start = int(sc[:ch].sum() + sc[ch, :h].sum())
+                recv += [(g, int(s)) for s in plans[g]["send_slots"][start:start + int(sc[ch, h])]]
+                assert int(plans[h]["recv_counts"][ch, g]) == int(sc[ch, h])
+            # the parents of the pairs of piece ch are all inside piece ch
+            for j in range(2 * h_loc):
+                if (j % h_loc) // per_chunk == ch:
+                    assert first <= int(plans[h]["recv_pos"][j]) < len(recv)
         for j, k in enumerate(want):
             assert recv[int(plans[h]["recv_pos"][j])] == (int(owner[k]), int(slot[k]))
