@@ -155,7 +155,9 @@ void shard_plan(uint64_t seed, uint64_t counter, uint64_t P, uint64_t n, int ran
     recv_pos.assign(n_loc, 0);
     std::vector<std::vector<uint32_t>> send_cell(cells);  // [chunk * world + dest]: my slots to send
     std::vector<std::vector<uint32_t>> recv_cell(cells);  // [chunk * world + src]: my local mating rows fed by src
-    for (int dest = 0; dest < world; ++dest) {
+    // every destination is independent (its own cells; only dest == rank fills the receive cells): one host thread
+    // per destination keeps this O(n) bookkeeping at O(n / world) wall time on every rank
+    auto plan_dest = [&](int dest) {
         for (uint64_t j = 0; j < n_loc; ++j) {
             const uint64_t pair = j < h_loc ? j : j - h_loc;
             const size_t chunk = (size_t)(pair / per_chunk);
@@ -165,6 +167,14 @@ void shard_plan(uint64_t seed, uint64_t counter, uint64_t P, uint64_t n, int ran
             if (owner == rank) send_cell[chunk * world + dest].push_back(surv_slot[k]);
             if (dest == rank) recv_cell[chunk * world + owner].push_back((uint32_t)j);
         }
+    };
+    if (world > 1 && n_loc >= 4096) {
+        std::vector<std::thread> workers;
+        for (int dest = 1; dest < world; ++dest) workers.emplace_back(plan_dest, dest);
+        plan_dest(0);
+        for (auto& w : workers) w.join();
+    } else {
+        for (int dest = 0; dest < world; ++dest) plan_dest(dest);
     }
     send_slots.clear();
     uint32_t pos = 0;
@@ -498,20 +508,36 @@ int temo_b200_shard_update_tables(const uint32_t* elite, uint64_t count, uint64_
         const uint64_t half = n / 2, h_loc = half / world, n_loc = 2 * h_loc;
         std::vector<int32_t> no(count);
         std::vector<uint32_t> ns(count);
-        uint64_t mine = 0;
-        for (uint64_t k = 0; k < count; ++k) {
-            const uint64_t e = elite[k];
-            if (e < P) {
-                no[k] = surv_owner[e];
-                ns[k] = surv_slot[e];
-            } else {
-                const uint64_t i = e - P, p = i < half ? i : i - half;
-                const uint64_t rk = p / h_loc;
-                const uint64_t j = i < half ? p - rk * h_loc : h_loc + p - rk * h_loc;
-                no[k] = (int32_t)rk;
-                ns[k] = free_all[rk * n_loc + j];
+        // ranges of survivors in parallel; the slots owned by `rank` are concatenated in survivor order afterwards
+        const unsigned parts = count >= 65536 ? std::min<unsigned>(8u, std::max(1u, std::thread::hardware_concurrency() / 2)) : 1u;
+        std::vector<std::vector<uint32_t>> mine_part(parts);
+        auto work = [&](unsigned part) {
+            const uint64_t k0 = count * part / parts, k1 = count * (part + 1) / parts;
+            for (uint64_t k = k0; k < k1; ++k) {
+                const uint64_t e = elite[k];
+                if (e < P) {
+                    no[k] = surv_owner[e];
+                    ns[k] = surv_slot[e];
+                } else {
+                    const uint64_t i = e - P, p = i < half ? i : i - half;
+                    const uint64_t rk = p / h_loc;
+                    const uint64_t j = i < half ? p - rk * h_loc : h_loc + p - rk * h_loc;
+                    no[k] = (int32_t)rk;
+                    ns[k] = free_all[rk * n_loc + j];
+                }
+                if (no[k] == rank) mine_part[part].push_back(ns[k]);
             }
-            if (no[k] == rank) own_slots[mine++] = ns[k];
+        };
+        {
+            std::vector<std::thread> workers;
+            for (unsigned part = 1; part < parts; ++part) workers.emplace_back(work, part);
+            work(0);
+            for (auto& w : workers) w.join();
+        }
+        uint64_t mine = 0;
+        for (const auto& v : mine_part) {
+            std::memcpy(own_slots + mine, v.data(), v.size() * sizeof(uint32_t));
+            mine += v.size();
         }
         std::memcpy(surv_owner, no.data(), count * sizeof(int32_t));
         std::memcpy(surv_slot, ns.data(), count * sizeof(uint32_t));

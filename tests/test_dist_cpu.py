@@ -231,3 +231,40 @@ def _check_plans(oracle, plans, n, d, world, P, seed, counter, owner, slot, chun
                     assert first <= int(plans[h]["recv_pos"][j]) < len(recv)
         for j, k in enumerate(want):
             assert recv[int(plans[h]["recv_pos"][j])] == (int(owner[k]), int(slot[k]))
+
+
+def test_shard_plan_and_tables_large_threaded(oracle):
+    """Sizes at which the host bookkeeping runs multi-threaded (one thread per destination / per survivor range):
+    same consistency properties, and the table update equals a straightforward numpy transcription."""
+    import ctypes as C
+    from paper_2404_01159_b200 import _lib
+    from paper_2404_01159_b200.dist import shard_plan, child_location
+    n, d, world, P, seed, counter = 4 * 8192, 3, 4, 30011, 5, 77
+    rng = np.random.default_rng(1)
+    owner = rng.integers(0, world, P).astype(np.int32)
+    slot = rng.integers(0, 50000, P).astype(np.uint32)
+    for chunks in (1, 4):
+        _check_plans(oracle, [shard_plan(seed, counter, P, n, d, r, world, owner, slot, chunks) for r in range(world)],
+                     n, d, world, P, seed, counter, owner, slot, chunks)
+    # survivor tables after a selection that keeps `count` rows of the merged population
+    n, world, P, count, rank = 1 << 17, 4, 100000, 90000, 2
+    n_loc = n // world
+    owner = rng.integers(0, world, max(P, count)).astype(np.int32)
+    slot = rng.integers(0, 1 << 20, max(P, count)).astype(np.uint32)
+    elite = np.sort(rng.choice(P + n, count, replace=False)).astype(np.uint32)
+    free_all = rng.integers(0, 1 << 20, world * n_loc).astype(np.uint32)
+    exp_owner, exp_slot = np.empty(count, np.int32), np.empty(count, np.uint32)
+    par = elite < P
+    exp_owner[par], exp_slot[par] = owner[elite[par]], slot[elite[par]]
+    rk, j = child_location(elite[~par].astype(np.int64) - P, n, world)
+    exp_owner[~par], exp_slot[~par] = rk, free_all[rk.astype(np.int64) * n_loc + j]
+    o, sl = owner.copy(), slot.copy()
+    own = np.empty(count, dtype=np.uint32)
+    own_count = C.c_uint64(0)
+    u32p, i32p = C.POINTER(C.c_uint32), C.POINTER(C.c_int32)
+    rc = _lib.load().temo_b200_shard_update_tables(elite.ctypes.data_as(u32p), C.c_uint64(count), C.c_uint64(P), C.c_uint64(n), rank, world,
+                                                   free_all.ctypes.data_as(u32p), o.ctypes.data_as(i32p), sl.ctypes.data_as(u32p),
+                                                   own.ctypes.data_as(u32p), C.byref(own_count))
+    assert rc == 0
+    assert np.array_equal(o[:count], exp_owner) and np.array_equal(sl[:count], exp_slot)
+    assert np.array_equal(own[: own_count.value], exp_slot[exp_owner == rank])
