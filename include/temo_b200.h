@@ -110,6 +110,20 @@ int temo_b200_polynomial_mutation(const double* x, uint64_t n, uint64_t d, uint6
 int temo_b200_ga_reproduce(const double* x, uint64_t n, uint64_t d, uint64_t seed,
                            uint64_t* counter, const temo_b200_ga_params* ga, const double* lower,
                            const double* upper, int rng_mode, double* out);
+/* ---- the reference's other reproduction operators, host buffers, bit-identical to the
+ * reference (no libm on these paths). `kernel_ms` (optional) receives the device time of the kernels of the call.
+ * de_reproduce (operators.hpp:166-200): DE/rand/1/bin, needs n >= 4; advances *counter by 4 n + n d.
+ * pso_reproduce (operators.hpp:205-240): velocities (n x d), pbest_x (n x d), pbest_score (n) are the SwarmState
+ *   (operators.hpp:46-60), updated in place; `scores` are the caller's scalarised fitness (apd_scores); 2 n d draws.
+ * cso_reproduce (operators.hpp:246-284): shuffle (n - 1 draws) + 3 (n / 2) d draws; velocities updated in place. */
+int temo_b200_de_reproduce(const double* x, uint64_t n, uint64_t d, uint64_t seed, uint64_t* counter, double f, double cr,
+                           const double* lower, const double* upper, int rng_mode, double* out, double* kernel_ms);
+int temo_b200_pso_reproduce(const double* x, const double* scores, uint64_t n, uint64_t d, uint64_t seed, uint64_t* counter,
+                            double inertia, double c1, double c2, double* velocities, double* pbest_x, double* pbest_score,
+                            const double* lower, const double* upper, int rng_mode, double* out, double* kernel_ms);
+int temo_b200_cso_reproduce(const double* x, const double* scores, uint64_t n, uint64_t d, uint64_t seed, uint64_t* counter, double phi,
+                            double* velocities, const double* lower, const double* upper, int rng_mode, double* out,
+                            double* kernel_ms);
 /* random_reproduce (operators.hpp:287-296): n*d draws. */
 int temo_b200_random_reproduce(uint64_t n, uint64_t d, uint64_t seed, uint64_t* counter,
                                const double* lower, const double* upper, int rng_mode, double* out);

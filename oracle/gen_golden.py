@@ -93,6 +93,32 @@ def main():
     ops["rr_counter"] = np.array([crr], dtype=np.uint64)
     np.savez(os.path.join(OUT, "operators.npz"), **ops)
 
+    # ---- DE / PSO / CSO (verify.hpp:117-182, ops 2..4: instance k of master seed 7002; two chained steps each)
+    sw = {}
+    for tag, op, k in (("de0", 2, 0), ("de1", 2, 17), ("pso0", 3, 0), ("pso1", 3, 41), ("cso0", 4, 0), ("cso1", 4, 63)):
+        seed = 7002 + op * 1000003 + k
+        g = Stream(ref, seed)
+        n, d, lower, upper, x = operator_instance(ref, g, 4 if op == 2 else 2, 16, 8)
+        scores = g.tensor(n, 1).reshape(-1)
+        sseed = seed ^ 0xabcdef
+        rec = dict(x=x, lower=lower, upper=upper, scores=scores, seed=np.array([sseed], dtype=np.uint64))
+        if op == 2:
+            y1, c1 = ref.de_reproduce(x, sseed, 0, lower, upper)
+            y2, c2 = ref.de_reproduce(y1, sseed, c1, lower, upper, p=(0.8, 0.4))
+            rec.update(y1=y1, y2=y2, counters=np.array([c1, c2], dtype=np.uint64))
+        elif op == 3:
+            vel, pbx, pbs = np.zeros_like(x), x * 0.5, scores + 0.25
+            y1, c1, v1, px1, ps1 = ref.pso_reproduce(x, scores, sseed, 0, lower, upper, vel, pbx, pbs)
+            y2, c2, v2, px2, ps2 = ref.pso_reproduce(y1, scores[::-1].copy(), sseed, c1, lower, upper, v1, px1, ps1)
+            rec.update(y1=y1, y2=y2, v1=v1, v2=v2, px2=px2, ps2=ps2, counters=np.array([c1, c2], dtype=np.uint64))
+        else:
+            y1, c1, v1 = ref.cso_reproduce(x, scores, sseed, 0, lower, upper, np.zeros_like(x))
+            y2, c2, v2 = ref.cso_reproduce(y1, scores[::-1].copy(), sseed, c1, lower, upper, v1)
+            rec.update(y1=y1, y2=y2, v1=v1, v2=v2, counters=np.array([c1, c2], dtype=np.uint64))
+        for key, val in rec.items():
+            sw[f"{tag}_{key}"] = val
+    np.savez(os.path.join(OUT, "swarm.npz"), **sw)
+
     # ---- problems ------------------------------------------------------------------
     pr = {}
     g = Stream(ref, 9100)

@@ -134,6 +134,36 @@ class Oracle(_Base):
         self.lib.to_ga_reproduce.restype = C.c_int
         return self._op(self.lib.to_ga_reproduce, x, seed, counter, ga, lower, upper)
 
+    # ---- DE / PSO / CSO (operators.hpp:166-284); states are copied in and returned
+    def de_reproduce(self, x, seed, counter, lower, upper, p=(0.5, 0.9)):
+        x = _f(x)
+        n, d = x.shape
+        out, c = np.empty_like(x), u64(counter)
+        rc = self.lib.to_de_reproduce(_p(x), u64(n), u64(d), u64(seed), C.byref(c), _p(_f(p)), _p(_f(lower)), _p(_f(upper)), _p(out))
+        if rc:
+            raise ValueError("de_reproduce: needs at least four rows")
+        return out, c.value
+
+    def pso_reproduce(self, x, scores, seed, counter, lower, upper, vel, pb_x, pb_score, p=(0.4, 1.5, 1.5)):
+        x = _f(x)
+        n, d = x.shape
+        vel, pb_x, pb_score = _f(vel).copy(), _f(pb_x).copy(), _f(pb_score).reshape(-1).copy()
+        out, c = np.empty_like(x), u64(counter)
+        self.lib.to_pso_reproduce(_p(x), _p(_f(scores)), u64(n), u64(d), u64(seed), C.byref(c), _p(_f(p)), _p(vel), _p(pb_x),
+                                  _p(pb_score), _p(_f(lower)), _p(_f(upper)), _p(out))
+        return out, c.value, vel, pb_x, pb_score
+
+    def cso_reproduce(self, x, scores, seed, counter, lower, upper, vel, p=(0.1,)):
+        x = _f(x)
+        n, d = x.shape
+        vel = _f(vel).copy()
+        out, c = np.empty_like(x), u64(counter)
+        rc = self.lib.to_cso_reproduce(_p(x), _p(_f(scores)), u64(n), u64(d), u64(seed), C.byref(c), _p(_f(p)), _p(vel),
+                                       _p(_f(lower)), _p(_f(upper)), _p(out))
+        if rc:
+            raise MemoryError("cso_reproduce")
+        return out, c.value, vel
+
     def random_reproduce(self, n, d, seed, counter, lower, upper):
         out = np.empty((n, d))
         c = u64(counter)
@@ -353,6 +383,39 @@ class Ref(_Base):
 
     def ga_reproduce(self, x, seed, counter, lower, upper, ga=GA_DEFAULT, scalar=False):
         return self._op(5 if scalar else 2, x, seed, counter, ga, lower, upper)
+
+    def de_reproduce(self, x, seed, counter, lower, upper, p=(0.5, 0.9), scalar=False):
+        x = _f(x)
+        n, d = x.shape
+        out, c = np.empty_like(x), u64(counter)
+        self._chk(self.lib.ref_de_reproduce(C.c_int(int(scalar)), _p(x), u64(n), u64(d), u64(seed), C.byref(c), _p(_f(p)),
+                                            _p(_f(lower)), _p(_f(upper)), _p(out)))
+        return out, c.value
+
+    def pso_reproduce(self, x, scores, seed, counter, lower, upper, vel, pb_x, pb_score, p=(0.4, 1.5, 1.5), scalar=False):
+        x = _f(x)
+        n, d = x.shape
+        vel, pb_x, pb_score = _f(vel).copy(), _f(pb_x).copy(), _f(pb_score).reshape(-1).copy()
+        out, c = np.empty_like(x), u64(counter)
+        self._chk(self.lib.ref_pso_reproduce(C.c_int(int(scalar)), _p(x), _p(_f(scores)), u64(n), u64(d), u64(seed), C.byref(c),
+                                             _p(_f(p)), _p(vel), _p(pb_x), _p(pb_score), _p(_f(lower)), _p(_f(upper)), _p(out)))
+        return out, c.value, vel, pb_x, pb_score
+
+    def cso_reproduce(self, x, scores, seed, counter, lower, upper, vel, p=(0.1,), scalar=False):
+        x = _f(x)
+        n, d = x.shape
+        vel = _f(vel).copy()
+        out, c = np.empty_like(x), u64(counter)
+        self._chk(self.lib.ref_cso_reproduce(C.c_int(int(scalar)), _p(x), _p(_f(scores)), u64(n), u64(d), u64(seed), C.byref(c),
+                                             _p(_f(p)), _p(vel), _p(_f(lower)), _p(_f(upper)), _p(out)))
+        return out, c.value, vel
+
+    def apd_scores(self, f, v, gamma, t, t_max, alpha=2.0):
+        f, v = _f(f), _f(v)
+        out = np.empty(f.shape[0])
+        self._chk(self.lib.ref_apd_scores(_p(f), u64(f.shape[0]), u64(f.shape[1]), _p(v), _p(_f(gamma)), u64(v.shape[0]), u64(t),
+                                          u64(t_max), C.c_double(alpha), _p(out)))
+        return out
 
     def random_reproduce(self, n, d, seed, counter, lower, upper):
         out = np.empty((n, d))

@@ -141,6 +141,62 @@ int ref_operator(int which, const double* x, std::uint64_t n, std::uint64_t d,
     });
 }
 
+// DE / PSO / CSO (operators.hpp:166-284); batched (scalar == 0) or the reference's scalar oracle (oracle.hpp:206-295)
+int ref_de_reproduce(int scalar, const double* x, std::uint64_t n, std::uint64_t d, std::uint64_t seed, std::uint64_t* counter,
+                     const double* p, const double* lower, const double* upper, double* out) {
+    return guarded([&] {
+        temo::RngStream s{seed, *counter};
+        const temo::Tensor2D xt = wrap(x, n, d), lo = wrap(lower, 1, d), hi = wrap(upper, 1, d);
+        const temo::DeParams dp{p[0], p[1]};
+        namespace orc = temo::oracle;
+        unwrap(scalar ? orc::to_tensor(orc::oracle_de(orc::to_matrix(xt), s, dp, lo.data, hi.data)) : temo::de_reproduce(xt, s, dp, lo, hi), out);
+        *counter = s.counter;
+    });
+}
+
+int ref_pso_reproduce(int scalar, const double* x, const double* scores, std::uint64_t n, std::uint64_t d, std::uint64_t seed,
+                      std::uint64_t* counter, const double* p, double* vel, double* pb_x, double* pb_score, const double* lower,
+                      const double* upper, double* out) {
+    return guarded([&] {
+        temo::RngStream s{seed, *counter};
+        const temo::Tensor2D xt = wrap(x, n, d), lo = wrap(lower, 1, d), hi = wrap(upper, 1, d), sc = wrap(scores, n, 1);
+        temo::SwarmState st{wrap(vel, n, d), wrap(pb_x, n, d), wrap(pb_score, n, 1)};
+        const temo::PsoParams pp{p[0], p[1], p[2]};
+        namespace orc = temo::oracle;
+        unwrap(scalar ? orc::to_tensor(orc::oracle_pso(orc::to_matrix(xt), st, sc.data, s, pp, lo.data, hi.data))
+                      : temo::pso_reproduce(xt, st, sc, s, pp, lo, hi),
+               out);
+        unwrap(st.velocities, vel);
+        unwrap(st.personal_best_x, pb_x);
+        unwrap(st.personal_best_score, pb_score);
+        *counter = s.counter;
+    });
+}
+
+int ref_cso_reproduce(int scalar, const double* x, const double* scores, std::uint64_t n, std::uint64_t d, std::uint64_t seed,
+                      std::uint64_t* counter, const double* p, double* vel, const double* lower, const double* upper, double* out) {
+    return guarded([&] {
+        temo::RngStream s{seed, *counter};
+        const temo::Tensor2D xt = wrap(x, n, d), lo = wrap(lower, 1, d), hi = wrap(upper, 1, d), sc = wrap(scores, n, 1);
+        temo::SwarmState st{wrap(vel, n, d), xt, sc};
+        const temo::CsoParams cp{p[0]};
+        namespace orc = temo::oracle;
+        unwrap(scalar ? orc::to_tensor(orc::oracle_cso(orc::to_matrix(xt), sc.data, s, cp, lo.data, hi.data, st))
+                      : temo::cso_reproduce(xt, sc, s, cp, lo, hi, st),
+               out);
+        unwrap(st.velocities, vel);
+        *counter = s.counter;
+    });
+}
+
+int ref_apd_scores(const double* f, std::uint64_t n, std::uint64_t m, const double* v, const double* gamma, std::uint64_t r,
+                   std::uint64_t t, std::uint64_t t_max, double alpha, double* scores) {
+    return guarded([&] {
+        temo::RefVectorSet refs{wrap(v, r, m), wrap(v, r, m), wrap(gamma, r, 1)};
+        unwrap(temo::apd_scores(wrap(f, n, m), refs, t, t_max, alpha), scores);
+    });
+}
+
 int ref_random_reproduce(std::uint64_t n, std::uint64_t d, std::uint64_t seed,
                          std::uint64_t* counter, const double* lower, const double* upper,
                          double* out) {

@@ -223,6 +223,103 @@ void to_random_reproduce(uint64_t n, uint64_t d, uint64_t seed, uint64_t* counte
     *counter = c + n * d;
 }
 
+/* ------------------------------------------- operators.hpp: DE / PSO / CSO */
+
+/* operators.hpp:166-200, DE/rand/1/bin. p = {f, cr}. Draw blocks: r_sel n x 3, r_j n x 1, r_cr n x d. */
+int to_de_reproduce(const double* x, uint64_t n, uint64_t d, uint64_t seed, uint64_t* counter, const double* p,
+                    const double* lower, const double* upper, double* out) {
+    if (n < 4) return 1;                                                 /* :169 */
+    const uint64_t c_sel = *counter, c_j = c_sel + 3 * n, c_cr = c_j + n;
+    const double nd = (double)n;
+    for (uint64_t i = 0; i < n; ++i) {
+        uint64_t r1 = (i + 1 + (uint64_t)(to_value_at(seed, c_sel + i * 3 + 0) * (nd - 1.0))) % n;   /* :177-178 */
+        const uint64_t excl_a = i < r1 ? i : r1, excl_b = i < r1 ? r1 : i;
+        uint64_t r2 = (uint64_t)(to_value_at(seed, c_sel + i * 3 + 1) * (nd - 2.0));
+        if (r2 >= excl_a) ++r2;
+        if (r2 >= excl_b) ++r2;
+        uint64_t e[3] = {i, r1, r2}, t;                                  /* sorted ascending, :183-184 */
+        if (e[0] > e[1]) t = e[0], e[0] = e[1], e[1] = t;
+        if (e[1] > e[2]) t = e[1], e[1] = e[2], e[2] = t;
+        if (e[0] > e[1]) t = e[0], e[0] = e[1], e[1] = t;
+        uint64_t r3 = (uint64_t)(to_value_at(seed, c_sel + i * 3 + 2) * (nd - 3.0));
+        for (int k = 0; k < 3; ++k)
+            if (r3 >= e[k]) ++r3;
+        const uint64_t j_rand = (uint64_t)(to_value_at(seed, c_j + i) * (double)d);
+        for (uint64_t j = 0; j < d; ++j) {
+            if (to_value_at(seed, c_cr + i * d + j) < p[1] || j == j_rand) {
+                const double trial = x[r1 * d + j] + p[0] * (x[r2 * d + j] - x[r3 * d + j]);        /* :191 */
+                out[i * d + j] = to_clip(trial, lower[j], upper[j]);
+            } else {
+                out[i * d + j] = x[i * d + j];
+            }
+        }
+    }
+    *counter = c_cr + n * d;
+    return 0;
+}
+
+/* operators.hpp:205-240. p = {inertia, c1, c2}; vel, pb_x (n x d) and pb_score (n) are the SwarmState, updated in place. */
+int to_pso_reproduce(const double* x, const double* scores, uint64_t n, uint64_t d, uint64_t seed, uint64_t* counter,
+                     const double* p, double* vel, double* pb_x, double* pb_score, const double* lower, const double* upper,
+                     double* out) {
+    for (uint64_t i = 0; i < n; ++i)
+        if (scores[i] < pb_score[i]) {                                   /* :213-219 */
+            pb_score[i] = scores[i];
+            memcpy(pb_x + i * d, x + i * d, d * sizeof(double));
+        }
+    uint64_t best = 0;
+    for (uint64_t i = 1; i < n; ++i)
+        if (pb_score[i] < pb_score[best]) best = i;                      /* :220-222 */
+    const uint64_t c1 = *counter, c2 = c1 + n * d;
+    const double* gbest = pb_x + best * d;
+    for (uint64_t i = 0; i < n; ++i)
+        for (uint64_t j = 0; j < d; ++j) {
+            const double xv = x[i * d + j];
+            const double v = p[0] * vel[i * d + j] + p[1] * to_value_at(seed, c1 + i * d + j) * (pb_x[i * d + j] - xv) +
+                             p[2] * to_value_at(seed, c2 + i * d + j) * (gbest[j] - xv);            /* :230-232 */
+            vel[i * d + j] = v;
+            out[i * d + j] = to_clip(xv + v, lower[j], upper[j]);
+        }
+    *counter = c2 + n * d;
+    return 0;
+}
+
+/* operators.hpp:246-284. p = {phi}; vel (n x d) updated in place. Shuffle (n - 1 draws), then r1, r2, r3 (pairs x d). */
+int to_cso_reproduce(const double* x, const double* scores, uint64_t n, uint64_t d, uint64_t seed, uint64_t* counter,
+                     const double* p, double* vel, const double* lower, const double* upper, double* out) {
+    uint64_t* perm = (uint64_t*)malloc((n ? n : 1) * sizeof(uint64_t));
+    double* mean = (double*)calloc(d ? d : 1, sizeof(double));
+    double* nv = (double*)malloc((n * d ? n * d : 1) * sizeof(double));
+    if (!perm || !mean || !nv) {
+        free(perm); free(mean); free(nv);
+        return 2;
+    }
+    to_shuffle_indices(seed, counter, n, perm);
+    const uint64_t pairs = n / 2, c1 = *counter, c2 = c1 + pairs * d, c3 = c2 + pairs * d;
+    for (uint64_t i = 0; i < n; ++i)
+        for (uint64_t j = 0; j < d; ++j) mean[j] += x[i * d + j];        /* :257-259 */
+    for (uint64_t j = 0; j < d; ++j) mean[j] /= (double)n;
+    memcpy(out, x, n * d * sizeof(double));
+    memcpy(nv, vel, n * d * sizeof(double));
+    for (uint64_t q = 0; q < pairs; ++q) {
+        const uint64_t a = perm[2 * q], b = perm[2 * q + 1];
+        uint64_t win = a, lose = b;
+        if (scores[b] < scores[a] || (scores[b] == scores[a] && b < a)) win = b, lose = a;          /* :267-271 */
+        for (uint64_t j = 0; j < d; ++j) {
+            const double xl = x[lose * d + j];
+            const double v = to_value_at(seed, c1 + q * d + j) * vel[lose * d + j] +
+                             to_value_at(seed, c2 + q * d + j) * (x[win * d + j] - xl) +
+                             p[0] * to_value_at(seed, c3 + q * d + j) * (mean[j] - xl);             /* :273-275 */
+            nv[lose * d + j] = v;
+            out[lose * d + j] = to_clip(xl + v, lower[j], upper[j]);
+        }
+    }
+    memcpy(vel, nv, n * d * sizeof(double));
+    *counter = c3 + pairs * d;
+    free(perm); free(mean); free(nv);
+    return 0;
+}
+
 /* ----------------------------------------------------------- problems.hpp */
 
 /* problems.hpp:69-92 with the g and shape helpers of :24-64 folded in. */

@@ -57,6 +57,10 @@ SIGNATURES = {
     "temo_b200_polynomial_mutation": (C.c_int, [f64p, u64, u64, u64, u64p, _GA, f64p, f64p, C.c_int, f64p]),
     "temo_b200_ga_reproduce": (C.c_int, [f64p, u64, u64, u64, u64p, _GA, f64p, f64p, C.c_int, f64p]),
     "temo_b200_random_reproduce": (C.c_int, [u64, u64, u64, u64p, f64p, f64p, C.c_int, f64p]),
+    "temo_b200_de_reproduce": (C.c_int, [f64p, u64, u64, u64, u64p, C.c_double, C.c_double, f64p, f64p, C.c_int, f64p, f64p]),
+    "temo_b200_pso_reproduce": (C.c_int, [f64p, f64p, u64, u64, u64, u64p, C.c_double, C.c_double, C.c_double, f64p, f64p, f64p,
+                                          f64p, f64p, C.c_int, f64p, f64p]),
+    "temo_b200_cso_reproduce": (C.c_int, [f64p, f64p, u64, u64, u64, u64p, C.c_double, f64p, f64p, f64p, C.c_int, f64p, f64p]),
     "temo_b200_evaluate": (C.c_int, [C.c_int, f64p, u64, u64, u64, f64p]),
     "temo_b200_problem_bounds": (C.c_int, [C.c_int, u64, u64, f64p, f64p]),
     "temo_b200_problem_default_dim": (u64, [C.c_int, u64]),

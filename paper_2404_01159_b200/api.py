@@ -10,7 +10,9 @@ free functions (reference paths under proj/include/temo/):
     dtlz_eval, ProblemInstance, make_problem             problems.hpp:69-92,246-296
     lattice_count, lattice_density_for, simplex_lattice,
     RefVectorSet, make_ref_set, min_vector_angles, adapt refvec.hpp:15-140
-    SelectionOutcome, rv_select                          selection.hpp:131-135,200-224
+    DeParams, PsoParams, CsoParams, SwarmState, make_swarm_state,
+    de_reproduce, pso_reproduce, cso_reproduce           operators.hpp:28-60,166-284
+    SelectionOutcome, rv_select, apd_scores              selection.hpp:131-135,200-234
     RunConfig, RunRecord, GenerationRow, rvea_run        algorithms.hpp:21-63,144-150,227-296
 
 A ``Tensor2D`` is a C-contiguous float64 numpy array of shape (rows, cols). Contract
@@ -163,6 +165,106 @@ def random_reproduce(n: int, d: int, stream: RngStream, lower, upper) -> np.ndar
     return out
 
 
+# ---- the other reproduction operators (operators.hpp:28-60,166-284)
+@dataclass
+class DeParams:
+    """reference: DeParams (operators.hpp:28-31)."""
+    f: float = 0.5
+    cr: float = 0.9
+
+
+@dataclass
+class PsoParams:
+    """reference: PsoParams (operators.hpp:33-37)."""
+    inertia: float = 0.4
+    c1: float = 1.5
+    c2: float = 1.5
+
+
+@dataclass
+class CsoParams:
+    """reference: CsoParams (operators.hpp:39-41)."""
+    phi: float = 0.1
+
+
+@dataclass
+class SwarmState:
+    """reference: SwarmState (operators.hpp:46-56); the operators update it in place."""
+    velocities: np.ndarray
+    personal_best_x: np.ndarray
+    personal_best_score: np.ndarray
+
+    def empty(self) -> bool:
+        return self.velocities.shape[0] == 0
+
+
+def make_swarm_state(x, scores) -> SwarmState:
+    """reference: make_swarm_state (operators.hpp:58-60)."""
+    x = _t(x)
+    return SwarmState(np.zeros_like(x), x.copy(), _t(scores).reshape(-1).copy())
+
+
+def _bounds(lower, upper, d, who):
+    lower, upper = _t(lower).reshape(-1), _t(upper).reshape(-1)
+    if lower.size != d or upper.size != d:
+        raise ValueError(f"{who}: bounds shape mismatch")
+    return lower, upper
+
+
+def de_reproduce(x, stream: RngStream, p: DeParams, lower, upper, timing: dict | None = None) -> np.ndarray:
+    """reference: de_reproduce (operators.hpp:166-200). `timing["kernel_ms"]` receives the device time."""
+    x = _t(x)
+    n, d = x.shape
+    lower, upper = _bounds(lower, upper, d, "de_reproduce")
+    p = p or DeParams()
+    out, c, ms = np.empty_like(x), u64(stream.counter), C.c_double(0.0)
+    _call(_lib.load().temo_b200_de_reproduce, _p(x), u64(n), u64(d), u64(stream.seed), C.byref(c), C.c_double(p.f), C.c_double(p.cr),
+          _p(lower), _p(upper), stream.mode, _p(out), C.cast(C.byref(ms), _lib.f64p))
+    stream.counter = c.value
+    if timing is not None:
+        timing["kernel_ms"] = ms.value
+    return out
+
+
+def pso_reproduce(x, state: SwarmState, scores, stream: RngStream, p: PsoParams, lower, upper, timing: dict | None = None) -> np.ndarray:
+    """reference: pso_reproduce (operators.hpp:205-240); `state` is updated in place."""
+    x, scores = _t(x), _t(scores).reshape(-1)
+    n, d = x.shape
+    if state.velocities.shape != (n, d) or state.personal_best_x.shape[0] != n or scores.size != n:
+        raise ValueError("pso_reproduce: state shape mismatch")  # operators.hpp:209-211
+    lower, upper = _bounds(lower, upper, d, "pso_reproduce")
+    p = p or PsoParams()
+    vel, pbx, pbs = _t(state.velocities).copy(), _t(state.personal_best_x).copy(), _t(state.personal_best_score).reshape(-1).copy()
+    out, c, ms = np.empty_like(x), u64(stream.counter), C.c_double(0.0)
+    _call(_lib.load().temo_b200_pso_reproduce, _p(x), _p(scores), u64(n), u64(d), u64(stream.seed), C.byref(c), C.c_double(p.inertia),
+          C.c_double(p.c1), C.c_double(p.c2), _p(vel), _p(pbx), _p(pbs), _p(lower), _p(upper), stream.mode, _p(out),
+          C.cast(C.byref(ms), _lib.f64p))
+    stream.counter = c.value
+    state.velocities, state.personal_best_x, state.personal_best_score = vel, pbx, pbs
+    if timing is not None:
+        timing["kernel_ms"] = ms.value
+    return out
+
+
+def cso_reproduce(x, scores, stream: RngStream, p: CsoParams, lower, upper, state: SwarmState, timing: dict | None = None) -> np.ndarray:
+    """reference: cso_reproduce (operators.hpp:246-284); `state.velocities` is updated in place."""
+    x, scores = _t(x), _t(scores).reshape(-1)
+    n, d = x.shape
+    if state.velocities.shape != (n, d) or scores.size != n:
+        raise ValueError("cso_reproduce: state shape mismatch")  # operators.hpp:251-253
+    lower, upper = _bounds(lower, upper, d, "cso_reproduce")
+    p = p or CsoParams()
+    vel = _t(state.velocities).copy()
+    out, c, ms = np.empty_like(x), u64(stream.counter), C.c_double(0.0)
+    _call(_lib.load().temo_b200_cso_reproduce, _p(x), _p(scores), u64(n), u64(d), u64(stream.seed), C.byref(c), C.c_double(p.phi),
+          _p(vel), _p(lower), _p(upper), stream.mode, _p(out), C.cast(C.byref(ms), _lib.f64p))
+    stream.counter = c.value
+    state.velocities = vel
+    if timing is not None:
+        timing["kernel_ms"] = ms.value
+    return out
+
+
 # -------------------------------------------------------------------------- problems.hpp
 def evaluate(problem: str | int, x, m: int) -> np.ndarray:
     pid = PROBLEM_IDS[problem] if isinstance(problem, str) else int(problem)
@@ -300,6 +402,11 @@ def rv_select(f, refs: RefVectorSet, t: int, t_max: int, alpha: float = 2.0) -> 
     _call(_lib.load().temo_b200_rv_select, _p(f), u64(n), u64(m), _p(v), _p(gamma), u64(r), u64(t), u64(t_max),
           C.c_double(alpha), _p(elite, u64p), C.byref(ne), _p(valid, u8p), _p(assoc, u64p), _p(theta), _p(apd))
     return SelectionOutcome(elite[: ne.value].copy(), valid, assoc, theta, apd)
+
+
+def apd_scores(f, refs: RefVectorSet, t: int, t_max: int, alpha: float = 2.0) -> np.ndarray:
+    """reference: apd_scores (selection.hpp:228-234): every row's APD against its associated vector, n x 1."""
+    return rv_select(f, refs, t, t_max, alpha).apd.reshape(-1, 1).copy()
 
 
 # ------------------------------------------------------------------------ algorithms.hpp

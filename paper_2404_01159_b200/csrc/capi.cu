@@ -243,6 +243,105 @@ int temo_b200_ga_reproduce(const double* x, uint64_t n, uint64_t d, uint64_t see
     return guarded([&] { host_operator(true, true, true, x, n, d, seed, counter, ga, lower, upper, rng_mode, out); });
 }
 
+// ---- operators.hpp:166-284: DE / PSO / CSO on host buffers -----------------------
+namespace {
+struct KernelTimer {  // device time of the kernels of one call (CUDA events on the library stream)
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    cudaStream_t s;
+    double* out;
+    KernelTimer(cudaStream_t st, double* o) : s(st), out(o) {
+        if (out) {
+            TEMO_CUDA(cudaEventCreate(&e0));
+            TEMO_CUDA(cudaEventCreate(&e1));
+            TEMO_CUDA(cudaEventRecord(e0, s));
+        }
+    }
+    void stop() {
+        if (out) TEMO_CUDA(cudaEventRecord(e1, s));
+    }
+    void read() {
+        if (!out) return;
+        float ms = 0.f;
+        TEMO_CUDA(cudaEventSynchronize(e1));
+        TEMO_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        *out = ms;
+    }
+    ~KernelTimer() {
+        if (e0) cudaEventDestroy(e0);
+        if (e1) cudaEventDestroy(e1);
+    }
+};
+}  // namespace
+
+int temo_b200_de_reproduce(const double* x, uint64_t n, uint64_t d, uint64_t seed, uint64_t* counter, double f, double cr,
+                           const double* lower, const double* upper, int rng_mode, double* out, double* kernel_ms) {
+    return guarded([&] {
+        require(x && counter && lower && upper && out, "de_reproduce: null argument");
+        require(n >= 4, "de_reproduce: needs at least four rows");  // operators.hpp:169
+        require(d >= 1, "de_reproduce: empty rows");
+        check_mode(rng_mode);
+        cudaStream_t s = ctx().stream;
+        DevBuf<double> dx(x, n * d, s), dlo(lower, d, s), dhi(upper, d, s), dout(n * d);
+        KernelTimer tm(s, kernel_ms);
+        launch_de(dx.p, n, d, make_rng(seed, rng_mode), *counter, f, cr, dlo.p, dhi.p, dout.p, s);
+        tm.stop();
+        dout.to_host(out, s);
+        TEMO_CUDA(cudaStreamSynchronize(s));
+        tm.read();
+        *counter += 4 * n + n * d;  // r_sel n x 3, r_j n x 1, r_cr n x d
+    });
+}
+
+int temo_b200_pso_reproduce(const double* x, const double* scores, uint64_t n, uint64_t d, uint64_t seed, uint64_t* counter,
+                            double inertia, double c1, double c2, double* velocities, double* pbest_x, double* pbest_score,
+                            const double* lower, const double* upper, int rng_mode, double* out, double* kernel_ms) {
+    return guarded([&] {
+        require(x && scores && counter && velocities && pbest_x && pbest_score && lower && upper && out, "pso_reproduce: null argument");
+        require(n >= 1 && d >= 1, "pso_reproduce: state shape mismatch");  // operators.hpp:209-211 (shapes are the caller's)
+        check_mode(rng_mode);
+        cudaStream_t s = ctx().stream;
+        DevBuf<double> dx(x, n * d, s), dsc(scores, n, s), dv(velocities, n * d, s), dpx(pbest_x, n * d, s), dps(pbest_score, n, s),
+            dlo(lower, d, s), dhi(upper, d, s), dout(n * d);
+        DevBuf<uint32_t> best(1);
+        KernelTimer tm(s, kernel_ms);
+        launch_pso(dx.p, dsc.p, n, d, make_rng(seed, rng_mode), *counter, inertia, c1, c2, dv.p, dpx.p, dps.p, best.p, dlo.p, dhi.p,
+                   dout.p, s);
+        tm.stop();
+        dout.to_host(out, s);
+        dv.to_host(velocities, s);
+        dpx.to_host(pbest_x, s);
+        dps.to_host(pbest_score, s);
+        TEMO_CUDA(cudaStreamSynchronize(s));
+        tm.read();
+        *counter += 2 * n * d;
+    });
+}
+
+int temo_b200_cso_reproduce(const double* x, const double* scores, uint64_t n, uint64_t d, uint64_t seed, uint64_t* counter, double phi,
+                            double* velocities, const double* lower, const double* upper, int rng_mode, double* out,
+                            double* kernel_ms) {
+    return guarded([&] {
+        require(x && scores && counter && velocities && lower && upper && out, "cso_reproduce: null argument");
+        require(n >= 1 && n < 0xffffffffULL && d >= 1, "cso_reproduce: state shape mismatch");  // operators.hpp:251-253
+        check_mode(rng_mode);
+        cudaStream_t s = ctx().stream;
+        uint64_t c = *counter;
+        std::vector<uint32_t> perm(n);
+        shuffle_indices(seed, c, n, perm.data());  // n - 1 draws (rng.hpp:69-78)
+        DevBuf<double> dx(x, n * d, s), dsc(scores, n, s), dv(velocities, n * d, s), dlo(lower, d, s), dhi(upper, d, s), dout(n * d),
+            dvo(n * d), dmean(d);
+        DevBuf<uint32_t> dperm(perm.data(), n, s);
+        KernelTimer tm(s, kernel_ms);
+        launch_cso(dx.p, dsc.p, n, d, make_rng(seed, rng_mode), c, phi, dperm.p, dmean.p, dv.p, dvo.p, dlo.p, dhi.p, dout.p, s);
+        tm.stop();
+        dout.to_host(out, s);
+        dvo.to_host(velocities, s);
+        TEMO_CUDA(cudaStreamSynchronize(s));
+        tm.read();
+        *counter = c + 3 * (n / 2) * d;
+    });
+}
+
 int temo_b200_random_reproduce(uint64_t n, uint64_t d, uint64_t seed, uint64_t* counter, const double* lower,
                                const double* upper, int rng_mode, double* out) {
     return guarded([&] {

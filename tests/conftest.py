@@ -82,6 +82,13 @@ def operator_instance(g, n_min, n_max, d_max):
     return n, d, lower, upper, x
 
 
+def swarm_instance(g, n_min, n_max, d_max):
+    """verify.hpp:83-103 including the scores the swarm operators use (drawn after x)."""
+    n, d, lower, upper, x = operator_instance(g, n_min, n_max, d_max)
+    scores = g.tensor(n, 1).reshape(-1)
+    return n, d, lower, upper, x, scores
+
+
 def ulp_diff(a, b):
     """Distance in units in the last place between two finite fp64 arrays."""
     a = np.ascontiguousarray(a, dtype=np.float64).view(np.int64)

@@ -247,6 +247,116 @@ def test_lockstep_wide_rows(tb, oracle):
     _lockstep(tb, oracle, "dtlz3", 128, 1000, 3, 5, 21)
 
 
+# ---- DE / PSO / CSO: bit-exact, there is no libm on these paths
+
+
+def test_swarm_operators_golden(tb):
+    g = golden("swarm")
+    for tag in ("de0", "de1", "pso0", "pso1", "cso0", "cso1"):
+        c = {k[len(tag) + 1:]: g[k] for k in g.files if k.startswith(tag + "_")}
+        x, lo, hi, sc, seed = c["x"], c["lower"], c["upper"], c["scores"], int(c["seed"][0])
+        st = tb.RngStream(seed, 0)
+        if tag.startswith("de"):
+            y1 = tb.de_reproduce(x, st, tb.DeParams(), lo, hi)
+            assert st.counter == int(c["counters"][0])
+            y2 = tb.de_reproduce(y1, st, tb.DeParams(0.8, 0.4), lo, hi)
+            assert st.counter == int(c["counters"][1]) and np.array_equal(y1, c["y1"]) and np.array_equal(y2, c["y2"]), tag
+        elif tag.startswith("pso"):
+            state = tb.SwarmState(np.zeros_like(x), x * 0.5, sc + 0.25)
+            y1 = tb.pso_reproduce(x, state, sc, st, tb.PsoParams(), lo, hi)
+            assert st.counter == int(c["counters"][0]) and np.array_equal(y1, c["y1"]) and np.array_equal(state.velocities, c["v1"]), tag
+            y2 = tb.pso_reproduce(y1, state, sc[::-1].copy(), st, tb.PsoParams(), lo, hi)
+            assert st.counter == int(c["counters"][1]) and np.array_equal(y2, c["y2"]) and np.array_equal(state.velocities, c["v2"]), tag
+            assert np.array_equal(state.personal_best_x, c["px2"]) and np.array_equal(state.personal_best_score, c["ps2"]), tag
+        else:
+            state = tb.make_swarm_state(x, sc)
+            y1 = tb.cso_reproduce(x, sc, st, tb.CsoParams(), lo, hi, state)
+            assert st.counter == int(c["counters"][0]) and np.array_equal(y1, c["y1"]) and np.array_equal(state.velocities, c["v1"]), tag
+            y2 = tb.cso_reproduce(y1, sc[::-1].copy(), st, tb.CsoParams(), lo, hi, state)
+            assert st.counter == int(c["counters"][1]) and np.array_equal(y2, c["y2"]) and np.array_equal(state.velocities, c["v2"]), tag
+
+
+def test_swarm_operator_suite_7002(tb, checkers):
+    """verify.hpp:117-182, ops 2..4 (de, pso, cso), 100 instances each: outputs, swarm state and counters bit-exact."""
+    from conftest import swarm_instance
+    chk = checkers[-1]
+    for op in (2, 3, 4):
+        for k in range(100):
+            seed = 7002 + op * 1000003 + k
+            g = Stream(chk, seed)
+            n, d, lo, hi, x, scores = swarm_instance(g, 4 if op == 2 else 2, 16, 8)
+            s = seed ^ 0xabcdef
+            st = tb.RngStream(s, 0)
+            if op == 2:
+                got = tb.de_reproduce(x, st, tb.DeParams(), lo, hi)
+                exp, c = chk.de_reproduce(x, s, 0, lo, hi)
+                assert st.counter == c and np.array_equal(got, exp), (op, k)
+            elif op == 3:
+                state = tb.SwarmState(np.zeros_like(x), x * 0.5, scores + 0.25)
+                got = tb.pso_reproduce(x, state, scores, st, tb.PsoParams(), lo, hi)
+                exp, c, v, px, ps = chk.pso_reproduce(x, scores, s, 0, lo, hi, np.zeros_like(x), x * 0.5, scores + 0.25)
+                assert st.counter == c and np.array_equal(got, exp) and np.array_equal(state.velocities, v), (op, k)
+                assert np.array_equal(state.personal_best_x, px) and np.array_equal(state.personal_best_score, ps), (op, k)
+            else:
+                state = tb.make_swarm_state(x, scores)
+                got = tb.cso_reproduce(x, scores, st, tb.CsoParams(), lo, hi, state)
+                exp, c, v = chk.cso_reproduce(x, scores, s, 0, lo, hi, np.zeros_like(x))
+                assert st.counter == c and np.array_equal(got, exp) and np.array_equal(state.velocities, v), (op, k)
+
+
+@pytest.mark.parametrize("shape", [(64, 500), (33, 501), (9, 5000), (200, 37)])
+def test_swarm_operators_larger_shapes_chained(tb, oracle, shape):
+    """Row widths beyond one CTA pass, odd populations (CSO leaves one row unpaired), tied scores, four chained steps."""
+    n, d = shape
+    rng = np.random.default_rng(n * 1000 + d)
+    lo, hi = -rng.random(d) - 1.0, rng.random(d) + 0.5
+    x = lo + rng.random((n, d)) * (hi - lo)
+    # DE
+    st, xo, xg, c = tb.RngStream(3, 50), x.copy(), x.copy(), 50
+    for _ in range(3):
+        xg = tb.de_reproduce(xg, st, tb.DeParams(0.6, 0.7), lo, hi)
+        xo, c = oracle.de_reproduce(xo, 3, c, lo, hi, p=(0.6, 0.7))
+        assert st.counter == c and np.array_equal(xg, xo)
+    # PSO
+    sc0 = np.round(rng.random(n), 1)
+    state = tb.make_swarm_state(x, sc0)
+    vo, pxo, pso_ = np.zeros_like(x), x.copy(), sc0.copy()
+    st, xo, xg, c = tb.RngStream(4, 0), x.copy(), x.copy(), 0
+    for _ in range(4):
+        sc = np.round(rng.random(n), 1)
+        xg = tb.pso_reproduce(xg, state, sc, st, tb.PsoParams(0.5, 1.2, 1.7), lo, hi)
+        xo, c, vo, pxo, pso_ = oracle.pso_reproduce(xo, sc, 4, c, lo, hi, vo, pxo, pso_, p=(0.5, 1.2, 1.7))
+        assert st.counter == c and np.array_equal(xg, xo) and np.array_equal(state.velocities, vo)
+        assert np.array_equal(state.personal_best_x, pxo) and np.array_equal(state.personal_best_score, pso_)
+    # CSO
+    state = tb.make_swarm_state(x, sc0)
+    vo = np.zeros_like(x)
+    st, xo, xg, c = tb.RngStream(6, 9), x.copy(), x.copy(), 9
+    for _ in range(4):
+        sc = np.round(rng.random(n), 1)
+        xg = tb.cso_reproduce(xg, sc, st, tb.CsoParams(0.3), lo, hi, state)
+        xo, c, vo = oracle.cso_reproduce(xo, sc, 6, c, lo, hi, vo, p=(0.3,))
+        assert st.counter == c and np.array_equal(xg, xo) and np.array_equal(state.velocities, vo)
+    with pytest.raises(ValueError):
+        tb.de_reproduce(x[:3], tb.RngStream(1, 0), tb.DeParams(), lo, hi)  # operators.hpp:169
+    with pytest.raises(ValueError):
+        tb.pso_reproduce(x, tb.make_swarm_state(x[:-1], sc0[:-1]), sc0, tb.RngStream(1, 0), tb.PsoParams(), lo, hi)
+
+
+def test_apd_scores(tb, checkers):
+    """apd_scores (selection.hpp:228-234) = the APD column of rv_core: within 1e-9 of the reference (acos)."""
+    chk = checkers[-1]
+    refs = tb.make_ref_set(3, 13)
+    rng = np.random.default_rng(5)
+    f = rng.random((300, 3)) * 10.0
+    got = tb.apd_scores(f, refs, 30, 100, 2.0)
+    assert got.shape == (300, 1)
+    sel = chk.rv_select(f, refs.v, refs.gamma, 30, 100, 2.0)
+    assert np.allclose(got.reshape(-1), sel.apd, rtol=0, atol=1e-9)
+    if hasattr(chk, "apd_scores"):
+        assert np.allclose(got.reshape(-1), chk.apd_scores(f, refs.v, refs.gamma, 30, 100, 2.0), rtol=0, atol=1e-9)
+
+
 # -------------------------------------------------------------------------- problems
 @pytest.mark.parametrize("m", [3, 2, 5, 10])
 def test_problems_golden(tb, m):

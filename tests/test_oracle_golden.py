@@ -214,3 +214,32 @@ def test_lsmop1_restatement_self_checks(oracle):
     xs = x.copy()
     xs[:, m - 1:] = 10.0 * xs[:, :1] / (1.0 + j1 / d)
     assert np.allclose(oracle.evaluate("lsmop1", xs, m).sum(axis=1), 1.0, atol=1e-9)
+
+
+def _swarm_cases():
+    g = golden("swarm")
+    for tag in ("de0", "de1", "pso0", "pso1", "cso0", "cso1"):
+        yield tag, {k[len(tag) + 1:]: g[k] for k in g.files if k.startswith(tag + "_")}
+
+
+def test_swarm_operators_golden(oracle):
+    """DE / PSO / CSO restatements against fixtures generated from the compiled reference (two chained steps each)."""
+    for tag, c in _swarm_cases():
+        x, lo, hi, sc, seed = c["x"], c["lower"], c["upper"], c["scores"], int(c["seed"][0])
+        c1, c2 = (int(v) for v in c["counters"])
+        if tag.startswith("de"):
+            y1, k1 = oracle.de_reproduce(x, seed, 0, lo, hi)
+            y2, k2 = oracle.de_reproduce(y1, seed, k1, lo, hi, p=(0.8, 0.4))
+            assert (k1, k2) == (c1, c2) and np.array_equal(y1, c["y1"]) and np.array_equal(y2, c["y2"]), tag
+        elif tag.startswith("pso"):
+            y1, k1, v1, px1, ps1 = oracle.pso_reproduce(x, sc, seed, 0, lo, hi, np.zeros_like(x), x * 0.5, sc + 0.25)
+            y2, k2, v2, px2, ps2 = oracle.pso_reproduce(y1, sc[::-1].copy(), seed, k1, lo, hi, v1, px1, ps1)
+            assert (k1, k2) == (c1, c2), tag
+            for a, b in ((y1, "y1"), (y2, "y2"), (v1, "v1"), (v2, "v2"), (px2, "px2"), (ps2, "ps2")):
+                assert np.array_equal(a, c[b]), (tag, b)
+        else:
+            y1, k1, v1 = oracle.cso_reproduce(x, sc, seed, 0, lo, hi, np.zeros_like(x))
+            y2, k2, v2 = oracle.cso_reproduce(y1, sc[::-1].copy(), seed, k1, lo, hi, v1)
+            assert (k1, k2) == (c1, c2), tag
+            for a, b in ((y1, "y1"), (y2, "y2"), (v1, "v1"), (v2, "v2")):
+                assert np.array_equal(a, c[b]), (tag, b)

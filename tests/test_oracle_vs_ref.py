@@ -101,3 +101,64 @@ def test_pipeline_and_lockstep(oracle, ref, cfg):
             assert np.array_equal(so[key], sr[key]), (t, key)
         assert so["counter"] == sr["counter"]
     assert np.array_equal(so["x"], a["x"]) and np.array_equal(so["f"], a["f"])
+
+
+def test_swarm_operators_suite_7002(oracle, ref):
+    """DE / PSO / CSO: the C restatement against the compiled reference, batched and
+    scalar-oracle forms, on the reference's own operator_suite instances (verify.hpp:117-182: master seed 7002,
+    ops 2..4, 100 instances each) - outputs, updated swarm state and draw counters bit for bit."""
+    from conftest import Stream, swarm_instance
+    for op in (2, 3, 4):
+        for k in range(100):
+            seed = 7002 + op * 1000003 + k
+            g = Stream(ref, seed)
+            n, d, lo, hi, x, scores = swarm_instance(g, 4 if op == 2 else 2, 16, 8)
+            s = seed ^ 0xabcdef
+            if op == 2:
+                got, c = oracle.de_reproduce(x, s, 0, lo, hi)
+                for scalar in (False, True):
+                    exp, ce = ref.de_reproduce(x, s, 0, lo, hi, scalar=scalar)
+                    assert c == ce and np.array_equal(got, exp), (k, scalar)
+            elif op == 3:
+                vel, pbx, pbs = np.zeros_like(x), x * 0.5, scores + 0.25  # verify.hpp:157-160
+                got = oracle.pso_reproduce(x, scores, s, 0, lo, hi, vel, pbx, pbs)
+                for scalar in (False, True):
+                    exp = ref.pso_reproduce(x, scores, s, 0, lo, hi, vel, pbx, pbs, scalar=scalar)
+                    assert got[1] == exp[1] and all(np.array_equal(a, b) for a, b in zip(got[::2] + got[3:4], exp[::2] + exp[3:4])), (k, scalar)
+            else:
+                vel = np.zeros_like(x)
+                got = oracle.cso_reproduce(x, scores, s, 0, lo, hi, vel)
+                for scalar in (False, True):
+                    exp = ref.cso_reproduce(x, scores, s, 0, lo, hi, vel, scalar=scalar)
+                    assert got[1] == exp[1] and np.array_equal(got[0], exp[0]) and np.array_equal(got[2], exp[2]), (k, scalar)
+
+
+def test_swarm_operators_multi_step_and_contracts(oracle, ref):
+    """Several chained steps (the state carries over), larger shapes, ties in the scores, and de_reproduce's n >= 4."""
+    rng = np.random.default_rng(3)
+    n, d = 37, 23
+    lo, hi = -rng.random(d) - 1.0, rng.random(d) + 0.5
+    x = lo + rng.random((n, d)) * (hi - lo)
+    scores = np.round(rng.random(n), 1)  # many ties
+    vo, pxo, pso_ = np.zeros_like(x), x.copy(), scores.copy()
+    vr, pxr, psr = vo.copy(), pxo.copy(), pso_.copy()
+    xo, xr, co, cr = x.copy(), x.copy(), 11, 11
+    for step in range(4):
+        sc = np.round(rng.random(n), 1)
+        xo, co, vo, pxo, pso_ = oracle.pso_reproduce(xo, sc, 5, co, lo, hi, vo, pxo, pso_)
+        xr, cr, vr, pxr, psr = ref.pso_reproduce(xr, sc, 5, cr, lo, hi, vr, pxr, psr)
+        assert co == cr and np.array_equal(xo, xr) and np.array_equal(vo, vr) and np.array_equal(pxo, pxr) and np.array_equal(pso_, psr)
+    vo = vr = np.zeros_like(x)
+    xo, xr, co, cr = x.copy(), x.copy(), 3, 3
+    for step in range(4):
+        sc = np.round(rng.random(n), 1)
+        xo, co, vo = oracle.cso_reproduce(xo, sc, 8, co, lo, hi, vo)
+        xr, cr, vr = ref.cso_reproduce(xr, sc, 8, cr, lo, hi, vr)
+        assert co == cr and np.array_equal(xo, xr) and np.array_equal(vo, vr)
+    a, ca = oracle.de_reproduce(x, 9, 100, lo, hi, p=(0.7, 0.3))
+    b, cb = ref.de_reproduce(x, 9, 100, lo, hi, p=(0.7, 0.3))
+    assert ca == cb == 100 + 4 * n + n * d and np.array_equal(a, b)
+    with pytest.raises(ValueError):
+        oracle.de_reproduce(x[:3], 1, 0, lo, hi)
+    with pytest.raises(Exception):
+        ref.de_reproduce(x[:3], 1, 0, lo, hi)
