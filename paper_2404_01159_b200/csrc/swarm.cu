@@ -122,34 +122,77 @@ __global__ void __launch_bounds__(256) pso_update_kernel(const double* __restric
 }
 
 // ---- competitive swarm ---------------------------------------------------------------------------------------
-// column means in the reference's order: rows added one after the other, then one division (operators.hpp:257-260)
+// column means in the reference's order: rows added one after the other, then one division (operators.hpp:257-260).
+// The additions of a column are inherently sequential, the loads are not: a CTA owns kMeanCols columns, all its threads
+// stream row tiles into a two-stage shared-memory ring with cp.async (LDGSTS) while kMeanCols threads add the previous
+// tile in row order.
+constexpr int kMeanCols = 8, kMeanRows = 128;
 __global__ void __launch_bounds__(256) col_mean_kernel(const double* __restrict__ x, uint64_t n, uint64_t d, double* __restrict__ mean) {
-    const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    if (j >= d) return;
+    __shared__ double buf[2][kMeanRows][kMeanCols];
+    const uint64_t j0 = blockIdx.x * (uint64_t)kMeanCols;
+    const uint32_t cols = (uint32_t)(d - j0 < (uint64_t)kMeanCols ? d - j0 : (uint64_t)kMeanCols);
+    const uint64_t tiles = (n + kMeanRows - 1) / kMeanRows;
+    auto issue = [&](uint64_t tile, int b) {
+        for (uint32_t e = threadIdx.x; e < kMeanRows * kMeanCols; e += blockDim.x) {
+            const uint32_t r = e / kMeanCols, c = e % kMeanCols;
+            const uint64_t row = tile * kMeanRows + r;
+            if (row < n && c < cols) {
+                const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&buf[b][r][c]);
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(x + row * d + j0 + c) : "memory");
+            }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
     double s = 0.0;
-    for (uint64_t i = 0; i < n; ++i) s += x[i * d + j];
-    mean[j] = s / (double)n;
+    if (tiles) issue(0, 0);
+    for (uint64_t t = 0; t < tiles; ++t) {
+        if (t + 1 < tiles) {
+            issue(t + 1, (int)((t + 1) & 1));
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+        __syncthreads();
+        if (threadIdx.x < cols) {
+            const uint64_t rows = n - t * kMeanRows < (uint64_t)kMeanRows ? n - t * kMeanRows : (uint64_t)kMeanRows;
+            for (uint64_t r = 0; r < rows; ++r) s += buf[t & 1][r][threadIdx.x];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x < cols) mean[j0 + threadIdx.x] = s / (double)n;
 }
 
 // one CTA per pair (perm[2q], perm[2q+1]); draws r1, r2, r3 (pairs x d each) at c, c + pairs d, c + 2 pairs d.
-// out / vel_out already hold copies of x / vel (winners and an unpaired row pass through bit-identically).
+// The winner's row and velocity pass through bit-identically (operators.hpp:263-264: out = x, new_vel = velocities);
+// CTA `pairs` copies the unpaired row of an odd population.
 template <int MODE>
-__global__ void __launch_bounds__(256) cso_kernel(const double* __restrict__ x, const double* __restrict__ scores, uint64_t pairs,
-                                                   uint64_t d, Rng rng, uint64_t c, double phi, const uint32_t* __restrict__ perm,
-                                                   const double* __restrict__ mean, const double* __restrict__ vel,
-                                                   const double* __restrict__ lower, const double* __restrict__ upper,
-                                                   double* __restrict__ vel_out, double* __restrict__ out) {
+__global__ void __launch_bounds__(256) cso_kernel(const double* __restrict__ x, const double* __restrict__ scores, uint64_t n,
+                                                   uint64_t pairs, uint64_t d, Rng rng, uint64_t c, double phi,
+                                                   const uint32_t* __restrict__ perm, const double* __restrict__ mean,
+                                                   const double* __restrict__ vel, const double* __restrict__ lower,
+                                                   const double* __restrict__ upper, double* __restrict__ vel_out,
+                                                   double* __restrict__ out) {
     const uint64_t q = blockIdx.x;
+    if (q >= pairs) {  // odd n: the last row of the shuffled order is nobody's partner
+        const uint64_t r = perm[n - 1];
+        for (uint64_t j = threadIdx.x; j < d; j += blockDim.x) {
+            out[r * d + j] = x[r * d + j];
+            vel_out[r * d + j] = vel[r * d + j];
+        }
+        return;
+    }
     const uint64_t a = perm[2 * q], b = perm[2 * q + 1];
     uint64_t win = a, lose = b;
     if (scores[b] < scores[a] || (scores[b] == scores[a] && b < a)) win = b, lose = a;  // operators.hpp:267-271
     const uint64_t c1 = c + q * d, c2 = c + pairs * d + q * d, c3 = c + 2 * pairs * d + q * d;
     for (uint64_t j = threadIdx.x; j < d; j += blockDim.x) {
-        const double xl = x[lose * d + j];
-        const double v = unit_draw<MODE>(rng, c1 + j) * vel[lose * d + j] + unit_draw<MODE>(rng, c2 + j) * (x[win * d + j] - xl) +
+        const double xl = x[lose * d + j], xw = x[win * d + j];
+        const double v = unit_draw<MODE>(rng, c1 + j) * vel[lose * d + j] + unit_draw<MODE>(rng, c2 + j) * (xw - xl) +
                          phi * unit_draw<MODE>(rng, c3 + j) * (mean[j] - xl);
         vel_out[lose * d + j] = v;
         out[lose * d + j] = clampd(xl + v, lower[j], upper[j]);
+        out[win * d + j] = xw;
+        vel_out[win * d + j] = vel[win * d + j];
     }
 }
 
@@ -184,15 +227,12 @@ void launch_cso(const double* x, const double* scores, uint64_t n, uint64_t d, R
                 const double* upper, double* out, cudaStream_t s) {
     require(n >= 1 && n < 0xffffffffULL, "cso_reproduce: bad row count");
     const uint64_t pairs = n / 2;
-    col_mean_kernel<<<(unsigned)((d + 255) / 256), 256, 0, s>>>(x, n, d, mean_scratch);
-    TEMO_CUDA(cudaMemcpyAsync(out, x, n * d * sizeof(double), cudaMemcpyDeviceToDevice, s));
-    TEMO_CUDA(cudaMemcpyAsync(vel_out, vel, n * d * sizeof(double), cudaMemcpyDeviceToDevice, s));
-    if (pairs) {
-        if (rng.mode == 0)
-            cso_kernel<0><<<(unsigned)pairs, 256, 0, s>>>(x, scores, pairs, d, rng, counter, phi, perm, mean_scratch, vel, lower, upper, vel_out, out);
-        else
-            cso_kernel<1><<<(unsigned)pairs, 256, 0, s>>>(x, scores, pairs, d, rng, counter, phi, perm, mean_scratch, vel, lower, upper, vel_out, out);
-    }
+    col_mean_kernel<<<(unsigned)((d + kMeanCols - 1) / kMeanCols), 256, 0, s>>>(x, n, d, mean_scratch);
+    const unsigned grid = (unsigned)(pairs + (n & 1));
+    if (rng.mode == 0)
+        cso_kernel<0><<<grid, 256, 0, s>>>(x, scores, n, pairs, d, rng, counter, phi, perm, mean_scratch, vel, lower, upper, vel_out, out);
+    else
+        cso_kernel<1><<<grid, 256, 0, s>>>(x, scores, n, pairs, d, rng, counter, phi, perm, mean_scratch, vel, lower, upper, vel_out, out);
     TEMO_CUDA(cudaGetLastError());
 }
 
