@@ -95,6 +95,48 @@ inline Tensor2D random_reproduce(std::size_t n, std::size_t d, RngStream& stream
     return out;
 }
 
+// DE / PSO / CSO (operators.hpp:166-284): same signatures, same in-place SwarmState updates, bit-identical results.
+inline Tensor2D de_reproduce(const Tensor2D& x, RngStream& stream, const DeParams& p, const Tensor2D& lower,
+                             const Tensor2D& upper) {
+    temo::detail::require(lower.size() == x.cols && upper.size() == x.cols, "de_reproduce: bounds shape mismatch");
+    Tensor2D out(x.rows, x.cols);
+    uint64_t counter = stream.counter;
+    detail::check(temo_b200_de_reproduce(x.data.data(), x.rows, x.cols, stream.seed, &counter, p.f, p.cr, lower.data.data(),
+                                         upper.data.data(), TEMO_B200_RNG_SPLITMIX64, out.data.data(), nullptr));
+    stream.counter = counter;
+    return out;
+}
+
+inline Tensor2D pso_reproduce(const Tensor2D& x, SwarmState& state, const Tensor2D& scores, RngStream& stream,
+                              const PsoParams& p, const Tensor2D& lower, const Tensor2D& upper) {
+    const std::size_t n = x.rows, d = x.cols;
+    temo::detail::require(state.velocities.rows == n && state.velocities.cols == d && state.personal_best_x.rows == n &&
+                              scores.rows == n,
+                          "pso_reproduce: state shape mismatch");  // operators.hpp:209-211
+    Tensor2D out(n, d);
+    uint64_t counter = stream.counter;
+    detail::check(temo_b200_pso_reproduce(x.data.data(), scores.data.data(), n, d, stream.seed, &counter, p.inertia, p.c1, p.c2,
+                                          state.velocities.data.data(), state.personal_best_x.data.data(),
+                                          state.personal_best_score.data.data(), lower.data.data(), upper.data.data(),
+                                          TEMO_B200_RNG_SPLITMIX64, out.data.data(), nullptr));
+    stream.counter = counter;
+    return out;
+}
+
+inline Tensor2D cso_reproduce(const Tensor2D& x, const Tensor2D& scores, RngStream& stream, const CsoParams& p,
+                              const Tensor2D& lower, const Tensor2D& upper, SwarmState& state) {
+    const std::size_t n = x.rows, d = x.cols;
+    temo::detail::require(state.velocities.rows == n && state.velocities.cols == d && scores.rows == n,
+                          "cso_reproduce: state shape mismatch");  // operators.hpp:251-253
+    Tensor2D out(n, d);
+    uint64_t counter = stream.counter;
+    detail::check(temo_b200_cso_reproduce(x.data.data(), scores.data.data(), n, d, stream.seed, &counter, p.phi,
+                                          state.velocities.data.data(), lower.data.data(), upper.data.data(),
+                                          TEMO_B200_RNG_SPLITMIX64, out.data.data(), nullptr));
+    stream.counter = counter;
+    return out;
+}
+
 // ---- problems.hpp ----------------------------------------------------------------------------
 inline Tensor2D dtlz_eval(int id, const Tensor2D& x, std::size_t m) {
     temo::detail::require(id >= 1 && id <= 4, "dtlz_eval: id must be in 1..4");
@@ -155,6 +197,19 @@ inline SelectionOutcome rv_select(const Tensor2D& f, const RefVectorSet& refs, s
         for (std::size_t i = 0; i < n; ++i) out.apd_table(i, assoc[i]) = apd[i];
     }
     return out;
+}
+
+/// apd_scores (selection.hpp:228-234): every row's APD against its associated vector, n x 1.
+inline Tensor2D apd_scores(const Tensor2D& f, const RefVectorSet& refs, std::size_t t, std::size_t t_max, double alpha) {
+    temo::detail::require(f.cols == refs.v.cols, "rv_select: objective count mismatch");
+    const std::size_t n = f.rows, r = refs.v.rows;
+    std::vector<uint64_t> elite(r ? r : 1);
+    std::vector<unsigned char> valid(r);
+    Tensor2D scores(n, 1);
+    uint64_t count = 0;
+    detail::check(temo_b200_rv_select(f.data.data(), n, f.cols, refs.v.data.data(), refs.gamma.data.data(), r, t, t_max, alpha,
+                                      elite.data(), &count, valid.data(), nullptr, nullptr, scores.data.data()));
+    return scores;
 }
 
 // ---- algorithms.hpp --------------------------------------------------------------------------

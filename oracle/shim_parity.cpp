@@ -6,7 +6,7 @@
 // replaces the batched CPU call by its temo::b200:: twin, comparing against the reference's scalar oracle
 // (temo::oracle::*) exactly like the reference does:
 //   rv_select_suite   verify.hpp:53-76   200 instances, seed 7001: elite indices + validity identical, APD 1e-9
-//   operator_suite    verify.hpp:117-144 100 x {sbx, pm}, seed 7002 + op*1000003 + k: here bit-identical
+//   operator_suite    verify.hpp:117-182 100 x {sbx, pm, de, pso, cso}, seed 7002 + op*1000003 + k: here bit-identical
 //   ga pipeline       test_operators.cpp:104-114
 //   whole run         test_algorithms.cpp:198-210 (seed 77) and BASELINE config #1
 // Exit code = number of failed suites.
@@ -66,6 +66,44 @@ static int operator_suite_gpu() {
         }
     }
     std::printf("operator_suite (gpu sbx/pm vs oracle, bit-exact): %d/200 failed\n", failed);
+    return failed;
+}
+
+// verify.hpp:117-182, ops 2..4: DE / PSO / CSO through the shim against the reference's scalar oracles, bit-exact
+static int swarm_suite_gpu() {
+    int failed = 0;
+    for (std::size_t op = 2; op < 5; ++op) {
+        for (std::size_t k = 0; k < 100; ++k) {
+            const std::uint64_t seed = 7002 + op * 1000003 + k;
+            RngStream g{seed, 0};
+            auto inst = verify::detail::random_operator_instance(g, op == 2 ? 4 : 2, 16, 8);
+            const oracle::Matrix xm = oracle::to_matrix(inst.x);
+            const oracle::Row lo = oracle::to_matrix(inst.lower)[0], hi = oracle::to_matrix(inst.upper)[0];
+            RngStream sa{seed ^ 0xabcdef, 0}, sb{seed ^ 0xabcdef, 0};
+            bool ok = true;
+            if (op == 2) {
+                const DeParams p;
+                ok = same_bits(b200::de_reproduce(inst.x, sa, p, inst.lower, inst.upper), oracle::to_tensor(oracle::oracle_de(xm, sb, p, lo, hi)));
+            } else if (op == 3) {
+                const PsoParams p;
+                SwarmState st_a = make_swarm_state(inst.x, inst.scores);
+                for (double& v : st_a.personal_best_x.data) v *= 0.5;
+                for (double& v : st_a.personal_best_score.data) v += 0.25;
+                SwarmState st_b = st_a;
+                const Tensor2D got = b200::pso_reproduce(inst.x, st_a, inst.scores, sa, p, inst.lower, inst.upper);
+                const Tensor2D exp = oracle::to_tensor(oracle::oracle_pso(xm, st_b, inst.scores.data, sb, p, lo, hi));
+                ok = same_bits(got, exp) && same_bits(st_a.velocities, st_b.velocities) && same_bits(st_a.personal_best_x, st_b.personal_best_x);
+            } else {
+                const CsoParams p;
+                SwarmState st_a = make_swarm_state(inst.x, inst.scores), st_b = st_a;
+                const Tensor2D got = b200::cso_reproduce(inst.x, inst.scores, sa, p, inst.lower, inst.upper, st_a);
+                const Tensor2D exp = oracle::to_tensor(oracle::oracle_cso(xm, inst.scores.data, sb, p, lo, hi, st_b));
+                ok = same_bits(got, exp) && same_bits(st_a.velocities, st_b.velocities);
+            }
+            failed += !(ok && sa.counter == sb.counter);
+        }
+    }
+    std::printf("operator_suite (gpu de/pso/cso vs oracle, bit-exact): %d/300 failed\n", failed);
     return failed;
 }
 
@@ -129,6 +167,7 @@ int main() {
     int failed = 0;
     failed += rv_select_suite_gpu() != 0;
     failed += operator_suite_gpu() != 0;
+    failed += swarm_suite_gpu() != 0;
     failed += ga_pipeline_gpu() != 0;
     failed += whole_run_gpu() != 0;
     std::printf("%s\n", failed ? "SHIM PARITY FAILED" : "SHIM PARITY OK");

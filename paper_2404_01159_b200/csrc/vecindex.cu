@@ -122,6 +122,94 @@ __global__ void node_build_kernel(const double* vp, uint64_t r, uint64_t m, uint
     }
 }
 
+// Same record for a node with many members (levels >= 2: spans of 1024 positions and more): one CTA per node instead
+// of one warp, so that the few big nodes at the top of the tree do not serialise the rebuild after an adaptation.
+// Identical arithmetic per member; the centre is again the member closest to the mean direction (ties -> lowest
+// position) and the radius is exact for that centre, so any difference in the mean's summation order can only pick
+// another valid centre.
+__global__ void __launch_bounds__(256) node_build_block_kernel(const double* vp, uint64_t r, uint64_t m, uint64_t span, uint64_t count,
+                                                                double* node, uint32_t* centre_pos) {
+    __shared__ double s_mean[kMaxObj];
+    __shared__ double s_val[8];
+    __shared__ uint64_t s_pos[8];
+    const uint64_t i = blockIdx.x;
+    if (i >= count) return;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint64_t a = i * span, b = (a + span < r) ? a + span : r;
+    for (uint64_t k = 0; k < m; ++k) {  // mean direction, one component at a time (m <= 32)
+        double acc = 0.0;
+        for (uint64_t p = a + threadIdx.x; p < b; p += blockDim.x) acc += vp[p * (m + 1) + k] / vp[p * (m + 1) + m];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+        if (lane == 0) s_val[warp] = acc;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            for (int w = 0; w < 8; ++w) t += s_val[w];
+            s_mean[k] = t;
+        }
+        __syncthreads();
+    }
+    double best = -INFINITY;
+    uint64_t best_p = a;
+    for (uint64_t p = a + threadIdx.x; p < b; p += blockDim.x) {
+        double dot = 0.0;
+        for (uint64_t k = 0; k < m; ++k) dot += s_mean[k] * vp[p * (m + 1) + k];
+        dot /= vp[p * (m + 1) + m];
+        if (dot > best) {
+            best = dot;
+            best_p = p;
+        }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, off);
+        const uint64_t op = __shfl_xor_sync(0xffffffffu, best_p, off);
+        if (ob > best || (ob == best && op < best_p)) {
+            best = ob;
+            best_p = op;
+        }
+    }
+    if (lane == 0) s_val[warp] = best, s_pos[warp] = best_p;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < 8; ++w)
+            if (s_val[w] > s_val[0] || (s_val[w] == s_val[0] && s_pos[w] < s_pos[0])) s_val[0] = s_val[w], s_pos[0] = s_pos[w];
+    }
+    __syncthreads();
+    const uint64_t c = s_pos[0];
+    __syncthreads();
+    const double* cv = vp + c * (m + 1);
+    const double cn = cv[m];
+    double lo = 2.0;
+    for (uint64_t p = a + threadIdx.x; p < b; p += blockDim.x) {
+        const double* pv = vp + p * (m + 1);
+        double dot = 0.0;
+        for (uint64_t k = 0; k < m; ++k) dot += cv[k] * pv[k];
+        const double cs = dot / (cn * pv[m]);
+        lo = cs < lo ? cs : lo;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        const double o = __shfl_xor_sync(0xffffffffu, lo, off);
+        lo = o < lo ? o : lo;
+    }
+    if (lane == 0) s_val[warp] = lo;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < 8; ++w) lo = s_val[w] < lo ? s_val[w] : lo;
+        double cr = lo - kSlack;
+        if (!(cr >= -1.0)) cr = -1.0;  // also catches NaN
+        if (cr > 1.0) cr = 1.0;
+        double* rec = node + i * (m + 3);
+        for (uint64_t k = 0; k < m; ++k) rec[k] = cv[k];
+        rec[m] = cn;
+        rec[m + 1] = cr;
+        rec[m + 2] = sqrt(fmax(0.0, 1.0 - cr * cr));
+        centre_pos[i] = (uint32_t)c;
+    }
+}
+
 struct IndexView {
     const double* vp;
     const uint32_t* orig;
@@ -467,8 +555,12 @@ void VecIndex::build(const double* v, const double* vn, cudaStream_t s) {
     uint64_t span = 1;
     for (int l = 1; l <= levels; ++l) {
         span *= 32;
-        const uint64_t threads = count[l] * 32;
-        node_build_kernel<<<(unsigned)((threads + 127) / 128), 128, 0, s>>>(vp, r, m, span, count[l], node[l], centre[l]);
+        if (l >= 2) {
+            node_build_block_kernel<<<(unsigned)count[l], 256, 0, s>>>(vp, r, m, span, count[l], node[l], centre[l]);
+        } else {
+            const uint64_t threads = count[l] * 32;
+            node_build_kernel<<<(unsigned)((threads + 127) / 128), 128, 0, s>>>(vp, r, m, span, count[l], node[l], centre[l]);
+        }
     }
     TEMO_CUDA(cudaGetLastError());
     built = true;
