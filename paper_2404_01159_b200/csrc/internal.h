@@ -132,6 +132,8 @@ struct SelectWorkspace {
     uint32_t* n_elite = nullptr;      // [1]
     uint32_t* err_flag = nullptr;     // [1] bit0: gamma <= 0
     uint32_t* tile_scratch = nullptr; // compaction tile counts
+    float* v32 = nullptr;             // [r x (m+1)] fp32 copy of v and 1/|v| (filtered association, m >= 5)
+    uint32_t* v32_flags = nullptr;    // [1] bit0: a vector component is negative / non-finite
     void alloc(uint64_t rows_cap_, uint64_t r_, uint64_t m_);
     void release();
 };
@@ -143,6 +145,11 @@ void launch_select(const double* f, uint64_t n_rows, const uint32_t* n_rows_dev,
                    const double* v, const double* gamma, uint64_t r, double penalty,
                    SelectWorkspace& ws, cudaStream_t s, VecIndex* index = nullptr);
 void launch_row_norms(const double* v, uint64_t r, uint64_t m, double* vn, cudaStream_t s);
+// Exact association + APD through a single-precision filter (many objectives, where the direction index prunes little);
+// same outputs as the other association kernels. ws.vn must hold the norms of v.
+bool assoc_filter_preferred(uint64_t m, uint64_t r);
+void launch_assoc_filter(const double* f, uint64_t n_rows, uint64_t m, const double* v, const double* gamma, uint64_t r, double penalty,
+                         SelectWorkspace& ws, uint32_t* assoc, double* theta, double* apd, cudaStream_t s, uint32_t row0);
 // the stages of launch_select, separately (the sharded run puts collectives between them)
 void launch_select_prepare(const double* f, uint64_t n_rows, uint64_t m, const double* gamma, uint64_t r,
                            SelectWorkspace& ws, cudaStream_t s);

@@ -157,6 +157,177 @@ __global__ void __launch_bounds__(kAssocThreads) assoc_kernel(
     atomicMin(&first_row[arg], (uint32_t)i);
 }
 
+// ---- exact association through a single-precision filter (many objectives) ---------------------------------------
+// For m >= 5 the direction index prunes little (in 10 dimensions every patch of the lattice is wide) and the exact scan
+// costs (rows x R) double-precision dots WITHOUT fused multiply-adds plus a divide per pair: 12 ms at BASELINE config #4
+// (131072 rows x 48620 vectors x 10), which is the FP64 pipe's peak. Here every pair is first scored in fp32
+// (cos32 = (u/|u|) . v / |v| with FFMA, half the instructions at twice the rate); only a pair whose fp32 score is within
+// kFilterTol of the row's running fp32 maximum is re-evaluated with the reference's exact fp64 expression
+// (selection.hpp:172-184), in ascending j with a strict >, so the result is the reference's first strict maximum.
+// Why this is exact: for non-negative u and v all terms of the dot product are non-negative, so the fp32 score has
+// relative error <= (m + 5) 2^-24 < 2.3e-6 (m <= 32); the running maximum never exceeds the final one, hence every j whose
+// exact cosine could reach the final exact maximum satisfies cos32_j >= max32 (1 - 2 * 2.3e-6) > running32 (1 - kFilterTol)
+// and is evaluated exactly. Rows or vector sets with a negative or non-finite component take the exact expression for
+// every j (threshold -inf).
+constexpr float kFilterTol = 1e-5f;
+constexpr int kFilterTile = 512;      // vectors per shared-memory tile
+constexpr int kFilterThreads = 128;   // two rows per thread: 256 rows per CTA keeps the grid several waves deep
+
+// fp32 copy of the vectors: row j = {v_j[0..m-1], 1 / |v_j|, 0 ...} padded to a multiple of four floats (128-bit reads)
+__host__ __device__ inline uint64_t v32_stride(uint64_t m) { return (m + 1 + 3) / 4 * 4; }
+
+__global__ void v32_kernel(const double* __restrict__ v, const double* __restrict__ vn, uint64_t r, uint64_t m, float* __restrict__ v32,
+                           uint32_t* __restrict__ flags) {
+    const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (j >= r) return;
+    const uint64_t stride = v32_stride(m);
+    bool bad = false;
+    for (uint64_t k = 0; k < m; ++k) {
+        const double x = v[j * m + k];
+        v32[j * stride + k] = (float)x;
+        if (!(x >= 0.0) || !(x < INFINITY)) bad = true;
+    }
+    const double nrm = vn[j];
+    v32[j * stride + m] = (float)(1.0 / nrm);
+    for (uint64_t k = m + 1; k < stride; ++k) v32[j * stride + k] = 0.0f;
+    if (!(nrm > 0.0) || !(nrm < INFINITY)) bad = true;
+    if (bad) atomicOr(flags, 1u);
+}
+
+template <int M>
+__global__ void __launch_bounds__(kFilterThreads, 4) assoc_filter_kernel(
+    const double* __restrict__ f, uint64_t n_rows, const uint32_t* n_rows_dev, uint64_t m_rt, const double* __restrict__ z,
+    const double* __restrict__ v, const double* __restrict__ vn, const float* __restrict__ v32, const uint32_t* __restrict__ vflags,
+    const double* __restrict__ gamma, uint64_t r, double penalty, uint32_t* __restrict__ assoc, double* __restrict__ theta_out,
+    double* __restrict__ apd_out, unsigned long long* __restrict__ best_key, uint32_t* __restrict__ first_row, uint32_t row0) {
+    constexpr int MM = M > 0 ? M : kMaxObj;
+    const int m = M > 0 ? M : (int)m_rt;
+    extern __shared__ __align__(16) float s_v32[];  // kFilterTile x stride: v_j[0..m-1], 1 / |v_j| in fp32, padding
+    const uint64_t n = n_rows_dev ? (uint64_t)*n_rows_dev : n_rows;
+    const bool v_ok = (*vflags & 1u) == 0;
+    uint64_t row[2];
+    bool live[2];
+    double fp[2][MM], nf[2], best_c[2];
+    float uf[2][MM], best32[2], thr[2];
+    uint32_t arg[2];
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+        row[t] = blockIdx.x * (uint64_t)(2 * kFilterThreads) + t * kFilterThreads + threadIdx.x;
+        live[t] = row[t] < n;
+        nf[t] = 0.0;
+        best_c[t] = -INFINITY;
+        arg[t] = 0;
+        bool filter = v_ok && live[t];
+        if (live[t]) {
+            double s = 0.0;
+#pragma unroll
+            for (int k = 0; k < MM; ++k)
+                if (k < m) {
+                    fp[t][k] = f[row[t] * m + k] - z[k];  // selection.hpp:155-157
+                    s += fp[t][k] * fp[t][k];
+                    if (!(fp[t][k] >= 0.0)) filter = false;
+                }
+            nf[t] = sqrt(s);
+            if (!(nf[t] < INFINITY)) filter = false;  // inf or NaN
+        }
+#pragma unroll
+        for (int k = 0; k < MM; ++k) uf[t][k] = (k < m && live[t] && nf[t] != 0.0) ? (float)(fp[t][k] / nf[t]) : 0.0f;
+        best32[t] = 0.0f;
+        thr[t] = filter ? 0.0f : -INFINITY;  // 0: every non-negative score passes until a maximum exists
+        if (!live[t] || nf[t] == 0.0) thr[t] = INFINITY;  // nothing to do (selection.hpp:167-169: arg 0, theta 0)
+    }
+    constexpr int SS = (MM + 1 + 3) / 4 * 4;  // compile-time stride when M is known
+    const int stride = M > 0 ? SS : (int)v32_stride(m);
+    for (uint64_t j0 = 0; j0 < r; j0 += kFilterTile) {
+        const int tile = (int)((r - j0) < (uint64_t)kFilterTile ? (r - j0) : kFilterTile);
+        __syncthreads();
+        {
+            const float4* src = reinterpret_cast<const float4*>(v32 + j0 * stride);
+            float4* dst = reinterpret_cast<float4*>(s_v32);
+            for (int e = threadIdx.x; e < tile * stride / 4; e += blockDim.x) dst[e] = src[e];
+        }
+        __syncthreads();
+        // two vectors per step: four independent FFMA chains per thread
+        for (int jj = 0; jj < tile; jj += 2) {
+            float vr[2][SS];
+            const bool second = jj + 1 < tile;
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const float4* p4 = reinterpret_cast<const float4*>(s_v32 + (jj + (u && second ? 1 : 0)) * stride);  // broadcast reads
+#pragma unroll
+                for (int k4 = 0; k4 < SS / 4; ++k4)
+                    if (4 * k4 < m + 1) {
+                        const float4 t4 = p4[k4];
+                        vr[u][4 * k4] = t4.x, vr[u][4 * k4 + 1] = t4.y, vr[u][4 * k4 + 2] = t4.z, vr[u][4 * k4 + 3] = t4.w;
+                    }
+            }
+            float sc[2][2] = {{0.0f, 0.0f}, {0.0f, 0.0f}};  // [vector][row]
+#pragma unroll
+            for (int k = 0; k < MM; ++k)
+                if (k < m) {
+                    sc[0][0] = fmaf(uf[0][k], vr[0][k], sc[0][0]);
+                    sc[0][1] = fmaf(uf[1][k], vr[0][k], sc[0][1]);
+                    sc[1][0] = fmaf(uf[0][k], vr[1][k], sc[1][0]);
+                    sc[1][1] = fmaf(uf[1][k], vr[1][k], sc[1][1]);
+                }
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                float rinv = vr[u][0];
+#pragma unroll
+                for (int k = 0; k <= MM; ++k)
+                    if (k == m) rinv = vr[u][k];
+                sc[u][0] *= rinv;
+                sc[u][1] *= rinv;
+            }
+            if (!second) sc[1][0] = sc[1][1] = -INFINITY;
+            // ascending j: vector jj first, then jj + 1 (the thresholds move in between)
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const bool h0 = sc[u][0] >= thr[0], h1 = sc[u][1] >= thr[1];
+                if (h0 | h1) {  // rare after the first few vectors: the reference's exact expression
+                    const uint64_t j = j0 + jj + u;
+#pragma unroll
+                    for (int t = 0; t < 2; ++t) {
+                        if (!(t == 0 ? h0 : h1)) continue;
+                        double dot = 0.0;
+#pragma unroll
+                        for (int k = 0; k < MM; ++k)
+                            if (k < m) dot += fp[t][k] * v[j * m + k];
+                        const double c = dot / (nf[t] * vn[j]);  // selection.hpp:178
+                        if (c > best_c[t]) {
+                            best_c[t] = c;
+                            arg[t] = (uint32_t)j;
+                        }
+                        const float s32 = sc[u][t];
+                        if (thr[t] > -INFINITY && s32 > best32[t]) {
+                            best32[t] = s32;
+                            thr[t] = s32 * (1.0f - kFilterTol);
+                        }
+                    }
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+        if (!live[t]) continue;
+        double theta = 0.0;  // a row at the ideal point: angle 0 to vector 0 (selection.hpp:167-169)
+        if (nf[t] != 0.0) {
+            double c = best_c[t];
+            if (c > 1.0) c = 1.0;
+            if (c < -1.0) c = -1.0;
+            theta = acos(c);  // tensor.hpp:79-83
+        }
+        const double apd = (1.0 + penalty * (theta / gamma[arg[t]])) * nf[t];  // selection.hpp:82-84
+        assoc[row[t]] = arg[t];
+        theta_out[row[t]] = theta;
+        apd_out[row[t]] = apd;
+        const unsigned long long key = (apd != apd) ? kKeyMax : order_key(apd);
+        atomicMin(&best_key[arg[t]], key);
+        atomicMin(&first_row[arg[t]], row0 + (uint32_t)row[t]);
+    }
+}
+
 // lowest row among those that attain the minimal APD of their vector
 __global__ void elite_rows_kernel(uint64_t n_rows, const uint32_t* n_rows_dev, const uint32_t* assoc,
                                   const double* apd, const unsigned long long* best_key,
@@ -233,13 +404,15 @@ void SelectWorkspace::alloc(uint64_t rows_cap_, uint64_t r_, uint64_t m_) {
     n_elite = dev_alloc<uint32_t>(1);
     err_flag = dev_alloc<uint32_t>(1);
     tile_scratch = dev_alloc<uint32_t>((r + kCompactTile - 1) / kCompactTile + 1);
+    v32 = dev_alloc<float>(r * ((m + 1 + 3) / 4 * 4));
+    v32_flags = dev_alloc<uint32_t>(1);
     TEMO_CUDA(cudaMemset(err_flag, 0, sizeof(uint32_t)));
 }
 
 void SelectWorkspace::release() {
     cudaFree(z); cudaFree(zkey); cudaFree(vn); cudaFree(assoc); cudaFree(theta); cudaFree(apd);
     cudaFree(best_key); cudaFree(best_row); cudaFree(first_row); cudaFree(elite); cudaFree(valid);
-    cudaFree(n_elite); cudaFree(err_flag); cudaFree(tile_scratch);
+    cudaFree(n_elite); cudaFree(err_flag); cudaFree(tile_scratch); cudaFree(v32); cudaFree(v32_flags);
     *this = SelectWorkspace{};
 }
 
@@ -290,12 +463,42 @@ void launch_select_finish(uint64_t r, SelectWorkspace& ws, bool nan_rule, cudaSt
     TEMO_CUDA(cudaGetLastError());
 }
 
+bool assoc_filter_preferred(uint64_t m, uint64_t r) { return m >= 5 && r >= 256; }
+
+void launch_assoc_filter(const double* f, uint64_t n_rows, uint64_t m, const double* v, const double* gamma, uint64_t r, double penalty,
+                         SelectWorkspace& ws, uint32_t* assoc, double* theta, double* apd, cudaStream_t s, uint32_t row0) {
+    require(ws.v32 != nullptr && r <= ws.r && m == ws.m, "rv_select: workspace has no fp32 vector copy");
+    TEMO_CUDA(cudaMemsetAsync(ws.v32_flags, 0, sizeof(uint32_t), s));
+    v32_kernel<<<(unsigned)((r + 255) / 256), 256, 0, s>>>(v, ws.vn, r, m, ws.v32, ws.v32_flags);
+    const unsigned grid = (unsigned)((n_rows + 2 * kFilterThreads - 1) / (2 * kFilterThreads));
+    const size_t smem = (size_t)kFilterTile * v32_stride(m) * sizeof(float);
+#define CALL(MV)                                                                                                                  \
+    {                                                                                                                             \
+        static bool configured = false;                                                                                           \
+        if (!configured && smem > 48 * 1024) {                                                                                    \
+            TEMO_CUDA(cudaFuncSetAttribute(assoc_filter_kernel<MV>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));    \
+            configured = true;                                                                                                    \
+        }                                                                                                                         \
+        assoc_filter_kernel<MV><<<grid, kFilterThreads, smem, s>>>(f, n_rows, nullptr, m, ws.z, v, ws.vn, ws.v32, ws.v32_flags, gamma, \
+                                                                   r, penalty, assoc, theta, apd, ws.best_key, ws.first_row, row0); \
+    }
+    switch (m) {
+    case 5: CALL(5); break;
+    case 10: CALL(10); break;
+    default: CALL(0); break;
+    }
+#undef CALL
+    TEMO_CUDA(cudaGetLastError());
+}
+
 void launch_select(const double* f, uint64_t n_rows, const uint32_t* n_rows_dev, uint64_t m,
                    const double* v, const double* gamma, uint64_t r, double penalty,
                    SelectWorkspace& ws, cudaStream_t s, VecIndex* index) {
     require(n_rows_dev == nullptr, "rv_select: device-side row counts are not supported here");
     launch_select_prepare(f, n_rows, m, gamma, r, ws, s);
-    if (index && index->built) {
+    if (assoc_filter_preferred(m, r)) {
+        launch_assoc_filter(f, n_rows, m, v, gamma, r, penalty, ws, ws.assoc, ws.theta, ws.apd, s, 0);
+    } else if (index && index->built) {
         launch_assoc_indexed(f, n_rows, nullptr, m, ws.z, *index, gamma, penalty, ws.assoc, ws.theta, ws.apd,
                              ws.best_key, ws.first_row, s);
     } else {

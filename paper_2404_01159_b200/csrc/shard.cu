@@ -386,9 +386,14 @@ struct Shard {
         require(lo <= hi && hi <= rows, "shard: bad row slice");
         const double penalty = apd_penalty(m, t, cfg.generations, cfg.alpha);
         launch_select_prepare(fm[cur], rows, m, gamma, r, ws, stream);
-        if (hi > lo)
-            launch_assoc_indexed(fm[cur] + lo * m, hi - lo, nullptr, m, ws.z, vindex, gamma, penalty, ws.assoc + lo,
-                                 ws.theta + lo, ws.apd + lo, ws.best_key, ws.first_row, stream, (uint32_t)lo);
+        if (hi > lo) {
+            if (assoc_filter_preferred(m, r))
+                launch_assoc_filter(fm[cur] + lo * m, hi - lo, m, v, gamma, r, penalty, ws, ws.assoc + lo, ws.theta + lo, ws.apd + lo,
+                                    stream, (uint32_t)lo);
+            else
+                launch_assoc_indexed(fm[cur] + lo * m, hi - lo, nullptr, m, ws.z, vindex, gamma, penalty, ws.assoc + lo,
+                                     ws.theta + lo, ws.apd + lo, ws.best_key, ws.first_row, stream, (uint32_t)lo);
+        }
         flip_keys_kernel<<<(unsigned)((r + 255) / 256), 256, 0, stream>>>(ws.best_key, r);
         flip_rows_kernel<<<(unsigned)((r + 255) / 256), 256, 0, stream>>>(ws.first_row, r);
     }

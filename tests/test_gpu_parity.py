@@ -500,6 +500,39 @@ def test_rv_select_mid_size(tb, oracle, cfg):
     _check_selection(tb.rv_select(f, tb.RefVectorSet(v0, v, gamma), 33, 100, 2.0), oracle.rv_select(f, v, gamma, 33, 100, 2.0))
 
 
+@pytest.mark.parametrize("cfg", [(5, 7, 3000, 1), (10, 4, 2500, 2), (10, 5, 4000, 3), (8, 5, 1500, 4), (6, 6, 2000, 5)])
+def test_rv_select_many_objectives_filter(tb, oracle, cfg):
+    """m >= 5 with R >= 256 takes the fp32-filtered exact scan (select.cu): association, validity and survivors must
+    still be the reference's, including exact ties between vectors (rows lying exactly between two lattice points),
+    duplicated rows, rows on a vector, at the ideal point, and rows the filter may not be used for (negative / NaN)."""
+    m, H, n, seed = cfg
+    v0, gamma = oracle.make_ref_set(m, H)
+    assert len(v0) >= 256
+    for adapted in (False, True):
+        v, g = (v0, gamma)
+        if adapted:
+            zmin = np.linspace(0.0, 0.2, m)
+            v, g = oracle.adapt(v0, v0, gamma, zmin, zmin + np.linspace(0.5, 3.0, m))
+        f = Stream(oracle, 9700 + seed).tensor(n, m) * np.linspace(1.0, 4.0, m) + 0.05
+        base = f.min(axis=0)
+        f[n // 2] = f[n // 3]                      # duplicated rows
+        f[5] = base                                # a row at the ideal point
+        f[7, 0] = np.nan                           # a NaN row
+        f[9] = v[min(17, len(v) - 1)] * 3.0 + base           # on a reference vector
+        f[11] = (v[20] + v[21]) * 1.5 + base                 # exactly between two vectors: equal cosines up to rounding
+        f[13] = (v0[3] + v0[40] + v0[41]) + base
+        f[15] = base + 1e-300                                # a denormal-scale direction
+        f[17] = base * 1.0
+        f[17, 1] += 1e120                                    # a huge component (far outside fp32)
+        _check_selection(tb.rv_select(f, tb.RefVectorSet(v0, v, g), 33, 100, 2.0), oracle.rv_select(f, v, g, 33, 100, 2.0))
+    # objectives below the ideal point cannot occur, but vectors with a negative component can be injected: no filter then
+    vneg = v0.copy()
+    vneg[3, 0] = -vneg[3, 0] - 0.1
+    gneg = oracle.min_vector_angles(vneg) if hasattr(oracle, "min_vector_angles") else gamma
+    f = Stream(oracle, 9800 + seed).tensor(500, m) + 0.1
+    _check_selection(tb.rv_select(f, tb.RefVectorSet(v0, vneg, gneg), 10, 100, 2.0), oracle.rv_select(f, vneg, gneg, 10, 100, 2.0))
+
+
 def test_selection_contracts_and_edges(tb, oracle):
     v0, gamma = oracle.make_ref_set(2, 2)
     refs = tb.RefVectorSet(v0, v0, gamma)
