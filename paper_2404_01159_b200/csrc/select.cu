@@ -248,6 +248,7 @@ __global__ void __launch_bounds__(kFilterThreads, 4) assoc_filter_kernel(
         }
         __syncthreads();
         // two vectors per step: four independent FFMA chains per thread
+#pragma unroll 2
         for (int jj = 0; jj < tile; jj += 2) {
             float vr[2][SS];
             const bool second = jj + 1 < tile;
