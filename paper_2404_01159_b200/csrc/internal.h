@@ -134,6 +134,8 @@ struct SelectWorkspace {
     uint32_t* tile_scratch = nullptr; // compaction tile counts
     float* v32 = nullptr;             // [r x (m+1)] fp32 copy of v and 1/|v| (filtered association, m >= 5)
     uint32_t* v32_flags = nullptr;    // [1] bit0: a vector component is negative / non-finite
+    double* part_c = nullptr;         // [chunks x rows_cap] per-chunk winners of the filtered association (m >= 5 only)
+    uint32_t* part_j = nullptr;
     void alloc(uint64_t rows_cap_, uint64_t r_, uint64_t m_);
     void release();
 };

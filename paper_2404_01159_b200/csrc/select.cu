@@ -171,6 +171,7 @@ __global__ void __launch_bounds__(kAssocThreads) assoc_kernel(
 // every j (threshold -inf).
 constexpr float kFilterTol = 1e-5f;
 constexpr int kFilterTile = 512;      // vectors per shared-memory tile
+constexpr int kFilterMaxChunks = 8;   // pieces the vector range is cut into (per-row winners merged afterwards)
 constexpr int kFilterThreads = 128;   // two rows per thread: 256 rows per CTA keeps the grid several waves deep
 
 // fp32 copy of the vectors: row j = {v_j[0..m-1], 1 / |v_j|, 0 ...} padded to a multiple of four floats (128-bit reads)
@@ -198,8 +199,9 @@ template <int M>
 __global__ void __launch_bounds__(kFilterThreads, 4) assoc_filter_kernel(
     const double* __restrict__ f, uint64_t n_rows, const uint32_t* n_rows_dev, uint64_t m_rt, const double* __restrict__ z,
     const double* __restrict__ v, const double* __restrict__ vn, const float* __restrict__ v32, const uint32_t* __restrict__ vflags,
-    const double* __restrict__ gamma, uint64_t r, double penalty, uint32_t* __restrict__ assoc, double* __restrict__ theta_out,
-    double* __restrict__ apd_out, unsigned long long* __restrict__ best_key, uint32_t* __restrict__ first_row, uint32_t row0) {
+    uint64_t r, uint64_t chunk_vecs, double* __restrict__ part_c, uint32_t* __restrict__ part_j) {
+    // blockIdx.y = chunk of the vector range [y * chunk_vecs, (y + 1) * chunk_vecs): the per-row winners of the chunks are
+    // merged in ascending chunk order by assoc_filter_merge_kernel (strict >: the first strict maximum overall)
     constexpr int MM = M > 0 ? M : kMaxObj;
     const int m = M > 0 ? M : (int)m_rt;
     extern __shared__ __align__(16) float s_v32[];  // kFilterTile x stride: v_j[0..m-1], 1 / |v_j| in fp32, padding
@@ -238,8 +240,9 @@ __global__ void __launch_bounds__(kFilterThreads, 4) assoc_filter_kernel(
     }
     constexpr int SS = (MM + 1 + 3) / 4 * 4;  // compile-time stride when M is known
     const int stride = M > 0 ? SS : (int)v32_stride(m);
-    for (uint64_t j0 = 0; j0 < r; j0 += kFilterTile) {
-        const int tile = (int)((r - j0) < (uint64_t)kFilterTile ? (r - j0) : kFilterTile);
+    const uint64_t j_begin = blockIdx.y * chunk_vecs, j_end = j_begin + chunk_vecs < r ? j_begin + chunk_vecs : r;
+    for (uint64_t j0 = j_begin; j0 < j_end; j0 += kFilterTile) {
+        const int tile = (int)((j_end - j0) < (uint64_t)kFilterTile ? (j_end - j0) : kFilterTile);
         __syncthreads();
         {
             const float4* src = reinterpret_cast<const float4*>(v32 + j0 * stride);
@@ -312,21 +315,50 @@ __global__ void __launch_bounds__(kFilterThreads, 4) assoc_filter_kernel(
 #pragma unroll
     for (int t = 0; t < 2; ++t) {
         if (!live[t]) continue;
-        double theta = 0.0;  // a row at the ideal point: angle 0 to vector 0 (selection.hpp:167-169)
-        if (nf[t] != 0.0) {
-            double c = best_c[t];
-            if (c > 1.0) c = 1.0;
-            if (c < -1.0) c = -1.0;
-            theta = acos(c);  // tensor.hpp:79-83
-        }
-        const double apd = (1.0 + penalty * (theta / gamma[arg[t]])) * nf[t];  // selection.hpp:82-84
-        assoc[row[t]] = arg[t];
-        theta_out[row[t]] = theta;
-        apd_out[row[t]] = apd;
-        const unsigned long long key = (apd != apd) ? kKeyMax : order_key(apd);
-        atomicMin(&best_key[arg[t]], key);
-        atomicMin(&first_row[arg[t]], row0 + (uint32_t)row[t]);
+        part_c[blockIdx.y * n_rows + row[t]] = best_c[t];
+        part_j[blockIdx.y * n_rows + row[t]] = arg[t];
     }
+}
+
+// merges the chunk winners of a row (ascending chunks = ascending j, strict >) and finishes theta / APD / per-vector minima
+__global__ void assoc_filter_merge_kernel(const double* __restrict__ f, uint64_t n_rows, uint64_t m, const double* __restrict__ z,
+                                          const double* __restrict__ part_c, const uint32_t* __restrict__ part_j, uint32_t chunks,
+                                          const double* __restrict__ gamma, double penalty, uint32_t* __restrict__ assoc,
+                                          double* __restrict__ theta_out, double* __restrict__ apd_out,
+                                          unsigned long long* __restrict__ best_key, uint32_t* __restrict__ first_row, uint32_t row0) {
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= n_rows) return;
+    double s = 0.0;
+    for (uint64_t k = 0; k < m; ++k) {
+        const double u = f[i * m + k] - z[k];  // selection.hpp:155-157, same operations as in the scan
+        s += u * u;
+    }
+    const double nf = sqrt(s);
+    double best_c = -INFINITY;
+    uint32_t arg = 0;
+    for (uint32_t c = 0; c < chunks; ++c) {
+        const double pc = part_c[c * n_rows + i];
+        if (pc > best_c) {
+            best_c = pc;
+            arg = part_j[c * n_rows + i];
+        }
+    }
+    double theta = 0.0;  // a row at the ideal point: angle 0 to vector 0 (selection.hpp:167-169)
+    if (nf != 0.0) {
+        double c = best_c;
+        if (c > 1.0) c = 1.0;
+        if (c < -1.0) c = -1.0;
+        theta = acos(c);  // tensor.hpp:79-83
+    } else {
+        arg = 0;
+    }
+    const double apd = (1.0 + penalty * (theta / gamma[arg])) * nf;  // selection.hpp:82-84
+    assoc[i] = arg;
+    theta_out[i] = theta;
+    apd_out[i] = apd;
+    const unsigned long long key = (apd != apd) ? kKeyMax : order_key(apd);
+    atomicMin(&best_key[arg], key);
+    atomicMin(&first_row[arg], row0 + (uint32_t)i);
 }
 
 // lowest row among those that attain the minimal APD of their vector
@@ -407,13 +439,17 @@ void SelectWorkspace::alloc(uint64_t rows_cap_, uint64_t r_, uint64_t m_) {
     tile_scratch = dev_alloc<uint32_t>((r + kCompactTile - 1) / kCompactTile + 1);
     v32 = dev_alloc<float>(r * ((m + 1 + 3) / 4 * 4));
     v32_flags = dev_alloc<uint32_t>(1);
+    if (assoc_filter_preferred(m, r)) {
+        part_c = dev_alloc<double>(rows_cap * kFilterMaxChunks);
+        part_j = dev_alloc<uint32_t>(rows_cap * kFilterMaxChunks);
+    }
     TEMO_CUDA(cudaMemset(err_flag, 0, sizeof(uint32_t)));
 }
 
 void SelectWorkspace::release() {
     cudaFree(z); cudaFree(zkey); cudaFree(vn); cudaFree(assoc); cudaFree(theta); cudaFree(apd);
     cudaFree(best_key); cudaFree(best_row); cudaFree(first_row); cudaFree(elite); cudaFree(valid);
-    cudaFree(n_elite); cudaFree(err_flag); cudaFree(tile_scratch); cudaFree(v32); cudaFree(v32_flags);
+    cudaFree(n_elite); cudaFree(err_flag); cudaFree(tile_scratch); cudaFree(v32); cudaFree(v32_flags); cudaFree(part_c); cudaFree(part_j);
     *this = SelectWorkspace{};
 }
 
@@ -471,7 +507,17 @@ void launch_assoc_filter(const double* f, uint64_t n_rows, uint64_t m, const dou
     require(ws.v32 != nullptr && r <= ws.r && m == ws.m, "rv_select: workspace has no fp32 vector copy");
     TEMO_CUDA(cudaMemsetAsync(ws.v32_flags, 0, sizeof(uint32_t), s));
     v32_kernel<<<(unsigned)((r + 255) / 256), 256, 0, s>>>(v, ws.vn, r, m, ws.v32, ws.v32_flags);
-    const unsigned grid = (unsigned)((n_rows + 2 * kFilterThreads - 1) / (2 * kFilterThreads));
+    const unsigned row_blocks = (unsigned)((n_rows + 2 * kFilterThreads - 1) / (2 * kFilterThreads));
+    // enough CTAs for several waves: the vector range is cut into chunks of whole tiles
+    uint64_t chunks = (4ull * kSMs * 4 + row_blocks - 1) / row_blocks;
+    const uint64_t tiles = (r + kFilterTile - 1) / kFilterTile;
+    if (chunks > (uint64_t)kFilterMaxChunks) chunks = kFilterMaxChunks;
+    if (chunks > tiles) chunks = tiles;
+    if (chunks < 1) chunks = 1;
+    const uint64_t chunk_vecs = (tiles + chunks - 1) / chunks * kFilterTile;
+    chunks = (r + chunk_vecs - 1) / chunk_vecs;
+    require(n_rows <= ws.rows_cap && ws.part_c != nullptr, "rv_select: workspace has no chunk scratch");
+    const dim3 grid(row_blocks, (unsigned)chunks);
     const size_t smem = (size_t)kFilterTile * v32_stride(m) * sizeof(float);
 #define CALL(MV)                                                                                                                  \
     {                                                                                                                             \
@@ -480,8 +526,8 @@ void launch_assoc_filter(const double* f, uint64_t n_rows, uint64_t m, const dou
             TEMO_CUDA(cudaFuncSetAttribute(assoc_filter_kernel<MV>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));    \
             configured = true;                                                                                                    \
         }                                                                                                                         \
-        assoc_filter_kernel<MV><<<grid, kFilterThreads, smem, s>>>(f, n_rows, nullptr, m, ws.z, v, ws.vn, ws.v32, ws.v32_flags, gamma, \
-                                                                   r, penalty, assoc, theta, apd, ws.best_key, ws.first_row, row0); \
+        assoc_filter_kernel<MV><<<grid, kFilterThreads, smem, s>>>(f, n_rows, nullptr, m, ws.z, v, ws.vn, ws.v32, ws.v32_flags, r,  \
+                                                                   chunk_vecs, ws.part_c, ws.part_j);                             \
     }
     switch (m) {
     case 5: CALL(5); break;
@@ -489,6 +535,9 @@ void launch_assoc_filter(const double* f, uint64_t n_rows, uint64_t m, const dou
     default: CALL(0); break;
     }
 #undef CALL
+    assoc_filter_merge_kernel<<<(unsigned)((n_rows + 255) / 256), 256, 0, s>>>(f, n_rows, m, ws.z, ws.part_c, ws.part_j, (uint32_t)chunks,
+                                                                               gamma, penalty, assoc, theta, apd, ws.best_key,
+                                                                               ws.first_row, row0);
     TEMO_CUDA(cudaGetLastError());
 }
 
