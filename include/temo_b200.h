@@ -58,7 +58,21 @@ typedef struct temo_b200_ga_params {
     double xi;  /* mutation distribution index */
 } temo_b200_ga_params;
 
-/* reference: RunConfig, algorithms.hpp:21-41 (GA operator, track_archive = false) */
+/* reproduction operator of the run loop: RunConfig::op, algorithms.hpp:250-271 */
+#define TEMO_B200_OP_GA 0
+#define TEMO_B200_OP_DE 1
+#define TEMO_B200_OP_PSO 2
+#define TEMO_B200_OP_CSO 3
+#define TEMO_B200_OP_RANDOM 4
+
+/* reference: DeParams / PsoParams / CsoParams, operators.hpp:28-41 */
+typedef struct temo_b200_op_params {
+    double de_f, de_cr;
+    double pso_inertia, pso_c1, pso_c2;
+    double cso_phi;
+} temo_b200_op_params;
+
+/* reference: RunConfig, algorithms.hpp:21-41 (track_archive = false) */
 typedef struct temo_b200_run_config {
     int32_t problem;      /* TEMO_B200_DTLZ1.. */
     int32_t rng_mode;     /* TEMO_B200_RNG_* */
@@ -73,7 +87,8 @@ typedef struct temo_b200_run_config {
     double time_budget_s; /* 0 -> run all generations */
     temo_b200_ga_params ga;
     int32_t fuse_eval;    /* 1: evaluate offspring inside the reproduction kernel (default) */
-    int32_t reserved;
+    int32_t op;           /* TEMO_B200_OP_* (0 = ga); de / pso / cso / random: algorithms.hpp:253-268 */
+    temo_b200_op_params opp;
 } temo_b200_run_config;
 
 /* ---- library / device ------------------------------------------------------------- */

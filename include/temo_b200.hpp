@@ -213,12 +213,24 @@ inline Tensor2D apd_scores(const Tensor2D& f, const RefVectorSet& refs, std::siz
 }
 
 // ---- algorithms.hpp --------------------------------------------------------------------------
-/// rvea_run with the GA operator and track_archive = false, device-resident for the whole run.
+/// rvea_run with track_archive = false, device-resident for the whole run; cfg.op = ga / de / pso / cso / random
+/// (algorithms.hpp:250-271).
 inline RunRecord rvea_run(const ProblemInstance& prob, const RunConfig& cfg) {
     temo::detail::require(cfg.pop >= 2 && cfg.generations >= 1, "rvea_run: bad config");
-    if (cfg.op != "ga") throw std::invalid_argument("rvea_run: unknown operator '" + cfg.op + "'");
+    static const char* const kOps[] = {"ga", "de", "pso", "cso", "random"};
+    int op = -1;
+    for (int k = 0; k < 5; ++k)
+        if (cfg.op == kOps[k]) op = k;
+    if (op < 0) throw std::invalid_argument("rvea_run: unknown operator '" + cfg.op + "'");  // algorithms.hpp:270
     temo_b200_run_config c;
     temo_b200_default_run_config(&c);
+    c.op = op;
+    c.opp.de_f = cfg.de.f;
+    c.opp.de_cr = cfg.de.cr;
+    c.opp.pso_inertia = cfg.pso.inertia;
+    c.opp.pso_c1 = cfg.pso.c1;
+    c.opp.pso_c2 = cfg.pso.c2;
+    c.opp.cso_phi = cfg.cso.phi;
     c.problem = detail::problem_id(prob);
     c.pop = cfg.pop;
     c.lattice_h = cfg.lattice_h;

@@ -194,6 +194,14 @@ def main():
              s77_x=s77["x"], s77_f=s77["f"], s77_pop=s77["pop_size"],
              d3_x=d3["x"], d3_f=d3["f"], d3_pop=d3["pop_size"],
              d4_x=d4["x"], d4_f=d4["f"], d4_pop=d4["pop_size"])
+    # ---- the run loop with the other operators (algorithms.hpp:253-268) ----
+    po = {}
+    for op in ("de", "pso", "cso", "random"):
+        for tag, (problem, n, d, m, H, gens, seed) in (("a", ("dtlz2", 40, 9, 3, 0, 12, 3)), ("b", ("dtlz1", 33, 15, 2, 0, 20, 8)),
+                                                        ("c", ("dtlz3", 64, 20, 4, 0, 15, 5))):
+            rr = ref.rvea_run_op(op, problem, n, d, m, gens, seed=seed, lattice_h=H)
+            po.update({f"{op}_{tag}_x": rr["x"], f"{op}_{tag}_f": rr["f"], f"{op}_{tag}_pop": rr["pop_size"]})
+    np.savez(os.path.join(OUT, "pipeline_ops.npz"), **po)
     total = sum(os.path.getsize(os.path.join(OUT, f)) for f in os.listdir(OUT))
     print(f"wrote {OUT}: {total/1024:.1f} KiB")
 

@@ -29,6 +29,7 @@ u8p = C.POINTER(C.c_ubyte)
 
 PROBLEM_IDS = {"dtlz1": 1, "dtlz2": 2, "dtlz3": 3, "dtlz4": 4, "lsmop1": 101}
 GA_DEFAULT = (1.0, 20.0, 1.0, 20.0)  # pc, eta, pm, xi — operators.hpp:22-27
+OPP_DEFAULT = (0.5, 0.9, 0.4, 1.5, 1.5, 0.1)  # de.f, de.cr, pso.inertia, pso.c1, pso.c2, cso.phi — operators.hpp:28-41
 
 
 def build(force: bool = False) -> None:
@@ -67,6 +68,54 @@ class _Base:
     # ---- shared numpy-level helpers -------------------------------------------------
     def take_generation(self, *a, **k):  # pragma: no cover - overridden
         raise NotImplementedError
+
+    def pool_scores(self, f, v, gamma, t, t_max, alpha):
+        """apd_scores (selection.hpp:228-234): rv_core's apd column."""
+        return self.rv_select(f, v, gamma, t, t_max, alpha).apd
+
+    def generation_op(self, op, problem, n, m, seed, counter, lower, upper, t, t_max, alpha, adapt_every,
+                      v0, v, gamma, x, f, swarm=None, ga=GA_DEFAULT, opp=OPP_DEFAULT):
+        """algorithms.hpp:246-281 for any operator of :250-271, composed from this checker's own stage functions.
+        `swarm` is the SwarmState dict {vel, pb_x, pb_score} (None = empty, created on first use like
+        make_swarm_state, operators.hpp:58-60); the updated one is returned under "swarm"."""
+        x, f = _f(x), _f(f)
+        P = x.shape[0]
+        pool_idx, c = self.parent_pool_indices(P, n, seed, counter)
+        idx = pool_idx.astype(np.int64)
+        pool = x[idx]
+        scores = None
+        if op in ("pso", "cso"):
+            scores = self.pool_scores(f[idx], v, gamma, t, t_max, alpha)
+            if swarm is None:
+                swarm = dict(vel=np.zeros_like(pool), pb_x=pool.copy(), pb_score=scores.copy())
+        if op == "ga":
+            off, c = self.ga_reproduce(pool, seed, c, lower, upper, ga)
+        elif op == "de":
+            off, c = self.de_reproduce(pool, seed, c, lower, upper, opp[0:2])
+        elif op == "pso":
+            off, c, vel, pbx, pbs = self.pso_reproduce(pool, scores, seed, c, lower, upper, swarm["vel"], swarm["pb_x"],
+                                                       swarm["pb_score"], opp[2:5])
+            swarm = dict(vel=vel, pb_x=pbx, pb_score=pbs)
+        elif op == "cso":
+            off, c, vel = self.cso_reproduce(pool, scores, seed, c, lower, upper, swarm["vel"], opp[5:6])
+            swarm = dict(swarm, vel=vel)
+        elif op == "random":
+            off, c = self.random_reproduce(n, pool.shape[1], seed, c, lower, upper)
+        else:
+            raise ValueError(f"rvea_run: unknown operator '{op}'")
+        f_off = self.evaluate(problem, off, m)
+        mx, mf = np.vstack([x, off]), np.vstack([f, f_off])
+        sel = self.rv_select(mf, v, gamma, t, t_max, alpha)
+        e = sel.elite.astype(np.int64)
+        nx, nf = mx[e], mf[e]
+        v, gamma = _f(v).copy(), _f(gamma).copy()
+        if (t + 1) % adapt_every == 0:
+            v, gamma = self.adapt(v0, v, gamma, nf.min(axis=0), nf.max(axis=0))
+        return dict(x=nx, f=nf, v=v, gamma=gamma, counter=c, offspring=off, f_off=f_off, elite=sel.elite, swarm=swarm,
+                    scores=scores)
+
+
+OPERATOR_IDS = {"ga": 0, "de": 1, "pso": 2, "cso": 3, "random": 4}
 
 
 class Oracle(_Base):
@@ -300,6 +349,22 @@ class Oracle(_Base):
             raise RuntimeError(f"rvea_run rc={rc}")
         k = rows.value
         return dict(x=x[:k].copy(), f=f[:k].copy(), pop_size=pops, v=v, gamma=gamma, counter=c.value)
+
+    def rvea_run_op(self, op, problem, n, d, m, generations, seed=42, lattice_h=0, alpha=2.0, fr=0.1, ga=GA_DEFAULT,
+                    opp=OPP_DEFAULT):
+        H = lattice_h or self.lattice_density_for(m, n)
+        r = self.lattice_count(m, H)
+        cap = max(n, r)
+        x, f = np.empty((cap, d)), np.empty((cap, m))
+        rows, c = u64(0), u64(0)
+        pops = np.zeros(generations, dtype=np.uint64)
+        rc = self.lib.to_rvea_run_op(C.c_int(PROBLEM_IDS[problem]), C.c_int(OPERATOR_IDS[op]), _p(_f(opp)), u64(n), u64(d), u64(m),
+                                     u64(lattice_h), u64(generations), C.c_double(alpha), C.c_double(fr), u64(seed), _p(_f(ga)),
+                                     _p(x), _p(f), C.byref(rows), _p(pops, u64p), C.byref(c))
+        if rc:
+            raise RuntimeError(f"rvea_run_op rc={rc}")
+        k = rows.value
+        return dict(x=x[:k].copy(), f=f[:k].copy(), pop_size=pops, counter=c.value)
 
 
 class Ref(_Base):
@@ -542,3 +607,19 @@ class Ref(_Base):
         k, g_done = rows.value, done.value
         return dict(x=None if x is None else x[:k].copy(), f=f[:k].copy(), pop_size=pops[:g_done],
                     elapsed_ms=ms[:g_done], igd=igd[:g_done])
+
+    def rvea_run_op(self, op, problem, n, d, m, generations, seed=42, lattice_h=0, alpha=2.0, fr=0.1, ga=GA_DEFAULT,
+                    opp=OPP_DEFAULT):
+        """The reference's own rvea_run with RunConfig::op = op (algorithms.hpp:250-271)."""
+        H = lattice_h or self.lattice_density_for(m, n)
+        r = self.lattice_count(m, H)
+        cap = max(n, r)
+        x, f = np.empty((cap, d)), np.empty((cap, m))
+        cfg_u = np.array([n, lattice_h, generations, seed, d, m], dtype=np.uint64)
+        cfg_d = np.array([alpha, fr, 0.0])
+        rows, done = u64(0), u64(0)
+        pops = np.zeros(generations, dtype=np.uint64)
+        self._chk(self.lib.ref_rvea_run_op(problem.encode(), op.encode(), _p(_f(opp)), _p(cfg_u, u64p), _p(cfg_d), _p(_f(ga)),
+                                           _p(x), _p(f), C.byref(rows), C.byref(done), _p(pops, u64p)))
+        k = rows.value
+        return dict(x=x[:k].copy(), f=f[:k].copy(), pop_size=pops[: done.value])

@@ -350,4 +350,41 @@ int ref_rvea_run(int which, const char* problem, const std::uint64_t* cfg_u, con
     });
 }
 
+// rvea_run with any operator of algorithms.hpp:250-271 (op = "ga" / "de" / "pso" / "cso" / "random");
+// opp = {de.f, de.cr, pso.inertia, pso.c1, pso.c2, cso.phi}; cfg_u / cfg_d as in ref_rvea_run.
+int ref_rvea_run_op(const char* problem, const char* op, const double* opp, const std::uint64_t* cfg_u, const double* cfg_d,
+                    const double* ga, double* final_x, double* final_f, std::uint64_t* final_rows, std::uint64_t* rows_done,
+                    std::uint64_t* pop_size) {
+    return guarded([&] {
+        temo::RunConfig cfg;
+        cfg.problem = problem;
+        cfg.op = op;
+        cfg.pop = cfg_u[0];
+        cfg.lattice_h = cfg_u[1];
+        cfg.generations = cfg_u[2];
+        cfg.seed = cfg_u[3];
+        cfg.dim = cfg_u[4];
+        cfg.obj = cfg_u[5];
+        cfg.alpha = cfg_d[0];
+        cfg.fr = cfg_d[1];
+        cfg.time_budget_s = cfg_d[2];
+        cfg.track_archive = false;
+        cfg.ga = ga_of(ga);
+        cfg.de.f = opp[0];
+        cfg.de.cr = opp[1];
+        cfg.pso.inertia = opp[2];
+        cfg.pso.c1 = opp[3];
+        cfg.pso.c2 = opp[4];
+        cfg.cso.phi = opp[5];
+        const temo::ProblemInstance prob = temo::make_problem(cfg.problem, cfg.dim, cfg.obj);
+        const temo::RunRecord rec = temo::rvea_run(prob, cfg, temo::MetricContext{});
+        *final_rows = rec.final_x.rows;
+        if (final_x) unwrap(rec.final_x, final_x);
+        if (final_f) unwrap(rec.final_f, final_f);
+        *rows_done = rec.rows.size();
+        for (std::size_t i = 0; i < rec.rows.size(); ++i)
+            if (pop_size) pop_size[i] = rec.rows[i].pop_size;
+    });
+}
+
 } // extern "C"

@@ -716,3 +716,105 @@ int to_rvea_run(int problem, uint64_t n, uint64_t d, uint64_t m, uint64_t lattic
     free(v0); free(v); free(gamma); free(lower); free(upper); free(x); free(f);
     return rc;
 }
+
+/* algorithms.hpp:227-296 with track_archive = false and any operator of :250-271.
+ * op: 0 ga, 1 de, 2 pso, 3 cso, 4 random. opp = {de.f, de.cr, pso.inertia, pso.c1, pso.c2, cso.phi}
+ * (operators.hpp:28-41). pso / cso take apd_scores of the pool's objectives as fitness (:257-258, :263-264)
+ * and carry a SwarmState created on first use (operators.hpp:58-60). */
+int to_rvea_run_op(int problem, int op, const double* opp, uint64_t n, uint64_t d, uint64_t m, uint64_t lattice_h,
+                   uint64_t generations, double alpha, double fr, uint64_t seed, const double* ga,
+                   double* x_out, double* f_out, uint64_t* rows_out, uint64_t* pop_size, uint64_t* counter_out) {
+    if (n < 2 || generations < 1 || m > 64 || op < 0 || op > 4) return -1;
+    const uint64_t H = lattice_h ? lattice_h : to_lattice_density_for(m, n);
+    const uint64_t r = to_lattice_count(m, H);
+    const uint64_t cap = (n > r ? n : r) + n; /* merged rows */
+    double* v0 = (double*)malloc(r * m * sizeof(double));
+    double* v = (double*)malloc(r * m * sizeof(double));
+    double* gamma = (double*)malloc(r * sizeof(double));
+    double* lower = (double*)malloc(d * sizeof(double));
+    double* upper = (double*)malloc(d * sizeof(double));
+    double* x = (double*)malloc(cap * d * sizeof(double));
+    double* f = (double*)malloc(cap * m * sizeof(double));
+    double* nx = (double*)malloc(cap * d * sizeof(double));
+    double* nf = (double*)malloc(cap * m * sizeof(double));
+    double* pool = (double*)malloc(n * d * sizeof(double));
+    double* pool_f = (double*)malloc(n * m * sizeof(double));
+    double* scores = (double*)malloc(n * sizeof(double));
+    double* vel = (double*)calloc(n * d, sizeof(double));
+    double* pb_x = (double*)malloc(n * d * sizeof(double));
+    double* pb_s = (double*)malloc(n * sizeof(double));
+    uint64_t* pool_idx = (uint64_t*)malloc(n * sizeof(uint64_t));
+    uint64_t* elite = (uint64_t*)malloc((r > cap ? r : cap) * sizeof(uint64_t));
+    unsigned char* valid = (unsigned char*)malloc(r);
+    if (!v0 || !v || !gamma || !lower || !upper || !x || !f || !nx || !nf || !pool || !pool_f || !scores || !vel || !pb_x ||
+        !pb_s || !pool_idx || !elite || !valid)
+        return -2;
+    int rc = to_make_ref_set(m, H, v0, gamma);
+    memcpy(v, v0, r * m * sizeof(double));
+    const double ae = ceil(fr * (double)generations);
+    const uint64_t adapt_every = ae < 1.0 ? 1 : (uint64_t)ae;
+    to_problem_bounds(problem, d, m, lower, upper);
+    uint64_t counter = 0, rows = n;
+    int swarm_empty = 1;
+    if (!rc) {
+        to_random_reproduce(n, d, seed, &counter, lower, upper, x);
+        rc = to_evaluate(problem, x, n, d, m, f);
+    }
+    for (uint64_t t = 0; !rc && t < generations; ++t) {
+        const uint64_t P = rows;
+        to_parent_pool_indices(P, n, seed, &counter, pool_idx);                                   /* :247 */
+        for (uint64_t i = 0; i < n; ++i) memcpy(pool + i * d, x + pool_idx[i] * d, d * sizeof(double));
+        double* off = x + P * d;   /* merged = parents first, then offspring (:274-275) */
+        double* f_off = f + P * m;
+        if (op == 2 || op == 3) {
+            for (uint64_t i = 0; i < n; ++i) memcpy(pool_f + i * m, f + pool_idx[i] * m, m * sizeof(double));
+            uint64_t cnt0 = 0;
+            rc = to_rv_select(pool_f, n, m, v, gamma, r, t, generations, alpha, elite, &cnt0, valid, NULL, NULL, scores);
+            if (rc) break;
+            if (swarm_empty) { /* make_swarm_state */
+                memset(vel, 0, n * d * sizeof(double));
+                memcpy(pb_x, pool, n * d * sizeof(double));
+                memcpy(pb_s, scores, n * sizeof(double));
+                swarm_empty = 0;
+            }
+        }
+        switch (op) {
+        case 0: rc = to_ga_reproduce(pool, n, d, seed, &counter, ga, lower, upper, off); break;
+        case 1: rc = to_de_reproduce(pool, n, d, seed, &counter, opp, lower, upper, off); break;
+        case 2: rc = to_pso_reproduce(pool, scores, n, d, seed, &counter, opp + 2, vel, pb_x, pb_s, lower, upper, off); break;
+        case 3: rc = to_cso_reproduce(pool, scores, n, d, seed, &counter, opp + 5, vel, lower, upper, off); break;
+        default: to_random_reproduce(n, d, seed, &counter, lower, upper, off); break;
+        }
+        if (!rc) rc = to_evaluate(problem, off, n, d, m, f_off);
+        uint64_t cnt = 0;
+        if (!rc) rc = to_rv_select(f, P + n, m, v, gamma, r, t, generations, alpha, elite, &cnt, valid, NULL, NULL, NULL);
+        if (rc) break;
+        for (uint64_t k = 0; k < cnt; ++k) {
+            memcpy(nx + k * d, x + elite[k] * d, d * sizeof(double));
+            memcpy(nf + k * m, f + elite[k] * m, m * sizeof(double));
+        }
+        memcpy(x, nx, cnt * d * sizeof(double));
+        memcpy(f, nf, cnt * m * sizeof(double));
+        rows = cnt;
+        if ((t + 1) % adapt_every == 0) {
+            double zmin[64], zmax[64];
+            for (uint64_t k = 0; k < m; ++k) zmin[k] = zmax[k] = f[k];
+            for (uint64_t i = 1; i < cnt; ++i)
+                for (uint64_t k = 0; k < m; ++k) {
+                    if (f[i * m + k] < zmin[k]) zmin[k] = f[i * m + k];
+                    if (f[i * m + k] > zmax[k]) zmax[k] = f[i * m + k];
+                }
+            rc = to_adapt(v0, v, gamma, r, m, zmin, zmax);
+        }
+        if (pop_size) pop_size[t] = rows;
+    }
+    if (!rc) {
+        memcpy(x_out, x, rows * d * sizeof(double));
+        memcpy(f_out, f, rows * m * sizeof(double));
+        *rows_out = rows;
+        if (counter_out) *counter_out = counter;
+    }
+    free(v0); free(v); free(gamma); free(lower); free(upper); free(x); free(f); free(nx); free(nf); free(pool);
+    free(pool_f); free(scores); free(vel); free(pb_x); free(pb_s); free(pool_idx); free(elite); free(valid);
+    return rc;
+}

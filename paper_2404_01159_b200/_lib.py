@@ -23,12 +23,17 @@ class GaParamsC(C.Structure):
     _fields_ = [("pc", C.c_double), ("eta", C.c_double), ("pm", C.c_double), ("xi", C.c_double)]
 
 
+class OpParamsC(C.Structure):
+    _fields_ = [("de_f", C.c_double), ("de_cr", C.c_double), ("pso_inertia", C.c_double), ("pso_c1", C.c_double),
+                ("pso_c2", C.c_double), ("cso_phi", C.c_double)]
+
+
 class RunConfigC(C.Structure):
     _fields_ = [
         ("problem", C.c_int32), ("rng_mode", C.c_int32),
         ("pop", u64), ("lattice_h", u64), ("generations", u64), ("seed", u64), ("dim", u64), ("obj", u64),
         ("alpha", C.c_double), ("fr", C.c_double), ("time_budget_s", C.c_double),
-        ("ga", GaParamsC), ("fuse_eval", C.c_int32), ("reserved", C.c_int32),
+        ("ga", GaParamsC), ("fuse_eval", C.c_int32), ("op", C.c_int32), ("opp", OpParamsC),
     ]
 
 

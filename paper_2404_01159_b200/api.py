@@ -410,9 +410,12 @@ def apd_scores(f, refs: RefVectorSet, t: int, t_max: int, alpha: float = 2.0) ->
 
 
 # ------------------------------------------------------------------------ algorithms.hpp
+OPERATOR_IDS = {"ga": 0, "de": 1, "pso": 2, "cso": 3, "random": 4}  # TEMO_B200_OP_*
+
+
 @dataclass
 class RunConfig:
-    """reference: RunConfig (algorithms.hpp:21-41), GA operator, track_archive = false."""
+    """reference: RunConfig (algorithms.hpp:21-41), track_archive = false; op = ga / de / pso / cso / random."""
     problem: str = "dtlz2"
     op: str = "ga"
     pop: int = 105
@@ -425,12 +428,15 @@ class RunConfig:
     dim: int = 0
     obj: int = 3
     ga: GaParams = field(default_factory=GaParams)
+    de: tuple = (0.5, 0.9)         # DeParams {f, cr}, operators.hpp:28-31
+    pso: tuple = (0.4, 1.5, 1.5)   # PsoParams {inertia, c1, c2}, operators.hpp:33-37
+    cso: tuple = (0.1,)            # CsoParams {phi}, operators.hpp:39-41
     rng_mode: int = RNG_SPLITMIX64
     fuse_eval: bool = True
 
     def c(self) -> RunConfigC:
-        if self.op != "ga":
-            raise ValueError(f"rvea_run: unknown operator '{self.op}'")  # only the GA path is in scope
+        if self.op not in OPERATOR_IDS:
+            raise ValueError(f"rvea_run: unknown operator '{self.op}'")  # algorithms.hpp:270
         if self.problem not in PROBLEM_IDS:
             raise ValueError(f"make_problem: unknown problem '{self.problem}'")
         cfg = RunConfigC()
@@ -442,6 +448,10 @@ class RunConfig:
         cfg.alpha, cfg.fr, cfg.time_budget_s = self.alpha, self.fr, self.time_budget_s
         cfg.ga = self.ga.c()
         cfg.fuse_eval = 1 if self.fuse_eval else 0
+        cfg.op = OPERATOR_IDS[self.op]
+        cfg.opp.de_f, cfg.opp.de_cr = self.de
+        cfg.opp.pso_inertia, cfg.opp.pso_c1, cfg.opp.pso_c2 = self.pso
+        (cfg.opp.cso_phi,) = self.cso
         return cfg
 
 

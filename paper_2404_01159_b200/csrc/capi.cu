@@ -80,6 +80,13 @@ RunConfig cfg_of(const temo_b200_run_config* c) {
     r.time_budget_s = c->time_budget_s;
     r.ga = ga_of(&c->ga);
     r.fuse_eval = c->fuse_eval;
+    r.op = c->op;
+    r.de_f = c->opp.de_f;
+    r.de_cr = c->opp.de_cr;
+    r.pso_inertia = c->opp.pso_inertia;
+    r.pso_c1 = c->opp.pso_c1;
+    r.pso_c2 = c->opp.pso_c2;
+    r.cso_phi = c->opp.cso_phi;
     require(r.rng_mode == 0 || r.rng_mode == 1, "unknown rng mode");
     return r;
 }
@@ -179,6 +186,13 @@ void temo_b200_default_run_config(temo_b200_run_config* cfg) {
     cfg->time_budget_s = 0.0;
     temo_b200_default_ga_params(&cfg->ga);
     cfg->fuse_eval = 1;
+    cfg->op = TEMO_B200_OP_GA;
+    cfg->opp.de_f = 0.5;  // operators.hpp:28-41
+    cfg->opp.de_cr = 0.9;
+    cfg->opp.pso_inertia = 0.4;
+    cfg->opp.pso_c1 = 1.5;
+    cfg->opp.pso_c2 = 1.5;
+    cfg->opp.cso_phi = 0.1;
 }
 
 // ---- rng.hpp ------------------------------------------------------------------------------

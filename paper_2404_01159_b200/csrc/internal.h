@@ -88,16 +88,18 @@ void launch_pow_batch(const double* x, const double* y, uint64_t n, double* out,
 
 // ---- the other reproduction operators (swarm.cu) ------------------------------------
 // de_reproduce (operators.hpp:166-200): draws consumed 4 n + n d.
+// src / dst (optional, all three): operand row i is read from storage row src[i] of x, child i is written to storage row
+// dst[i] of out (the device-resident run addresses its pool this way); nullptr = dense matrices.
 void launch_de(const double* x, uint64_t n, uint64_t d, Rng rng, uint64_t counter, double f, double cr, const double* lower,
-               const double* upper, double* out, cudaStream_t s);
+               const double* upper, double* out, cudaStream_t s, const uint32_t* src = nullptr, const uint32_t* dst = nullptr);
 // pso_reproduce (operators.hpp:205-240): vel / pb_x / pb_score are the SwarmState, updated in place; draws 2 n d.
 void launch_pso(const double* x, const double* scores, uint64_t n, uint64_t d, Rng rng, uint64_t counter, double inertia, double c1,
                 double c2, double* vel, double* pb_x, double* pb_score, uint32_t* best_scratch, const double* lower,
-                const double* upper, double* out, cudaStream_t s);
+                const double* upper, double* out, cudaStream_t s, const uint32_t* src = nullptr, const uint32_t* dst = nullptr);
 // cso_reproduce (operators.hpp:246-284) after the caller's shuffle_indices (n - 1 draws): draws 3 (n / 2) d from `counter`.
 void launch_cso(const double* x, const double* scores, uint64_t n, uint64_t d, Rng rng, uint64_t counter, double phi,
                 const uint32_t* perm, double* mean_scratch, const double* vel, double* vel_out, const double* lower,
-                const double* upper, double* out, cudaStream_t s);
+                const double* upper, double* out, cudaStream_t s, const uint32_t* src = nullptr, const uint32_t* dst = nullptr);
 
 // ---- K2: evaluation -------------------------------------------------------------------------
 struct EvalArgs {

@@ -29,13 +29,22 @@ namespace {
 // (algorithms.hpp:211-221); mating row i is pool row perm[i] (operators.hpp:155-158).
 template <int MODE>
 __global__ void build_src_kernel(const uint32_t* perm, const uint32_t* parent_slot, uint64_t n, uint64_t P,
-                                 Rng rng, uint64_t c_pool, uint32_t* src) {
+                                 Rng rng, uint64_t c_pool, uint32_t* src, uint32_t* pool_idx_out) {
     const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const uint64_t q = perm[i];
+    const uint64_t q = perm ? perm[i] : i;  // no mating shuffle for de / pso / cso: pool order
     uint64_t k = q;
     if (P != n) k = (uint64_t)(word_to_unit(draw_word<MODE>(rng, c_pool + q)) * (double)P);
     src[i] = parent_slot[k];
+    if (pool_idx_out) pool_idx_out[i] = (uint32_t)k;  // survivor index of pool row i (its objective row)
+}
+
+// pool_f = take_rows(f, pool_idx) (algorithms.hpp:257,263)
+__global__ void gather_f_kernel(const double* f, const uint32_t* idx, uint64_t n, uint64_t m, double* out) {
+    const uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (e >= n * m) return;
+    const uint64_t i = e / m, j = e - i * m;
+    out[e] = f[(uint64_t)idx[i] * m + j];
 }
 
 // Survivor k takes over the storage slot and the objective row of merged row elite[k]
@@ -93,6 +102,8 @@ Run::Run(const RunConfig& c) : cfg(c) {
     require(cfg.pop >= 2 && cfg.generations >= 1, "rvea_run: bad config");  // algorithms.hpp:229
     require(problem_known(cfg.problem), "make_problem: unknown problem");
     require(cfg.obj >= 2 && cfg.obj <= (uint64_t)kMaxObj, "rvea_run: objective count out of range");
+    require(cfg.op >= kOpGa && cfg.op <= kOpRandom, "rvea_run: unknown operator");  // algorithms.hpp:270
+    if (cfg.op == kOpDe) require(cfg.pop >= 4, "de_reproduce: needs at least four rows");
     n = cfg.pop;
     m = cfg.obj;
     d = cfg.dim ? cfg.dim : problem_default_dim(cfg.problem, m);
@@ -118,6 +129,20 @@ Run::Run(const RunConfig& c) : cfg(c) {
     }
     src = dev_alloc<uint32_t>(n);
     perm_dev = dev_alloc<uint32_t>(n);
+    if (cfg.op == kOpPso || cfg.op == kOpCso) {  // SwarmState + the scalarised fitness of the pool (algorithms.hpp:255-268)
+        pool_idx_dev = dev_alloc<uint32_t>(n);
+        pool_f = dev_alloc<double>(n * m);
+        scores = dev_alloc<double>(n);
+        sw_vel[0] = dev_alloc<double>(n * d);
+        if (cfg.op == kOpPso) {
+            sw_pbx = dev_alloc<double>(n * d);
+            sw_pbs = dev_alloc<double>(n);
+            sw_best = dev_alloc<uint32_t>(1);
+        } else {
+            sw_vel[1] = dev_alloc<double>(n * d);
+            sw_mean = dev_alloc<double>(d);
+        }
+    }
     used = dev_alloc<unsigned char>(cap);
     d_P = dev_alloc<uint32_t>(1);
     free_scratch = dev_alloc<uint32_t>((cap + kCompactTile - 1) / kCompactTile + 1);
@@ -185,6 +210,8 @@ Run::~Run() {
     cudaFree(src); cudaFree(perm_dev); cudaFree(used); cudaFree(d_P); cudaFree(free_scratch);
     cudaFree(v0); cudaFree(v); cudaFree(gamma); cudaFree(lower); cudaFree(upper);
     cudaFree(zmin); cudaFree(zmax); cudaFree(zscratch); cudaFree(skip_flag); cudaFree(f_off_saved);
+    cudaFree(pool_idx_dev); cudaFree(pool_f); cudaFree(scores); cudaFree(sw_vel[0]); cudaFree(sw_vel[1]);
+    cudaFree(sw_pbx); cudaFree(sw_pbs); cudaFree(sw_mean); cudaFree(sw_best);
     cudaFreeHost(h_status);
     ws.release();
     vindex.release();
@@ -207,17 +234,27 @@ Run::Plan Run::plan_for(uint64_t P_now, uint64_t c) const {
     p.c_pool = c;
     if (P_now != n) c += n;
     p.c_shuffle = c;
-    c += n - 1;
+    if (uses_perm()) c += n - 1;  // ga: operators.hpp:155, cso: operators.hpp:254
     p.c_sbx = c;
     const uint64_t h = n / 2;
-    c += 3 * h * d + h;
-    p.c_pm = c;
-    c += 2 * n * d;
+    switch (cfg.op) {
+    case kOpGa:
+        c += 3 * h * d + h;
+        p.c_pm = c;
+        c += 2 * n * d;
+        break;
+    case kOpDe: c += 4 * n + n * d; break;   // operators.hpp:170-172
+    case kOpPso: c += 2 * n * d; break;      // operators.hpp:223-224
+    case kOpCso: c += 3 * h * d; break;      // operators.hpp:256-258
+    default: c += n * d; break;              // random_reproduce, operators.hpp:289
+    }
+    if (cfg.op != kOpGa) p.c_pm = c;
     p.c_end = c;
     return p;
 }
 
 void Run::ensure_permutation(const Plan& p) {
+    if (!uses_perm()) return;
     if (spec_valid && spec_c_shuffle == p.c_shuffle) return;  // speculation hit
     uint64_t c = p.c_shuffle;
     shuffle_indices(cfg.seed, c, n, h_perm[hp]);
@@ -227,10 +264,59 @@ void Run::ensure_permutation(const Plan& p) {
 
 void Run::launch_mating_table(const Plan& p) {
     const unsigned g = (unsigned)((n + 255) / 256);
+    // ga mates rows in shuffled order; the other operators address the pool in its own order (cso applies its
+    // permutation to pool rows itself)
+    const uint32_t* perm = cfg.op == kOpGa ? perm_dev : nullptr;
     if (rng.mode == 0)
-        build_src_kernel<0><<<g, 256, 0, stream>>>(perm_dev, parent_slot[cur], n, P, rng, p.c_pool, src);
+        build_src_kernel<0><<<g, 256, 0, stream>>>(perm, parent_slot[cur], n, P, rng, p.c_pool, src, pool_idx_dev);
     else
-        build_src_kernel<1><<<g, 256, 0, stream>>>(perm_dev, parent_slot[cur], n, P, rng, p.c_pool, src);
+        build_src_kernel<1><<<g, 256, 0, stream>>>(perm, parent_slot[cur], n, P, rng, p.c_pool, src, pool_idx_dev);
+}
+
+// de / pso / cso / random in place of ga_reproduce (algorithms.hpp:253-268): operands are read through src[] (pool row
+// i = storage row src[i]), children go to the free slots; pso and cso take apd_scores of the pool's objectives as
+// fitness and carry the SwarmState, which is indexed by pool row like the reference's.
+uint64_t Run::launch_other_operator(const Plan& p) {
+    uint64_t launches = 0;
+    if (cfg.op == kOpPso || cfg.op == kOpCso) {
+        gather_f_kernel<<<(unsigned)((n * m + 255) / 256), 256, 0, stream>>>(fm[cur], pool_idx_dev, n, m, pool_f);  // :257,263
+        const double penalty = apd_penalty(m, t, cfg.generations, cfg.alpha);
+        launch_select(pool_f, n, nullptr, m, v, gamma, r, penalty, ws, stream, &vindex);  // apd_scores = rv_core's apd column
+        TEMO_CUDA(cudaMemcpyAsync(scores, ws.apd, n * sizeof(double), cudaMemcpyDeviceToDevice, stream));
+        launches += 1 + 9;
+        if (!swarm_ready) {  // make_swarm_state (operators.hpp:58-60): zero velocities, personal bests = the pool
+            TEMO_CUDA(cudaMemsetAsync(sw_vel[0], 0, n * d * sizeof(double), stream));
+            if (cfg.op == kOpPso) {
+                gather_rows_kernel<<<(unsigned)n, 256, 0, stream>>>(pool, src, n, d, sw_pbx);
+                TEMO_CUDA(cudaMemcpyAsync(sw_pbs, scores, n * sizeof(double), cudaMemcpyDeviceToDevice, stream));
+                ++launches;
+            }
+            sw_cur = 0;
+            swarm_ready = true;
+        }
+    }
+    switch (cfg.op) {
+    case kOpDe:
+        launch_de(pool, n, d, rng, p.c_sbx, cfg.de_f, cfg.de_cr, lower, upper, pool, stream, src, free_slot[cur]);
+        launches += 1;
+        break;
+    case kOpPso:
+        launch_pso(pool, scores, n, d, rng, p.c_sbx, cfg.pso_inertia, cfg.pso_c1, cfg.pso_c2, sw_vel[0], sw_pbx, sw_pbs, sw_best,
+                   lower, upper, pool, stream, src, free_slot[cur]);
+        launches += 3;
+        break;
+    case kOpCso:
+        launch_cso(pool, scores, n, d, rng, p.c_sbx, cfg.cso_phi, perm_dev, sw_mean, sw_vel[sw_cur], sw_vel[sw_cur ^ 1], lower,
+                   upper, pool, stream, src, free_slot[cur]);
+        sw_cur ^= 1;
+        launches += 2;
+        break;
+    default:  // random_reproduce (algorithms.hpp:266-267)
+        launch_random_reproduce(pool, free_slot[cur], n, d, rng, p.c_sbx, lower, upper, stream);
+        launches += 1;
+        break;
+    }
+    return launches;
 }
 
 void Run::launch_reproduction(const Plan& p, bool fused) {
@@ -270,7 +356,7 @@ void Run::launch_offspring_eval() {
     launch_evaluate(ea, stream);
 }
 
-bool Run::fusable() const { return cfg.fuse_eval && cfg.problem >= kDtlz1 && cfg.problem <= kDtlz4; }
+bool Run::fusable() const { return cfg.op == kOpGa && cfg.fuse_eval && cfg.problem >= kDtlz1 && cfg.problem <= kDtlz4; }
 
 uint64_t Run::step(double* survivors_f_host, const double* f_off_inject) {
     require(t < cfg.generations, "rvea_run: all generations already done");
@@ -281,15 +367,21 @@ uint64_t Run::step(double* survivors_f_host, const double* f_off_inject) {
     const double host1 = now_ms();
 
     TEMO_CUDA(cudaEventRecord(ev[0], stream));
-    TEMO_CUDA(cudaMemcpyAsync(perm_dev, h_perm[hp], n * sizeof(uint32_t), cudaMemcpyHostToDevice, stream));
+    if (uses_perm())
+        TEMO_CUDA(cudaMemcpyAsync(perm_dev, h_perm[hp], n * sizeof(uint32_t), cudaMemcpyHostToDevice, stream));
     const bool fused = fusable();
     launch_mating_table(p);
     TEMO_CUDA(cudaEventRecord(ev[1], stream));
-    launch_reproduction(p, fused);
+    uint64_t launches = 1 + (fused ? 0 : 1) + 9 + 4;
+    if (cfg.op == kOpGa) {
+        launch_reproduction(p, fused);
+        ++launches;
+    } else {
+        launches += launch_other_operator(p);
+    }
     TEMO_CUDA(cudaEventRecord(ev[2], stream));
     if (!fused) launch_offspring_eval();
     TEMO_CUDA(cudaEventRecord(ev[3], stream));
-    uint64_t launches = 2 + (fused ? 0 : 1) + 9 + 4;
     if (f_off_inject) {  // lock-step testing: keep the device's objectives aside, select on the given ones
         if (!f_off_saved) f_off_saved = dev_alloc<double>(n * m);
         TEMO_CUDA(cudaMemcpyAsync(f_off_saved, fm[cur] + P * m, n * m * sizeof(double), cudaMemcpyDeviceToDevice, stream));
@@ -430,6 +522,7 @@ void Run::last_generation(double* offspring, double* f_off, uint64_t* elite_out)
 
 double Run::time_stage(int stage, int reps) {
     require(reps >= 1, "time_stage: reps must be positive");
+    require(cfg.op == kOpGa, "time_stage: the isolated stages are those of the ga loop");
     const Plan p = plan_for(P, counter);
     ensure_permutation(p);
     TEMO_CUDA(cudaMemcpyAsync(perm_dev, h_perm[hp], n * sizeof(uint32_t), cudaMemcpyHostToDevice, stream));

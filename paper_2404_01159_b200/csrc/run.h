@@ -13,14 +13,21 @@ struct RunConfig {  // reference: RunConfig, algorithms.hpp:21-41
     double alpha = 2.0, fr = 0.1, time_budget_s = 0.0;
     GaParams ga;
     int fuse_eval = 1;
+    // reproduction operator (algorithms.hpp:250-268): 0 ga, 1 de, 2 pso, 3 cso, 4 random; the swarm operators take
+    // apd_scores of the parent pool as fitness and carry a SwarmState across generations
+    int op = 0;
+    double de_f = 0.5, de_cr = 0.9;                          // DeParams, operators.hpp:28-31
+    double pso_inertia = 0.4, pso_c1 = 1.5, pso_c2 = 1.5;    // PsoParams, operators.hpp:33-37
+    double cso_phi = 0.1;                                    // CsoParams, operators.hpp:39-41
 };
+constexpr int kOpGa = 0, kOpDe = 1, kOpPso = 2, kOpCso = 3, kOpRandom = 4;  // TEMO_B200_OP_*
 
 void flush_l2();
 
 struct Run {
     static constexpr int kNumEvents = 6;
     struct Plan {
-        uint64_t c_pool, c_shuffle, c_sbx, c_pm, c_end;
+        uint64_t c_pool, c_shuffle, c_sbx, c_pm, c_end;  // c_sbx doubles as the first draw of de / pso / cso
     };
 
     explicit Run(const RunConfig& c);
@@ -52,6 +59,14 @@ struct Run {
     int cur = 0;
     uint32_t* src = nullptr;
     uint32_t* perm_dev = nullptr;
+    // pso / cso: survivor index of every pool row (its objective row), and the swarm state
+    uint32_t* pool_idx_dev = nullptr;
+    double *pool_f = nullptr, *scores = nullptr;                         // n x m, n
+    double *sw_vel[2] = {nullptr, nullptr}, *sw_pbx = nullptr, *sw_pbs = nullptr;  // SwarmState (operators.hpp:46-56)
+    double* sw_mean = nullptr;
+    uint32_t* sw_best = nullptr;
+    int sw_cur = 0;
+    bool swarm_ready = false;
     unsigned char* used = nullptr;
     uint32_t* d_P = nullptr;
     uint32_t* free_scratch = nullptr;
@@ -79,6 +94,8 @@ private:
     void ensure_permutation(const Plan& p);
     void launch_mating_table(const Plan& p);
     void launch_reproduction(const Plan& p, bool fused);
+    uint64_t launch_other_operator(const Plan& p);  // returns its launch count
+    bool uses_perm() const { return cfg.op == kOpGa || cfg.op == kOpCso; }
     void launch_offspring_eval();
     bool fusable() const;
     uint64_t P_prev() const { return P_before; }

@@ -21,7 +21,8 @@ __device__ __forceinline__ double unit_draw(const Rng& g, uint64_t k) {
 // ---- DE/rand/1/bin -----------------------------------------------------------------------------------------
 // draws: r_sel n x 3 at c, r_j n x 1 at c + 3n, r_cr n x d at c + 4n
 template <int MODE>
-__global__ void __launch_bounds__(256) de_kernel(const double* __restrict__ x, uint64_t n, uint64_t d, Rng rng, uint64_t c, double f,
+__global__ void __launch_bounds__(256) de_kernel(const double* __restrict__ x, const uint32_t* __restrict__ src,
+                                                  const uint32_t* __restrict__ dst, uint64_t n, uint64_t d, Rng rng, uint64_t c, double f,
                                                   double cr, const double* __restrict__ lower, const double* __restrict__ upper,
                                                   double* __restrict__ out) {
     const uint64_t i = blockIdx.x;
@@ -42,8 +43,10 @@ __global__ void __launch_bounds__(256) de_kernel(const double* __restrict__ x, u
     if (r3 >= e2) ++r3;
     const uint64_t j_rand = (uint64_t)(unit_draw<MODE>(rng, c + 3 * n + i) * (double)d);
     const uint64_t c_cr = c + 4 * n + i * d;
-    const double *xi = x + i * d, *x1 = x + r1 * d, *x2 = x + r2 * d, *x3 = x + r3 * d;
-    double* oi = out + i * d;
+    // row i of the operand lives in storage row src[i], the child goes to storage row dst[i] (nullptr: i)
+    const auto at = [&](uint64_t row) { return x + (src ? (uint64_t)src[row] : row) * d; };
+    const double *xi = at(i), *x1 = at(r1), *x2 = at(r2), *x3 = at(r3);
+    double* oi = out + (dst ? (uint64_t)dst[i] : i) * d;
     for (uint64_t j = threadIdx.x; j < d; j += blockDim.x) {
         double o;
         if (unit_draw<MODE>(rng, c_cr + j) < cr || j == j_rand) {
@@ -58,11 +61,13 @@ __global__ void __launch_bounds__(256) de_kernel(const double* __restrict__ x, u
 
 // ---- particle swarm ------------------------------------------------------------------------------------------
 // personal bests refresh where the score improved (operators.hpp:213-219)
-__global__ void __launch_bounds__(256) pso_pbest_kernel(const double* __restrict__ x, const double* __restrict__ scores, uint64_t d,
-                                                         double* __restrict__ pb_x, double* __restrict__ pb_score) {
+__global__ void __launch_bounds__(256) pso_pbest_kernel(const double* __restrict__ x, const uint32_t* __restrict__ src,
+                                                         const double* __restrict__ scores, uint64_t d, double* __restrict__ pb_x,
+                                                         double* __restrict__ pb_score) {
     const uint64_t i = blockIdx.x;
     if (!(scores[i] < pb_score[i])) return;  // CTA-uniform
-    for (uint64_t j = threadIdx.x; j < d; j += blockDim.x) pb_x[i * d + j] = x[i * d + j];
+    const double* xi = x + (src ? (uint64_t)src[i] : i) * d;
+    for (uint64_t j = threadIdx.x; j < d; j += blockDim.x) pb_x[i * d + j] = xi[j];
     __syncthreads();
     if (threadIdx.x == 0) pb_score[i] = scores[i];
 }
@@ -104,7 +109,8 @@ __global__ void __launch_bounds__(1024) argmin_first_kernel(const double* __rest
 
 // draws: r1 n x d at c, r2 n x d at c + n d (operators.hpp:223-224); velocity and position update (:230-236)
 template <int MODE>
-__global__ void __launch_bounds__(256) pso_update_kernel(const double* __restrict__ x, uint64_t n, uint64_t d, Rng rng, uint64_t c,
+__global__ void __launch_bounds__(256) pso_update_kernel(const double* __restrict__ x, const uint32_t* __restrict__ src,
+                                                          const uint32_t* __restrict__ dst, uint64_t n, uint64_t d, Rng rng, uint64_t c,
                                                           double inertia, double c1, double c2, const double* __restrict__ pb_x,
                                                           const uint32_t* __restrict__ best, double* __restrict__ vel,
                                                           const double* __restrict__ lower, const double* __restrict__ upper,
@@ -112,12 +118,14 @@ __global__ void __launch_bounds__(256) pso_update_kernel(const double* __restric
     const uint64_t i = blockIdx.x;
     const double* gbest = pb_x + (uint64_t)*best * d;
     const uint64_t c_r1 = c + i * d, c_r2 = c + n * d + i * d;
+    const double* xi = x + (src ? (uint64_t)src[i] : i) * d;
+    double* oi = out + (dst ? (uint64_t)dst[i] : i) * d;
     for (uint64_t j = threadIdx.x; j < d; j += blockDim.x) {
-        const double xv = x[i * d + j];
+        const double xv = xi[j];
         const double v = inertia * vel[i * d + j] + c1 * unit_draw<MODE>(rng, c_r1 + j) * (pb_x[i * d + j] - xv) +
                          c2 * unit_draw<MODE>(rng, c_r2 + j) * (gbest[j] - xv);
         vel[i * d + j] = v;
-        out[i * d + j] = clampd(xv + v, lower[j], upper[j]);
+        oi[j] = clampd(xv + v, lower[j], upper[j]);
     }
 }
 
@@ -127,7 +135,8 @@ __global__ void __launch_bounds__(256) pso_update_kernel(const double* __restric
 // stream row tiles into a two-stage shared-memory ring with cp.async (LDGSTS) while kMeanCols threads add the previous
 // tile in row order.
 constexpr int kMeanCols = 8, kMeanRows = 128;
-__global__ void __launch_bounds__(256) col_mean_kernel(const double* __restrict__ x, uint64_t n, uint64_t d, double* __restrict__ mean) {
+__global__ void __launch_bounds__(256) col_mean_kernel(const double* __restrict__ x, const uint32_t* __restrict__ src, uint64_t n, uint64_t d,
+                                                        double* __restrict__ mean) {
     __shared__ double buf[2][kMeanRows][kMeanCols];
     const uint64_t j0 = blockIdx.x * (uint64_t)kMeanCols;
     const uint32_t cols = (uint32_t)(d - j0 < (uint64_t)kMeanCols ? d - j0 : (uint64_t)kMeanCols);
@@ -138,7 +147,8 @@ __global__ void __launch_bounds__(256) col_mean_kernel(const double* __restrict_
             const uint64_t row = tile * kMeanRows + r;
             if (row < n && c < cols) {
                 const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&buf[b][r][c]);
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(x + row * d + j0 + c) : "memory");
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(x + (src ? (uint64_t)src[row] : row) * d + j0 + c)
+                             : "memory");
             }
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
@@ -166,7 +176,8 @@ __global__ void __launch_bounds__(256) col_mean_kernel(const double* __restrict_
 // The winner's row and velocity pass through bit-identically (operators.hpp:263-264: out = x, new_vel = velocities);
 // CTA `pairs` copies the unpaired row of an odd population.
 template <int MODE>
-__global__ void __launch_bounds__(256) cso_kernel(const double* __restrict__ x, const double* __restrict__ scores, uint64_t n,
+__global__ void __launch_bounds__(256) cso_kernel(const double* __restrict__ x, const uint32_t* __restrict__ src,
+                                                   const uint32_t* __restrict__ dst, const double* __restrict__ scores, uint64_t n,
                                                    uint64_t pairs, uint64_t d, Rng rng, uint64_t c, double phi,
                                                    const uint32_t* __restrict__ perm, const double* __restrict__ mean,
                                                    const double* __restrict__ vel, const double* __restrict__ lower,
@@ -175,8 +186,10 @@ __global__ void __launch_bounds__(256) cso_kernel(const double* __restrict__ x, 
     const uint64_t q = blockIdx.x;
     if (q >= pairs) {  // odd n: the last row of the shuffled order is nobody's partner
         const uint64_t r = perm[n - 1];
+        const double* xr = x + (src ? (uint64_t)src[r] : r) * d;
+        double* orow = out + (dst ? (uint64_t)dst[r] : r) * d;
         for (uint64_t j = threadIdx.x; j < d; j += blockDim.x) {
-            out[r * d + j] = x[r * d + j];
+            orow[j] = xr[j];
             vel_out[r * d + j] = vel[r * d + j];
         }
         return;
@@ -185,13 +198,15 @@ __global__ void __launch_bounds__(256) cso_kernel(const double* __restrict__ x, 
     uint64_t win = a, lose = b;
     if (scores[b] < scores[a] || (scores[b] == scores[a] && b < a)) win = b, lose = a;  // operators.hpp:267-271
     const uint64_t c1 = c + q * d, c2 = c + pairs * d + q * d, c3 = c + 2 * pairs * d + q * d;
+    const double *xlose = x + (src ? (uint64_t)src[lose] : lose) * d, *xwin = x + (src ? (uint64_t)src[win] : win) * d;
+    double *olose = out + (dst ? (uint64_t)dst[lose] : lose) * d, *owin = out + (dst ? (uint64_t)dst[win] : win) * d;
     for (uint64_t j = threadIdx.x; j < d; j += blockDim.x) {
-        const double xl = x[lose * d + j], xw = x[win * d + j];
+        const double xl = xlose[j], xw = xwin[j];
         const double v = unit_draw<MODE>(rng, c1 + j) * vel[lose * d + j] + unit_draw<MODE>(rng, c2 + j) * (xw - xl) +
                          phi * unit_draw<MODE>(rng, c3 + j) * (mean[j] - xl);
         vel_out[lose * d + j] = v;
-        out[lose * d + j] = clampd(xl + v, lower[j], upper[j]);
-        out[win * d + j] = xw;
+        olose[j] = clampd(xl + v, lower[j], upper[j]);
+        owin[j] = xw;
         vel_out[win * d + j] = vel[win * d + j];
     }
 }
@@ -199,40 +214,40 @@ __global__ void __launch_bounds__(256) cso_kernel(const double* __restrict__ x, 
 }  // namespace
 
 void launch_de(const double* x, uint64_t n, uint64_t d, Rng rng, uint64_t counter, double f, double cr, const double* lower,
-               const double* upper, double* out, cudaStream_t s) {
+               const double* upper, double* out, cudaStream_t s, const uint32_t* src, const uint32_t* dst) {
     require(n >= 4, "de_reproduce: needs at least four rows");  // operators.hpp:169
     require(n < 0xffffffffULL, "de_reproduce: too many rows");
     if (rng.mode == 0)
-        de_kernel<0><<<(unsigned)n, 256, 0, s>>>(x, n, d, rng, counter, f, cr, lower, upper, out);
+        de_kernel<0><<<(unsigned)n, 256, 0, s>>>(x, src, dst, n, d, rng, counter, f, cr, lower, upper, out);
     else
-        de_kernel<1><<<(unsigned)n, 256, 0, s>>>(x, n, d, rng, counter, f, cr, lower, upper, out);
+        de_kernel<1><<<(unsigned)n, 256, 0, s>>>(x, src, dst, n, d, rng, counter, f, cr, lower, upper, out);
     TEMO_CUDA(cudaGetLastError());
 }
 
 void launch_pso(const double* x, const double* scores, uint64_t n, uint64_t d, Rng rng, uint64_t counter, double inertia, double c1,
                 double c2, double* vel, double* pb_x, double* pb_score, uint32_t* best_scratch, const double* lower,
-                const double* upper, double* out, cudaStream_t s) {
+                const double* upper, double* out, cudaStream_t s, const uint32_t* src, const uint32_t* dst) {
     require(n >= 1 && n < 0xffffffffULL, "pso_reproduce: bad row count");
-    pso_pbest_kernel<<<(unsigned)n, 256, 0, s>>>(x, scores, d, pb_x, pb_score);
+    pso_pbest_kernel<<<(unsigned)n, 256, 0, s>>>(x, src, scores, d, pb_x, pb_score);
     argmin_first_kernel<<<1, 1024, 0, s>>>(pb_score, n, best_scratch);
     if (rng.mode == 0)
-        pso_update_kernel<0><<<(unsigned)n, 256, 0, s>>>(x, n, d, rng, counter, inertia, c1, c2, pb_x, best_scratch, vel, lower, upper, out);
+        pso_update_kernel<0><<<(unsigned)n, 256, 0, s>>>(x, src, dst, n, d, rng, counter, inertia, c1, c2, pb_x, best_scratch, vel, lower, upper, out);
     else
-        pso_update_kernel<1><<<(unsigned)n, 256, 0, s>>>(x, n, d, rng, counter, inertia, c1, c2, pb_x, best_scratch, vel, lower, upper, out);
+        pso_update_kernel<1><<<(unsigned)n, 256, 0, s>>>(x, src, dst, n, d, rng, counter, inertia, c1, c2, pb_x, best_scratch, vel, lower, upper, out);
     TEMO_CUDA(cudaGetLastError());
 }
 
 void launch_cso(const double* x, const double* scores, uint64_t n, uint64_t d, Rng rng, uint64_t counter, double phi,
                 const uint32_t* perm, double* mean_scratch, const double* vel, double* vel_out, const double* lower,
-                const double* upper, double* out, cudaStream_t s) {
+                const double* upper, double* out, cudaStream_t s, const uint32_t* src, const uint32_t* dst) {
     require(n >= 1 && n < 0xffffffffULL, "cso_reproduce: bad row count");
     const uint64_t pairs = n / 2;
-    col_mean_kernel<<<(unsigned)((d + kMeanCols - 1) / kMeanCols), 256, 0, s>>>(x, n, d, mean_scratch);
+    col_mean_kernel<<<(unsigned)((d + kMeanCols - 1) / kMeanCols), 256, 0, s>>>(x, src, n, d, mean_scratch);
     const unsigned grid = (unsigned)(pairs + (n & 1));
     if (rng.mode == 0)
-        cso_kernel<0><<<grid, 256, 0, s>>>(x, scores, n, pairs, d, rng, counter, phi, perm, mean_scratch, vel, lower, upper, vel_out, out);
+        cso_kernel<0><<<grid, 256, 0, s>>>(x, src, dst, scores, n, pairs, d, rng, counter, phi, perm, mean_scratch, vel, lower, upper, vel_out, out);
     else
-        cso_kernel<1><<<grid, 256, 0, s>>>(x, scores, n, pairs, d, rng, counter, phi, perm, mean_scratch, vel, lower, upper, vel_out, out);
+        cso_kernel<1><<<grid, 256, 0, s>>>(x, src, dst, scores, n, pairs, d, rng, counter, phi, perm, mean_scratch, vel, lower, upper, vel_out, out);
     TEMO_CUDA(cudaGetLastError());
 }
 

@@ -602,6 +602,70 @@ def test_lockstep_other_problems(tb, oracle, cfg):
     _lockstep(tb, oracle, problem, n, d, m, gens, seed)
 
 
+def _lockstep_op(tb, chk, op, problem, n, d, m, gens, seed, H=0):
+    """_lockstep for RunConfig::op = de / pso / cso / random (algorithms.hpp:253-268). The SwarmState is NOT injected: it
+    lives on the device for the whole run and must evolve exactly like the CPU's, which the bit-identical offspring of
+    every generation prove (velocities, personal bests and the global best all feed the next children)."""
+    cfg = tb.RunConfig(problem=problem, op=op, pop=n, dim=d, obj=m, generations=gens, seed=seed, lattice_h=H)
+    Hh = H or chk.lattice_density_for(m, n)
+    v0, gamma = chk.make_ref_set(m, Hh)
+    lo, hi = chk.problem_bounds(problem, d, m)
+    x, c = chk.random_reproduce(n, d, seed, 0, lo, hi)
+    st = dict(x=x, f=chk.evaluate(problem, x, m), v=v0, gamma=gamma, counter=c, swarm=None)
+    adapt_every = max(1, int(np.ceil(cfg.fr * gens)))
+    with tb.RveaRun(cfg) as run:
+        for t in range(gens):
+            nxt = chk.generation_op(op, problem, n, m, seed, st["counter"], lo, hi, t, gens, cfg.alpha, adapt_every,
+                                    v0, st["v"], st["gamma"], st["x"], st["f"], st["swarm"])
+            run.inject(x=st["x"], f=st["f"], v=st["v"], gamma=st["gamma"], counter=st["counter"], t=t)
+            pop = run.step_injected(nxt["f_off"])
+            got = run.last_generation()
+            assert np.array_equal(got["offspring"], nxt["offspring"]), f"{op}: offspring differ at generation {t}"
+            assert close_rel(got["f_off"], nxt["f_off"], 1e-12), f"{op}: objectives differ at generation {t}"
+            assert pop == nxt["x"].shape[0], (op, t)
+            assert np.array_equal(got["elite"], nxt["elite"]), f"{op}: survivor set differs at generation {t}"
+            assert run.state()["counter"] == nxt["counter"], (op, t)
+            now = run.download()
+            assert np.array_equal(now["x"], nxt["x"]) and np.array_equal(now["f"], nxt["f"]), (op, t)
+            st = nxt
+
+
+@pytest.mark.parametrize("op", ["de", "pso", "cso", "random"])
+@pytest.mark.parametrize("cfg", [("dtlz2", 40, 9, 3, 12, 3), ("dtlz1", 105, 12, 3, 30, 42), ("dtlz3", 65, 40, 4, 10, 5),
+                                 ("dtlz2", 300, 500, 3, 8, 7), ("lsmop1", 121, 300, 3, 8, 9)])
+def test_lockstep_other_operators(tb, checkers, op, cfg):
+    """The device-resident loop with the other reproduction operators, lock-step against the CPU (odd and even
+    populations, |P| == n in generation 0 and |P| != n afterwards, one- and two-segment bounds)."""
+    problem, n, d, m, gens, seed = cfg
+    chk = checkers[0] if problem == "lsmop1" else checkers[-1]  # the reference has no LSMOP1: the C restatement checks it
+    _lockstep_op(tb, chk, op, problem, n, d, m, gens, seed)
+
+
+@pytest.mark.parametrize("op", ["de", "pso", "cso", "random"])
+def test_free_running_other_operators(tb, oracle, op):
+    """Nothing injected: the run follows the recorded reference run (tests/golden/pipeline_ops.npz) exactly while the
+    survivor counts agree (device objectives differ from the CPU's by ulps, which can only flip near-ties)."""
+    from conftest import golden
+    g = golden("pipeline_ops")
+    problem, n, d, m, gens, seed = "dtlz2", 40, 9, 3, 12, 3
+    rec = tb.rvea_run(tb.make_problem(problem, d, m), tb.RunConfig(op=op, pop=n, generations=gens, seed=seed))
+    pops = np.array([r.pop_size for r in rec.rows])
+    exp = g[f"{op}_a_pop"]
+    same = pops == exp
+    agree = int(np.argmax(~same)) if not same.all() else len(pops)
+    print(f"free-running {op}: survivor counts identical for the first {agree}/{gens} generations")
+    assert agree >= 3
+    if agree == gens:
+        assert np.array_equal(rec.final_x, g[f"{op}_a_x"]) and close_rel(rec.final_f, g[f"{op}_a_f"], 1e-12)
+    lo, hi = oracle.problem_bounds(problem, d, m)
+    assert ((rec.final_x >= lo) & (rec.final_x <= hi)).all()
+
+
+def test_unknown_operator_is_rejected(tb):
+    with pytest.raises(ValueError, match="unknown operator"):
+        tb.RveaRun(tb.RunConfig(op="sa"))
+
+
 def test_free_running_c1_against_reference_run(tb, checkers):
     """Free-running (nothing injected) at config #1. Offspring are bit-identical as long as the
     survivor sets are; objectives carry the device evaluator's ulps (cos/sin, tree reduction),

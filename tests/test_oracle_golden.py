@@ -190,6 +190,20 @@ def test_pipeline_golden(oracle):
     assert np.array_equal(r["x"], g["d4_x"]) and np.array_equal(r["f"], g["d4_f"])
 
 
+OPS_CASES = {"a": ("dtlz2", 40, 9, 3, 0, 12, 3), "b": ("dtlz1", 33, 15, 2, 0, 20, 8), "c": ("dtlz3", 64, 20, 4, 0, 15, 5)}
+
+
+@pytest.mark.parametrize("op", ["de", "pso", "cso", "random"])
+def test_pipeline_other_operators_golden(oracle, op):
+    """rvea_run with RunConfig::op = de / pso / cso / random (algorithms.hpp:253-268): the C restatement against
+    fixtures recorded from the compiled reference (oracle/gen_golden.py)."""
+    g = golden("pipeline_ops")
+    for tag, (problem, n, d, m, H, gens, seed) in OPS_CASES.items():
+        r = oracle.rvea_run_op(op, problem, n, d, m, gens, seed=seed, lattice_h=H)
+        assert np.array_equal(r["x"], g[f"{op}_{tag}_x"]) and np.array_equal(r["f"], g[f"{op}_{tag}_f"]), (op, tag)
+        assert np.array_equal(r["pop_size"], g[f"{op}_{tag}_pop"]), (op, tag)
+
+
 def test_lsmop1_restatement_self_checks(oracle):
     """LSMOP1 is not in the reference (parity unpinned): check the restatement against an
     independent numpy transcription of the published definition and its basic properties."""

@@ -103,6 +103,27 @@ def test_pipeline_and_lockstep(oracle, ref, cfg):
     assert np.array_equal(so["x"], a["x"]) and np.array_equal(so["f"], a["f"])
 
 
+@pytest.mark.parametrize("op", ["de", "pso", "cso", "random"])
+def test_pipeline_other_operators(oracle, ref, op):
+    """The run loop with the other operators (algorithms.hpp:253-268): the C restatement's free run, and a run stepped
+    generation by generation on explicit state (the form the GPU lock-step tests use), against the reference's rvea_run."""
+    for problem, n, d, m, H, gens, seed in (("dtlz2", 40, 9, 3, 0, 12, 3), ("dtlz4", 57, 11, 3, 0, 10, 4)):
+        a = oracle.rvea_run_op(op, problem, n, d, m, gens, seed=seed, lattice_h=H)
+        b = ref.rvea_run_op(op, problem, n, d, m, gens, seed=seed, lattice_h=H)
+        assert np.array_equal(a["x"], b["x"]) and np.array_equal(a["f"], b["f"]) and np.array_equal(a["pop_size"], b["pop_size"])
+        for chk in (oracle, ref):
+            v0, gamma = chk.make_ref_set(m, H or chk.lattice_density_for(m, n))
+            lo, hi = chk.problem_bounds(problem, d, m)
+            x, c = chk.random_reproduce(n, d, seed, 0, lo, hi)
+            st = dict(x=x, f=chk.evaluate(problem, x, m), v=v0, gamma=gamma, counter=c, swarm=None)
+            adapt_every = max(1, int(np.ceil(0.1 * gens)))
+            for t in range(gens):
+                st = chk.generation_op(op, problem, n, m, seed, st["counter"], lo, hi, t, gens, 2.0, adapt_every, v0, st["v"],
+                                       st["gamma"], st["x"], st["f"], st["swarm"])
+                assert st["x"].shape[0] == b["pop_size"][t]
+            assert np.array_equal(st["x"], b["x"]) and np.array_equal(st["f"], b["f"]) and st["counter"] == a["counter"]
+
+
 def test_swarm_operators_suite_7002(oracle, ref):
     """DE / PSO / CSO: the C restatement against the compiled reference, batched and
     scalar-oracle forms, on the reference's own operator_suite instances (verify.hpp:117-182: master seed 7002,
