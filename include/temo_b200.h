@@ -214,6 +214,24 @@ int temo_b200_rvea_run(const temo_b200_run_config* cfg, double* final_x, double*
                        uint64_t* final_rows, uint64_t* rows_done, uint64_t* pop_size,
                        double* elapsed_ms);
 
+/* ---- metrics.hpp (quality indicators) ----------------------- */
+/* igd (metrics.hpp:21-44): mean distance from each row of f_ref (n_ref x m) to its nearest row of f (n x m). */
+int temo_b200_igd(const double* f, uint64_t n, uint64_t m, const double* f_ref, uint64_t n_ref, double* out);
+/* hv_mc_box (metrics.hpp:76-117): Monte-Carlo hypervolume of f inside the box [lo, ref] (m values each);
+ * sample s uses draws s*m .. s*m+m-1 of RngStream{seed}. std_error may be NULL. */
+int temo_b200_hv_mc_box(const double* f, uint64_t n, uint64_t m, const double* lo, const double* ref,
+                        uint64_t samples, uint64_t seed, double* value, double* std_error);
+/* hv_mc (metrics.hpp:121-124): the box is [col_min(f), ref]. */
+int temo_b200_hv_mc(const double* f, uint64_t n, uint64_t m, const double* ref, uint64_t samples,
+                    uint64_t seed, double* value, double* std_error);
+/* MetricContext (algorithms.hpp:46-54) of a run: pf_ref (n_ref x m; n_ref = 0: no IGD), hv_ref (m values or
+ * NULL: no HV), hv_scale, hv_samples, hv_seed, maximization. */
+int temo_b200_run_set_metrics(temo_b200_run* run, const double* pf_ref, uint64_t n_ref, const double* hv_ref,
+                              double hv_scale, uint64_t hv_samples, uint64_t hv_seed, int maximization);
+/* fill_metrics (algorithms.hpp:161-180) on the current survivors' objectives without copying them to the host
+ * (m = 2: hv_exact_2d on a host copy of rows x 2 values). NaN where the context has no reference. */
+int temo_b200_run_metrics(temo_b200_run* run, double* igd, double* hv);
+
 /* ---- device-pointer stage API (used by bench.py kernel timings and the multi-GPU host
  * orchestration in paper_2404_01159_b200/dist.py). Pointers are CUDA device pointers of
  * this process; all launches go to the library stream. ------------------------------ */

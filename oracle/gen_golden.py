@@ -202,6 +202,21 @@ def main():
             rr = ref.rvea_run_op(op, problem, n, d, m, gens, seed=seed, lattice_h=H)
             po.update({f"{op}_{tag}_x": rr["x"], f"{op}_{tag}_f": rr["f"], f"{op}_{tag}_pop": rr["pop_size"]})
     np.savez(os.path.join(OUT, "pipeline_ops.npz"), **po)
+    # ---- quality indicators (metrics.hpp:21-44, 76-124) ----
+    me = {}
+    for tag, (n, m, n_ref, samples, seed) in (("a", (40, 3, 91, 2048, 9001)), ("b", (300, 5, 126, 1000, 17)), ("c", (7, 2, 11, 500, 3)),
+                                               ("d", (1, 4, 35, 257, 5))):
+        g = Stream(ref, 8800 + n)
+        f = g.tensor(n, m) * 1.5
+        pf = ref.dtlz_pf_reference(2, m, {3: 12, 5: 5, 2: 10, 4: 4}[m])[:n_ref]
+        rp = np.full(m, 1.2)
+        lo = np.full(m, 0.05)
+        me.update({f"{tag}_f": f, f"{tag}_pf": pf, f"{tag}_ref": rp, f"{tag}_lo": lo, f"{tag}_samples": np.array([samples, seed]),
+                   f"{tag}_igd": np.array([ref.igd(f, pf)]), f"{tag}_hv_box": np.array(ref.hv_mc_box(f, lo, rp, samples, seed)),
+                   f"{tag}_hv": np.array(ref.hv_mc_box(f, None, rp, samples, seed))})
+    tr = ref.rvea_run_metrics("dtlz2", 60, 10, 3, 15, pf_ref=ref.dtlz_pf_reference(2, 3, 12), hv_ref=np.full(3, 1.1), seed=6)
+    me.update(run_pop=tr["pop_size"], run_igd=tr["igd"], run_hv=tr["hv"])
+    np.savez(os.path.join(OUT, "metrics.npz"), **me)
     total = sum(os.path.getsize(os.path.join(OUT, f)) for f in os.listdir(OUT))
     print(f"wrote {OUT}: {total/1024:.1f} KiB")
 

@@ -304,6 +304,26 @@ class Oracle(_Base):
             raise ValueError(f"rv_select contract violation rc={rc}")
         return Selection(elite[: ne.value].copy(), valid, assoc, theta, apd)
 
+    # ---- metrics.hpp
+    def igd(self, f, pf):
+        f, pf = _f(f), _f(pf)
+        out = C.c_double(0)
+        if self.lib.to_igd(_p(f), u64(f.shape[0]), u64(f.shape[1]), _p(pf), u64(pf.shape[0]), C.byref(out)):
+            raise ValueError("igd: empty set")
+        return out.value
+
+    def hv_mc_box(self, f, lo, ref, samples, seed):
+        """(value, std_error); lo=None -> hv_mc (box from col_min(f))."""
+        f, ref = _f(f), _f(ref)
+        out = np.zeros(2)
+        if lo is None:
+            rc = self.lib.to_hv_mc(_p(f), u64(f.shape[0]), u64(f.shape[1]), _p(ref), u64(samples), u64(seed), _p(out))
+        else:
+            rc = self.lib.to_hv_mc_box(_p(f), u64(f.shape[0]), u64(f.shape[1]), _p(_f(lo)), _p(ref), u64(samples), u64(seed), _p(out))
+        if rc:
+            raise ValueError("hv_mc: bad arguments")
+        return out[0], out[1]
+
     # algorithms
     def generation(self, problem, n, m, seed, counter, lower, upper, t, t_max, alpha, adapt_every,
                    v0, v, gamma, x, f, ga=GA_DEFAULT):
@@ -568,6 +588,28 @@ class Ref(_Base):
         out = C.c_double(0)
         self._chk(self.lib.ref_igd(_p(f), u64(f.shape[0]), u64(f.shape[1]), _p(pf), u64(pf.shape[0]), C.byref(out)))
         return out.value
+
+    def hv_mc_box(self, f, lo, ref, samples, seed):
+        """(value, std_error) of hv_mc_box; lo=None -> hv_mc (metrics.hpp:76-124)."""
+        f = _f(f)
+        out = np.zeros(2)
+        self._chk(self.lib.ref_hv_mc_box(_p(f), u64(f.shape[0]), u64(f.shape[1]), None if lo is None else _p(_f(lo)), _p(_f(ref)),
+                                         u64(samples), u64(seed), _p(out)))
+        return out[0], out[1]
+
+    def rvea_run_metrics(self, problem, n, d, m, generations, pf_ref=None, hv_ref=None, seed=42, lattice_h=0, alpha=2.0, fr=0.1,
+                         op="ga", hv_scale=1.0, hv_samples=2048, hv_seed=9001, maximization=False):
+        """The reference's rvea_run with a MetricContext: per-generation pop_size, igd, hv of the population."""
+        cfg_u = np.array([n, lattice_h, generations, seed, d, m], dtype=np.uint64)
+        cfg_d = np.array([alpha, fr, 0.0])
+        mcp = np.array([hv_scale, float(hv_samples), float(hv_seed), 1.0 if maximization else 0.0])
+        pops = np.zeros(generations, dtype=np.uint64)
+        g, h = np.full(generations, np.nan), np.full(generations, np.nan)
+        pf = None if pf_ref is None else _f(pf_ref)
+        self._chk(self.lib.ref_rvea_run_metrics(problem.encode(), op.encode(), _p(cfg_u, u64p), _p(cfg_d), None if pf is None else _p(pf),
+                                                u64(0 if pf is None else pf.shape[0]), None if hv_ref is None else _p(_f(hv_ref)),
+                                                _p(mcp), _p(pops, u64p), _p(g), _p(h)))
+        return dict(pop_size=pops, igd=g, hv=h)
 
     def generation(self, problem, n, m, seed, counter, lower, upper, t, t_max, alpha, adapt_every,
                    v0, v, gamma, x, f, ga=GA_DEFAULT):

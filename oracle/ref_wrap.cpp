@@ -387,4 +387,50 @@ int ref_rvea_run_op(const char* problem, const char* op, const double* opp, cons
     });
 }
 
+// hv_mc_box / hv_mc with the standard error (metrics.hpp:76-124); lo == nullptr selects hv_mc. out = {value, std_error}.
+int ref_hv_mc_box(const double* f, std::uint64_t n, std::uint64_t m, const double* lo, const double* ref_point,
+                  std::uint64_t samples, std::uint64_t seed, double* out) {
+    return guarded([&] {
+        const temo::HvEstimate e = lo ? temo::hv_mc_box(wrap(f, n, m), wrap(lo, 1, m), wrap(ref_point, 1, m), samples, seed)
+                                      : temo::hv_mc(wrap(f, n, m), wrap(ref_point, 1, m), samples, seed);
+        out[0] = e.value;
+        out[1] = e.std_error;
+    });
+}
+
+// rvea_run with a MetricContext (algorithms.hpp:46-54, 161-180, 288): per-generation IGD / HV of the population.
+// hv_ref may be nullptr; mcp = {hv_scale, hv_samples, hv_seed, maximization}.
+int ref_rvea_run_metrics(const char* problem, const char* op, const std::uint64_t* cfg_u, const double* cfg_d, const double* pf_ref,
+                         std::uint64_t n_ref, const double* hv_ref, const double* mcp, std::uint64_t* pop_size, double* igd_out,
+                         double* hv_out) {
+    return guarded([&] {
+        temo::RunConfig cfg;
+        cfg.problem = problem;
+        cfg.op = op;
+        cfg.pop = cfg_u[0];
+        cfg.lattice_h = cfg_u[1];
+        cfg.generations = cfg_u[2];
+        cfg.seed = cfg_u[3];
+        cfg.dim = cfg_u[4];
+        cfg.obj = cfg_u[5];
+        cfg.alpha = cfg_d[0];
+        cfg.fr = cfg_d[1];
+        cfg.track_archive = false;
+        const temo::ProblemInstance prob = temo::make_problem(cfg.problem, cfg.dim, cfg.obj);
+        temo::MetricContext mc;
+        if (pf_ref && n_ref) mc.pf_ref = wrap(pf_ref, n_ref, cfg.obj);
+        if (hv_ref) mc.hv_ref = wrap(hv_ref, 1, cfg.obj);
+        mc.hv_scale = mcp[0];
+        mc.hv_samples = static_cast<std::size_t>(mcp[1]);
+        mc.hv_seed = static_cast<std::uint64_t>(mcp[2]);
+        mc.maximization = mcp[3] != 0.0;
+        const temo::RunRecord rec = temo::rvea_run(prob, cfg, mc);
+        for (std::size_t i = 0; i < rec.rows.size(); ++i) {
+            pop_size[i] = rec.rows[i].pop_size;
+            igd_out[i] = rec.rows[i].igd_value;
+            hv_out[i] = rec.rows[i].hv_value;
+        }
+    });
+}
+
 } // extern "C"

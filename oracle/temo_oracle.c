@@ -818,3 +818,63 @@ int to_rvea_run_op(int problem, int op, const double* opp, uint64_t n, uint64_t 
     free(pool_f); free(scores); free(vel); free(pb_x); free(pb_s); free(pool_idx); free(elite); free(valid);
     return rc;
 }
+
+/* ------------------------------------------------------------------ metrics.hpp */
+
+/* metrics.hpp:21-44 */
+int to_igd(const double* f, uint64_t n, uint64_t m, const double* f_ref, uint64_t n_ref, double* out) {
+    if (n < 1 || n_ref < 1) return 1;
+    double sum = 0.0;
+    for (uint64_t i = 0; i < n_ref; ++i) {
+        double best = INFINITY;
+        for (uint64_t j = 0; j < n; ++j) {
+            double s = 0.0;
+            for (uint64_t k = 0; k < m; ++k) {
+                const double diff = f[j * m + k] - f_ref[i * m + k];
+                s += diff * diff;
+            }
+            if (s < best) best = s;
+        }
+        sum += sqrt(best);
+    }
+    *out = sum / (double)n_ref;
+    return 0;
+}
+
+/* metrics.hpp:76-117: sample s uses draws s*m .. s*m+m-1 of RngStream{seed}. out = {value, std_error}. */
+int to_hv_mc_box(const double* f, uint64_t n, uint64_t m, const double* lo, const double* ref, uint64_t samples,
+                 uint64_t seed, double* out) {
+    if (samples < 1 || n < 1 || m > 64) return 1;
+    double volume = 1.0;
+    for (uint64_t k = 0; k < m; ++k) {
+        const double side = ref[k] - lo[k];
+        if (side <= 0.0) { out[0] = out[1] = 0.0; return 0; }
+        volume *= side;
+    }
+    uint64_t hits = 0;
+    double pt[64];
+    for (uint64_t s = 0; s < samples; ++s) {
+        for (uint64_t k = 0; k < m; ++k) pt[k] = lo[k] + to_value_at(seed, s * m + k) * (ref[k] - lo[k]);
+        for (uint64_t i = 0; i < n; ++i) {
+            int all_le = 1;
+            for (uint64_t k = 0; k < m; ++k)
+                if (f[i * m + k] > pt[k]) { all_le = 0; break; }
+            if (all_le) { ++hits; break; }
+        }
+    }
+    const double p = (double)hits / (double)samples;
+    out[0] = volume * p;
+    out[1] = volume * sqrt(p * (1.0 - p) / (double)samples);
+    return 0;
+}
+
+/* metrics.hpp:121-124: the box is [col_min(f), ref]. */
+int to_hv_mc(const double* f, uint64_t n, uint64_t m, const double* ref, uint64_t samples, uint64_t seed, double* out) {
+    if (n < 1 || m > 64) return 1;
+    double lo[64];
+    for (uint64_t k = 0; k < m; ++k) lo[k] = f[k];
+    for (uint64_t i = 1; i < n; ++i)
+        for (uint64_t k = 0; k < m; ++k)
+            if (f[i * m + k] < lo[k]) lo[k] = f[i * m + k];
+    return to_hv_mc_box(f, n, m, lo, ref, samples, seed, out);
+}

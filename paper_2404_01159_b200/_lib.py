@@ -78,6 +78,11 @@ SIGNATURES = {
     "temo_b200_rv_select": (C.c_int, [f64p, u64, u64, f64p, f64p, u64, u64, u64, C.c_double, u64p, u64p, u8p,
                                       u64p, f64p, f64p]),
     "temo_b200_apd_penalty": (C.c_double, [u64, u64, u64, C.c_double]),
+    "temo_b200_igd": (C.c_int, [f64p, u64, u64, f64p, u64, f64p]),
+    "temo_b200_hv_mc_box": (C.c_int, [f64p, u64, u64, f64p, f64p, u64, u64, f64p, f64p]),
+    "temo_b200_hv_mc": (C.c_int, [f64p, u64, u64, f64p, u64, u64, f64p, f64p]),
+    "temo_b200_run_set_metrics": (C.c_int, [_RUN, f64p, u64, f64p, C.c_double, u64, u64, C.c_int]),
+    "temo_b200_run_metrics": (C.c_int, [_RUN, f64p, f64p]),
     "temo_b200_run_create": (C.c_int, [_CFG, C.POINTER(_RUN)]),
     "temo_b200_run_step": (C.c_int, [_RUN, u64p, f64p]),
     "temo_b200_run_step_injected": (C.c_int, [_RUN, f64p, u64p]),

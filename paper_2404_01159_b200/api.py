@@ -460,6 +460,66 @@ class GenerationRow:
     t: int
     elapsed_ms: float
     pop_size: int
+    igd_value: float = float("nan")
+    hv_value: float = float("nan")
+
+
+# ---- metrics.hpp --------------------------------------------------------------------------
+@dataclass
+class HvEstimate:
+    """reference: HvEstimate (metrics.hpp:68-71)."""
+    value: float = 0.0
+    std_error: float = 0.0
+
+
+@dataclass
+class MetricContext:
+    """reference: MetricContext (algorithms.hpp:46-54); the expected-utility weights are not on this path."""
+    pf_ref: np.ndarray | None = None   # IGD reference front (None -> no IGD)
+    hv_ref: np.ndarray | None = None   # reference point, m values (None -> no HV)
+    hv_scale: float = 1.0
+    hv_samples: int = 2048
+    hv_seed: int = 9001
+    maximization: bool = False
+
+
+def igd(f, f_ref) -> float:
+    """reference: igd (metrics.hpp:21-44)."""
+    f, f_ref = _t(f), _t(f_ref)
+    if f.shape[0] < 1 or f_ref.shape[0] < 1:
+        raise ValueError("igd: empty set")
+    if f.shape[1] != f_ref.shape[1]:
+        raise ValueError("igd: objective count mismatch")
+    out = C.c_double(0)
+    _call(_lib.load().temo_b200_igd, _p(f), u64(f.shape[0]), u64(f.shape[1]), _p(f_ref), u64(f_ref.shape[0]), C.byref(out))
+    return out.value
+
+
+def hv_mc_box(f, lo, ref, samples: int, seed: int) -> HvEstimate:
+    """reference: hv_mc_box (metrics.hpp:76-117)."""
+    f, lo, ref = _t(f), _t(lo).reshape(-1), _t(ref).reshape(-1)
+    if samples < 1:
+        raise ValueError("hv_mc: needs at least one sample")
+    if f.shape[0] < 1 or ref.shape[0] != f.shape[1]:
+        raise ValueError("hv_mc: bad shapes")
+    if lo.shape[0] != f.shape[1]:
+        raise ValueError("hv_mc: bad box")
+    v, e = C.c_double(0), C.c_double(0)
+    _call(_lib.load().temo_b200_hv_mc_box, _p(f), u64(f.shape[0]), u64(f.shape[1]), _p(lo), _p(ref), u64(samples), u64(seed),
+          C.byref(v), C.byref(e))
+    return HvEstimate(v.value, e.value)
+
+
+def hv_mc(f, ref, samples: int, seed: int) -> HvEstimate:
+    """reference: hv_mc (metrics.hpp:121-124): the box is [col_min(f), ref]."""
+    f, ref = _t(f), _t(ref).reshape(-1)
+    if samples < 1:
+        raise ValueError("hv_mc: needs at least one sample")
+    if f.shape[0] < 1 or ref.shape[0] != f.shape[1]:
+        raise ValueError("hv_mc: bad shapes")
+    v, e = C.c_double(0), C.c_double(0)
+    _call(_lib.load().temo_b200_hv_mc, _p(f), u64(f.shape[0]), u64(f.shape[1]), _p(ref), u64(samples), u64(seed), C.byref(v), C.byref(e))
+    return HvEstimate(v.value, e.value)
 
 
 @dataclass
@@ -551,16 +611,48 @@ class RveaRun:
         return dict(generation=ms[0], reproduce=ms[1], evaluate=ms[2], select=ms[3], adapt=ms[4], host_perm=ms[5],
                     launches=int(ms[6]), prep=ms[7])
 
+    def set_metrics(self, mc: MetricContext) -> None:
+        """MetricContext of this run (algorithms.hpp:46-54): the references move to the device once."""
+        pf = None if mc.pf_ref is None else _t(mc.pf_ref)
+        hv = None if mc.hv_ref is None else _t(mc.hv_ref).reshape(-1)
+        if pf is not None and pf.shape[1] != self.m:
+            raise ValueError("igd: objective count mismatch")
+        if hv is not None and hv.shape[0] != self.m:
+            raise ValueError("hv_mc: bad shapes")
+        _call(self._L.temo_b200_run_set_metrics, self._h, _p(pf), u64(0 if pf is None else pf.shape[0]), _p(hv),
+              C.c_double(mc.hv_scale), u64(mc.hv_samples), u64(mc.hv_seed), int(mc.maximization))
+
+    def metrics(self) -> tuple:
+        """fill_metrics (algorithms.hpp:161-180) on the survivors' objectives, evaluated on the device: (igd, hv)."""
+        a, b = C.c_double(0), C.c_double(0)
+        _call(self._L.temo_b200_run_metrics, self._h, C.byref(a), C.byref(b))
+        return a.value, b.value
+
     def time_stage(self, stage: int, reps: int = 5) -> float:
         out = C.c_double(0)
         _call(self._L.temo_b200_run_time_stage, self._h, stage, reps, C.byref(out))
         return out.value
 
 
-def rvea_run(prob: ProblemInstance, cfg: RunConfig) -> RunRecord:
+def rvea_run(prob: ProblemInstance, cfg: RunConfig, mc: MetricContext | None = None) -> RunRecord:
     """reference: rvea_run (algorithms.hpp:227-296). `prob` supplies name/dim/num_obj like the
-    reference's ProblemInstance; the evaluator itself runs on the device."""
+    reference's ProblemInstance; the evaluator itself runs on the device. With a MetricContext every
+    GenerationRow carries igd_value / hv_value of the population (fill_metrics, track_archive = false)."""
     cfg = RunConfig(**{**cfg.__dict__, "problem": prob.name, "dim": prob.dim, "obj": prob.num_obj})
+    if mc is not None and (mc.pf_ref is not None or mc.hv_ref is not None):
+        t0 = time.perf_counter()
+        rows = []
+        with RveaRun(cfg) as run:
+            run.set_metrics(mc)
+            for t in range(cfg.generations):
+                pop = run.step()
+                g, h = run.metrics()
+                ms = (time.perf_counter() - t0) * 1e3
+                rows.append(GenerationRow(t, ms, pop, g, h))
+                if cfg.time_budget_s > 0.0 and ms >= cfg.time_budget_s * 1e3:
+                    break
+            out = run.download()
+        return RunRecord(rows, out["x"], out["f"])
     ccfg = cfg.c()
     L = _lib.load()
     H = cfg.lattice_h or lattice_density_for(prob.num_obj, cfg.pop)

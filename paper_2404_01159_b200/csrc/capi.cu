@@ -645,6 +645,63 @@ int temo_b200_rvea_run(const temo_b200_run_config* cfg, double* final_x, double*
     });
 }
 
+// ---- metrics.hpp ------------------------------------------------------------------------------------------
+int temo_b200_igd(const double* f, uint64_t n, uint64_t m, const double* f_ref, uint64_t n_ref, double* out) {
+    return guarded([&] {
+        require(f && f_ref && out, "igd: null argument");
+        require(n >= 1 && n_ref >= 1, "igd: empty set");  // metrics.hpp:22
+        cudaStream_t s = ctx().stream;
+        DevBuf<double> df(f, n * m, s), dr(f_ref, n_ref * m, s), dn(n_ref);
+        *out = device_igd(df.p, nullptr, n, m, dr.p, n_ref, dn.p, s);
+    });
+}
+
+int temo_b200_hv_mc_box(const double* f, uint64_t n, uint64_t m, const double* lo, const double* ref, uint64_t samples,
+                        uint64_t seed, double* value, double* std_error) {
+    return guarded([&] {
+        require(f && lo && ref && value, "hv_mc: null argument");
+        require(samples >= 1, "hv_mc: needs at least one sample");  // metrics.hpp:78
+        require(n >= 1, "hv_mc: bad shapes");
+        cudaStream_t s = ctx().stream;
+        DevBuf<double> df(f, n * m, s), dl(lo, m, s), dr(ref, m, s);
+        DevBuf<unsigned long long> hits(1);
+        device_hv_mc_box(df.p, nullptr, n, m, dl.p, lo, false, dr.p, ref, 1.0, samples, seed, hits.p, value, std_error, s);
+    });
+}
+
+int temo_b200_hv_mc(const double* f, uint64_t n, uint64_t m, const double* ref, uint64_t samples, uint64_t seed,
+                    double* value, double* std_error) {
+    return guarded([&] {
+        require(f && ref && value, "hv_mc: null argument");
+        require(samples >= 1, "hv_mc: needs at least one sample");
+        require(n >= 1, "col_min: empty tensor");  // tensor.hpp:212
+        require(m >= 1 && m <= (uint64_t)kMaxObj, "hv_mc: unsupported objective count");
+        cudaStream_t s = ctx().stream;
+        DevBuf<double> df(f, n * m, s), dl(m), dr(ref, m, s);
+        DevBuf<unsigned long long> hits(1), scratch(2 * m);
+        launch_col_minmax(df.p, n, nullptr, m, dl.p, nullptr, scratch.p, s);
+        double lo[kMaxObj];
+        dl.to_host(lo, s);
+        TEMO_CUDA(cudaStreamSynchronize(s));
+        device_hv_mc_box(df.p, nullptr, n, m, dl.p, lo, false, dr.p, ref, 1.0, samples, seed, hits.p, value, std_error, s);
+    });
+}
+
+int temo_b200_run_set_metrics(temo_b200_run* run, const double* pf_ref, uint64_t n_ref, const double* hv_ref, double hv_scale,
+                              uint64_t hv_samples, uint64_t hv_seed, int maximization) {
+    return guarded([&] {
+        require(run && run->impl, "run_set_metrics: null run");
+        run->impl->set_metrics(pf_ref, n_ref, hv_ref, hv_scale, hv_samples, hv_seed, maximization != 0);
+    });
+}
+
+int temo_b200_run_metrics(temo_b200_run* run, double* igd, double* hv) {
+    return guarded([&] {
+        require(run && run->impl, "run_metrics: null run");
+        run->impl->metrics(igd, hv);
+    });
+}
+
 // ---- device-pointer helpers -------------------------------------------------------------------------------
 void* temo_b200_dev_alloc(size_t bytes) {
     void* p = nullptr;

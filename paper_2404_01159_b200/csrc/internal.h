@@ -174,6 +174,18 @@ void launch_adapt_vectors(const double* v0, double* v, double* vn, uint64_t r, u
                           const double* zmin, const double* zmax, uint32_t* skip_flag,
                           uint32_t* err_flag, cudaStream_t s);
 
+// ---- quality indicators (metrics.cu) -----------------------------------------
+// igd (metrics.hpp:21-44) of the n (or *n_dev) rows of f against f_ref; nearest_scratch holds n_ref doubles.
+double device_igd(const double* f, const uint32_t* n_dev, uint64_t n, uint64_t m, const double* f_ref, uint64_t n_ref,
+                  double* nearest_scratch, cudaStream_t s);
+// hv_mc_box (metrics.hpp:76-117) of f / scale inside [lo, ref] (lo_scaled: the box corner is lo / scale, as when it is
+// col_min of the unscaled objectives). lo / ref are given on both sides (device for the kernel, host for the volume).
+void device_hv_mc_box(const double* f, const uint32_t* n_dev, uint64_t n, uint64_t m, const double* lo_dev, const double* lo_host,
+                      bool lo_scaled, const double* ref_dev, const double* ref_host, double scale, uint64_t samples, uint64_t seed,
+                      unsigned long long* hits_scratch, double* value, double* std_error, cudaStream_t s);
+// hv_exact_2d (metrics.hpp:48-66) on a host copy of an n x 2 objective matrix divided by scale.
+double host_hv_exact_2d(const double* f, uint64_t n, const double* ref, double scale);
+
 // ---- host-side pieces (host_ops.cu) ---------------------------------------------------------------
 uint64_t lattice_count(uint64_t m, uint64_t H);
 uint64_t lattice_density_for(uint64_t m, uint64_t target);

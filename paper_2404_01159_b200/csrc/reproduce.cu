@@ -346,12 +346,18 @@ struct PairCtx {
     uint32_t cross;  // pair-level crossover switch hc = H(r3 - pc) == 0 (operators.hpp:82)
     uint32_t pad;
 };
+#ifndef TEMO_PAIR_TOUCH
+#define TEMO_PAIR_TOUCH 0                                    // 1: sector touch loads at the tile start, 0: prefetch.global.L2 hints
+#endif
 struct WarpSmem {
     double beta[kTileGenes];
     unsigned short list[kTileGenes];
     double2 side[kPairCand];  // final children {a, b} of a candidate gene
     PairCtx ctx;
     unsigned short cand[kPairCand];
+#if TEMO_PAIR_TOUCH
+    double2 sink[32];         // landing zone of the touch loads (never read)
+#endif
 };
 struct PairSlot {
     double part[2][kVirtWarps];  // per-warp totals of the two children
@@ -613,6 +619,21 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
             if (kmax == 0) break;
             const uint32_t q_first = (blk0 + v) * 32 + lane;  // this lane's vector in the tile's first block
             const uint64_t pos = W.ctx.pos;
+#if TEMO_PAIR_TOUCH
+            {   // this warp's parent blocks of this tile into L2, where pass C finds them: one 16-byte asynchronous copy
+                // (LDGSTS, no register, no scoreboard) per 32-byte sector, lanes 0-15 on parent a, 16-31 on parent b. Unlike
+                // prefetch hints these are real loads and cannot be dropped under load; DRAM then has passes A and B to
+                // deliver. The copies land in a sink nobody reads.
+                const char* row = reinterpret_cast<const char*>(lane < 16 ? W.ctx.pa : W.ctx.pb);
+                const uint32_t row_bytes = (uint32_t)a.d * 8u, sink = sm_w + (uint32_t)offsetof(WarpSmem, sink) + lane * 16;
+                uint32_t off = (blk0 + v) * 512 + (lane & 15) * 32;
+                for (uint32_t k = 0; k < kmax; ++k, off += kVirtWarps * 512) {
+                    if (off + 16 <= row_bytes)
+                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sink), "l"(row + off) : "memory");
+                }
+                asm volatile("cp.async.commit_group;" ::: "memory");
+            }
+#else
             {   // this warp's parent blocks of this tile into L2 (they are read in pass C)
                 const uint32_t kk = lane & 15, blk = blk0 + v + kk * kVirtWarps;
                 if (kk < kmax && blk < nblk) {
@@ -621,6 +642,7 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
                     for (int o = 0; o < 512; o += 128) prefetch_l2(p + o);
                 }
             }
+#endif
             // ---- pass A: crossing genes and mutation candidates (hashes only)
             uint32_t total = 0, ncand = 0;
             {

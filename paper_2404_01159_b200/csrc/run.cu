@@ -210,6 +210,7 @@ Run::~Run() {
     cudaFree(src); cudaFree(perm_dev); cudaFree(used); cudaFree(d_P); cudaFree(free_scratch);
     cudaFree(v0); cudaFree(v); cudaFree(gamma); cudaFree(lower); cudaFree(upper);
     cudaFree(zmin); cudaFree(zmax); cudaFree(zscratch); cudaFree(skip_flag); cudaFree(f_off_saved);
+    cudaFree(mc_pf); cudaFree(mc_nearest); cudaFree(mc_hv_ref); cudaFree(mc_hits);
     cudaFree(pool_idx_dev); cudaFree(pool_f); cudaFree(scores); cudaFree(sw_vel[0]); cudaFree(sw_vel[1]);
     cudaFree(sw_pbx); cudaFree(sw_pbs); cudaFree(sw_mean); cudaFree(sw_best);
     cudaFreeHost(h_status);
@@ -518,6 +519,58 @@ void Run::last_generation(double* offspring, double* f_off, uint64_t* elite_out)
         TEMO_CUDA(cudaMemcpy(tmp.data(), ws.elite, P * sizeof(uint32_t), cudaMemcpyDeviceToHost));
         for (uint64_t k = 0; k < P; ++k) elite_out[k] = tmp[k];
     }
+}
+
+void Run::set_metrics(const double* pf_ref, uint64_t n_ref, const double* hv_ref, double hv_scale, uint64_t hv_samples,
+                      uint64_t hv_seed, bool maximization) {
+    TEMO_CUDA(cudaStreamSynchronize(stream));
+    cudaFree(mc_pf); cudaFree(mc_nearest); cudaFree(mc_hv_ref); cudaFree(mc_hits);
+    mc_pf = mc_nearest = mc_hv_ref = nullptr;
+    mc_hits = nullptr;
+    mc_n_ref = 0;
+    mc_hv_ref_host.clear();
+    if (pf_ref && n_ref) {
+        mc_pf = dev_alloc<double>(n_ref * m);
+        mc_nearest = dev_alloc<double>(n_ref);
+        TEMO_CUDA(cudaMemcpy(mc_pf, pf_ref, n_ref * m * sizeof(double), cudaMemcpyHostToDevice));
+        mc_n_ref = n_ref;
+    }
+    if (hv_ref) {
+        require(hv_samples >= 1, "hv_mc: needs at least one sample");
+        require(maximization || hv_scale > 0.0, "fill_metrics: hv_scale must be positive");
+        mc_hv_ref_host.assign(hv_ref, hv_ref + m);
+        if (maximization)  // algorithms.hpp:168-170: minimise f against -ref, unscaled
+            for (double& x : mc_hv_ref_host) x = -x;
+        mc_scale = maximization ? 1.0 : hv_scale;
+        mc_samples = hv_samples;
+        mc_seed = hv_seed;
+        mc_hv_ref = dev_alloc<double>(m);
+        mc_hits = dev_alloc<unsigned long long>(1);
+        TEMO_CUDA(cudaMemcpy(mc_hv_ref, mc_hv_ref_host.data(), m * sizeof(double), cudaMemcpyHostToDevice));
+    }
+}
+
+// fill_metrics (algorithms.hpp:161-180) with track_archive = false: the population's objectives.
+void Run::metrics(double* igd_out, double* hv_out) {
+    const double nan = std::nan("");
+    if (igd_out) *igd_out = mc_n_ref ? device_igd(fm[cur], nullptr, P, m, mc_pf, mc_n_ref, mc_nearest, stream) : nan;
+    if (!hv_out) return;
+    *hv_out = nan;
+    if (mc_hv_ref_host.empty()) return;
+    if (m == 2) {  // hv_exact_2d: a sort-based sweep, on a host copy of P x 2 values
+        std::vector<double> f(P * 2);
+        TEMO_CUDA(cudaMemcpyAsync(f.data(), fm[cur], P * 2 * sizeof(double), cudaMemcpyDeviceToHost, stream));
+        TEMO_CUDA(cudaStreamSynchronize(stream));
+        *hv_out = host_hv_exact_2d(f.data(), P, mc_hv_ref_host.data(), mc_scale);
+        return;
+    }
+    // hv_mc: the box's lower corner is col_min of the (scaled) objectives (metrics.hpp:121-124)
+    launch_col_minmax(fm[cur], P, nullptr, m, zmin, zmax, zscratch, stream);
+    double lo[kMaxObj];
+    TEMO_CUDA(cudaMemcpyAsync(lo, zmin, m * sizeof(double), cudaMemcpyDeviceToHost, stream));
+    TEMO_CUDA(cudaStreamSynchronize(stream));
+    device_hv_mc_box(fm[cur], nullptr, P, m, zmin, lo, /*lo_scaled=*/true, mc_hv_ref, mc_hv_ref_host.data(), mc_scale, mc_samples,
+                     mc_seed, mc_hits, hv_out, nullptr, stream);
 }
 
 double Run::time_stage(int stage, int reps) {

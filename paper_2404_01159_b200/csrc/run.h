@@ -1,5 +1,6 @@
 // Device-resident RVEA run state (see run.cu). reference: rvea_run, algorithms.hpp:227-296.
 #pragma once
+#include <vector>
 
 #include "internal.h"
 #include "vecindex.h"
@@ -41,6 +42,11 @@ struct Run {
     void download(double* x, double* f, double* v_out, double* gamma_out);
     void last_generation(double* offspring, double* f_off, uint64_t* elite_out);
     double time_stage(int stage, int reps);
+    // MetricContext (algorithms.hpp:46-54) and fill_metrics (:161-180) on the current survivors' objectives, which stay
+    // in HBM: IGD against pf_ref (n_ref x m, n_ref = 0: none), hypervolume against hv_ref (m values, nullptr: none).
+    void set_metrics(const double* pf_ref, uint64_t n_ref, const double* hv_ref, double hv_scale, uint64_t hv_samples,
+                     uint64_t hv_seed, bool maximization);
+    void metrics(double* igd_out, double* hv_out);
 
     RunConfig cfg;
     uint64_t n = 0, d = 0, m = 0, r = 0, H = 0, adapt_every = 1;
@@ -75,6 +81,14 @@ struct Run {
     double *zmin = nullptr, *zmax = nullptr;
     unsigned long long* zscratch = nullptr;
     uint32_t* skip_flag = nullptr;
+    double* mc_pf = nullptr;       // IGD reference front on the device
+    uint64_t mc_n_ref = 0;
+    double* mc_nearest = nullptr;  // [n_ref]
+    double* mc_hv_ref = nullptr;   // [m] (sign already applied)
+    std::vector<double> mc_hv_ref_host;
+    double mc_scale = 1.0;
+    uint64_t mc_samples = 2048, mc_seed = 9001;
+    unsigned long long* mc_hits = nullptr;
     double* f_off_saved = nullptr;  // device objectives of the last offspring when selection ran on injected ones
     bool f_off_was_injected = false;
     SelectWorkspace ws;

@@ -666,6 +666,87 @@ def test_unknown_operator_is_rejected(tb):
         tb.RveaRun(tb.RunConfig(op="sa"))
 
 
+# -------------------------------------------------------------------------- quality indicators (metrics.hpp)
+def test_metrics_golden_and_checkers(tb, checkers):
+    """igd / hv_mc_box / hv_mc on the device against the recorded reference values and every CPU checker: bit-exact
+    (minimum of exactly reproduced squared distances, host-ordered sum of square roots; integer hit counts)."""
+    g = golden("metrics")
+    for tag in "abcd":
+        f, pf, rp, lo = g[f"{tag}_f"], g[f"{tag}_pf"], g[f"{tag}_ref"], g[f"{tag}_lo"]
+        samples, seed = (int(v) for v in g[f"{tag}_samples"])
+        assert tb.igd(f, pf) == g[f"{tag}_igd"][0], tag
+        e = tb.hv_mc_box(f, lo, rp, samples, seed)
+        assert (e.value, e.std_error) == tuple(g[f"{tag}_hv_box"]), tag
+        e = tb.hv_mc(f, rp, samples, seed)
+        assert (e.value, e.std_error) == tuple(g[f"{tag}_hv"]), tag
+    chk = checkers[-1]
+    rng = np.random.default_rng(5)
+    for n, m, n_ref, samples in ((5000, 3, 300, 4096), (1, 2, 1, 1), (33, 10, 77, 999), (20000, 4, 1000, 2048)):
+        f, pf = rng.random((n, m)) * 2.0, rng.random((n_ref, m))
+        rp = np.full(m, 1.7)
+        assert tb.igd(f, pf) == chk.igd(f, pf), (n, m)
+        e = tb.hv_mc(f, rp, samples, 9001)
+        assert (e.value, e.std_error) == chk.hv_mc_box(f, None, rp, samples, 9001), (n, m)
+    e = tb.hv_mc_box(g["a_f"], g["a_ref"], g["a_lo"], 100, 1)  # ref below lo: empty box
+    assert (e.value, e.std_error) == (0.0, 0.0)
+    with pytest.raises(ValueError, match="empty set"):
+        tb.igd(np.zeros((0, 3)), g["a_pf"])
+    with pytest.raises(ValueError, match="at least one sample"):
+        tb.hv_mc(g["a_f"], g["a_ref"], 0, 1)
+
+
+@pytest.mark.parametrize("m", [3, 2])
+def test_run_metrics_lockstep(tb, checkers, m):
+    """fill_metrics (algorithms.hpp:161-180) evaluated on the device-resident survivors: every generation of a lock-step
+    run reports exactly the CPU's IGD and hypervolume of the same population (m = 2 takes hv_exact_2d)."""
+    chk = checkers[-1]
+    problem, n, d, gens, seed = "dtlz2", 60, 10, 12, 6
+    cfg = tb.RunConfig(problem=problem, pop=n, dim=d, obj=m, generations=gens, seed=seed)
+    pf = chk.dtlz_pf_reference(2, m, 12 if m == 3 else 30)
+    rp = np.full(m, 1.1)
+    v0, gamma = chk.make_ref_set(m, chk.lattice_density_for(m, n))
+    lo, hi = chk.problem_bounds(problem, d, m)
+    x, c = chk.random_reproduce(n, d, seed, 0, lo, hi)
+    st = dict(x=x, f=chk.evaluate(problem, x, m), v=v0, gamma=gamma, counter=c)
+    with tb.RveaRun(cfg) as run:
+        run.set_metrics(tb.MetricContext(pf_ref=pf, hv_ref=rp, hv_scale=1.25, hv_samples=1024, hv_seed=11))
+        for t in range(gens):
+            nxt = chk.generation(problem, n, m, seed, st["counter"], lo, hi, t, gens, cfg.alpha, 2, v0, st["v"], st["gamma"],
+                                 st["x"], st["f"])
+            run.inject(x=st["x"], f=st["f"], v=st["v"], gamma=st["gamma"], counter=st["counter"], t=t)
+            run.step_injected(nxt["f_off"])
+            got_igd, got_hv = run.metrics()
+            assert got_igd == chk.igd(nxt["f"], pf), t
+            fs = nxt["f"] / 1.25
+            if m == 2:
+                pts = sorted((a, b) for a, b in fs if a <= rp[0] and b <= rp[1])  # metrics.hpp:48-66
+                area, prev = 0.0, rp[1]
+                for a, b in pts:
+                    if b < prev:
+                        area += (rp[0] - a) * (prev - b)
+                        prev = b
+                assert got_hv == area, t
+            else:
+                assert got_hv == chk.hv_mc_box(fs, None, rp, 1024, 11)[0], t
+            st = nxt
+
+
+def test_run_metrics_trajectory_against_reference_run(tb):
+    """Free-running IGD / HV trajectory against the reference's own rvea_run with a MetricContext (recorded in
+    tests/golden/metrics.npz): identical while the survivor counts agree, close afterwards."""
+    g = golden("metrics")
+    pf = g["a_pf"]  # dtlz_pf_reference(2, 3, 12): 91 points
+    rec = tb.rvea_run(tb.make_problem("dtlz2", 10, 3), tb.RunConfig(pop=60, generations=15, seed=6),
+                      tb.MetricContext(pf_ref=pf, hv_ref=np.full(3, 1.1)))
+    pops = np.array([r.pop_size for r in rec.rows])
+    same = pops == g["run_pop"]
+    agree = int(np.argmax(~same)) if not same.all() else len(pops)
+    assert agree >= 3
+    for t in range(agree):
+        assert abs(rec.rows[t].igd_value - g["run_igd"][t]) <= 1e-12 and abs(rec.rows[t].hv_value - g["run_hv"][t]) <= 5e-3, t
+    assert abs(rec.rows[-1].igd_value - g["run_igd"][-1]) <= 0.05
+
+
 def test_free_running_c1_against_reference_run(tb, checkers):
     """Free-running (nothing injected) at config #1. Offspring are bit-identical as long as the
     survivor sets are; objectives carry the device evaluator's ulps (cos/sin, tree reduction),

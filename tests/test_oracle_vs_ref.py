@@ -124,6 +124,19 @@ def test_pipeline_other_operators(oracle, ref, op):
             assert np.array_equal(st["x"], b["x"]) and np.array_equal(st["f"], b["f"]) and st["counter"] == a["counter"]
 
 
+def test_metrics_against_reference(oracle, ref):
+    """igd and the Monte-Carlo hypervolume of the C restatement against metrics.hpp on random instances."""
+    from conftest import Stream
+    for k in range(12):
+        g = Stream(ref, 4400 + k)
+        n, m, n_ref = g.pick(1, 80), g.pick(2, 6), g.pick(1, 50)
+        f, pf = g.tensor(n, m) * 2.0, g.tensor(n_ref, m)
+        rp, lo = np.full(m, 1.5), np.full(m, 0.1 * (k % 3))
+        assert oracle.igd(f, pf) == ref.igd(f, pf)
+        assert oracle.hv_mc_box(f, lo, rp, 300 + k, 77 + k) == ref.hv_mc_box(f, lo, rp, 300 + k, 77 + k)
+        assert oracle.hv_mc_box(f, None, rp, 300 + k, 77 + k) == ref.hv_mc_box(f, None, rp, 300 + k, 77 + k)
+
+
 def test_swarm_operators_suite_7002(oracle, ref):
     """DE / PSO / CSO: the C restatement against the compiled reference, batched and
     scalar-oracle forms, on the reference's own operator_suite instances (verify.hpp:117-182: master seed 7002,
