@@ -224,6 +224,16 @@ int temo_b200_hv_mc_box(const double* f, uint64_t n, uint64_t m, const double* l
 /* hv_mc (metrics.hpp:121-124): the box is [col_min(f), ref]. */
 int temo_b200_hv_mc(const double* f, uint64_t n, uint64_t m, const double* ref, uint64_t samples,
                     uint64_t seed, double* value, double* std_error);
+/* Archive::insert (algorithms.hpp:72-122) on host buffers: the archive (x_old n_old x d, f_old n_old x m) receives the
+ * rows (x_new, f_new); exact duplicates keep their earliest copy, dominated rows leave, kept archive rows come first and
+ * insertion order is preserved; cap > 0 truncates by crowding distance (truncate_by_crowding, :124-143). The O(n^2)
+ * dominance filter runs on the device, compaction and the crowding sort on the host. x_out / f_out hold up to
+ * n_old + n_new rows and may not alias the inputs. */
+int temo_b200_archive_insert(const double* x_old, const double* f_old, uint64_t n_old, const double* x_new,
+                             const double* f_new, uint64_t n_new, uint64_t d, uint64_t m, uint64_t cap,
+                             double* x_out, double* f_out, uint64_t* n_out);
+/* crowding_distance (selection.hpp:289-312) of a k x m front (host code, no GPU needed). */
+int temo_b200_crowding_distance(const double* front, uint64_t k, uint64_t m, double* dist);
 /* MetricContext (algorithms.hpp:46-54) of a run: pf_ref (n_ref x m; n_ref = 0: no IGD), hv_ref (m values or
  * NULL: no HV), hv_scale, hv_samples, hv_seed, maximization. */
 int temo_b200_run_set_metrics(temo_b200_run* run, const double* pf_ref, uint64_t n_ref, const double* hv_ref,

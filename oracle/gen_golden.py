@@ -216,6 +216,20 @@ def main():
                    f"{tag}_hv": np.array(ref.hv_mc_box(f, None, rp, samples, seed))})
     tr = ref.rvea_run_metrics("dtlz2", 60, 10, 3, 15, pf_ref=ref.dtlz_pf_reference(2, 3, 12), hv_ref=np.full(3, 1.1), seed=6)
     me.update(run_pop=tr["pop_size"], run_igd=tr["igd"], run_hv=tr["hv"])
+    # Archive::insert / crowding_distance (algorithms.hpp:72-144, selection.hpp:289-312): coarse objective grids give exact
+    # duplicates and many dominance relations; two successive insertions, the second one capped
+    for tag, (n0, n1, n2, d, m, q, cap) in (("ar0", (30, 40, 35, 4, 3, 5.0, 12)), ("ar1", (0, 25, 60, 3, 2, 8.0, 5)),
+                                             ("ar2", (50, 50, 50, 2, 4, 3.0, 20))):
+        g = Stream(ref, 5100 + n1)
+        xs = [g.tensor(k, d) if k else np.empty((0, d)) for k in (n0, n1, n2)]
+        fs = [np.floor(g.tensor(k, m) * q) / q if k else np.empty((0, m)) for k in (n0, n1, n2)]
+        a0 = ref.archive_insert(None, None, xs[0], fs[0]) if n0 else (None, None)
+        a1 = ref.archive_insert(a0[0], a0[1], xs[1], fs[1])
+        a2 = ref.archive_insert(a1[0], a1[1], xs[2], fs[2], cap)
+        me.update({f"{tag}_x{k}": xs[k] for k in range(3)})
+        me.update({f"{tag}_f{k}": fs[k] for k in range(3)})
+        me.update({f"{tag}_cap": np.array([cap]), f"{tag}_a1x": a1[0], f"{tag}_a1f": a1[1], f"{tag}_a2x": a2[0], f"{tag}_a2f": a2[1],
+                   f"{tag}_crowd": ref.crowding_distance(a1[1])})
     np.savez(os.path.join(OUT, "metrics.npz"), **me)
     total = sum(os.path.getsize(os.path.join(OUT, f)) for f in os.listdir(OUT))
     print(f"wrote {OUT}: {total/1024:.1f} KiB")

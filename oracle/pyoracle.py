@@ -69,6 +69,20 @@ class _Base:
     def take_generation(self, *a, **k):  # pragma: no cover - overridden
         raise NotImplementedError
 
+    def _archive(self, fn_insert, x_old, f_old, x_new, f_new, cap):
+        x_new, f_new = _f(x_new), _f(f_new)
+        d, m = x_new.shape[1], f_new.shape[1]
+        x_old = np.empty((0, d)) if x_old is None else _f(x_old).reshape(-1, d)
+        f_old = np.empty((0, m)) if f_old is None else _f(f_old).reshape(-1, m)
+        n_old, n_new = f_old.shape[0], f_new.shape[0]
+        xo, fo = np.empty((n_old + n_new, d)), np.empty((n_old + n_new, m))
+        rows = u64(0)
+        rc = fn_insert(_p(x_old) if n_old else None, _p(f_old) if n_old else None, u64(n_old), _p(x_new), _p(f_new), u64(n_new),
+                       u64(d), u64(m), u64(cap), _p(xo), _p(fo), C.byref(rows))
+        if rc:
+            raise RuntimeError(f"archive_insert rc={rc}")
+        return xo[: rows.value].copy(), fo[: rows.value].copy()
+
     def pool_scores(self, f, v, gamma, t, t_max, alpha):
         """apd_scores (selection.hpp:228-234): rv_core's apd column."""
         return self.rv_select(f, v, gamma, t, t_max, alpha).apd
@@ -303,6 +317,17 @@ class Oracle(_Base):
         if rc:
             raise ValueError(f"rv_select contract violation rc={rc}")
         return Selection(elite[: ne.value].copy(), valid, assoc, theta, apd)
+
+    def archive_insert(self, x_old, f_old, x_new, f_new, cap=0):
+        """Archive::insert (algorithms.hpp:72-144) -> (x, f) of the updated archive."""
+        return self._archive(self.lib.to_archive_insert, x_old, f_old, x_new, f_new, cap)
+
+    def crowding_distance(self, front):
+        front = _f(front)
+        out = np.empty(front.shape[0])
+        if self.lib.to_crowding_distance(_p(front), u64(front.shape[0]), u64(front.shape[1]), _p(out)):
+            raise ValueError("crowding_distance: empty front")
+        return out
 
     # ---- metrics.hpp
     def igd(self, f, pf):
@@ -588,6 +613,16 @@ class Ref(_Base):
         out = C.c_double(0)
         self._chk(self.lib.ref_igd(_p(f), u64(f.shape[0]), u64(f.shape[1]), _p(pf), u64(pf.shape[0]), C.byref(out)))
         return out.value
+
+    def archive_insert(self, x_old, f_old, x_new, f_new, cap=0):
+        """The reference's Archive::insert (algorithms.hpp:72-144) -> (x, f) of the updated archive."""
+        return self._archive(self.lib.ref_archive_insert, x_old, f_old, x_new, f_new, cap)
+
+    def crowding_distance(self, front):
+        front = _f(front)
+        out = np.empty(front.shape[0])
+        self._chk(self.lib.ref_crowding_distance(_p(front), u64(front.shape[0]), u64(front.shape[1]), _p(out)))
+        return out
 
     def hv_mc_box(self, f, lo, ref, samples, seed):
         """(value, std_error) of hv_mc_box; lo=None -> hv_mc (metrics.hpp:76-124)."""

@@ -433,4 +433,25 @@ int ref_rvea_run_metrics(const char* problem, const char* op, const std::uint64_
     });
 }
 
+// Archive::insert (algorithms.hpp:72-144) on flat arrays; x_out / f_out hold n_old + n_new rows.
+int ref_archive_insert(const double* x_old, const double* f_old, std::uint64_t n_old, const double* x_new, const double* f_new,
+                       std::uint64_t n_new, std::uint64_t d, std::uint64_t m, std::uint64_t cap, double* x_out, double* f_out,
+                       std::uint64_t* n_out) {
+    return guarded([&] {
+        temo::Archive a;
+        if (n_old) {
+            a.x = wrap(x_old, n_old, d);
+            a.f = wrap(f_old, n_old, m);
+        }
+        a.insert(wrap(x_new, n_new, d), wrap(f_new, n_new, m), cap);
+        *n_out = a.f.rows;
+        unwrap(a.x, x_out);
+        unwrap(a.f, f_out);
+    });
+}
+
+int ref_crowding_distance(const double* front, std::uint64_t k, std::uint64_t m, double* dist) {
+    return guarded([&] { unwrap(temo::crowding_distance(wrap(front, k, m)), dist); });
+}
+
 } // extern "C"

@@ -878,3 +878,107 @@ int to_hv_mc(const double* f, uint64_t n, uint64_t m, const double* ref, uint64_
             if (f[i * m + k] < lo[k]) lo[k] = f[i * m + k];
     return to_hv_mc_box(f, n, m, lo, ref, samples, seed, out);
 }
+
+/* ------------------------------------------------ Archive::insert (algorithms.hpp:72-144), crowding_distance */
+
+static int to_dominates(const double* a, const double* b, uint64_t m) { /* selection.hpp:240-247 */
+    int strict = 0;
+    for (uint64_t k = 0; k < m; ++k) {
+        if (a[k] > b[k]) return 0;
+        if (a[k] < b[k]) strict = 1;
+    }
+    return strict;
+}
+static int to_equal(const double* a, const double* b, uint64_t m) {
+    for (uint64_t k = 0; k < m; ++k)
+        if (!(a[k] == b[k])) return 0;
+    return 1;
+}
+
+/* selection.hpp:289-312; ties in the per-objective order go to the lower row. */
+static const double* g_sort_f;
+static uint64_t g_sort_m, g_sort_obj;
+static int to_cmp_obj(const void* pa, const void* pb) {
+    const uint64_t a = *(const uint64_t*)pa, b = *(const uint64_t*)pb;
+    const double fa = g_sort_f[a * g_sort_m + g_sort_obj], fb = g_sort_f[b * g_sort_m + g_sort_obj];
+    if (fa != fb) return fa < fb ? -1 : 1;
+    return a < b ? -1 : (a > b ? 1 : 0);
+}
+int to_crowding_distance(const double* front, uint64_t k, uint64_t m, double* dist) {
+    if (k < 1) return 1;
+    for (uint64_t i = 0; i < k; ++i) dist[i] = k <= 2 ? INFINITY : 0.0;
+    if (k <= 2) return 0;
+    uint64_t* order = (uint64_t*)malloc(k * sizeof(uint64_t));
+    if (!order) return 2;
+    for (uint64_t obj = 0; obj < m; ++obj) {
+        for (uint64_t i = 0; i < k; ++i) order[i] = i;
+        g_sort_f = front; g_sort_m = m; g_sort_obj = obj;
+        qsort(order, k, sizeof(uint64_t), to_cmp_obj); /* a total order: any sort gives the same permutation */
+        const double range = front[order[k - 1] * m + obj] - front[order[0] * m + obj];
+        if (range <= 0.0) continue;
+        dist[order[0]] = INFINITY;
+        dist[order[k - 1]] = INFINITY;
+        for (uint64_t i = 1; i + 1 < k; ++i)
+            dist[order[i]] += (front[order[i + 1] * m + obj] - front[order[i - 1] * m + obj]) / range;
+    }
+    free(order);
+    return 0;
+}
+
+static const double* g_crowd;
+static int to_cmp_crowd(const void* pa, const void* pb) {
+    const uint64_t a = *(const uint64_t*)pa, b = *(const uint64_t*)pb;
+    if (g_crowd[a] != g_crowd[b]) return g_crowd[a] > g_crowd[b] ? -1 : 1;
+    return a < b ? -1 : (a > b ? 1 : 0);
+}
+static int to_cmp_u64(const void* pa, const void* pb) {
+    const uint64_t a = *(const uint64_t*)pa, b = *(const uint64_t*)pb;
+    return a < b ? -1 : (a > b ? 1 : 0);
+}
+
+/* x_out / f_out hold n_old + n_new rows. */
+int to_archive_insert(const double* x_old, const double* f_old, uint64_t n_old, const double* x_new, const double* f_new,
+                      uint64_t n_new, uint64_t d, uint64_t m, uint64_t cap, double* x_out, double* f_out, uint64_t* n_out) {
+    uint64_t row = 0;
+    for (uint64_t j = 0; j < n_old; ++j) { /* :91-100 */
+        int keep = 1;
+        for (uint64_t i = 0; i < n_new && keep; ++i)
+            if (to_dominates(f_new + i * m, f_old + j * m, m)) keep = 0;
+        if (!keep) continue;
+        memcpy(x_out + row * d, x_old + j * d, d * sizeof(double));
+        memcpy(f_out + row * m, f_old + j * m, m * sizeof(double));
+        ++row;
+    }
+    for (uint64_t i = 0; i < n_new; ++i) { /* :76-90 */
+        const double* fi = f_new + i * m;
+        int keep = 1;
+        for (uint64_t j = 0; j < n_old && keep; ++j)
+            if (to_equal(fi, f_old + j * m, m) || to_dominates(f_old + j * m, fi, m)) keep = 0;
+        for (uint64_t k = 0; k < n_new && keep; ++k) {
+            if (k == i) continue;
+            if (to_dominates(f_new + k * m, fi, m) || (k < i && to_equal(fi, f_new + k * m, m))) keep = 0;
+        }
+        if (!keep) continue;
+        memcpy(x_out + row * d, x_new + i * d, d * sizeof(double));
+        memcpy(f_out + row * m, fi, m * sizeof(double));
+        ++row;
+    }
+    if (cap > 0 && row > cap) { /* truncate_by_crowding, :124-143 */
+        double* crowd = (double*)malloc(row * sizeof(double));
+        uint64_t* order = (uint64_t*)malloc(row * sizeof(uint64_t));
+        if (!crowd || !order) return 2;
+        to_crowding_distance(f_out, row, m, crowd);
+        for (uint64_t i = 0; i < row; ++i) order[i] = i;
+        g_crowd = crowd;
+        qsort(order, row, sizeof(uint64_t), to_cmp_crowd);
+        qsort(order, cap, sizeof(uint64_t), to_cmp_u64);
+        for (uint64_t i = 0; i < cap; ++i) {
+            memmove(x_out + i * d, x_out + order[i] * d, d * sizeof(double));
+            memmove(f_out + i * m, f_out + order[i] * m, m * sizeof(double));
+        }
+        row = cap;
+        free(crowd); free(order);
+    }
+    *n_out = row;
+    return 0;
+}

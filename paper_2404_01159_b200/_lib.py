@@ -81,6 +81,8 @@ SIGNATURES = {
     "temo_b200_igd": (C.c_int, [f64p, u64, u64, f64p, u64, f64p]),
     "temo_b200_hv_mc_box": (C.c_int, [f64p, u64, u64, f64p, f64p, u64, u64, f64p, f64p]),
     "temo_b200_hv_mc": (C.c_int, [f64p, u64, u64, f64p, u64, u64, f64p, f64p]),
+    "temo_b200_archive_insert": (C.c_int, [f64p, f64p, u64, f64p, f64p, u64, u64, u64, u64, f64p, f64p, u64p]),
+    "temo_b200_crowding_distance": (C.c_int, [f64p, u64, u64, f64p]),
     "temo_b200_run_set_metrics": (C.c_int, [_RUN, f64p, u64, f64p, C.c_double, u64, u64, C.c_int]),
     "temo_b200_run_metrics": (C.c_int, [_RUN, f64p, f64p]),
     "temo_b200_run_create": (C.c_int, [_CFG, C.POINTER(_RUN)]),

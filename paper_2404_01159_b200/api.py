@@ -483,6 +483,36 @@ class MetricContext:
     maximization: bool = False
 
 
+def crowding_distance(front) -> np.ndarray:
+    """reference: crowding_distance (selection.hpp:289-312); host code."""
+    front = _t(front)
+    if front.shape[0] < 1:
+        raise ValueError("crowding_distance: empty front")
+    out = np.empty(front.shape[0])
+    _call(_lib.load().temo_b200_crowding_distance, _p(front), u64(front.shape[0]), u64(front.shape[1]), _p(out))
+    return out
+
+
+class Archive:
+    """reference: Archive (algorithms.hpp:68-144): running set of mutually nondominated solutions."""
+
+    def __init__(self):
+        self.x = np.empty((0, 0))
+        self.f = np.empty((0, 0))
+
+    def insert(self, xn, fn, cap: int = 0) -> None:
+        xn, fn = _t(xn), _t(fn)
+        n_old, n_new = self.f.shape[0], fn.shape[0]
+        d, m = xn.shape[1], fn.shape[1]
+        x_out, f_out = np.empty((n_old + n_new, d)), np.empty((n_old + n_new, m))
+        rows = u64(0)
+        xo = _t(self.x) if n_old else None
+        fo = _t(self.f) if n_old else None
+        _call(_lib.load().temo_b200_archive_insert, _p(xo), _p(fo), u64(n_old), _p(xn), _p(fn), u64(n_new), u64(d), u64(m), u64(cap),
+              _p(x_out), _p(f_out), C.byref(rows))
+        self.x, self.f = x_out[: rows.value].copy(), f_out[: rows.value].copy()
+
+
 def igd(f, f_ref) -> float:
     """reference: igd (metrics.hpp:21-44)."""
     f, f_ref = _t(f), _t(f_ref)

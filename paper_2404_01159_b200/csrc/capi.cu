@@ -8,6 +8,7 @@
 
 #include "../../include/temo_b200.h"
 #include "glibc_pow.cuh"
+#include <algorithm>
 #include "internal.h"
 #include "run.h"
 #include "vecindex.h"
@@ -684,6 +685,61 @@ int temo_b200_hv_mc(const double* f, uint64_t n, uint64_t m, const double* ref, 
         dl.to_host(lo, s);
         TEMO_CUDA(cudaStreamSynchronize(s));
         device_hv_mc_box(df.p, nullptr, n, m, dl.p, lo, false, dr.p, ref, 1.0, samples, seed, hits.p, value, std_error, s);
+    });
+}
+
+int temo_b200_crowding_distance(const double* front, uint64_t k, uint64_t m, double* dist) {
+    return guarded([&] {
+        require(front && dist, "crowding_distance: null argument");
+        crowding_distance_host(front, k, m, dist);
+    });
+}
+
+int temo_b200_archive_insert(const double* x_old, const double* f_old, uint64_t n_old, const double* x_new, const double* f_new,
+                             uint64_t n_new, uint64_t d, uint64_t m, uint64_t cap, double* x_out, double* f_out, uint64_t* n_out) {
+    return guarded([&] {
+        require(x_out && f_out && n_out, "Archive::insert: null output");
+        require((n_old == 0 || (x_old && f_old)) && (n_new == 0 || (x_new && f_new)), "Archive::insert: null input");
+        std::vector<unsigned char> keep_old(n_old), keep_new(n_new);
+        if (n_old + n_new) {
+            cudaStream_t s = ctx().stream;
+            DevBuf<double> dfo(f_old, n_old * m, s), dfn(f_new, n_new * m, s);
+            DevBuf<unsigned char> dko(n_old), dkn(n_new);
+            launch_archive_filter(dfo.p, n_old, dfn.p, n_new, m, dko.p, dkn.p, s);
+            dko.to_host(keep_old.data(), s, n_old);
+            dkn.to_host(keep_new.data(), s, n_new);
+            TEMO_CUDA(cudaStreamSynchronize(s));
+        }
+        // kept archive rows first, then kept new rows, both in their own order (algorithms.hpp:101-120)
+        uint64_t row = 0;
+        auto take = [&](const double* x, const double* f, uint64_t i) {
+            std::memcpy(x_out + row * d, x + i * d, d * sizeof(double));
+            std::memcpy(f_out + row * m, f + i * m, m * sizeof(double));
+            ++row;
+        };
+        for (uint64_t j = 0; j < n_old; ++j)
+            if (keep_old[j]) take(x_old, f_old, j);
+        for (uint64_t i = 0; i < n_new; ++i)
+            if (keep_new[i]) take(x_new, f_new, i);
+        if (cap > 0 && row > cap) {  // truncate_by_crowding (algorithms.hpp:124-143)
+            std::vector<double> crowd(row);
+            crowding_distance_host(f_out, row, m, crowd.data());
+            std::vector<uint64_t> order(row);
+            for (uint64_t i = 0; i < row; ++i) order[i] = i;
+            std::sort(order.begin(), order.end(), [&](uint64_t a, uint64_t b) {
+                if (crowd[a] != crowd[b]) return crowd[a] > crowd[b];
+                return a < b;
+            });
+            order.resize(cap);
+            std::sort(order.begin(), order.end());  // keep insertion order
+            for (uint64_t i = 0; i < cap; ++i) {    // order[i] >= i: an in-place forward compaction is safe
+                if (order[i] == i) continue;
+                std::memmove(x_out + i * d, x_out + order[i] * d, d * sizeof(double));
+                std::memmove(f_out + i * m, f_out + order[i] * m, m * sizeof(double));
+            }
+            row = cap;
+        }
+        *n_out = row;
     });
 }
 

@@ -6,6 +6,9 @@
 #include <cstring>
 #include <mutex>
 
+#include <algorithm>
+#include <limits>
+#include <vector>
 #include "internal.h"
 
 namespace temo_b200 {
@@ -160,6 +163,33 @@ BoundSegments find_bound_segments(const double* lower, const double* upper, uint
     g.lo[1] = split < d ? lower[split] : lower[0];
     g.hi[1] = split < d ? upper[split] : upper[0];
     return g;
+}
+
+// crowding_distance (selection.hpp:289-312): per objective a (value, index)-ordered sort; the boundary rows get
+// infinity, the inner rows accumulate (next - previous) / range in objective order.
+void crowding_distance_host(const double* front, uint64_t k, uint64_t m, double* dist) {
+    require(k >= 1, "crowding_distance: empty front");
+    const double inf = std::numeric_limits<double>::infinity();
+    if (k <= 2) {
+        for (uint64_t i = 0; i < k; ++i) dist[i] = inf;
+        return;
+    }
+    for (uint64_t i = 0; i < k; ++i) dist[i] = 0.0;
+    std::vector<uint64_t> order(k);
+    for (uint64_t obj = 0; obj < m; ++obj) {
+        for (uint64_t i = 0; i < k; ++i) order[i] = i;
+        std::sort(order.begin(), order.end(), [&](uint64_t a, uint64_t b) {
+            const double fa = front[a * m + obj], fb = front[b * m + obj];
+            if (fa != fb) return fa < fb;
+            return a < b;
+        });
+        const double range = front[order[k - 1] * m + obj] - front[order[0] * m + obj];
+        if (range <= 0.0) continue;
+        dist[order[0]] = inf;
+        dist[order[k - 1]] = inf;
+        for (uint64_t i = 1; i + 1 < k; ++i)
+            dist[order[i]] += (front[order[i + 1] * m + obj] - front[order[i - 1] * m + obj]) / range;
+    }
 }
 
 }  // namespace temo_b200

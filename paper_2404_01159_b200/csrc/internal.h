@@ -183,6 +183,11 @@ double device_igd(const double* f, const uint32_t* n_dev, uint64_t n, uint64_t m
 void device_hv_mc_box(const double* f, const uint32_t* n_dev, uint64_t n, uint64_t m, const double* lo_dev, const double* lo_host,
                       bool lo_scaled, const double* ref_dev, const double* ref_host, double scale, uint64_t samples, uint64_t seed,
                       unsigned long long* hits_scratch, double* value, double* std_error, cudaStream_t s);
+// Archive::insert's dominance filter (algorithms.hpp:76-100): keep flags of the archive rows and of the inserted rows.
+void launch_archive_filter(const double* f_old, uint64_t n_old, const double* f_new, uint64_t n_new, uint64_t m, unsigned char* keep_old,
+                           unsigned char* keep_new, cudaStream_t s);
+// crowding_distance (selection.hpp:289-312), host: k x m front -> k distances.
+void crowding_distance_host(const double* front, uint64_t k, uint64_t m, double* dist);
 // hv_exact_2d (metrics.hpp:48-66) on a host copy of an n x 2 objective matrix divided by scale.
 double host_hv_exact_2d(const double* f, uint64_t n, const double* ref, double scale);
 

@@ -83,7 +83,67 @@ __global__ void __launch_bounds__(256) hv_mc_kernel(const double* __restrict__ f
     if (dominated && lane == 0) atomicAdd(hits, 1ULL);
 }
 
+
+// ---- Archive::insert (algorithms.hpp:72-122): the O(n^2) dominance filter ------------------------------------
+// a dominates b: a <= b everywhere and a < b somewhere (selection.hpp:240-247)
+__device__ __forceinline__ bool dominates_dev(const double* a, const double* b, uint64_t m) {
+    bool strict = false;
+    for (uint64_t k = 0; k < m; ++k) {
+        if (a[k] > b[k]) return false;
+        if (a[k] < b[k]) strict = true;
+    }
+    return strict;
+}
+__device__ __forceinline__ bool equal_rows(const double* a, const double* b, uint64_t m) {
+    for (uint64_t k = 0; k < m; ++k)
+        if (!(a[k] == b[k])) return false;
+    return true;
+}
+
+// One warp per row. Rows [0, n_old) are the archive, [n_old, n_old + n_new) the inserted rows.
+//   new row i is dropped when an archive row equals or dominates it, a new row dominates it, or an earlier new row
+//   equals it (algorithms.hpp:76-90); an archive row is dropped when a new row dominates it (:91-100).
+__global__ void __launch_bounds__(256) archive_filter_kernel(const double* __restrict__ f_old, uint64_t n_old, const double* __restrict__ f_new,
+                                                              uint64_t n_new, uint64_t m, unsigned char* __restrict__ keep_old,
+                                                              unsigned char* __restrict__ keep_new) {
+    const uint64_t row = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+    const uint32_t lane = threadIdx.x & 31;
+    if (row >= n_old + n_new) return;
+    double mine[kMaxObj];
+    const bool is_new = row >= n_old;
+    const uint64_t i = is_new ? row - n_old : row;
+    const double* me = (is_new ? f_new : f_old) + i * m;
+    for (uint64_t k = 0; k < m; ++k) mine[k] = me[k];
+    bool drop = false;
+    if (is_new) {
+        for (uint64_t j0 = 0; j0 < n_old && !drop; j0 += 32) {
+            const uint64_t j = j0 + lane;
+            const bool hit = j < n_old && (equal_rows(mine, f_old + j * m, m) || dominates_dev(f_old + j * m, mine, m));
+            drop = __any_sync(0xffffffffu, hit);
+        }
+    }
+    for (uint64_t k0 = 0; k0 < n_new && !drop; k0 += 32) {
+        const uint64_t k = k0 + lane;
+        bool hit = false;
+        if (k < n_new && !(is_new && k == i)) {
+            const double* fk = f_new + k * m;
+            hit = dominates_dev(fk, mine, m) || (is_new && k < i && equal_rows(mine, fk, m));
+        }
+        drop = __any_sync(0xffffffffu, hit);
+    }
+    if (lane == 0) (is_new ? keep_new : keep_old)[i] = drop ? 0 : 1;
+}
+
 }  // namespace
+
+void launch_archive_filter(const double* f_old, uint64_t n_old, const double* f_new, uint64_t n_new, uint64_t m, unsigned char* keep_old,
+                           unsigned char* keep_new, cudaStream_t s) {
+    require(m >= 1 && m <= (uint64_t)kMaxObj, "Archive::insert: unsupported objective count");
+    const uint64_t rows = n_old + n_new;
+    if (rows == 0) return;
+    archive_filter_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, s>>>(f_old, n_old, f_new, n_new, m, keep_old, keep_new);
+    TEMO_CUDA(cudaGetLastError());
+}
 
 double device_igd(const double* f, const uint32_t* n_dev, uint64_t n, uint64_t m, const double* f_ref, uint64_t n_ref,
                   double* nearest_scratch, cudaStream_t s) {

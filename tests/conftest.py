@@ -96,3 +96,16 @@ def ulp_diff(a, b):
     a = np.where(a < 0, np.int64(-2**63) - a, a)
     b = np.where(b < 0, np.int64(-2**63) - b, b)
     return np.abs(a - b)
+
+
+def _archive_case(ins, crowd, g, tag):
+    """Two successive Archive::insert calls (the second capped) and crowding_distance against the recorded reference."""
+    xs, fs = [g[f"{tag}_x{k}"] for k in range(3)], [g[f"{tag}_f{k}"] for k in range(3)]
+    cap = int(g[f"{tag}_cap"][0])
+    a = ins(None, None, xs[0], fs[0], 0) if fs[0].shape[0] else (None, None)
+    a = ins(a[0], a[1], xs[1], fs[1], 0)
+    assert np.array_equal(a[0], g[f"{tag}_a1x"]) and np.array_equal(a[1], g[f"{tag}_a1f"]), tag
+    assert np.array_equal(crowd(a[1]), g[f"{tag}_crowd"]), tag
+    a = ins(a[0], a[1], xs[2], fs[2], cap)
+    assert np.array_equal(a[0], g[f"{tag}_a2x"]) and np.array_equal(a[1], g[f"{tag}_a2f"]), tag
+    assert a[1].shape[0] <= cap

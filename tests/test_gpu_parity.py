@@ -695,6 +695,37 @@ def test_metrics_golden_and_checkers(tb, checkers):
         tb.hv_mc(g["a_f"], g["a_ref"], 0, 1)
 
 
+def test_archive_insert_golden_and_checkers(tb, checkers):
+    """Archive::insert through the C ABI (device dominance filter, host compaction and crowding cap) against the recorded
+    reference archives and against the CPU checkers at a size where the filter does real work."""
+    from conftest import _archive_case
+
+    def ins(xo, fo, xn, fn, cap):
+        a = tb.Archive()
+        if fo is not None:
+            a.x, a.f = xo, fo
+        a.insert(xn, fn, cap)
+        return a.x, a.f
+
+    g = golden("metrics")
+    for tag in ("ar0", "ar1", "ar2"):
+        _archive_case(ins, tb.crowding_distance, g, tag)
+    chk = checkers[-1]
+    rng = np.random.default_rng(11)
+    for n0, n1, d, m, q, cap in ((3000, 2500, 6, 3, 40.0, 0), (2000, 3000, 3, 5, 6.0, 300), (1, 1, 2, 2, 2.0, 0)):
+        x0, x1 = rng.random((n0, d)), rng.random((n1, d))
+        f0, f1 = np.floor(rng.random((n0, m)) * q) / q, np.floor(rng.random((n1, m)) * q) / q
+        a = chk.archive_insert(None, None, x0, f0)
+        b = ins(None, None, x0, f0, 0)
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+        a, b = chk.archive_insert(a[0], a[1], x1, f1, cap), ins(b[0], b[1], x1, f1, cap)
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]), (n0, n1, cap)
+        # the archive is mutually nondominated and free of duplicates
+        fa = b[1]
+        le = (fa[:, None, :] <= fa[None, :, :]).all(-1) & (fa[:, None, :] < fa[None, :, :]).any(-1)
+        assert not le.any() and len(np.unique(fa, axis=0)) == len(fa)
+
+
 @pytest.mark.parametrize("m", [3, 2])
 def test_run_metrics_lockstep(tb, checkers, m):
     """fill_metrics (algorithms.hpp:161-180) evaluated on the device-resident survivors: every generation of a lock-step

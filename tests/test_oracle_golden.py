@@ -219,6 +219,14 @@ def test_metrics_golden(oracle):
         oracle.igd(np.zeros((0, 3)), g["a_pf"])
 
 
+def test_archive_golden(oracle):
+    """Archive::insert with duplicates, dominated rows and a crowding-distance cap (algorithms.hpp:72-144)."""
+    from conftest import _archive_case
+    g = golden("metrics")
+    for tag in ("ar0", "ar1", "ar2"):
+        _archive_case(lambda xo, fo, xn, fn, cap: oracle.archive_insert(xo, fo, xn, fn, cap), oracle.crowding_distance, g, tag)
+
+
 def test_lsmop1_restatement_self_checks(oracle):
     """LSMOP1 is not in the reference (parity unpinned): check the restatement against an
     independent numpy transcription of the published definition and its basic properties."""

@@ -137,6 +137,22 @@ def test_metrics_against_reference(oracle, ref):
         assert oracle.hv_mc_box(f, None, rp, 300 + k, 77 + k) == ref.hv_mc_box(f, None, rp, 300 + k, 77 + k)
 
 
+def test_archive_against_reference(oracle, ref):
+    from conftest import Stream
+    for k in range(10):
+        g = Stream(ref, 6600 + k)
+        n0, n1, d, m = g.pick(0, 40), g.pick(1, 60), g.pick(1, 5), g.pick(2, 5)
+        q = float(g.pick(2, 9))
+        x0, x1 = (g.tensor(n0, d) if n0 else np.empty((0, d))), g.tensor(n1, d)
+        f0, f1 = (np.floor(g.tensor(n0, m) * q) / q if n0 else np.empty((0, m))), np.floor(g.tensor(n1, m) * q) / q
+        a = ref.archive_insert(None, None, x0, f0) if n0 else (None, None)
+        b = oracle.archive_insert(None, None, x0, f0) if n0 else (None, None)
+        for cap in (0, 7):
+            ra, rb = ref.archive_insert(a[0], a[1], x1, f1, cap), oracle.archive_insert(b[0], b[1], x1, f1, cap)
+            assert np.array_equal(ra[0], rb[0]) and np.array_equal(ra[1], rb[1]), (k, cap)
+        assert np.array_equal(ref.crowding_distance(f1), oracle.crowding_distance(f1))
+
+
 def test_swarm_operators_suite_7002(oracle, ref):
     """DE / PSO / CSO: the C restatement against the compiled reference, batched and
     scalar-oracle forms, on the reference's own operator_suite instances (verify.hpp:117-182: master seed 7002,
