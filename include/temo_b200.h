@@ -214,6 +214,31 @@ int temo_b200_rvea_run(const temo_b200_run_config* cfg, double* final_x, double*
                        uint64_t* final_rows, uint64_t* rows_done, uint64_t* pop_size,
                        double* elapsed_ms);
 
+/* ---- NSGA-II baseline ---------------------------------------- */
+/* nondominated_sort (selection.hpp:251-283): front rank of each of the n rows of f (rank 0 = nondominated). */
+int temo_b200_nondominated_sort(const double* f, uint64_t n, uint64_t m, uint64_t* rank);
+/* nsga2_select (selection.hpp:316-346): `target` row indices, fronts in ascending rank, the last front split by
+ * descending crowding distance (ties: lowest row). */
+int temo_b200_nsga2_select(const double* f, uint64_t n, uint64_t m, uint64_t target, uint64_t* selected);
+/* nsga2_run (algorithms.hpp:301-369, track_archive = false) as a device-resident session; cfg as for rvea_run
+ * (lattice_h / alpha / fr / op are not used). */
+typedef struct temo_b200_nsga2 temo_b200_nsga2; /* opaque */
+int temo_b200_nsga2_create(const temo_b200_run_config* cfg, temo_b200_nsga2** out);
+/* One generation. f_off (optional, n x m): selection runs on these offspring objectives instead of the device's
+ * (lock-step testing). */
+int temo_b200_nsga2_step(temo_b200_nsga2* run, const double* f_off);
+int temo_b200_nsga2_inject(temo_b200_nsga2* run, const double* x, const double* f, uint64_t counter, uint64_t t);
+int temo_b200_nsga2_state(temo_b200_nsga2* run, uint64_t* counter, uint64_t* t, uint64_t* d);
+int temo_b200_nsga2_download(temo_b200_nsga2* run, double* x, double* f);
+/* offspring (n x d), their device-evaluated objectives (n x m), the selected merged rows (n; parents first) and
+ * the tournament winners (n) of the last generation; any may be NULL. */
+int temo_b200_nsga2_last_generation(temo_b200_nsga2* run, double* offspring, double* f_off, uint64_t* selected,
+                                    uint64_t* pool_idx);
+int temo_b200_nsga2_destroy(temo_b200_nsga2* run);
+/* whole run: final_x (pop x d), final_f (pop x m), cumulative elapsed ms per generation (may be NULL). */
+int temo_b200_nsga2_run(const temo_b200_run_config* cfg, double* final_x, double* final_f, uint64_t* rows_done,
+                        double* elapsed_ms);
+
 /* ---- metrics.hpp (quality indicators) ----------------------- */
 /* igd (metrics.hpp:21-44): mean distance from each row of f_ref (n_ref x m) to its nearest row of f (n x m). */
 int temo_b200_igd(const double* f, uint64_t n, uint64_t m, const double* f_ref, uint64_t n_ref, double* out);

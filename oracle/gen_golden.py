@@ -231,6 +231,17 @@ def main():
         me.update({f"{tag}_cap": np.array([cap]), f"{tag}_a1x": a1[0], f"{tag}_a1f": a1[1], f"{tag}_a2x": a2[0], f"{tag}_a2f": a2[1],
                    f"{tag}_crowd": ref.crowding_distance(a1[1])})
     np.savez(os.path.join(OUT, "metrics.npz"), **me)
+    # ---- NSGA-II baseline (selection.hpp:251-346, algorithms.hpp:301-369) ----
+    ns = {}
+    for tag, (n, m, q) in (("s0", (60, 3, 6.0)), ("s1", (200, 2, 50.0)), ("s2", (120, 5, 3.0)), ("s3", (1, 3, 2.0))):
+        g = Stream(ref, 7300 + n)
+        f = np.floor(g.tensor(n, m) * q) / q
+        ns.update({f"{tag}_f": f, f"{tag}_rank": ref.nondominated_sort(f), f"{tag}_sel_half": ref.nsga2_select(f, n // 2),
+                   f"{tag}_sel_third": ref.nsga2_select(f, (n + 2) // 3), f"{tag}_sel_all": ref.nsga2_select(f, n)})
+    for tag, (problem, n, d, m, gens, seed) in (("r0", ("dtlz2", 40, 9, 3, 12, 3)), ("r1", ("dtlz1", 33, 15, 2, 15, 8))):
+        rr = ref.nsga2_run(problem, n, d, m, gens, seed=seed)
+        ns.update({f"{tag}_x": rr["x"], f"{tag}_f": rr["f"]})
+    np.savez(os.path.join(OUT, "nsga2.npz"), **ns)
     total = sum(os.path.getsize(os.path.join(OUT, f)) for f in os.listdir(OUT))
     print(f"wrote {OUT}: {total/1024:.1f} KiB")
 

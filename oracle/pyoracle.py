@@ -329,6 +329,44 @@ class Oracle(_Base):
             raise ValueError("crowding_distance: empty front")
         return out
 
+    # ---- NSGA-II baseline (selection.hpp:251-346, algorithms.hpp:301-369)
+    def nondominated_sort(self, f):
+        f = _f(f)
+        rank = np.zeros(f.shape[0], dtype=np.uint64)
+        if self.lib.to_nondominated_sort(_p(f), u64(f.shape[0]), u64(f.shape[1]), _p(rank, u64p)):
+            raise MemoryError("nondominated_sort")
+        return rank
+
+    def nsga2_select(self, f, target):
+        f = _f(f)
+        sel = np.zeros(target, dtype=np.uint64)
+        if self.lib.to_nsga2_select(_p(f), u64(f.shape[0]), u64(f.shape[1]), u64(target), _p(sel, u64p)):
+            raise ValueError("nsga2_select: target exceeds population")
+        return sel
+
+    def nsga2_generation(self, problem, m, seed, counter, lower, upper, x, f, ga=GA_DEFAULT):
+        """One generation of nsga2_run on explicit state -> dict(x, f, counter, offspring, f_off, sel, pool_idx)."""
+        x, f = _f(x).copy(), _f(f).copy()
+        n, d = x.shape
+        off, f_off = np.empty((n, d)), np.empty((n, m))
+        sel, pool_idx = np.zeros(n, dtype=np.uint64), np.zeros(n, dtype=np.uint64)
+        c = u64(counter)
+        rc = self.lib.to_nsga2_generation(C.c_int(PROBLEM_IDS[problem]), u64(n), u64(d), u64(m), u64(seed), C.byref(c), _p(_f(ga)),
+                                          _p(_f(lower)), _p(_f(upper)), _p(x), _p(f), _p(off), _p(f_off), _p(sel, u64p),
+                                          _p(pool_idx, u64p))
+        if rc:
+            raise RuntimeError(f"nsga2_generation rc={rc}")
+        return dict(x=x, f=f, counter=c.value, offspring=off, f_off=f_off, sel=sel, pool_idx=pool_idx)
+
+    def nsga2_run(self, problem, n, d, m, generations, seed=42, ga=GA_DEFAULT):
+        x, f = np.empty((n, d)), np.empty((n, m))
+        c = u64(0)
+        rc = self.lib.to_nsga2_run(C.c_int(PROBLEM_IDS[problem]), u64(n), u64(d), u64(m), u64(generations), u64(seed), _p(_f(ga)),
+                                   _p(x), _p(f), C.byref(c))
+        if rc:
+            raise RuntimeError(f"nsga2_run rc={rc}")
+        return dict(x=x, f=f, counter=c.value)
+
     # ---- metrics.hpp
     def igd(self, f, pf):
         f, pf = _f(f), _f(pf)
@@ -623,6 +661,25 @@ class Ref(_Base):
         out = np.empty(front.shape[0])
         self._chk(self.lib.ref_crowding_distance(_p(front), u64(front.shape[0]), u64(front.shape[1]), _p(out)))
         return out
+
+    def nondominated_sort(self, f):
+        f = _f(f)
+        rank = np.zeros(f.shape[0], dtype=np.uint64)
+        self._chk(self.lib.ref_nondominated_sort(_p(f), u64(f.shape[0]), u64(f.shape[1]), _p(rank, u64p)))
+        return rank
+
+    def nsga2_select(self, f, target):
+        f = _f(f)
+        sel = np.zeros(target, dtype=np.uint64)
+        self._chk(self.lib.ref_nsga2_select(_p(f), u64(f.shape[0]), u64(f.shape[1]), u64(target), _p(sel, u64p)))
+        return sel
+
+    def nsga2_run(self, problem, n, d, m, generations, seed=42, ga=GA_DEFAULT):
+        """The reference's nsga2_run (algorithms.hpp:301-369), track_archive = false."""
+        x, f = np.empty((n, d)), np.empty((n, m))
+        cfg_u = np.array([n, generations, seed, d, m], dtype=np.uint64)
+        self._chk(self.lib.ref_nsga2_run(problem.encode(), _p(cfg_u, u64p), _p(_f(ga)), _p(x), _p(f)))
+        return dict(x=x, f=f)
 
     def hv_mc_box(self, f, lo, ref, samples, seed):
         """(value, std_error) of hv_mc_box; lo=None -> hv_mc (metrics.hpp:76-124)."""

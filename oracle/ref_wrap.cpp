@@ -454,4 +454,38 @@ int ref_crowding_distance(const double* front, std::uint64_t k, std::uint64_t m,
     return guarded([&] { unwrap(temo::crowding_distance(wrap(front, k, m)), dist); });
 }
 
+// ---- NSGA-II baseline (selection.hpp:251-346, algorithms.hpp:301-369) ----------------------------
+int ref_nondominated_sort(const double* f, std::uint64_t n, std::uint64_t m, std::uint64_t* rank) {
+    return guarded([&] {
+        const std::vector<std::size_t> r = temo::nondominated_sort(wrap(f, n, m));
+        for (std::size_t i = 0; i < r.size(); ++i) rank[i] = r[i];
+    });
+}
+
+int ref_nsga2_select(const double* f, std::uint64_t n, std::uint64_t m, std::uint64_t target, std::uint64_t* selected) {
+    return guarded([&] {
+        const std::vector<std::size_t> s = temo::nsga2_select(wrap(f, n, m), target);
+        for (std::size_t i = 0; i < s.size(); ++i) selected[i] = s[i];
+    });
+}
+
+// cfg_u: {pop, generations, seed, dim, obj}
+int ref_nsga2_run(const char* problem, const std::uint64_t* cfg_u, const double* ga, double* final_x, double* final_f) {
+    return guarded([&] {
+        temo::RunConfig cfg;
+        cfg.problem = problem;
+        cfg.pop = cfg_u[0];
+        cfg.generations = cfg_u[1];
+        cfg.seed = cfg_u[2];
+        cfg.dim = cfg_u[3];
+        cfg.obj = cfg_u[4];
+        cfg.track_archive = false;
+        cfg.ga = ga_of(ga);
+        const temo::ProblemInstance prob = temo::make_problem(cfg.problem, cfg.dim, cfg.obj);
+        const temo::RunRecord rec = temo::nsga2_run(prob, cfg, temo::MetricContext{});
+        unwrap(rec.final_x, final_x);
+        unwrap(rec.final_f, final_f);
+    });
+}
+
 } // extern "C"

@@ -982,3 +982,153 @@ int to_archive_insert(const double* x_old, const double* f_old, uint64_t n_old, 
     *n_out = row;
     return 0;
 }
+
+/* ------------------------------------------- NSGA-II baseline */
+
+/* selection.hpp:251-283. rank[i] = index of the front row i is peeled in = length of the longest chain of
+ * dominators above it; computed here by peeling with dominator counts like the reference. */
+int to_nondominated_sort(const double* f, uint64_t n, uint64_t m, uint64_t* rank) {
+    uint32_t* cnt = (uint32_t*)calloc(n ? n : 1, sizeof(uint32_t));
+    unsigned char* done = (unsigned char*)calloc(n ? n : 1, 1);
+    uint64_t* cur = (uint64_t*)malloc((n ? n : 1) * sizeof(uint64_t));
+    if (!cnt || !done || !cur) return 2;
+    for (uint64_t i = 0; i < n; ++i)
+        for (uint64_t j = 0; j < n; ++j)
+            if (i != j && to_dominates(f + j * m, f + i * m, m)) ++cnt[i];
+    uint64_t left = n, level = 0;
+    while (left) {
+        uint64_t k = 0;
+        for (uint64_t i = 0; i < n; ++i)
+            if (!done[i] && cnt[i] == 0) cur[k++] = i;
+        if (!k) break; /* cannot happen for a strict partial order */
+        for (uint64_t a = 0; a < k; ++a) {
+            const uint64_t i = cur[a];
+            rank[i] = level;
+            done[i] = 1;
+        }
+        for (uint64_t a = 0; a < k; ++a)
+            for (uint64_t j = 0; j < n; ++j)
+                if (!done[j] && to_dominates(f + cur[a] * m, f + j * m, m)) --cnt[j];
+        left -= k;
+        ++level;
+    }
+    free(cnt); free(done); free(cur);
+    return 0;
+}
+
+static const uint64_t* g_front_rows;
+static int to_cmp_crowd_rows(const void* pa, const void* pb) { /* selection.hpp:336-339 */
+    const uint64_t a = *(const uint64_t*)pa, b = *(const uint64_t*)pb;
+    if (g_crowd[a] != g_crowd[b]) return g_crowd[a] > g_crowd[b] ? -1 : 1;
+    return g_front_rows[a] < g_front_rows[b] ? -1 : (g_front_rows[a] > g_front_rows[b] ? 1 : 0);
+}
+
+/* selection.hpp:316-346: fill by ascending rank, split the last front by descending crowding distance. */
+int to_nsga2_select(const double* f, uint64_t n, uint64_t m, uint64_t target, uint64_t* selected) {
+    if (target > n) return 1;
+    uint64_t* rank = (uint64_t*)malloc((n ? n : 1) * sizeof(uint64_t));
+    uint64_t* rows = (uint64_t*)malloc((n ? n : 1) * sizeof(uint64_t));
+    uint64_t* by = (uint64_t*)malloc((n ? n : 1) * sizeof(uint64_t));
+    double* front = (double*)malloc((n * m ? n * m : 1) * sizeof(double));
+    double* crowd = (double*)malloc((n ? n : 1) * sizeof(double));
+    if (!rank || !rows || !by || !front || !crowd) return 2;
+    int rc = to_nondominated_sort(f, n, m, rank);
+    uint64_t cnt = 0;
+    for (uint64_t level = 0; !rc && cnt < target; ++level) {
+        uint64_t k = 0;
+        for (uint64_t i = 0; i < n; ++i)
+            if (rank[i] == level) rows[k++] = i;
+        if (cnt + k <= target) {
+            for (uint64_t a = 0; a < k; ++a) selected[cnt++] = rows[a];
+            continue;
+        }
+        for (uint64_t a = 0; a < k; ++a) memcpy(front + a * m, f + rows[a] * m, m * sizeof(double));
+        to_crowding_distance(front, k, m, crowd);
+        for (uint64_t a = 0; a < k; ++a) by[a] = a;
+        g_crowd = crowd;
+        g_front_rows = rows;
+        qsort(by, k, sizeof(uint64_t), to_cmp_crowd_rows);
+        for (uint64_t a = 0; cnt < target; ++a) selected[cnt++] = rows[by[a]];
+    }
+    free(rank); free(rows); free(by); free(front); free(crowd);
+    return rc;
+}
+
+/* One generation of nsga2_run (algorithms.hpp:314-356) on explicit state: x (n x d), f (n x m) in/out, *counter in/out.
+ * Optional outputs: offspring (n x d), f_off (n x m), sel (n merged-row indices), pool_idx (n). */
+int to_nsga2_generation(int problem, uint64_t n, uint64_t d, uint64_t m, uint64_t seed, uint64_t* counter, const double* ga,
+                        const double* lower, const double* upper, double* x, double* f, double* offspring_out, double* f_off_out,
+                        uint64_t* sel_out, uint64_t* pool_idx_out) {
+    uint64_t* rank = (uint64_t*)malloc(n * sizeof(uint64_t));
+    uint64_t* members = (uint64_t*)malloc(n * sizeof(uint64_t));
+    uint64_t* pool_idx = (uint64_t*)malloc(n * sizeof(uint64_t));
+    uint64_t* sel = (uint64_t*)malloc(n * sizeof(uint64_t));
+    double* crowd = (double*)calloc(n, sizeof(double));
+    double* front = (double*)malloc(n * m * sizeof(double));
+    double* cd = (double*)malloc(n * sizeof(double));
+    double* pool = (double*)malloc(n * d * sizeof(double));
+    double* crossed = (double*)malloc(n * d * sizeof(double));
+    double* mx = (double*)malloc(2 * n * d * sizeof(double));
+    double* mf = (double*)malloc(2 * n * m * sizeof(double));
+    if (!rank || !members || !pool_idx || !sel || !crowd || !front || !cd || !pool || !crossed || !mx || !mf) return 2;
+    int rc = to_nondominated_sort(f, n, m, rank);
+    uint64_t levels = 0;
+    for (uint64_t i = 0; i < n; ++i)
+        if (rank[i] + 1 > levels) levels = rank[i] + 1;
+    for (uint64_t level = 0; level < levels; ++level) { /* :316-329 */
+        uint64_t k = 0;
+        for (uint64_t i = 0; i < n; ++i)
+            if (rank[i] == level) members[k++] = i;
+        if (!k) continue;
+        for (uint64_t a = 0; a < k; ++a) memcpy(front + a * m, f + members[a] * m, m * sizeof(double));
+        to_crowding_distance(front, k, m, cd);
+        for (uint64_t a = 0; a < k; ++a) crowd[members[a]] = cd[a];
+    }
+    for (uint64_t i = 0; i < n; ++i) { /* binary tournament, :332-345 */
+        const uint64_t a = (uint64_t)(to_value_at(seed, (*counter)++) * (double)n);
+        const uint64_t b = (uint64_t)(to_value_at(seed, (*counter)++) * (double)n);
+        int a_wins;
+        if (rank[a] != rank[b]) a_wins = rank[a] < rank[b];
+        else if (crowd[a] != crowd[b]) a_wins = crowd[a] > crowd[b];
+        else a_wins = a <= b;
+        pool_idx[i] = a_wins ? a : b;
+    }
+    for (uint64_t i = 0; i < n; ++i) memcpy(pool + i * d, x + pool_idx[i] * d, d * sizeof(double));
+    to_sbx(pool, n, d, seed, counter, ga, lower, upper, crossed);               /* :347 */
+    memcpy(mx, x, n * d * sizeof(double));
+    memcpy(mf, f, n * m * sizeof(double));
+    to_polynomial_mutation(crossed, n, d, seed, counter, ga, lower, upper, mx + n * d); /* :348-349 */
+    if (!rc) rc = to_evaluate(problem, mx + n * d, n, d, m, mf + n * m);
+    if (!rc) rc = to_nsga2_select(mf, 2 * n, m, n, sel);                         /* :353 */
+    if (!rc) {
+        if (offspring_out) memcpy(offspring_out, mx + n * d, n * d * sizeof(double));
+        if (f_off_out) memcpy(f_off_out, mf + n * m, n * m * sizeof(double));
+        for (uint64_t k = 0; k < n; ++k) {
+            memcpy(x + k * d, mx + sel[k] * d, d * sizeof(double));
+            memcpy(f + k * m, mf + sel[k] * m, m * sizeof(double));
+            if (sel_out) sel_out[k] = sel[k];
+            if (pool_idx_out) pool_idx_out[k] = pool_idx[k];
+        }
+    }
+    free(rank); free(members); free(pool_idx); free(sel); free(crowd); free(front); free(cd); free(pool); free(crossed);
+    free(mx); free(mf);
+    return rc;
+}
+
+/* algorithms.hpp:301-369 with track_archive = false. */
+int to_nsga2_run(int problem, uint64_t n, uint64_t d, uint64_t m, uint64_t generations, uint64_t seed, const double* ga,
+                 double* x_out, double* f_out, uint64_t* counter_out) {
+    if (n < 2 || generations < 1 || m > 64) return -1;
+    double* lower = (double*)malloc(d * sizeof(double));
+    double* upper = (double*)malloc(d * sizeof(double));
+    if (!lower || !upper) return -2;
+    to_problem_bounds(problem, d, m, lower, upper);
+    uint64_t counter = 0;
+    to_random_reproduce(n, d, seed, &counter, lower, upper, x_out);
+    int rc = to_evaluate(problem, x_out, n, d, m, f_out);
+    for (uint64_t t = 0; !rc && t < generations; ++t)
+        rc = to_nsga2_generation(problem, n, d, m, seed, &counter, ga, lower, upper, x_out, f_out, NULL, NULL, NULL, NULL);
+    if (counter_out) *counter_out = counter;
+    free(lower); free(upper);
+    return rc;
+}

@@ -78,6 +78,16 @@ SIGNATURES = {
     "temo_b200_rv_select": (C.c_int, [f64p, u64, u64, f64p, f64p, u64, u64, u64, C.c_double, u64p, u64p, u8p,
                                       u64p, f64p, f64p]),
     "temo_b200_apd_penalty": (C.c_double, [u64, u64, u64, C.c_double]),
+    "temo_b200_nondominated_sort": (C.c_int, [f64p, u64, u64, u64p]),
+    "temo_b200_nsga2_select": (C.c_int, [f64p, u64, u64, u64, u64p]),
+    "temo_b200_nsga2_create": (C.c_int, [_CFG, C.POINTER(_RUN)]),
+    "temo_b200_nsga2_step": (C.c_int, [_RUN, f64p]),
+    "temo_b200_nsga2_inject": (C.c_int, [_RUN, f64p, f64p, u64, u64]),
+    "temo_b200_nsga2_state": (C.c_int, [_RUN, u64p, u64p, u64p]),
+    "temo_b200_nsga2_download": (C.c_int, [_RUN, f64p, f64p]),
+    "temo_b200_nsga2_last_generation": (C.c_int, [_RUN, f64p, f64p, u64p, u64p]),
+    "temo_b200_nsga2_destroy": (C.c_int, [_RUN]),
+    "temo_b200_nsga2_run": (C.c_int, [_CFG, f64p, f64p, u64p, f64p]),
     "temo_b200_igd": (C.c_int, [f64p, u64, u64, f64p, u64, f64p]),
     "temo_b200_hv_mc_box": (C.c_int, [f64p, u64, u64, f64p, f64p, u64, u64, f64p, f64p]),
     "temo_b200_hv_mc": (C.c_int, [f64p, u64, u64, f64p, u64, u64, f64p, f64p]),

@@ -664,6 +664,92 @@ class RveaRun:
         return out.value
 
 
+# ---- NSGA-II baseline ---------------------------------------------
+def nondominated_sort(f) -> np.ndarray:
+    """reference: nondominated_sort (selection.hpp:251-283): front rank of every row."""
+    f = _t(f)
+    rank = np.zeros(f.shape[0], dtype=np.uint64)
+    _call(_lib.load().temo_b200_nondominated_sort, _p(f), u64(f.shape[0]), u64(f.shape[1]), _p(rank, u64p))
+    return rank
+
+
+def nsga2_select(f, target: int) -> np.ndarray:
+    """reference: nsga2_select (selection.hpp:316-346)."""
+    f = _t(f)
+    if target > f.shape[0]:
+        raise ValueError("nsga2_select: target exceeds population")
+    sel = np.zeros(target, dtype=np.uint64)
+    _call(_lib.load().temo_b200_nsga2_select, _p(f), u64(f.shape[0]), u64(f.shape[1]), u64(target), _p(sel, u64p))
+    return sel
+
+
+class Nsga2Run:
+    """Device-resident NSGA-II loop (session form of nsga2_run, algorithms.hpp:301-369)."""
+
+    def __init__(self, cfg: RunConfig):
+        self._L = _lib.load()
+        self._h = C.c_void_p()
+        ccfg = cfg.c()
+        _call(self._L.temo_b200_nsga2_create, C.byref(ccfg), C.byref(self._h))
+        self.n, self.m = cfg.pop, cfg.obj
+        self.d = self.state()["d"]
+
+    def close(self):
+        if self._h:
+            self._L.temo_b200_nsga2_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def state(self) -> dict:
+        vals = [u64(0) for _ in range(3)]
+        _call(self._L.temo_b200_nsga2_state, self._h, *[C.byref(v) for v in vals])
+        return dict(zip(("counter", "t", "d"), (v.value for v in vals)))
+
+    def step(self, f_off=None) -> None:
+        f_off = None if f_off is None else _t(f_off)
+        if f_off is not None and f_off.shape != (self.n, self.m):
+            raise ValueError("nsga2 step: f_off must be n x m")
+        _call(self._L.temo_b200_nsga2_step, self._h, _p(f_off))
+
+    def inject(self, x=None, f=None, counter=0, t=0) -> None:
+        x = None if x is None else _t(x)
+        f = None if f is None else _t(f)
+        _call(self._L.temo_b200_nsga2_inject, self._h, _p(x), _p(f), u64(counter), u64(t))
+
+    def download(self) -> dict:
+        x, f = np.empty((self.n, self.d)), np.empty((self.n, self.m))
+        _call(self._L.temo_b200_nsga2_download, self._h, _p(x), _p(f))
+        return dict(x=x, f=f)
+
+    def last_generation(self) -> dict:
+        off, f_off = np.empty((self.n, self.d)), np.empty((self.n, self.m))
+        sel, pool = np.zeros(self.n, dtype=np.uint64), np.zeros(self.n, dtype=np.uint64)
+        _call(self._L.temo_b200_nsga2_last_generation, self._h, _p(off), _p(f_off), _p(sel, u64p), _p(pool, u64p))
+        return dict(offspring=off, f_off=f_off, sel=sel, pool_idx=pool)
+
+
+def nsga2_run(prob: ProblemInstance, cfg: RunConfig) -> RunRecord:
+    """reference: nsga2_run (algorithms.hpp:301-369), track_archive = false."""
+    cfg = RunConfig(**{**cfg.__dict__, "problem": prob.name, "dim": prob.dim, "obj": prob.num_obj})
+    ccfg = cfg.c()
+    x, f = np.empty((cfg.pop, prob.dim)), np.empty((cfg.pop, prob.num_obj))
+    done = u64(0)
+    ms = np.zeros(cfg.generations)
+    _call(_lib.load().temo_b200_nsga2_run, C.byref(ccfg), _p(x), _p(f), C.byref(done), _p(ms))
+    return RunRecord([GenerationRow(t, float(ms[t]), cfg.pop) for t in range(done.value)], x, f)
+
+
 def rvea_run(prob: ProblemInstance, cfg: RunConfig, mc: MetricContext | None = None) -> RunRecord:
     """reference: rvea_run (algorithms.hpp:227-296). `prob` supplies name/dim/num_obj like the
     reference's ProblemInstance; the evaluator itself runs on the device. With a MetricContext every

@@ -10,6 +10,7 @@
 #include "glibc_pow.cuh"
 #include <algorithm>
 #include "internal.h"
+#include "nsga2.h"
 #include "run.h"
 #include "vecindex.h"
 
@@ -642,6 +643,111 @@ int temo_b200_rvea_run(const temo_b200_run_config* cfg, double* final_x, double*
         }
         run.download(final_x, final_f, nullptr, nullptr);
         if (final_rows) *final_rows = run.P;
+        if (rows_done) *rows_done = done;
+    });
+}
+
+// ---- NSGA-II baseline ------------------------------------------------------------------------------------
+int temo_b200_nondominated_sort(const double* f, uint64_t n, uint64_t m, uint64_t* rank) {
+    return guarded([&] {
+        require(n == 0 || (f && rank), "nondominated_sort: null argument");
+        if (n == 0) return;
+        cudaStream_t s = ctx().stream;
+        DevBuf<double> df(f, n * m, s);
+        SortScratch sc;
+        struct Guard { SortScratch& x; ~Guard() { x.release(); } } guard{sc};
+        sc.alloc(n);
+        std::vector<uint32_t> r(n);
+        device_nondominated_sort(df.p, n, m, sc, r.data(), s);
+        for (uint64_t i = 0; i < n; ++i) rank[i] = r[i];
+    });
+}
+
+int temo_b200_nsga2_select(const double* f, uint64_t n, uint64_t m, uint64_t target, uint64_t* selected) {
+    return guarded([&] {
+        require(target <= n, "nsga2_select: target exceeds population");  // selection.hpp:317
+        if (target == 0) return;
+        require(f && selected, "nsga2_select: null argument");
+        cudaStream_t s = ctx().stream;
+        DevBuf<double> df(f, n * m, s);
+        SortScratch sc;
+        struct Guard { SortScratch& x; ~Guard() { x.release(); } } guard{sc};
+        sc.alloc(n);
+        std::vector<uint32_t> r(n), sel(target);
+        device_nondominated_sort(df.p, n, m, sc, r.data(), s);
+        nsga2_select_host(f, r.data(), n, m, target, sel.data());
+        for (uint64_t k = 0; k < target; ++k) selected[k] = sel[k];
+    });
+}
+
+struct temo_b200_nsga2 {
+    std::unique_ptr<Nsga2Run> impl;
+};
+
+int temo_b200_nsga2_create(const temo_b200_run_config* cfg, temo_b200_nsga2** out) {
+    return guarded([&] {
+        require(out != nullptr, "nsga2_create: null output");
+        *out = nullptr;
+        std::unique_ptr<temo_b200_nsga2> h(new temo_b200_nsga2);
+        h->impl.reset(new Nsga2Run(cfg_of(cfg)));
+        *out = h.release();
+    });
+}
+
+int temo_b200_nsga2_step(temo_b200_nsga2* run, const double* f_off) {
+    return guarded([&] {
+        require(run && run->impl, "nsga2_step: null run");
+        run->impl->step(f_off);
+    });
+}
+
+int temo_b200_nsga2_inject(temo_b200_nsga2* run, const double* x, const double* f, uint64_t counter, uint64_t t) {
+    return guarded([&] {
+        require(run && run->impl, "nsga2_inject: null run");
+        run->impl->inject(x, f, counter, t);
+    });
+}
+
+int temo_b200_nsga2_state(temo_b200_nsga2* run, uint64_t* counter, uint64_t* t, uint64_t* d) {
+    return guarded([&] {
+        require(run && run->impl, "nsga2_state: null run");
+        if (counter) *counter = run->impl->counter;
+        if (t) *t = run->impl->t;
+        if (d) *d = run->impl->d;
+    });
+}
+
+int temo_b200_nsga2_download(temo_b200_nsga2* run, double* x, double* f) {
+    return guarded([&] {
+        require(run && run->impl, "nsga2_download: null run");
+        run->impl->download(x, f);
+    });
+}
+
+int temo_b200_nsga2_last_generation(temo_b200_nsga2* run, double* offspring, double* f_off, uint64_t* selected, uint64_t* pool_idx) {
+    return guarded([&] {
+        require(run && run->impl, "nsga2_last_generation: null run");
+        run->impl->last_generation(offspring, f_off, selected, pool_idx);
+    });
+}
+
+int temo_b200_nsga2_destroy(temo_b200_nsga2* run) {
+    return guarded([&] { delete run; });
+}
+
+int temo_b200_nsga2_run(const temo_b200_run_config* cfg, double* final_x, double* final_f, uint64_t* rows_done, double* elapsed_ms) {
+    return guarded([&] {
+        const auto t0 = std::chrono::steady_clock::now();
+        Nsga2Run run(cfg_of(cfg));
+        uint64_t done = 0;
+        for (uint64_t t = 0; t < run.cfg.generations; ++t) {
+            run.step();
+            const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+            if (elapsed_ms) elapsed_ms[t] = ms;
+            ++done;
+            if (run.cfg.time_budget_s > 0.0 && ms >= run.cfg.time_budget_s * 1e3) break;  // algorithms.hpp:364
+        }
+        run.download(final_x, final_f);
         if (rows_done) *rows_done = done;
     });
 }

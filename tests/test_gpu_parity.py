@@ -666,6 +666,71 @@ def test_unknown_operator_is_rejected(tb):
         tb.RveaRun(tb.RunConfig(op="sa"))
 
 
+# -------------------------------------------------------------------------- NSGA-II baseline
+def test_nondominated_sort_and_select(tb, checkers):
+    """Front ranks and nsga2_select through the C ABI against the recorded reference and the CPU checkers (coarse grids:
+    duplicates, long domination chains, single-front and single-row inputs)."""
+    g = golden("nsga2")
+    for tag in ("s0", "s1", "s2", "s3"):
+        f = g[f"{tag}_f"]
+        n = f.shape[0]
+        assert np.array_equal(tb.nondominated_sort(f), g[f"{tag}_rank"]), tag
+        assert np.array_equal(tb.nsga2_select(f, n // 2), g[f"{tag}_sel_half"]), tag
+        assert np.array_equal(tb.nsga2_select(f, (n + 2) // 3), g[f"{tag}_sel_third"]), tag
+        assert np.array_equal(tb.nsga2_select(f, n), g[f"{tag}_sel_all"]), tag
+    chk = checkers[-1]
+    rng = np.random.default_rng(8)
+    for n, m, q in ((3000, 3, 12.0), (2048, 2, 1e6), (1500, 10, 4.0), (700, 3, 1.0)):
+        f = np.floor(rng.random((n, m)) * q) / q
+        assert np.array_equal(tb.nondominated_sort(f), chk.nondominated_sort(f)), (n, m)
+        assert np.array_equal(tb.nsga2_select(f, n // 2), chk.nsga2_select(f, n // 2)), (n, m)
+    chain = np.arange(40, dtype=float)[:, None] * np.ones((1, 3))   # a single chain: 40 fronts
+    assert np.array_equal(tb.nondominated_sort(chain), np.arange(40))
+    with pytest.raises(ValueError, match="target exceeds"):
+        tb.nsga2_select(chain, 41)
+
+
+@pytest.mark.parametrize("cfg", [("dtlz2", 40, 9, 3, 12, 3), ("dtlz1", 33, 15, 2, 15, 8), ("dtlz3", 64, 600, 4, 6, 5),
+                                 ("lsmop1", 50, 300, 3, 6, 9)])
+def test_nsga2_lockstep(tb, oracle, cfg):
+    """nsga2_run on the device, lock-step against the C restatement (itself pinned against the reference's nsga2_run):
+    tournament winners, offspring, selected rows and the draw counter bit for bit; objectives within 1e-12."""
+    problem, n, d, m, gens, seed = cfg
+    lo, hi = oracle.problem_bounds(problem, d, m)
+    x, c = oracle.random_reproduce(n, d, seed, 0, lo, hi)
+    st = dict(x=x, f=oracle.evaluate(problem, x, m), counter=c)
+    with tb.Nsga2Run(tb.RunConfig(problem=problem, pop=n, dim=d, obj=m, generations=gens, seed=seed)) as run:
+        init = run.download()
+        assert np.array_equal(init["x"], x) and close_rel(init["f"], st["f"], 1e-12) and run.state()["counter"] == c
+        for t in range(gens):
+            nxt = oracle.nsga2_generation(problem, m, seed, st["counter"], lo, hi, st["x"], st["f"])
+            run.inject(x=st["x"], f=st["f"], counter=st["counter"], t=t)
+            run.step(nxt["f_off"])
+            got = run.last_generation()
+            assert np.array_equal(got["pool_idx"], nxt["pool_idx"]), f"tournament differs at generation {t}"
+            assert np.array_equal(got["offspring"], nxt["offspring"]), f"offspring differ at generation {t}"
+            assert close_rel(got["f_off"], nxt["f_off"], 1e-12), t
+            assert np.array_equal(got["sel"], nxt["sel"]), f"selection differs at generation {t}"
+            assert run.state()["counter"] == nxt["counter"]
+            now = run.download()
+            assert np.array_equal(now["x"], nxt["x"]) and np.array_equal(now["f"], nxt["f"]), t
+            st = nxt
+
+
+def test_nsga2_free_running(tb):
+    """Nothing injected: the device run against the recorded reference run (tests/golden/nsga2.npz). Device objectives
+    carry ulp-level differences, so exact equality is required only of the shape and bounds; the fronts must agree
+    closely (mean objective sums)."""
+    g = golden("nsga2")
+    rec = tb.nsga2_run(tb.make_problem("dtlz2", 9, 3), tb.RunConfig(pop=40, generations=12, seed=3))
+    assert rec.final_x.shape == g["r0_x"].shape and len(rec.rows) == 12
+    assert ((rec.final_x >= 0.0) & (rec.final_x <= 1.0)).all()
+    assert close_rel(rec.final_f, tb.evaluate("dtlz2", rec.final_x, 3), 1e-12)
+    if np.array_equal(rec.final_x, g["r0_x"]):
+        assert close_rel(rec.final_f, g["r0_f"], 1e-12)
+    assert abs(rec.final_f.sum(axis=1).mean() - g["r0_f"].sum(axis=1).mean()) <= 0.1 * g["r0_f"].sum(axis=1).mean()
+
+
 # -------------------------------------------------------------------------- quality indicators (metrics.hpp)
 def test_metrics_golden_and_checkers(tb, checkers):
     """igd / hv_mc_box / hv_mc on the device against the recorded reference values and every CPU checker: bit-exact

@@ -227,6 +227,21 @@ def test_archive_golden(oracle):
         _archive_case(lambda xo, fo, xn, fn, cap: oracle.archive_insert(xo, fo, xn, fn, cap), oracle.crowding_distance, g, tag)
 
 
+def test_nsga2_golden(oracle):
+    """nondominated_sort, nsga2_select and nsga2_run of the C restatement against the recorded reference."""
+    g = golden("nsga2")
+    for tag in ("s0", "s1", "s2", "s3"):
+        f = g[f"{tag}_f"]
+        n = f.shape[0]
+        assert np.array_equal(oracle.nondominated_sort(f), g[f"{tag}_rank"]), tag
+        assert np.array_equal(oracle.nsga2_select(f, n // 2), g[f"{tag}_sel_half"]), tag
+        assert np.array_equal(oracle.nsga2_select(f, (n + 2) // 3), g[f"{tag}_sel_third"]), tag
+        assert np.array_equal(oracle.nsga2_select(f, n), g[f"{tag}_sel_all"]), tag
+    for tag, (problem, n, d, m, gens, seed) in (("r0", ("dtlz2", 40, 9, 3, 12, 3)), ("r1", ("dtlz1", 33, 15, 2, 15, 8))):
+        r = oracle.nsga2_run(problem, n, d, m, gens, seed=seed)
+        assert np.array_equal(r["x"], g[f"{tag}_x"]) and np.array_equal(r["f"], g[f"{tag}_f"]), tag
+
+
 def test_lsmop1_restatement_self_checks(oracle):
     """LSMOP1 is not in the reference (parity unpinned): check the restatement against an
     independent numpy transcription of the published definition and its basic properties."""

@@ -153,6 +153,25 @@ def test_archive_against_reference(oracle, ref):
         assert np.array_equal(ref.crowding_distance(f1), oracle.crowding_distance(f1))
 
 
+def test_nsga2_against_reference(oracle, ref):
+    rng = np.random.default_rng(2)
+    for n, m, q in ((50, 3, 6.0), (200, 2, 50.0), (120, 5, 3.0), (1, 3, 2.0), (2, 2, 2.0), (90, 4, 1000.0)):
+        f = np.floor(rng.random((n, m)) * q) / q
+        assert np.array_equal(oracle.nondominated_sort(f), ref.nondominated_sort(f)), (n, m)
+        for t in (0, n // 3, n // 2, n):
+            assert np.array_equal(oracle.nsga2_select(f, t), ref.nsga2_select(f, t)), (n, m, t)
+    for problem, n, d, m, gens, seed in (("dtlz2", 41, 9, 3, 10, 3), ("dtlz3", 64, 20, 4, 8, 5)):
+        a, b = oracle.nsga2_run(problem, n, d, m, gens, seed=seed), ref.nsga2_run(problem, n, d, m, gens, seed=seed)
+        assert np.array_equal(a["x"], b["x"]) and np.array_equal(a["f"], b["f"])
+        # the generation stepped on explicit state (what the GPU lock-step test uses) reproduces the free run
+        lo, hi = oracle.problem_bounds(problem, d, m)
+        x, c = oracle.random_reproduce(n, d, seed, 0, lo, hi)
+        st = dict(x=x, f=oracle.evaluate(problem, x, m), counter=c)
+        for _ in range(gens):
+            st = oracle.nsga2_generation(problem, m, seed, st["counter"], lo, hi, st["x"], st["f"])
+        assert np.array_equal(st["x"], b["x"]) and np.array_equal(st["f"], b["f"]) and st["counter"] == a["counter"]
+
+
 def test_swarm_operators_suite_7002(oracle, ref):
     """DE / PSO / CSO: the C restatement against the compiled reference, batched and
     scalar-oracle forms, on the reference's own operator_suite instances (verify.hpp:117-182: master seed 7002,
