@@ -8,7 +8,7 @@
 // std::runtime_error otherwise). Requires the reference headers on the include path.
 //
 // reference interfaces mirrored: rng.hpp:55-78, operators.hpp:65-161,287-296, problems.hpp:69-92,
-// refvec.hpp:81-140, selection.hpp:131-135,200-224, algorithms.hpp:21-63,144-150,211-296.
+// refvec.hpp:81-140, selection.hpp:131-135,200-346, algorithms.hpp:21-144,211-369, metrics.hpp:21-124.
 #pragma once
 
 #include <stdexcept>
@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "temo/algorithms.hpp"
+#include "temo/metrics.hpp"
 #include "temo/operators.hpp"
 #include "temo/problems.hpp"
 #include "temo/refvec.hpp"
@@ -261,6 +262,93 @@ inline RunRecord rvea_run(const ProblemInstance& prob, const RunConfig& cfg) {
     rec.final_f = Tensor2D(rows, prob.num_obj);
     std::copy_n(x.data.begin(), rows * prob.dim, rec.final_x.data.begin());
     std::copy_n(f.data.begin(), rows * prob.num_obj, rec.final_f.data.begin());
+    return rec;
+}
+
+// ---- metrics.hpp / Archive / NSGA-II baseline -----------------------------
+/// igd (metrics.hpp:21-44).
+inline double igd(const Tensor2D& f, const Tensor2D& f_ref) {
+    temo::detail::require(f.rows >= 1 && f_ref.rows >= 1, "igd: empty set");
+    temo::detail::require(f.cols == f_ref.cols, "igd: objective count mismatch");
+    double out = 0.0;
+    detail::check(temo_b200_igd(f.data.data(), f.rows, f.cols, f_ref.data.data(), f_ref.rows, &out));
+    return out;
+}
+
+/// hv_mc_box (metrics.hpp:76-117).
+inline HvEstimate hv_mc_box(const Tensor2D& f, const Tensor2D& lo, const Tensor2D& ref, std::size_t samples, std::uint64_t seed) {
+    temo::detail::require(samples >= 1, "hv_mc: needs at least one sample");
+    temo::detail::require(f.rows >= 1 && ref.rows == 1 && ref.cols == f.cols, "hv_mc: bad shapes");
+    temo::detail::require(lo.rows == 1 && lo.cols == f.cols, "hv_mc: bad box");
+    HvEstimate e;
+    detail::check(temo_b200_hv_mc_box(f.data.data(), f.rows, f.cols, lo.data.data(), ref.data.data(), samples, seed, &e.value,
+                                      &e.std_error));
+    return e;
+}
+
+/// hv_mc (metrics.hpp:121-124).
+inline HvEstimate hv_mc(const Tensor2D& f, const Tensor2D& ref, std::size_t samples, std::uint64_t seed) {
+    temo::detail::require(samples >= 1, "hv_mc: needs at least one sample");
+    temo::detail::require(f.rows >= 1 && ref.rows == 1 && ref.cols == f.cols, "hv_mc: bad shapes");
+    HvEstimate e;
+    detail::check(temo_b200_hv_mc(f.data.data(), f.rows, f.cols, ref.data.data(), samples, seed, &e.value, &e.std_error));
+    return e;
+}
+
+/// Archive::insert (algorithms.hpp:72-122) as a free function on the reference's Archive.
+inline void archive_insert(Archive& a, const Tensor2D& xn, const Tensor2D& fn, std::size_t cap = 0) {
+    const std::size_t n_old = a.f.rows, n_new = fn.rows, total = n_old + n_new;
+    Tensor2D nx(total, xn.cols), nf(total, fn.cols);
+    uint64_t rows = 0;
+    detail::check(temo_b200_archive_insert(a.x.data.data(), a.f.data.data(), n_old, xn.data.data(), fn.data.data(), n_new, xn.cols,
+                                           fn.cols, cap, nx.data.data(), nf.data.data(), &rows));
+    a.x = Tensor2D(rows, xn.cols);
+    a.f = Tensor2D(rows, fn.cols);
+    std::copy_n(nx.data.begin(), rows * xn.cols, a.x.data.begin());
+    std::copy_n(nf.data.begin(), rows * fn.cols, a.f.data.begin());
+}
+
+/// nondominated_sort (selection.hpp:251-283).
+inline std::vector<std::size_t> nondominated_sort(const Tensor2D& f) {
+    std::vector<uint64_t> r(f.rows);
+    detail::check(temo_b200_nondominated_sort(f.data.data(), f.rows, f.cols, r.data()));
+    return std::vector<std::size_t>(r.begin(), r.end());
+}
+
+/// nsga2_select (selection.hpp:316-346).
+inline std::vector<std::size_t> nsga2_select(const Tensor2D& f, std::size_t target) {
+    temo::detail::require(target <= f.rows, "nsga2_select: target exceeds population");
+    std::vector<uint64_t> s(target);
+    detail::check(temo_b200_nsga2_select(f.data.data(), f.rows, f.cols, target, s.data()));
+    return std::vector<std::size_t>(s.begin(), s.end());
+}
+
+/// nsga2_run (algorithms.hpp:301-369) with track_archive = false, device-resident for the whole run.
+inline RunRecord nsga2_run(const ProblemInstance& prob, const RunConfig& cfg) {
+    temo::detail::require(cfg.pop >= 2 && cfg.generations >= 1, "nsga2_run: bad config");
+    temo_b200_run_config c;
+    temo_b200_default_run_config(&c);
+    c.problem = detail::problem_id(prob);
+    c.pop = cfg.pop;
+    c.generations = cfg.generations;
+    c.seed = cfg.seed;
+    c.dim = prob.dim;
+    c.obj = prob.num_obj;
+    c.time_budget_s = cfg.time_budget_s;
+    c.ga = detail::ga_of(cfg.ga);
+    RunRecord rec;
+    rec.final_x = Tensor2D(cfg.pop, prob.dim);
+    rec.final_f = Tensor2D(cfg.pop, prob.num_obj);
+    std::vector<double> ms(cfg.generations);
+    uint64_t done = 0;
+    detail::check(temo_b200_nsga2_run(&c, rec.final_x.data.data(), rec.final_f.data.data(), &done, ms.data()));
+    for (uint64_t t = 0; t < done; ++t) {
+        GenerationRow row;
+        row.t = t;
+        row.elapsed_ms = ms[t];
+        row.pop_size = cfg.pop;
+        rec.rows.push_back(row);
+    }
     return rec;
 }
 

@@ -159,6 +159,75 @@ static int whole_run_gpu() {
     return failed;
 }
 
+// metrics.hpp, Archive::insert and the NSGA-II selection pieces with the GPU path swapped in: all bit-identical
+// (integer ranks / indices / hit counts; minima of exactly reproduced distances).
+static int widened_suite_gpu() {
+    int failed = 0;
+    for (std::uint64_t k = 0; k < 40; ++k) {
+        RngStream g{9000 + k, 0};
+        const std::size_t n = verify::detail::pick(g, 1, 90), m = verify::detail::pick(g, 2, 6), n_ref = verify::detail::pick(g, 1, 40);
+        const double q = static_cast<double>(verify::detail::pick(g, 2, 12));
+        Tensor2D f = uniform_tensor(g, n, m), pf = uniform_tensor(g, n_ref, m), x = uniform_tensor(g, n, 3);
+        for (double& v : f.data) v = std::floor(v * q) / q;  // coarse grid: duplicates and domination chains
+        Tensor2D ref_pt(1, m, 1.25), lo(1, m, 0.0);
+        bool ok = b200::igd(f, pf) == igd(f, pf);
+        const HvEstimate a = b200::hv_mc(f, ref_pt, 700 + k, 5 + k), b = hv_mc(f, ref_pt, 700 + k, 5 + k);
+        ok = ok && a.value == b.value && a.std_error == b.std_error;
+        const HvEstimate c = b200::hv_mc_box(f, lo, ref_pt, 300, k), d = hv_mc_box(f, lo, ref_pt, 300, k);
+        ok = ok && c.value == d.value && c.std_error == d.std_error;
+        ok = ok && b200::nondominated_sort(f) == nondominated_sort(f);
+        ok = ok && b200::nsga2_select(f, n / 2) == nsga2_select(f, n / 2);
+        Archive ga, ca;
+        const std::size_t half = n / 2;
+        if (half) {
+            Tensor2D x0(half, 3), f0(half, m);
+            std::copy_n(x.data.begin(), half * 3, x0.data.begin());
+            std::copy_n(f.data.begin(), half * m, f0.data.begin());
+            b200::archive_insert(ga, x0, f0);
+            ca.insert(x0, f0);
+        }
+        b200::archive_insert(ga, x, f, 7);
+        ca.insert(x, f, 7);
+        ok = ok && same_bits(ga.x, ca.x) && same_bits(ga.f, ca.f);
+        failed += !ok;
+    }
+    std::printf("metrics / archive / nondominated_sort / nsga2_select (gpu vs reference, bit-exact): %d/40 failed\n", failed);
+    return failed;
+}
+
+// rvea_run with RunConfig::op = de / pso / cso / random through the shim against the reference's own rvea_run
+// (free-running: exact while the survivor counts agree).
+static int operator_runs_gpu() {
+    int failed = 0;
+    for (const char* op : {"de", "pso", "cso", "random"}) {
+        RunConfig cfg;
+        cfg.problem = "dtlz2";
+        cfg.op = op;
+        cfg.pop = 40;
+        cfg.generations = 12;
+        cfg.seed = 3;
+        cfg.track_archive = false;
+        const ProblemInstance prob = make_problem("dtlz2", 9, 3);
+        const RunRecord a = b200::rvea_run(prob, cfg), b = rvea_run(prob, cfg);
+        std::size_t agree = 0;
+        while (agree < a.rows.size() && agree < b.rows.size() && a.rows[agree].pop_size == b.rows[agree].pop_size) ++agree;
+        const bool x_same = same_bits(a.final_x, b.final_x);
+        std::printf("rvea_run op=%s: survivor counts equal in the first %zu/%zu generations, final x %s\n", op, agree, b.rows.size(),
+                    x_same ? "bit-identical" : "differs");
+        failed += !(a.rows.size() == b.rows.size() && agree >= 3);
+    }
+    bool threw = false;
+    try {
+        RunConfig cfg;
+        cfg.op = "sa";
+        (void)b200::rvea_run(make_problem("dtlz2", 9, 3), cfg);
+    } catch (const std::invalid_argument&) {
+        threw = true;
+    }
+    failed += !threw;
+    return failed;
+}
+
 int main() {
     if (temo_b200_device_count() < 1) {
         std::printf("no CUDA device\n");
@@ -170,6 +239,8 @@ int main() {
     failed += swarm_suite_gpu() != 0;
     failed += ga_pipeline_gpu() != 0;
     failed += whole_run_gpu() != 0;
+    failed += widened_suite_gpu() != 0;
+    failed += operator_runs_gpu() != 0;
     std::printf("%s\n", failed ? "SHIM PARITY FAILED" : "SHIM PARITY OK");
     return failed;
 }
