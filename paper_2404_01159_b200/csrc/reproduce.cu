@@ -58,6 +58,7 @@ struct ReproK {
     double* f_out;
     uint64_t f_row0;
     const uint32_t* f_row0_dev;
+    uint32_t* work_counter;  // pair kernel: pairs handed out beyond the first one of every team (nullptr: static round-robin)
 };
 
 // polynomial_delta (operators.hpp:106-121): both branches evaluated, blended by steps. Rare path (about one
@@ -346,6 +347,9 @@ struct PairCtx {
     uint32_t cross;  // pair-level crossover switch hc = H(r3 - pc) == 0 (operators.hpp:82)
     uint32_t pad;
 };
+#ifndef TEMO_PAIR_STAGE
+#define TEMO_PAIR_STAGE 0                                    // 1: the tile's parent blocks are staged in shared memory by LDGSTS at the tile start
+#endif
 #ifndef TEMO_PAIR_TOUCH
 #define TEMO_PAIR_TOUCH 0                                    // 1: sector touch loads at the tile start, 0: prefetch.global.L2 hints
 #endif
@@ -358,6 +362,9 @@ struct WarpSmem {
 #if TEMO_PAIR_TOUCH
     double2 sink[32];         // landing zone of the touch loads (never read)
 #endif
+#if TEMO_PAIR_STAGE
+    double2 stage[2][kPairBlocks][32];  // parents a / b of this tile: lane l's own vector of every block
+#endif
 };
 struct PairSlot {
     double part[2][kVirtWarps];  // per-warp totals of the two children
@@ -365,10 +372,15 @@ struct PairSlot {
     uint32_t arrived;            // warps that have delivered their partials
     uint32_t done;               // pairs completed through this slot
 };
+constexpr int kUnitRing = 8;                                 // pairs a team's warps may be apart
 struct PairSmem {
     PowSmem pow;
     WarpSmem w[kVirtWarps];
     PairSlot slot[kPairSlots];
+    // dynamic pair hand-out: turn T of this team works on pair ring[T % kUnitRing]
+    uint32_t ring[kUnitRing];
+    uint32_t progress[kVirtWarps];  // turns every warp has finished
+    uint32_t claiming, published;   // highest turn being fetched / already published
 };
 
 // mix64 (rng.hpp:23-30) on 32-bit halves; a 64-bit product costs one wide multiply and two multiply-adds.
@@ -583,6 +595,8 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
         S.slot[threadIdx.x].arrived = 0;
         S.slot[threadIdx.x].done = 0;
     }
+    if (threadIdx.x < kVirtWarps) S.progress[threadIdx.x] = 0;
+    if (threadIdx.x == 0) S.claiming = S.published = 0;
     __syncthreads();  // the only CTA barrier: from here on every warp is on its own
     const PowTables T = pow_tables(S.pow);
 
@@ -594,7 +608,12 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
     const uint32_t sm_w = opaque(smem_u32(&W)), sm_lane = opaque(smem_u32(&W) + lane * 16);  // beta tile is first in WarpSmem
 
     uint32_t turn = 0;   // pairs this team has started
-    for (uint64_t unit = a.unit0 + blockIdx.x; unit < a.unit_end; unit += gridDim.x, ++turn) {
+    // Pairs are handed out dynamically: the hardware arbiter favours one of the three teams of an SM, so with a fixed
+    // share per team the favoured one would leave early and the SM would finish the launch with 16, then 8 warps.
+    // A team's first pair is its block index; for every later turn the first warp to get there draws the next pair
+    // from a global counter and publishes it to the team through a small ring (the warps of a team are never more
+    // than kUnitRing turns apart).
+    for (uint64_t unit = a.unit0 + blockIdx.x; unit < a.unit_end; ++turn) {
         PairSlot& slot = S.slot[turn % kPairSlots];
         if (lane == 0) {
             const uint64_t row_a = unit, row_b = a.half + unit, g_unit = a.g_unit0 + unit;
@@ -619,7 +638,23 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
             if (kmax == 0) break;
             const uint32_t q_first = (blk0 + v) * 32 + lane;  // this lane's vector in the tile's first block
             const uint64_t pos = W.ctx.pos;
-#if TEMO_PAIR_TOUCH
+#if TEMO_PAIR_STAGE
+            {   // every lane copies its own vector of each of the tile's blocks, both parents, into shared memory with
+                // asynchronous 16-byte copies (LDGSTS: no register, no scoreboard): HBM has passes A and B to deliver, and
+                // pass C starts from shared memory. A lane only ever reads what it copied itself, so cp.async.wait_all in
+                // that lane is the only synchronisation needed.
+                const double2* pa2s = reinterpret_cast<const double2*>(W.ctx.pa);
+                const double2* pb2s = reinterpret_cast<const double2*>(W.ctx.pb);
+                uint32_t q = q_first, sa = sm_w + (uint32_t)offsetof(WarpSmem, stage) + lane * 16;
+                for (uint32_t k = 0; k < kmax; ++k, q += kVirtWarps * 32, sa += 512) {
+                    if (q < nvec) {
+                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(pa2s + q) : "memory");
+                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa + kPairBlocks * 512), "l"(pb2s + q) : "memory");
+                    }
+                }
+                asm volatile("cp.async.commit_group;" ::: "memory");
+            }
+#elif TEMO_PAIR_TOUCH
             {   // this warp's parent blocks of this tile into L2, where pass C finds them: one 16-byte asynchronous copy
                 // (LDGSTS, no register, no scoreboard) per 32-byte sector, lanes 0-15 on parent a, 16-31 on parent b. Unlike
                 // prefetch hints these are real loads and cannot be dropped under load; DRAM then has passes A and B to
@@ -685,6 +720,9 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
                 double acc[2] = {acc_a, acc_b};
                 tile_plain<MODE, EVAL>(a, blk0, v, kmax, acc, W, slot.pos);
                 acc_a = acc[0], acc_b = acc[1];
+#if TEMO_PAIR_STAGE
+                asm volatile("cp.async.wait_all;" ::: "memory");  // the staging buffer is reused by the next tile
+#endif
                 __syncwarp();
                 continue;
             }
@@ -738,6 +776,13 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
                 const double seg_lo = a.seg_lo[seg_hi_side ? 1 : 0], seg_hi = a.seg_hi[seg_hi_side ? 1 : 0];
                 const double2* __restrict__ pa2 = reinterpret_cast<const double2*>(W.ctx.pa);
                 const double2* __restrict__ pb2 = reinterpret_cast<const double2*>(W.ctx.pb);
+#if TEMO_PAIR_STAGE
+                uint32_t q = q_first, sm_b = sm_lane, sm_s = sm_w + (uint32_t)offsetof(WarpSmem, stage) + lane * 16;
+                asm volatile("cp.async.wait_all;" ::: "memory");
+                for (uint32_t k = 0; k < kmax; ++k, q += kVirtWarps * 32, sm_b += 512, sm_s += 512) {
+                    if (q >= nvec) break;  // only in the last block of the row
+                    const double2 va = lds_f64x2(sm_s), vb = lds_f64x2(sm_s + kPairBlocks * 512);
+#else
                 uint32_t q = q_first, sm_b = sm_lane;
                 const double2 zero2 = make_double2(0.0, 0.0);
                 // the parents of the next two blocks are always in flight (register double buffer)
@@ -759,6 +804,7 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
                             fb = __ldcs(pb2 + qf);
                         }
                     }
+#endif
                     double2 vlo, vhi;
                     if (SEG) {
                         if (seg_mixed) {  // this tile holds the split: per gene
@@ -837,8 +883,55 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
             }
         }
         __syncwarp();
+        // ---- the team's next pair
+        if (a.work_counter == nullptr) {
+            unit += gridDim.x;
+            continue;
+        }
+        uint32_t next = 0;
+        if (lane == 0) {
+            const uint32_t T = turn + 1;
+            *reinterpret_cast<volatile uint32_t*>(&S.progress[v]) = T;
+            for (;;) {
+                if (*reinterpret_cast<volatile uint32_t*>(&S.published) >= T) {
+                    next = *reinterpret_cast<volatile uint32_t*>(&S.ring[T % kUnitRing]);
+                    break;
+                }
+                if (atomicCAS(&S.claiming, T - 1, T) == T - 1) {  // this warp fetches turn T for the team
+                    if (T >= (uint32_t)kUnitRing)                 // the ring entry is free once everybody has finished turn T - kUnitRing
+                        for (int w = 0; w < kVirtWarps; ++w)
+                            while (*reinterpret_cast<volatile uint32_t*>(&S.progress[w]) + kUnitRing <= T) __nanosleep(100);
+                    next = atomicAdd(a.work_counter, 1u);
+                    *reinterpret_cast<volatile uint32_t*>(&S.ring[T % kUnitRing]) = next;
+                    __threadfence_block();
+                    *reinterpret_cast<volatile uint32_t*>(&S.published) = T;
+                    break;
+                }
+                __nanosleep(100);
+            }
+        }
+        next = __shfl_sync(0xffffffffu, next, 0);
+        unit = a.unit0 + gridDim.x + next;
     }
 }
+
+struct K1Options {
+    int generic, bound_arrays, cand_cap;
+    int dynamic_pairs;  // pair kernel: pairs handed out through a global counter (1, default) or round-robin (0)
+};
+inline int env_int(const char* name, int dflt) {
+    const char* e = getenv(name);
+    return e ? atoi(e) : dflt;
+}
+inline K1Options& k1_options() {
+    static K1Options o{env_int("TEMO_B200_GENERIC_K1", 0), env_int("TEMO_B200_K1_BOUND_ARRAYS", 0),
+                       std::max(0, std::min(kPairCand, env_int("TEMO_B200_K1_CAND_CAP", kPairCand))),
+                       env_int("TEMO_B200_K1_DYNAMIC_PAIRS", 1)};
+    return o;
+}
+inline bool force_generic_kernel() { return k1_options().generic != 0; }
+inline bool no_bound_segments() { return k1_options().bound_arrays != 0; }
+inline int pair_cand_cap() { return k1_options().cand_cap; }
 
 template <int MODE, int EVAL, bool SEG>
 void launch_pairs_seg(const ReproK& k, uint64_t units, cudaStream_t s) {
@@ -851,7 +944,20 @@ void launch_pairs_seg(const ReproK& k, uint64_t units, cudaStream_t s) {
         TEMO_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
         grid = (sms > 0 ? sms : kSMs) * TEMO_PAIR_MIN_BLOCKS;
     }
-    reproduce_pairs_kernel<MODE, EVAL, SEG><<<(unsigned)std::min<uint64_t>(units, (uint64_t)grid), kVirtWarps * 32, sizeof(PairSmem), s>>>(k);
+    ReproK kk = k;
+    kk.work_counter = nullptr;
+    if (k1_options().dynamic_pairs) {
+        // one zeroed counter per launch out of a small ring (launches of different streams may overlap)
+        static uint32_t* counters = nullptr;
+        static unsigned next_counter = 0;
+        constexpr unsigned kCounters = 64;
+        if (!counters) {
+            counters = dev_alloc<uint32_t>(kCounters);
+        }
+        kk.work_counter = counters + (next_counter++ % kCounters);
+        TEMO_CUDA(cudaMemsetAsync(kk.work_counter, 0, sizeof(uint32_t), s));
+    }
+    reproduce_pairs_kernel<MODE, EVAL, SEG><<<(unsigned)std::min<uint64_t>(units, (uint64_t)grid), kVirtWarps * 32, sizeof(PairSmem), s>>>(kk);
 }
 
 template <int MODE, int EVAL>
@@ -940,22 +1046,6 @@ __global__ void pow_batch_kernel(const double* x, const double* y, uint64_t n, d
 //                       they are piecewise constant                       TEMO_B200_K1_BOUND_ARRAYS
 //   k1_cand_cap      mutation-candidate slots per warp tile of the pair
 //                    kernel, 0..kPairCand (0 forces its plain-tile path)  TEMO_B200_K1_CAND_CAP
-struct K1Options {
-    int generic, bound_arrays, cand_cap;
-};
-inline int env_int(const char* name, int dflt) {
-    const char* e = getenv(name);
-    return e ? atoi(e) : dflt;
-}
-inline K1Options& k1_options() {
-    static K1Options o{env_int("TEMO_B200_GENERIC_K1", 0), env_int("TEMO_B200_K1_BOUND_ARRAYS", 0),
-                       std::max(0, std::min(kPairCand, env_int("TEMO_B200_K1_CAND_CAP", kPairCand)))};
-    return o;
-}
-inline bool force_generic_kernel() { return k1_options().generic != 0; }
-inline bool no_bound_segments() { return k1_options().bound_arrays != 0; }
-inline int pair_cand_cap() { return k1_options().cand_cap; }
-
 inline unsigned stream_grid(uint64_t total, int block) {
     uint64_t g = (total + block - 1) / block;
     const uint64_t cap = (uint64_t)kSMs * 16;
@@ -1084,6 +1174,7 @@ bool set_k1_option(const char* name, long value) {
     if (key == "k1_generic") o.generic = value != 0;
     else if (key == "k1_bound_arrays") o.bound_arrays = value != 0;
     else if (key == "k1_cand_cap") o.cand_cap = (int)std::max(0L, std::min((long)kPairCand, value));
+    else if (key == "k1_dynamic_pairs") o.dynamic_pairs = value != 0;
     else return false;
     return true;
 }
