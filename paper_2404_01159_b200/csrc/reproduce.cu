@@ -330,7 +330,10 @@ constexpr int kVirtWarps = 8;                                // warps of the can
 constexpr int kPairBlocks = TEMO_PAIR_BLOCKS;                // 64-gene blocks per warp and tile
 constexpr int kTileGenes = kPairBlocks * 64;                 // genes of one warp tile
 constexpr int kPairCand = 8;                                 // mutation candidates per warp tile
-constexpr int kPairSlots = 4;                                // pairs a team can have in flight
+#ifndef TEMO_PAIR_SLOTS
+#define TEMO_PAIR_SLOTS 3
+#endif
+constexpr int kPairSlots = TEMO_PAIR_SLOTS;                  // pairs a team can have in flight
 constexpr uint32_t kBetaTagHi = 0x7ff80000u;                 // high word of the tagged NaN
 #ifndef TEMO_PAIR_MIN_BLOCKS
 #define TEMO_PAIR_MIN_BLOCKS 3                               // teams per SM
@@ -372,7 +375,10 @@ struct PairSlot {
     uint32_t arrived;            // warps that have delivered their partials
     uint32_t done;               // pairs completed through this slot
 };
-constexpr int kUnitRing = 8;                                 // pairs a team's warps may be apart
+#ifndef TEMO_PAIR_RING
+#define TEMO_PAIR_RING 4
+#endif
+constexpr int kUnitRing = TEMO_PAIR_RING;                    // pairs a team's warps may be apart
 struct PairSmem {
     PowSmem pow;
     WarpSmem w[kVirtWarps];
@@ -668,7 +674,7 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
                 }
                 asm volatile("cp.async.commit_group;" ::: "memory");
             }
-#else
+#elif !defined(TEMO_PAIR_NO_L2HINT)
             {   // this warp's parent blocks of this tile into L2 (they are read in pass C)
                 const uint32_t kk = lane & 15, blk = blk0 + v + kk * kVirtWarps;
                 if (kk < kmax && blk < nblk) {
