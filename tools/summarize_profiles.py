@@ -14,7 +14,10 @@ METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.
            "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio",
            "smsp__average_warps_issue_stalled_wait_per_issue_active.ratio",
            "smsp__average_warps_issue_stalled_math_pipe_throttle_per_issue_active.ratio",
-           "smsp__average_warp_latency_per_inst_issued.ratio", "smsp__thread_inst_executed_per_inst_executed.ratio"]
+           "smsp__average_warp_latency_per_inst_issued.ratio", "smsp__thread_inst_executed_per_inst_executed.ratio",
+           "sm__warps_active.avg.per_cycle_active", "smsp__warps_active.avg.per_cycle_active",
+           "smsp__average_warps_issue_stalled_not_selected_per_issue_active.ratio",
+           "smsp__average_warps_issue_stalled_sleeping_per_issue_active.ratio", "lts__t_sector_hit_rate.pct"]
 
 shutil.copy("gpurun_out/launches.csv", f"profiles/{tag}_launches.csv")
 rows = list(csv.reader(open("gpurun_out/launches.csv")))
