@@ -22,6 +22,8 @@
 #include <cstdlib>
 
 #include "glibc_pow_dev.cuh"
+#include <type_traits>
+
 #include "internal.h"
 #include "problems.cuh"
 
@@ -350,6 +352,12 @@ struct PairCtx {
     uint32_t cross;  // pair-level crossover switch hc = H(r3 - pc) == 0 (operators.hpp:82)
     uint32_t pad;
 };
+#ifndef TEMO_PAIR_SLEEP
+#define TEMO_PAIR_SLEEP 200                                  // ns between two polls of a pair slot that is still in use
+#endif
+#ifndef TEMO_PAIR_PINGPONG
+#define TEMO_PAIR_PINGPONG 1                                 // pass C: two alternating register sets (1) or the rotating three-set loop (0)
+#endif
 #ifndef TEMO_PAIR_STAGE
 #define TEMO_PAIR_STAGE 0                                    // 1: the tile's parent blocks are staged in shared memory by LDGSTS at the tile start
 #endif
@@ -586,7 +594,7 @@ __device__ __noinline__ void tile_plain(const ReproK& a, uint32_t blk0, uint32_t
     acc[0] = acc_a, acc[1] = acc_b;
 }
 
-template <int MODE, int EVAL, bool SEG>
+template <int MODE, int EVAL, int SEG>  // SEG: 0 bound arrays, 1 one constant segment, 2 two constant segments
 __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reproduce_pairs_kernel(const __grid_constant__ ReproK a) {
     extern __shared__ __align__(16) unsigned char pair_smem_raw[];
     PairSmem& S = *reinterpret_cast<PairSmem*>(pair_smem_raw);
@@ -631,7 +639,7 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
             W.ctx.cross = !(word_to_unit(draw_word<MODE>(a.rng, a.c_r3 + g_unit)) - a.pc >= 0.0) ? 1u : 0u;
             // the slot is free once the pair that used it kPairSlots turns ago has been written out
             if (EVAL != 0) {
-                while (*reinterpret_cast<volatile uint32_t*>(&slot.done) < turn / kPairSlots) __nanosleep(200);
+                while (*reinterpret_cast<volatile uint32_t*>(&slot.done) < turn / kPairSlots) __nanosleep(TEMO_PAIR_SLEEP);
             }
         }
         __syncwarp();
@@ -778,10 +786,80 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
                 // piecewise-constant bounds from the launch constants (SEG): one side of the split for the whole tile,
                 // unless the tile's blocks straddle it
                 const uint32_t tile_g0 = (blk0 + v) * 64, tile_g1 = (blk0 + v + (kmax - 1) * kVirtWarps) * 64 + 64;
-                const bool seg_hi_side = tile_g0 >= a.seg_split, seg_mixed = SEG && !seg_hi_side && tile_g1 > a.seg_split;
+                const bool seg_hi_side = tile_g0 >= a.seg_split, seg_mixed = SEG != 0 && !seg_hi_side && tile_g1 > a.seg_split;
                 const double seg_lo = a.seg_lo[seg_hi_side ? 1 : 0], seg_hi = a.seg_hi[seg_hi_side ? 1 : 0];
                 const double2* __restrict__ pa2 = reinterpret_cast<const double2*>(W.ctx.pa);
                 const double2* __restrict__ pb2 = reinterpret_cast<const double2*>(W.ctx.pb);
+#if TEMO_PAIR_PINGPONG && !TEMO_PAIR_STAGE
+                constexpr bool kPingPong = true;
+#else
+                constexpr bool kPingPong = false;
+#endif
+                if constexpr (kPingPong) {
+                // Two register sets for the parents, used alternately by a loop unrolled by two: block k is blended out of
+                // set k & 1, and as soon as its children exist the same registers receive block k + 2 — two blocks are
+                // always in flight and no value is ever moved between registers (the rotating three-set form of the earlier
+                // kernel spent ~30 of its ~135 instructions per block on moves). One instance of the loop only: a second
+                // copy for the tile that holds the bounds split cost more in instruction fetch than the moves it saved
+                // (no_instruction stalls 0.2 -> 1.1 per issue), so two-segment bounds (SEG == 2) are selected per gene.
+                {
+                    uint32_t q = q_first, sm_b = sm_lane;
+                    const double2 zero2 = make_double2(0.0, 0.0);
+                    double2 a0 = q < nvec ? __ldcs(pa2 + q) : zero2, b0 = q < nvec ? __ldcs(pb2 + q) : zero2;
+                    double2 a1 = zero2, b1 = zero2;
+                    if (kmax > 1 && q + kVirtWarps * 32 < nvec) {
+                        a1 = __ldcs(pa2 + q + kVirtWarps * 32);
+                        b1 = __ldcs(pb2 + q + kVirtWarps * 32);
+                    }
+                    auto block = [&](uint32_t k, double2& pa_v, double2& pb_v) {
+                        double lo_x, lo_y, hi_x, hi_y;
+                        if (SEG == 1) {
+                            lo_x = lo_y = seg_lo, hi_x = hi_y = seg_hi;
+                        } else if (SEG == 2) {
+                            const bool sx = 2 * q >= a.seg_split, sy = 2 * q + 1 >= a.seg_split;
+                            lo_x = sx ? a.seg_lo[1] : a.seg_lo[0], lo_y = sy ? a.seg_lo[1] : a.seg_lo[0];
+                            hi_x = sx ? a.seg_hi[1] : a.seg_hi[0], hi_y = sy ? a.seg_hi[1] : a.seg_hi[0];
+                        } else {
+                            const double2 vlo = __ldg(lo2 + q), vhi = __ldg(hi2 + q);
+                            lo_x = vlo.x, lo_y = vlo.y, hi_x = vhi.x, hi_y = vhi.y;
+                        }
+                        const double2 vbeta = lds_f64x2(sm_b);
+                        double ca0, cb0, ca1, cb1;
+                        sbx_children(pa_v.x, pb_v.x, vbeta.x, lo_x, hi_x, ca0, cb0);
+                        sbx_children(pa_v.y, pb_v.y, vbeta.y, lo_y, hi_y, ca1, cb1);
+                        {   // the set is free: block k + 2 goes into it
+                            const uint32_t qf = q + 2 * kVirtWarps * 32;
+                            if (k + 2 < kmax && qf < nvec) {
+                                pa_v = __ldcs(pa2 + qf);
+                                pb_v = __ldcs(pb2 + qf);
+                            }
+                        }
+                        if (max(__double2hiint(vbeta.x), __double2hiint(vbeta.y)) >= (int)kBetaTagHi) {  // rare: parked children
+                            if (__double2hiint(vbeta.x) >= (int)kBetaTagHi) {
+                                const double2 ch = lds_f64x2(sm_w + kOffSide + 16 * __double2loint(vbeta.x));
+                                ca0 = ch.x;
+                                cb0 = ch.y;
+                            }
+                            if (__double2hiint(vbeta.y) >= (int)kBetaTagHi) {
+                                const double2 ch = lds_f64x2(sm_w + kOffSide + 16 * __double2loint(vbeta.y));
+                                ca1 = ch.x;
+                                cb1 = ch.y;
+                            }
+                        }
+                        accumulate_vector<EVAL>(2 * q, m1, ca0, cb0, ca1, cb1, acc_a, acc_b, slot.pos);
+                        __stcs(oa2 + q, make_double2(ca0, ca1));
+                        __stcs(ob2 + q, make_double2(cb0, cb1));
+                        q += kVirtWarps * 32;
+                        sm_b += 512;
+                    };
+                    for (uint32_t k = 0; k < kmax; k += 2) {
+                        if (q >= nvec) break;  // only in the last block of the row
+                        block(k, a0, b0);
+                        if (k + 1 >= kmax || q >= nvec) break;
+                        block(k + 1, a1, b1);
+                    }
+                }
+                } else {
 #if TEMO_PAIR_STAGE
                 uint32_t q = q_first, sm_b = sm_lane, sm_s = sm_w + (uint32_t)offsetof(WarpSmem, stage) + lane * 16;
                 asm volatile("cp.async.wait_all;" ::: "memory");
@@ -812,7 +890,7 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
                     }
 #endif
                     double2 vlo, vhi;
-                    if (SEG) {
+                    if (SEG != 0) {
                         if (seg_mixed) {  // this tile holds the split: per gene
                             const int sx = 2 * q >= a.seg_split, sy = 2 * q + 1 >= a.seg_split;
                             vlo = make_double2(a.seg_lo[sx], a.seg_lo[sy]);
@@ -844,6 +922,7 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
                     accumulate_vector<EVAL>(2 * q, m1, ca0, cb0, ca1, cb1, acc_a, acc_b, slot.pos);
                     __stcs(oa2 + q, make_double2(ca0, ca1));
                     __stcs(ob2 + q, make_double2(cb0, cb1));
+                }
                 }
             }
             __syncwarp();
@@ -939,7 +1018,7 @@ inline bool force_generic_kernel() { return k1_options().generic != 0; }
 inline bool no_bound_segments() { return k1_options().bound_arrays != 0; }
 inline int pair_cand_cap() { return k1_options().cand_cap; }
 
-template <int MODE, int EVAL, bool SEG>
+template <int MODE, int EVAL, int SEG>
 void launch_pairs_seg(const ReproK& k, uint64_t units, cudaStream_t s) {
     static int grid = 0;  // per instantiation
     if (grid == 0) {
@@ -967,15 +1046,16 @@ void launch_pairs_seg(const ReproK& k, uint64_t units, cudaStream_t s) {
 }
 
 template <int MODE, int EVAL>
-void launch_pairs_eval(const ReproK& k, uint64_t units, bool seg, cudaStream_t s) {
-    if (seg)
-        launch_pairs_seg<MODE, EVAL, true>(k, units, s);
-    else
-        launch_pairs_seg<MODE, EVAL, false>(k, units, s);
+void launch_pairs_eval(const ReproK& k, uint64_t units, int seg, cudaStream_t s) {
+    switch (seg) {
+    case 1: launch_pairs_seg<MODE, EVAL, 1>(k, units, s); break;
+    case 2: launch_pairs_seg<MODE, EVAL, 2>(k, units, s); break;
+    default: launch_pairs_seg<MODE, EVAL, 0>(k, units, s); break;
+    }
 }
 
 template <int MODE>
-void launch_pairs(const ReproK& k, uint64_t units, int eval, bool seg, cudaStream_t s) {
+void launch_pairs(const ReproK& k, uint64_t units, int eval, int seg, cudaStream_t s) {
     switch (eval) {
     case 0: launch_pairs_eval<MODE, 0>(k, units, seg, s); break;
     case kDtlz1: launch_pairs_eval<MODE, kDtlz1>(k, units, seg, s); break;
@@ -1134,10 +1214,15 @@ void launch_reproduce(const ReproArgs& a, cudaStream_t s) {
     if (a.do_sbx && a.do_pm && vec == 2 && block == 256 && unit_lo < std::min(unit_hi, k.half) && a.d * 8 < (1ULL << 32) &&
         cand_per_warp <= 1.0 && aligned16(a.pool) && aligned16(a.out) && aligned16(a.lower) && aligned16(a.upper) &&
         !force_generic_kernel()) {
-        const bool seg = a.seg.valid && a.seg.split <= a.d && !no_bound_segments();
-        if (seg) {
+        // bounds as launch constants: 0 arrays, 1 one constant segment (DTLZ), 2 two constant segments (LSMOP)
+        int seg = 0;
+        if (a.seg.valid && a.seg.split <= a.d && !no_bound_segments()) {
+            seg = a.seg.split == 0 || a.seg.split >= a.d ? 1 : 2;
             k.seg_split = (uint32_t)a.seg.split;
-            for (int i = 0; i < 2; ++i) k.seg_lo[i] = a.seg.lo[i], k.seg_hi[i] = a.seg.hi[i];
+            for (int i = 0; i < 2; ++i) {
+                const int from = seg == 1 ? (a.seg.split == 0 ? 1 : 0) : i;  // one segment: both entries hold it
+                k.seg_lo[i] = a.seg.lo[from], k.seg_hi[i] = a.seg.hi[from];
+            }
         }
         k.unit0 = unit_lo;
         k.unit_end = std::min(unit_hi, k.half);

@@ -287,7 +287,9 @@ __global__ void __launch_bounds__(kFilterThreads, 4) assoc_filter_kernel(
             // ascending j: vector jj first, then jj + 1 (the thresholds move in between)
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
-                const bool h0 = sc[u][0] >= thr[0], h1 = sc[u][1] >= thr[1];
+                // the phantom second vector of an odd tile end must not pass a disabled filter (thr = -inf: -inf >= -inf)
+                const bool real = u == 0 || second;
+                const bool h0 = real && sc[u][0] >= thr[0], h1 = real && sc[u][1] >= thr[1];
                 if (h0 | h1) {  // rare after the first few vectors: the reference's exact expression
                     const uint64_t j = j0 + jj + u;
 #pragma unroll
