@@ -273,7 +273,7 @@ def run_ours(args):
         "achieved": gbs(16.0 * nd, dom_ms), "peak": peak, "unit": "GB/s", "frac": gbs(16.0 * nd, dom_ms) / peak,
         # dram__bytes_read.sum + dram__bytes_write.sum of one launch, `ncu --set full` capture of this build at the
         # headline shape (profiles/r1c_ncu_top_kernels.csv); null for any other shape
-        "traffic": (5.683408e9 + 5.231592e9) if (n == 1 << 17 and d == 5000 and fused_ok) else None,
+        "traffic": (5.717772e9 + 5.230673e9) if (n == 1 << 17 and d == 5000 and fused_ok) else None,
         "traffic_source": "profiles/r1c_ncu_top_kernels.csv",
         "peak_source": peak_src, "algorithmic_bytes": 16.0 * nd, "ms": dom_ms,
         "share_of_step": dom_ms / float(np.mean(stage["generation"])),
