@@ -336,7 +336,9 @@ int temo_b200_flush_l2(void);
 /* Path-selection knobs for tests and A/B measurements (no reference counterpart; results are identical on every
  * path): "k1_generic" 0/1 routes reproduction through the generic kernel instead of the phased pair kernel;
  * "k1_bound_arrays" 0/1 makes the pair kernel read the bound arrays even when they are piecewise constant;
- * "k1_cand_cap" 0..8 sets its mutation-candidate slots per warp tile (0 forces the plain per-gene tile path).
+ * "k1_cand_cap" 0..8 sets its mutation-candidate slots per warp tile (0 forces the plain per-gene tile path);
+ * "k1_dynamic_pairs" 1/0 hands the mating pairs to the persistent teams through a global counter (default) or
+ * round-robin over the grid.
  * Returns TEMO_B200_EINVAL for an unknown name. */
 int temo_b200_set_option(const char* name, long value);
 

@@ -172,6 +172,7 @@ def k1_options(tb):
     tb.set_option("k1_generic", 0)
     tb.set_option("k1_bound_arrays", 0)
     tb.set_option("k1_cand_cap", 8)
+    tb.set_option("k1_dynamic_pairs", 1)
 
 
 @pytest.mark.parametrize("shape", [(16, 512), (12, 5120), (6, 5122), (6, 10240), (5, 20000), (9, 2002)])
@@ -240,6 +241,27 @@ def test_pair_kernel_runs_equal_generic_kernel_runs(tb, k1_options, problem):
     for pops, x, f in outs[1:]:
         assert pops == outs[0][0]
         assert np.array_equal(x, outs[0][1]) and np.array_equal(f, outs[0][2])
+
+
+@pytest.mark.parametrize("problem", ["dtlz2", "lsmop1"])
+def test_pair_hand_out_is_invisible(tb, oracle, k1_options, problem):
+    """Pairs handed out through the global counter (default) or round-robin over the grid: more pairs than teams, so
+    every team takes several turns and the ring of published pairs wraps; offspring against the oracle, whole
+    generations (fused sums through the per-pair slots where the problem allows it) against each other."""
+    n, d = 2048, 640   # 1024 pairs on 444 teams
+    lo, hi = oracle.problem_bounds(problem, d, 3)
+    x, _ = oracle.random_reproduce(n, d, 41, 0, lo, hi)
+    exp, _ = oracle.ga_reproduce(x, 9, 100, lo, hi)
+    outs = []
+    for dyn in (1, 0):
+        k1_options("k1_dynamic_pairs", dyn)
+        got = tb.ga_reproduce(x, tb.RngStream(9, 100), tb.GaParams(), lo, hi)
+        assert np.array_equal(got, exp), (dyn, ulp_diff(got, exp).max())
+        with tb.RveaRun(tb.RunConfig(problem=problem, pop=n, dim=d, obj=3, generations=3, seed=4)) as run:
+            pops = [run.step() for _ in range(3)]
+            out = run.download()
+        outs.append((pops, out["x"], out["f"]))
+    assert outs[0][0] == outs[1][0] and np.array_equal(outs[0][1], outs[1][1]) and np.array_equal(outs[0][2], outs[1][2])
 
 
 def test_lockstep_wide_rows(tb, oracle):
