@@ -352,6 +352,9 @@ struct PairCtx {
     uint32_t cross;  // pair-level crossover switch hc = H(r3 - pc) == 0 (operators.hpp:82)
     uint32_t pad;
 };
+#ifndef TEMO_PAIR_SETS
+#define TEMO_PAIR_SETS 3                                     // pass C: parent register sets = blocks in flight; 3 applies without fused sums only
+#endif
 #ifndef TEMO_PAIR_SLEEP
 #define TEMO_PAIR_SLEEP 200                                  // ns between two polls of a pair slot that is still in use
 #endif
@@ -811,6 +814,16 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
                         a1 = __ldcs(pa2 + q + kVirtWarps * 32);
                         b1 = __ldcs(pb2 + q + kVirtWarps * 32);
                     }
+                    // three sets (three blocks in flight) pay without the fused sums only: with them the larger loop body costs
+                    // more in instruction fetch than the extra block in flight saves (3.32 vs 3.05 ms)
+                    constexpr int kSets = (TEMO_PAIR_SETS == 3 && EVAL == 0) ? 3 : 2;
+                    double2 a2 = zero2, b2 = zero2;
+                    if constexpr (kSets == 3) {
+                        if (kmax > 2 && q + 2 * kVirtWarps * 32 < nvec) {
+                            a2 = __ldcs(pa2 + q + 2 * kVirtWarps * 32);
+                            b2 = __ldcs(pb2 + q + 2 * kVirtWarps * 32);
+                        }
+                    }
                     auto block = [&](uint32_t k, double2& pa_v, double2& pb_v) {
                         double lo_x, lo_y, hi_x, hi_y;
                         if (SEG == 1) {
@@ -827,9 +840,9 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
                         double ca0, cb0, ca1, cb1;
                         sbx_children(pa_v.x, pb_v.x, vbeta.x, lo_x, hi_x, ca0, cb0);
                         sbx_children(pa_v.y, pb_v.y, vbeta.y, lo_y, hi_y, ca1, cb1);
-                        {   // the set is free: block k + 2 goes into it
-                            const uint32_t qf = q + 2 * kVirtWarps * 32;
-                            if (k + 2 < kmax && qf < nvec) {
+                        {   // the set is free: block k + kSets goes into it
+                            const uint32_t qf = q + kSets * kVirtWarps * 32;
+                            if (k + kSets < kmax && qf < nvec) {
                                 pa_v = __ldcs(pa2 + qf);
                                 pb_v = __ldcs(pb2 + qf);
                             }
@@ -852,11 +865,15 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
                         q += kVirtWarps * 32;
                         sm_b += 512;
                     };
-                    for (uint32_t k = 0; k < kmax; k += 2) {
+                    for (uint32_t k = 0; k < kmax; k += kSets) {
                         if (q >= nvec) break;  // only in the last block of the row
                         block(k, a0, b0);
                         if (k + 1 >= kmax || q >= nvec) break;
                         block(k + 1, a1, b1);
+                        if constexpr (kSets == 3) {
+                            if (k + 2 >= kmax || q >= nvec) break;
+                            block(k + 2, a2, b2);
+                        }
                     }
                 }
                 } else {
