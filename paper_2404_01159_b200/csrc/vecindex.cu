@@ -360,7 +360,10 @@ __device__ __forceinline__ void search_row(const IndexView& ix, const Row<M>& ro
     *best_j = s.best_j;
 }
 
-constexpr int kWarpsPerCta = 4;
+#ifndef TEMO_INDEX_WARPS
+#define TEMO_INDEX_WARPS 4
+#endif
+constexpr int kWarpsPerCta = TEMO_INDEX_WARPS;
 
 // Association + APD for the merged objective rows (selection.hpp:148-192), one warp per row.
 template <int M>
