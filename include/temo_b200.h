@@ -272,6 +272,10 @@ int temo_b200_run_metrics(temo_b200_run* run, double* igd, double* hv);
  * this process; all launches go to the library stream. ------------------------------ */
 void* temo_b200_dev_alloc(size_t bytes);
 int temo_b200_dev_free(void* p);
+/* Page-locked host memory for buffers handed to the host-buffer entry points (e.g. the survivors_f of
+ * temo_b200_run_step): copies to and from it run at full PCIe rate. Plain malloc'ed buffers work everywhere too. */
+void* temo_b200_host_alloc(size_t bytes);
+int temo_b200_host_free(void* p);
 int temo_b200_dev_upload(void* dst, const void* src, size_t bytes);
 int temo_b200_dev_download(void* dst, const void* src, size_t bytes);
 int temo_b200_dev_sync(void);

@@ -107,6 +107,8 @@ SIGNATURES = {
     "temo_b200_rvea_run": (C.c_int, [_CFG, f64p, f64p, u64p, u64p, u64p, f64p]),
     "temo_b200_dev_alloc": (C.c_void_p, [C.c_size_t]),
     "temo_b200_dev_free": (C.c_int, [C.c_void_p]),
+    "temo_b200_host_alloc": (C.c_void_p, [C.c_size_t]),
+    "temo_b200_host_free": (C.c_int, [C.c_void_p]),
     "temo_b200_dev_upload": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t]),
     "temo_b200_dev_download": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t]),
     "temo_b200_dev_sync": (C.c_int, []),

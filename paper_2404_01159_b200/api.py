@@ -559,6 +559,29 @@ class RunRecord:
     final_f: np.ndarray
 
 
+class _PinnedBlock:
+    """Owner of one temo_b200_host_alloc block; freed when the last numpy view on it is gone."""
+
+    def __init__(self, ptr):
+        self.ptr = ptr
+
+    def __del__(self):
+        try:
+            _lib.load().temo_b200_host_free(C.c_void_p(self.ptr))
+        except Exception:
+            pass
+
+
+def _pinned_array(rows: int, cols: int) -> np.ndarray:
+    """rows x cols float64 in page-locked host memory (pageable numpy memory if the allocation fails)."""
+    ptr = _lib.load().temo_b200_host_alloc(rows * cols * 8)
+    if not ptr:
+        return np.empty((rows, cols))
+    buf = (C.c_double * (rows * cols)).from_address(ptr)
+    buf._owner = _PinnedBlock(ptr)  # the array's base keeps the block alive
+    return np.ctypeslib.as_array(buf).reshape(rows, cols)
+
+
 class RveaRun:
     """Device-resident generation loop (session form of rvea_run): create -> step()* -> download()."""
 
@@ -570,7 +593,9 @@ class RveaRun:
         self.cfg = cfg
         st = self.state()
         self.r, self.d, self.m, self.n = st["r"], st["d"], st["m"], cfg.pop
-        self._fbuf = np.empty((max(self.r, self.n), self.m))
+        # survivors' objectives land in page-locked memory (full-rate D2H); the views handed out are valid until close()
+        rows = max(self.r, self.n)
+        self._fbuf = _pinned_array(rows, self.m)
 
     def close(self):
         if self._h:

@@ -874,6 +874,19 @@ void* temo_b200_dev_alloc(size_t bytes) {
     return rc ? nullptr : p;
 }
 
+void* temo_b200_host_alloc(size_t bytes) {
+    void* p = nullptr;
+    const int rc = guarded([&] {
+        ctx();
+        TEMO_CUDA(cudaMallocHost(&p, bytes ? bytes : 1));
+    });
+    return rc ? nullptr : p;
+}
+
+int temo_b200_host_free(void* p) {
+    return guarded([&] { TEMO_CUDA(cudaFreeHost(p)); });
+}
+
 int temo_b200_dev_free(void* p) {
     return guarded([&] { TEMO_CUDA(cudaFree(p)); });
 }
