@@ -97,6 +97,7 @@ void launch_pso(const double* x, const double* scores, uint64_t n, uint64_t d, R
                 double c2, double* vel, double* pb_x, double* pb_score, uint32_t* best_scratch, const double* lower,
                 const double* upper, double* out, cudaStream_t s, const uint32_t* src = nullptr, const uint32_t* dst = nullptr);
 // cso_reproduce (operators.hpp:246-284) after the caller's shuffle_indices (n - 1 draws): draws 3 (n / 2) d from `counter`.
+// vel_out may be vel itself (in-place update: the winners' velocities are not rewritten).
 void launch_cso(const double* x, const double* scores, uint64_t n, uint64_t d, Rng rng, uint64_t counter, double phi,
                 const uint32_t* perm, double* mean_scratch, const double* vel, double* vel_out, const double* lower,
                 const double* upper, double* out, cudaStream_t s, const uint32_t* src = nullptr, const uint32_t* dst = nullptr);

@@ -139,7 +139,6 @@ Run::Run(const RunConfig& c) : cfg(c) {
             sw_pbs = dev_alloc<double>(n);
             sw_best = dev_alloc<uint32_t>(1);
         } else {
-            sw_vel[1] = dev_alloc<double>(n * d);
             sw_mean = dev_alloc<double>(d);
         }
     }
@@ -307,9 +306,8 @@ uint64_t Run::launch_other_operator(const Plan& p) {
         launches += 3;
         break;
     case kOpCso:
-        launch_cso(pool, scores, n, d, rng, p.c_sbx, cfg.cso_phi, perm_dev, sw_mean, sw_vel[sw_cur], sw_vel[sw_cur ^ 1], lower,
+        launch_cso(pool, scores, n, d, rng, p.c_sbx, cfg.cso_phi, perm_dev, sw_mean, sw_vel[0], sw_vel[0] /* in place: a row's velocity is touched by its own pair only */, lower,
                    upper, pool, stream, src, free_slot[cur]);
-        sw_cur ^= 1;
         launches += 2;
         break;
     default:  // random_reproduce (algorithms.hpp:266-267)

@@ -180,8 +180,8 @@ __global__ void __launch_bounds__(256) cso_kernel(const double* __restrict__ x, 
                                                    const uint32_t* __restrict__ dst, const double* __restrict__ scores, uint64_t n,
                                                    uint64_t pairs, uint64_t d, Rng rng, uint64_t c, double phi,
                                                    const uint32_t* __restrict__ perm, const double* __restrict__ mean,
-                                                   const double* __restrict__ vel, const double* __restrict__ lower,
-                                                   const double* __restrict__ upper, double* __restrict__ vel_out,
+                                                   const double* vel, const double* __restrict__ lower,
+                                                   const double* __restrict__ upper, double* vel_out,
                                                    double* __restrict__ out) {
     const uint64_t q = blockIdx.x;
     if (q >= pairs) {  // odd n: the last row of the shuffled order is nobody's partner
@@ -190,7 +190,7 @@ __global__ void __launch_bounds__(256) cso_kernel(const double* __restrict__ x, 
         double* orow = out + (dst ? (uint64_t)dst[r] : r) * d;
         for (uint64_t j = threadIdx.x; j < d; j += blockDim.x) {
             orow[j] = xr[j];
-            vel_out[r * d + j] = vel[r * d + j];
+            if (vel_out != vel) vel_out[r * d + j] = vel[r * d + j];
         }
         return;
     }
@@ -207,7 +207,7 @@ __global__ void __launch_bounds__(256) cso_kernel(const double* __restrict__ x, 
         vel_out[lose * d + j] = v;
         olose[j] = clampd(xl + v, lower[j], upper[j]);
         owin[j] = xw;
-        vel_out[win * d + j] = vel[win * d + j];
+        if (vel_out != vel) vel_out[win * d + j] = vel[win * d + j];  // in place (vel_out == vel): the winner's velocity stays
     }
 }
 
