@@ -683,6 +683,29 @@ def test_free_running_other_operators(tb, oracle, op):
     assert ((rec.final_x >= lo) & (rec.final_x <= hi)).all()
 
 
+@pytest.mark.parametrize("op", ["ga", "de", "pso", "cso", "random"])
+def test_operator_loops_philox_invariants(tb, oracle, op):
+    """Philox mode is not in the reference (parity unpinned): every operator loop is covered by invariants only —
+    draw counters follow the documented per-operator plan, survivors lie inside the bounds and F is the evaluation of X."""
+    n, d, m, gens = 256, 640, 3, 4
+    cfg = tb.RunConfig(problem="dtlz2", op=op, pop=n, dim=d, obj=m, generations=gens, seed=3, rng_mode=tb.RNG_PHILOX)
+    h = n // 2
+    per_op = {"ga": (n - 1) + 3 * h * d + h + 2 * n * d, "de": 4 * n + n * d, "pso": 2 * n * d, "cso": (n - 1) + 3 * h * d,
+              "random": n * d}[op]
+    with tb.RveaRun(cfg) as run:
+        c, P = n * d, n
+        for _ in range(gens):
+            pop, f = run.step(want_f=True)
+            c += (0 if P == n else n) + per_op
+            assert run.state()["counter"] == c, op
+            P = pop
+        out = run.download()
+    assert out["x"].shape == (P, d) and ((out["x"] >= 0.0) & (out["x"] <= 1.0)).all()
+    assert close_rel(out["f"], oracle.evaluate("dtlz2", out["x"], m), 1e-12)
+    assert np.array_equal(out["f"], f)                       # the page-locked result view of the last step
+    assert len(np.unique(out["x"], axis=0)) >= P // 2        # survivors are (mostly) distinct rows
+
+
 def test_unknown_operator_is_rejected(tb):
     with pytest.raises(ValueError, match="unknown operator"):
         tb.RveaRun(tb.RunConfig(op="sa"))
