@@ -282,6 +282,25 @@ class Oracle(_Base):
             raise ValueError(f"min_vector_angles rc={rc}")
         return g
 
+    def min_vector_angles_rows(self, v, rows, want_cos=False):
+        """gamma of the vectors `rows` against the full set (refvec.hpp:81-100 per sampled vector)."""
+        v = _f(v)
+        rows = np.ascontiguousarray(rows, dtype=np.uint64)
+        g, c = np.empty(rows.size), np.empty(rows.size)
+        rc = self.lib.to_min_vector_angles_rows(_p(v), u64(v.shape[0]), u64(v.shape[1]), _p(rows, u64p), u64(rows.size), _p(g), _p(c))
+        if rc:
+            raise ValueError(f"min_vector_angles_rows rc={rc}")
+        return (g, c) if want_cos else g
+
+    def adapt_vectors(self, v0, zmin, zmax):
+        """adapt_vectors (refvec.hpp:119-131) without the gamma recomputation."""
+        v0 = _f(v0)
+        v = v0.copy()
+        rc = self.lib.to_adapt_vectors(_p(v0), _p(v), u64(v0.shape[0]), u64(v0.shape[1]), _p(_f(zmin)), _p(_f(zmax)))
+        if rc < 0:
+            raise ValueError(f"adapt_vectors rc={rc}")
+        return v
+
     def make_ref_set(self, m, H):
         r = self.lattice_count(m, H)
         v0, g = np.empty((r, m)), np.empty(r)

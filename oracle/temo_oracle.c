@@ -507,6 +507,46 @@ int to_min_vector_angles(const double* v, uint64_t r, uint64_t m, double* gamma)
     return bad ? -1 : 0;
 }
 
+/* refvec.hpp:81-100 for a SAMPLE of vectors: gamma[q] of vector rows[q] against the full set (every j != rows[q],
+ * ascending j). The per-vector loop body is the one above; used where the full O(R^2) scan (or the reference's
+ * R x R matrix, 137 GB at R = 130816) is out of reach: the BASELINE-size parity tests. */
+int to_min_vector_angles_rows(const double* v, uint64_t r, uint64_t m, const uint64_t* rows, uint64_t n_rows,
+                              double* gamma, double* best_cos) {
+    if (r < 2) return -3;
+    double* norms = (double*)malloc(r * sizeof(double));
+    if (!norms) return -2;
+    to_row_norms(v, r, m, norms);
+    for (uint64_t q = 0; q < n_rows; ++q) {
+        const uint64_t i = rows[q];
+        if (i >= r) { free(norms); return -3; }
+        double best = -INFINITY;
+        for (uint64_t j = 0; j < r; ++j) {
+            if (j == i) continue;
+            double dot = 0.0;
+            for (uint64_t k = 0; k < m; ++k) dot += v[i * m + k] * v[j * m + k];
+            const double c = dot / (norms[i] * norms[j]);
+            if (c > best) best = c;
+        }
+        gamma[q] = to_acos_clamped(best);
+        if (best_cos) best_cos[q] = best;
+    }
+    free(norms);
+    return 0;
+}
+
+/* refvec.hpp:119-131 (adapt_vectors alone, no gamma): v = unit(v0 (*) (zmax - zmin)); returns 1 when skipped. */
+int to_adapt_vectors(const double* v0, double* v, uint64_t r, uint64_t m, const double* zmin, const double* zmax) {
+    for (uint64_t k = 0; k < m; ++k)
+        if (!(zmax[k] > zmin[k])) return 1;
+    double* scaled = (double*)malloc(r * m * sizeof(double));
+    if (!scaled) return -2;
+    for (uint64_t i = 0; i < r; ++i)
+        for (uint64_t k = 0; k < m; ++k) scaled[i * m + k] = v0[i * m + k] * (zmax[k] - zmin[k]);
+    int rc = to_normalize_to_unit(scaled, r, m, v);
+    free(scaled);
+    return rc;
+}
+
 /* refvec.hpp:108-114. v0 and v start identical. */
 int to_make_ref_set(uint64_t m, uint64_t H, double* v0, double* gamma) {
     const uint64_t r = to_lattice_count(m, H);

@@ -22,6 +22,15 @@ def pytest_configure(config):
 
 
 @pytest.fixture(scope="session")
+def tb():
+    """The product package bound to cuda:0 (GPU tests only; there is no CPU fallback)."""
+    import paper_2404_01159_b200 as tb
+    assert tb.device_count() >= 1, "GPU tests need a CUDA device"
+    tb.init(0)
+    return tb
+
+
+@pytest.fixture(scope="session")
 def oracle():
     from oracle.pyoracle import Oracle
     return Oracle()
