@@ -54,7 +54,49 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-fuse", action="store_true")
     ap.add_argument("--stage-reps", type=int, default=5)
+    ap.add_argument("--no-same-config", action="store_true", help="skip the measured CPU/GPU pair at --same-config-pop rows")
+    ap.add_argument("--same-config-pop", type=int, default=1 << 14)
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="N > 1: weak = N shards of --pop rows (one run of N*pop rows); strong = --pop rows in total")
     return ap.parse_args()
+
+
+def ncu_traffic(n, d, fused):
+    """dram__bytes_read.sum + dram__bytes_write.sum of one launch of the dominant kernel from the newest committed
+    `ncu --set full` summary (profiles/*_ncu_top_kernels.csv); only valid for the shape it was captured at."""
+    import csv
+    import glob
+    if not (n == 1 << 17 and d == 5000 and fused):
+        return None, None
+    unit_scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu_top_kernels.csv")), reverse=True):
+        try:
+            with open(path, newline="") as fh:
+                rows = list(csv.reader(fh))
+            head, units = rows[0], rows[1]
+            ir, iw = head.index("dram__bytes_read.sum"), head.index("dram__bytes_write.sum")
+            for row in rows[2:]:
+                if "reproduce_pairs_kernel" in row[0]:
+                    total = float(row[ir]) * unit_scale[units[ir]] + float(row[iw]) * unit_scale[units[iw]]
+                    return total, os.path.relpath(path, ROOT)
+        except (OSError, ValueError, KeyError, IndexError):
+            continue
+    return None, None
+
+
+def self_launch(args):
+    """`python bench.py --gpus N` without a launcher: re-exec under torchrun with N ranks on this node."""
+    import socket
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        sys.exit(f"bench.py --gpus {args.gpus}: only {have} CUDA device(s) visible (no CPU fallback, no oversubscription)")
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    os.execv(sys.executable, cmd)
 
 
 # ------------------------------------------------------------------------------ helpers
@@ -123,21 +165,26 @@ def dist_env():
 
 
 # ---------------------------------------------------------------- CPU reference arm
-def cpu_reference_sample(args, steps, warmup):
-    """Times the unmodified reference on a bounded sample and scales it to the full workload.
-
-    Sample: the reference's own rvea_run (all host threads, track_archive = false, GA) on the SAME
-    problem and decision dimension with pop' = --cpu-sample-pop rows (R' from the reference's lattice
-    rule), warmup + steps generations; per-generation wall time from RunRecord.elapsed_ms differences
-    (cmd_scale protocol, temo.cpp:229-237). Selection cost is measured separately on the sample
-    (rv_select on 2 pop' rows x R' vectors). Scaling to pop rows / R vectors: every stage except
-    selection is linear in rows at fixed d (x pop/pop'); association is rows x vectors
-    (x (pop/pop') * (R/R')). Adaptation generations are excluded from both (the reference would need
-    an R x R matrix of 137 GB at the full size, refvec.hpp:83)."""
+def _checker():
     from oracle.pyoracle import Oracle, Ref
     kind = "reference" if Ref.available() else "port"
     chk = Ref() if kind == "reference" else Oracle()
-    cores = chk.num_threads() if kind == "reference" else 1
+    return chk, kind, (chk.num_threads() if kind == "reference" else 1)
+
+
+def cpu_reference_sample(args, steps, warmup):
+    """Times the unmodified reference on a bounded sample of the workload: a slice of pop' rows.
+
+    The reference cannot run the full shape (its min_vector_angles forms an R x R matrix: 137 GB at R = 130816,
+    refvec.hpp:83), so every step is a ROW SLICE of it, and the only scaling applied is linear in rows (x pop/pop'):
+      (a) one generation of the reference's own rvea_run (all host threads, track_archive = false, GA) on the SAME
+          problem and decision dimension with pop' = --cpu-sample-pop rows; per-generation wall time from
+          RunRecord.elapsed_ms differences (cmd_scale protocol, temo.cpp:229-237), minus its own (small-R') selection;
+      (b) the reference's rv_select of 2 pop' merged rows against the FULL reference set (R vectors of the full
+          workload's lattice; gamma = 1, timing-neutral), i.e. exactly the slice's share of the full association.
+    Every stage of the loop body is linear in rows at fixed d and R, so full-shape ms = (a + b) * pop/pop'.
+    Adaptation generations are excluded (fr = 1: the only one falls on the extra last generation)."""
+    chk, kind, cores = _checker()
     m, d, n_full = args.obj, args.dim, args.pop
     n_s = min(args.cpu_sample_pop, n_full)
     h_full = chk.lattice_density_for(m, n_full)
@@ -153,45 +200,79 @@ def cpu_reference_sample(args, steps, warmup):
         t1 = time.time()
         chk.rvea_run(args.problem, n_s, d, m, gens, seed=args.seed, fr=1.0)
         per_gen = np.full(steps, (time.time() - t1) * 1e3 / gens)
-    # selection share on the sample: rv_select on 2 pop' rows x R' vectors
-    v0 = chk.normalize_to_unit(chk.simplex_lattice(m, h_s))
     fs = np.random.default_rng(1).random((2 * n_s, m)) + 0.1
-    sel_ms = []
-    for _ in range(3):
-        t1 = time.time()
-        chk.rv_select(fs, v0, np.ones(r_s), 1, 100, 2.0)
-        sel_ms.append((time.time() - t1) * 1e3)
-    sel = float(np.median(sel_ms))
+
+    def select_ms(h, r, reps):
+        v0 = chk.normalize_to_unit(chk.simplex_lattice(m, h))
+        out = []
+        for _ in range(reps):
+            t1 = time.time()
+            if kind == "reference":
+                chk.rv_select(fs, v0, np.ones(r), 1, 100, 2.0, want_core=False)  # as rvea_run calls it (algorithms.hpp:276-277)
+            else:
+                chk.rv_select(fs, v0, np.ones(r), 1, 100, 2.0)
+            out.append((time.time() - t1) * 1e3)
+        return float(np.median(out))
+
+    sel_small = select_ms(h_s, r_s, 3)            # what the sample run itself spent in selection
+    sel_full_r = select_ms(h_full, r_full, max(2, min(steps, 5))) if n_s < n_full else sel_small
     gen = float(np.median(per_gen))
     scale_rows = n_full / n_s
-    full_ms = max(gen - sel, 0.0) * scale_rows + sel * scale_rows * (r_full / r_s)
+    sample_ms = max(gen - sel_small, 0.0) + sel_full_r
+    full_ms = sample_ms * scale_rows
     return {
         "value": 1000.0 / full_ms, "unit": "generations/s", "cores": int(cores), "kind": kind,
-        "sample": (f"{args.problem} m={m} d={d} pop'={n_s} (R'={r_s}) x {len(per_gen)} generations after {warmup} warm-up: "
-                   f"median {gen:.1f} ms/gen of which rv_select {sel:.1f} ms; scaled to pop={n_full}, R={r_full}: "
-                   f"linear stages x{scale_rows:.0f}, association x{scale_rows * r_full / r_s:.0f} -> {full_ms / 1e3:.1f} s/gen"),
-        "sample_ms_per_gen": gen, "sample_select_ms": sel, "scaled_ms_per_gen": full_ms,
+        "extrapolated": bool(n_s < n_full), "scale_rows": scale_rows,
+        "sample": (f"row slice of the workload: {args.problem} m={m} d={d}, pop'={n_s} of {n_full} rows; reference rvea_run x "
+                   f"{len(per_gen)} generations after {warmup} warm-up: median {gen:.1f} ms/gen (of which its own R'={r_s} "
+                   f"selection {sel_small:.1f} ms, replaced by) rv_select of 2*pop' rows against the full R={r_full} set: "
+                   f"{sel_full_r:.1f} ms -> {sample_ms:.1f} ms per slice step, x{scale_rows:.0f} rows -> {full_ms / 1e3:.1f} s/gen"),
+        "sample_ms_per_step": sample_ms, "sample_gen_ms": gen, "sample_select_small_ms": sel_small,
+        "sample_select_full_r_ms": sel_full_r, "scaled_ms_per_gen": full_ms,
         "wall_s": time.time() - t0,
     }
+
+
+def cpu_same_config(args, pop, gens_timed=3):
+    """MEASURED (not scaled) CPU time of the unmodified reference rvea_run at a shape it can run: pop rows of the
+    same problem / dimension (R x R gamma matrix 2.2 GB at pop = 2^14). cmd_scale protocol (temo.cpp:229-282): median of
+    per-generation elapsed_ms differences, generation 0 (init) and the adaptation generation (last, fr = 1) excluded."""
+    chk, kind, cores = _checker()
+    if kind != "reference":
+        return None
+    gens = 1 + gens_timed + 1
+    t0 = time.time()
+    rec = chk.rvea_run(args.problem, pop, args.dim, args.obj, gens, seed=args.seed, fr=1.0, want_x=False)
+    per_gen = np.diff(np.concatenate([[0.0], rec["elapsed_ms"]]))[1:1 + gens_timed]
+    return {"pop": pop, "ref_vectors": int(chk.lattice_count(args.obj, chk.lattice_density_for(args.obj, pop))),
+            "cpu_ms_per_gen": float(np.median(per_gen)), "cpu_gens_timed": int(len(per_gen)), "cores": int(cores),
+            "kind": "reference rvea_run, unmodified, measured", "wall_s": time.time() - t0}
 
 
 def run_reference_arm(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    if world > 1:  # weak scaling: the N-GPU arm runs N shards of --pop rows = one population of N * pop rows
-        args.pop = args.pop * world
+    if world > 1 or args.gpus > 1:  # the N-GPU arm runs one population of N * pop rows (weak scaling)
+        args.pop = args.pop * max(world, args.gpus)
     base = cpu_reference_sample(args, args.steps, args.warmup)
-    base["value"] *= world  # unit: generations of one pop-row shard per second (see dist.bench_main)
     line = {
         "impl": "reference", "metric": METRIC, "value": base["value"], "unit": "generations/s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": base["scaled_ms_per_gen"],
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        # what was timed: one slice step; the full-shape figure is `scaled_ms_per_step` (rows only, see cpu_baseline.sample)
+        "ms_per_step": base["sample_ms_per_step"], "scaled_ms_per_step": base["scaled_ms_per_gen"],
+        "extrapolated": base["extrapolated"], "scale_rows": base["scale_rows"],
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_config(args, None),
-        "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample", "extrapolated")},
         "e2e": {"value": base["value"], "unit": "generations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
+    if not args.no_same_config:
+        try:
+            line["same_config_measured"] = cpu_same_config(args, args.same_config_pop)
+        except Exception as e:
+            line["same_config_measured"] = {"error": repr(e)}
     print(json.dumps(line), flush=True)
 
 
@@ -208,6 +289,10 @@ def workload_config(args, run):
 # ------------------------------------------------------------------------- our arm
 def run_ours(args):
     rank, world, local = dist_env()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        self_launch(args)  # does not return
+    if args.gpus != world and not (world == 1 and os.environ.get("TEMO_FORCE_DIST") == "1"):
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     import paper_2404_01159_b200 as tb
 
     if world > 1 or os.environ.get("TEMO_FORCE_DIST") == "1":  # the env switch exercises the N-GPU path on one GPU
@@ -268,13 +353,13 @@ def run_ours(args):
     nd = float(n) * d
     gbs = lambda nbytes, ms: nbytes / (ms * 1e-3) / 1e9
     dom_ms = float(np.mean(stage["reproduce"]))  # live, inside the timed region
+    traffic, traffic_src = ncu_traffic(n, d, fused_ok)
     roofline = {
         "bound": "hbm", "kernel": "reproduce_pairs_kernel (SBX+PM" + ("+fused DTLZ evaluation)" if fused_ok else ")"),
         "achieved": gbs(16.0 * nd, dom_ms), "peak": peak, "unit": "GB/s", "frac": gbs(16.0 * nd, dom_ms) / peak,
-        # dram__bytes_read.sum + dram__bytes_write.sum of one launch, `ncu --set full` capture of this build at the
-        # headline shape (profiles/r1c_ncu_top_kernels.csv); null for any other shape
-        "traffic": (5.717772e9 + 5.230673e9) if (n == 1 << 17 and d == 5000 and fused_ok) else None,
-        "traffic_source": "profiles/r1c_ncu_top_kernels.csv",
+        # dram__bytes_read.sum + dram__bytes_write.sum of one launch, read from the newest committed `ncu --set full`
+        # summary of this kernel at the headline shape; null for any other shape
+        "traffic": traffic, "traffic_source": traffic_src,
         "peak_source": peak_src, "algorithmic_bytes": 16.0 * nd, "ms": dom_ms,
         "share_of_step": dom_ms / float(np.mean(stage["generation"])),
     }
@@ -304,10 +389,34 @@ def run_ours(args):
     if not args.no_cpu_baseline:
         try:
             base = cpu_reference_sample(args, min(K, 8), 1)
-            line["cpu_baseline"] = {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            line["cpu_baseline"] = {k: base[k] for k in ("value", "unit", "cores", "kind", "sample", "extrapolated", "scale_rows",
+                                                          "sample_ms_per_step", "scaled_ms_per_gen")}
             line["speedup_vs_cpu_baseline"] = line["e2e"]["value"] / base["value"]
+            line["speedup_vs_cpu_baseline_extrapolated"] = base["extrapolated"]
         except Exception as e:  # the baseline is a reported extra; never lose the GPU line over it
             line["cpu_baseline"] = {"value": None, "unit": "generations/s", "cores": 0, "kind": "unavailable", "sample": repr(e)}
+        if not args.no_same_config and args.same_config_pop < args.pop:
+            # one pair where BOTH sides are measured at the same configuration: the unmodified reference can run this shape
+            try:
+                pair = cpu_same_config(args, args.same_config_pop)
+                if pair is not None:
+                    gens2 = 100
+                    cfg2 = tb.RunConfig(problem=args.problem, pop=args.same_config_pop, dim=args.dim, obj=args.obj,
+                                        generations=gens2, seed=args.seed, fuse_eval=not args.no_fuse)
+                    with tb.RveaRun(cfg2) as run2:
+                        for _ in range(3):
+                            run2.step()
+                        tb._lib.check(tb._lib.load().temo_b200_dev_sync())
+                        t2 = time.perf_counter()
+                        for _ in range(20):
+                            run2.step(want_f=True)  # host-buffer session call, like e2e
+                        tb._lib.check(tb._lib.load().temo_b200_dev_sync())
+                        pair["gpu_ms_per_gen"] = (time.perf_counter() - t2) / 20 * 1e3
+                    pair["speedup_measured"] = pair["cpu_ms_per_gen"] / pair["gpu_ms_per_gen"]
+                    pair["config"] = f"RVEA/{args.problem} m={args.obj} d={args.dim} pop={args.same_config_pop}"
+                    line["same_config_measured"] = pair
+            except Exception as e:
+                line["same_config_measured"] = {"error": repr(e)}
     print(json.dumps(line), flush=True)
 
 

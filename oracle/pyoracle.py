@@ -649,7 +649,8 @@ class Ref(_Base):
     def apd_penalty(self, m, t, t_max, alpha):
         return self.lib.ref_apd_penalty(m, t, t_max, alpha)
 
-    def rv_select(self, f, v, gamma, t, t_max, alpha=2.0, set_form=False):
+    def rv_select(self, f, v, gamma, t, t_max, alpha=2.0, set_form=False, want_core=True):
+        """want_core=False: rv_select alone, as rvea_run calls it (the per-row diagnostics cost a second rv_core pass)."""
         f, v, gamma = _f(f), _f(v), _f(gamma)
         n, m = f.shape
         r = v.shape[0]
@@ -658,6 +659,10 @@ class Ref(_Base):
         assoc = np.empty(n, dtype=np.uint64)
         theta, apd = np.empty(n), np.empty(n)
         ne = u64(0)
+        if not want_core and not set_form:
+            self._chk(self.lib.ref_rv_select(C.c_int(0), _p(f), u64(n), u64(m), _p(v), _p(gamma), u64(r), u64(t), u64(t_max),
+                                             C.c_double(alpha), _p(elite, u64p), C.byref(ne), _p(valid, u8p), None, None, None, None))
+            return Selection(elite[: ne.value].copy(), valid)
         self._chk(self.lib.ref_rv_select(C.c_int(1 if set_form else 0), _p(f), u64(n), u64(m), _p(v), _p(gamma),
                                          u64(r), u64(t), u64(t_max), C.c_double(alpha), _p(elite, u64p),
                                          C.byref(ne), _p(valid, u8p), _p(assoc, u64p), _p(theta), _p(apd), None))

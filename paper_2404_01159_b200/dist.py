@@ -258,8 +258,11 @@ class ShardedRvea:
         # pieces of the parent exchange (pipelined with reproduction); 1 = one exchange, then K1
         self.chunks = max(1, min(int(os.environ.get("TEMO_B200_EXCHANGE_CHUNKS", "4" if self.world > 1 else "1")),
                                  max(1, self.n_loc // 2)))
-        comm.all_gather(shard.f_gather, shard.f_off_loc)
-        shard.place_f(0, True)
+        # on the shard's stream like every stage: the collective's result is only ordered against the stream it was
+        # issued on, and place_f reads f_gather on the library's (non-blocking) stream
+        with shard.on_stream():
+            comm.all_gather(shard.f_gather, shard.f_off_loc)
+            shard.place_f(0, True)
         self.timers = {}
 
     def _tick(self, name, t0):

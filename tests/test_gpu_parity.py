@@ -676,9 +676,9 @@ def test_free_running_other_operators(tb, oracle, op):
     same = pops == exp
     agree = int(np.argmax(~same)) if not same.all() else len(pops)
     print(f"free-running {op}: survivor counts identical for the first {agree}/{gens} generations")
-    assert agree >= 3
-    if agree == gens:
-        assert np.array_equal(rec.final_x, g[f"{op}_a_x"]) and close_rel(rec.final_f, g[f"{op}_a_f"], 1e-12)
+    # observed on B200 (round 2): all four operators follow the recorded reference run to the final population
+    assert agree == gens
+    assert np.array_equal(rec.final_x, g[f"{op}_a_x"]) and close_rel(rec.final_f, g[f"{op}_a_f"], 1e-12)
     lo, hi = oracle.problem_bounds(problem, d, m)
     assert ((rec.final_x >= lo) & (rec.final_x <= hi)).all()
 
@@ -771,9 +771,9 @@ def test_nsga2_free_running(tb):
     assert rec.final_x.shape == g["r0_x"].shape and len(rec.rows) == 12
     assert ((rec.final_x >= 0.0) & (rec.final_x <= 1.0)).all()
     assert close_rel(rec.final_f, tb.evaluate("dtlz2", rec.final_x, 3), 1e-12)
-    if np.array_equal(rec.final_x, g["r0_x"]):
-        assert close_rel(rec.final_f, g["r0_f"], 1e-12)
-    assert abs(rec.final_f.sum(axis=1).mean() - g["r0_f"].sum(axis=1).mean()) <= 0.1 * g["r0_f"].sum(axis=1).mean()
+    # observed on B200 (round 2): the free-running device run ends on exactly the reference's final population
+    assert np.array_equal(rec.final_x, g["r0_x"])
+    assert close_rel(rec.final_f, g["r0_f"], 1e-12)
 
 
 # -------------------------------------------------------------------------- quality indicators (metrics.hpp)
@@ -882,10 +882,10 @@ def test_run_metrics_trajectory_against_reference_run(tb):
     pops = np.array([r.pop_size for r in rec.rows])
     same = pops == g["run_pop"]
     agree = int(np.argmax(~same)) if not same.all() else len(pops)
-    assert agree >= 3
+    assert agree == len(pops)  # observed on B200 (round 2): survivor counts identical for all 15 generations
     for t in range(agree):
-        assert abs(rec.rows[t].igd_value - g["run_igd"][t]) <= 1e-12 and abs(rec.rows[t].hv_value - g["run_hv"][t]) <= 5e-3, t
-    assert abs(rec.rows[-1].igd_value - g["run_igd"][-1]) <= 0.05
+        # IGD: square roots of ulp-different objectives (<= 1e-12); HV: an integer hit count, observed identical
+        assert abs(rec.rows[t].igd_value - g["run_igd"][t]) <= 1e-12 and rec.rows[t].hv_value == g["run_hv"][t], t
 
 
 def test_free_running_c1_against_reference_run(tb, checkers):
@@ -902,8 +902,15 @@ def test_free_running_c1_against_reference_run(tb, checkers):
     agree = int(np.argmax(~same)) if not same.all() else len(pops)
     print(f"free-running C1: survivor counts identical for the first {agree}/100 generations; "
           f"mean |dpop| {np.abs(pops.astype(float) - exp['pop_size']).mean():.2f}")
-    assert agree >= 5
-    assert np.abs(pops.astype(float) - exp["pop_size"]).mean() <= 8.0
+    # observed on B200 (round 2): identical survivor counts for all 100 generations; of the 103 final rows 83 are
+    # bit-identical and 20 are the ulp-level twin of the CPU's row (a child that copies its parent up to one rounding
+    # of the blend won or lost the APD tie the other way): max |dx| = 2.2e-16, max |df| = 1.6e-13
+    assert agree == 100
+    rows = int(exp["pop_size"][-1])
+    assert rec.final_x.shape[0] == rows
+    ex, ef = exp["x"][:rows], exp["f"][:rows]
+    assert int((rec.final_x == ex).all(axis=1).sum()) >= 80
+    assert np.abs(rec.final_x - ex).max() <= 4.5e-16 and np.abs(rec.final_f - ef).max() <= 1e-12
     # convergence quality: the sum of objectives on DTLZ1's front tends to 0.5 for both
     assert abs(np.median(rec.final_f.sum(axis=1)) - np.median(exp["f"].sum(axis=1))) <= 0.25 * np.median(exp["f"].sum(axis=1))
 
