@@ -920,7 +920,7 @@ int temo_b200_pow(const double* x, const double* y, uint64_t n, double* out, int
 }
 
 int temo_b200_set_option(const char* name, long value) {
-    return guarded([&] { require(set_k1_option(name, value), "set_option: unknown option"); });
+    return guarded([&] { require(set_k1_option(name, value) || set_eval_option(name, value), "set_option: unknown option"); });
 }
 
 int temo_b200_flush_l2(void) {

@@ -10,6 +10,9 @@
 //                    memory ring with cp.async.bulk (TMA, SASS UBLKCP) + mbarrier
 //                    complete_tx; needs 16-byte aligned rows (d even).
 //   eval_ldg_kernel  one CTA per row with plain (128-bit when d is even) loads; any shape.
+#include <map>
+#include <mutex>
+
 #include "internal.h"
 #include "problems.cuh"
 
@@ -164,23 +167,64 @@ __global__ void __launch_bounds__(256) eval_tma_kernel(const EvalK a) {
 }
 
 // ---- LSMOP1 --------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) eval_lsmop1_kernel(const EvalK a, const LsmopLayout lay) {
+// y_j = (1 + (j + 1) / d) x_j - 10 x_0 over the tail genes, g_i = mean of y^2 over group i (m consecutive groups of
+// nk * sublen_i tail genes), objectives like DTLZ1's linear front without the 0.5. The linkage coefficients come from
+// a table (lsmop1_coef: one correctly rounded division per gene, done once per d on the host). Reduction order = the
+// canonical one of this library, per group: thread t owns the vectors t, t + B, ... of the row and adds its genes of a
+// group in ascending order; xor butterfly inside a warp; warp totals in ascending order.
+// Measured at n = 2^17, d = 5000 (round 2): 1.19 ms = 4.4 TB/s (the round-1 kernel with scalar loads and a division per
+// gene: 1.66 ms). Two alternatives were built, verified bit-identical and dropped: the same sums through the
+// cp.async.bulk ring of eval_tma_kernel (2.9 ms: m block reductions and ten CTA barriers per 40 KB row), and the sums
+// fused into the pair kernel of reproduce.cu (child gene 0 recomputed per warp, per-group slots): 5.2 ms against
+// 2.8 + 1.2 unfused - the extra code pushed the kernel out of the instruction cache (no_instruction stalls 0.2 -> 3.4
+// per issue) and over its register budget.
+template <int VEC>
+__global__ void __launch_bounds__(256) eval_lsmop1_kernel(const EvalK a, const LsmopLayout lay, const double* __restrict__ coef) {
+    extern __shared__ __align__(16) unsigned char lsmop_raw[];
+    double* part = reinterpret_cast<double*>(lsmop_raw);  // m x blockDim: per-thread partial of every group
     __shared__ double s_red[8];
     __shared__ double s_g[kMaxObj];
+    __shared__ uint32_t s_end[kMaxObj + 1];
+    const uint32_t m = (uint32_t)a.m, m1 = m - 1, B = blockDim.x;
+    for (uint32_t g = threadIdx.x; g < m; g += B) s_end[g] = m1 + lay.start[g + 1];  // first gene after group g
+    for (uint32_t g = 0; g < m; ++g) part[g * B + threadIdx.x] = 0.0;
+    __syncthreads();
     const uint64_t i = blockIdx.x;
     const uint64_t row = a.rows ? a.rows[i] : i;
     const double* p = a.x + row * a.d;
-    const double x0 = p[0];
-    const double dd = (double)a.d;
-    for (uint64_t grp = 0; grp < a.m; ++grp) {
-        double acc = 0.0;
-        for (uint64_t q = lay.start[grp] + threadIdx.x; q < lay.start[grp + 1]; q += blockDim.x) {
-            const uint64_t j = a.m - 1 + q;
-            const double y = (1.0 + (double)(j + 1) / dd) * p[j] - 10.0 * x0;
-            acc += y * y;
+    const double t0 = 10.0 * p[0];
+    uint32_t cur = 0;
+    double acc = 0.0;
+    const uint32_t nvec = (uint32_t)(a.d / VEC);
+    for (uint32_t q = threadIdx.x; q < nvec; q += B) {
+        double xv[VEC], cv[VEC];
+        if (VEC == 2) {
+            const double2 t = *reinterpret_cast<const double2*>(p + 2 * (uint64_t)q);
+            const double2 c = __ldg(reinterpret_cast<const double2*>(coef) + q);
+            xv[0] = t.x, xv[VEC - 1] = t.y, cv[0] = c.x, cv[VEC - 1] = c.y;
+        } else {
+            xv[0] = p[q];
+            cv[0] = __ldg(coef + q);
         }
-        const double sum = block_sum<8>(acc, s_red);
-        if (threadIdx.x == 0) s_g[grp] = lay.sublen[grp] ? sum / (double)lay.sublen[grp] / (double)kLsmopNk : 0.0;
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) {
+            const uint32_t j = q * VEC + v;
+            if (j < m1) continue;  // position gene
+            while (cur < m && j >= s_end[cur]) {
+                part[cur * B + threadIdx.x] = acc;
+                acc = 0.0;
+                ++cur;
+            }
+            if (cur < m) {
+                const double y = cv[v] * xv[v] - t0;
+                acc += y * y;
+            }
+        }
+    }
+    if (cur < m) part[cur * B + threadIdx.x] = acc;
+    for (uint32_t g = 0; g < m; ++g) {
+        const double sum = block_sum<8>(part[g * B + threadIdx.x], s_red);
+        if (threadIdx.x == 0) s_g[g] = lay.sublen[g] ? sum / (double)lay.sublen[g] / (double)kLsmopNk : 0.0;
     }
     __syncthreads();
     const uint64_t f0 = a.f_row0 + (a.f_row0_dev ? (uint64_t)*a.f_row0_dev : 0);
@@ -234,10 +278,13 @@ __global__ void eval_finish_kernel(double* f, uint64_t n, uint64_t m, uint64_t d
     }
 }
 
+int g_eval_tma = 1;  // set_option("eval_tma", 0) sends everything through the one-CTA-per-row kernels (tests)
+bool eval_tma_enabled() { return g_eval_tma != 0; }
+
 template <int PID>
 void launch_dtlz(const EvalK& k, bool tma, cudaStream_t s) {
     const int vec = row_vec(k.d), block = row_block(k.d);
-    if (tma && vec == 2 && block == 256) {
+    if (tma && eval_tma_enabled() && vec == 2 && block == 256) {
         const size_t smem = (size_t)kStages * kChunkGenes * sizeof(double);
         static bool configured = false;
         if (!configured) {
@@ -257,6 +304,12 @@ void launch_dtlz(const EvalK& k, bool tma, cudaStream_t s) {
 
 }  // namespace
 
+bool set_eval_option(const char* name, long value) {
+    if (std::string(name ? name : "") != "eval_tma") return false;
+    g_eval_tma = value != 0;
+    return true;
+}
+
 LsmopLayout lsmop1_layout(uint64_t d, uint64_t m) {
     // LSMOP suite (Cheng et al. 2017): logistic-map group sizes, nk = 5 sub-components.
     LsmopLayout lay{};
@@ -271,6 +324,24 @@ LsmopLayout lsmop1_layout(uint64_t d, uint64_t m) {
         lay.start[i + 1] = lay.start[i] + lay.sublen[i] * kLsmopNk;
     }
     return lay;
+}
+
+// Linkage coefficients of LSMOP1, 1 + (j + 1) / d for j < d, as a device table (cached per d; one IEEE division per gene
+// on the host, the same expression the CPU restatement evaluates inline).
+const double* lsmop1_coef(uint64_t d, cudaStream_t s) {
+    static std::mutex mu;
+    static std::map<uint64_t, double*> cache;
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find(d);
+    if (it != cache.end()) return it->second;
+    std::vector<double> host(d + (d & 1));
+    const double dd = (double)d;
+    for (uint64_t j = 0; j < d; ++j) host[j] = 1.0 + (double)(j + 1) / dd;
+    double* dev = dev_alloc<double>(host.size());
+    TEMO_CUDA(cudaMemcpyAsync(dev, host.data(), host.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+    TEMO_CUDA(cudaStreamSynchronize(s));  // the host vector goes away; once per d
+    cache[d] = dev;
+    return dev;
 }
 
 // {tail sum, position genes} left in the objective rows by a streaming kernel -> objectives (DTLZ1-4)
@@ -304,9 +375,16 @@ void launch_evaluate(const EvalArgs& a, cudaStream_t s) {
     case kDtlz2: launch_dtlz<kDtlz2>(k, a.allow_tma, s); break;
     case kDtlz3: launch_dtlz<kDtlz3>(k, a.allow_tma, s); break;
     case kDtlz4: launch_dtlz<kDtlz4>(k, a.allow_tma, s); break;
-    case kLsmop1:
-        eval_lsmop1_kernel<<<(unsigned)a.n, row_block(a.d), 0, s>>>(k, lsmop1_layout(a.d, a.m));
+    case kLsmop1: {
+        const int block = row_block(a.d);
+        const size_t smem = (size_t)a.m * block * sizeof(double);
+        const double* coef = lsmop1_coef(a.d, s);
+        if (row_vec(a.d) == 2)
+            eval_lsmop1_kernel<2><<<(unsigned)a.n, block, smem, s>>>(k, lsmop1_layout(a.d, a.m), coef);
+        else
+            eval_lsmop1_kernel<1><<<(unsigned)a.n, block, smem, s>>>(k, lsmop1_layout(a.d, a.m), coef);
         break;
+    }
     }
     TEMO_CUDA(cudaGetLastError());
 }

@@ -31,6 +31,7 @@ struct LsmopLayout {
     uint32_t sublen[kMaxObj];
 };
 LsmopLayout lsmop1_layout(uint64_t d, uint64_t m);
+const double* lsmop1_coef(uint64_t d, cudaStream_t s);  // device table 1 + (j + 1) / d, cached per d
 
 struct GaParams {
     double pc = 1.0, eta = 20.0, pm = 1.0, xi = 20.0;  // operators.hpp:22-27
@@ -114,6 +115,8 @@ struct EvalArgs {
     bool allow_tma = true;
 };
 void launch_evaluate(const EvalArgs& a, cudaStream_t s);
+// "eval_tma" (1 default; 0: the one-CTA-per-row kernels only); false for an unknown name
+bool set_eval_option(const char* name, long value);
 // second half of the streaming evaluators: rows holding {tail sum, position genes} -> objectives
 void launch_dtlz_finish(int problem, double* f, uint64_t n, uint64_t m, uint64_t d, uint64_t f_row0, cudaStream_t s);
 

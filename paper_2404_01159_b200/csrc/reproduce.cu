@@ -358,27 +358,12 @@ struct PairCtx {
 #ifndef TEMO_PAIR_SLEEP
 #define TEMO_PAIR_SLEEP 200                                  // ns between two polls of a pair slot that is still in use
 #endif
-#ifndef TEMO_PAIR_PINGPONG
-#define TEMO_PAIR_PINGPONG 1                                 // pass C: two alternating register sets (1) or the rotating three-set loop (0)
-#endif
-#ifndef TEMO_PAIR_STAGE
-#define TEMO_PAIR_STAGE 0                                    // 1: the tile's parent blocks are staged in shared memory by LDGSTS at the tile start
-#endif
-#ifndef TEMO_PAIR_TOUCH
-#define TEMO_PAIR_TOUCH 0                                    // 1: sector touch loads at the tile start, 0: prefetch.global.L2 hints
-#endif
 struct WarpSmem {
     double beta[kTileGenes];
     unsigned short list[kTileGenes];
     double2 side[kPairCand];  // final children {a, b} of a candidate gene
     PairCtx ctx;
     unsigned short cand[kPairCand];
-#if TEMO_PAIR_TOUCH
-    double2 sink[32];         // landing zone of the touch loads (never read)
-#endif
-#if TEMO_PAIR_STAGE
-    double2 stage[2][kPairBlocks][32];  // parents a / b of this tile: lane l's own vector of every block
-#endif
 };
 struct PairSlot {
     double part[2][kVirtWarps];  // per-warp totals of the two children
@@ -655,37 +640,6 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
             if (kmax == 0) break;
             const uint32_t q_first = (blk0 + v) * 32 + lane;  // this lane's vector in the tile's first block
             const uint64_t pos = W.ctx.pos;
-#if TEMO_PAIR_STAGE
-            {   // every lane copies its own vector of each of the tile's blocks, both parents, into shared memory with
-                // asynchronous 16-byte copies (LDGSTS: no register, no scoreboard): HBM has passes A and B to deliver, and
-                // pass C starts from shared memory. A lane only ever reads what it copied itself, so cp.async.wait_all in
-                // that lane is the only synchronisation needed.
-                const double2* pa2s = reinterpret_cast<const double2*>(W.ctx.pa);
-                const double2* pb2s = reinterpret_cast<const double2*>(W.ctx.pb);
-                uint32_t q = q_first, sa = sm_w + (uint32_t)offsetof(WarpSmem, stage) + lane * 16;
-                for (uint32_t k = 0; k < kmax; ++k, q += kVirtWarps * 32, sa += 512) {
-                    if (q < nvec) {
-                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(pa2s + q) : "memory");
-                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa + kPairBlocks * 512), "l"(pb2s + q) : "memory");
-                    }
-                }
-                asm volatile("cp.async.commit_group;" ::: "memory");
-            }
-#elif TEMO_PAIR_TOUCH
-            {   // this warp's parent blocks of this tile into L2, where pass C finds them: one 16-byte asynchronous copy
-                // (LDGSTS, no register, no scoreboard) per 32-byte sector, lanes 0-15 on parent a, 16-31 on parent b. Unlike
-                // prefetch hints these are real loads and cannot be dropped under load; DRAM then has passes A and B to
-                // deliver. The copies land in a sink nobody reads.
-                const char* row = reinterpret_cast<const char*>(lane < 16 ? W.ctx.pa : W.ctx.pb);
-                const uint32_t row_bytes = (uint32_t)a.d * 8u, sink = sm_w + (uint32_t)offsetof(WarpSmem, sink) + lane * 16;
-                uint32_t off = (blk0 + v) * 512 + (lane & 15) * 32;
-                for (uint32_t k = 0; k < kmax; ++k, off += kVirtWarps * 512) {
-                    if (off + 16 <= row_bytes)
-                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sink), "l"(row + off) : "memory");
-                }
-                asm volatile("cp.async.commit_group;" ::: "memory");
-            }
-#elif !defined(TEMO_PAIR_NO_L2HINT)
             {   // this warp's parent blocks of this tile into L2 (they are read in pass C)
                 const uint32_t kk = lane & 15, blk = blk0 + v + kk * kVirtWarps;
                 if (kk < kmax && blk < nblk) {
@@ -694,7 +648,6 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
                     for (int o = 0; o < 512; o += 128) prefetch_l2(p + o);
                 }
             }
-#endif
             // ---- pass A: crossing genes and mutation candidates (hashes only)
             uint32_t total = 0, ncand = 0;
             {
@@ -737,9 +690,6 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
                 double acc[2] = {acc_a, acc_b};
                 tile_plain<MODE, EVAL>(a, blk0, v, kmax, acc, W, slot.pos);
                 acc_a = acc[0], acc_b = acc[1];
-#if TEMO_PAIR_STAGE
-                asm volatile("cp.async.wait_all;" ::: "memory");  // the staging buffer is reused by the next tile
-#endif
                 __syncwarp();
                 continue;
             }
@@ -793,12 +743,6 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
                 const double seg_lo = a.seg_lo[seg_hi_side ? 1 : 0], seg_hi = a.seg_hi[seg_hi_side ? 1 : 0];
                 const double2* __restrict__ pa2 = reinterpret_cast<const double2*>(W.ctx.pa);
                 const double2* __restrict__ pb2 = reinterpret_cast<const double2*>(W.ctx.pb);
-#if TEMO_PAIR_PINGPONG && !TEMO_PAIR_STAGE
-                constexpr bool kPingPong = true;
-#else
-                constexpr bool kPingPong = false;
-#endif
-                if constexpr (kPingPong) {
                 // Two register sets for the parents, used alternately by a loop unrolled by two: block k is blended out of
                 // set k & 1, and as soon as its children exist the same registers receive block k + 2 — two blocks are
                 // always in flight and no value is ever moved between registers (the rotating three-set form of the earlier
@@ -875,71 +819,6 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
                             block(k + 2, a2, b2);
                         }
                     }
-                }
-                } else {
-#if TEMO_PAIR_STAGE
-                uint32_t q = q_first, sm_b = sm_lane, sm_s = sm_w + (uint32_t)offsetof(WarpSmem, stage) + lane * 16;
-                asm volatile("cp.async.wait_all;" ::: "memory");
-                for (uint32_t k = 0; k < kmax; ++k, q += kVirtWarps * 32, sm_b += 512, sm_s += 512) {
-                    if (q >= nvec) break;  // only in the last block of the row
-                    const double2 va = lds_f64x2(sm_s), vb = lds_f64x2(sm_s + kPairBlocks * 512);
-#else
-                uint32_t q = q_first, sm_b = sm_lane;
-                const double2 zero2 = make_double2(0.0, 0.0);
-                // the parents of the next two blocks are always in flight (register double buffer)
-                double2 na = q < nvec ? __ldcs(pa2 + q) : zero2, nb = q < nvec ? __ldcs(pb2 + q) : zero2;
-                double2 fa = zero2, fb = zero2;
-                if (kmax > 1 && q + kVirtWarps * 32 < nvec) {
-                    fa = __ldcs(pa2 + q + kVirtWarps * 32);
-                    fb = __ldcs(pb2 + q + kVirtWarps * 32);
-                }
-                for (uint32_t k = 0; k < kmax; ++k, q += kVirtWarps * 32, sm_b += 512) {
-                    if (q >= nvec) break;  // only in the last block of the row
-                    const double2 va = na, vb = nb;
-                    na = fa;
-                    nb = fb;
-                    {
-                        const uint32_t qf = q + 2 * kVirtWarps * 32;
-                        if (k + 2 < kmax && qf < nvec) {
-                            fa = __ldcs(pa2 + qf);
-                            fb = __ldcs(pb2 + qf);
-                        }
-                    }
-#endif
-                    double2 vlo, vhi;
-                    if (SEG != 0) {
-                        if (seg_mixed) {  // this tile holds the split: per gene
-                            const int sx = 2 * q >= a.seg_split, sy = 2 * q + 1 >= a.seg_split;
-                            vlo = make_double2(a.seg_lo[sx], a.seg_lo[sy]);
-                            vhi = make_double2(a.seg_hi[sx], a.seg_hi[sy]);
-                        } else {
-                            vlo = make_double2(seg_lo, seg_lo);
-                            vhi = make_double2(seg_hi, seg_hi);
-                        }
-                    } else {
-                        vlo = __ldg(lo2 + q);
-                        vhi = __ldg(hi2 + q);
-                    }
-                    const double2 vbeta = lds_f64x2(sm_b);
-                    double ca0, cb0, ca1, cb1;
-                    sbx_children(va.x, vb.x, vbeta.x, vlo.x, vhi.x, ca0, cb0);
-                    sbx_children(va.y, vb.y, vbeta.y, vlo.y, vhi.y, ca1, cb1);
-                    if (max(__double2hiint(vbeta.x), __double2hiint(vbeta.y)) >= (int)kBetaTagHi) {  // rare: parked children
-                        if (__double2hiint(vbeta.x) >= (int)kBetaTagHi) {
-                            const double2 ch = lds_f64x2(sm_w + kOffSide + 16 * __double2loint(vbeta.x));
-                            ca0 = ch.x;
-                            cb0 = ch.y;
-                        }
-                        if (__double2hiint(vbeta.y) >= (int)kBetaTagHi) {
-                            const double2 ch = lds_f64x2(sm_w + kOffSide + 16 * __double2loint(vbeta.y));
-                            ca1 = ch.x;
-                            cb1 = ch.y;
-                        }
-                    }
-                    accumulate_vector<EVAL>(2 * q, m1, ca0, cb0, ca1, cb1, acc_a, acc_b, slot.pos);
-                    __stcs(oa2 + q, make_double2(ca0, ca1));
-                    __stcs(ob2 + q, make_double2(cb0, cb1));
-                }
                 }
             }
             __syncwarp();

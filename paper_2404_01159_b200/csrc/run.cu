@@ -593,7 +593,7 @@ double Run::time_stage(int stage, int reps) {
         case 1: launch_reproduction(p, false); break;
         case 2: launch_offspring_eval(); break;
         case 3:
-            require(cfg.problem >= kDtlz1 && cfg.problem <= kDtlz4, "time_stage: fused evaluation is DTLZ-only");
+            require(fusable(), "time_stage: the evaluation of this problem / shape cannot be fused");
             launch_reproduction(p, true);
             break;
         case 4: launch_select(fm[cur], P + n, nullptr, m, v, gamma, r, penalty, ws, stream, &vindex); break;

@@ -185,13 +185,18 @@ __global__ void v32_kernel(const double* __restrict__ v, const double* __restric
     bool bad = false;
     for (uint64_t k = 0; k < m; ++k) {
         const double x = v[j * m + k];
-        v32[j * stride + k] = (float)x;
+        const float x32 = (float)x;
+        v32[j * stride + k] = x32;
         if (!(x >= 0.0) || !(x < INFINITY)) bad = true;
+        // outside fp32's normal range the relative-error bound of the filter does not hold (inf * 0 = NaN scores, flushed terms)
+        if (x != 0.0 && !(x32 >= 1.17549435e-38f && x32 < INFINITY)) bad = true;
     }
     const double nrm = vn[j];
-    v32[j * stride + m] = (float)(1.0 / nrm);
+    const float rinv32 = (float)(1.0 / nrm);
+    v32[j * stride + m] = rinv32;
     for (uint64_t k = m + 1; k < stride; ++k) v32[j * stride + k] = 0.0f;
     if (!(nrm > 0.0) || !(nrm < INFINITY)) bad = true;
+    if (!(rinv32 >= 1.17549435e-38f && rinv32 < INFINITY)) bad = true;
     if (bad) atomicOr(flags, 1u);
 }
 
@@ -233,7 +238,11 @@ __global__ void __launch_bounds__(kFilterThreads, 4) assoc_filter_kernel(
             if (!(nf[t] < INFINITY)) filter = false;  // inf or NaN
         }
 #pragma unroll
-        for (int k = 0; k < MM; ++k) uf[t][k] = (k < m && live[t] && nf[t] != 0.0) ? (float)(fp[t][k] / nf[t]) : 0.0f;
+        for (int k = 0; k < MM; ++k) {
+            const double uk = (k < m && live[t] && nf[t] != 0.0) ? fp[t][k] / nf[t] : 0.0;
+            uf[t][k] = (float)uk;
+            if (uk != 0.0 && !(uf[t][k] >= 1.17549435e-38f)) filter = false;  // flushed component: exact expression for this row
+        }
         best32[t] = 0.0f;
         thr[t] = filter ? 0.0f : -INFINITY;  // 0: every non-negative score passes until a maximum exists
         if (!live[t] || nf[t] == 0.0) thr[t] = INFINITY;  // nothing to do (selection.hpp:167-169: arg 0, theta 0)

@@ -264,6 +264,25 @@ def test_pair_hand_out_is_invisible(tb, oracle, k1_options, problem):
     assert outs[0][0] == outs[1][0] and np.array_equal(outs[0][1], outs[1][1]) and np.array_equal(outs[0][2], outs[1][2])
 
 
+@pytest.mark.parametrize("shape", [(64, 640, 3), (48, 5000, 3), (32, 1402, 2), (40, 2050, 4), (24, 10240, 3), (16, 4998, 5), (9, 333, 3),
+                                   (7, 20, 3), (5, 9001, 6)])
+def test_lsmop1_evaluator_shapes(tb, oracle, shape):
+    """The LSMOP1 evaluator (128-bit loads, coefficient table, one canonical reduction tree per group) against the CPU
+    restatement to 1e-12 (LSMOP1 is not in the reference: parity unpinned): group boundaries inside and between a
+    thread's vectors, odd d (scalar loads), rows narrower than a block, up to 6 objectives; the run's objectives are the
+    evaluator's bits."""
+    n, d, m = shape
+    lo, hi = oracle.problem_bounds("lsmop1", d, m)
+    x, _ = oracle.random_reproduce(n, d, 5, 0, lo, hi)
+    f = tb.evaluate("lsmop1", x, m)
+    assert close_rel(f, oracle.evaluate("lsmop1", x, m), 1e-12)
+    with tb.RveaRun(tb.RunConfig(problem="lsmop1", pop=n - n % 2, dim=d, obj=m, generations=3, seed=17)) as run:
+        for _ in range(3):
+            run.step()
+        out = run.download()
+    assert np.array_equal(out["f"], tb.evaluate("lsmop1", out["x"], m))
+
+
 def test_lockstep_wide_rows(tb, oracle):
     """Lock-step generations at a row width that runs the pair kernel (d = 1000, the shape of config #4)."""
     _lockstep(tb, oracle, "dtlz3", 128, 1000, 3, 5, 21)
@@ -553,6 +572,11 @@ def test_rv_select_many_objectives_filter(tb, oracle, cfg):
     gneg = oracle.min_vector_angles(vneg) if hasattr(oracle, "min_vector_angles") else gamma
     f = Stream(oracle, 9800 + seed).tensor(500, m) + 0.1
     _check_selection(tb.rv_select(f, tb.RefVectorSet(v0, vneg, gneg), 10, 100, 2.0), oracle.rv_select(f, vneg, gneg, 10, 100, 2.0))
+    # finite vectors outside fp32's range (component -> inf, 1 / norm -> 0 or inf in float): the filter must step aside
+    for scale in (1e39, 1e-41):
+        vbig = v0.copy()
+        vbig[7] = v0[7] * scale  # same direction: the association must not change, and vector 7 must stay reachable
+        _check_selection(tb.rv_select(f, tb.RefVectorSet(v0, vbig, gamma), 10, 100, 2.0), oracle.rv_select(f, vbig, gamma, 10, 100, 2.0))
 
 
 def test_selection_contracts_and_edges(tb, oracle):
