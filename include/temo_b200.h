@@ -263,6 +263,15 @@ int temo_b200_crowding_distance(const double* front, uint64_t k, uint64_t m, dou
  * NULL: no HV), hv_scale, hv_samples, hv_seed, maximization. */
 int temo_b200_run_set_metrics(temo_b200_run* run, const double* pf_ref, uint64_t n_ref, const double* hv_ref,
                               double hv_scale, uint64_t hv_samples, uint64_t hv_seed, int maximization);
+/* Archive of a device-resident run (Archive, algorithms.hpp:68-142; RunConfig::track_archive / archive_cap, :31-33).
+ * temo_b200_run_track_archive must follow temo_b200_run_create directly: it inserts the initial population
+ * (algorithms.hpp:243); every later step inserts its survivors (:282) and temo_b200_run_metrics then reports the
+ * archive's objectives (:288). archive_cap = 0: unbounded. The archive stays in HBM (dominance filter, compaction and
+ * row gather on the device; crowding truncation beyond the cap on the host). temo_b200_run_archive copies out
+ * x (rows x d) and f (rows x m) in insertion order; either may be NULL. */
+int temo_b200_run_track_archive(temo_b200_run* run, uint64_t archive_cap);
+int temo_b200_run_archive_rows(temo_b200_run* run, uint64_t* rows);
+int temo_b200_run_archive(temo_b200_run* run, double* x, double* f);
 /* fill_metrics (algorithms.hpp:161-180) on the current survivors' objectives without copying them to the host
  * (m = 2: hv_exact_2d on a host copy of rows x 2 values). NaN where the context has no reference. */
 int temo_b200_run_metrics(temo_b200_run* run, double* igd, double* hv);

@@ -214,9 +214,11 @@ inline Tensor2D apd_scores(const Tensor2D& f, const RefVectorSet& refs, std::siz
 }
 
 // ---- algorithms.hpp --------------------------------------------------------------------------
-/// rvea_run with track_archive = false, device-resident for the whole run; cfg.op = ga / de / pso / cso / random
-/// (algorithms.hpp:250-271).
-inline RunRecord rvea_run(const ProblemInstance& prob, const RunConfig& cfg) {
+/// rvea_run (algorithms.hpp:227-296), device-resident for the whole run; cfg.op = ga / de / pso / cso / random
+/// (algorithms.hpp:250-271). cfg.track_archive keeps the Archive in HBM (algorithms.hpp:243, 282) and fills
+/// RunRecord.archive / archive_f_history; with a MetricContext every GenerationRow carries igd_value / hv_value of the
+/// archive (of the population without one), algorithms.hpp:288. The expected-utility indicator is not on this path.
+inline RunRecord rvea_run(const ProblemInstance& prob, const RunConfig& cfg, const MetricContext& mc = {}) {
     temo::detail::require(cfg.pop >= 2 && cfg.generations >= 1, "rvea_run: bad config");
     static const char* const kOps[] = {"ga", "de", "pso", "cso", "random"};
     int op = -1;
@@ -246,17 +248,61 @@ inline RunRecord rvea_run(const ProblemInstance& prob, const RunConfig& cfg) {
     const std::size_t h = cfg.lattice_h ? cfg.lattice_h : lattice_density_for(prob.num_obj, cfg.pop);
     const std::size_t cap = std::max<std::size_t>(cfg.pop, lattice_count(prob.num_obj, h));
     Tensor2D x(cap, prob.dim), f(cap, prob.num_obj);
-    std::vector<uint64_t> pops(cfg.generations);
-    std::vector<double> ms(cfg.generations);
-    uint64_t rows = 0, done = 0;
-    detail::check(temo_b200_rvea_run(&c, x.data.data(), f.data.data(), &rows, &done, pops.data(), ms.data()));
     RunRecord rec;
-    for (uint64_t t = 0; t < done; ++t) {
-        GenerationRow row;
-        row.t = t;
-        row.elapsed_ms = ms[t];
-        row.pop_size = pops[t];
-        rec.rows.push_back(row);
+    uint64_t rows = 0;
+    const bool with_metrics = mc.pf_ref.rows > 0 || mc.hv_ref.rows > 0;
+    if (!cfg.track_archive && !with_metrics) {  // one call for the whole run
+        std::vector<uint64_t> pops(cfg.generations);
+        std::vector<double> ms(cfg.generations);
+        uint64_t done = 0;
+        detail::check(temo_b200_rvea_run(&c, x.data.data(), f.data.data(), &rows, &done, pops.data(), ms.data()));
+        for (uint64_t t = 0; t < done; ++t) {
+            GenerationRow row;
+            row.t = t;
+            row.elapsed_ms = ms[t];
+            row.pop_size = pops[t];
+            rec.rows.push_back(row);
+        }
+    } else {  // the session calls: one step per generation, archive and indicators stay on the device
+        const temo::detail::GenerationTimer timer;
+        temo_b200_run* run = nullptr;
+        detail::check(temo_b200_run_create(&c, &run));
+        struct Closer {
+            temo_b200_run* r;
+            ~Closer() { temo_b200_run_destroy(r); }
+        } closer{run};
+        auto fetch_archive = [&](Tensor2D* ax, Tensor2D& af) {
+            uint64_t arows = 0;
+            detail::check(temo_b200_run_archive_rows(run, &arows));
+            if (ax) *ax = Tensor2D(arows, prob.dim);
+            af = Tensor2D(arows, prob.num_obj);
+            detail::check(temo_b200_run_archive(run, ax ? ax->data.data() : nullptr, af.data.data()));
+        };
+        if (cfg.track_archive) detail::check(temo_b200_run_track_archive(run, cfg.archive_cap));
+        if (with_metrics)
+            detail::check(temo_b200_run_set_metrics(run, mc.pf_ref.rows ? mc.pf_ref.data.data() : nullptr, mc.pf_ref.rows,
+                                                    mc.hv_ref.rows ? mc.hv_ref.data.data() : nullptr, mc.hv_scale, mc.hv_samples,
+                                                    mc.hv_seed, mc.maximization ? 1 : 0));
+        for (std::size_t t = 0; t < cfg.generations; ++t) {
+            uint64_t pop = 0;
+            detail::check(temo_b200_run_step(run, &pop, nullptr));
+            GenerationRow row;
+            row.t = t;
+            row.pop_size = pop;
+            if (with_metrics) detail::check(temo_b200_run_metrics(run, &row.igd_value, &row.hv_value));
+            if (cfg.track_archive && cfg.archive_history) {
+                Tensor2D af;
+                fetch_archive(nullptr, af);
+                rec.archive_f_history.push_back(std::move(af));
+            }
+            row.elapsed_ms = timer.elapsed_ms();
+            rec.rows.push_back(row);
+            if (cfg.time_budget_s > 0.0 && row.elapsed_ms >= cfg.time_budget_s * 1e3) break;
+        }
+        uint64_t counter = 0, tt = 0, r = 0, d = 0, m = 0;
+        detail::check(temo_b200_run_state(run, &rows, &counter, &tt, &r, &d, &m));
+        detail::check(temo_b200_run_download(run, x.data.data(), f.data.data(), nullptr, nullptr));
+        if (cfg.track_archive) fetch_archive(&rec.archive.x, rec.archive.f);
     }
     rec.final_x = Tensor2D(rows, prob.dim);
     rec.final_f = Tensor2D(rows, prob.num_obj);

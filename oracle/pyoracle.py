@@ -727,6 +727,23 @@ class Ref(_Base):
                                                 _p(mcp), _p(pops, u64p), _p(g), _p(h)))
         return dict(pop_size=pops, igd=g, hv=h)
 
+    def rvea_run_archive(self, problem, n, d, m, generations, pf_ref=None, seed=42, lattice_h=0, alpha=2.0, fr=0.1, archive_cap=0,
+                         scalar=False, arch_capacity=0):
+        """The reference's rvea_run (or oracle_rvea_run) with track_archive = true: per-generation survivor counts, archive
+        sizes and archive IGD, and the final archive."""
+        cfg_u = np.array([n, lattice_h, generations, seed, d, m], dtype=np.uint64)
+        cfg_d = np.array([alpha, fr, 0.0])
+        pops, sizes = np.zeros(generations, dtype=np.uint64), np.zeros(generations, dtype=np.uint64)
+        g = np.full(generations, np.nan)
+        pf = None if pf_ref is None else _f(pf_ref)
+        cap = arch_capacity or 64 * max(n, 128)
+        ax, af = np.empty((cap, d)), np.empty((cap, m))
+        rows = u64(0)
+        self._chk(self.lib.ref_rvea_run_archive(C.c_int(1 if scalar else 0), problem.encode(), _p(cfg_u, u64p), _p(cfg_d), u64(archive_cap),
+                                                None if pf is None else _p(pf), u64(0 if pf is None else pf.shape[0]),
+                                                _p(pops, u64p), _p(sizes, u64p), _p(g), _p(ax), _p(af), u64(cap), C.byref(rows)))
+        return dict(pop_size=pops, archive_size=sizes, igd=g, archive_x=ax[: rows.value].copy(), archive_f=af[: rows.value].copy())
+
     def generation(self, problem, n, m, seed, counter, lower, upper, t, t_max, alpha, adapt_every,
                    v0, v, gamma, x, f, ga=GA_DEFAULT):
         """algorithms.hpp:246-281 composed from the reference's own stage functions."""

@@ -387,6 +387,42 @@ int ref_rvea_run_op(const char* problem, const char* op, const double* opp, cons
     });
 }
 
+// rvea_run / oracle_rvea_run with track_archive = true (algorithms.hpp:243, 282-288): per-generation survivor count,
+// archive size and IGD of the ARCHIVE against pf_ref; final archive in arch_x / arch_f (capacity arch_cap_rows rows).
+int ref_rvea_run_archive(int which, const char* problem, const std::uint64_t* cfg_u, const double* cfg_d, std::uint64_t archive_cap,
+                         const double* pf_ref, std::uint64_t n_ref, std::uint64_t* pop_size, std::uint64_t* arch_size,
+                         double* igd_out, double* arch_x, double* arch_f, std::uint64_t arch_cap_rows, std::uint64_t* arch_rows) {
+    return guarded([&] {
+        temo::RunConfig cfg;
+        cfg.problem = problem;
+        cfg.op = "ga";
+        cfg.pop = cfg_u[0];
+        cfg.lattice_h = cfg_u[1];
+        cfg.generations = cfg_u[2];
+        cfg.seed = cfg_u[3];
+        cfg.dim = cfg_u[4];
+        cfg.obj = cfg_u[5];
+        cfg.alpha = cfg_d[0];
+        cfg.fr = cfg_d[1];
+        cfg.track_archive = true;
+        cfg.archive_history = true;
+        cfg.archive_cap = archive_cap;
+        const temo::ProblemInstance prob = temo::make_problem(cfg.problem, cfg.dim, cfg.obj);
+        temo::MetricContext mc;
+        if (pf_ref && n_ref) mc.pf_ref = wrap(pf_ref, n_ref, cfg.obj);
+        const temo::RunRecord rec = which == 0 ? temo::rvea_run(prob, cfg, mc) : temo::oracle::oracle_rvea_run(prob, cfg, mc);
+        for (std::size_t i = 0; i < rec.rows.size(); ++i) {
+            pop_size[i] = rec.rows[i].pop_size;
+            igd_out[i] = rec.rows[i].igd_value;
+            arch_size[i] = i < rec.archive_f_history.size() ? rec.archive_f_history[i].rows : 0;
+        }
+        *arch_rows = rec.archive.f.rows;
+        if (rec.archive.f.rows > arch_cap_rows) throw std::runtime_error("archive larger than the caller's buffers");
+        if (arch_x) unwrap(rec.archive.x, arch_x);
+        if (arch_f) unwrap(rec.archive.f, arch_f);
+    });
+}
+
 // hv_mc_box / hv_mc with the standard error (metrics.hpp:76-124); lo == nullptr selects hv_mc. out = {value, std_error}.
 int ref_hv_mc_box(const double* f, std::uint64_t n, std::uint64_t m, const double* lo, const double* ref_point,
                   std::uint64_t samples, std::uint64_t seed, double* out) {

@@ -228,6 +228,33 @@ static int operator_runs_gpu() {
     return failed;
 }
 
+// The reference's convergence set-up (tests/acceptance.cpp:66-98) through the shim with the default track_archive = true:
+// RunRecord.archive filled from the device-resident archive, archive IGD per generation, against the reference's own run.
+static int archive_run_gpu() {
+    RunConfig cfg;
+    cfg.problem = "dtlz2";
+    cfg.pop = 105;
+    cfg.lattice_h = 13;
+    cfg.generations = 200;
+    cfg.seed = 4242;
+    cfg.archive_history = true;
+    const ProblemInstance prob = make_problem("dtlz2");
+    MetricContext mc;
+    std::size_t h = 1;
+    while (lattice_count(prob.num_obj, h) < 300) ++h;
+    mc.pf_ref = dtlz_pf_reference(prob.dtlz_id, prob.num_obj, h);
+    const RunRecord a = b200::rvea_run(prob, cfg, mc);
+    const RunRecord b = rvea_run(prob, cfg, mc);
+    const double ia = a.rows.back().igd_value, ib = b.rows.back().igd_value;
+    bool ok = a.rows.size() == b.rows.size() && a.archive.f.rows >= cfg.pop && a.archive.x.rows == a.archive.f.rows &&
+              a.archive_f_history.size() == a.rows.size() && same_bits(a.archive_f_history.back(), a.archive.f);
+    ok = ok && ia == igd(a.archive.f, mc.pf_ref);           // the device's IGD is the reference's arithmetic
+    ok = ok && std::abs(ia - ib) <= 0.05 * ib && ia <= 1.1 * 0.037367406771666209;
+    std::printf("rvea_run track_archive (dtlz2, 200 generations, seed 4242): archive %zu rows (reference %zu), final archive IGD %.17g "
+                "(reference %.17g, pinned 0.037367406771666209)\n", a.archive.f.rows, b.archive.f.rows, ia, ib);
+    return ok ? 0 : 1;
+}
+
 int main() {
     if (temo_b200_device_count() < 1) {
         std::printf("no CUDA device\n");
@@ -241,6 +268,7 @@ int main() {
     failed += whole_run_gpu() != 0;
     failed += widened_suite_gpu() != 0;
     failed += operator_runs_gpu() != 0;
+    failed += archive_run_gpu() != 0;
     std::printf("%s\n", failed ? "SHIM PARITY FAILED" : "SHIM PARITY OK");
     return failed;
 }

@@ -95,6 +95,9 @@ SIGNATURES = {
     "temo_b200_crowding_distance": (C.c_int, [f64p, u64, u64, f64p]),
     "temo_b200_run_set_metrics": (C.c_int, [_RUN, f64p, u64, f64p, C.c_double, u64, u64, C.c_int]),
     "temo_b200_run_metrics": (C.c_int, [_RUN, f64p, f64p]),
+    "temo_b200_run_track_archive": (C.c_int, [_RUN, u64]),
+    "temo_b200_run_archive_rows": (C.c_int, [_RUN, u64p]),
+    "temo_b200_run_archive": (C.c_int, [_RUN, f64p, f64p]),
     "temo_b200_run_create": (C.c_int, [_CFG, C.POINTER(_RUN)]),
     "temo_b200_run_step": (C.c_int, [_RUN, u64p, f64p]),
     "temo_b200_run_step_injected": (C.c_int, [_RUN, f64p, u64p]),

@@ -415,7 +415,8 @@ OPERATOR_IDS = {"ga": 0, "de": 1, "pso": 2, "cso": 3, "random": 4}  # TEMO_B200_
 
 @dataclass
 class RunConfig:
-    """reference: RunConfig (algorithms.hpp:21-41), track_archive = false; op = ga / de / pso / cso / random."""
+    """reference: RunConfig (algorithms.hpp:21-41); op = ga / de / pso / cso / random. track_archive defaults to false
+    here (the reference's default is true; its own timing harness switches it off, temo.cpp:260)."""
     problem: str = "dtlz2"
     op: str = "ga"
     pop: int = 105
@@ -433,6 +434,9 @@ class RunConfig:
     cso: tuple = (0.1,)            # CsoParams {phi}, operators.hpp:39-41
     rng_mode: int = RNG_SPLITMIX64
     fuse_eval: bool = True
+    track_archive: bool = False    # algorithms.hpp:31
+    archive_cap: int = 0           # algorithms.hpp:32 (0: unbounded)
+    archive_history: bool = False  # algorithms.hpp:33
 
     def c(self) -> RunConfigC:
         if self.op not in OPERATOR_IDS:
@@ -554,9 +558,12 @@ def hv_mc(f, ref, samples: int, seed: int) -> HvEstimate:
 
 @dataclass
 class RunRecord:
+    """reference: RunRecord (algorithms.hpp:144-150); archive = (x, f) in insertion order or None."""
     rows: list
     final_x: np.ndarray
     final_f: np.ndarray
+    archive: tuple | None = None
+    archive_f_history: list = field(default_factory=list)
 
 
 class _PinnedBlock:
@@ -677,8 +684,22 @@ class RveaRun:
         _call(self._L.temo_b200_run_set_metrics, self._h, _p(pf), u64(0 if pf is None else pf.shape[0]), _p(hv),
               C.c_double(mc.hv_scale), u64(mc.hv_samples), u64(mc.hv_seed), int(mc.maximization))
 
+    def track_archive(self, cap: int = 0) -> None:
+        """Archive of the run kept in HBM (algorithms.hpp:68-142): call right after construction (inserts the initial
+        population, algorithms.hpp:243); every step then inserts its survivors and metrics() reports the archive."""
+        _call(self._L.temo_b200_run_track_archive, self._h, u64(cap))
+
+    def archive(self) -> tuple:
+        """(x, f) of the archive in insertion order."""
+        rows = u64(0)
+        _call(self._L.temo_b200_run_archive_rows, self._h, C.byref(rows))
+        x, f = np.empty((rows.value, self.d)), np.empty((rows.value, self.m))
+        _call(self._L.temo_b200_run_archive, self._h, _p(x), _p(f))
+        return x, f
+
     def metrics(self) -> tuple:
-        """fill_metrics (algorithms.hpp:161-180) on the survivors' objectives, evaluated on the device: (igd, hv)."""
+        """fill_metrics (algorithms.hpp:161-180) on the survivors' objectives (the archive's when one is tracked),
+        evaluated on the device: (igd, hv)."""
         a, b = C.c_double(0), C.c_double(0)
         _call(self._L.temo_b200_run_metrics, self._h, C.byref(a), C.byref(b))
         return a.value, b.value
@@ -778,22 +799,30 @@ def nsga2_run(prob: ProblemInstance, cfg: RunConfig) -> RunRecord:
 def rvea_run(prob: ProblemInstance, cfg: RunConfig, mc: MetricContext | None = None) -> RunRecord:
     """reference: rvea_run (algorithms.hpp:227-296). `prob` supplies name/dim/num_obj like the
     reference's ProblemInstance; the evaluator itself runs on the device. With a MetricContext every
-    GenerationRow carries igd_value / hv_value of the population (fill_metrics, track_archive = false)."""
+    GenerationRow carries igd_value / hv_value of the population, or of the archive with cfg.track_archive
+    (fill_metrics, algorithms.hpp:288); RunRecord.archive / archive_f_history as in the reference."""
     cfg = RunConfig(**{**cfg.__dict__, "problem": prob.name, "dim": prob.dim, "obj": prob.num_obj})
-    if mc is not None and (mc.pf_ref is not None or mc.hv_ref is not None):
+    with_metrics = mc is not None and (mc.pf_ref is not None or mc.hv_ref is not None)
+    if with_metrics or cfg.track_archive:
         t0 = time.perf_counter()
-        rows = []
+        rows, history = [], []
         with RveaRun(cfg) as run:
-            run.set_metrics(mc)
+            if cfg.track_archive:
+                run.track_archive(cfg.archive_cap)
+            if with_metrics:
+                run.set_metrics(mc)
             for t in range(cfg.generations):
                 pop = run.step()
-                g, h = run.metrics()
+                g, h = run.metrics() if with_metrics else (float("nan"), float("nan"))
+                if cfg.track_archive and cfg.archive_history:
+                    history.append(run.archive()[1])
                 ms = (time.perf_counter() - t0) * 1e3
                 rows.append(GenerationRow(t, ms, pop, g, h))
                 if cfg.time_budget_s > 0.0 and ms >= cfg.time_budget_s * 1e3:
                     break
             out = run.download()
-        return RunRecord(rows, out["x"], out["f"])
+            arch = run.archive() if cfg.track_archive else None
+        return RunRecord(rows, out["x"], out["f"], arch, history)
     ccfg = cfg.c()
     L = _lib.load()
     H = cfg.lattice_h or lattice_density_for(prob.num_obj, cfg.pop)

@@ -857,6 +857,28 @@ int temo_b200_run_set_metrics(temo_b200_run* run, const double* pf_ref, uint64_t
     });
 }
 
+int temo_b200_run_track_archive(temo_b200_run* run, uint64_t archive_cap) {
+    return guarded([&] {
+        require(run && run->impl, "run_track_archive: null run");
+        run->impl->enable_archive(archive_cap);
+    });
+}
+
+int temo_b200_run_archive_rows(temo_b200_run* run, uint64_t* rows) {
+    return guarded([&] {
+        require(run && run->impl && rows, "run_archive_rows: null argument");
+        require(run->impl->track_archive, "archive: this run does not track one");
+        *rows = run->impl->arch_rows;
+    });
+}
+
+int temo_b200_run_archive(temo_b200_run* run, double* x, double* f) {
+    return guarded([&] {
+        require(run && run->impl, "run_archive: null run");
+        run->impl->archive_download(x, f);
+    });
+}
+
 int temo_b200_run_metrics(temo_b200_run* run, double* igd, double* hv) {
     return guarded([&] {
         require(run && run->impl, "run_metrics: null run");

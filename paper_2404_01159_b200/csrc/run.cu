@@ -16,6 +16,8 @@
 #include <cmath>
 #include <cstring>
 
+#include <algorithm>
+
 #include "compact.cuh"
 #include "internal.h"
 #include "run.h"
@@ -212,6 +214,8 @@ Run::~Run() {
     cudaFree(mc_pf); cudaFree(mc_nearest); cudaFree(mc_hv_ref); cudaFree(mc_hits);
     cudaFree(pool_idx_dev); cudaFree(pool_f); cudaFree(scores); cudaFree(sw_vel[0]); cudaFree(sw_vel[1]);
     cudaFree(sw_pbx); cudaFree(sw_pbs); cudaFree(sw_mean); cudaFree(sw_best);
+    cudaFree(arch_x[0]); cudaFree(arch_x[1]); cudaFree(arch_f[0]); cudaFree(arch_f[1]);
+    cudaFree(arch_keep); cudaFree(arch_list); cudaFree(arch_scratch); cudaFree(arch_count);
     cudaFreeHost(h_status);
     ws.release();
     vindex.release();
@@ -431,6 +435,7 @@ uint64_t Run::step(double* survivors_f_host, const double* f_off_inject) {
     ++t;
     if (survivors_f_host)
         TEMO_CUDA(cudaMemcpy(survivors_f_host, fm[cur], P * m * sizeof(double), cudaMemcpyDeviceToHost));
+    if (track_archive) archive_insert();  // algorithms.hpp:282
     float ms = 0.f;
     cudaEventElapsedTime(&ms, ev[0], ev[5]); timings[0] = ms;
     cudaEventElapsedTime(&ms, ev[1], ev[2]); timings[1] = ms;
@@ -548,27 +553,149 @@ void Run::set_metrics(const double* pf_ref, uint64_t n_ref, const double* hv_ref
     }
 }
 
-// fill_metrics (algorithms.hpp:161-180) with track_archive = false: the population's objectives.
+// fill_metrics (algorithms.hpp:161-180) of the population's objectives, or of the archive's when one is tracked (:288).
 void Run::metrics(double* igd_out, double* hv_out) {
     const double nan = std::nan("");
-    if (igd_out) *igd_out = mc_n_ref ? device_igd(fm[cur], nullptr, P, m, mc_pf, mc_n_ref, mc_nearest, stream) : nan;
+    const double* fs = track_archive ? arch_f[acur] : fm[cur];
+    const uint64_t rows = track_archive ? arch_rows : P;
+    if (igd_out) *igd_out = mc_n_ref ? device_igd(fs, nullptr, rows, m, mc_pf, mc_n_ref, mc_nearest, stream) : nan;
     if (!hv_out) return;
     *hv_out = nan;
     if (mc_hv_ref_host.empty()) return;
-    if (m == 2) {  // hv_exact_2d: a sort-based sweep, on a host copy of P x 2 values
-        std::vector<double> f(P * 2);
-        TEMO_CUDA(cudaMemcpyAsync(f.data(), fm[cur], P * 2 * sizeof(double), cudaMemcpyDeviceToHost, stream));
+    if (m == 2) {  // hv_exact_2d: a sort-based sweep, on a host copy of rows x 2 values
+        std::vector<double> f(rows * 2);
+        TEMO_CUDA(cudaMemcpyAsync(f.data(), fs, rows * 2 * sizeof(double), cudaMemcpyDeviceToHost, stream));
         TEMO_CUDA(cudaStreamSynchronize(stream));
-        *hv_out = host_hv_exact_2d(f.data(), P, mc_hv_ref_host.data(), mc_scale);
+        *hv_out = host_hv_exact_2d(f.data(), rows, mc_hv_ref_host.data(), mc_scale);
         return;
     }
     // hv_mc: the box's lower corner is col_min of the (scaled) objectives (metrics.hpp:121-124)
-    launch_col_minmax(fm[cur], P, nullptr, m, zmin, zmax, zscratch, stream);
+    launch_col_minmax(fs, rows, nullptr, m, zmin, zmax, zscratch, stream);
     double lo[kMaxObj];
     TEMO_CUDA(cudaMemcpyAsync(lo, zmin, m * sizeof(double), cudaMemcpyDeviceToHost, stream));
     TEMO_CUDA(cudaStreamSynchronize(stream));
-    device_hv_mc_box(fm[cur], nullptr, P, m, zmin, lo, /*lo_scaled=*/true, mc_hv_ref, mc_hv_ref_host.data(), mc_scale, mc_samples,
+    device_hv_mc_box(fs, nullptr, rows, m, zmin, lo, /*lo_scaled=*/true, mc_hv_ref, mc_hv_ref_host.data(), mc_scale, mc_samples,
                      mc_seed, mc_hits, hv_out, nullptr, stream);
+}
+
+// ---- Archive of the run (algorithms.hpp:68-142), resident in HBM -----------------------------------------------------
+namespace {
+struct KeepPred {
+    const unsigned char* keep;
+    __device__ bool operator()(uint64_t i) const { return keep[i] != 0; }
+};
+struct IndexVal {
+    __device__ uint32_t operator()(uint64_t i) const { return (uint32_t)i; }
+};
+// out row k <- archive row list[k] (k < k_old) or survivor list[k] - n_old of the population (pool row through the slot table)
+__global__ void archive_gather_kernel(const uint32_t* __restrict__ list, const uint32_t* __restrict__ counts, uint32_t n_old,
+                                      const double* __restrict__ ax, const double* __restrict__ af, const double* __restrict__ pool,
+                                      const uint32_t* __restrict__ slot, const double* __restrict__ pf, uint64_t d, uint64_t m,
+                                      double* __restrict__ ox, double* __restrict__ of) {
+    const uint32_t k = blockIdx.x;
+    if (k >= counts[0]) return;
+    const uint32_t e = list[k];
+    const double* sx;
+    const double* sf;
+    if (e < n_old) {
+        sx = ax + (uint64_t)e * d;
+        sf = af + (uint64_t)e * m;
+    } else {
+        sx = pool + (uint64_t)slot[e - n_old] * d;
+        sf = pf + (uint64_t)(e - n_old) * m;
+    }
+    for (uint64_t j = threadIdx.x; j < d; j += blockDim.x) ox[(uint64_t)k * d + j] = sx[j];
+    for (uint64_t j = threadIdx.x; j < m; j += blockDim.x) of[(uint64_t)k * m + j] = sf[j];
+}
+// out row k <- archive row list[k]
+__global__ void archive_take_kernel(const uint32_t* __restrict__ list, const double* __restrict__ ax, const double* __restrict__ af,
+                                    uint64_t d, uint64_t m, double* __restrict__ ox, double* __restrict__ of) {
+    const uint64_t k = blockIdx.x, e = list[k];
+    for (uint64_t j = threadIdx.x; j < d; j += blockDim.x) ox[k * d + j] = ax[e * d + j];
+    for (uint64_t j = threadIdx.x; j < m; j += blockDim.x) of[k * m + j] = af[e * m + j];
+}
+}  // namespace
+
+void Run::archive_reserve(uint64_t rows) {
+    if (rows <= arch_capacity) return;
+    uint64_t want = arch_capacity ? arch_capacity : 2 * pcap;
+    while (want < rows) want *= 2;
+    TEMO_CUDA(cudaStreamSynchronize(stream));
+    for (int b = 0; b < 2; ++b) {
+        double* nx = dev_alloc<double>(want * d);
+        double* nf = dev_alloc<double>(want * m);
+        if (b == acur && arch_rows) {
+            TEMO_CUDA(cudaMemcpy(nx, arch_x[b], arch_rows * d * sizeof(double), cudaMemcpyDeviceToDevice));
+            TEMO_CUDA(cudaMemcpy(nf, arch_f[b], arch_rows * m * sizeof(double), cudaMemcpyDeviceToDevice));
+        }
+        cudaFree(arch_x[b]);
+        cudaFree(arch_f[b]);
+        arch_x[b] = nx;
+        arch_f[b] = nf;
+    }
+    cudaFree(arch_keep); cudaFree(arch_list); cudaFree(arch_scratch);
+    arch_keep = dev_alloc<unsigned char>(want);
+    arch_list = dev_alloc<uint32_t>(want);
+    arch_scratch = dev_alloc<uint32_t>((want + kCompactTile - 1) / kCompactTile + 1);
+    if (!arch_count) arch_count = dev_alloc<uint32_t>(2);
+    arch_capacity = want;
+}
+
+// Archive::insert(x, f, cap) with the current survivors (algorithms.hpp:72-122): the O(n^2 m) dominance / duplicate
+// filter, the order-preserving compaction (kept archive rows first, then kept new rows) and the row gather run on the
+// device; only the two row counts (and, beyond the cap, the objectives for the crowding sort) come back to the host.
+void Run::archive_insert() {
+    const uint64_t n_old = arch_rows, n_new = P;
+    archive_reserve(n_old + n_new);
+    unsigned char* keep_old = arch_keep;
+    unsigned char* keep_new = arch_keep + n_old;
+    launch_archive_filter(arch_f[acur], n_old, fm[cur], n_new, m, keep_old, keep_new, stream);
+    // one compaction over the concatenated flags keeps "archive rows first, then new rows", each in its own order
+    launch_compact(n_old + n_new, KeepPred{arch_keep}, IndexVal{}, arch_scratch, n_old + n_new, arch_list, arch_count, stream);
+    uint32_t kept = 0;
+    TEMO_CUDA(cudaMemcpyAsync(&kept, arch_count, sizeof(uint32_t), cudaMemcpyDeviceToHost, stream));
+    TEMO_CUDA(cudaStreamSynchronize(stream));
+    if (kept)
+        archive_gather_kernel<<<kept, 256, 0, stream>>>(arch_list, arch_count, (uint32_t)n_old, arch_x[acur], arch_f[acur], pool,
+                                                        parent_slot[cur], fm[cur], d, m, arch_x[acur ^ 1], arch_f[acur ^ 1]);
+    TEMO_CUDA(cudaGetLastError());
+    acur ^= 1;
+    arch_rows = kept;
+    if (archive_cap > 0 && arch_rows > archive_cap) {  // truncate_by_crowding (algorithms.hpp:124-143): two host sorts
+        std::vector<double> f(arch_rows * m), crowd(arch_rows);
+        TEMO_CUDA(cudaMemcpyAsync(f.data(), arch_f[acur], f.size() * sizeof(double), cudaMemcpyDeviceToHost, stream));
+        TEMO_CUDA(cudaStreamSynchronize(stream));
+        crowding_distance_host(f.data(), arch_rows, m, crowd.data());
+        std::vector<uint32_t> order(arch_rows);
+        for (uint64_t i = 0; i < arch_rows; ++i) order[i] = (uint32_t)i;
+        std::sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) {
+            if (crowd[a] != crowd[b]) return crowd[a] > crowd[b];
+            return a < b;
+        });
+        order.resize(archive_cap);
+        std::sort(order.begin(), order.end());  // keep insertion order
+        TEMO_CUDA(cudaMemcpyAsync(arch_list, order.data(), archive_cap * sizeof(uint32_t), cudaMemcpyHostToDevice, stream));
+        archive_take_kernel<<<(unsigned)archive_cap, 256, 0, stream>>>(arch_list, arch_x[acur], arch_f[acur], d, m, arch_x[acur ^ 1],
+                                                                       arch_f[acur ^ 1]);
+        TEMO_CUDA(cudaGetLastError());
+        TEMO_CUDA(cudaStreamSynchronize(stream));  // `order` goes away
+        acur ^= 1;
+        arch_rows = archive_cap;
+    }
+}
+
+void Run::enable_archive(uint64_t cap_rows) {
+    require(!track_archive, "track_archive: already enabled");
+    track_archive = true;
+    archive_cap = cap_rows;
+    archive_insert();  // algorithms.hpp:243
+}
+
+void Run::archive_download(double* x, double* f) {
+    require(track_archive, "archive: this run does not track one");
+    TEMO_CUDA(cudaStreamSynchronize(stream));
+    if (x && arch_rows) TEMO_CUDA(cudaMemcpy(x, arch_x[acur], arch_rows * d * sizeof(double), cudaMemcpyDeviceToHost));
+    if (f && arch_rows) TEMO_CUDA(cudaMemcpy(f, arch_f[acur], arch_rows * m * sizeof(double), cudaMemcpyDeviceToHost));
 }
 
 double Run::time_stage(int stage, int reps) {

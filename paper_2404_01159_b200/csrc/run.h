@@ -47,6 +47,11 @@ struct Run {
     void set_metrics(const double* pf_ref, uint64_t n_ref, const double* hv_ref, double hv_scale, uint64_t hv_samples,
                      uint64_t hv_seed, bool maximization);
     void metrics(double* igd_out, double* hv_out);
+    // Archive (algorithms.hpp:68-142) of a device-resident run, kept in HBM: enable_archive inserts the current
+    // population (algorithms.hpp:243); every later step() inserts its survivors (:282). cap = RunConfig::archive_cap
+    // (0: unbounded). With an archive the metrics are those of the archive's objectives (:288).
+    void enable_archive(uint64_t archive_cap);
+    void archive_download(double* x, double* f);
 
     RunConfig cfg;
     uint64_t n = 0, d = 0, m = 0, r = 0, H = 0, adapt_every = 1;
@@ -89,6 +94,14 @@ struct Run {
     double mc_scale = 1.0;
     uint64_t mc_samples = 2048, mc_seed = 9001;
     unsigned long long* mc_hits = nullptr;
+    bool track_archive = false;
+    uint64_t archive_cap = 0, arch_rows = 0, arch_capacity = 0;
+    double *arch_x[2] = {nullptr, nullptr}, *arch_f[2] = {nullptr, nullptr};  // double buffered: rows in insertion order
+    int acur = 0;
+    unsigned char* arch_keep = nullptr;   // [arch_capacity]: keep flags, archive rows first, then the inserted rows
+    uint32_t* arch_list = nullptr;        // [arch_capacity]: kept archive rows, then kept inserted rows
+    uint32_t* arch_scratch = nullptr;
+    uint32_t* arch_count = nullptr;       // [2]
     double* f_off_saved = nullptr;  // device objectives of the last offspring when selection ran on injected ones
     bool f_off_was_injected = false;
     SelectWorkspace ws;
@@ -112,6 +125,8 @@ private:
     bool uses_perm() const { return cfg.op == kOpGa || cfg.op == kOpCso; }
     void launch_offspring_eval();
     bool fusable() const;
+    void archive_reserve(uint64_t rows);
+    void archive_insert();
     uint64_t P_prev() const { return P_before; }
 };
 

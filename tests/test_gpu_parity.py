@@ -939,6 +939,82 @@ def test_free_running_c1_against_reference_run(tb, checkers):
     assert abs(np.median(rec.final_f.sum(axis=1)) - np.median(exp["f"].sum(axis=1))) <= 0.25 * np.median(exp["f"].sum(axis=1))
 
 
+# ---- the archive of a device-resident run (algorithms.hpp:68-142, 243, 282-288)
+PINNED_BASELINE_IGD = 0.037367406771666209  # the reference's acceptance value (tests/acceptance.cpp:66-70)
+
+
+def _convergence_front(chk, m=3):
+    h = 1
+    while chk.lattice_count(m, h) < 300:  # acceptance.cpp:86-92
+        h += 1
+    return chk.dtlz_pf_reference(2, m, h)
+
+
+@pytest.mark.parametrize("cap", [0, 150])
+def test_run_archive_lockstep_and_pinned_igd(tb, ref, cap):
+    """track_archive inside the device-resident run, lock-step on the reference's acceptance configuration (DTLZ2 m = 3,
+    H = 13, n = 105, GA, 200 generations, seed 4242): every generation the device inserts its (bit-identical) survivors
+    into the archive it keeps in HBM; the archive must equal the CPU's Archive::insert chain bit for bit, also through the
+    crowding truncation (cap = 150), and the archive IGD of the unbounded run is the reference's pinned baseline."""
+    chk = ref
+    n, d, m, gens, seed, H = 105, 12, 3, 200 if cap == 0 else 60, 4242, 13
+    cfg = tb.RunConfig(problem="dtlz2", pop=n, dim=d, obj=m, generations=gens, seed=seed, lattice_h=H)
+    pf = _convergence_front(chk)
+    v0, gamma = chk.make_ref_set(m, H)
+    lo, hi = chk.problem_bounds("dtlz2", d, m)
+    x, c = chk.random_reproduce(n, d, seed, 0, lo, hi)
+    st = dict(x=x, f=chk.evaluate("dtlz2", x, m), v=v0, gamma=gamma, counter=c)
+    adapt_every = max(1, int(np.ceil(cfg.fr * gens)))
+    ax, af = chk.archive_insert(np.empty((0, d)), np.empty((0, m)), st["x"], st["f"], cap)
+    with tb.RveaRun(cfg) as run:
+        run.inject(x=st["x"], f=st["f"], v=st["v"], gamma=st["gamma"], counter=st["counter"], t=0)
+        run.track_archive(cap)
+        run.set_metrics(tb.MetricContext(pf_ref=pf))
+        for t in range(gens):
+            nxt = chk.generation("dtlz2", n, m, seed, st["counter"], lo, hi, t, gens, cfg.alpha, adapt_every,
+                                 v0, st["v"], st["gamma"], st["x"], st["f"])
+            run.inject(x=st["x"], f=st["f"], v=st["v"], gamma=st["gamma"], counter=st["counter"], t=t)
+            run.step_injected(nxt["f_off"])
+            ax, af = chk.archive_insert(ax, af, nxt["x"], nxt["f"], cap)
+            if t % 20 == 19 or t == gens - 1:
+                gx, gf = run.archive()
+                assert np.array_equal(gf, af) and np.array_equal(gx, ax), t
+                assert run.metrics()[0] == chk.igd(af, pf), t
+            st = nxt
+        igd_final = run.metrics()[0]
+    if cap == 0:
+        assert igd_final == PINNED_BASELINE_IGD
+        exp = chk.rvea_run_archive("dtlz2", n, d, m, gens, pf_ref=pf, seed=seed, lattice_h=H)
+        assert np.array_equal(exp["archive_f"], af) and exp["igd"][-1] == PINNED_BASELINE_IGD
+    else:
+        assert len(af) <= cap
+
+
+def test_run_archive_acceptance_criterion_5(tb, ref):
+    """The reference's convergence criterion (tests/acceptance.cpp:206-226) through the product, free-running: seeds
+    101..105, median final archive IGD < 0.1 x initial and <= 1.1 x the pinned baseline; RunRecord.archive is filled and
+    mutually nondominated, archive_f_history has one snapshot per generation."""
+    pf = _convergence_front(ref)
+    initial, final = [], []
+    for rep in range(5):
+        cfg = tb.RunConfig(pop=105, lattice_h=13, generations=200, seed=101 + rep, track_archive=True, archive_history=rep == 0)
+        rec = tb.rvea_run(tb.make_problem("dtlz2"), cfg, tb.MetricContext(pf_ref=pf))
+        initial.append(rec.rows[0].igd_value)
+        final.append(rec.rows[-1].igd_value)
+        ax, af = rec.archive
+        assert ax.shape == (af.shape[0], 12) and af.shape[0] >= 105
+        assert close_rel(af, tb.evaluate("dtlz2", ax, 3), 1e-12)
+        assert rec.rows[-1].igd_value == tb.igd(af, pf)
+        if rep == 0:
+            assert len(rec.archive_f_history) == 200 and np.array_equal(rec.archive_f_history[-1], af)
+            exp = ref.rvea_run_archive("dtlz2", 105, 12, 3, 200, pf_ref=pf, seed=101, lattice_h=13)
+            print(f"free-running archive run, seed 101: final IGD {rec.rows[-1].igd_value!r} (reference {exp['igd'][-1]!r}), "
+                  f"archive rows {af.shape[0]} (reference {exp['archive_f'].shape[0]})")
+            assert abs(rec.rows[-1].igd_value - exp["igd"][-1]) <= 0.05 * exp["igd"][-1]
+    assert np.median(final) < 0.1 * np.median(initial)
+    assert np.median(final) <= 1.1 * PINNED_BASELINE_IGD
+
+
 def test_run_properties_mid_scale(tb):
     """Size-independent properties at a shape the oracle would take minutes on: survivors are
     unique pool rows, F equals a re-evaluation of X, bounds hold, counters follow Appendix A."""
