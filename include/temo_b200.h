@@ -43,6 +43,8 @@ extern "C" {
 #define TEMO_B200_DTLZ3 3
 #define TEMO_B200_DTLZ4 4
 #define TEMO_B200_LSMOP1 101
+#define TEMO_B200_TOY2 201   /* make_problem("toy2"): MLP 4-16-2 policy on the toy environment, 2 objectives (problems.hpp:279-294) */
+#define TEMO_B200_TOY3 202   /* 3 objectives */
 
 /* RNG policy. SPLITMIX64 reproduces RngStream::value_at bit for bit (rng.hpp:23-43) and is
  * the only mode with draw-for-draw parity; PHILOX is the north star's Philox4x32-10
@@ -89,6 +91,7 @@ typedef struct temo_b200_run_config {
     int32_t fuse_eval;    /* 1: evaluate offspring inside the reproduction kernel (default) */
     int32_t op;           /* TEMO_B200_OP_* (0 = ga); de / pso / cso / random: algorithms.hpp:253-268 */
     temo_b200_op_params opp;
+    uint64_t horizon;     /* toy2 / toy3: episode length (RunConfig::horizon, algorithms.hpp:35; 0 -> 100) */
 } temo_b200_run_config;
 
 /* ---- library / device ------------------------------------------------------------- */
@@ -146,6 +149,16 @@ int temo_b200_random_reproduce(uint64_t n, uint64_t d, uint64_t seed, uint64_t* 
 /* ---- problems.hpp ----------------------------------------------------------------- */
 /* dtlz_eval (problems.hpp:69-92) and ProblemInstance::evaluate (problems.hpp:252); also LSMOP1. */
 int temo_b200_evaluate(int problem, const double* x, uint64_t n, uint64_t d, uint64_t m, double* f);
+/* Neuroevolution evaluator, bit-identical to the reference on an FMA host (tanh follows the
+ * C library's operation sequence, glibc_tanh.cuh).
+ * env_rollout (problems.hpp:211-241): params n x d flat MLP parameters (d = 4h + h + 2h + 2, h = hidden <= 64) -> f n x num_obj
+ *   cumulative returns of one episode of `horizon` steps, maximisation orientation; -1e9 for rows with non-finite parameters.
+ * mlp_forward (problems.hpp:149-163), batched: obs n x 4 -> action n x 2.
+ * temo_b200_evaluate_h: temo_b200_evaluate with the episode length make_problem(name, dim, m, horizon) takes (toy2 / toy3
+ *   evaluate to the NEGATED returns, problems.hpp:288-292; temo_b200_evaluate uses horizon 100). */
+int temo_b200_env_rollout(const double* params, uint64_t n, uint64_t d, uint64_t hidden, uint64_t horizon, uint64_t num_obj, double* f);
+int temo_b200_mlp_forward(const double* params, uint64_t n, uint64_t d, uint64_t hidden, const double* obs, double* action);
+int temo_b200_evaluate_h(int problem, const double* x, uint64_t n, uint64_t d, uint64_t m, uint64_t horizon, double* f);
 /* make_problem bounds (problems.hpp:271-272): lower/upper 1 x d. */
 int temo_b200_problem_bounds(int problem, uint64_t d, uint64_t m, double* lower, double* upper);
 uint64_t temo_b200_problem_default_dim(int problem, uint64_t m);
@@ -344,6 +357,8 @@ int temo_b200_shard_download(temo_b200_shard* s, const uint32_t* slots, uint64_t
  * evaluated by the device kernel (on_device = 1) or by its host twin (on_device = 0, no GPU
  * needed). Must equal the host C library's pow bit for bit on the main path. */
 int temo_b200_pow(const double* x, const double* y, uint64_t n, double* out, int on_device);
+/* The same for tanh (glibc_tanh.cuh: the toy environment's policy network, problems.hpp:149-163). */
+int temo_b200_tanh(const double* x, uint64_t n, double* out, int on_device);
 /* Overwrites >= bytes of scratch HBM (L2 flush between timed iterations). */
 int temo_b200_flush_l2(void);
 /* Path-selection knobs for tests and A/B measurements (no reference counterpart; results are identical on every

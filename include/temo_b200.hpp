@@ -41,6 +41,8 @@ inline temo_b200_ga_params ga_of(const GaParams& p) { return {p.pc, p.eta, p.pm,
 inline int problem_id(const ProblemInstance& prob) {
     if (prob.dtlz_id >= 1 && prob.dtlz_id <= 4) return prob.dtlz_id;
     if (prob.name == "lsmop1") return TEMO_B200_LSMOP1;
+    if (prob.name == "toy2") return TEMO_B200_TOY2;
+    if (prob.name == "toy3") return TEMO_B200_TOY3;
     throw std::invalid_argument("temo::b200: problem '" + prob.name + "' has no device evaluator");
 }
 
@@ -146,12 +148,21 @@ inline Tensor2D dtlz_eval(int id, const Tensor2D& x, std::size_t m) {
     return f;
 }
 
-/// A ProblemInstance whose evaluate() runs on the device (drop-in for make_problem("dtlzN", ...)).
-inline ProblemInstance make_problem(const std::string& name, std::size_t dim = 0, std::size_t m = 3) {
-    ProblemInstance p = temo::make_problem(name, dim, m);
-    const int id = p.dtlz_id;
+/// A ProblemInstance whose evaluate() runs on the device (drop-in for make_problem: dtlz1..dtlz4, toy2, toy3).
+inline ProblemInstance make_problem(const std::string& name, std::size_t dim = 0, std::size_t m = 3, std::size_t toy_horizon = 100) {
+    ProblemInstance p = temo::make_problem(name, dim, m, toy_horizon);
     const std::size_t mm = p.num_obj;
-    p.evaluate = [id, mm](const Tensor2D& x) { return temo::b200::dtlz_eval(id, x, mm); };
+    if (p.dtlz_id != 0) {
+        const int id = p.dtlz_id;
+        p.evaluate = [id, mm](const Tensor2D& x) { return temo::b200::dtlz_eval(id, x, mm); };
+    } else {  // toy2 / toy3: the negated returns of env_rollout (problems.hpp:288-292)
+        const int id = name == "toy2" ? TEMO_B200_TOY2 : TEMO_B200_TOY3;
+        p.evaluate = [id, mm, toy_horizon](const Tensor2D& x) {
+            Tensor2D f(x.rows, mm);
+            detail::check(temo_b200_evaluate_h(id, x.data.data(), x.rows, x.cols, mm, toy_horizon, f.data.data()));
+            return f;
+        };
+    }
     return p;
 }
 
@@ -213,6 +224,26 @@ inline Tensor2D apd_scores(const Tensor2D& f, const RefVectorSet& refs, std::siz
     return scores;
 }
 
+/// env_rollout (problems.hpp:211-241): n x d flat MLP parameters -> n x num_obj returns (maximisation orientation).
+inline Tensor2D env_rollout(const Tensor2D& params, const ToyEnvSpec& spec, const MlpArch& arch) {
+    temo::detail::require(params.cols == arch.param_count(), "env_rollout: parameter length mismatch");
+    temo::detail::require(arch.obs_dim == toy_obs_dim && arch.act_dim == toy_act_dim, "env_rollout: arch does not match the environment");
+    temo::detail::require(arch.hidden <= 64, "env_rollout: hidden layer too wide");
+    Tensor2D f(params.rows, spec.num_obj);
+    detail::check(temo_b200_env_rollout(params.data.data(), params.rows, params.cols, arch.hidden, spec.horizon, spec.num_obj,
+                                        f.data.data()));
+    return f;
+}
+
+/// mlp_forward (problems.hpp:149-163) for a batch: individual i (row i of params) acts on observation i.
+inline Tensor2D mlp_forward(const Tensor2D& params, const MlpArch& arch, const Tensor2D& obs) {
+    temo::detail::require(params.cols == arch.param_count(), "mlp_decode: length mismatch");
+    temo::detail::require(obs.rows == params.rows && obs.cols == toy_obs_dim, "mlp_forward: observations must be n x 4");
+    Tensor2D act(params.rows, toy_act_dim);
+    detail::check(temo_b200_mlp_forward(params.data.data(), params.rows, params.cols, arch.hidden, obs.data.data(), act.data.data()));
+    return act;
+}
+
 // ---- algorithms.hpp --------------------------------------------------------------------------
 /// rvea_run (algorithms.hpp:227-296), device-resident for the whole run; cfg.op = ga / de / pso / cso / random
 /// (algorithms.hpp:250-271). cfg.track_archive keeps the Archive in HBM (algorithms.hpp:243, 282) and fills
@@ -245,6 +276,7 @@ inline RunRecord rvea_run(const ProblemInstance& prob, const RunConfig& cfg, con
     c.fr = cfg.fr;
     c.time_budget_s = cfg.time_budget_s;
     c.ga = detail::ga_of(cfg.ga);
+    c.horizon = cfg.horizon;
     const std::size_t h = cfg.lattice_h ? cfg.lattice_h : lattice_density_for(prob.num_obj, cfg.pop);
     const std::size_t cap = std::max<std::size_t>(cfg.pop, lattice_count(prob.num_obj, h));
     Tensor2D x(cap, prob.dim), f(cap, prob.num_obj);

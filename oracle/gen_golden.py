@@ -56,9 +56,41 @@ def operator_instance(ref, g, n_min, n_max, d_max):
     return n, d, lower, upper, x
 
 
+def toyenv_fixture(ref):
+    """MLP policy + toy control environment (problems.hpp:105-241) and short RVEA runs on toy2 / toy3 (a second-round
+    fixture, written by `python -m oracle.gen_golden toyenv` without touching the others)."""
+    te = {}
+    g = Stream(ref, 9400)
+    p = g.tensor(40, 114) * 2.0 - 1.0
+    p[7, 3] = np.nan        # problems.hpp:224-230: non-finite parameters score -1e9
+    p[9, 113] = np.inf
+    te["params"] = p
+    for T, m in ((100, 2), (100, 3), (1, 2), (37, 3)):
+        te[f"ret_T{T}_m{m}"] = ref.env_rollout(p, T, m)
+    p64 = g.tensor(6, 4 * 64 + 64 + 2 * 64 + 2) * 6.0 - 3.0   # the widest network env_rollout accepts, saturating tanh
+    te["params_h64"] = p64
+    te["ret_h64"] = ref.env_rollout(p64, 50, 3, hidden=64)
+    obs = g.tensor(40, 4) * 4.0 - 2.0
+    ok = np.isfinite(p).all(axis=1)
+    te["obs"] = obs
+    te["act"] = ref.mlp_forward(np.where(np.isfinite(p), p, 0.0), obs)
+    te["f_toy2"] = ref.evaluate("toy2", p[ok], 2)              # make_problem's evaluate: the negated returns
+    te["f_toy3_T20"] = ref.evaluate("toy3", p[ok], 3, horizon=20)
+    for tag, (problem, m, n, gens, seed) in (("run2", ("toy2", 2, 40, 12, 5)), ("run3", ("toy3", 3, 66, 10, 8))):
+        rr = ref.rvea_run(problem, n, 114, m, gens, seed=seed)
+        te[f"{tag}_pop"] = rr["pop_size"]
+        te[f"{tag}_x"] = rr["x"]
+        te[f"{tag}_f"] = rr["f"]
+    np.savez(os.path.join(OUT, "toyenv.npz"), **te)
+
+
 def main():
+    import sys
     ref = Ref()
     os.makedirs(OUT, exist_ok=True)
+    if sys.argv[1:] == ["toyenv"]:
+        toyenv_fixture(ref)
+        return
 
     # ---- rng -----------------------------------------------------------------------
     seeds = np.array([0, 7, 42, 99, 2**63 + 12345], dtype=np.uint64)
@@ -242,6 +274,7 @@ def main():
         rr = ref.nsga2_run(problem, n, d, m, gens, seed=seed)
         ns.update({f"{tag}_x": rr["x"], f"{tag}_f": rr["f"]})
     np.savez(os.path.join(OUT, "nsga2.npz"), **ns)
+    toyenv_fixture(ref)
     total = sum(os.path.getsize(os.path.join(OUT, f)) for f in os.listdir(OUT))
     print(f"wrote {OUT}: {total/1024:.1f} KiB")
 

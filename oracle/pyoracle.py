@@ -27,7 +27,7 @@ f64p = C.POINTER(C.c_double)
 u64p = C.POINTER(C.c_uint64)
 u8p = C.POINTER(C.c_ubyte)
 
-PROBLEM_IDS = {"dtlz1": 1, "dtlz2": 2, "dtlz3": 3, "dtlz4": 4, "lsmop1": 101}
+PROBLEM_IDS = {"dtlz1": 1, "dtlz2": 2, "dtlz3": 3, "dtlz4": 4, "lsmop1": 101, "toy2": 201, "toy3": 202}
 GA_DEFAULT = (1.0, 20.0, 1.0, 20.0)  # pc, eta, pm, xi — operators.hpp:22-27
 OPP_DEFAULT = (0.5, 0.9, 0.4, 1.5, 1.5, 0.1)  # de.f, de.cr, pso.inertia, pso.c1, pso.c2, cso.phi — operators.hpp:28-41
 
@@ -244,6 +244,8 @@ class Oracle(_Base):
         pid = PROBLEM_IDS[problem]
         if pid == 101:
             rc = self.lib.to_lsmop1_eval(_p(x), u64(n), u64(d), u64(m), _p(f))
+        elif pid in (201, 202):
+            rc = self.lib.to_toy_eval(C.c_int(pid), _p(x), u64(n), u64(d), u64(m), u64(100), _p(f))
         else:
             rc = self.lib.to_dtlz_eval(C.c_int(pid), _p(x), u64(n), u64(d), u64(m), _p(f))
         if rc:
@@ -254,6 +256,21 @@ class Oracle(_Base):
         lo, hi = np.empty(d), np.empty(d)
         self.lib.to_problem_bounds(C.c_int(PROBLEM_IDS[problem]), u64(d), u64(m), _p(lo), _p(hi))
         return lo, hi
+
+    def env_rollout(self, params, horizon=100, num_obj=2, hidden=16):
+        """env_rollout (problems.hpp:211-241): returns in maximisation orientation."""
+        params = _f(params)
+        f = np.empty((params.shape[0], num_obj))
+        if self.lib.to_env_rollout(_p(params), u64(params.shape[0]), u64(params.shape[1]), u64(hidden), u64(horizon), u64(num_obj), _p(f)):
+            raise ValueError("env_rollout: parameter length mismatch")
+        return f
+
+    def mlp_forward(self, params, obs, hidden=16):
+        params, obs = _f(params), _f(obs)
+        act = np.empty((params.shape[0], 2))
+        for i in range(params.shape[0]):
+            self.lib.to_mlp_forward(_p(params[i]), u64(hidden), _p(obs[i]), _p(act[i : i + 1]))
+        return act
 
     # refvec
     def lattice_count(self, m, H):
@@ -593,18 +610,38 @@ class Ref(_Base):
     def polynomial_delta(self, u, x, lo, hi, xi):
         return self.lib.ref_polynomial_delta(u, x, lo, hi, xi)
 
-    def evaluate(self, problem, x, m):
+    def evaluate(self, problem, x, m, horizon=100):
         pid = PROBLEM_IDS[problem]
-        if pid > 4:
+        if pid == 101:
             raise NotImplementedError("the reference has no LSMOP1")
         x = _f(x)
         n, d = x.shape
         f = np.empty((n, m))
+        if pid > 4:  # toy2 / toy3 through make_problem(...).evaluate (the negated returns)
+            self._chk(self.lib.ref_problem_evaluate(problem.encode(), u64(d), u64(m), u64(horizon), _p(x), u64(n), _p(f), None, None,
+                                                    None, None))
+            return f
         self._chk(self.lib.ref_dtlz_eval(C.c_int(pid), _p(x), u64(n), u64(d), u64(m), _p(f)))
         return f
 
     def problem_bounds(self, problem, d, m):
+        if problem in ("toy2", "toy3"):
+            return -np.ones(d), np.ones(d)  # problems.hpp:285-286
         return np.zeros(d), np.ones(d)  # problems.hpp:271-272
+
+    def env_rollout(self, params, horizon=100, num_obj=2, hidden=16):
+        """The reference's env_rollout (problems.hpp:211-241): returns in maximisation orientation."""
+        params = _f(params)
+        f = np.empty((params.shape[0], num_obj))
+        self._chk(self.lib.ref_env_rollout(_p(params), u64(params.shape[0]), u64(hidden), u64(horizon), u64(num_obj), _p(f)))
+        return f
+
+    def mlp_forward(self, params, obs, hidden=16):
+        params, obs = _f(params), _f(obs)
+        act = np.empty((params.shape[0], 2))
+        for i in range(params.shape[0]):
+            self._chk(self.lib.ref_mlp_forward(_p(params[i]), u64(hidden), _p(obs[i]), _p(act[i : i + 1])))
+        return act
 
     def dtlz_pf_reference(self, pid, m, H):
         out = np.empty((self.lattice_count(m, H), m))

@@ -217,6 +217,36 @@ int ref_dtlz_eval(int id, const double* x, std::uint64_t n, std::uint64_t d, std
     return guarded([&] { unwrap(temo::dtlz_eval(id, wrap(x, n, d), m), f); });
 }
 
+// env_rollout / mlp_forward (problems.hpp:149-241) and make_problem("toy2"/"toy3").evaluate (:279-294)
+int ref_env_rollout(const double* params, std::uint64_t n, std::uint64_t hidden, std::uint64_t horizon, std::uint64_t num_obj,
+                    double* f) {
+    return guarded([&] {
+        const temo::MlpArch arch{temo::toy_obs_dim, hidden, temo::toy_act_dim};
+        unwrap(temo::env_rollout(wrap(params, n, arch.param_count()), temo::ToyEnvSpec{horizon, num_obj}, arch), f);
+    });
+}
+
+int ref_mlp_forward(const double* params, std::uint64_t hidden, const double* obs, double* action) {
+    return guarded([&] {
+        const temo::MlpArch arch{temo::toy_obs_dim, hidden, temo::toy_act_dim};
+        const temo::MlpWeights w = temo::mlp_decode({params, arch.param_count()}, arch);
+        temo::mlp_forward(w, {obs, temo::toy_obs_dim}, {action, temo::toy_act_dim});
+    });
+}
+
+// any registered problem through make_problem(name, dim, m, horizon).evaluate; lower / upper may be NULL
+int ref_problem_evaluate(const char* name, std::uint64_t dim, std::uint64_t m, std::uint64_t horizon, const double* x,
+                         std::uint64_t n, double* f, double* lower, double* upper, std::uint64_t* dim_out, std::uint64_t* m_out) {
+    return guarded([&] {
+        const temo::ProblemInstance prob = temo::make_problem(name, dim, m, horizon);
+        if (dim_out) *dim_out = prob.dim;
+        if (m_out) *m_out = prob.num_obj;
+        if (lower) unwrap(prob.lower, lower);
+        if (upper) unwrap(prob.upper, upper);
+        if (x && f && n) unwrap(prob.evaluate(wrap(x, n, prob.dim)), f);
+    });
+}
+
 int ref_dtlz_pf_reference(int id, std::uint64_t m, std::uint64_t H, double* out) {
     return guarded([&] { unwrap(temo::dtlz_pf_reference(id, m, H), out); });
 }

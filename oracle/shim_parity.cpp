@@ -255,6 +255,41 @@ static int archive_run_gpu() {
     return ok ? 0 : 1;
 }
 
+// MLP policy + toy environment through the shim: env_rollout, mlp_forward and make_problem("toy2" / "toy3").evaluate
+// bit-identical to the reference's, a whole rvea_run on toy3 identical to the reference's run.
+static int toyenv_gpu() {
+    int failed = 0;
+    RngStream g{9400, 0};
+    const MlpArch arch{toy_obs_dim, 16, toy_act_dim};
+    Tensor2D p = uniform_tensor(g, 300, arch.param_count());
+    for (double& v : p.data) v = 2.0 * v - 1.0;
+    p(5, 7) = std::numeric_limits<double>::quiet_NaN();
+    for (const std::size_t m : {std::size_t{2}, std::size_t{3}}) {
+        const ToyEnvSpec spec{m == 2 ? std::size_t{100} : std::size_t{41}, m};
+        failed += !same_bits(b200::env_rollout(p, spec, arch), env_rollout(p, spec, arch));
+    }
+    Tensor2D obs = uniform_tensor(g, 300, toy_obs_dim), act(300, toy_act_dim);
+    p(5, 7) = 0.25;
+    for (std::size_t i = 0; i < 300; ++i) {
+        const MlpWeights w = mlp_decode(p.row(i), arch);
+        mlp_forward(w, obs.row(i), act.row(i));
+    }
+    failed += !same_bits(b200::mlp_forward(p, arch, obs), act);
+    const ProblemInstance a = b200::make_problem("toy2", 0, 3, 60), b = make_problem("toy2", 0, 3, 60);
+    failed += !same_bits(a.evaluate(p), b.evaluate(p));
+    RunConfig cfg;
+    cfg.problem = "toy3";
+    cfg.pop = 66;
+    cfg.generations = 10;
+    cfg.seed = 8;
+    cfg.track_archive = false;
+    const ProblemInstance prob = make_problem("toy3");
+    const RunRecord ra = b200::rvea_run(prob, cfg), rb = rvea_run(prob, cfg);
+    failed += !(same_bits(ra.final_x, rb.final_x) && same_bits(ra.final_f, rb.final_f));
+    std::printf("toy environment (env_rollout, mlp_forward, make_problem, rvea_run on toy3; bit-exact): %d/6 failed\n", failed);
+    return failed;
+}
+
 int main() {
     if (temo_b200_device_count() < 1) {
         std::printf("no CUDA device\n");
@@ -269,6 +304,7 @@ int main() {
     failed += widened_suite_gpu() != 0;
     failed += operator_runs_gpu() != 0;
     failed += archive_run_gpu() != 0;
+    failed += toyenv_gpu() != 0;
     std::printf("%s\n", failed ? "SHIM PARITY FAILED" : "SHIM PARITY OK");
     return failed;
 }

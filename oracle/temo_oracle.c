@@ -419,6 +419,72 @@ int to_lsmop1_eval(const double* x, uint64_t n, uint64_t d, uint64_t m, double* 
     return 0;
 }
 
+/* MLP policy + toy control environment (problems.hpp:105-241). Parameters in the fixed order W1 (hidden x 4,
+ * row-major), b1, W2 (2 x hidden, row-major), b2 (mlp_decode, problems.hpp:126-138). */
+void to_mlp_forward(const double* p, uint64_t hidden, const double* obs, double* action) { /* problems.hpp:149-163 */
+    const double *w1 = p, *b1 = p + 4 * hidden, *w2 = b1 + hidden, *b2 = w2 + 2 * hidden;
+    double hid[64];
+    for (uint64_t i = 0; i < hidden; ++i) {
+        double s = b1[i];
+        for (uint64_t j = 0; j < 4; ++j) s += w1[i * 4 + j] * obs[j];
+        hid[i] = tanh(s);
+    }
+    for (uint64_t i = 0; i < 2; ++i) {
+        double s = b2[i];
+        for (uint64_t j = 0; j < hidden; ++j) s += w2[i * hidden + j] * hid[j];
+        action[i] = tanh(s);
+    }
+}
+
+/* env_rollout (problems.hpp:211-241) over toy_rollout (:176-206): n x d parameters -> n x num_obj returns
+ * (maximisation orientation); a row with a non-finite parameter scores -1e9 everywhere. */
+int to_env_rollout(const double* params, uint64_t n, uint64_t d, uint64_t hidden, uint64_t horizon, uint64_t num_obj, double* f) {
+    if (hidden < 1 || hidden > 64 || d != 4 * hidden + hidden + 2 * hidden + 2 || (num_obj != 2 && num_obj != 3)) return -1;
+    const double two_pi = 2.0 * 3.141592653589793238462643383279502884, h0 = 1.0;
+    for (uint64_t r = 0; r < n; ++r) {
+        const double* p = params + r * d;
+        double* fr = f + r * num_obj;
+        int finite = 1;
+        for (uint64_t k = 0; k < d; ++k)
+            if (!isfinite(p[k])) finite = 0;
+        if (!finite) {
+            for (uint64_t j = 0; j < num_obj; ++j) fr[j] = -1e9;
+            continue;
+        }
+        double v = 0.0, h = h0, fwd = 0.0, ctrl = 0.0, height = 0.0, obs[4], act[2];
+        for (uint64_t t = 0; t < horizon; ++t) {
+            const double phase = two_pi * (double)t / (double)horizon;
+            obs[0] = v;
+            obs[1] = h;
+            obs[2] = sin(phase);
+            obs[3] = cos(phase);
+            to_mlp_forward(p, hidden, obs, act);
+            v = 0.9 * v + 0.1 * act[0];
+            h = to_clip(0.95 * h + 0.1 * act[1], 0.0, 2.0);
+            fwd += v;
+            ctrl -= act[0] * act[0] + act[1] * act[1];
+            height += 10.0 * (h - h0);
+        }
+        fr[0] = fwd;
+        if (num_obj == 2) {
+            fr[1] = ctrl;
+        } else {
+            fr[1] = height;
+            fr[2] = ctrl;
+        }
+    }
+    return 0;
+}
+
+/* make_problem("toy2" / "toy3").evaluate (problems.hpp:279-294): MlpArch{4, 16, 2}, the negated returns */
+int to_toy_eval(int problem, const double* x, uint64_t n, uint64_t d, uint64_t m, uint64_t horizon, double* f) {
+    if (m != (problem == 201 ? 2u : 3u)) return -1;
+    const int rc = to_env_rollout(x, n, d, 16, horizon, m, f);
+    if (rc) return rc;
+    for (uint64_t e = 0; e < n * m; ++e) f[e] = -f[e];
+    return 0;
+}
+
 /* ------------------------------------------------------------- refvec.hpp */
 
 /* refvec.hpp:15-19: C(H+m-1, m-1) by the incremental product. */
@@ -650,11 +716,16 @@ int to_rv_select(const double* f, uint64_t n, uint64_t m, const double* v, const
 static int to_evaluate(int problem, const double* x, uint64_t n, uint64_t d, uint64_t m, double* f) {
     if (problem >= 1 && problem <= 4) return to_dtlz_eval(problem, x, n, d, m, f);
     if (problem == 101) return to_lsmop1_eval(x, n, d, m, f);
+    if (problem == 201 || problem == 202) return to_toy_eval(problem, x, n, d, m, 100, f);  /* RunConfig::horizon default */
     return -1;
 }
 
 void to_problem_bounds(int problem, uint64_t d, uint64_t m, double* lower, double* upper) {
     if (problem == 101) { to_lsmop1_bounds(d, m, lower, upper); return; }
+    if (problem == 201 || problem == 202) { /* problems.hpp:285-286 */
+        for (uint64_t j = 0; j < d; ++j) { lower[j] = -1.0; upper[j] = 1.0; }
+        return;
+    }
     for (uint64_t j = 0; j < d; ++j) { lower[j] = 0.0; upper[j] = 1.0; }
 }
 

@@ -34,6 +34,7 @@ class RunConfigC(C.Structure):
         ("pop", u64), ("lattice_h", u64), ("generations", u64), ("seed", u64), ("dim", u64), ("obj", u64),
         ("alpha", C.c_double), ("fr", C.c_double), ("time_budget_s", C.c_double),
         ("ga", GaParamsC), ("fuse_eval", C.c_int32), ("op", C.c_int32), ("opp", OpParamsC),
+        ("horizon", u64),
     ]
 
 
@@ -67,6 +68,9 @@ SIGNATURES = {
                                           f64p, f64p, C.c_int, f64p, f64p]),
     "temo_b200_cso_reproduce": (C.c_int, [f64p, f64p, u64, u64, u64, u64p, C.c_double, f64p, f64p, f64p, C.c_int, f64p, f64p]),
     "temo_b200_evaluate": (C.c_int, [C.c_int, f64p, u64, u64, u64, f64p]),
+    "temo_b200_evaluate_h": (C.c_int, [C.c_int, f64p, u64, u64, u64, u64, f64p]),
+    "temo_b200_env_rollout": (C.c_int, [f64p, u64, u64, u64, u64, u64, f64p]),
+    "temo_b200_mlp_forward": (C.c_int, [f64p, u64, u64, u64, f64p, f64p]),
     "temo_b200_problem_bounds": (C.c_int, [C.c_int, u64, u64, f64p, f64p]),
     "temo_b200_problem_default_dim": (u64, [C.c_int, u64]),
     "temo_b200_lattice_count": (u64, [u64, u64]),
@@ -138,6 +142,7 @@ SIGNATURES = {
     "temo_b200_shard_commit": (C.c_int, [_RUN, u64, C.POINTER(C.c_uint32), u64, u64]),
     "temo_b200_shard_download": (C.c_int, [_RUN, C.POINTER(C.c_uint32), u64, f64p, u64, f64p, f64p, f64p]),
     "temo_b200_pow": (C.c_int, [f64p, f64p, u64, f64p, C.c_int]),
+    "temo_b200_tanh": (C.c_int, [f64p, u64, f64p, C.c_int]),
     "temo_b200_flush_l2": (C.c_int, []),
     "temo_b200_set_option": (C.c_int, [C.c_char_p, C.c_long]),
 }

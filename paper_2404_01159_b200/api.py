@@ -32,7 +32,8 @@ import numpy as np
 from . import _lib
 from ._lib import GaParamsC, RunConfigC, TemoB200Error, f64p, u64, u64p, u8p
 
-PROBLEM_IDS = {"dtlz1": 1, "dtlz2": 2, "dtlz3": 3, "dtlz4": 4, "lsmop1": 101}
+PROBLEM_IDS = {"dtlz1": 1, "dtlz2": 2, "dtlz3": 3, "dtlz4": 4, "lsmop1": 101, "toy2": 201, "toy3": 202}
+TOY_HIDDEN = 16  # make_problem's MlpArch{4, 16, 2} (problems.hpp:280)
 RNG_SPLITMIX64, RNG_PHILOX = 0, 1
 
 
@@ -75,6 +76,14 @@ def pow_like_host(x, y, on_device: bool = True) -> np.ndarray:
     x, y = _t(x).reshape(-1), _t(y).reshape(-1)
     out = np.empty_like(x)
     _call(_lib.load().temo_b200_pow, _p(x), _p(y), u64(x.size), _p(out), 1 if on_device else 0)
+    return out
+
+
+def tanh_like_host(x, on_device: bool = True) -> np.ndarray:
+    """tanh with the host libm's bits (csrc/glibc_tanh.cuh): the device kernel, or its host twin (no GPU needed)."""
+    x = _t(x).reshape(-1)
+    out = np.empty_like(x)
+    _call(_lib.load().temo_b200_tanh, _p(x), u64(x.size), _p(out), 1 if on_device else 0)
     return out
 
 
@@ -266,15 +275,44 @@ def cso_reproduce(x, scores, stream: RngStream, p: CsoParams, lower, upper, stat
 
 
 # -------------------------------------------------------------------------- problems.hpp
-def evaluate(problem: str | int, x, m: int) -> np.ndarray:
+def evaluate(problem: str | int, x, m: int, horizon: int = 100) -> np.ndarray:
+    """ProblemInstance::evaluate of make_problem(problem, d, m, horizon) (problems.hpp:261-296), minimisation orientation."""
     pid = PROBLEM_IDS[problem] if isinstance(problem, str) else int(problem)
     x = _t(x)
     if x.ndim != 2:
         raise ValueError("evaluate: x must be a 2-D tensor")
     n, d = x.shape
     f = np.empty((n, m))
-    _call(_lib.load().temo_b200_evaluate, pid, _p(x), u64(n), u64(d), u64(m), _p(f))
+    _call(_lib.load().temo_b200_evaluate_h, pid, _p(x), u64(n), u64(d), u64(m), u64(horizon), _p(f))
     return f
+
+
+def mlp_param_count(hidden: int = TOY_HIDDEN) -> int:
+    """reference: MlpArch::param_count (problems.hpp:113-115) for obs_dim 4, act_dim 2."""
+    return 4 * hidden + hidden + hidden * 2 + 2
+
+
+def env_rollout(params, horizon: int = 100, num_obj: int = 2, hidden: int = TOY_HIDDEN) -> np.ndarray:
+    """reference: env_rollout (problems.hpp:211-241): n x d flat MLP parameters -> n x num_obj returns (maximisation)."""
+    params = _t(params)
+    if params.ndim != 2 or params.shape[1] != mlp_param_count(hidden):
+        raise ValueError("env_rollout: parameter length mismatch")
+    n, d = params.shape
+    f = np.empty((n, num_obj))
+    _call(_lib.load().temo_b200_env_rollout, _p(params), u64(n), u64(d), u64(hidden), u64(horizon), u64(num_obj), _p(f))
+    return f
+
+
+def mlp_forward(params, obs, hidden: int = TOY_HIDDEN) -> np.ndarray:
+    """reference: mlp_forward (problems.hpp:149-163), batched: individual i on observation i; n x 4 -> n x 2."""
+    params, obs = _t(params), _t(obs)
+    if params.ndim != 2 or params.shape[1] != mlp_param_count(hidden):
+        raise ValueError("mlp_decode: length mismatch")
+    if obs.shape != (params.shape[0], 4):
+        raise ValueError("mlp_forward: observations must be n x 4")
+    act = np.empty((params.shape[0], 2))
+    _call(_lib.load().temo_b200_mlp_forward, _p(params), u64(params.shape[0]), u64(params.shape[1]), u64(hidden), _p(obs), _p(act))
+    return act
 
 
 def dtlz_eval(id: int, x, m: int) -> np.ndarray:
@@ -296,24 +334,30 @@ class ProblemInstance:
     pf_extent: float = 1.0
     maximization: bool = False
     problem_id: int = 0
+    horizon: int = 100  # toy environments: make_problem's toy_horizon
 
     def evaluate(self, x) -> np.ndarray:
-        return evaluate(self.problem_id, x, self.num_obj)
+        return evaluate(self.problem_id, x, self.num_obj, self.horizon)
 
 
-def make_problem(name: str, dim: int = 0, m: int = 3) -> ProblemInstance:
-    """reference: make_problem (problems.hpp:261-296) for the DTLZ family, plus 'lsmop1'."""
+def make_problem(name: str, dim: int = 0, m: int = 3, toy_horizon: int = 100) -> ProblemInstance:
+    """reference: make_problem (problems.hpp:261-296): dtlz1..dtlz4, toy2, toy3, plus 'lsmop1' (an extension)."""
     if name not in PROBLEM_IDS:
         raise ValueError(f"make_problem: unknown problem '{name}'")
     pid = PROBLEM_IDS[name]
     L = _lib.load()
+    toy = name in ("toy2", "toy3")
+    if toy:
+        m = 2 if name == "toy2" else 3
+        if dim not in (0, mlp_param_count()):
+            raise ValueError("make_problem: toy env dimension is fixed")
     d = dim or int(L.temo_b200_problem_default_dim(pid, u64(m)))
     if d < m:
         raise ValueError("make_problem: DTLZ needs d >= m")
     lo, hi = np.empty(d), np.empty(d)
     _call(L.temo_b200_problem_bounds, pid, u64(d), u64(m), _p(lo), _p(hi))
     return ProblemInstance(name, d, m, lo, hi, dtlz_id=pid if pid <= 4 else 0,
-                           pf_extent=0.5 if pid == 1 else 1.0, problem_id=pid)
+                           pf_extent=0.5 if pid == 1 else 1.0, problem_id=pid, maximization=toy, horizon=toy_horizon)
 
 
 # ---------------------------------------------------------------------------- refvec.hpp
@@ -434,6 +478,7 @@ class RunConfig:
     cso: tuple = (0.1,)            # CsoParams {phi}, operators.hpp:39-41
     rng_mode: int = RNG_SPLITMIX64
     fuse_eval: bool = True
+    horizon: int = 100             # algorithms.hpp:35 (toy environments)
     track_archive: bool = False    # algorithms.hpp:31
     archive_cap: int = 0           # algorithms.hpp:32 (0: unbounded)
     archive_history: bool = False  # algorithms.hpp:33
@@ -456,6 +501,7 @@ class RunConfig:
         cfg.opp.de_f, cfg.opp.de_cr = self.de
         cfg.opp.pso_inertia, cfg.opp.pso_c1, cfg.opp.pso_c2 = self.pso
         (cfg.opp.cso_phi,) = self.cso
+        cfg.horizon = self.horizon
         return cfg
 
 
@@ -787,7 +833,7 @@ class Nsga2Run:
 
 def nsga2_run(prob: ProblemInstance, cfg: RunConfig) -> RunRecord:
     """reference: nsga2_run (algorithms.hpp:301-369), track_archive = false."""
-    cfg = RunConfig(**{**cfg.__dict__, "problem": prob.name, "dim": prob.dim, "obj": prob.num_obj})
+    cfg = RunConfig(**{**cfg.__dict__, "problem": prob.name, "dim": prob.dim, "obj": prob.num_obj, "horizon": prob.horizon})
     ccfg = cfg.c()
     x, f = np.empty((cfg.pop, prob.dim)), np.empty((cfg.pop, prob.num_obj))
     done = u64(0)
@@ -801,7 +847,7 @@ def rvea_run(prob: ProblemInstance, cfg: RunConfig, mc: MetricContext | None = N
     reference's ProblemInstance; the evaluator itself runs on the device. With a MetricContext every
     GenerationRow carries igd_value / hv_value of the population, or of the archive with cfg.track_archive
     (fill_metrics, algorithms.hpp:288); RunRecord.archive / archive_f_history as in the reference."""
-    cfg = RunConfig(**{**cfg.__dict__, "problem": prob.name, "dim": prob.dim, "obj": prob.num_obj})
+    cfg = RunConfig(**{**cfg.__dict__, "problem": prob.name, "dim": prob.dim, "obj": prob.num_obj, "horizon": prob.horizon})
     with_metrics = mc is not None and (mc.pf_ref is not None or mc.hv_ref is not None)
     if with_metrics or cfg.track_archive:
         t0 = time.perf_counter()

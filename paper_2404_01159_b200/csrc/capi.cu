@@ -89,6 +89,7 @@ RunConfig cfg_of(const temo_b200_run_config* c) {
     r.pso_c1 = c->opp.pso_c1;
     r.pso_c2 = c->opp.pso_c2;
     r.cso_phi = c->opp.cso_phi;
+    r.horizon = c->horizon ? c->horizon : 100;
     require(r.rng_mode == 0 || r.rng_mode == 1, "unknown rng mode");
     return r;
 }
@@ -195,6 +196,7 @@ void temo_b200_default_run_config(temo_b200_run_config* cfg) {
     cfg->opp.pso_c1 = 1.5;
     cfg->opp.pso_c2 = 1.5;
     cfg->opp.cso_phi = 0.1;
+    cfg->horizon = 100;  // algorithms.hpp:35
 }
 
 // ---- rng.hpp ------------------------------------------------------------------------------
@@ -388,6 +390,50 @@ int temo_b200_evaluate(int problem, const double* x, uint64_t n, uint64_t d, uin
         a.d = d;
         a.m = m;
         a.f = df.p;
+        launch_evaluate(a, s);
+        df.to_host(f, s);
+        TEMO_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+// env_rollout (problems.hpp:211-241): returns in maximisation orientation, -1e9 for non-finite parameter rows
+int temo_b200_env_rollout(const double* params, uint64_t n, uint64_t d, uint64_t hidden, uint64_t horizon, uint64_t num_obj, double* f) {
+    return guarded([&] {
+        require(params && f, "env_rollout: null argument");
+        cudaStream_t s = ctx().stream;
+        DevBuf<double> dx(params, n * d, s), df(n * num_obj);
+        launch_env_rollout(dx.p, nullptr, n, d, hidden, horizon, num_obj, /*negate=*/false, df.p, 0, nullptr, s);
+        df.to_host(f, s);
+        TEMO_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+// mlp_forward (problems.hpp:149-163), batched: individual i acts on observation i (obs n x 4 -> action n x 2)
+int temo_b200_mlp_forward(const double* params, uint64_t n, uint64_t d, uint64_t hidden, const double* obs, double* action) {
+    return guarded([&] {
+        require(params && obs && action, "mlp_forward: null argument");
+        cudaStream_t s = ctx().stream;
+        DevBuf<double> dx(params, n * d, s), dobs(obs, n * 4, s), dact(n * 2);
+        launch_mlp_forward(dx.p, n, d, hidden, dobs.p, dact.p, s);
+        dact.to_host(action, s);
+        TEMO_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+// problem evaluators with an episode length (toy2 / toy3; ignored by the others): make_problem(name, dim, m, horizon)
+int temo_b200_evaluate_h(int problem, const double* x, uint64_t n, uint64_t d, uint64_t m, uint64_t horizon, double* f) {
+    return guarded([&] {
+        require(x && f, "evaluate: null argument");
+        cudaStream_t s = ctx().stream;
+        DevBuf<double> dx(x, n * d, s), df(n * m);
+        EvalArgs a;
+        a.problem = problem;
+        a.x = dx.p;
+        a.n = n;
+        a.d = d;
+        a.m = m;
+        a.f = df.p;
+        a.horizon = horizon;
         launch_evaluate(a, s);
         df.to_host(f, s);
         TEMO_CUDA(cudaStreamSynchronize(s));
@@ -936,6 +982,21 @@ int temo_b200_pow(const double* x, const double* y, uint64_t n, double* out, int
         cudaStream_t s = cx.stream;
         DevBuf<double> dx(x, n, s), dy(y, n, s), dout(n);
         launch_pow_batch(dx.p, dy.p, n, dout.p, s);
+        dout.to_host(out, s);
+        TEMO_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int temo_b200_tanh(const double* x, uint64_t n, double* out, int on_device) {
+    return guarded([&] {
+        require(x && out, "tanh: null argument");
+        if (!on_device) {
+            tanh_batch_host(x, n, out);
+            return;
+        }
+        cudaStream_t s = ctx().stream;
+        DevBuf<double> dx(x, n, s), dout(n);
+        launch_tanh_batch(dx.p, n, dout.p, s);
         dout.to_host(out, s);
         TEMO_CUDA(cudaStreamSynchronize(s));
     });

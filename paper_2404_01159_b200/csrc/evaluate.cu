@@ -360,6 +360,11 @@ void launch_dtlz_finish(int problem, double* f, uint64_t n, uint64_t m, uint64_t
 
 void launch_evaluate(const EvalArgs& a, cudaStream_t s) {
     require(problem_known(a.problem), "evaluate: unknown problem");
+    if (a.problem == kToy2 || a.problem == kToy3) {  // make_problem's toy evaluators (problems.hpp:279-294): negated returns
+        require(a.m == (a.problem == kToy2 ? 2u : 3u), "make_problem: toy2 has 2 objectives, toy3 has 3");
+        launch_env_rollout(a.x, a.rows, a.n, a.d, kToyHidden, a.horizon, a.m, /*negate=*/true, a.f, a.f_row0, a.f_row0_dev, s);
+        return;
+    }
     if (a.problem <= kDtlz4) require(a.problem >= 1, "dtlz_eval: id must be in 1..4");  // problems.hpp:70
     require(a.m >= 2, "dtlz_eval: m must be at least 2");                                // problems.hpp:71
     require(a.d >= a.m, "dtlz_eval: d must be at least m");                              // problems.hpp:72

@@ -92,11 +92,17 @@ double apd_penalty(uint64_t m, uint64_t t, uint64_t t_max, double alpha) {
     return (double)m * std::pow((double)t / (double)t_max, alpha);
 }
 
-bool problem_known(int problem) { return (problem >= kDtlz1 && problem <= kDtlz4) || problem == kLsmop1; }
+bool problem_known(int problem) {
+    return (problem >= kDtlz1 && problem <= kDtlz4) || problem == kLsmop1 || problem == kToy2 || problem == kToy3;
+}
 
 // problems.hpp:266-272 (DTLZ: [0,1]^d); LSMOP1: position genes [0,1], tail genes [0,10].
 void problem_bounds(int problem, uint64_t d, uint64_t m, double* lower, double* upper) {
     require(problem_known(problem), "make_problem: unknown problem");
+    if (problem == kToy2 || problem == kToy3) {  // problems.hpp:285-286: MLP parameters in [-1, 1]
+        for (uint64_t j = 0; j < d; ++j) lower[j] = -1.0, upper[j] = 1.0;
+        return;
+    }
     for (uint64_t j = 0; j < d; ++j) {
         lower[j] = 0.0;
         upper[j] = (problem == kLsmop1 && j + 1 >= m) ? 10.0 : 1.0;
@@ -107,6 +113,7 @@ void problem_bounds(int problem, uint64_t d, uint64_t m, double* lower, double* 
 uint64_t problem_default_dim(int problem, uint64_t m) {
     if (problem == kDtlz1) return 7;
     if (problem >= kDtlz2 && problem <= kDtlz4) return 12;
+    if (problem == kToy2 || problem == kToy3) return mlp_param_count(kToyHidden);  // problems.hpp:283
     return 100 * m;
 }
 

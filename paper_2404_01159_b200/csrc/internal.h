@@ -10,7 +10,8 @@
 namespace temo_b200 {
 
 // Problem ids (mirrors include/temo_b200.h).
-constexpr int kDtlz1 = 1, kDtlz2 = 2, kDtlz3 = 3, kDtlz4 = 4, kLsmop1 = 101;
+constexpr int kDtlz1 = 1, kDtlz2 = 2, kDtlz3 = 3, kDtlz4 = 4, kLsmop1 = 101, kToy2 = 201, kToy3 = 202;
+constexpr uint64_t kToyHidden = 16;  // make_problem's MlpArch{4, 16, 2} (problems.hpp:280)
 constexpr int kMaxObj = 32;   // objectives supported by the on-device evaluators/selection
 constexpr int kLsmopNk = 5;
 
@@ -113,12 +114,22 @@ struct EvalArgs {
     uint64_t f_row0 = 0;
     const uint32_t* f_row0_dev = nullptr;
     bool allow_tma = true;
+    uint64_t horizon = 100;         // toy2 / toy3: episode length (RunConfig::horizon, algorithms.hpp:35)
 };
 void launch_evaluate(const EvalArgs& a, cudaStream_t s);
 // "eval_tma" (1 default; 0: the one-CTA-per-row kernels only); false for an unknown name
 bool set_eval_option(const char* name, long value);
 // second half of the streaming evaluators: rows holding {tail sum, position genes} -> objectives
 void launch_dtlz_finish(int problem, double* f, uint64_t n, uint64_t m, uint64_t d, uint64_t f_row0, cudaStream_t s);
+
+// ---- neuroevolution evaluator (toyenv.cu) ----------------------------------------------
+uint64_t mlp_param_count(uint64_t hidden);
+void launch_tanh_batch(const double* x, uint64_t n, double* out, cudaStream_t s);
+void tanh_batch_host(const double* x, uint64_t n, double* out);
+void launch_env_rollout(const double* params, const uint32_t* rows, uint64_t n, uint64_t d, uint64_t hidden, uint64_t horizon,
+                        uint64_t m, bool negate, double* f, uint64_t f_row0, const uint32_t* f_row0_dev, cudaStream_t s);
+void launch_mlp_forward(const double* params, uint64_t n, uint64_t d, uint64_t hidden, const double* obs, double* action,
+                        cudaStream_t s);
 
 // ---- K3: selection ----------------------------------------------------------------------------
 struct SelectWorkspace {

@@ -168,6 +168,10 @@ Nsga2Run::Nsga2Run(const RunConfig& c) : cfg(c) {
     require(cfg.obj >= 2 && cfg.obj <= (uint64_t)kMaxObj, "nsga2_run: objective count out of range");
     n = cfg.pop;
     m = cfg.obj;
+    if (cfg.problem == kToy2 || cfg.problem == kToy3) {  // problems.hpp:279-287: the environment fixes m and d
+        m = cfg.problem == kToy2 ? 2 : 3;
+        require(cfg.dim == 0 || cfg.dim == problem_default_dim(cfg.problem, m), "make_problem: toy env dimension is fixed");
+    }
     d = cfg.dim ? cfg.dim : problem_default_dim(cfg.problem, m);
     require(d >= m, "make_problem: DTLZ needs d >= m");
     require(2 * n < 0xffffffffULL, "nsga2_run: population too large");
@@ -199,6 +203,7 @@ Nsga2Run::Nsga2Run(const RunConfig& c) : cfg(c) {
     ea.n = n;
     ea.d = d;
     ea.m = m;
+    ea.horizon = cfg.horizon;
     ea.f = fm;
     launch_evaluate(ea, stream);
     TEMO_CUDA(cudaMemcpyAsync(f_host.data(), fm, n * m * sizeof(double), cudaMemcpyDeviceToHost, stream));
@@ -307,6 +312,7 @@ void Nsga2Run::step(const double* f_off_inject) {
         ea.n = n;
         ea.d = d;
         ea.m = m;
+        ea.horizon = cfg.horizon;
         ea.f = fm;
         ea.f_row0 = n;
         launch_evaluate(ea, stream);

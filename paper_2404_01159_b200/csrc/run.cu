@@ -108,6 +108,10 @@ Run::Run(const RunConfig& c) : cfg(c) {
     if (cfg.op == kOpDe) require(cfg.pop >= 4, "de_reproduce: needs at least four rows");
     n = cfg.pop;
     m = cfg.obj;
+    if (cfg.problem == kToy2 || cfg.problem == kToy3) {  // problems.hpp:279-287: the environment fixes m and d
+        m = cfg.problem == kToy2 ? 2 : 3;
+        require(cfg.dim == 0 || cfg.dim == problem_default_dim(cfg.problem, m), "make_problem: toy env dimension is fixed");
+    }
     d = cfg.dim ? cfg.dim : problem_default_dim(cfg.problem, m);
     require(d >= m, "make_problem: DTLZ needs d >= m");  // problems.hpp:269
     H = cfg.lattice_h ? cfg.lattice_h : lattice_density_for(m, n);  // algorithms.hpp:233-235
@@ -188,6 +192,7 @@ Run::Run(const RunConfig& c) : cfg(c) {
     ea.n = n;
     ea.d = d;
     ea.m = m;
+    ea.horizon = cfg.horizon;
     ea.f = fm[0];
     launch_evaluate(ea, stream);
     P = n;
@@ -354,6 +359,7 @@ void Run::launch_offspring_eval() {
     ea.n = n;
     ea.d = d;
     ea.m = m;
+    ea.horizon = cfg.horizon;
     ea.f = fm[cur];
     ea.f_row0 = P;
     launch_evaluate(ea, stream);
@@ -468,6 +474,8 @@ void Run::inject(uint64_t rows, const double* x, const double* f, const double* 
         ea.n = rows;
         ea.d = d;
         ea.m = m;
+        ea.horizon = cfg.horizon;
+    ea.horizon = cfg.horizon;
         ea.f = fm[cur];
         launch_evaluate(ea, stream);
     }

@@ -20,6 +20,7 @@ struct RunConfig {  // reference: RunConfig, algorithms.hpp:21-41
     double de_f = 0.5, de_cr = 0.9;                          // DeParams, operators.hpp:28-31
     double pso_inertia = 0.4, pso_c1 = 1.5, pso_c2 = 1.5;    // PsoParams, operators.hpp:33-37
     double cso_phi = 0.1;                                    // CsoParams, operators.hpp:39-41
+    uint64_t horizon = 100;                                  // toy environments: episode length (algorithms.hpp:35)
 };
 constexpr int kOpGa = 0, kOpDe = 1, kOpPso = 2, kOpCso = 3, kOpRandom = 4;  // TEMO_B200_OP_*
 

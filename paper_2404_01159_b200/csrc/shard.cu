@@ -220,6 +220,7 @@ struct Shard {
         require(problem_known(cfg.problem), "make_problem: unknown problem");
         n = cfg.pop;
         m = cfg.obj;
+        if (cfg.problem == kToy2 || cfg.problem == kToy3) m = cfg.problem == kToy2 ? 2 : 3;  // problems.hpp:279-287
         d = cfg.dim ? cfg.dim : problem_default_dim(cfg.problem, m);
         require(n % (2 * (uint64_t)world) == 0, "shard: population must be divisible by 2 * world size");
         require(d >= m && m >= 2 && m <= (uint64_t)kMaxObj, "shard: bad problem shape");
@@ -281,6 +282,7 @@ struct Shard {
         ea.n = rows0;
         ea.d = d;
         ea.m = m;
+        ea.horizon = cfg.horizon;
         ea.f = f_off_loc;  // n/world = n_loc rows
         launch_evaluate(ea, stream);
         TEMO_CUDA(cudaMemsetAsync(used, 0, cap_loc, stream));
@@ -363,6 +365,7 @@ struct Shard {
             ea.n = n_loc;
             ea.d = d;
             ea.m = m;
+            ea.horizon = cfg.horizon;
             ea.f = f_off_loc;
             launch_evaluate(ea, stream);
         }
@@ -569,6 +572,7 @@ int temo_b200_shard_create(const temo_b200_run_config* cfg, int rank, int world,
         rc.ga.pm = cfg->ga.pm;
         rc.ga.xi = cfg->ga.xi;
         rc.fuse_eval = cfg->fuse_eval;
+        rc.horizon = cfg->horizon ? cfg->horizon : 100;
         *out = new temo_b200_shard{new Shard(rc, rank, world)};
     });
 }

@@ -51,9 +51,10 @@ def test_header_compiles_as_plain_c(tmp_path):
 def test_struct_layout_matches_header(lib):
     from paper_2404_01159_b200._lib import GaParamsC, RunConfigC
     assert C.sizeof(GaParamsC) == 32
-    assert C.sizeof(RunConfigC) == 8 + 6 * 8 + 3 * 8 + 32 + 8 + 6 * 8
+    assert C.sizeof(RunConfigC) == 8 + 6 * 8 + 3 * 8 + 32 + 8 + 6 * 8 + 8
     cfg = RunConfigC()
     lib.temo_b200_default_run_config(C.byref(cfg))
+    assert cfg.horizon == 100  # algorithms.hpp:35
     # reference defaults: RunConfig (algorithms.hpp:21-41), GaParams (operators.hpp:22-27)
     assert (cfg.pop, cfg.generations, cfg.seed, cfg.obj, cfg.alpha, cfg.fr) == (105, 100, 42, 3, 2.0, 0.1)
     assert (cfg.ga.pc, cfg.ga.eta, cfg.ga.pm, cfg.ga.xi) == (1.0, 20.0, 1.0, 20.0)

@@ -60,3 +60,35 @@ def test_device_pow_is_bit_exact_with_libm():
     exp = libm_pow(x, y)
     bad = got.view(np.uint64) != exp.view(np.uint64)
     assert not bad.any(), (x[bad][:5], y[bad][:5], got[bad][:5], exp[bad][:5])
+
+
+# ---- tanh (csrc/glibc_tanh.cuh): the toy environment's policy network chains 18 of them per step
+def libm_tanh(x):
+    libm = ctypes.CDLL("libm.so.6")
+    libm.tanh.restype = ctypes.c_double
+    libm.tanh.argtypes = [ctypes.c_double]
+    return np.array([libm.tanh(float(a)) for a in x])
+
+
+def tanh_domain(n, seed):
+    rng = np.random.default_rng(seed)
+    u = rng.uniform(-1.0, 1.0, (5, n))
+    special = np.array([0.0, -0.0, 1.0, -1.0, 22.0, -22.0, 21.999999, 0.34657359027997264, 1.0397207708399179, 19.4, 38.9, 1e-300,
+                        5e-324, 1e300, np.inf, -np.inf, 0.25, -0.25, 0.125, 2.0**-55, 2.0**-54, 0.5493061443340549])
+    return np.concatenate([u[0] * 25.0, u[1], u[2] * 0.35, u[3] * 3.0, np.ldexp(u[4], rng.integers(-60, 20, n)), special])
+
+
+def test_tanh_host_twin_is_bit_exact_with_libm():
+    import paper_2404_01159_b200 as tb
+    x = tanh_domain(60000, 3)
+    got, exp = tb.tanh_like_host(x, on_device=False), libm_tanh(x)
+    assert np.array_equal(got.view(np.uint64), exp.view(np.uint64))
+
+
+@pytest.mark.gpu
+def test_device_tanh_is_bit_exact_with_libm():
+    import paper_2404_01159_b200 as tb
+    x = tanh_domain(100000, 4)
+    got, exp = tb.tanh_like_host(x, on_device=True), libm_tanh(x)
+    bad = got.view(np.uint64) != exp.view(np.uint64)
+    assert not bad.any(), (x[bad][:5], got[bad][:5], exp[bad][:5])
