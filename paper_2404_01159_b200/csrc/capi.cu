@@ -471,7 +471,14 @@ int temo_b200_min_vector_angles(const double* v, uint64_t r, uint64_t m, double*
         DevBuf<uint32_t> err(1);
         TEMO_CUDA(cudaMemsetAsync(err.p, 0, sizeof(uint32_t), s));
         launch_row_norms(dv.p, r, m, dvn.p, s);
-        if (r >= kIndexMinVectors) {
+        if (assoc_filter_preferred(m, r)) {  // many objectives: the fp32-filtered exact scan (select.cu)
+            SelectWorkspace ws;
+            ws.alloc(r, r, m);
+            struct Guard { SelectWorkspace& w; ~Guard() { w.release(); } } guard{ws};
+            launch_row_norms(dv.p, r, m, ws.vn, s);
+            launch_gamma_filter(dv.p, r, m, ws, dg.p, err.p, nullptr, s);
+            TEMO_CUDA(cudaStreamSynchronize(s));
+        } else if (r >= kIndexMinVectors) {
             VecIndex index;
             index.alloc(r, m);
             struct Guard { VecIndex& x; ~Guard() { x.release(); } } guard{index};
@@ -514,7 +521,14 @@ int temo_b200_adapt(const double* v0, double* v, double* gamma, uint64_t r, uint
         DevBuf<uint32_t> flags(2);
         TEMO_CUDA(cudaMemsetAsync(flags.p, 0, 2 * sizeof(uint32_t), s));
         launch_adapt_vectors(dv0.p, dv.p, dvn.p, r, m, dzmin.p, dzmax.p, flags.p + 1, flags.p, s);
-        if (r >= kIndexMinVectors) {
+        if (assoc_filter_preferred(m, r)) {
+            SelectWorkspace ws;
+            ws.alloc(r, r, m);
+            struct Guard { SelectWorkspace& w; ~Guard() { w.release(); } } guard{ws};
+            TEMO_CUDA(cudaMemcpyAsync(ws.vn, dvn.p, r * sizeof(double), cudaMemcpyDeviceToDevice, s));
+            launch_gamma_filter(dv.p, r, m, ws, dg.p, flags.p, flags.p + 1, s);
+            TEMO_CUDA(cudaStreamSynchronize(s));
+        } else if (r >= kIndexMinVectors) {
             VecIndex index;
             index.alloc(r, m);
             struct Guard { VecIndex& x; ~Guard() { x.release(); } } guard{index};

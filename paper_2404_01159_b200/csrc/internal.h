@@ -153,6 +153,8 @@ struct SelectWorkspace {
     uint32_t* v32_flags = nullptr;    // [1] bit0: a vector component is negative / non-finite
     double* part_c = nullptr;         // [chunks x rows_cap] per-chunk winners of the filtered association (m >= 5 only)
     uint32_t* part_j = nullptr;
+    unsigned char* row_flag = nullptr;  // [rows_cap] rows of the filtered scan that need the exact fallback
+    float* seed32 = nullptr;            // [rows_cap] starting value of a row's running fp32 maximum (subsample scan)
     void alloc(uint64_t rows_cap_, uint64_t r_, uint64_t m_);
     void release();
 };
@@ -169,6 +171,12 @@ void launch_row_norms(const double* v, uint64_t r, uint64_t m, double* vn, cudaS
 bool assoc_filter_preferred(uint64_t m, uint64_t r);
 void launch_assoc_filter(const double* f, uint64_t n_rows, uint64_t m, const double* v, const double* gamma, uint64_t r, double penalty,
                          SelectWorkspace& ws, uint32_t* assoc, double* theta, double* apd, cudaStream_t s, uint32_t row0);
+// min_vector_angles through the same filtered scan (m >= 5); ws.vn must hold the norms of v. launch_gamma_auto picks the
+// filtered scan or the direction index (index may be nullptr only when the filter is preferred).
+void launch_gamma_filter(const double* v, uint64_t r, uint64_t m, SelectWorkspace& ws, double* gamma, uint32_t* err_flag,
+                         const uint32_t* skip_flag, cudaStream_t s);
+void launch_gamma_auto(const double* v, uint64_t r, uint64_t m, SelectWorkspace& ws, VecIndex* index, double* gamma,
+                       uint32_t* err_flag, const uint32_t* skip_flag, cudaStream_t s);
 // the stages of launch_select, separately (the sharded run puts collectives between them)
 void launch_select_prepare(const double* f, uint64_t n_rows, uint64_t m, const double* gamma, uint64_t r,
                            SelectWorkspace& ws, cudaStream_t s);

@@ -171,8 +171,8 @@ Run::Run(const RunConfig& c) : cfg(c) {
     launch_row_norms(v, r, m, ws.vn, stream);
     vindex.alloc(r, m);
     vindex.set_order(unit.data(), stream);
-    vindex.build(v, ws.vn, stream);
-    launch_gamma_indexed(v, ws.vn, r, m, vindex, gamma, ws.err_flag, nullptr, stream);
+    if (!assoc_filter_preferred(m, r)) vindex.build(v, ws.vn, stream);  // m >= 5: the fp32-filtered scans need no index
+    launch_gamma_auto(v, r, m, ws, &vindex, gamma, ws.err_flag, nullptr, stream);
 
     std::vector<double> lo(d), hi(d);
     problem_bounds(cfg.problem, d, m, lo.data(), hi.data());
@@ -413,8 +413,8 @@ uint64_t Run::step(double* survivors_f_host, const double* f_off_inject) {
     if ((t + 1) % adapt_every == 0) {
         launch_col_minmax(fm[cur ^ 1], pcap, d_P, m, zmin, zmax, zscratch, stream);
         launch_adapt_vectors(v0, v, ws.vn, r, m, zmin, zmax, skip_flag, ws.err_flag, stream);
-        vindex.build(v, ws.vn, stream);
-        launch_gamma_indexed(v, ws.vn, r, m, vindex, gamma, ws.err_flag, skip_flag, stream);
+        if (!assoc_filter_preferred(m, r)) vindex.build(v, ws.vn, stream);  // m >= 5: the fp32-filtered scans need no index
+        launch_gamma_auto(v, r, m, ws, &vindex, gamma, ws.err_flag, skip_flag, stream);
         launches += 6 + vindex.levels;
     }
     TEMO_CUDA(cudaEventRecord(ev[5], stream));
@@ -482,7 +482,7 @@ void Run::inject(uint64_t rows, const double* x, const double* f, const double* 
     if (v_in) {
         TEMO_CUDA(cudaMemcpy(v, v_in, r * m * sizeof(double), cudaMemcpyHostToDevice));
         launch_row_norms(v, r, m, ws.vn, stream);
-        vindex.build(v, ws.vn, stream);
+        if (!assoc_filter_preferred(m, r)) vindex.build(v, ws.vn, stream);  // m >= 5: the fp32-filtered scans need no index
     }
     if (gamma_in) TEMO_CUDA(cudaMemcpy(gamma, gamma_in, r * sizeof(double), cudaMemcpyHostToDevice));
     P = rows;
@@ -732,7 +732,7 @@ double Run::time_stage(int stage, int reps) {
             launch_reproduction(p, true);
             break;
         case 4: launch_select(fm[cur], P + n, nullptr, m, v, gamma, r, penalty, ws, stream, &vindex); break;
-        case 5: launch_gamma_indexed(v, ws.vn, r, m, vindex, gamma, ws.err_flag, nullptr, stream); break;
+        case 5: launch_gamma_auto(v, r, m, ws, &vindex, gamma, ws.err_flag, nullptr, stream); break;
         case 6: launch_select(fm[cur], P + n, nullptr, m, v, gamma, r, penalty, ws, stream, nullptr); break;
         case 7: launch_gamma(v, ws.vn, r, m, gamma, ws.err_flag, nullptr, stream); break;
         default: fail(1, "time_stage: unknown stage");

@@ -161,94 +161,201 @@ __global__ void __launch_bounds__(kAssocThreads) assoc_kernel(
 // For m >= 5 the direction index prunes little (in 10 dimensions every patch of the lattice is wide) and the exact scan
 // costs (rows x R) double-precision dots WITHOUT fused multiply-adds plus a divide per pair: 12 ms at BASELINE config #4
 // (131072 rows x 48620 vectors x 10), which is the FP64 pipe's peak. Here every pair is first scored in fp32
-// (cos32 = (u/|u|) . v / |v| with FFMA, half the instructions at twice the rate); only a pair whose fp32 score is within
-// kFilterTol of the row's running fp32 maximum is re-evaluated with the reference's exact fp64 expression
+// (cos32 = (u/|u|) . (v/|v|) with FFMA: 6.4e10 of them at config #4 = 1.7 ms at the FP32 peak); only a pair whose fp32
+// score is within kFilterTol of the row's running fp32 maximum is re-evaluated with the reference's exact fp64 expression
 // (selection.hpp:172-184), in ascending j with a strict >, so the result is the reference's first strict maximum.
 // Why this is exact: for non-negative u and v all terms of the dot product are non-negative, so the fp32 score has
-// relative error <= (m + 5) 2^-24 < 2.3e-6 (m <= 32); the running maximum never exceeds the final one, hence every j whose
-// exact cosine could reach the final exact maximum satisfies cos32_j >= max32 (1 - 2 * 2.3e-6) > running32 (1 - kFilterTol)
-// and is evaluated exactly. Rows or vector sets with a negative or non-finite component take the exact expression for
-// every j (threshold -inf).
+// relative error <= (m + 2) 2^-24 < 2.1e-6 (m <= 32: one rounding per input, one per FFMA); the running maximum never
+// exceeds the final one, hence every j whose exact cosine could reach the final exact maximum satisfies
+// cos32_j >= max32 (1 - 2 * 2.1e-6) > running32 (1 - kFilterTol) and is evaluated exactly. Rows or vector sets with a
+// negative, non-finite or fp32-unrepresentable component take the exact expression for every j (threshold -inf).
+// Shape of the scan (round 2): a thread keeps kFilterRows = 4 unit rows in registers and scores them against two vectors
+// per step (eight independent FFMA chains, the vectors read once per step as 128-bit shared-memory broadcasts); the
+// vectors are stored pre-normalised so that the score needs no scaling; the exact expression lives out of line and
+// reloads its operands (it runs for a few dozen of the 48620 vectors of a row). With SELF the rows are the vectors
+// themselves and j == row is skipped: the same scan gives gamma's max off-diagonal cosine (refvec.hpp:81-100).
 constexpr float kFilterTol = 1e-5f;
+constexpr float kFltMin = 1.17549435e-38f;
 constexpr int kFilterTile = 512;      // vectors per shared-memory tile
 constexpr int kFilterMaxChunks = 8;   // pieces the vector range is cut into (per-row winners merged afterwards)
-constexpr int kFilterThreads = 128;   // two rows per thread: 256 rows per CTA keeps the grid several waves deep
+constexpr int kFilterThreads = 128;
+constexpr int kFilterRows = 4;        // rows per thread: 512 rows per CTA
+#ifndef TEMO_FILTER_VECS
+#define TEMO_FILTER_VECS 4
+#endif
+constexpr int kFilterVecs = TEMO_FILTER_VECS;  // vectors per step: kFilterRows x kFilterVecs independent FFMA chains per thread
 
-// fp32 copy of the vectors: row j = {v_j[0..m-1], 1 / |v_j|, 0 ...} padded to a multiple of four floats (128-bit reads)
-__host__ __device__ inline uint64_t v32_stride(uint64_t m) { return (m + 1 + 3) / 4 * 4; }
+// fp32 copy of the unit vectors: row j = v_j / |v_j| padded with zeros to a multiple of four floats (128-bit reads)
+__host__ __device__ inline uint64_t v32_stride(uint64_t m) { return (m + 3) / 4 * 4; }
 
 __global__ void v32_kernel(const double* __restrict__ v, const double* __restrict__ vn, uint64_t r, uint64_t m, float* __restrict__ v32,
                            uint32_t* __restrict__ flags) {
     const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (j >= r) return;
     const uint64_t stride = v32_stride(m);
-    bool bad = false;
+    const double nrm = vn[j];
+    bool bad = !(nrm > 0.0) || !(nrm < INFINITY);
     for (uint64_t k = 0; k < m; ++k) {
         const double x = v[j * m + k];
-        const float x32 = (float)x;
-        v32[j * stride + k] = x32;
+        const double q = x / nrm;
+        const float q32 = (float)q;
+        v32[j * stride + k] = q32;
         if (!(x >= 0.0) || !(x < INFINITY)) bad = true;
-        // outside fp32's normal range the relative-error bound of the filter does not hold (inf * 0 = NaN scores, flushed terms)
-        if (x != 0.0 && !(x32 >= 1.17549435e-38f && x32 < INFINITY)) bad = true;
+        // outside fp32's normal range the relative-error bound of the filter does not hold (flushed or infinite terms)
+        if (x != 0.0 && !(q32 >= kFltMin && q32 < INFINITY)) bad = true;
     }
-    const double nrm = vn[j];
-    const float rinv32 = (float)(1.0 / nrm);
-    v32[j * stride + m] = rinv32;
-    for (uint64_t k = m + 1; k < stride; ++k) v32[j * stride + k] = 0.0f;
-    if (!(nrm > 0.0) || !(nrm < INFINITY)) bad = true;
-    if (!(rinv32 >= 1.17549435e-38f && rinv32 < INFINITY)) bad = true;
+    for (uint64_t k = m; k < stride; ++k) v32[j * stride + k] = 0.0f;
     if (bad) atomicOr(flags, 1u);
 }
 
-template <int M>
-__global__ void __launch_bounds__(kFilterThreads, 4) assoc_filter_kernel(
-    const double* __restrict__ f, uint64_t n_rows, const uint32_t* n_rows_dev, uint64_t m_rt, const double* __restrict__ z,
-    const double* __restrict__ v, const double* __restrict__ vn, const float* __restrict__ v32, const uint32_t* __restrict__ vflags,
-    uint64_t r, uint64_t chunk_vecs, double* __restrict__ part_c, uint32_t* __restrict__ part_j) {
-    // blockIdx.y = chunk of the vector range [y * chunk_vecs, (y + 1) * chunk_vecs): the per-row winners of the chunks are
-    // merged in ascending chunk order by assoc_filter_merge_kernel (strict >: the first strict maximum overall)
+// the reference's expression for one (row, vector) pair (selection.hpp:172-178 / refvec.hpp:89-92): ascending-k dot of the
+// translated row with v_j, divided by the product of the norms
+__device__ __noinline__ double exact_cosine(const double* __restrict__ frow, const double* __restrict__ z, const double* __restrict__ vj,
+                                            double nf, double vnj, int m) {
+    double dot = 0.0;
+    for (int k = 0; k < m; ++k) dot += (z ? frow[k] - z[k] : frow[k]) * vj[k];
+    return dot / (nf * vnj);
+}
+
+// Seed of the running threshold: the best fp32 score of a row over every kFilterSeedStep-th vector (6 % of the scan's
+// work). Any real score is a lower bound of the final maximum, so starting from it is as exact as starting from zero,
+// and with it only the handful of vectors that beat the subsample's best ever become candidates (a scan that starts
+// from zero sees a new running maximum ~ln(R) times per chunk: 38 % of the warp steps took the candidate branch).
+constexpr int kFilterSeedStep = 16;
+
+constexpr int kSeedRows = 2;  // rows per thread of the seed scan: twice the CTAs of the main scan (it has no chunks)
+
+template <int M, bool SELF>
+__global__ void __launch_bounds__(kFilterThreads) filter_seed_kernel(const double* __restrict__ f, uint64_t n_rows, uint64_t m_rt,
+                                                                     const double* __restrict__ z, const double* __restrict__ vn,
+                                                                     const float* __restrict__ v32, uint64_t r, float* __restrict__ seed,
+                                                                     const uint32_t* skip_flag) {
+    if (skip_flag && *skip_flag) return;
     constexpr int MM = M > 0 ? M : kMaxObj;
+    constexpr int R = kSeedRows;
     const int m = M > 0 ? M : (int)m_rt;
-    extern __shared__ __align__(16) float s_v32[];  // kFilterTile x stride: v_j[0..m-1], 1 / |v_j| in fp32, padding
-    const uint64_t n = n_rows_dev ? (uint64_t)*n_rows_dev : n_rows;
-    const bool v_ok = (*vflags & 1u) == 0;
-    uint64_t row[2];
-    bool live[2];
-    double fp[2][MM], nf[2], best_c[2];
-    float uf[2][MM], best32[2], thr[2];
-    uint32_t arg[2];
+    constexpr int SS = (MM + 3) / 4 * 4;
+    const int stride = M > 0 ? SS : (int)v32_stride(m);
+    extern __shared__ __align__(16) float s_v32[];  // kFilterTile subsampled unit vectors
+    uint32_t row[R];
+    float uf[R][MM], best[R];
 #pragma unroll
-    for (int t = 0; t < 2; ++t) {
-        row[t] = blockIdx.x * (uint64_t)(2 * kFilterThreads) + t * kFilterThreads + threadIdx.x;
-        live[t] = row[t] < n;
-        nf[t] = 0.0;
-        best_c[t] = -INFINITY;
-        arg[t] = 0;
-        bool filter = v_ok && live[t];
-        if (live[t]) {
+    for (int t = 0; t < R; ++t) {
+        row[t] = (uint32_t)(blockIdx.x * (uint64_t)(R * kFilterThreads) + t * kFilterThreads + threadIdx.x);
+        const bool live = row[t] < n_rows;
+        double fp[MM], s = 0.0;
+#pragma unroll
+        for (int k = 0; k < MM; ++k)
+            if (k < m) {
+                fp[k] = !live ? 0.0 : (SELF ? f[(uint64_t)row[t] * m + k] : f[(uint64_t)row[t] * m + k] - z[k]);
+                s += fp[k] * fp[k];
+            }
+        const double nf = !live ? 0.0 : (SELF ? vn[row[t]] : sqrt(s));
+#pragma unroll
+        for (int k = 0; k < MM; ++k) uf[t][k] = (float)((k < m && nf != 0.0) ? fp[k] / nf : 0.0);  // the scan's own conversion
+        best[t] = 0.0f;
+    }
+    const uint64_t n_sub = (r + kFilterSeedStep - 1) / kFilterSeedStep;  // vectors 0, 16, 32, ...
+    for (uint64_t q0 = 0; q0 < n_sub; q0 += kFilterTile) {
+        const int tile = (int)((n_sub - q0) < (uint64_t)kFilterTile ? (n_sub - q0) : kFilterTile);
+        __syncthreads();
+        for (int e = threadIdx.x; e < tile * stride / 4; e += blockDim.x) {
+            const int jj = e / (stride / 4), part = e - jj * (stride / 4);
+            reinterpret_cast<float4*>(s_v32)[e] = __ldg(reinterpret_cast<const float4*>(v32 + (q0 + jj) * kFilterSeedStep * stride) + part);
+        }
+        __syncthreads();
+#pragma unroll 2
+        for (int jj = 0; jj < tile; ++jj) {
+            float vr[SS];
+            const float4* p4 = reinterpret_cast<const float4*>(s_v32 + jj * stride);
+#pragma unroll
+            for (int k4 = 0; k4 < SS / 4; ++k4)
+                if (4 * k4 < m) {
+                    const float4 t4 = p4[k4];
+                    vr[4 * k4] = t4.x, vr[4 * k4 + 1] = t4.y, vr[4 * k4 + 2] = t4.z, vr[4 * k4 + 3] = t4.w;
+                }
+            float sc[R];
+#pragma unroll
+            for (int t = 0; t < R; ++t) sc[t] = 0.0f;
+#pragma unroll
+            for (int k = 0; k < MM; ++k)
+                if (k < m) {
+#pragma unroll
+                    for (int t = 0; t < R; ++t) sc[t] = fmaf(uf[t][k], vr[k], sc[t]);
+                }
+            const uint32_t j = (uint32_t)((q0 + jj) * kFilterSeedStep);
+#pragma unroll
+            for (int t = 0; t < R; ++t)
+                if (!(SELF && j == row[t])) best[t] = fmaxf(best[t], sc[t]);  // a NaN score (bad vector set: filter off) is ignored
+        }
+    }
+#pragma unroll
+    for (int t = 0; t < R; ++t)
+        if (row[t] < n_rows) seed[row[t]] = best[t];
+}
+
+// Candidates of a row: vectors whose fp32 score reached the row's running threshold. Their exact evaluation is deferred
+// to the end of the scan - the threshold only depends on the fp32 scores - when most of them have fallen below the final
+// threshold and are dropped: a few exact evaluations per row remain instead of one per running-maximum record.
+constexpr int kFilterCand = 6;  // candidate slots per row (pruned against the risen threshold when full)
+
+template <int M, bool SELF>
+__global__ void __launch_bounds__(kFilterThreads, 4) assoc_filter_kernel(
+    const double* __restrict__ f, uint64_t n_rows, uint64_t m_rt, const double* __restrict__ z, const double* __restrict__ v,
+    const double* __restrict__ vn, const float* __restrict__ v32, const uint32_t* __restrict__ vflags, uint64_t r, uint64_t chunk_vecs,
+    double* __restrict__ part_c, uint32_t* __restrict__ part_j, unsigned char* __restrict__ row_flag, const float* __restrict__ seed,
+    const uint32_t* skip_flag) {
+    // blockIdx.y = chunk of the vector range [y * chunk_vecs, (y + 1) * chunk_vecs): the per-row winners of the chunks are
+    // merged in ascending chunk order afterwards (strict >: the first strict maximum overall)
+    if (skip_flag && *skip_flag) return;
+    constexpr int MM = M > 0 ? M : kMaxObj;
+    constexpr int R = kFilterRows, CAP = kFilterCand, V = kFilterVecs;
+    const int m = M > 0 ? M : (int)m_rt;
+    extern __shared__ __align__(16) float s_v32[];  // (kFilterTile + V) x stride unit vectors in fp32, then the candidate slots
+    constexpr int SS = (MM + 3) / 4 * 4;  // compile-time stride when M is known
+    const int stride = M > 0 ? SS : (int)v32_stride(m);
+    // candidate slot e of this thread's row t: index (t * CAP + e) * blockDim + tid (conflict-free)
+    uint32_t* cand_j = reinterpret_cast<uint32_t*>(s_v32 + (kFilterTile + V) * stride);
+    float* cand_s = reinterpret_cast<float*>(cand_j + R * CAP * kFilterThreads);
+    const bool v_ok = (*vflags & 1u) == 0;
+    uint32_t row[R], cnt[R];
+    float uf[R][MM], best32[R], thr[R];
+    bool overflow[R];
+#pragma unroll
+    for (int t = 0; t < R; ++t) {
+        row[t] = (uint32_t)(blockIdx.x * (uint64_t)(R * kFilterThreads) + t * kFilterThreads + threadIdx.x);
+        const bool live = row[t] < n_rows;
+        cnt[t] = 0;
+        overflow[t] = false;
+        bool filter = v_ok && live;
+        double fp[MM], nf = 0.0;
+        if (live) {
             double s = 0.0;
 #pragma unroll
             for (int k = 0; k < MM; ++k)
                 if (k < m) {
-                    fp[t][k] = f[row[t] * m + k] - z[k];  // selection.hpp:155-157
-                    s += fp[t][k] * fp[t][k];
-                    if (!(fp[t][k] >= 0.0)) filter = false;
+                    fp[k] = SELF ? f[(uint64_t)row[t] * m + k] : f[(uint64_t)row[t] * m + k] - z[k];  // selection.hpp:155-157
+                    s += fp[k] * fp[k];
+                    if (!(fp[k] >= 0.0)) filter = false;
                 }
-            nf[t] = sqrt(s);
-            if (!(nf[t] < INFINITY)) filter = false;  // inf or NaN
+            nf = SELF ? vn[row[t]] : sqrt(s);  // refvec.hpp:84: the same row_norms the vectors' norms come from
+            if (!(nf < INFINITY)) filter = false;  // inf or NaN
         }
 #pragma unroll
         for (int k = 0; k < MM; ++k) {
-            const double uk = (k < m && live[t] && nf[t] != 0.0) ? fp[t][k] / nf[t] : 0.0;
+            const double uk = (k < m && live && nf != 0.0) ? fp[k] / nf : 0.0;
             uf[t][k] = (float)uk;
-            if (uk != 0.0 && !(uf[t][k] >= 1.17549435e-38f)) filter = false;  // flushed component: exact expression for this row
+            if (uk != 0.0 && !(uf[t][k] >= kFltMin)) filter = false;  // flushed component: no filter for this row
         }
-        best32[t] = 0.0f;
-        thr[t] = filter ? 0.0f : -INFINITY;  // 0: every non-negative score passes until a maximum exists
-        if (!live[t] || nf[t] == 0.0) thr[t] = INFINITY;  // nothing to do (selection.hpp:167-169: arg 0, theta 0)
+        best32[t] = live ? seed[row[t]] : 0.0f;           // a real score of this row: a lower bound of its maximum
+        thr[t] = best32[t] * (1.0f - kFilterTol);         // (0 when the subsample was empty: every score passes)
+        if (!live || nf == 0.0) {
+            thr[t] = INFINITY;  // nothing to do (selection.hpp:167-169: arg 0, theta 0)
+        } else if (!filter) {   // the exact expression for every vector: filter_fallback_kernel
+            thr[t] = INFINITY;
+            overflow[t] = true;
+        }
     }
-    constexpr int SS = (MM + 1 + 3) / 4 * 4;  // compile-time stride when M is known
-    const int stride = M > 0 ? SS : (int)v32_stride(m);
     const uint64_t j_begin = blockIdx.y * chunk_vecs, j_end = j_begin + chunk_vecs < r ? j_begin + chunk_vecs : r;
     for (uint64_t j0 = j_begin; j0 < j_end; j0 += kFilterTile) {
         const int tile = (int)((j_end - j0) < (uint64_t)kFilterTile ? (j_end - j0) : kFilterTile);
@@ -257,78 +364,185 @@ __global__ void __launch_bounds__(kFilterThreads, 4) assoc_filter_kernel(
             const float4* src = reinterpret_cast<const float4*>(v32 + j0 * stride);
             float4* dst = reinterpret_cast<float4*>(s_v32);
             for (int e = threadIdx.x; e < tile * stride / 4; e += blockDim.x) dst[e] = src[e];
+            // a partial last step: its phantom vectors score zero
+            if (threadIdx.x < (V - 1) * stride / 4) dst[tile * stride / 4 + threadIdx.x] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
         __syncthreads();
-        // two vectors per step: four independent FFMA chains per thread
-#pragma unroll 2
-        for (int jj = 0; jj < tile; jj += 2) {
-            float vr[2][SS];
-            const bool second = jj + 1 < tile;
+#pragma unroll 1
+        for (int jj = 0; jj < tile; jj += V) {
+            float vr[V][SS];
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
-                const float4* p4 = reinterpret_cast<const float4*>(s_v32 + (jj + (u && second ? 1 : 0)) * stride);  // broadcast reads
+            for (int u = 0; u < V; ++u) {
+                const float4* p4 = reinterpret_cast<const float4*>(s_v32 + (jj + u) * stride);  // broadcast reads
 #pragma unroll
                 for (int k4 = 0; k4 < SS / 4; ++k4)
-                    if (4 * k4 < m + 1) {
+                    if (4 * k4 < m) {
                         const float4 t4 = p4[k4];
                         vr[u][4 * k4] = t4.x, vr[u][4 * k4 + 1] = t4.y, vr[u][4 * k4 + 2] = t4.z, vr[u][4 * k4 + 3] = t4.w;
                     }
             }
-            float sc[2][2] = {{0.0f, 0.0f}, {0.0f, 0.0f}};  // [vector][row]
+            float sc[V][R];
+#pragma unroll
+            for (int u = 0; u < V; ++u)
+#pragma unroll
+                for (int t = 0; t < R; ++t) sc[u][t] = 0.0f;
 #pragma unroll
             for (int k = 0; k < MM; ++k)
                 if (k < m) {
-                    sc[0][0] = fmaf(uf[0][k], vr[0][k], sc[0][0]);
-                    sc[0][1] = fmaf(uf[1][k], vr[0][k], sc[0][1]);
-                    sc[1][0] = fmaf(uf[0][k], vr[1][k], sc[1][0]);
-                    sc[1][1] = fmaf(uf[1][k], vr[1][k], sc[1][1]);
+#pragma unroll
+                    for (int u = 0; u < V; ++u)
+#pragma unroll
+                        for (int t = 0; t < R; ++t) sc[u][t] = fmaf(uf[t][k], vr[u][k], sc[u][t]);
                 }
+            bool any = false;
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
-                float rinv = vr[u][0];
+            for (int t = 0; t < R; ++t) {
+                float mx = sc[0][t];
 #pragma unroll
-                for (int k = 0; k <= MM; ++k)
-                    if (k == m) rinv = vr[u][k];
-                sc[u][0] *= rinv;
-                sc[u][1] *= rinv;
+                for (int u = 1; u < V; ++u) mx = fmaxf(mx, sc[u][t]);
+                any |= mx >= thr[t];
             }
-            if (!second) sc[1][0] = sc[1][1] = -INFINITY;
-            // ascending j: vector jj first, then jj + 1 (the thresholds move in between)
+            if (any) {  // a candidate: remember it, raise the threshold (ascending j)
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
-                // the phantom second vector of an odd tile end must not pass a disabled filter (thr = -inf: -inf >= -inf)
-                const bool real = u == 0 || second;
-                const bool h0 = real && sc[u][0] >= thr[0], h1 = real && sc[u][1] >= thr[1];
-                if (h0 | h1) {  // rare after the first few vectors: the reference's exact expression
-                    const uint64_t j = j0 + jj + u;
+                for (int u = 0; u < V; ++u) {
+                    const uint32_t j = (uint32_t)(j0 + jj + u);
+                    if (jj + u >= tile) continue;  // a phantom vector of the partial last step
 #pragma unroll
-                    for (int t = 0; t < 2; ++t) {
-                        if (!(t == 0 ? h0 : h1)) continue;
-                        double dot = 0.0;
-#pragma unroll
-                        for (int k = 0; k < MM; ++k)
-                            if (k < m) dot += fp[t][k] * v[j * m + k];
-                        const double c = dot / (nf[t] * vn[j]);  // selection.hpp:178
-                        if (c > best_c[t]) {
-                            best_c[t] = c;
-                            arg[t] = (uint32_t)j;
-                        }
+                    for (int t = 0; t < R; ++t) {
                         const float s32 = sc[u][t];
-                        if (thr[t] > -INFINITY && s32 > best32[t]) {
+                        if (!(s32 >= thr[t])) continue;
+                        if (SELF && j == row[t]) continue;  // refvec.hpp:91
+                        if (s32 > best32[t]) {
                             best32[t] = s32;
                             thr[t] = s32 * (1.0f - kFilterTol);
                         }
+                        if (cnt[t] == CAP) {  // drop the candidates the threshold has left behind
+                            uint32_t keep = 0;
+                            for (uint32_t e = 0; e < CAP; ++e) {
+                                const uint32_t at = (t * CAP + e) * kFilterThreads + threadIdx.x;
+                                const float se = cand_s[at];
+                                if (se >= thr[t]) {
+                                    const uint32_t to = (t * CAP + keep) * kFilterThreads + threadIdx.x;
+                                    cand_s[to] = se;
+                                    cand_j[to] = cand_j[at];
+                                    ++keep;
+                                }
+                            }
+                            cnt[t] = keep;
+                            if (keep == CAP) {  // more near-ties than slots: this row goes to the exact fallback
+                                overflow[t] = true;
+                                thr[t] = INFINITY;
+                                continue;
+                            }
+                        }
+                        const uint32_t at = (t * CAP + cnt[t]) * kFilterThreads + threadIdx.x;
+                        cand_s[at] = s32;
+                        cand_j[at] = j;
+                        ++cnt[t];
                     }
                 }
             }
         }
     }
+    // the candidates that survive the final threshold, in ascending j, with the reference's exact expression
 #pragma unroll
-    for (int t = 0; t < 2; ++t) {
-        if (!live[t]) continue;
-        part_c[blockIdx.y * n_rows + row[t]] = best_c[t];
-        part_j[blockIdx.y * n_rows + row[t]] = arg[t];
+    for (int t = 0; t < R; ++t) {
+        if (row[t] >= n_rows) continue;
+        double best_c = -INFINITY;
+        uint32_t arg = 0;
+        if (overflow[t]) {
+            row_flag[row[t]] = 1;
+        } else if (cnt[t]) {
+            const double nf = SELF ? vn[row[t]] : [&] {
+                double s = 0.0;
+                for (int k = 0; k < m; ++k) {
+                    const double x = f[(uint64_t)row[t] * m + k] - z[k];
+                    s += x * x;
+                }
+                return sqrt(s);
+            }();
+            for (uint32_t e = 0; e < cnt[t]; ++e) {
+                const uint32_t at = (t * CAP + e) * kFilterThreads + threadIdx.x;
+                if (!(cand_s[at] >= thr[t])) continue;
+                const uint32_t j = cand_j[at];
+                const double c = exact_cosine(f + (uint64_t)row[t] * m, SELF ? nullptr : z, v + (uint64_t)j * m, nf, vn[j], m);
+                if (c > best_c) {
+                    best_c = c;
+                    arg = j;
+                }
+            }
+        }
+        part_c[blockIdx.y * n_rows + row[t]] = best_c;
+        part_j[blockIdx.y * n_rows + row[t]] = arg;
     }
+}
+
+// Rows the filter does not apply to (a negative / non-finite / fp32-unrepresentable component, a bad vector set, or more
+// near-ties than candidate slots): the reference's expression for every vector, one warp per flagged row, first strict
+// maximum (lexicographic max cosine / lowest j across the lanes). Result into chunk slot 0 (the scan left -inf everywhere).
+template <bool SELF>
+__global__ void filter_fallback_kernel(const double* __restrict__ f, uint64_t n_rows, uint64_t m, const double* __restrict__ z,
+                                       const double* __restrict__ v, const double* __restrict__ vn, uint64_t r,
+                                       const unsigned char* __restrict__ row_flag, double* __restrict__ part_c,
+                                       uint32_t* __restrict__ part_j, const uint32_t* skip_flag) {
+    if (skip_flag && *skip_flag) return;
+    const uint64_t row = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint32_t lane = threadIdx.x & 31;
+    if (row >= n_rows || !row_flag[row]) return;
+    double nf;
+    if (SELF) {
+        nf = vn[row];
+    } else {
+        double s = 0.0;
+        for (uint64_t k = 0; k < m; ++k) {
+            const double x = f[row * m + k] - z[k];
+            s += x * x;
+        }
+        nf = sqrt(s);
+    }
+    double best_c = -INFINITY;
+    uint32_t arg = 0xffffffffu;
+    for (uint64_t j = lane; j < r; j += 32) {
+        if (SELF && j == row) continue;
+        double dot = 0.0;
+        for (uint64_t k = 0; k < m; ++k) dot += (SELF ? f[row * m + k] : f[row * m + k] - z[k]) * v[j * m + k];
+        const double c = dot / (nf * vn[j]);
+        if (c > best_c) {
+            best_c = c;
+            arg = (uint32_t)j;
+        }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        const double oc = __shfl_xor_sync(0xffffffffu, best_c, off);
+        const uint32_t oj = __shfl_xor_sync(0xffffffffu, arg, off);
+        if (oc > best_c || (oc == best_c && oj < arg)) {
+            best_c = oc;
+            arg = oj;
+        }
+    }
+    if (lane == 0) {
+        part_c[row] = best_c;
+        part_j[row] = arg == 0xffffffffu ? 0u : arg;
+    }
+}
+
+// gamma_i = acos(max over the chunk winners) (refvec.hpp:93-98)
+__global__ void gamma_filter_merge_kernel(uint64_t r, const double* __restrict__ part_c, uint32_t chunks, double* __restrict__ gamma,
+                                          uint32_t* err_flag, const uint32_t* skip_flag) {
+    if (skip_flag && *skip_flag) return;
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= r) return;
+    double c = -INFINITY;
+    for (uint32_t k = 0; k < chunks; ++k) {
+        const double pc = part_c[k * r + i];
+        if (pc > c) c = pc;
+    }
+    if (c > 1.0) c = 1.0;
+    if (c < -1.0) c = -1.0;
+    const double g = acos(c);  // tensor.hpp:79-83
+    gamma[i] = g;
+    if (!(g > 0.0)) atomicOr(err_flag, 1u);  // refvec.hpp:97-98
 }
 
 // merges the chunk winners of a row (ascending chunks = ascending j, strict >) and finishes theta / APD / per-vector minima
@@ -448,11 +662,13 @@ void SelectWorkspace::alloc(uint64_t rows_cap_, uint64_t r_, uint64_t m_) {
     n_elite = dev_alloc<uint32_t>(1);
     err_flag = dev_alloc<uint32_t>(1);
     tile_scratch = dev_alloc<uint32_t>((r + kCompactTile - 1) / kCompactTile + 1);
-    v32 = dev_alloc<float>(r * ((m + 1 + 3) / 4 * 4));
+    v32 = dev_alloc<float>(r * v32_stride(m));
     v32_flags = dev_alloc<uint32_t>(1);
     if (assoc_filter_preferred(m, r)) {
         part_c = dev_alloc<double>(rows_cap * kFilterMaxChunks);
         part_j = dev_alloc<uint32_t>(rows_cap * kFilterMaxChunks);
+        row_flag = dev_alloc<unsigned char>(rows_cap);
+        seed32 = dev_alloc<float>(rows_cap);
     }
     TEMO_CUDA(cudaMemset(err_flag, 0, sizeof(uint32_t)));
 }
@@ -460,7 +676,7 @@ void SelectWorkspace::alloc(uint64_t rows_cap_, uint64_t r_, uint64_t m_) {
 void SelectWorkspace::release() {
     cudaFree(z); cudaFree(zkey); cudaFree(vn); cudaFree(assoc); cudaFree(theta); cudaFree(apd);
     cudaFree(best_key); cudaFree(best_row); cudaFree(first_row); cudaFree(elite); cudaFree(valid);
-    cudaFree(n_elite); cudaFree(err_flag); cudaFree(tile_scratch); cudaFree(v32); cudaFree(v32_flags); cudaFree(part_c); cudaFree(part_j);
+    cudaFree(n_elite); cudaFree(err_flag); cudaFree(tile_scratch); cudaFree(v32); cudaFree(v32_flags); cudaFree(part_c); cudaFree(part_j); cudaFree(row_flag); cudaFree(seed32);
     *this = SelectWorkspace{};
 }
 
@@ -513,12 +729,16 @@ void launch_select_finish(uint64_t r, SelectWorkspace& ws, bool nan_rule, cudaSt
 
 bool assoc_filter_preferred(uint64_t m, uint64_t r) { return m >= 5 && r >= 256; }
 
-void launch_assoc_filter(const double* f, uint64_t n_rows, uint64_t m, const double* v, const double* gamma, uint64_t r, double penalty,
-                         SelectWorkspace& ws, uint32_t* assoc, double* theta, double* apd, cudaStream_t s, uint32_t row0) {
+namespace {
+// the filtered scan over (rows x r): per-chunk winners into ws.part_c / ws.part_j; returns the number of chunks
+template <bool SELF>
+uint32_t launch_filter_scan(const double* rows, uint64_t n_rows, uint64_t m, const double* z, const double* v, uint64_t r,
+                            SelectWorkspace& ws, const uint32_t* skip_flag, cudaStream_t s) {
     require(ws.v32 != nullptr && r <= ws.r && m == ws.m, "rv_select: workspace has no fp32 vector copy");
     TEMO_CUDA(cudaMemsetAsync(ws.v32_flags, 0, sizeof(uint32_t), s));
     v32_kernel<<<(unsigned)((r + 255) / 256), 256, 0, s>>>(v, ws.vn, r, m, ws.v32, ws.v32_flags);
-    const unsigned row_blocks = (unsigned)((n_rows + 2 * kFilterThreads - 1) / (2 * kFilterThreads));
+    const uint64_t rows_per_cta = (uint64_t)kFilterRows * kFilterThreads;
+    const unsigned row_blocks = (unsigned)((n_rows + rows_per_cta - 1) / rows_per_cta);
     // enough CTAs for several waves: the vector range is cut into chunks of whole tiles
     uint64_t chunks = (4ull * kSMs * 4 + row_blocks - 1) / row_blocks;
     const uint64_t tiles = (r + kFilterTile - 1) / kFilterTile;
@@ -529,16 +749,23 @@ void launch_assoc_filter(const double* f, uint64_t n_rows, uint64_t m, const dou
     chunks = (r + chunk_vecs - 1) / chunk_vecs;
     require(n_rows <= ws.rows_cap && ws.part_c != nullptr, "rv_select: workspace has no chunk scratch");
     const dim3 grid(row_blocks, (unsigned)chunks);
-    const size_t smem = (size_t)kFilterTile * v32_stride(m) * sizeof(float);
+    const size_t smem = (size_t)(kFilterTile + kFilterVecs) * v32_stride(m) * sizeof(float) +
+                        (size_t)kFilterRows * kFilterCand * kFilterThreads * (sizeof(uint32_t) + sizeof(float));
+    require(ws.row_flag != nullptr, "rv_select: workspace has no row flags");
+    TEMO_CUDA(cudaMemsetAsync(ws.row_flag, 0, n_rows, s));
+    float* seed = ws.seed32;
 #define CALL(MV)                                                                                                                  \
     {                                                                                                                             \
         static bool configured = false;                                                                                           \
         if (!configured && smem > 48 * 1024) {                                                                                    \
-            TEMO_CUDA(cudaFuncSetAttribute(assoc_filter_kernel<MV>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));    \
+            TEMO_CUDA(cudaFuncSetAttribute(assoc_filter_kernel<MV, SELF>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024)); \
             configured = true;                                                                                                    \
         }                                                                                                                         \
-        assoc_filter_kernel<MV><<<grid, kFilterThreads, smem, s>>>(f, n_rows, nullptr, m, ws.z, v, ws.vn, ws.v32, ws.v32_flags, r,  \
-                                                                   chunk_vecs, ws.part_c, ws.part_j);                             \
+        filter_seed_kernel<MV, SELF><<<(unsigned)((n_rows + kSeedRows * kFilterThreads - 1) / (kSeedRows * kFilterThreads)),     \
+                                       kFilterThreads, (size_t)kFilterTile * v32_stride(m) * sizeof(float), s>>>(                \
+            rows, n_rows, m, z, ws.vn, ws.v32, r, seed, skip_flag);                                                               \
+        assoc_filter_kernel<MV, SELF><<<grid, kFilterThreads, smem, s>>>(rows, n_rows, m, z, v, ws.vn, ws.v32, ws.v32_flags, r,    \
+                                                                         chunk_vecs, ws.part_c, ws.part_j, ws.row_flag, seed, skip_flag); \
     }
     switch (m) {
     case 5: CALL(5); break;
@@ -546,10 +773,39 @@ void launch_assoc_filter(const double* f, uint64_t n_rows, uint64_t m, const dou
     default: CALL(0); break;
     }
 #undef CALL
-    assoc_filter_merge_kernel<<<(unsigned)((n_rows + 255) / 256), 256, 0, s>>>(f, n_rows, m, ws.z, ws.part_c, ws.part_j, (uint32_t)chunks,
+    filter_fallback_kernel<SELF><<<(unsigned)((n_rows + 3) / 4), 128, 0, s>>>(rows, n_rows, m, z, v, ws.vn, r, ws.row_flag, ws.part_c,
+                                                                            ws.part_j, skip_flag);
+    TEMO_CUDA(cudaGetLastError());
+    return (uint32_t)chunks;
+}
+}  // namespace
+
+void launch_assoc_filter(const double* f, uint64_t n_rows, uint64_t m, const double* v, const double* gamma, uint64_t r, double penalty,
+                         SelectWorkspace& ws, uint32_t* assoc, double* theta, double* apd, cudaStream_t s, uint32_t row0) {
+    const uint32_t chunks = launch_filter_scan<false>(f, n_rows, m, ws.z, v, r, ws, nullptr, s);
+    assoc_filter_merge_kernel<<<(unsigned)((n_rows + 255) / 256), 256, 0, s>>>(f, n_rows, m, ws.z, ws.part_c, ws.part_j, chunks,
                                                                                gamma, penalty, assoc, theta, apd, ws.best_key,
                                                                                ws.first_row, row0);
     TEMO_CUDA(cudaGetLastError());
+}
+
+// min_vector_angles (refvec.hpp:81-100) through the same filtered scan (many objectives): ws.vn must hold the norms of v
+void launch_gamma_filter(const double* v, uint64_t r, uint64_t m, SelectWorkspace& ws, double* gamma, uint32_t* err_flag,
+                         const uint32_t* skip_flag, cudaStream_t s) {
+    require(r >= 2, "min_vector_angles: needs at least two vectors");  // refvec.hpp:82
+    const uint32_t chunks = launch_filter_scan<true>(v, r, m, nullptr, v, r, ws, skip_flag, s);
+    gamma_filter_merge_kernel<<<(unsigned)((r + 255) / 256), 256, 0, s>>>(r, ws.part_c, chunks, gamma, err_flag, skip_flag);
+    TEMO_CUDA(cudaGetLastError());
+}
+
+void launch_gamma_auto(const double* v, uint64_t r, uint64_t m, SelectWorkspace& ws, VecIndex* index, double* gamma,
+                       uint32_t* err_flag, const uint32_t* skip_flag, cudaStream_t s) {
+    if (assoc_filter_preferred(m, r) && ws.part_c != nullptr && r <= ws.rows_cap) {
+        launch_gamma_filter(v, r, m, ws, gamma, err_flag, skip_flag, s);
+    } else {
+        require(index != nullptr && index->built, "min_vector_angles: no direction index");
+        launch_gamma_indexed(v, ws.vn, r, m, *index, gamma, err_flag, skip_flag, s);
+    }
 }
 
 void launch_select(const double* f, uint64_t n_rows, const uint32_t* n_rows_dev, uint64_t m,

@@ -265,8 +265,8 @@ struct Shard {
         launch_row_norms(v, r, m, ws.vn, stream);
         vindex.alloc(r, m);
         vindex.set_order(unit.data(), stream);
-        vindex.build(v, ws.vn, stream);
-        launch_gamma_indexed(v, ws.vn, r, m, vindex, gamma, ws.err_flag, nullptr, stream);
+        if (!assoc_filter_preferred(m, r)) vindex.build(v, ws.vn, stream);  // m >= 5: the fp32-filtered scans need no index
+        launch_gamma_auto(v, r, m, ws, &vindex, gamma, ws.err_flag, nullptr, stream);
         std::vector<double> lo(d), hi(d);
         problem_bounds(cfg.problem, d, m, lo.data(), hi.data());
         bound_seg = find_bound_segments(lo.data(), hi.data(), d);
@@ -434,8 +434,8 @@ struct Shard {
         if ((t + 1) % adapt_every == 0) {  // algorithms.hpp:281 (replicated: every rank adapts identically)
             launch_col_minmax(fm[cur], cnt, nullptr, m, zmin, zmax, zscratch, stream);
             launch_adapt_vectors(v0, v, ws.vn, r, m, zmin, zmax, skip_flag, ws.err_flag, stream);
-            vindex.build(v, ws.vn, stream);
-            launch_gamma_indexed(v, ws.vn, r, m, vindex, gamma, ws.err_flag, skip_flag, stream);
+            if (!assoc_filter_preferred(m, r)) vindex.build(v, ws.vn, stream);  // m >= 5: the fp32-filtered scans need no index
+            launch_gamma_auto(v, r, m, ws, &vindex, gamma, ws.err_flag, skip_flag, stream);
         }
         TEMO_CUDA(cudaStreamSynchronize(stream));  // host staging arrays may go away
         check();

@@ -579,6 +579,30 @@ def test_rv_select_many_objectives_filter(tb, oracle, cfg):
         _check_selection(tb.rv_select(f, tb.RefVectorSet(v0, vbig, gamma), 10, 100, 2.0), oracle.rv_select(f, vbig, gamma, 10, 100, 2.0))
 
 
+@pytest.mark.parametrize("mh", [(10, 5), (5, 10), (6, 6)])
+def test_gamma_many_objectives_filter(tb, oracle, mh):
+    """min_vector_angles for m >= 5 and R >= 256 goes through the fp32-filtered exact scan (rows = the vectors themselves,
+    the diagonal skipped): the max off-diagonal cosine is the reference's exact expression, gamma within acos' 2 ulp;
+    isotropic and adapted sets, a set with a negative component (filter off), exact duplicates -> the reference's error."""
+    m, H = mh
+    v0, gamma0 = oracle.make_ref_set(m, H)
+    assert len(v0) >= 256
+    assert ulp_diff(tb.min_vector_angles(v0), gamma0).max() <= 2
+    zmin = np.linspace(0.0, 0.2, m)
+    v, g = oracle.adapt(v0, v0, gamma0, zmin, zmin + np.linspace(0.5, 3.0, m))
+    assert ulp_diff(tb.min_vector_angles(v), g).max() <= 2
+    refs = tb.RefVectorSet(v0, v0.copy(), gamma0.copy())
+    tb.adapt(refs, zmin, zmin + np.linspace(0.5, 3.0, m))
+    assert np.array_equal(refs.v, v) and ulp_diff(refs.gamma, g).max() <= 2
+    vneg = v0.copy()
+    vneg[3, 0] = -vneg[3, 0] - 0.1
+    assert ulp_diff(tb.min_vector_angles(vneg), oracle.min_vector_angles(vneg)).max() <= 2
+    vdup = v0.copy()
+    vdup[11] = vdup[200] * 3.0   # same direction: angle 0
+    with pytest.raises(ValueError):
+        tb.min_vector_angles(vdup)   # refvec.hpp:97-98
+
+
 def test_selection_contracts_and_edges(tb, oracle):
     v0, gamma = oracle.make_ref_set(2, 2)
     refs = tb.RefVectorSet(v0, v0, gamma)
