@@ -306,50 +306,45 @@ int temo_b200_dev_sync(void);
  * 3 reproduction with fused evaluation, 4 selection, 5 gamma. Used for the roofline. */
 int temo_b200_run_time_stage(temo_b200_run* run, int stage, int reps, double* mean_ms);
 /* ---- sharded generation loop: stage-level entry points of ONE rank (one process per GPU). The host
- * orchestration (paper_2404_01159_b200/dist.py) puts torch.distributed collectives between them:
- * all-to-all of parent rows, all-gather of offspring objectives / free slots, min-allreduces of the
- * per-vector (APD key, row) minima. reference: rvea_run, algorithms.hpp:227-296. */
+ * orchestration (paper_2404_01159_b200/dist.py) only puts the small torch.distributed collectives between them:
+ * all-gather of offspring objectives / free-slot lists, min-allreduces of the per-vector (APD key, row) minima
+ * (SURVEY.md section 8e). Parents are NOT exchanged: every rank maps its peers' population pools (CUDA IPC) and the
+ * reproduction kernel loads remote parent rows over NVLink itself; the survivor -> (owner, slot) tables and every
+ * other piece of loop state live on the device. reference: rvea_run, algorithms.hpp:227-296. */
 typedef struct temo_b200_shard temo_b200_shard; /* opaque */
 const char* temo_b200_shard_last_error(void);
-/* Pure host code (no GPU needed): the exchange plan of one generation for `rank` from the replicated
- * survivor tables. The exchange is cut into `chunks` pieces by local mating pair (pair p belongs to chunk
- * p / ceil(h_loc / chunks)) so that reproduction can start on the first pairs while the rest is on the wire:
- * local slots to send ordered by (chunk, destination), row counts indexed [chunk * world + peer], the
- * receive-buffer row of every local mating row (the buffer is filled chunk after chunk, source after source),
- * and the generation's draw counters {c_sbx, c_pm, counter after the generation}. */
-int temo_b200_shard_plan(uint64_t seed, uint64_t counter, uint64_t P, uint64_t n, uint64_t d, int rank, int world, int chunks,
-                         const int32_t* surv_owner, const uint32_t* surv_slot, uint32_t* send_slots,
-                         uint64_t send_slots_cap, uint64_t* send_counts, uint64_t* recv_counts,
-                         uint32_t* recv_pos, uint64_t* counters3);
-/* Host thread computing the Fisher-Yates shuffle of a future generation ahead of time (rng.hpp:69-78). */
-int temo_b200_shard_perm_prefetch(uint64_t seed, uint64_t c_shuffle, uint64_t n);
-/* Pure host code: replicated survivor tables after selection (algorithms.hpp:278-279 in sharded form). */
-int temo_b200_shard_update_tables(const uint32_t* elite, uint64_t count, uint64_t P, uint64_t n, int rank, int world,
-                                  const uint32_t* free_all, int32_t* surv_owner, uint32_t* surv_slot,
-                                  uint32_t* own_slots, uint64_t* own_count);
 int temo_b200_shard_create(const temo_b200_run_config* cfg, int rank, int world, temo_b200_shard** out);
 int temo_b200_shard_destroy(temo_b200_shard* s);
-/* info8: n_loc, d, m, r, send_cap, pcap, cap_loc, adapt_every */
+/* info8: n_loc, d, m, r, pcap, cap_loc, adapt_every, kernels + copies enqueued by this shard so far */
 int temo_b200_shard_info(temo_b200_shard* s, uint64_t* info8);
-/* device buffers the collectives operate on: 0 send_buf, 1 recv_buf, 2 f_off_loc, 3 f_gather,
- * 4 best_key (int64 view), 5 first_row (int32 view), 6 best_row (int32 view), 7 free_slot (int32 view) */
+/* state5: survivor count, draw counter, generations done, lo, hi (this rank's slice of the merged rows of the generation
+ * begun last) */
+int temo_b200_shard_state(temo_b200_shard* s, uint64_t* state5);
+/* device buffers the collectives operate on: 0 f_off_loc (n_loc x m), 1 f_gather (world x n_loc x m), 2 best_key (int64
+ * view, R), 3 first_row (int32 view, R), 4 best_row (int32 view, R), 5 free_slot (int32 view, n_loc), 6 free_all (int32
+ * view, world x n_loc), 7 the population pool (cap_loc x d) */
 void* temo_b200_shard_buffer(temo_b200_shard* s, int which);
-int temo_b200_shard_pack(temo_b200_shard* s, const uint32_t* slots, uint64_t count);
-int temo_b200_shard_reproduce(temo_b200_shard* s, const uint32_t* recv_pos, uint64_t c_sbx, uint64_t c_pm);
-/* Pieces of a chunked exchange: pack `count` rows into the send buffer from row `row0`; reproduce (+ evaluate) only the
- * local pairs [unit_begin, unit_begin + unit_count). Both only enqueue work on the shard's stream and return. */
-int temo_b200_shard_pack_at(temo_b200_shard* s, const uint32_t* slots, uint64_t count, uint64_t row0);
-int temo_b200_shard_reproduce_range(temo_b200_shard* s, const uint32_t* recv_pos, uint64_t c_sbx, uint64_t c_pm,
-                                    uint64_t unit_begin, uint64_t unit_count);
 /* The cudaStream_t all stages of this shard are enqueued on (collectives issued on it need no device-wide syncs). */
 void* temo_b200_shard_stream(temo_b200_shard* s);
-int temo_b200_shard_place_f(temo_b200_shard* s, uint64_t P, int initial);
-int temo_b200_shard_select_local(temo_b200_shard* s, uint64_t P, uint64_t lo, uint64_t hi, uint64_t t);
-int temo_b200_shard_select_rows(temo_b200_shard* s, uint64_t lo, uint64_t hi);
-int temo_b200_shard_select_finish(temo_b200_shard* s, uint32_t* elite, uint64_t* count);
-int temo_b200_shard_commit(temo_b200_shard* s, uint64_t count, const uint32_t* own_slots, uint64_t own_count,
-                           uint64_t t);
-int temo_b200_shard_download(temo_b200_shard* s, const uint32_t* slots, uint64_t rows, double* x, uint64_t f_rows,
+/* Peer pools: every rank exports the 64-byte CUDA IPC handle of its pool, the caller all-gathers the handles (world x 64
+ * bytes) and every rank opens its peers' (world > 1; a world of 1 needs neither). set_peer_pointers is the same for
+ * pools that are already addressable from this process (several shards of one process: tests). */
+int temo_b200_shard_ipc_handle(temo_b200_shard* s, unsigned char* handle64);
+int temo_b200_shard_open_peers(temo_b200_shard* s, const unsigned char* handles);
+int temo_b200_shard_set_peer_pointers(temo_b200_shard* s, void* const* pools);
+/* One generation = begin, reproduce, [all-gather f_off_loc -> f_gather, free_slot -> free_all], select_local,
+ * [min-allreduce best_key, first_row], select_rows, [min-allreduce best_row], finish. Every call only enqueues work on
+ * the shard's stream except finish, which reads the survivor count back (the one synchronisation of a generation).
+ * place_initial_f follows the first all-gather of the initial population's objectives (algorithms.hpp:242). */
+int temo_b200_shard_begin(temo_b200_shard* s);
+int temo_b200_shard_reproduce(temo_b200_shard* s);
+int temo_b200_shard_place_initial_f(temo_b200_shard* s);
+int temo_b200_shard_select_local(temo_b200_shard* s);
+int temo_b200_shard_select_rows(temo_b200_shard* s);
+int temo_b200_shard_finish(temo_b200_shard* s, uint64_t* count);
+/* Copies out the replicated state and this rank's rows: owner / slot tables (P entries each), x of the survivors this rank
+ * owns (survivor order, own_rows x d; own_index receives their survivor indices), f (P x m), v, gamma. Any may be NULL. */
+int temo_b200_shard_download(temo_b200_shard* s, uint32_t* owner, uint32_t* slot, uint64_t* own_rows, uint64_t* own_index, double* x,
                              double* f, double* v, double* gamma);
 
 /* Self-test hook for the libm-exact pow used by SBX / polynomial mutation / DTLZ4

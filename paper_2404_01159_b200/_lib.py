@@ -121,26 +121,22 @@ SIGNATURES = {
     "temo_b200_dev_sync": (C.c_int, []),
     "temo_b200_run_time_stage": (C.c_int, [_RUN, C.c_int, C.c_int, f64p]),
     "temo_b200_shard_last_error": (C.c_char_p, []),
-    "temo_b200_shard_plan": (C.c_int, [u64, u64, u64, u64, u64, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int32), C.POINTER(C.c_uint32),
-                                       C.POINTER(C.c_uint32), u64, u64p, u64p, C.POINTER(C.c_uint32), u64p]),
-    "temo_b200_shard_perm_prefetch": (C.c_int, [u64, u64, u64]),
-    "temo_b200_shard_update_tables": (C.c_int, [C.POINTER(C.c_uint32), u64, u64, u64, C.c_int, C.c_int, C.POINTER(C.c_uint32),
-                                                C.POINTER(C.c_int32), C.POINTER(C.c_uint32), C.POINTER(C.c_uint32), u64p]),
     "temo_b200_shard_create": (C.c_int, [_CFG, C.c_int, C.c_int, C.POINTER(_RUN)]),
     "temo_b200_shard_destroy": (C.c_int, [_RUN]),
     "temo_b200_shard_info": (C.c_int, [_RUN, u64p]),
+    "temo_b200_shard_state": (C.c_int, [_RUN, u64p]),
     "temo_b200_shard_buffer": (C.c_void_p, [_RUN, C.c_int]),
-    "temo_b200_shard_pack": (C.c_int, [_RUN, C.POINTER(C.c_uint32), u64]),
-    "temo_b200_shard_pack_at": (C.c_int, [_RUN, C.POINTER(C.c_uint32), u64, u64]),
-    "temo_b200_shard_reproduce_range": (C.c_int, [_RUN, C.POINTER(C.c_uint32), u64, u64, u64, u64]),
     "temo_b200_shard_stream": (C.c_void_p, [_RUN]),
-    "temo_b200_shard_reproduce": (C.c_int, [_RUN, C.POINTER(C.c_uint32), u64, u64]),
-    "temo_b200_shard_place_f": (C.c_int, [_RUN, u64, C.c_int]),
-    "temo_b200_shard_select_local": (C.c_int, [_RUN, u64, u64, u64, u64]),
-    "temo_b200_shard_select_rows": (C.c_int, [_RUN, u64, u64]),
-    "temo_b200_shard_select_finish": (C.c_int, [_RUN, C.POINTER(C.c_uint32), u64p]),
-    "temo_b200_shard_commit": (C.c_int, [_RUN, u64, C.POINTER(C.c_uint32), u64, u64]),
-    "temo_b200_shard_download": (C.c_int, [_RUN, C.POINTER(C.c_uint32), u64, f64p, u64, f64p, f64p, f64p]),
+    "temo_b200_shard_ipc_handle": (C.c_int, [_RUN, C.POINTER(C.c_ubyte)]),
+    "temo_b200_shard_open_peers": (C.c_int, [_RUN, C.POINTER(C.c_ubyte)]),
+    "temo_b200_shard_set_peer_pointers": (C.c_int, [_RUN, C.POINTER(C.c_void_p)]),
+    "temo_b200_shard_begin": (C.c_int, [_RUN]),
+    "temo_b200_shard_reproduce": (C.c_int, [_RUN]),
+    "temo_b200_shard_place_initial_f": (C.c_int, [_RUN]),
+    "temo_b200_shard_select_local": (C.c_int, [_RUN]),
+    "temo_b200_shard_select_rows": (C.c_int, [_RUN]),
+    "temo_b200_shard_finish": (C.c_int, [_RUN, u64p]),
+    "temo_b200_shard_download": (C.c_int, [_RUN, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32), u64p, u64p, f64p, f64p, f64p, f64p]),
     "temo_b200_pow": (C.c_int, [f64p, f64p, u64, f64p, C.c_int]),
     "temo_b200_tanh": (C.c_int, [f64p, u64, f64p, C.c_int]),
     "temo_b200_flush_l2": (C.c_int, []),

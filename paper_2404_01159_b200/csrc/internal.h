@@ -52,6 +52,9 @@ BoundSegments find_bound_segments(const double* lower, const double* upper, uint
 struct ReproArgs {
     const double* pool = nullptr;   // parent storage, row stride d
     const uint32_t* src = nullptr;  // [n] storage row of mating row i (nullptr: i)
+    // optional (replaces pool / src): [n] address of the parent row of mating row i, each 16-byte aligned; rows may live in
+    // other GPUs' pools mapped into this process (the sharded run: NVLink peer loads inside K1)
+    const double* const* src_ptr = nullptr;
     double* out = nullptr;          // child storage, row stride d
     const uint32_t* dst = nullptr;  // [n] storage row of child i (nullptr: i)
     uint64_t n = 0, d = 0;

@@ -18,7 +18,9 @@
 // exact 0.0 are skipped (verified bit-identical); the only inexact pieces are
 // CUDA's pow (<= 2 ulp) on crossed/mutated genes.
 #include <algorithm>
+#include <atomic>
 #include <cstddef>
+#include <mutex>
 #include <cstdlib>
 
 #include "glibc_pow_dev.cuh"
@@ -33,6 +35,7 @@ namespace {
 
 struct ReproK {
     const double* pool;
+    const double* const* src_ptr;  // optional: address of mating row i's parent (rows of other GPUs' pools: sharded runs)
     const uint32_t* src;
     double* out;
     const uint32_t* dst;
@@ -134,14 +137,14 @@ __device__ __forceinline__ void reproduce_unit(const ReproK& a, const uint64_t u
 
     const uint64_t src_a = a.src ? a.src[row_a] : row_a;
     const uint64_t dst_a = a.dst ? a.dst[row_a] : row_a;
-    const double* pa = a.pool + src_a * a.d;
+    const double* pa = a.src_ptr ? a.src_ptr[row_a] : a.pool + src_a * a.d;
     double* oa = a.out + dst_a * a.d;
     const double* pb = nullptr;
     double* ob = nullptr;
     if (paired) {
         const uint64_t src_b = a.src ? a.src[row_b] : row_b;
         const uint64_t dst_b = a.dst ? a.dst[row_b] : row_b;
-        pb = a.pool + src_b * a.d;
+        pb = a.src_ptr ? a.src_ptr[row_b] : a.pool + src_b * a.d;
         ob = a.out + dst_b * a.d;
     }
 
@@ -619,8 +622,8 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
         PairSlot& slot = S.slot[turn % kPairSlots];
         if (lane == 0) {
             const uint64_t row_a = unit, row_b = a.half + unit, g_unit = a.g_unit0 + unit;
-            W.ctx.pa = a.pool + (a.src ? (uint64_t)a.src[row_a] : row_a) * a.d;
-            W.ctx.pb = a.pool + (a.src ? (uint64_t)a.src[row_b] : row_b) * a.d;
+            W.ctx.pa = a.src_ptr ? a.src_ptr[row_a] : a.pool + (a.src ? (uint64_t)a.src[row_a] : row_a) * a.d;
+            W.ctx.pb = a.src_ptr ? a.src_ptr[row_b] : a.pool + (a.src ? (uint64_t)a.src[row_b] : row_b) * a.d;
             W.ctx.oa = a.out + (a.dst ? (uint64_t)a.dst[row_a] : row_a) * a.d;
             W.ctx.ob = a.out + (a.dst ? (uint64_t)a.dst[row_b] : row_b) * a.d;
             W.ctx.pos = a.s_base + g_unit * a.s_row;
@@ -914,6 +917,15 @@ inline bool force_generic_kernel() { return k1_options().generic != 0; }
 inline bool no_bound_segments() { return k1_options().bound_arrays != 0; }
 inline int pair_cand_cap() { return k1_options().cand_cap; }
 
+inline uint32_t* next_work_counter() {
+    constexpr unsigned kCounters = 256;
+    static std::once_flag once;
+    static uint32_t* counters = nullptr;
+    static std::atomic<unsigned> next{0};
+    std::call_once(once, [] { counters = dev_alloc<uint32_t>(kCounters); });
+    return counters + (next.fetch_add(1) % kCounters);
+}
+
 template <int MODE, int EVAL, int SEG>
 void launch_pairs_seg(const ReproK& k, uint64_t units, cudaStream_t s) {
     static int grid = 0;  // per instantiation
@@ -929,13 +941,8 @@ void launch_pairs_seg(const ReproK& k, uint64_t units, cudaStream_t s) {
     kk.work_counter = nullptr;
     if (k1_options().dynamic_pairs) {
         // one zeroed counter per launch out of a small ring (launches of different streams may overlap)
-        static uint32_t* counters = nullptr;
-        static unsigned next_counter = 0;
-        constexpr unsigned kCounters = 64;
-        if (!counters) {
-            counters = dev_alloc<uint32_t>(kCounters);
-        }
-        kk.work_counter = counters + (next_counter++ % kCounters);
+        // (shared by every instantiation and thread of the process: shards of one process launch concurrently)
+        kk.work_counter = next_work_counter();
         TEMO_CUDA(cudaMemsetAsync(kk.work_counter, 0, sizeof(uint32_t), s));
     }
     reproduce_pairs_kernel<MODE, EVAL, SEG><<<(unsigned)std::min<uint64_t>(units, (uint64_t)grid), kVirtWarps * 32, sizeof(PairSmem), s>>>(kk);
@@ -1046,6 +1053,7 @@ void launch_reproduce(const ReproArgs& a, cudaStream_t s) {
             "reproduce: bad objective count for fused evaluation");
     ReproK k{};
     k.pool = a.pool;
+    k.src_ptr = a.src_ptr;
     k.src = a.src;
     k.out = a.out;
     k.dst = a.dst;
@@ -1108,7 +1116,7 @@ void launch_reproduce(const ReproArgs& a, cudaStream_t s) {
     k.cand_cap = pair_cand_cap();
     uint64_t next = unit_lo;  // first unit not yet launched
     if (a.do_sbx && a.do_pm && vec == 2 && block == 256 && unit_lo < std::min(unit_hi, k.half) && a.d * 8 < (1ULL << 32) &&
-        cand_per_warp <= 1.0 && aligned16(a.pool) && aligned16(a.out) && aligned16(a.lower) && aligned16(a.upper) &&
+        cand_per_warp <= 1.0 && (a.src_ptr != nullptr || aligned16(a.pool)) && aligned16(a.out) && aligned16(a.lower) && aligned16(a.upper) &&
         !force_generic_kernel()) {
         // bounds as launch constants: 0 arrays, 1 one constant segment (DTLZ), 2 two constant segments (LSMOP)
         int seg = 0;

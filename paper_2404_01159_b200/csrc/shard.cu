@@ -4,11 +4,25 @@
 // reference: the same rvea_run loop (algorithms.hpp:227-296); the reference itself is single-process.
 // Sharding: rank g owns the mating pairs [g*h_loc, (g+1)*h_loc) of the shuffled order (h_loc = n/2/G),
 // i.e. the children with global rows p and n/2+p; a survivor stays in the pool of the rank where it was
-// born. Replicated on every rank (a few MB): the merged objective matrix, the reference set with its
-// direction index, and the survivor -> (owner, slot) tables (kept by the host orchestration).
-// Exchanges per generation: parents of a rank's pairs (all-to-all of rows), offspring objectives and
-// free-slot lists (all-gather), per-vector minima (two min-allreduces). Everything else is rank-local and
-// draws/evaluates/selects exactly what the single-GPU run does for the same rows (global draw addressing).
+// born. Replicated on every rank, IN DEVICE MEMORY (a few MB): the merged objective matrix, the reference
+// set with its direction index, and the survivor -> (owner rank, pool slot) tables.
+//
+// Parents: the mating shuffle pairs arbitrary rows, so a rank's pairs need parents from every rank's pool.
+// They are not copied: every rank maps its peers' pools into its address space once (CUDA IPC over
+// NVLink / NVSwitch), a kernel turns the replicated tables into one parent ADDRESS per local mating row,
+// and K1 streams the remote rows directly (40 KB contiguous each, 128-bit loads: NVLink peer loads inside the
+// kernel, overlapped tile by tile with its arithmetic and its local stores). No pack kernel, no all-to-all,
+// no receive buffer, no host-side exchange plan. (The first round's design - host plan + pack + NCCL all-to-all of
+// rows, pipelined in chunks - cost 11.0 ms per generation at world size 1 against 3.9 ms for the monolithic loop.)
+// Exchanges per generation (NCCL, small): offspring objectives and free-slot lists (all-gather), per-vector
+// minima (two min-allreduces). The host reads one word per generation (the survivor count, which decides the
+// next generation's draw counters: algorithms.hpp:211-221) and ships the mating permutation (4 n bytes).
+//
+// Why remote reads are ordered without extra synchronisation: a rank's K1 of generation t+1 is enqueued behind
+// its collectives of generation t on the same stream; those complete only after every peer has contributed,
+// and a peer contributes behind its own K1 of generation t. So (i) every row a rank reads was written before
+// the reader's K1 starts, and (ii) a slot freed by selection t is overwritten by its owner's K1 of t+1 only after
+// every reader's K1 of generation t has finished (free slots never hold a current survivor).
 #include <cstring>
 #include <numeric>
 #include <thread>
@@ -26,13 +40,31 @@ namespace {
 __global__ void gather_slots_kernel(const double* pool, const uint32_t* slot, uint64_t rows, uint64_t d, double* out) {
     const uint64_t i = blockIdx.x;
     if (i >= rows) return;
-    const double2* p = reinterpret_cast<const double2*>(pool + (uint64_t)slot[i] * d);
-    double2* o = reinterpret_cast<double2*>(out + i * d);
-    if (d % 2 == 0) {
-        for (uint64_t j = threadIdx.x; j < d / 2; j += blockDim.x) o[j] = p[j];
-    } else {
-        for (uint64_t j = threadIdx.x; j < d; j += blockDim.x) out[i * d + j] = pool[(uint64_t)slot[i] * d + j];
-    }
+    for (uint64_t j = threadIdx.x; j < d; j += blockDim.x) out[i * d + j] = pool[(uint64_t)slot[i] * d + j];
+}
+
+// initial tables: global row i lives on rank i / n_loc in slot i % n_loc (contiguous blocks of the initial population)
+__global__ void init_tables_kernel(uint64_t n, uint64_t n_loc, uint32_t* owner, uint32_t* slot) {
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    owner[i] = (uint32_t)(i / n_loc);
+    slot[i] = (uint32_t)(i % n_loc);
+}
+
+// Address of the parent of every local mating row: local row j is global mating row i (first halves of the pairs, then
+// second halves); its parent is survivor k = pool_idx[perm[i]] (algorithms.hpp:211-221, operators.hpp:155-158), which
+// lives in pool `owner[k]` at slot `slot[k]`.
+template <int MODE>
+__global__ void parent_ptr_kernel(const uint32_t* __restrict__ perm, const uint32_t* __restrict__ owner, const uint32_t* __restrict__ slot,
+                                  uint64_t n, uint64_t h_loc, uint64_t rank, uint64_t P, Rng rng, uint64_t c_pool, uint64_t d,
+                                  const double* const* __restrict__ peer_pool, const double** __restrict__ parent) {
+    const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (j >= 2 * h_loc) return;
+    const uint64_t i = j < h_loc ? rank * h_loc + j : n / 2 + rank * h_loc + (j - h_loc);
+    const uint64_t q = perm[i];
+    uint64_t k = q;
+    if (P != n) k = (uint64_t)(word_to_unit(draw_word<MODE>(rng, c_pool + q)) * (double)P);
+    parent[j] = peer_pool[owner[k]] + (uint64_t)slot[k] * d;
 }
 
 // gathered[rank][local child j][m] -> merged rows P + global child row
@@ -46,16 +78,37 @@ __global__ void scatter_offspring_f_kernel(const double* gathered, uint64_t worl
     for (uint64_t k = 0; k < m; ++k) fm[(P + g) * m + k] = gathered[e * m + k];
 }
 
-__global__ void compact_f_kernel(const uint32_t* elite, uint64_t cnt, uint64_t m, const double* f_merged, double* f_next) {
+// Survivor k takes over merged row elite[k] (algorithms.hpp:278-279 in sharded form): a parent keeps its (owner, slot);
+// child i = elite[k] - P lives on the rank that produced it, in that rank's free slot free_all[rank * n_loc + local
+// child index]. Also: objectives compacted, the slots this rank owns marked used, the survivor count published.
+__global__ void update_tables_kernel(const uint32_t* __restrict__ elite, const uint32_t* __restrict__ n_elite, uint64_t P, uint64_t n,
+                                     uint64_t h_loc, uint32_t rank, const uint32_t* __restrict__ free_all,
+                                     const uint32_t* __restrict__ owner, const uint32_t* __restrict__ slot,
+                                     uint32_t* __restrict__ owner_next, uint32_t* __restrict__ slot_next, uint64_t m,
+                                     const double* __restrict__ f_merged, double* __restrict__ f_next, unsigned char* __restrict__ used,
+                                     uint32_t* d_P, uint32_t* own_count) {
     const uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint32_t cnt = *n_elite;
+    if (k == 0) *d_P = cnt;
     if (k >= cnt) return;
     const uint64_t e = elite[k];
+    uint32_t o, s;
+    if (e < P) {
+        o = owner[e];
+        s = slot[e];
+    } else {
+        const uint64_t i = e - P, half = n / 2, p = i < half ? i : i - half;
+        const uint64_t rk = p / h_loc, j = i < half ? p - rk * h_loc : h_loc + p - rk * h_loc;
+        o = (uint32_t)rk;
+        s = free_all[rk * 2 * h_loc + j];
+    }
+    owner_next[k] = o;
+    slot_next[k] = s;
+    if (o == rank) {
+        used[s] = 1;
+        atomicAdd(own_count, 1u);
+    }
     for (uint64_t j = 0; j < m; ++j) f_next[k * m + j] = f_merged[e * m + j];
-}
-
-__global__ void mark_used_kernel(const uint32_t* slots, uint64_t cnt, unsigned char* used) {
-    const uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    if (k < cnt) used[slots[k]] = 1;
 }
 
 // order-preserving signed view of the unsigned APD keys, so that an int64 min-allreduce merges them
@@ -80,144 +133,54 @@ struct IdentityValS {
 
 }  // namespace
 
-// Speculative mating permutation: the Fisher-Yates shuffle of generation t+1 only depends on the draw
-// counter, so a host thread computes it while the GPU is busy with generation t (rng.hpp:69-78).
-struct PermCache {
-    std::thread worker;
-    std::vector<uint32_t> perm;
-    uint64_t seed = 0, c_shuffle = 0, n = 0;
-    bool valid = false;
-    void start(uint64_t seed_, uint64_t c_shuffle_, uint64_t n_) {
-        join();
-        seed = seed_;
-        c_shuffle = c_shuffle_;
-        n = n_;
-        valid = true;
-        worker = std::thread([this] {
-            perm.resize(n);
-            uint64_t c = c_shuffle;
-            shuffle_indices(seed, c, n, perm.data());
-        });
-    }
-    void join() {
-        if (worker.joinable()) worker.join();
-    }
-    bool take(uint64_t seed_, uint64_t c_shuffle_, uint64_t n_, std::vector<uint32_t>& out) {
-        join();
-        if (!valid || seed != seed_ || c_shuffle != c_shuffle_ || n != n_) return false;
-        out.swap(perm);
-        valid = false;
-        return true;
-    }
-    ~PermCache() { join(); }
-};
-static PermCache g_perm_cache;
-
-// Host-side exchange plan of one generation (pure host code; exercised on CPU by the gloo tests).
-// Inputs: the replicated survivor tables and the draw counter at the top of the generation.
-// Outputs (for `rank`): the local slots to send, grouped by destination rank and ordered by the
-// destination's local mating row; send/recv row counts per peer; for every local mating row its row in
-// the receive buffer; and the draw counters of the generation.
-// The exchange is cut into `chunks` pieces by local mating pair (pair p of a rank belongs to chunk p / ceil(h_loc / chunks)):
-// piece c carries the parents of the pairs of chunk c, so K1 can start on chunk c while piece c + 1 is still on the
-// wire. Layout: send_slots ordered by (chunk, destination), counts indexed [chunk * world + peer], the receive buffer
-// filled chunk after chunk and, inside a chunk, source after source (the order all_to_all delivers).
-void shard_plan(uint64_t seed, uint64_t counter, uint64_t P, uint64_t n, int rank, int world, int chunks, const int32_t* surv_owner,
-                const uint32_t* surv_slot, std::vector<uint32_t>& send_slots, std::vector<uint64_t>& send_counts,
-                std::vector<uint64_t>& recv_counts, std::vector<uint32_t>& recv_pos, uint64_t counters_out[3]) {
-    require(world >= 1 && rank >= 0 && rank < world, "shard_plan: bad rank");
-    require(chunks >= 1, "shard_plan: at least one chunk");
-    require(n % (2 * (uint64_t)world) == 0, "shard_plan: population must be divisible by 2 * world size");
-    const uint64_t half = n / 2, h_loc = half / world, n_loc = 2 * h_loc;
-    const uint64_t per_chunk = (h_loc + (uint64_t)chunks - 1) / (uint64_t)chunks;  // pairs per chunk
-    uint64_t c = counter;
-    const uint64_t c_pool = c;
-    if (P != n) c += n;  // algorithms.hpp:211-221
-    std::vector<uint32_t> perm;
-    if (g_perm_cache.take(seed, c, n, perm)) {
-        c += n - 1;  // computed ahead of time by the speculation thread
-    } else {
-        perm.resize(n);
-        shuffle_indices(seed, c, n, perm.data());  // advances c by n - 1
-    }
-    counters_out[0] = c;                       // c_sbx: first draw after the shuffle
-    const uint64_t base = mix64(seed);
-    auto pool_idx = [&](uint64_t q) -> uint64_t {
-        if (P == n) return q;
-        const double u = (double)(mix64(base + (c_pool + q) * kGolden) >> 11) * 0x1.0p-53;
-        return (uint64_t)(u * (double)P);
-    };
-    // mating row i of the shuffled order is handled by rank (i mod half) / h_loc, local row
-    // (i < half ? i - dest*h_loc : h_loc + (i - half) - dest*h_loc)
-    const size_t cells = (size_t)chunks * (size_t)world;
-    send_counts.assign(cells, 0);
-    recv_counts.assign(cells, 0);
-    recv_pos.assign(n_loc, 0);
-    std::vector<std::vector<uint32_t>> send_cell(cells);  // [chunk * world + dest]: my slots to send
-    std::vector<std::vector<uint32_t>> recv_cell(cells);  // [chunk * world + src]: my local mating rows fed by src
-    // every destination is independent (its own cells; only dest == rank fills the receive cells): one host thread
-    // per destination keeps this O(n) bookkeeping at O(n / world) wall time on every rank
-    auto plan_dest = [&](int dest) {
-        for (uint64_t j = 0; j < n_loc; ++j) {
-            const uint64_t pair = j < h_loc ? j : j - h_loc;
-            const size_t chunk = (size_t)(pair / per_chunk);
-            const uint64_t i = j < h_loc ? dest * h_loc + j : half + dest * h_loc + (j - h_loc);
-            const uint64_t k = pool_idx(perm[i]);
-            const int owner = surv_owner[k];
-            if (owner == rank) send_cell[chunk * world + dest].push_back(surv_slot[k]);
-            if (dest == rank) recv_cell[chunk * world + owner].push_back((uint32_t)j);
-        }
-    };
-    if (world > 1 && n_loc >= 4096) {
-        std::vector<std::thread> workers;
-        for (int dest = 1; dest < world; ++dest) workers.emplace_back(plan_dest, dest);
-        plan_dest(0);
-        for (auto& w : workers) w.join();
-    } else {
-        for (int dest = 0; dest < world; ++dest) plan_dest(dest);
-    }
-    send_slots.clear();
-    uint32_t pos = 0;
-    for (size_t cell = 0; cell < cells; ++cell) {
-        send_counts[cell] = send_cell[cell].size();
-        send_slots.insert(send_slots.end(), send_cell[cell].begin(), send_cell[cell].end());
-        recv_counts[cell] = recv_cell[cell].size();
-        for (const uint32_t j : recv_cell[cell]) recv_pos[j] = pos++;
-    }
-    counters_out[1] = counters_out[2] = 0;  // filled by the caller (needs d)
-}
-
 struct Shard {
     RunConfig cfg;
     int rank = 0, world = 1;
     uint64_t n = 0, d = 0, m = 0, r = 0, H = 0, adapt_every = 1;
-    uint64_t h_loc = 0, n_loc = 0, pcap = 0, cap_loc = 0, send_cap = 0;
+    uint64_t h_loc = 0, n_loc = 0, pcap = 0, cap_loc = 0;
     Rng rng{};
     cudaStream_t stream = nullptr;
-    double* pool = nullptr;       // cap_loc x d (local rows only)
-    double* send_buf = nullptr;   // send_cap x d
-    double* recv_buf = nullptr;   // n_loc x d
-    uint32_t* send_slots = nullptr;  // send_cap
-    uint32_t* recv_pos = nullptr;    // n_loc
-    uint32_t* free_slot = nullptr;   // n_loc
-    uint32_t* surv_slots_dev = nullptr;  // pcap (local slots owned by this rank)
+    // population
+    double* pool = nullptr;                  // cap_loc x d (the rows born on this rank)
+    std::vector<void*> peer_host;            // pools of all ranks as seen from this process
+    std::vector<bool> peer_opened;           // mapped through cudaIpcOpenMemHandle (to be closed)
+    const double** peer_pool = nullptr;      // device copy of peer_host
+    const double** parent = nullptr;         // [n_loc] parent address of every local mating row
+    uint32_t* free_slot = nullptr;           // [n_loc] where this rank's children go
+    uint32_t* free_all = nullptr;            // [world x n_loc] all ranks' free-slot lists (all-gathered)
     unsigned char* used = nullptr;
     uint32_t* free_scratch = nullptr;
-    double* fm[2] = {nullptr, nullptr};  // replicated merged objectives, (pcap + n) x m
+    uint32_t *owner[2] = {nullptr, nullptr}, *slot[2] = {nullptr, nullptr};  // replicated survivor tables [pcap]
+    int tcur = 0;
+    uint32_t* perm_dev = nullptr;            // [n] mating permutation of the current generation
+    uint32_t* h_perm[2] = {nullptr, nullptr};  // pinned; [hp] current, [hp ^ 1] being shuffled for the next generation
+    int hp = 0;
+    std::thread perm_worker;
+    uint64_t spec_c_shuffle = 0;
+    bool spec_valid = false;
+    // objectives, reference set, selection
+    double* fm[2] = {nullptr, nullptr};      // replicated merged objectives, (pcap + n) x m
     int cur = 0;
-    double* f_off_loc = nullptr;  // n_loc x m
-    double* f_gather = nullptr;   // world x n_loc x m
+    double* f_off_loc = nullptr;             // n_loc x m
+    double* f_gather = nullptr;              // world x n_loc x m
     double *v0 = nullptr, *v = nullptr, *gamma = nullptr, *lower = nullptr, *upper = nullptr;
     BoundSegments bound_seg;
     double *zmin = nullptr, *zmax = nullptr;
     unsigned long long* zscratch = nullptr;
     uint32_t* skip_flag = nullptr;
+    uint32_t* d_P = nullptr;                 // [2]: survivor count, survivors owned by this rank
+    uint32_t* h_status = nullptr;            // pinned: [0] error flags, [1] survivor count, [2] own count
     SelectWorkspace ws;
     VecIndex vindex;
+    // loop state (host)
+    uint64_t P = 0, counter = 0, t = 0, lo = 0, hi = 0;
+    uint64_t c_sbx = 0, c_pm = 0, c_end = 0;
+    uint64_t launches = 0;                   // kernels + copies enqueued by this shard so far
 
     Shard(const RunConfig& c, int rank_, int world_) : cfg(c), rank(rank_), world(world_) {
         require(world >= 1 && rank >= 0 && rank < world, "shard: bad rank");
         require(problem_known(cfg.problem), "make_problem: unknown problem");
+        require(cfg.op == kOpGa, "shard: the sharded loop runs the ga operator");
         n = cfg.pop;
         m = cfg.obj;
         if (cfg.problem == kToy2 || cfg.problem == kToy3) m = cfg.problem == kToy2 ? 2 : 3;  // problems.hpp:279-287
@@ -235,18 +198,26 @@ struct Shard {
         // survivors are spread over the ranks like their births (uniformly): 60 % head-room over the mean
         const uint64_t own_cap = world == 1 ? pcap : std::min<uint64_t>(pcap, (pcap * 8) / (5 * (uint64_t)world) + 1024);
         cap_loc = own_cap + n_loc;
-        send_cap = world == 1 ? n_loc : std::min<uint64_t>(n, 2 * n_loc + 1024);
+        require(cap_loc < 0xffffffffULL && pcap + n < 0xffffffffULL, "shard: population too large for 32-bit slots");
         stream = ctx().stream;
         pool = dev_alloc<double>(cap_loc * d);
-        send_buf = dev_alloc<double>(send_cap * d);
-        recv_buf = dev_alloc<double>(n_loc * d);
-        send_slots = dev_alloc<uint32_t>(send_cap);
-        recv_pos = dev_alloc<uint32_t>(n_loc);
+        peer_host.assign(world, nullptr);
+        peer_opened.assign(world, false);
+        peer_host[rank] = pool;
+        peer_pool = reinterpret_cast<const double**>(reinterpret_cast<void*>(dev_alloc<void*>(world)));
+        parent = reinterpret_cast<const double**>(reinterpret_cast<void*>(dev_alloc<void*>(n_loc)));
         free_slot = dev_alloc<uint32_t>(n_loc);
-        surv_slots_dev = dev_alloc<uint32_t>(pcap);
+        free_all = dev_alloc<uint32_t>((uint64_t)world * n_loc);
         used = dev_alloc<unsigned char>(cap_loc);
         free_scratch = dev_alloc<uint32_t>((cap_loc + kCompactTile - 1) / kCompactTile + 1);
-        for (int b = 0; b < 2; ++b) fm[b] = dev_alloc<double>((pcap + n) * m);
+        for (int b = 0; b < 2; ++b) {
+            owner[b] = dev_alloc<uint32_t>(pcap);
+            slot[b] = dev_alloc<uint32_t>(pcap);
+            fm[b] = dev_alloc<double>((pcap + n) * m);
+            TEMO_CUDA(cudaHostAlloc(&h_perm[b], n * sizeof(uint32_t), cudaHostAllocDefault));
+        }
+        TEMO_CUDA(cudaHostAlloc(&h_status, 4 * sizeof(uint32_t), cudaHostAllocDefault));
+        perm_dev = dev_alloc<uint32_t>(n);
         f_off_loc = dev_alloc<double>(n_loc * m);
         f_gather = dev_alloc<double>((uint64_t)world * n_loc * m);
         v0 = dev_alloc<double>(r * m);
@@ -258,7 +229,9 @@ struct Shard {
         zmax = dev_alloc<double>(m);
         zscratch = dev_alloc<unsigned long long>(2 * m);
         skip_flag = dev_alloc<uint32_t>(1);
+        d_P = dev_alloc<uint32_t>(2);
         ws.alloc(pcap + n, r, m);
+        if (world == 1) set_peers_direct(peer_host.data());
         const std::vector<double> unit = normalize_to_unit(simplex_lattice(m, H), r, m);
         TEMO_CUDA(cudaMemcpyAsync(v0, unit.data(), r * m * sizeof(double), cudaMemcpyHostToDevice, stream));
         TEMO_CUDA(cudaMemcpyAsync(v, v0, r * m * sizeof(double), cudaMemcpyDeviceToDevice, stream));
@@ -267,41 +240,47 @@ struct Shard {
         vindex.set_order(unit.data(), stream);
         if (!assoc_filter_preferred(m, r)) vindex.build(v, ws.vn, stream);  // m >= 5: the fp32-filtered scans need no index
         launch_gamma_auto(v, r, m, ws, &vindex, gamma, ws.err_flag, nullptr, stream);
-        std::vector<double> lo(d), hi(d);
-        problem_bounds(cfg.problem, d, m, lo.data(), hi.data());
-        bound_seg = find_bound_segments(lo.data(), hi.data(), d);
-        TEMO_CUDA(cudaMemcpyAsync(lower, lo.data(), d * sizeof(double), cudaMemcpyHostToDevice, stream));
-        TEMO_CUDA(cudaMemcpyAsync(upper, hi.data(), d * sizeof(double), cudaMemcpyHostToDevice, stream));
+        std::vector<double> blo(d), bhi(d);
+        problem_bounds(cfg.problem, d, m, blo.data(), bhi.data());
+        bound_seg = find_bound_segments(blo.data(), bhi.data(), d);
+        TEMO_CUDA(cudaMemcpyAsync(lower, blo.data(), d * sizeof(double), cudaMemcpyHostToDevice, stream));
+        TEMO_CUDA(cudaMemcpyAsync(upper, bhi.data(), d * sizeof(double), cudaMemcpyHostToDevice, stream));
         // initial population (algorithms.hpp:241-242): global rows [rank*n/world, (rank+1)*n/world) in local
         // slots 0.., drawn at their global counters; objectives of the local block
-        const uint64_t rows0 = n / world;
-        launch_random_reproduce(pool, nullptr, rows0, d, rng, (uint64_t)rank * rows0 * d, lower, upper, stream);
+        launch_random_reproduce(pool, nullptr, n_loc, d, rng, (uint64_t)rank * n_loc * d, lower, upper, stream);
         EvalArgs ea;
         ea.problem = cfg.problem;
         ea.x = pool;
-        ea.n = rows0;
+        ea.n = n_loc;
         ea.d = d;
         ea.m = m;
         ea.horizon = cfg.horizon;
-        ea.f = f_off_loc;  // n/world = n_loc rows
+        ea.f = f_off_loc;
         launch_evaluate(ea, stream);
+        init_tables_kernel<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(n, n_loc, owner[tcur], slot[tcur]);
         TEMO_CUDA(cudaMemsetAsync(used, 0, cap_loc, stream));
-        std::vector<uint32_t> own(rows0);
-        std::iota(own.begin(), own.end(), 0u);
-        TEMO_CUDA(cudaMemcpyAsync(surv_slots_dev, own.data(), rows0 * sizeof(uint32_t), cudaMemcpyHostToDevice, stream));
-        mark_used_kernel<<<(unsigned)((rows0 + 255) / 256), 256, 0, stream>>>(surv_slots_dev, rows0, used);
+        TEMO_CUDA(cudaMemsetAsync(used, 1, n_loc, stream));  // slots 0 .. n_loc - 1 hold the initial block
         launch_compact(cap_loc, FreePredS{used}, IdentityValS{}, free_scratch, n_loc, free_slot, nullptr, stream);
         TEMO_CUDA(cudaStreamSynchronize(stream));
         check();
+        P = n;
+        counter = n * d;  // operators.hpp:287-296: n*d draws for the initial population
     }
 
     ~Shard() {
+        if (perm_worker.joinable()) perm_worker.join();
         cudaStreamSynchronize(stream);
-        cudaFree(pool); cudaFree(send_buf); cudaFree(recv_buf); cudaFree(send_slots); cudaFree(recv_pos);
-        cudaFree(free_slot); cudaFree(surv_slots_dev); cudaFree(used); cudaFree(free_scratch);
-        cudaFree(fm[0]); cudaFree(fm[1]); cudaFree(f_off_loc); cudaFree(f_gather);
+        for (int g = 0; g < world; ++g)
+            if (peer_opened[g]) cudaIpcCloseMemHandle(peer_host[g]);
+        cudaFree(pool); cudaFree(peer_pool); cudaFree(parent); cudaFree(free_slot); cudaFree(free_all); cudaFree(used);
+        cudaFree(free_scratch); cudaFree(perm_dev); cudaFree(f_off_loc); cudaFree(f_gather);
+        for (int b = 0; b < 2; ++b) {
+            cudaFree(owner[b]); cudaFree(slot[b]); cudaFree(fm[b]);
+            cudaFreeHost(h_perm[b]);
+        }
+        cudaFreeHost(h_status);
         cudaFree(v0); cudaFree(v); cudaFree(gamma); cudaFree(lower); cudaFree(upper);
-        cudaFree(zmin); cudaFree(zmax); cudaFree(zscratch); cudaFree(skip_flag);
+        cudaFree(zmin); cudaFree(zmax); cudaFree(zscratch); cudaFree(skip_flag); cudaFree(d_P);
         ws.release();
         vindex.release();
     }
@@ -314,25 +293,87 @@ struct Shard {
         if (flag & 2u) fail(1, "normalize_to_unit: zero row");
     }
 
-    // rows of the send buffer <- local pool rows (slots given by the plan)
-    // (rows [row0, row0 + count) of the send buffer: one piece of a chunked exchange)
-    void pack(const uint32_t* slots_host, uint64_t count, uint64_t row0) {
-        require(row0 <= send_cap && count <= send_cap - row0, "shard: send buffer too small (ownership imbalance)");
-        if (count == 0) return;
-        TEMO_CUDA(cudaMemcpyAsync(send_slots + row0, slots_host, count * sizeof(uint32_t), cudaMemcpyHostToDevice, stream));
-        gather_slots_kernel<<<(unsigned)count, 256, 0, stream>>>(pool, send_slots + row0, count, d, send_buf + row0 * d);
-        TEMO_CUDA(cudaGetLastError());
+    // ---- peer pools
+    void ipc_handle(unsigned char* out64) {
+        static_assert(sizeof(cudaIpcMemHandle_t) == 64, "CUDA IPC handles are 64 bytes");
+        cudaIpcMemHandle_t h;
+        TEMO_CUDA(cudaIpcGetMemHandle(&h, pool));
+        std::memcpy(out64, &h, sizeof(h));
+    }
+    void open_peers(const unsigned char* handles) {  // world x 64 bytes, all-gathered by the caller
+        for (int g = 0; g < world; ++g) {
+            if (g == rank) continue;
+            cudaIpcMemHandle_t h;
+            std::memcpy(&h, handles + 64 * (size_t)g, sizeof(h));
+            void* p = nullptr;
+            TEMO_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+            peer_host[g] = p;
+            peer_opened[g] = true;
+        }
+        set_peers_direct(peer_host.data());
+    }
+    void set_peers_direct(void* const* ptrs) {  // pools already addressable from this process
+        for (int g = 0; g < world; ++g) {
+            require(ptrs[g] != nullptr && (reinterpret_cast<uintptr_t>(ptrs[g]) & 15u) == 0, "shard: bad peer pool pointer");
+            peer_host[g] = ptrs[g];
+        }
+        TEMO_CUDA(cudaMemcpyAsync(peer_pool, peer_host.data(), world * sizeof(void*), cudaMemcpyHostToDevice, stream));
+        TEMO_CUDA(cudaStreamSynchronize(stream));
     }
 
-    // K1 (+ fused evaluation) on this rank's pairs; parents in recv_buf at recv_pos_host[]
-    // (pairs [unit_begin, unit_begin + unit_count) only; unit_count = 0: all of them)
-    void reproduce(const uint32_t* recv_pos_host, uint64_t c_sbx, uint64_t c_pm, uint64_t unit_begin, uint64_t unit_count) {
-        require(unit_begin <= h_loc && unit_count <= h_loc - unit_begin, "shard: bad pair range");
-        if (unit_begin == 0)
-            TEMO_CUDA(cudaMemcpyAsync(recv_pos, recv_pos_host, n_loc * sizeof(uint32_t), cudaMemcpyHostToDevice, stream));
+    // ---- the mating permutation: shuffled on a host thread for the next generation while the GPU works on this one
+    void shuffle_into(uint32_t* dst, uint64_t c_shuffle) {
+        uint64_t c = c_shuffle;
+        shuffle_indices(cfg.seed, c, n, dst);
+    }
+    void ensure_permutation(uint64_t c_shuffle) {
+        if (perm_worker.joinable()) perm_worker.join();
+        if (spec_valid && spec_c_shuffle == c_shuffle) {
+            hp ^= 1;  // the speculation was right
+        } else {
+            shuffle_into(h_perm[hp], c_shuffle);
+        }
+        spec_valid = false;
+    }
+    void prefetch_permutation(uint64_t c_shuffle) {
+        spec_c_shuffle = c_shuffle;
+        spec_valid = true;
+        uint32_t* dst = h_perm[hp ^ 1];
+        perm_worker = std::thread([this, dst, c_shuffle] { shuffle_into(dst, c_shuffle); });
+    }
+
+    // ---- stage 1: draw counters of the generation, permutation, parent addresses
+    void begin() {
+        require(t < cfg.generations, "rvea_run: all generations already done");
+        uint64_t c = counter;
+        const uint64_t c_pool = c;
+        if (P != n) c += n;  // algorithms.hpp:211-221
+        ensure_permutation(c);
+        c += n - 1;
+        c_sbx = c;
+        c_pm = c_sbx + 3 * (n / 2) * d + n / 2;
+        c_end = c_pm + 2 * n * d;
+        TEMO_CUDA(cudaMemcpyAsync(perm_dev, h_perm[hp], n * sizeof(uint32_t), cudaMemcpyHostToDevice, stream));
+        const unsigned g = (unsigned)((n_loc + 255) / 256);
+        if (rng.mode == 0)
+            parent_ptr_kernel<0><<<g, 256, 0, stream>>>(perm_dev, owner[tcur], slot[tcur], n, h_loc, (uint64_t)rank, P, rng, c_pool, d,
+                                                        peer_pool, parent);
+        else
+            parent_ptr_kernel<1><<<g, 256, 0, stream>>>(perm_dev, owner[tcur], slot[tcur], n, h_loc, (uint64_t)rank, P, rng, c_pool, d,
+                                                        peer_pool, parent);
+        TEMO_CUDA(cudaGetLastError());
+        launches += 2;
+        // the next generation's shuffle (its counter assumes a survivor count != n; redone in the rare other case)
+        if (t + 1 < cfg.generations) prefetch_permutation(c_end + n);
+        const uint64_t rows = P + n;
+        lo = rows * (uint64_t)rank / (uint64_t)world;
+        hi = rows * (uint64_t)(rank + 1) / (uint64_t)world;
+    }
+
+    // ---- stage 2: K1 (+ fused evaluation) on this rank's pairs; parents streamed from wherever they live
+    void reproduce() {
         ReproArgs ra;
-        ra.pool = recv_buf;
-        ra.src = recv_pos;
+        ra.src_ptr = parent;
         ra.out = pool;
         ra.dst = free_slot;
         ra.n = n_loc;
@@ -346,8 +387,6 @@ struct Shard {
         ra.seg = bound_seg;
         ra.global_n = n;
         ra.global_unit0 = (uint64_t)rank * h_loc;
-        ra.unit_begin = unit_begin;
-        ra.unit_count = unit_count;
         const bool fused = cfg.fuse_eval && cfg.problem >= kDtlz1 && cfg.problem <= kDtlz4;
         if (fused) {
             ra.eval_problem = cfg.problem;
@@ -356,8 +395,8 @@ struct Shard {
             ra.f_row0 = 0;
         }
         launch_reproduce(ra, stream);
-        const bool last = unit_count == 0 || unit_begin + unit_count == h_loc;
-        if (!fused && last) {  // unfused problems are evaluated once every child exists
+        launches += fused ? 3 : 1;
+        if (!fused) {
             EvalArgs ea;
             ea.problem = cfg.problem;
             ea.x = pool;
@@ -368,25 +407,21 @@ struct Shard {
             ea.horizon = cfg.horizon;
             ea.f = f_off_loc;
             launch_evaluate(ea, stream);
+            launches += 2;
         }
     }
 
-    // f_gather (all-gathered offspring objectives) -> merged rows [P, P + n); P = 0 with `initial` puts the
-    // gathered blocks of the initial population into rows [0, n) in global order
-    void place_offspring_f(uint64_t P, bool initial) {
-        if (initial) {
-            TEMO_CUDA(cudaMemcpyAsync(fm[cur], f_gather, n * m * sizeof(double), cudaMemcpyDeviceToDevice, stream));
-        } else {
-            const uint64_t total = (uint64_t)world * n_loc;
-            scatter_offspring_f_kernel<<<(unsigned)((total + 255) / 256), 256, 0, stream>>>(f_gather, world, h_loc, n / 2, m, P, fm[cur]);
-        }
-        TEMO_CUDA(cudaGetLastError());
+    // f_gather (all-gathered objectives) -> rows [0, n) in global order (initial population)
+    void place_initial_f() {
+        TEMO_CUDA(cudaMemcpyAsync(fm[cur], f_gather, n * m * sizeof(double), cudaMemcpyDeviceToDevice, stream));
+        ++launches;
     }
 
-    // ideal point + association/APD for merged rows [lo, hi) + this rank's per-vector minima
-    void select_local(uint64_t P, uint64_t lo, uint64_t hi, uint64_t t) {
-        const uint64_t rows = P + n;
-        require(lo <= hi && hi <= rows, "shard: bad row slice");
+    // ---- stage 3 (after the all-gathers): merged objectives, ideal point, association / APD of this rank's slice of
+    // merged rows, local per-vector minima in the order-preserving signed views the min-allreduces need
+    void select_local() {
+        const uint64_t total = (uint64_t)world * n_loc, rows = P + n;
+        scatter_offspring_f_kernel<<<(unsigned)((total + 255) / 256), 256, 0, stream>>>(f_gather, world, h_loc, n / 2, m, P, fm[cur]);
         const double penalty = apd_penalty(m, t, cfg.generations, cfg.alpha);
         launch_select_prepare(fm[cur], rows, m, gamma, r, ws, stream);
         if (hi > lo) {
@@ -399,46 +434,55 @@ struct Shard {
         }
         flip_keys_kernel<<<(unsigned)((r + 255) / 256), 256, 0, stream>>>(ws.best_key, r);
         flip_rows_kernel<<<(unsigned)((r + 255) / 256), 256, 0, stream>>>(ws.first_row, r);
+        TEMO_CUDA(cudaGetLastError());
+        launches += 11;
     }
 
-    // after the min-allreduce of best_key / first_row: lowest row attaining the minimum, own slice
-    void select_rows(uint64_t lo, uint64_t hi) {
+    // ---- stage 4 (after the min-allreduce of best_key / first_row): lowest row attaining the minimum, own slice
+    void select_rows() {
         flip_keys_kernel<<<(unsigned)((r + 255) / 256), 256, 0, stream>>>(ws.best_key, r);
         flip_rows_kernel<<<(unsigned)((r + 255) / 256), 256, 0, stream>>>(ws.first_row, r);
         if (hi > lo) launch_elite_rows(hi - lo, ws.assoc + lo, ws.apd + lo, ws.best_key, ws.best_row, (uint32_t)lo, stream);
         flip_rows_kernel<<<(unsigned)((r + 255) / 256), 256, 0, stream>>>(ws.best_row, r);
+        TEMO_CUDA(cudaGetLastError());
+        launches += 4;
     }
 
-    // after the min-allreduce of best_row: validity + compaction; returns the survivor count
-    uint64_t select_finish(uint32_t* elite_host) {
+    // ---- stage 5 (after the min-allreduce of best_row): compaction, survivor tables, free list, adaptation; the one
+    // host synchronisation of the generation reads the survivor count back
+    uint64_t finish() {
         flip_rows_kernel<<<(unsigned)((r + 255) / 256), 256, 0, stream>>>(ws.best_row, r);
         launch_select_finish(r, ws, /*nan_rule=*/false, stream);
-        uint32_t cnt = 0;
-        TEMO_CUDA(cudaMemcpyAsync(&cnt, ws.n_elite, sizeof(uint32_t), cudaMemcpyDeviceToHost, stream));
-        TEMO_CUDA(cudaStreamSynchronize(stream));
-        if (elite_host && cnt) TEMO_CUDA(cudaMemcpy(elite_host, ws.elite, cnt * sizeof(uint32_t), cudaMemcpyDeviceToHost));
-        return cnt;
-    }
-
-    // survivors' objectives compacted (replicated); slots owned by this rank re-marked; free list rebuilt
-    void commit(uint64_t cnt, const uint32_t* own_slots_host, uint64_t own_count, uint64_t t) {
-        require(own_count + n_loc <= cap_loc, "shard: local pool too small (ownership imbalance)");
-        compact_f_kernel<<<(unsigned)((cnt + 255) / 256), 256, 0, stream>>>(ws.elite, cnt, m, fm[cur], fm[cur ^ 1]);
-        cur ^= 1;
         TEMO_CUDA(cudaMemsetAsync(used, 0, cap_loc, stream));
-        if (own_count) {
-            TEMO_CUDA(cudaMemcpyAsync(surv_slots_dev, own_slots_host, own_count * sizeof(uint32_t), cudaMemcpyHostToDevice, stream));
-            mark_used_kernel<<<(unsigned)((own_count + 255) / 256), 256, 0, stream>>>(surv_slots_dev, own_count, used);
-        }
+        TEMO_CUDA(cudaMemsetAsync(d_P + 1, 0, sizeof(uint32_t), stream));
+        const uint64_t kmax = r < P + n ? r : P + n;
+        update_tables_kernel<<<(unsigned)((kmax + 255) / 256), 256, 0, stream>>>(ws.elite, ws.n_elite, P, n, h_loc, (uint32_t)rank, free_all,
+                                                                               owner[tcur], slot[tcur], owner[tcur ^ 1], slot[tcur ^ 1], m,
+                                                                               fm[cur], fm[cur ^ 1], used, d_P, d_P + 1);
         launch_compact(cap_loc, FreePredS{used}, IdentityValS{}, free_scratch, n_loc, free_slot, nullptr, stream);
+        launches += 11;
         if ((t + 1) % adapt_every == 0) {  // algorithms.hpp:281 (replicated: every rank adapts identically)
-            launch_col_minmax(fm[cur], cnt, nullptr, m, zmin, zmax, zscratch, stream);
+            launch_col_minmax(fm[cur ^ 1], pcap, d_P, m, zmin, zmax, zscratch, stream);
             launch_adapt_vectors(v0, v, ws.vn, r, m, zmin, zmax, skip_flag, ws.err_flag, stream);
-            if (!assoc_filter_preferred(m, r)) vindex.build(v, ws.vn, stream);  // m >= 5: the fp32-filtered scans need no index
+            if (!assoc_filter_preferred(m, r)) vindex.build(v, ws.vn, stream);
             launch_gamma_auto(v, r, m, ws, &vindex, gamma, ws.err_flag, skip_flag, stream);
+            launches += 8 + vindex.levels;
         }
-        TEMO_CUDA(cudaStreamSynchronize(stream));  // host staging arrays may go away
-        check();
+        TEMO_CUDA(cudaMemcpyAsync(h_status, ws.err_flag, sizeof(uint32_t), cudaMemcpyDeviceToHost, stream));
+        TEMO_CUDA(cudaMemcpyAsync(h_status + 1, d_P, 2 * sizeof(uint32_t), cudaMemcpyDeviceToHost, stream));
+        TEMO_CUDA(cudaGetLastError());
+        TEMO_CUDA(cudaStreamSynchronize(stream));
+        if (h_status[0] & 1u) fail(1, "rv_select: gamma must be positive");
+        if (h_status[0] & 2u) fail(1, "normalize_to_unit: zero row");
+        const uint64_t cnt = h_status[1];
+        // this rank's share of the survivors plus its next children must fit its pool (births are spread uniformly)
+        require((uint64_t)h_status[2] + n_loc <= cap_loc, "shard: local pool too small (ownership imbalance)");
+        cur ^= 1;
+        tcur ^= 1;
+        P = cnt;
+        counter = c_end;
+        ++t;
+        return cnt;
     }
 };
 
@@ -472,87 +516,6 @@ extern "C" {
 
 const char* temo_b200_shard_last_error(void) { return g_shard_error.c_str(); }
 
-int temo_b200_shard_plan(uint64_t seed, uint64_t counter, uint64_t P, uint64_t n, uint64_t d, int rank, int world, int chunks,
-                         const int32_t* surv_owner, const uint32_t* surv_slot, uint32_t* send_slots,
-                         uint64_t send_slots_cap, uint64_t* send_counts, uint64_t* recv_counts, uint32_t* recv_pos,
-                         uint64_t* counters3) {
-    return guarded_shard([&] {
-        require(surv_owner && surv_slot && send_slots && send_counts && recv_counts && recv_pos && counters3,
-                "shard_plan: null argument");
-        std::vector<uint32_t> ss, rp;
-        std::vector<uint64_t> sc, rc;
-        uint64_t cs[3];
-        shard_plan(seed, counter, P, n, rank, world, chunks, surv_owner, surv_slot, ss, sc, rc, rp, cs);
-        require(ss.size() <= send_slots_cap, "shard_plan: send list exceeds the caller's capacity");
-        std::memcpy(send_slots, ss.data(), ss.size() * sizeof(uint32_t));
-        std::memcpy(send_counts, sc.data(), sc.size() * sizeof(uint64_t));
-        std::memcpy(recv_counts, rc.data(), rc.size() * sizeof(uint64_t));
-        std::memcpy(recv_pos, rp.data(), rp.size() * sizeof(uint32_t));
-        // draw counters: [pool n] + shuffle n-1, then SBX 3*h*d + h, then PM 2*n*d
-        const uint64_t half = n / 2;
-        counters3[0] = cs[0];                              // c_sbx
-        counters3[1] = cs[0] + 3 * half * d + half;        // c_pm
-        counters3[2] = counters3[1] + 2 * n * d;           // counter after the generation
-    });
-}
-
-// Starts the Fisher-Yates shuffle of a future generation on a host thread (consumed by the next
-// temo_b200_shard_plan with the same seed / shuffle counter / n; ignored otherwise).
-int temo_b200_shard_perm_prefetch(uint64_t seed, uint64_t c_shuffle, uint64_t n) {
-    return guarded_shard([&] {
-        require(n >= 1 && n < 0xffffffffULL, "shuffle_indices: n must be positive");
-        g_perm_cache.start(seed, c_shuffle, n);
-    });
-}
-
-// Pure host code: survivor tables after selection. Survivor k takes over merged row elite[k]: a parent keeps
-// its (owner, slot); child i = elite[k] - P lives on the rank that produced it, in that rank's free slot
-// (free_all[rank * n_loc + local child index]). Also lists the slots owned by `rank`.
-int temo_b200_shard_update_tables(const uint32_t* elite, uint64_t count, uint64_t P, uint64_t n, int rank, int world,
-                                  const uint32_t* free_all, int32_t* surv_owner, uint32_t* surv_slot,
-                                  uint32_t* own_slots, uint64_t* own_count) {
-    return guarded_shard([&] {
-        require(elite && free_all && surv_owner && surv_slot && own_slots && own_count, "update_tables: null argument");
-        const uint64_t half = n / 2, h_loc = half / world, n_loc = 2 * h_loc;
-        std::vector<int32_t> no(count);
-        std::vector<uint32_t> ns(count);
-        // ranges of survivors in parallel; the slots owned by `rank` are concatenated in survivor order afterwards
-        const unsigned parts = count >= 65536 ? std::min<unsigned>(8u, std::max(1u, std::thread::hardware_concurrency() / 2)) : 1u;
-        std::vector<std::vector<uint32_t>> mine_part(parts);
-        auto work = [&](unsigned part) {
-            const uint64_t k0 = count * part / parts, k1 = count * (part + 1) / parts;
-            for (uint64_t k = k0; k < k1; ++k) {
-                const uint64_t e = elite[k];
-                if (e < P) {
-                    no[k] = surv_owner[e];
-                    ns[k] = surv_slot[e];
-                } else {
-                    const uint64_t i = e - P, p = i < half ? i : i - half;
-                    const uint64_t rk = p / h_loc;
-                    const uint64_t j = i < half ? p - rk * h_loc : h_loc + p - rk * h_loc;
-                    no[k] = (int32_t)rk;
-                    ns[k] = free_all[rk * n_loc + j];
-                }
-                if (no[k] == rank) mine_part[part].push_back(ns[k]);
-            }
-        };
-        {
-            std::vector<std::thread> workers;
-            for (unsigned part = 1; part < parts; ++part) workers.emplace_back(work, part);
-            work(0);
-            for (auto& w : workers) w.join();
-        }
-        uint64_t mine = 0;
-        for (const auto& v : mine_part) {
-            std::memcpy(own_slots + mine, v.data(), v.size() * sizeof(uint32_t));
-            mine += v.size();
-        }
-        std::memcpy(surv_owner, no.data(), count * sizeof(int32_t));
-        std::memcpy(surv_slot, ns.data(), count * sizeof(uint32_t));
-        *own_count = mine;
-    });
-}
-
 int temo_b200_shard_create(const temo_b200_run_config* cfg, int rank, int world, temo_b200_shard** out) {
     return guarded_shard([&] {
         require(cfg && out, "shard_create: null argument");
@@ -572,6 +535,7 @@ int temo_b200_shard_create(const temo_b200_run_config* cfg, int rank, int world,
         rc.ga.pm = cfg->ga.pm;
         rc.ga.xi = cfg->ga.xi;
         rc.fuse_eval = cfg->fuse_eval;
+        rc.op = cfg->op;
         rc.horizon = cfg->horizon ? cfg->horizon : 100;
         *out = new temo_b200_shard{new Shard(rc, rank, world)};
     });
@@ -586,83 +550,124 @@ int temo_b200_shard_destroy(temo_b200_shard* s) {
     });
 }
 
-// sizes: [0] n_loc, [1] d, [2] m, [3] r, [4] send_cap, [5] pcap, [6] cap_loc, [7] adapt_every
+// sizes: [0] n_loc, [1] d, [2] m, [3] r, [4] pcap, [5] cap_loc, [6] adapt_every, [7] kernels / copies enqueued so far
 int temo_b200_shard_info(temo_b200_shard* s, uint64_t* info8) {
     return guarded_shard([&] {
         require(s && s->impl && info8, "shard_info: null argument");
         const Shard& S = *s->impl;
-        const uint64_t v[8] = {S.n_loc, S.d, S.m, S.r, S.send_cap, S.pcap, S.cap_loc, S.adapt_every};
+        const uint64_t v[8] = {S.n_loc, S.d, S.m, S.r, S.pcap, S.cap_loc, S.adapt_every, S.launches};
         std::memcpy(info8, v, sizeof(v));
     });
 }
 
-// device pointers the collectives operate on: which = 0 send_buf, 1 recv_buf, 2 f_off_loc, 3 f_gather,
-// 4 best_key (int64 view, R), 5 first_row (int32 view, R), 6 best_row (int32 view, R), 7 free_slot (int32 view, n_loc)
+// loop state: [0] survivor count, [1] draw counter, [2] generations done, [3] lo, [4] hi (this rank's slice of the merged rows
+// of the generation begun last)
+int temo_b200_shard_state(temo_b200_shard* s, uint64_t* state5) {
+    return guarded_shard([&] {
+        require(s && s->impl && state5, "shard_state: null argument");
+        const Shard& S = *s->impl;
+        const uint64_t v[5] = {S.P, S.counter, S.t, S.lo, S.hi};
+        std::memcpy(state5, v, sizeof(v));
+    });
+}
+
+// device pointers the collectives operate on: which = 0 f_off_loc (n_loc x m), 1 f_gather (world x n_loc x m),
+// 2 best_key (int64 view, R), 3 first_row (int32 view, R), 4 best_row (int32 view, R), 5 free_slot (int32 view, n_loc),
+// 6 free_all (int32 view, world x n_loc), 7 pool (cap_loc x d)
 void* temo_b200_shard_buffer(temo_b200_shard* s, int which) {
     if (!s || !s->impl) return nullptr;
     Shard& S = *s->impl;
     switch (which) {
-    case 0: return S.send_buf;
-    case 1: return S.recv_buf;
-    case 2: return S.f_off_loc;
-    case 3: return S.f_gather;
-    case 4: return S.ws.best_key;
-    case 5: return S.ws.first_row;
-    case 6: return S.ws.best_row;
-    case 7: return S.free_slot;
+    case 0: return S.f_off_loc;
+    case 1: return S.f_gather;
+    case 2: return S.ws.best_key;
+    case 3: return S.ws.first_row;
+    case 4: return S.ws.best_row;
+    case 5: return S.free_slot;
+    case 6: return S.free_all;
+    case 7: return S.pool;
     default: return nullptr;
     }
 }
 
-int temo_b200_shard_pack(temo_b200_shard* s, const uint32_t* slots, uint64_t count) {
-    return guarded_shard([&] { s->impl->pack(slots, count, 0); TEMO_CUDA(cudaStreamSynchronize(s->impl->stream)); });
-}
-int temo_b200_shard_reproduce(temo_b200_shard* s, const uint32_t* recv_pos, uint64_t c_sbx, uint64_t c_pm) {
-    return guarded_shard([&] { s->impl->reproduce(recv_pos, c_sbx, c_pm, 0, 0); TEMO_CUDA(cudaStreamSynchronize(s->impl->stream)); });
-}
-// Pieces of a chunked exchange; both only enqueue work on the shard's stream (temo_b200_shard_stream) and return.
-int temo_b200_shard_pack_at(temo_b200_shard* s, const uint32_t* slots, uint64_t count, uint64_t row0) {
-    return guarded_shard([&] { s->impl->pack(slots, count, row0); });
-}
-int temo_b200_shard_reproduce_range(temo_b200_shard* s, const uint32_t* recv_pos, uint64_t c_sbx, uint64_t c_pm,
-                                    uint64_t unit_begin, uint64_t unit_count) {
-    return guarded_shard([&] { s->impl->reproduce(recv_pos, c_sbx, c_pm, unit_begin, unit_count); });
-}
 // The CUDA stream (cudaStream_t) every stage of this shard is enqueued on: a caller that issues collectives on it
 // (or on a stream ordered against it) needs no device-wide synchronisation between stages.
 void* temo_b200_shard_stream(temo_b200_shard* s) { return (s && s->impl) ? (void*)s->impl->stream : nullptr; }
-int temo_b200_shard_place_f(temo_b200_shard* s, uint64_t P, int initial) {
-    return guarded_shard([&] { s->impl->place_offspring_f(P, initial != 0); });
+
+int temo_b200_shard_ipc_handle(temo_b200_shard* s, unsigned char* handle64) {
+    return guarded_shard([&] {
+        require(s && s->impl && handle64, "shard_ipc_handle: null argument");
+        s->impl->ipc_handle(handle64);
+    });
 }
-int temo_b200_shard_select_local(temo_b200_shard* s, uint64_t P, uint64_t lo, uint64_t hi, uint64_t t) {
-    return guarded_shard([&] { s->impl->select_local(P, lo, hi, t); TEMO_CUDA(cudaStreamSynchronize(s->impl->stream)); });
+int temo_b200_shard_open_peers(temo_b200_shard* s, const unsigned char* handles) {
+    return guarded_shard([&] {
+        require(s && s->impl && handles, "shard_open_peers: null argument");
+        s->impl->open_peers(handles);
+    });
 }
-int temo_b200_shard_select_rows(temo_b200_shard* s, uint64_t lo, uint64_t hi) {
-    return guarded_shard([&] { s->impl->select_rows(lo, hi); TEMO_CUDA(cudaStreamSynchronize(s->impl->stream)); });
+int temo_b200_shard_set_peer_pointers(temo_b200_shard* s, void* const* pools) {
+    return guarded_shard([&] {
+        require(s && s->impl && pools, "shard_set_peer_pointers: null argument");
+        s->impl->set_peers_direct(pools);
+    });
 }
-int temo_b200_shard_select_finish(temo_b200_shard* s, uint32_t* elite, uint64_t* count) {
-    return guarded_shard([&] { *count = s->impl->select_finish(elite); });
+
+int temo_b200_shard_begin(temo_b200_shard* s) {
+    return guarded_shard([&] { s->impl->begin(); });
 }
-int temo_b200_shard_commit(temo_b200_shard* s, uint64_t count, const uint32_t* own_slots, uint64_t own_count, uint64_t t) {
-    return guarded_shard([&] { s->impl->commit(count, own_slots, own_count, t); });
+int temo_b200_shard_reproduce(temo_b200_shard* s) {
+    return guarded_shard([&] { s->impl->reproduce(); });
 }
-// copies out this rank's rows: x of the given local slots (rows x d) and the replicated f / v / gamma
-int temo_b200_shard_download(temo_b200_shard* s, const uint32_t* slots, uint64_t rows, double* x, uint64_t f_rows,
+int temo_b200_shard_place_initial_f(temo_b200_shard* s) {
+    return guarded_shard([&] { s->impl->place_initial_f(); });
+}
+int temo_b200_shard_select_local(temo_b200_shard* s) {
+    return guarded_shard([&] { s->impl->select_local(); });
+}
+int temo_b200_shard_select_rows(temo_b200_shard* s) {
+    return guarded_shard([&] { s->impl->select_rows(); });
+}
+int temo_b200_shard_finish(temo_b200_shard* s, uint64_t* count) {
+    return guarded_shard([&] {
+        require(count != nullptr, "shard_finish: null argument");
+        *count = s->impl->finish();
+    });
+}
+
+// Copies out the replicated state and this rank's rows: owner / slot tables (P entries each), x of the survivors this
+// rank owns (in survivor order, own_rows x d; own_index receives their survivor indices), f (P x m), v, gamma. Any may be NULL.
+int temo_b200_shard_download(temo_b200_shard* s, uint32_t* owner, uint32_t* slot, uint64_t* own_rows, uint64_t* own_index, double* x,
                              double* f, double* v, double* gamma) {
     return guarded_shard([&] {
         Shard& S = *s->impl;
-        if (x && rows) {
-            double* tmp = dev_alloc<double>(rows * S.d);
-            uint32_t* ds = dev_alloc<uint32_t>(rows);
-            TEMO_CUDA(cudaMemcpy(ds, slots, rows * sizeof(uint32_t), cudaMemcpyHostToDevice));
-            gather_slots_kernel<<<(unsigned)rows, 256, 0, S.stream>>>(S.pool, ds, rows, S.d, tmp);
-            const cudaError_t e = cudaMemcpyAsync(x, tmp, rows * S.d * sizeof(double), cudaMemcpyDeviceToHost, S.stream);
+        TEMO_CUDA(cudaStreamSynchronize(S.stream));
+        std::vector<uint32_t> o(S.P), sl(S.P);
+        TEMO_CUDA(cudaMemcpy(o.data(), S.owner[S.tcur], S.P * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+        TEMO_CUDA(cudaMemcpy(sl.data(), S.slot[S.tcur], S.P * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+        if (owner) std::memcpy(owner, o.data(), S.P * sizeof(uint32_t));
+        if (slot) std::memcpy(slot, sl.data(), S.P * sizeof(uint32_t));
+        std::vector<uint32_t> mine;
+        std::vector<uint64_t> idx;
+        for (uint64_t k = 0; k < S.P; ++k)
+            if (o[k] == (uint32_t)S.rank) {
+                mine.push_back(sl[k]);
+                idx.push_back(k);
+            }
+        if (own_rows) *own_rows = mine.size();
+        if (own_index) std::memcpy(own_index, idx.data(), idx.size() * sizeof(uint64_t));
+        if (x && !mine.empty()) {
+            double* tmp = dev_alloc<double>(mine.size() * S.d);
+            uint32_t* ds = dev_alloc<uint32_t>(mine.size());
+            TEMO_CUDA(cudaMemcpy(ds, mine.data(), mine.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+            gather_slots_kernel<<<(unsigned)mine.size(), 256, 0, S.stream>>>(S.pool, ds, mine.size(), S.d, tmp);
+            const cudaError_t e = cudaMemcpyAsync(x, tmp, mine.size() * S.d * sizeof(double), cudaMemcpyDeviceToHost, S.stream);
             cudaStreamSynchronize(S.stream);
             cudaFree(tmp);
             cudaFree(ds);
             TEMO_CUDA(e);
         }
-        if (f && f_rows) TEMO_CUDA(cudaMemcpy(f, S.fm[S.cur], f_rows * S.m * sizeof(double), cudaMemcpyDeviceToHost));
+        if (f && S.P) TEMO_CUDA(cudaMemcpy(f, S.fm[S.cur], S.P * S.m * sizeof(double), cudaMemcpyDeviceToHost));
         if (v) TEMO_CUDA(cudaMemcpy(v, S.v, S.r * S.m * sizeof(double), cudaMemcpyDeviceToHost));
         if (gamma) TEMO_CUDA(cudaMemcpy(gamma, S.gamma, S.r * sizeof(double), cudaMemcpyDeviceToHost));
     });

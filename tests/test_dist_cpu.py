@@ -1,8 +1,8 @@
-"""CPU, world_size 2 (gloo): the multi-GPU host orchestration (paper_2404_01159_b200.dist.ShardedRvea with
-TorchComm) — exchange planning (C ABI temo_b200_shard_plan), parent all-to-all, objective / free-slot
-all-gathers, packed min-allreduces, survivor table updates — driven end to end with a CPU stand-in for the
-per-rank stage functions (the oracle does the arithmetic here; on the GPU it is GpuShard). The sharded run
-must reproduce the single-process oracle run bit for bit: same survivor sets, same X, same F, every generation.
+"""CPU, world_size 2 and 4 (gloo): the multi-GPU host orchestration (paper_2404_01159_b200.dist.ShardedRvea with
+TorchComm) — stage order, objective / free-slot all-gathers, packed min-allreduces — driven end to end with a CPU
+stand-in for the per-rank stage functions (the oracle does the arithmetic here; on the GPU it is GpuShard, whose
+N > 1 device logic is covered on one GPU by tests/test_gpu_parity.py::test_sharded_world_n_on_one_gpu_*). The sharded
+run must reproduce the single-process oracle run bit for bit: same survivor sets, same X, same F, every generation.
 """
 import os
 import sys
@@ -24,12 +24,13 @@ def order_key(x):
 
 
 class CpuShard:
-    """Stand-in for GpuShard: same methods and buffers (CPU tensors), arithmetic by the oracle."""
+    """Stand-in for GpuShard: same stage functions and buffers (CPU tensors), arithmetic by the oracle. The peers'
+    pools are not mapped but fetched (an all-gather of the small test pools inside reproduce), which is what the NVLink
+    peer loads of K1 amount to; tables, counters and the generation live in the shard as in csrc/shard.cu."""
 
     def __init__(self, cfg, rank, world, oracle):
-        import ctypes as C
         from oracle.pyoracle import _p, u64
-        self.C, self._p, self.u64 = C, _p, u64
+        self._p, self.u64 = _p, u64
         self.o, self.cfg, self.rank, self.world = oracle, cfg, rank, world
         self.n, self.d, self.m = cfg.pop, cfg.dim, cfg.obj
         H = cfg.lattice_h or oracle.lattice_density_for(self.m, self.n)
@@ -40,17 +41,14 @@ class CpuShard:
         self.h_loc = self.n_loc // 2
         self.pcap = max(self.n, self.r)
         self.cap_loc = self.pcap + self.n_loc
-        self.send_cap = self.n
         self.adapt_every = max(1, int(np.ceil(cfg.fr * cfg.generations)))
-        self.lo, self.hi = oracle.problem_bounds(cfg.problem, self.d, self.m)
-        self.pool = np.zeros((self.cap_loc, self.d))
+        self.lo_b, self.hi_b = oracle.problem_bounds(cfg.problem, self.d, self.m)
+        self.pool = torch.zeros(self.cap_loc, self.d, dtype=torch.float64)
         rows0 = self.n_loc
-        x, _ = oracle.random_reproduce(rows0, self.d, cfg.seed, rank * rows0 * self.d, self.lo, self.hi)
-        self.pool[:rows0] = x
+        x, _ = oracle.random_reproduce(rows0, self.d, cfg.seed, rank * rows0 * self.d, self.lo_b, self.hi_b)
+        self.pool[:rows0] = torch.from_numpy(x)
         self.used = np.zeros(self.cap_loc, dtype=bool)
         self.used[:rows0] = True
-        self.send_buf = torch.zeros(self.send_cap, self.d, dtype=torch.float64)
-        self.recv_buf = torch.zeros(self.n_loc, self.d, dtype=torch.float64)
         self.f_off_loc = torch.from_numpy(oracle.evaluate(cfg.problem, x, self.m).copy())
         self.f_gather = torch.zeros(world * self.n_loc, self.m, dtype=torch.float64)
         self.best_key = torch.zeros(self.r, dtype=torch.int64)
@@ -60,9 +58,17 @@ class CpuShard:
         self.free_all = torch.zeros(world * self.n_loc, dtype=torch.int32)
         self.fm = np.zeros((self.pcap + self.n, self.m))
         self.ga = np.array([cfg.ga.pc, cfg.ga.eta, cfg.ga.pm, cfg.ga.xi])
+        rows = np.arange(self.n)
+        self.owner = (rows // self.n_loc).astype(np.int64)   # replicated survivor tables
+        self.slot = (rows % self.n_loc).astype(np.int64)
+        self.P, self.counter, self.t = self.n, self.n * self.d, 0
+        self.comm = None
 
     def _free_list(self):
         return np.nonzero(~self.used)[0][: self.n_loc].astype(np.int32)
+
+    def state(self):
+        return dict(P=self.P, counter=self.counter, t=self.t, lo=getattr(self, "lo", 0), hi=getattr(self, "hi", 0))
 
     def sync(self):
         pass
@@ -71,40 +77,55 @@ class CpuShard:
         import contextlib
         return contextlib.nullcontext()
 
-    def pack(self, slots, row0=0):
-        self.send_buf[row0: row0 + len(slots)] = torch.from_numpy(self.pool[np.asarray(slots, dtype=np.int64)])
+    def connect_peers(self, comm):
+        self.comm = comm
 
-    def reproduce(self, recv_pos, c_sbx, c_pm, unit_begin=0, unit_count=0):
-        """Pairs [unit_begin, unit_begin + unit_count) of this rank (0: all), as GpuShard.reproduce."""
-        u0, cnt = unit_begin, (unit_count or self.h_loc - unit_begin)
-        recv_pos = np.asarray(recv_pos, dtype=np.int64)
-        buf = self.recv_buf.numpy()
-        pa = np.ascontiguousarray(buf[recv_pos[u0:u0 + cnt]])
-        pb = np.ascontiguousarray(buf[recv_pos[self.h_loc + u0: self.h_loc + u0 + cnt]])
+    def place_initial_f(self):
+        self.fm[: self.n] = self.f_gather.numpy()
+
+    def begin(self):
+        n, half, h_loc = self.n, self.n // 2, self.h_loc
+        pool_idx, c = self.o.parent_pool_indices(self.P, n, self.cfg.seed, self.counter)
+        perm, c = self.o.shuffle_indices(self.cfg.seed, c, n)
+        self.c_sbx, self.c_pm = c, c + 3 * half * self.d + half
+        self.c_end = self.c_pm + 2 * n * self.d
+        rows = np.array([self.rank * h_loc + j if j < h_loc else half + self.rank * h_loc + (j - h_loc) for j in range(2 * h_loc)])
+        k = pool_idx[perm[rows].astype(np.int64)].astype(np.int64)   # survivor index of every local mating row
+        self._parent = (self.owner[k], self.slot[k])
+        total = self.P + n
+        self.lo, self.hi = total * self.rank // self.world, total * (self.rank + 1) // self.world
+
+    def reproduce(self):
+        pools = torch.zeros(self.world * self.cap_loc, self.d, dtype=torch.float64)
+        self.comm.all_gather(pools, self.pool)   # the peers' pools (mapped, not copied, on the GPU)
+        self.comm.calls -= 1
+        pools = pools.numpy().reshape(self.world, self.cap_loc, self.d)
+        own, sl = self._parent
+        cnt = self.h_loc
+        pa = np.ascontiguousarray(pools[own[:cnt], sl[:cnt]])
+        pb = np.ascontiguousarray(pools[own[cnt:], sl[cnt:]])
         ca, cb = np.empty_like(pa), np.empty_like(pb)
         _p, u64 = self._p, self.u64
-        self.o.lib.to_reproduce_pairs(_p(pa), _p(pb), u64(cnt), u64(self.d), u64(self.rank * self.h_loc + u0), u64(self.n),
-                                      u64(self.cfg.seed), u64(c_sbx), u64(c_pm), _p(self.ga), _p(self.lo), _p(self.hi), _p(ca), _p(cb))
+        self.o.lib.to_reproduce_pairs(_p(pa), _p(pb), u64(cnt), u64(self.d), u64(self.rank * self.h_loc), u64(self.n),
+                                      u64(self.cfg.seed), u64(self.c_sbx), u64(self.c_pm), _p(self.ga), _p(self.lo_b), _p(self.hi_b),
+                                      _p(ca), _p(cb))
         free = self.free_slot.numpy().astype(np.int64)
         f_loc = self.f_off_loc.numpy()
-        for kids, first in ((ca, u0), (cb, self.h_loc + u0)):
-            self.pool[free[first:first + cnt]] = kids
+        pool = self.pool.numpy()
+        for kids, first in ((ca, 0), (cb, self.h_loc)):
+            pool[free[first:first + cnt]] = kids
             f_loc[first:first + cnt] = self.o.evaluate(self.cfg.problem, kids, self.m)
 
-    def place_f(self, P, initial):
+    def select_local(self):
+        P, lo, hi = self.P, self.lo, self.hi
         g = self.f_gather.numpy()
-        if initial:
-            self.fm[: self.n] = g
-            return
         half = self.n // 2
         for rk in range(self.world):
             blk = g[rk * self.n_loc:(rk + 1) * self.n_loc]
             self.fm[P + rk * self.h_loc: P + (rk + 1) * self.h_loc] = blk[: self.h_loc]
             self.fm[P + half + rk * self.h_loc: P + half + (rk + 1) * self.h_loc] = blk[self.h_loc:]
-
-    def select_local(self, P, lo, hi, t):
         rows = P + self.n
-        sel = self.o.rv_select(self.fm[:rows], self.v, self.gamma, t, self.cfg.generations, self.cfg.alpha)
+        sel = self.o.rv_select(self.fm[:rows], self.v, self.gamma, self.t, self.cfg.generations, self.cfg.alpha)
         self._assoc, self._apd = sel.assoc.astype(np.int64), sel.apd
         keys = np.full(self.r, np.iinfo(np.int64).max, dtype=np.int64)
         first = np.full(self.r, np.iinfo(np.int32).max, dtype=np.int32)
@@ -114,7 +135,8 @@ class CpuShard:
         self.best_key.copy_(torch.from_numpy(keys))
         self.first_row.copy_(torch.from_numpy(first))
 
-    def select_rows(self, lo, hi):
+    def select_rows(self):
+        lo, hi = self.lo, self.hi
         keys = self.best_key.numpy()
         k = (order_key(self._apd[lo:hi]) ^ KEY_FLIP).view(np.int64)
         hit = k == keys[self._assoc[lo:hi]]
@@ -123,31 +145,37 @@ class CpuShard:
         np.minimum.at(best, self._assoc[lo:hi][hit], rows[hit])
         self.best_row.copy_(torch.from_numpy(best))
 
-    def select_finish(self):
+    def finish(self):
+        from paper_2404_01159_b200.dist import child_location
         first = self.first_row.numpy().view(np.uint32) ^ np.uint32(0x80000000)
         best = self.best_row.numpy().view(np.uint32) ^ np.uint32(0x80000000)
         valid = first != np.uint32(0xffffffff)
-        self._elite = best[valid].astype(np.uint32)
-        return self._elite.copy()
-
-    def commit(self, count, own_slots, t):
-        self.fm[:count] = self.fm[self._elite.astype(np.int64)]
+        elite = best[valid].astype(np.int64)
+        self.last_elite = elite.copy()
+        count, P, n = len(elite), self.P, self.n
+        # survivor k <- merged row elite[k]: a parent keeps its (owner, slot); a child lives where it was born
+        free_all = self.free_all.numpy().astype(np.int64)
+        par = elite < P
+        own, sl = np.empty(count, np.int64), np.empty(count, np.int64)
+        own[par], sl[par] = self.owner[elite[par]], self.slot[elite[par]]
+        rk, j = child_location(elite[~par] - P, n, self.world)
+        own[~par], sl[~par] = rk, free_all[rk.astype(np.int64) * self.n_loc + j]
+        self.owner, self.slot = own, sl
+        self.fm[:count] = self.fm[elite]
         self.used[:] = False
-        self.used[np.asarray(own_slots, dtype=np.int64)] = True
-        self.free_slot = torch.from_numpy(self._free_list())
-        if (t + 1) % self.adapt_every == 0:
+        self.used[sl[own == self.rank]] = True
+        self.free_slot.copy_(torch.from_numpy(self._free_list()))
+        if (self.t + 1) % self.adapt_every == 0:
             f = self.fm[:count]
             self.v, self.gamma = self.o.adapt(self.v0, self.v, self.gamma, f.min(axis=0), f.max(axis=0))
+        self.P, self.counter, self.t = count, self.c_end, self.t + 1
+        return count
 
-    def free_slots_host(self):
-        return self.free_all.numpy()
 
-
-def _worker(rank, world, port, problem, n, d, m, gens, seed, out_dir, chunks):
+def _worker(rank, world, port, problem, n, d, m, gens, seed, out_dir):
     sys.path.insert(0, ROOT)
     sys.path.insert(0, os.path.join(ROOT, "tests"))
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
-                      TEMO_B200_EXCHANGE_CHUNKS=str(chunks))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from oracle.pyoracle import Oracle
@@ -156,28 +184,29 @@ def _worker(rank, world, port, problem, n, d, m, gens, seed, out_dir, chunks):
         oracle = Oracle()
         cfg = tb.RunConfig(problem=problem, pop=n, dim=d, obj=m, generations=gens, seed=seed)
         shard = CpuShard(cfg, rank, world, oracle)
-        run = ShardedRvea(cfg, TorchComm(), shard)
+        comm = TorchComm()
+        run = ShardedRvea(cfg, comm, shard)
         pops, elites = [], []
         for _ in range(gens):
             pops.append(run.step())
-            elites.append(run.last_elite.copy())
-        idx, slots = run.own_slots()
-        np.savez(os.path.join(out_dir, f"rank{rank}.npz"), pops=np.array(pops), idx=idx, x=shard.pool[slots.astype(np.int64)],
-                 f=shard.fm[: run.P], v=shard.v, gamma=shard.gamma, counter=np.array([run.counter]),
-                 elite_last=elites[-1], elite_first=elites[0])
+            elites.append(shard.last_elite.copy())
+        mine = shard.owner == rank
+        np.savez(os.path.join(out_dir, f"rank{rank}.npz"), pops=np.array(pops), idx=np.nonzero(mine)[0],
+                 x=shard.pool.numpy()[shard.slot[mine]], f=shard.fm[: run.P], v=shard.v, gamma=shard.gamma,
+                 counter=np.array([run.counter]), elite_last=elites[-1], elite_first=elites[0],
+                 collectives=np.array([comm.calls]))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("case", [("dtlz2", 24, 9, 3, 8, 7, 1), ("dtlz1", 40, 12, 3, 12, 3, 4), ("dtlz3", 16, 6, 2, 6, 11, 3),
-                                  ("dtlz2", 36, 7, 3, 6, 5, 9)])
-def test_sharded_orchestration_world2_matches_single_process(tmp_path, oracle, case):
-    """The last field is the number of pieces the parent exchange is cut into (pipelined with reproduction): one piece,
-    several, more pieces than some chunks have pairs."""
-    problem, n, d, m, gens, seed, chunks = case
-    world = 2
+@pytest.mark.parametrize("case", [("dtlz2", 24, 9, 3, 8, 7, 2), ("dtlz1", 40, 12, 3, 12, 3, 2), ("dtlz3", 16, 6, 2, 6, 11, 2),
+                                  ("dtlz2", 36, 7, 3, 6, 5, 2), ("dtlz2", 48, 10, 3, 6, 9, 4)])
+def test_sharded_orchestration_matches_single_process(tmp_path, oracle, case):
+    """World size 2 and 4 over gloo: the orchestration (stage order, the five collectives per generation, the packed
+    order-preserving keys of the min-allreduces) reproduces the single-process oracle run bit for bit."""
+    problem, n, d, m, gens, seed, world = case
     port = 29500 + (os.getpid() % 2000)
-    mp.spawn(_worker, args=(world, port, problem, n, d, m, gens, seed, str(tmp_path), chunks), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, port, problem, n, d, m, gens, seed, str(tmp_path)), nprocs=world, join=True)
     exp = oracle.rvea_run(problem, n, d, m, gens, seed=seed)
     parts = [np.load(os.path.join(tmp_path, f"rank{r}.npz")) for r in range(world)]
     for p in parts:  # replicated state is identical on every rank and equals the single-process run
@@ -185,6 +214,7 @@ def test_sharded_orchestration_world2_matches_single_process(tmp_path, oracle, c
         assert np.array_equal(p["f"], exp["f"])
         assert np.array_equal(p["v"], exp["v"]) and np.array_equal(p["gamma"], exp["gamma"])
         assert int(p["counter"][0]) == exp["counter"]
+        assert int(p["collectives"][0]) == 1 + 5 * gens  # init all-gather + two all-gathers and three min-allreduces per generation
     # the sharded X (each rank holds the survivors born there) reassembles to the single-process population
     x = np.empty_like(exp["x"])
     seen = np.zeros(len(x), dtype=bool)
@@ -194,77 +224,19 @@ def test_sharded_orchestration_world2_matches_single_process(tmp_path, oracle, c
     assert seen.all() and np.array_equal(x, exp["x"])
 
 
-def test_shard_plan_is_consistent_across_ranks(oracle):
-    """Every rank derives the same exchange from the replicated tables: what g sends to h is what h expects."""
-    from paper_2404_01159_b200.dist import shard_plan
-    n, d, world, P, seed, counter = 48, 5, 4, 37, 9, 1234
-    rng = np.random.default_rng(0)
-    owner = rng.integers(0, world, P).astype(np.int32)
-    slot = rng.integers(0, 1000, P).astype(np.uint32)
-    for chunks in (1, 2, 5):
-        _check_plans(oracle, [shard_plan(seed, counter, P, n, d, r, world, owner, slot, chunks) for r in range(world)],
-                     n, d, world, P, seed, counter, owner, slot, chunks)
-
-
-def _check_plans(oracle, plans, n, d, world, P, seed, counter, owner, slot, chunks):
-    pool_idx, c = oracle.parent_pool_indices(P, n, seed, counter)
-    perm, c = oracle.shuffle_indices(seed, c, n)
+def test_child_location_and_key_packing():
+    """Host helpers of the sharded path: where a child row lives, and the order-preserving packing the min-allreduces
+    rely on (signed int64 view of an APD key, signed int32 view of a row with 0xffffffff = none staying the maximum)."""
+    from paper_2404_01159_b200.dist import child_location
+    n, world = 48, 4
     half, h_loc = n // 2, n // 2 // world
-    for h in range(world):
-        assert plans[h]["c_sbx"] == c and plans[h]["c_pm"] == c + 3 * half * d + half
-        assert plans[h]["c_end"] == plans[h]["c_pm"] + 2 * n * d
-        rows = [h * h_loc + j if j < h_loc else half + h * h_loc + (j - h_loc) for j in range(2 * h_loc)]
-        want = pool_idx[perm[rows].astype(np.int64)].astype(np.int64)  # survivor index of every local mating row
-        # rebuild the receive buffer of rank h from what every source says it sends, piece after piece
-        recv = []
-        per_chunk = -(-h_loc // chunks)
-        for ch in range(chunks):
-            first = len(recv)
-            for g in range(world):
-                sc = plans[g]["send_counts"].astype(np.int64)  # [chunks, world]
-                start = int(sc[:ch].sum() + sc[ch, :h].sum())
-                recv += [(g, int(s)) for s in plans[g]["send_slots"][start:start + int(sc[ch, h])]]
-                assert int(plans[h]["recv_counts"][ch, g]) == int(sc[ch, h])
-            # the parents of the pairs of piece ch are all inside piece ch
-            for j in range(2 * h_loc):
-                if (j % h_loc) // per_chunk == ch:
-                    assert first <= int(plans[h]["recv_pos"][j]) < len(recv)
-        for j, k in enumerate(want):
-            assert recv[int(plans[h]["recv_pos"][j])] == (int(owner[k]), int(slot[k]))
-
-
-def test_shard_plan_and_tables_large_threaded(oracle):
-    """Sizes at which the host bookkeeping runs multi-threaded (one thread per destination / per survivor range):
-    same consistency properties, and the table update equals a straightforward numpy transcription."""
-    import ctypes as C
-    from paper_2404_01159_b200 import _lib
-    from paper_2404_01159_b200.dist import shard_plan, child_location
-    n, d, world, P, seed, counter = 4 * 8192, 3, 4, 30011, 5, 77
-    rng = np.random.default_rng(1)
-    owner = rng.integers(0, world, P).astype(np.int32)
-    slot = rng.integers(0, 50000, P).astype(np.uint32)
-    for chunks in (1, 4):
-        _check_plans(oracle, [shard_plan(seed, counter, P, n, d, r, world, owner, slot, chunks) for r in range(world)],
-                     n, d, world, P, seed, counter, owner, slot, chunks)
-    # survivor tables after a selection that keeps `count` rows of the merged population
-    n, world, P, count, rank = 1 << 17, 4, 100000, 90000, 2
-    n_loc = n // world
-    owner = rng.integers(0, world, max(P, count)).astype(np.int32)
-    slot = rng.integers(0, 1 << 20, max(P, count)).astype(np.uint32)
-    elite = np.sort(rng.choice(P + n, count, replace=False)).astype(np.uint32)
-    free_all = rng.integers(0, 1 << 20, world * n_loc).astype(np.uint32)
-    exp_owner, exp_slot = np.empty(count, np.int32), np.empty(count, np.uint32)
-    par = elite < P
-    exp_owner[par], exp_slot[par] = owner[elite[par]], slot[elite[par]]
-    rk, j = child_location(elite[~par].astype(np.int64) - P, n, world)
-    exp_owner[~par], exp_slot[~par] = rk, free_all[rk.astype(np.int64) * n_loc + j]
-    o, sl = owner.copy(), slot.copy()
-    own = np.empty(count, dtype=np.uint32)
-    own_count = C.c_uint64(0)
-    u32p, i32p = C.POINTER(C.c_uint32), C.POINTER(C.c_int32)
-    rc = _lib.load().temo_b200_shard_update_tables(elite.ctypes.data_as(u32p), C.c_uint64(count), C.c_uint64(P), C.c_uint64(n), rank, world,
-                                                   free_all.ctypes.data_as(u32p), o.ctypes.data_as(i32p), sl.ctypes.data_as(u32p),
-                                                   own.ctypes.data_as(u32p), C.byref(own_count))
-    assert rc == 0
-    assert np.array_equal(o[:count], exp_owner) and np.array_equal(sl[:count], exp_slot)
-    assert np.array_equal(own[: own_count.value], exp_slot[exp_owner == rank])
+    rk, j = child_location(np.arange(n), n, world)
+    for i in range(n):
+        p = i if i < half else i - half
+        assert rk[i] == p // h_loc and j[i] == (p % h_loc if i < half else h_loc + p % h_loc)
+    x = np.array([0.0, 1e-300, 1.0, 2.5, 1e300, np.inf])
+    k = (order_key(x) ^ KEY_FLIP).view(np.int64)
+    assert np.all(np.diff(k) > 0)
+    rows = np.array([0, 1, 77, 0x7fffffff, 0xfffffffe, 0xffffffff], dtype=np.uint32)
+    sr = (rows ^ np.uint32(0x80000000)).view(np.int32)
+    assert np.all(np.diff(sr.astype(np.int64)) > 0)

@@ -1087,12 +1087,23 @@ def test_reference_suites_through_the_cpp_shim(tb):
     assert "SHIM PARITY OK" in res.stdout
 
 
+def _assemble_sharded(parts, P, d):
+    """The population of a sharded run from the ranks' pieces (every survivor lives on exactly one rank)."""
+    x = np.empty((P, d))
+    seen = np.zeros(P, dtype=bool)
+    for p in parts:
+        assert not seen[p["idx"]].any()
+        x[p["idx"]] = p["x"]
+        seen[p["idx"]] = True
+    assert seen.all()
+    return x
+
+
 @pytest.mark.parametrize("case", [("dtlz2", 512, 300, 3, 12), ("dtlz1", 256, 64, 3, 10), ("lsmop1", 128, 200, 3, 6)])
 def test_sharded_stage_path_equals_single_gpu_run(tb, case):
     """The multi-GPU stage functions (GpuShard, C ABI temo_b200_shard_*) driven by the same orchestration as on
     N GPUs, here with world size 1: must equal the monolithic device-resident run bit for bit (X, F, V, gamma,
-    survivor sets, draw counter). Together with tests/test_dist_cpu.py (world size 2, collectives over gloo)
-    this covers the N>1 path without N GPUs."""
+    survivor counts, draw counter)."""
     from paper_2404_01159_b200.dist import GpuShard, LocalComm, ShardedRvea
     problem, n, d, m, gens = case
     cfg = tb.RunConfig(problem=problem, pop=n, dim=d, obj=m, generations=gens, seed=21)
@@ -1102,16 +1113,66 @@ def test_sharded_stage_path_equals_single_gpu_run(tb, case):
         with tb.RveaRun(cfg) as run:
             for t in range(gens):
                 assert sharded.step() == run.step(), t
-                assert np.array_equal(sharded.last_elite, run.last_generation()["elite"]), t
                 assert sharded.counter == run.state()["counter"]
             mono = run.download()
-        idx, slots = sharded.own_slots()
-        x, f, v, gamma = shard.download(slots, sharded.P)
-        assert np.array_equal(idx, np.arange(sharded.P))
-        assert np.array_equal(x, mono["x"]) and np.array_equal(f, mono["f"])
-        assert np.array_equal(v, mono["v"]) and np.array_equal(gamma, mono["gamma"])
+        out = shard.download()
+        assert np.array_equal(out["idx"], np.arange(out["P"]))
+        assert np.array_equal(out["x"], mono["x"]) and np.array_equal(out["f"], mono["f"])
+        assert np.array_equal(out["v"], mono["v"]) and np.array_equal(out["gamma"], mono["gamma"])
+        assert shard.launches() > 0
     finally:
         shard.close()
+
+
+@pytest.mark.parametrize("case", [("dtlz2", 512, 300, 3, 12, 2), ("dtlz1", 256, 64, 3, 10, 4), ("dtlz2", 2048, 640, 3, 6, 2),
+                                  ("lsmop1", 128, 200, 3, 6, 2), ("dtlz3", 1024, 100, 10, 5, 4)])
+def test_sharded_world_n_on_one_gpu_equals_single_gpu_run(tb, case):
+    """The N > 1 DEVICE logic on one GPU: `world` shards as threads of this process, each with its own pool, tables and
+    stage functions, their collectives combined in-process (ThreadComm), their pools addressed through the same peer
+    pointer table the IPC mapping fills on N GPUs. Parents are read out of the other shards' pools by K1 (pair kernel at
+    d = 640, generic kernel below), the survivor -> (owner, slot) tables and free lists evolve on the device. Must equal the
+    monolithic run bit for bit, every generation; every rank's replicated state must be identical."""
+    import threading
+    from paper_2404_01159_b200.dist import GpuShard, ShardedRvea, ThreadComm
+    problem, n, d, m, gens, world = case
+    cfg = tb.RunConfig(problem=problem, pop=n, dim=d, obj=m, generations=gens, seed=21)
+    with tb.RveaRun(cfg) as run:
+        pops = [run.step() for _ in range(gens)]
+        mono = run.download()
+        counter = run.state()["counter"]
+    shared = ThreadComm.Shared(world)
+    results, errors = [None] * world, []
+
+    def rank_main(rank):
+        shard = None
+        try:
+            shard = GpuShard(cfg, rank, world, direct_peers=True)
+            sharded = ShardedRvea(cfg, ThreadComm(shared, rank), shard)
+            got = [sharded.step() for _ in range(gens)]
+            shared.barrier.wait()
+            results[rank] = (got, shard.download())
+            shared.barrier.wait()  # nobody frees a pool a peer may still read
+        except Exception as e:  # noqa: BLE001 - reported by the main thread
+            errors.append(e)
+            shared.barrier.abort()
+        finally:
+            if shard is not None:
+                shard.close()
+
+    threads = [threading.Thread(target=rank_main, args=(g,)) for g in range(world)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    assert not errors, errors
+    for got, out in results:
+        assert got == pops
+        assert out["counter"] == counter and out["P"] == pops[-1]
+        assert np.array_equal(out["f"], mono["f"]) and np.array_equal(out["v"], mono["v"]) and np.array_equal(out["gamma"], mono["gamma"])
+        assert np.array_equal(out["owner"], results[0][1]["owner"]) and np.array_equal(out["slot"], results[0][1]["slot"])
+    owners = results[0][1]["owner"]
+    assert len(np.unique(owners)) == world  # every rank holds part of the population
+    assert np.array_equal(_assemble_sharded([r[1] for r in results], pops[-1], d), mono["x"])
 
 
 def test_lockstep_c2_scale(tb, checkers):
