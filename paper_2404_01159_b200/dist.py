@@ -49,12 +49,26 @@ class TorchComm:
         self.world = dist.get_world_size()
         self.calls = 0
 
+    def _staged(self, t):
+        """gloo has no CUDA collectives: device tensors go through the host (tests on one GPU; NCCL takes them as they are)."""
+        return t.is_cuda and self.dist.get_backend() == "gloo"
+
     def all_gather(self, out, inp):
         self.calls += 1
+        if self._staged(inp):
+            host = out.cpu()
+            self.dist.all_gather_into_tensor(host, inp.cpu())
+            out.copy_(host)
+            return
         self.dist.all_gather_into_tensor(out, inp)
 
     def all_reduce_min(self, t):
         self.calls += 1
+        if self._staged(t):
+            host = t.cpu()
+            self.dist.all_reduce(host, op=self.dist.ReduceOp.MIN)
+            t.copy_(host)
+            return
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MIN)
 
     def all_gather_bytes(self, payload) -> list:

@@ -12,6 +12,8 @@ Bars (BASELINE.json north_star / SURVEY.md §8d):
   * values that pass through cos/sin/acos (CUDA libm <= 2 ulp vs glibc < 1 ulp) or a tree
     reduction: objectives within 1e-12 relative, APD within 1e-9 (verify.hpp:53), gamma <= 2 ulp.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -1173,6 +1175,58 @@ def test_sharded_world_n_on_one_gpu_equals_single_gpu_run(tb, case):
     owners = results[0][1]["owner"]
     assert len(np.unique(owners)) == world  # every rank holds part of the population
     assert np.array_equal(_assemble_sharded([r[1] for r in results], pops[-1], d), mono["x"])
+
+
+def _ipc_rank_main(rank, world, port, case, out_dir):
+    import os
+    import sys
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2404_01159_b200 as tb
+        from paper_2404_01159_b200.dist import GpuShard, ShardedRvea, TorchComm
+        torch.cuda.set_device(0)
+        tb.init(0)
+        problem, n, d, m, gens = case
+        cfg = tb.RunConfig(problem=problem, pop=n, dim=d, obj=m, generations=gens, seed=21)
+        shard = GpuShard(cfg, rank, world)  # peers through cudaIpcGetMemHandle / cudaIpcOpenMemHandle
+        run = ShardedRvea(cfg, TorchComm(), shard)
+        pops = [run.step() for _ in range(gens)]
+        out = shard.download()
+        np.savez(os.path.join(out_dir, f"rank{rank}.npz"), pops=np.array(pops), idx=out["idx"], x=out["x"], f=out["f"], v=out["v"],
+                 gamma=out["gamma"], counter=np.array([out["counter"]]), owner=out["owner"])
+        dist.barrier()  # nobody unmaps / frees a pool a peer may still read
+        shard.close()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("case", [("dtlz2", 1024, 640, 3, 6), ("dtlz1", 256, 64, 3, 8)])
+def test_sharded_two_processes_ipc_on_one_gpu(tb, tmp_path, case):
+    """The real multi-process path on one GPU: two processes, each with its own CUDA context and GpuShard, map each other's
+    pools through CUDA IPC handles (exchanged with all_gather_object) and K1 reads the peer's rows through the mapping.
+    NCCL refuses two ranks on one device, so the small collectives run over gloo (staged through the host); everything
+    else is the N-GPU code. Bit-exact against the monolithic run."""
+    import torch.multiprocessing as mp
+    problem, n, d, m, gens = case
+    cfg = tb.RunConfig(problem=problem, pop=n, dim=d, obj=m, generations=gens, seed=21)
+    with tb.RveaRun(cfg) as run:
+        pops = [run.step() for _ in range(gens)]
+        mono = run.download()
+        counter = run.state()["counter"]
+    port = 31500 + (os.getpid() % 2000)
+    mp.spawn(_ipc_rank_main, args=(2, port, case, str(tmp_path)), nprocs=2, join=True)
+    parts = [np.load(os.path.join(tmp_path, f"rank{r}.npz")) for r in range(2)]
+    for p in parts:
+        assert list(p["pops"]) == pops and int(p["counter"][0]) == counter
+        assert np.array_equal(p["f"], mono["f"]) and np.array_equal(p["v"], mono["v"]) and np.array_equal(p["gamma"], mono["gamma"])
+    assert len(np.unique(parts[0]["owner"])) == 2
+    assert np.array_equal(_assemble_sharded(parts, pops[-1], d), mono["x"])
 
 
 def test_lockstep_c2_scale(tb, checkers):
