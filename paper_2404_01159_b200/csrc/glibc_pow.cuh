@@ -196,6 +196,9 @@ __host__ __device__ inline bool glibc_pow_main(double x, double y, const PowTabl
 // instruction streams interleave). Same operations, same bits; returns false when the result is not valid
 // (|y log x| >= 512: never for the SBX spread factor) and the caller must fall back to the general routine.
 // x must be positive and normal.
+// STRICT: the |y log x| < 2^-54 case is reported as not valid as well (the caller's general routine handles it), which
+// drops its add and select from the instruction stream.
+template <bool STRICT = false>
 __host__ __device__ __forceinline__ bool glibc_pow_narrow_flat(double x, double y, const PowTables& T, double* out) {
     const unsigned long long ix = TEMO_AS_U64(x);
     const unsigned long long tmp = ix - 0x3fe6955500000000ULL;
@@ -253,6 +256,10 @@ __host__ __device__ __forceinline__ bool glibc_pow_narrow_flat(double x, double 
     const double tmpv = TEMO_FMA(c45, r4, acc);
     const double scale = TEMO_AS_DOUBLE(sbits);
     const double res = TEMO_FMA(tmpv, scale, scale);
+    if (STRICT) {
+        *out = res;
+        return abstop - 0x3c9u <= 0x3eu;
+    }
     *out = tiny ? TEMO_ADD(ehi, 1.0) : res;
     return valid;
 }

@@ -365,7 +365,6 @@ struct WarpSmem {
     double beta[kTileGenes];
     unsigned short list[kTileGenes];
     double2 side[kPairCand];  // final children {a, b} of a candidate gene
-    PairCtx ctx;
     unsigned short cand[kPairCand];
 };
 struct PairSlot {
@@ -382,8 +381,10 @@ struct PairSmem {
     PowSmem pow;
     WarpSmem w[kVirtWarps];
     PairSlot slot[kPairSlots];
-    // dynamic pair hand-out: turn T of this team works on pair ring[T % kUnitRing]
+    // pair hand-out: turn T of this team works on pair ring[T % kUnitRing], described by ringctx[T % kUnitRing] (filled once
+    // per pair by the warp that fetched it)
     uint32_t ring[kUnitRing];
+    PairCtx ringctx[kUnitRing];
     uint32_t progress[kVirtWarps];  // turns every warp has finished
     uint32_t claiming, published;   // highest turn being fetched / already published
 };
@@ -548,12 +549,38 @@ __device__ __forceinline__ void accumulate_vector(uint32_t j0, uint32_t m1, doub
     }
 }
 
+// Pass B of a tile with the general pow (base 0, or an exponent outside the narrow path's range): same list, same stores.
+template <int MODE>
+__device__ __noinline__ void pass_b_general(const ReproK& a, uint64_t pos_tile, uint32_t total, uint32_t sm_w, uint32_t lane) {
+    constexpr uint64_t SG = MODE == 0 ? kGolden : 1ULL;
+    constexpr uint32_t kOffList = offsetof(WarpSmem, list);
+    for (uint32_t t = lane; t < total; t += 32) {
+        const uint32_t e = lds_u16(sm_w + kOffList + 2 * t);
+        const uint32_t j = e + (e >> 6) * (kVirtWarps * 64 - 64);
+        const SpreadIn s = spread_inputs<MODE>(a.rng.seed, pos_tile + (uint64_t)j * SG, a.dl_r1, a.inv_exp);
+        const double p = pow_spread_slow(s.base, s.yexp);
+        sts_f64(sm_w + 8 * e, s.up ? p : -p);
+    }
+}
+
+// Everything the warps of a team need to know about pair `unit`: computed once per pair by the warp that fetched it.
+template <int MODE>
+__device__ __forceinline__ void fill_pair_ctx(PairCtx& c, const ReproK& a, uint64_t unit) {
+    const uint64_t row_a = unit, row_b = a.half + unit, g_unit = a.g_unit0 + unit;
+    c.pa = a.src_ptr ? a.src_ptr[row_a] : a.pool + (a.src ? (uint64_t)a.src[row_a] : row_a) * a.d;
+    c.pb = a.src_ptr ? a.src_ptr[row_b] : a.pool + (a.src ? (uint64_t)a.src[row_b] : row_b) * a.d;
+    c.oa = a.out + (a.dst ? (uint64_t)a.dst[row_a] : row_a) * a.d;
+    c.ob = a.out + (a.dst ? (uint64_t)a.dst[row_b] : row_b) * a.d;
+    c.pos = a.s_base + g_unit * a.s_row;
+    c.cross = !(word_to_unit(draw_word<MODE>(a.rng, a.c_r3 + g_unit)) - a.pc >= 0.0) ? 1u : 0u;  // operators.hpp:82
+}
+
 // The literal per-gene formulation of one warp tile (blocks v + 8k of the row tile starting at blk0): used when
 // the candidate slots of the phased passes overflow. Same bits, same accumulation order.
 template <int MODE, int EVAL>
-__device__ __noinline__ void tile_plain(const ReproK& a, uint32_t blk0, uint32_t v, uint32_t kmax, double* acc, WarpSmem& W,
+__device__ __noinline__ void tile_plain(const ReproK& a, uint32_t blk0, uint32_t v, uint32_t kmax, double* acc, const PairCtx* ctx,
                                         double (*pos)[kMaxObj]) {
-    const PairCtx c = W.ctx;
+    const PairCtx c = *ctx;
     constexpr uint64_t SG = MODE == 0 ? kGolden : 1ULL;
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t nvec = (uint32_t)(a.d >> 1), m1 = (uint32_t)a.m - 1;
@@ -601,14 +628,18 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
         S.slot[threadIdx.x].done = 0;
     }
     if (threadIdx.x < kVirtWarps) S.progress[threadIdx.x] = 0;
-    if (threadIdx.x == 0) S.claiming = S.published = 0;
+    if (threadIdx.x == 0) {
+        S.claiming = S.published = 0;
+        if (a.unit0 + blockIdx.x < a.unit_end) fill_pair_ctx<MODE>(S.ringctx[0], a, a.unit0 + blockIdx.x);  // the team's first pair
+    }
     __syncthreads();  // the only CTA barrier: from here on every warp is on its own
     const PowTables T = pow_tables(S.pow);
 
     const uint64_t seed = a.rng.seed;
     const uint32_t nvec = (uint32_t)(a.d >> 1);
     const uint32_t nblk = (nvec + 31) >> 5;  // 64-gene blocks in a row
-    const uint32_t lt = opaque((1u << lane) - 1u);
+    uint32_t lt;  // lanes below this one (kept in a register: an asm volatile result cannot be rematerialised in the loops)
+    asm volatile("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
     const uint32_t top_thr = a.mask_never ? 0u : ((a.mask_top << 11) | 0x7ffu);  // (top >> 11) <= mask_top
     const uint32_t sm_w = opaque(smem_u32(&W)), sm_lane = opaque(smem_u32(&W) + lane * 16);  // beta tile is first in WarpSmem
 
@@ -620,20 +651,10 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
     // than kUnitRing turns apart).
     for (uint64_t unit = a.unit0 + blockIdx.x; unit < a.unit_end; ++turn) {
         PairSlot& slot = S.slot[turn % kPairSlots];
-        if (lane == 0) {
-            const uint64_t row_a = unit, row_b = a.half + unit, g_unit = a.g_unit0 + unit;
-            W.ctx.pa = a.src_ptr ? a.src_ptr[row_a] : a.pool + (a.src ? (uint64_t)a.src[row_a] : row_a) * a.d;
-            W.ctx.pb = a.src_ptr ? a.src_ptr[row_b] : a.pool + (a.src ? (uint64_t)a.src[row_b] : row_b) * a.d;
-            W.ctx.oa = a.out + (a.dst ? (uint64_t)a.dst[row_a] : row_a) * a.d;
-            W.ctx.ob = a.out + (a.dst ? (uint64_t)a.dst[row_b] : row_b) * a.d;
-            W.ctx.pos = a.s_base + g_unit * a.s_row;
-            W.ctx.cross = !(word_to_unit(draw_word<MODE>(a.rng, a.c_r3 + g_unit)) - a.pc >= 0.0) ? 1u : 0u;
-            // the slot is free once the pair that used it kPairSlots turns ago has been written out
-            if (EVAL != 0) {
-                while (*reinterpret_cast<volatile uint32_t*>(&slot.done) < turn / kPairSlots) __nanosleep(TEMO_PAIR_SLEEP);
-            }
-        }
-        __syncwarp();
+        const PairCtx& C = S.ringctx[turn % kUnitRing];
+        if (EVAL != 0 && lane == 0)  // the slot is free once the pair that used it kPairSlots turns ago has been written out
+            while (*reinterpret_cast<volatile uint32_t*>(&slot.done) < turn / kPairSlots) __nanosleep(TEMO_PAIR_SLEEP);
+        __syncwarp();  // also orders the reads of the pair's context behind lane 0's look at the hand-out ring
 
         double acc_a = 0.0, acc_b = 0.0;
         for (uint32_t blk0 = 0; blk0 < nblk; blk0 += kVirtWarps * kPairBlocks) {
@@ -642,11 +663,11 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
             const uint32_t kmax = opaque(min(left, (uint32_t)kPairBlocks));
             if (kmax == 0) break;
             const uint32_t q_first = (blk0 + v) * 32 + lane;  // this lane's vector in the tile's first block
-            const uint64_t pos = W.ctx.pos;
+            const uint64_t pos = C.pos;
             {   // this warp's parent blocks of this tile into L2 (they are read in pass C)
                 const uint32_t kk = lane & 15, blk = blk0 + v + kk * kVirtWarps;
                 if (kk < kmax && blk < nblk) {
-                    const char* p = reinterpret_cast<const char*>(lane < 16 ? W.ctx.pa : W.ctx.pb) + (uint64_t)blk * 512;
+                    const char* p = reinterpret_cast<const char*>(lane < 16 ? C.pa : C.pb) + (uint64_t)blk * 512;
 #pragma unroll
                     for (int o = 0; o < 512; o += 128) prefetch_l2(p + o);
                 }
@@ -654,7 +675,7 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
             // ---- pass A: crossing genes and mutation candidates (hashes only)
             uint32_t total = 0, ncand = 0;
             {
-                const bool cross = W.ctx.cross != 0;
+                const bool cross = C.cross != 0;
                 const uint64_t first = pos + (uint64_t)(2 * q_first) * SG;
                 uint64_t p_r2 = first + a.dl_r2, p_ma = first + a.dl_mask_a, p_mb = first + a.dl_mask_b;
                 uint32_t q = q_first, e = lane * 2, sm_b = sm_lane;
@@ -691,32 +712,43 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
             __syncwarp();
             if (ncand > (uint32_t)a.cand_cap) {  // practically never: the literal formulation of this tile
                 double acc[2] = {acc_a, acc_b};
-                tile_plain<MODE, EVAL>(a, blk0, v, kmax, acc, W, slot.pos);
+                tile_plain<MODE, EVAL>(a, blk0, v, kmax, acc, &C, slot.pos);
                 acc_a = acc[0], acc_b = acc[1];
                 __syncwarp();
                 continue;
             }
-            // ---- pass B: signed spread factor of the crossing genes, 32 at a time
+            // ---- pass B: signed spread factor of the crossing genes, 64 at a time
             {
                 const uint64_t pos_tile = pos + (uint64_t)((blk0 + v) * 64) * SG;  // gene (blk0 + v) * 64
+                // Anything off the common path (a base of exactly 0, a result within 2^-54 of 1, an exponent outside the narrow
+                // range) only raises `redo`: the general routine then recomputes the tile's list after the loop, so the loop
+                // itself carries no call, no fallback selects and no per-iteration look at the launch constants.
+                bool redo = !a.narrow_pow;
+                const uint32_t inv_hi = (uint32_t)__double2hiint(a.inv_exp), inv_lo = (uint32_t)__double2loint(a.inv_exp);
                 for (uint32_t t = lane; t < total; t += 64) {  // two genes per lane: their pow chains interleave
                     const bool two = t + 32 < total;
                     const uint32_t e0 = lds_u16(sm_w + kOffList + 2 * t), e1 = two ? lds_u16(sm_w + kOffList + 2 * t + 64) : e0;
                     // gene index relative to the tile's first gene
                     const uint32_t j0 = e0 + (e0 >> 6) * (kVirtWarps * 64 - 64), j1 = e1 + (e1 >> 6) * (kVirtWarps * 64 - 64);
-                    const SpreadIn s0 = spread_inputs<MODE>(seed, pos_tile + (uint64_t)j0 * SG, a.dl_r1, a.inv_exp);
-                    const SpreadIn s1 = spread_inputs<MODE>(seed, pos_tile + (uint64_t)j1 * SG, a.dl_r1, a.inv_exp);
-                    const bool f0 = s0.base > 0.0 && a.narrow_pow, f1 = s1.base > 0.0 && a.narrow_pow;
+                    const uint64_t at0 = pos_tile + (uint64_t)j0 * SG, at1 = pos_tile + (uint64_t)j1 * SG;
+                    const double mc0 = word_to_unit(draw_full<MODE>(seed, at0)), mc1 = word_to_unit(draw_full<MODE>(seed, at1));
+                    const uint32_t r10 = draw_top<MODE>(seed, at0 + a.dl_r1), r11 = draw_top<MODE>(seed, at1 + a.dl_r1);
+                    // live spread branch only (hm = H(0.5 - mc)): base 2 mc with exponent 1 / (eta + 1), or 2 - 2 mc with its negative
+                    const bool low0 = 0.5 - mc0 >= 0.0, low1 = 0.5 - mc1 >= 0.0;
+                    const double b0 = low0 ? 2.0 * mc0 : 2.0 - 2.0 * mc0, b1 = low1 ? 2.0 * mc1 : 2.0 - 2.0 * mc1;
+                    const double y0 = __hiloint2double((int)(inv_hi ^ (low0 ? 0u : 0x80000000u)), (int)inv_lo);
+                    const double y1 = __hiloint2double((int)(inv_hi ^ (low1 ? 0u : 0x80000000u)), (int)inv_lo);
                     double p0, p1;
-                    const bool ok0 = glibc_pow_narrow_flat(f0 ? s0.base : 1.0, s0.yexp, T, &p0) && f0;
-                    const bool ok1 = glibc_pow_narrow_flat(f1 ? s1.base : 1.0, s1.yexp, T, &p1) && f1;
-                    if (!(ok0 && ok1)) {  // never for ordinary eta
-                        if (!ok0) p0 = pow_spread_slow(s0.base, s0.yexp);
-                        if (!ok1) p1 = pow_spread_slow(s1.base, s1.yexp);
-                    }
-                    sts_f64(sm_w + 8 * e0, s0.up ? p0 : -p0);
-                    if (two) sts_f64(sm_w + 8 * e1, s1.up ? p1 : -p1);
+                    const bool ok0 = glibc_pow_narrow_flat<true>(b0, y0, T, &p0);
+                    const bool ok1 = glibc_pow_narrow_flat<true>(b1, y1, T, &p1);
+                    redo |= !(ok0 && ok1) || !(b0 > 0.0) || !(b1 > 0.0);
+                    // sgn(r1 - 0.5): the spread factor is positive, so its sign is planted from the draw's top bit
+                    const double q0 = __hiloint2double(__double2hiint(p0) ^ (int)(~r10 & 0x80000000u), __double2loint(p0));
+                    const double q1 = __hiloint2double(__double2hiint(p1) ^ (int)(~r11 & 0x80000000u), __double2loint(p1));
+                    sts_f64(sm_w + 8 * e0, q0);
+                    if (two) sts_f64(sm_w + 8 * e1, q1);
                 }
+                if (__any_sync(0xffffffffu, redo)) pass_b_general<MODE>(a, pos_tile, total, sm_w, lane);
             }
             __syncwarp();
             // ---- pass M: the mutation candidates of this tile (usually none)
@@ -727,7 +759,7 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
                 const uint64_t at = pos + (uint64_t)j * SG;
                 const double2 ch = mutated_children<MODE>(seed, at + a.dl_mask_a, at + a.dl_mask_b, a.dl_mut_a - a.dl_mask_a,
                                                           a.mask_thresh, a.xi, (entry & 0x2000u) != 0, (entry & 0x4000u) != 0,
-                                                          W.ctx.pa[j], W.ctx.pb[j], W.beta[e], a.lower[j], a.upper[j]);
+                                                          C.pa[j], C.pb[j], W.beta[e], a.lower[j], a.upper[j]);
                 W.side[t] = ch;
                 W.beta[e] = __hiloint2double((int)kBetaTagHi, (int)t);
             }
@@ -735,8 +767,8 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
             // ---- pass C: stream the rows
             {
                 const uint32_t m1 = (uint32_t)a.m - 1;  // first tail gene (fused evaluation)
-                double2* __restrict__ oa2 = reinterpret_cast<double2*>(W.ctx.oa);
-                double2* __restrict__ ob2 = reinterpret_cast<double2*>(W.ctx.ob);
+                double2* __restrict__ oa2 = reinterpret_cast<double2*>(C.oa);
+                double2* __restrict__ ob2 = reinterpret_cast<double2*>(C.ob);
                 const double2* __restrict__ lo2 = reinterpret_cast<const double2*>(a.lower);
                 const double2* __restrict__ hi2 = reinterpret_cast<const double2*>(a.upper);
                 // piecewise-constant bounds from the launch constants (SEG): one side of the split for the whole tile,
@@ -744,8 +776,8 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
                 const uint32_t tile_g0 = (blk0 + v) * 64, tile_g1 = (blk0 + v + (kmax - 1) * kVirtWarps) * 64 + 64;
                 const bool seg_hi_side = tile_g0 >= a.seg_split, seg_mixed = SEG != 0 && !seg_hi_side && tile_g1 > a.seg_split;
                 const double seg_lo = a.seg_lo[seg_hi_side ? 1 : 0], seg_hi = a.seg_hi[seg_hi_side ? 1 : 0];
-                const double2* __restrict__ pa2 = reinterpret_cast<const double2*>(W.ctx.pa);
-                const double2* __restrict__ pb2 = reinterpret_cast<const double2*>(W.ctx.pb);
+                const double2* __restrict__ pa2 = reinterpret_cast<const double2*>(C.pa);
+                const double2* __restrict__ pb2 = reinterpret_cast<const double2*>(C.pb);
                 // Two register sets for the parents, used alternately by a loop unrolled by two: block k is blended out of
                 // set k & 1, and as soon as its children exist the same registers receive block k + 2 — two blocks are
                 // always in flight and no value is ever moved between registers (the rotating three-set form of the earlier
@@ -867,11 +899,7 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
             }
         }
         __syncwarp();
-        // ---- the team's next pair
-        if (a.work_counter == nullptr) {
-            unit += gridDim.x;
-            continue;
-        }
+        // ---- the team's next pair (round-robin over the grid without a work counter)
         uint32_t next = 0;
         if (lane == 0) {
             const uint32_t T = turn + 1;
@@ -885,7 +913,8 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
                     if (T >= (uint32_t)kUnitRing)                 // the ring entry is free once everybody has finished turn T - kUnitRing
                         for (int w = 0; w < kVirtWarps; ++w)
                             while (*reinterpret_cast<volatile uint32_t*>(&S.progress[w]) + kUnitRing <= T) __nanosleep(100);
-                    next = atomicAdd(a.work_counter, 1u);
+                    next = a.work_counter ? atomicAdd(a.work_counter, 1u) : (T - 1) * gridDim.x + blockIdx.x;
+                    if (a.unit0 + gridDim.x + next < a.unit_end) fill_pair_ctx<MODE>(S.ringctx[T % kUnitRing], a, a.unit0 + gridDim.x + next);
                     *reinterpret_cast<volatile uint32_t*>(&S.ring[T % kUnitRing]) = next;
                     __threadfence_block();
                     *reinterpret_cast<volatile uint32_t*>(&S.published) = T;

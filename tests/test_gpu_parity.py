@@ -178,10 +178,12 @@ def k1_options(tb):
 
 
 @pytest.mark.parametrize("shape", [(16, 512), (12, 5120), (6, 5122), (6, 10240), (5, 20000), (9, 2002)])
-@pytest.mark.parametrize("ga", [(1.0, 20.0, 1.0, 20.0), (0.6, 5.0, 3.0, 7.0)])
+@pytest.mark.parametrize("ga", [(1.0, 20.0, 1.0, 20.0), (0.6, 5.0, 3.0, 7.0), (1.0, 3000.0, 1.0, 20.0), (1.0, 0.0, 2.0, 0.5)])
 def test_pair_kernel_vs_oracle(tb, oracle, shape, ga):
     """Rows wide enough for the pair kernel (d even, >= 512): one and several row tiles, a partial last block, an odd
-    population (the last row goes through the generic kernel), pairs that do not cross (pc < 1), several mutations per row."""
+    population (the last row goes through the generic kernel), pairs that do not cross (pc < 1), several mutations per row,
+    an exponent 1 / (eta + 1) outside the narrow pow path (eta = 3000: every tile's spread factors are recomputed by the
+    general routine after the loop) and eta = 0 (exponent 1)."""
     n, d = shape
     lo, hi = np.zeros(d), np.ones(d)
     x, _ = oracle.random_reproduce(n, d, 23, 0, lo, hi)
