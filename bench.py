@@ -291,11 +291,12 @@ def run_ours(args):
     rank, world, local = dist_env()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         self_launch(args)  # does not return
-    if args.gpus != world and not (world == 1 and os.environ.get("TEMO_FORCE_DIST") == "1"):
+    force_dist = os.environ.get("TEMO_FORCE_DIST", "") in ("1", "nccl")  # the N-GPU path on one GPU (nccl: collectives through NCCL)
+    if args.gpus != world and not (world == 1 and force_dist):
         sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     import paper_2404_01159_b200 as tb
 
-    if world > 1 or os.environ.get("TEMO_FORCE_DIST") == "1":  # the env switch exercises the N-GPU path on one GPU
+    if world > 1 or force_dist:
         from paper_2404_01159_b200 import dist as tdist
         return tdist.bench_main(args, METRIC, workload_config, measured_peaks, ClockSampler)
 

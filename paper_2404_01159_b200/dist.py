@@ -371,7 +371,14 @@ def bench_main(args, metric, workload_config, measured_peaks, ClockSampler):
     rank, world, local = int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     tb.init(local)
-    if world > 1:
+    use_nccl = world > 1 or os.environ.get("TEMO_FORCE_DIST") == "nccl"  # "nccl": the collectives of a world of 1 through NCCL
+    if use_nccl:
+        if "MASTER_ADDR" not in os.environ:  # not under torchrun: a single-rank rendezvous on the loopback
+            import socket
+            with socket.socket() as sk:
+                sk.bind(("127.0.0.1", 0))
+                port = sk.getsockname()[1]
+            os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK="0", WORLD_SIZE="1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         comm = TorchComm()
     else:
@@ -439,5 +446,5 @@ def bench_main(args, metric, workload_config, measured_peaks, ClockSampler):
         }
         print(json.dumps(line), flush=True)
     shard.close()
-    if world > 1:
+    if use_nccl:
         dist.destroy_process_group()
