@@ -5,9 +5,9 @@
 // 4 - hidden - 2 tanh network (W1 row-major, b1, W2 row-major, b2); an episode runs `horizon` steps of the point-mass
 // dynamics with the network as policy and returns 2 or 3 cumulative rewards (maximisation orientation).
 //
-// Compute-bound and strictly sequential per individual (18 tanh per step, every step feeds the next): one thread per
-// individual walks the episode; the parameters of a CTA's individuals sit in shared memory, parameter-major, so a
-// warp's reads of "parameter k of my individual" are conflict-free. Every operation is the reference's, in its order
+// Compute-bound and strictly sequential per individual (18 tanh per step, every step feeds the next): sixteen lanes
+// share an individual (one hidden unit each, parameters in registers), two individuals per warp. Every operation is the
+// reference's, in its order
 // (--fmad=false keeps `s += w * x` a multiply and an add like -ffp-contract=off); tanh follows the host libm operation
 // for operation (glibc_tanh.cuh) and sin / cos of the phase come from a table the host libm fills once per horizon, so
 // the returns are bit-identical to env_rollout's.
@@ -39,55 +39,86 @@ struct ToyK {
     const double* obs;      // mlp_forward mode: n x 4 observations (nullptr: episodes)
 };
 
-// action = tanh(W2 tanh(W1 obs + b1) + b2) (problems.hpp:149-163); w(k) reads parameter k of this thread's individual
-template <class W>
-__device__ __forceinline__ void mlp_forward_dev(const W& w, uint32_t H, const double* obs, double* hid, double* act) {
-    const uint32_t o_b1 = H * kToyObs, o_w2 = o_b1 + H, o_b2 = o_w2 + kToyAct * H;
-    for (uint32_t i = 0; i < H; ++i) {
-        double s = w(o_b1 + i);
-        for (uint32_t j = 0; j < (uint32_t)kToyObs; ++j) s += w(i * kToyObs + j) * obs[j];
-        hid[i] = glibc_tanh(s);
-    }
-    for (uint32_t i = 0; i < (uint32_t)kToyAct; ++i) {
-        double s = w(o_b2 + i);
-        for (uint32_t j = 0; j < H; ++j) s += w(o_w2 + i * H + j) * hid[j];
-        act[i] = glibc_tanh(s);
-    }
-}
+// Sixteen lanes per individual (two individuals per warp): lane s owns the hidden units s, s + 16, ... (U = ceil(hidden / 16)
+// of them, their W1 rows, biases and W2 columns in registers). One step of the episode:
+//   hidden unit i:  s = b1[i]; s += W1(i, j) * obs[j] for j = 0..3; h_i = tanh(s)              (problems.hpp:151-156, all units at once)
+//   output o:       p_i = W2(o, i) * h_i goes to shared memory; even lanes then add b2[0] + p_0 + p_1 + ... in ascending i (the
+//                   reference's order, problems.hpp:157-162), odd lanes the same for output 1, and take its tanh
+//   state update:   every lane keeps (v, h, returns) redundantly (problems.hpp:196-201)
+// The thread-per-individual form of the first version is 4x leaner in instructions but cannot be kept busy: at the paper's
+// population of 10^4 it gives 68 threads per SM and every instruction waits out its full FP64 latency (1.94 ms per
+// evaluation; this form: see DESIGN.md section 3.9).
+constexpr int kToyLanes = 16;
 
-__global__ void toy_rollout_kernel(const ToyK a) {
-    extern __shared__ double s_w[];  // d x blockDim: parameter k of thread t at s_w[k * blockDim + t]
-    const uint32_t B = blockDim.x;
-    const uint64_t row0 = blockIdx.x * (uint64_t)B;
-    // cooperative, coalesced staging of the CTA's rows
-    for (uint32_t t = 0; t < B; ++t) {
-        const uint64_t i = row0 + t;
-        if (i >= a.n) break;
-        const double* p = a.params + (a.rows ? (uint64_t)a.rows[i] : i) * a.d;
-        for (uint32_t k = threadIdx.x; k < a.d; k += B) s_w[k * B + t] = p[k];
-    }
-    __syncthreads();
-    const uint64_t i = row0 + threadIdx.x;
-    if (i >= a.n) return;
-    const auto w = [&](uint32_t k) { return s_w[k * B + threadIdx.x]; };
-    const uint64_t f0 = a.f_row0 + (a.f_row0_dev ? (uint64_t)*a.f_row0_dev : 0);
-    double hid[kToyMaxHidden], act[kToyAct];
-    if (a.obs) {  // a single forward pass per individual
-        double ob[kToyObs];
-        for (int j = 0; j < kToyObs; ++j) ob[j] = a.obs[i * kToyObs + j];
-        mlp_forward_dev(w, a.hidden, ob, hid, act);
-        a.f[i * kToyAct] = act[0];
-        a.f[i * kToyAct + 1] = act[1];
-        return;
-    }
-    double* fr = a.f + (f0 + i) * a.m;
+template <int U>
+__global__ void __launch_bounds__(128) toy_rollout_kernel(const ToyK a) {
+    __shared__ __align__(16) double s_p[4][2][kToyAct][kToyMaxHidden];  // [warp][group][output][hidden unit]
+    const uint32_t lane = threadIdx.x & 31, sub = lane & (kToyLanes - 1), grp = lane >> 4, warp = threadIdx.x >> 5;
+    const uint64_t i = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / kToyLanes;
+    const bool live = i < a.n;
+    const uint32_t H = a.hidden;
+    const uint32_t o_b1 = H * kToyObs, o_w2 = o_b1 + H, o_b2 = o_w2 + kToyAct * H;
+    const double* p = a.params + (live ? (a.rows ? (uint64_t)a.rows[i] : i) : 0) * a.d;
+    double w1[U][kToyObs], b1[U], w2[U][kToyAct];
     bool finite = true;
-    for (uint32_t k = 0; k < a.d; ++k) {
-        const double p = w(k);
-        if (!(fabs(p) < INFINITY)) finite = false;  // problems.hpp:224-226
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const uint32_t unit = sub + kToyLanes * u;
+        const bool has = unit < H;
+#pragma unroll
+        for (int j = 0; j < kToyObs; ++j) w1[u][j] = has ? p[unit * kToyObs + j] : 0.0;
+        b1[u] = has ? p[o_b1 + unit] : 0.0;
+#pragma unroll
+        for (int o = 0; o < kToyAct; ++o) w2[u][o] = has ? p[o_w2 + o * H + unit] : 0.0;
+#pragma unroll
+        for (int j = 0; j < kToyObs; ++j) finite &= fabs(w1[u][j]) < INFINITY;
+        finite &= fabs(b1[u]) < INFINITY && fabs(w2[u][0]) < INFINITY && fabs(w2[u][1]) < INFINITY;
     }
-    if (!finite) {
-        for (uint32_t j = 0; j < a.m; ++j) fr[j] = a.negate ? 1e9 : -1e9;  // problems.hpp:227-230
+    const double b2_0 = p[o_b2], b2_1 = p[o_b2 + 1];
+    finite &= fabs(b2_0) < INFINITY && fabs(b2_1) < INFINITY;
+    const unsigned bad = __ballot_sync(0xffffffffu, !finite);
+    finite = ((bad >> (grp * kToyLanes)) & 0xffffu) == 0;  // problems.hpp:224-226: any non-finite parameter of the individual
+    double (*sp)[kToyMaxHidden] = s_p[warp][grp];
+
+    // one policy evaluation: ob -> (act0, act1), the same bits in every lane of the group
+    auto policy = [&](const double* ob, double& act0, double& act1) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t unit = sub + kToyLanes * u;
+            double s = b1[u];
+#pragma unroll
+            for (int j = 0; j < kToyObs; ++j) s += w1[u][j] * ob[j];
+            const double hid = glibc_tanh(s);
+            if (unit < H) {
+                sp[0][unit] = w2[u][0] * hid;
+                sp[1][unit] = w2[u][1] * hid;
+            }
+        }
+        __syncwarp();
+        // even lanes add output 0, odd lanes output 1 (one add per hidden unit and warp instead of two)
+        const double* mine = sp[sub & 1];
+        double so = (sub & 1) ? b2_1 : b2_0;
+        for (uint32_t k = 0; k + 1 < H; k += 2) {  // ascending hidden unit, two per 128-bit read
+            const double2 q = *reinterpret_cast<const double2*>(&mine[k]);
+            so += q.x;
+            so += q.y;
+        }
+        if (H & 1) so += mine[H - 1];
+        __syncwarp();
+        const double act = glibc_tanh(so);  // lanes 0 / 1 of the group hold the two actions
+        act0 = __shfl_sync(0xffffffffu, act, grp * kToyLanes);
+        act1 = __shfl_sync(0xffffffffu, act, grp * kToyLanes + 1);
+    };
+
+    if (a.obs) {  // mlp_forward: a single evaluation per individual
+        double ob[kToyObs], act0, act1;
+#pragma unroll
+        for (int j = 0; j < kToyObs; ++j) ob[j] = live ? a.obs[i * kToyObs + j] : 0.0;
+        policy(ob, act0, act1);
+        if (live && sub == 0) {
+            a.f[i * kToyAct] = act0;
+            a.f[i * kToyAct + 1] = act1;
+        }
         return;
     }
     const double h0 = 1.0;
@@ -98,12 +129,20 @@ __global__ void toy_rollout_kernel(const ToyK a) {
         ob[1] = h;
         ob[2] = a.phase[2 * t];
         ob[3] = a.phase[2 * t + 1];
-        mlp_forward_dev(w, a.hidden, ob, hid, act);
-        v = 0.9 * v + 0.1 * act[0];
-        h = clampd(0.95 * h + 0.1 * act[1], 0.0, 2.0);
+        double act0, act1;
+        policy(ob, act0, act1);
+        v = 0.9 * v + 0.1 * act0;
+        h = clampd(0.95 * h + 0.1 * act1, 0.0, 2.0);
         fwd += v;
-        ctrl -= act[0] * act[0] + act[1] * act[1];
+        ctrl -= act0 * act0 + act1 * act1;
         height += 10.0 * (h - h0);
+    }
+    if (!live || sub != 0) return;
+    const uint64_t f0 = a.f_row0 + (a.f_row0_dev ? (uint64_t)*a.f_row0_dev : 0);
+    double* fr = a.f + (f0 + i) * a.m;
+    if (!finite) {
+        for (uint32_t j = 0; j < a.m; ++j) fr[j] = a.negate ? 1e9 : -1e9;  // problems.hpp:227-230
+        return;
     }
     if (a.m == 2) {
         fr[0] = a.negate ? -fwd : fwd;
@@ -137,18 +176,14 @@ const double* toy_phase_table(uint64_t horizon, cudaStream_t s) {
     return dev;
 }
 
-void launch_toy_kernel(ToyK k, cudaStream_t s) {
-    // threads per CTA: as many individuals as fit ~100 KB of parameters (two CTAs per SM), a multiple of 32, at most 128
-    uint32_t B = (uint32_t)(100 * 1024 / (k.d * sizeof(double))) / 32 * 32;
-    if (B < 32) B = 32;
-    if (B > 128) B = 128;
-    const size_t smem = (size_t)k.d * B * sizeof(double);
-    static size_t configured = 0;
-    if (smem > configured) {
-        TEMO_CUDA(cudaFuncSetAttribute(toy_rollout_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        configured = smem;
+void launch_toy_kernel(const ToyK& k, cudaStream_t s) {
+    const unsigned grid = (unsigned)((k.n * kToyLanes + 127) / 128);
+    switch ((k.hidden + kToyLanes - 1) / kToyLanes) {  // hidden units per lane
+    case 1: toy_rollout_kernel<1><<<grid, 128, 0, s>>>(k); break;
+    case 2: toy_rollout_kernel<2><<<grid, 128, 0, s>>>(k); break;
+    case 3: toy_rollout_kernel<3><<<grid, 128, 0, s>>>(k); break;
+    default: toy_rollout_kernel<4><<<grid, 128, 0, s>>>(k); break;
     }
-    toy_rollout_kernel<<<(unsigned)((k.n + B - 1) / B), B, smem, s>>>(k);
     TEMO_CUDA(cudaGetLastError());
 }
 
