@@ -385,9 +385,17 @@ struct PairSmem {
     // per pair by the warp that fetched it)
     uint32_t ring[kUnitRing];
     PairCtx ringctx[kUnitRing];
+    PairCtx warpctx[kVirtWarps];    // single-warp pairs (TEAM == 1): every warp describes its own
+    PairSlot warpslot[kVirtWarps];  // ... and collects its own totals
     uint32_t progress[kVirtWarps];  // turns every warp has finished
     uint32_t claiming, published;   // highest turn being fetched / already published
 };
+
+static_assert(sizeof(PairSmem) + 1024 <= (228 * 1024) / TEMO_PAIR_MIN_BLOCKS, "the teams of an SM must fit its shared memory");
+template <int N> struct ShowSize;
+#ifdef TEMO_SHOW_SMEM
+ShowSize<sizeof(PairSmem)> show_pair_smem;
+#endif
 
 // mix64 (rng.hpp:23-30) on 32-bit halves; a 64-bit product costs one wide multiply and two multiply-adds.
 struct Hash64 {
@@ -551,12 +559,13 @@ __device__ __forceinline__ void accumulate_vector(uint32_t j0, uint32_t m1, doub
 
 // Pass B of a tile with the general pow (base 0, or an exponent outside the narrow path's range): same list, same stores.
 template <int MODE>
-__device__ __noinline__ void pass_b_general(const ReproK& a, uint64_t pos_tile, uint32_t total, uint32_t sm_w, uint32_t lane) {
+__device__ __noinline__ void pass_b_general(const ReproK& a, uint64_t pos_tile, uint32_t total, uint32_t sm_w, uint32_t lane,
+                                            uint32_t stride) {
     constexpr uint64_t SG = MODE == 0 ? kGolden : 1ULL;
     constexpr uint32_t kOffList = offsetof(WarpSmem, list);
     for (uint32_t t = lane; t < total; t += 32) {
         const uint32_t e = lds_u16(sm_w + kOffList + 2 * t);
-        const uint32_t j = e + (e >> 6) * (kVirtWarps * 64 - 64);
+        const uint32_t j = e + (e >> 6) * (stride * 64 - 64);
         const SpreadIn s = spread_inputs<MODE>(a.rng.seed, pos_tile + (uint64_t)j * SG, a.dl_r1, a.inv_exp);
         const double p = pow_spread_slow(s.base, s.yexp);
         sts_f64(sm_w + 8 * e, s.up ? p : -p);
@@ -579,7 +588,7 @@ __device__ __forceinline__ void fill_pair_ctx(PairCtx& c, const ReproK& a, uint6
 // the candidate slots of the phased passes overflow. Same bits, same accumulation order.
 template <int MODE, int EVAL>
 __device__ __noinline__ void tile_plain(const ReproK& a, uint32_t blk0, uint32_t v, uint32_t kmax, double* acc, const PairCtx* ctx,
-                                        double (*pos)[kMaxObj]) {
+                                        double (*pos)[kMaxObj], uint32_t stride) {
     const PairCtx c = *ctx;
     constexpr uint64_t SG = MODE == 0 ? kGolden : 1ULL;
     const uint32_t lane = threadIdx.x & 31;
@@ -588,7 +597,7 @@ __device__ __noinline__ void tile_plain(const ReproK& a, uint32_t blk0, uint32_t
     const PowTables T = pow_tables_global();
     double acc_a = acc[0], acc_b = acc[1];
     for (uint32_t k = 0; k < kmax; ++k) {
-        const uint32_t q = (blk0 + v + k * kVirtWarps) * 32 + lane;
+        const uint32_t q = (blk0 + v + k * stride) * 32 + lane;
         if (q >= nvec) break;
         double xa[2], xb[2], lo[2], hi[2], ca[2], cb[2];
         const double2 va = reinterpret_cast<const double2*>(c.pa)[q], vb = reinterpret_cast<const double2*>(c.pb)[q];
@@ -612,15 +621,23 @@ __device__ __noinline__ void tile_plain(const ReproK& a, uint32_t blk0, uint32_t
     acc[0] = acc_a, acc[1] = acc_b;
 }
 
-template <int MODE, int EVAL, int SEG>  // SEG: 0 bound arrays, 1 one constant segment, 2 two constant segments
+// TEAM: warps that share a pair. 8: the team of the description above (wide rows). 1: narrow rows - every warp takes whole
+// pairs on its own and walks the row's blocks consecutively (a row of d = 1000 is 16 blocks: two per warp of a team, and the
+// per-pair and per-tile work of eight warps for them; one warp makes a ten- and a six-block tile of it). Without the fused
+// sums only: their canonical order is that of the eight-warp mapping.
+template <int MODE, int EVAL, int SEG, int TEAM, int STRIDE>  // SEG: 0 bound arrays, 1 one constant segment, 2 two constant segments
 __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reproduce_pairs_kernel(const __grid_constant__ ReproK a) {
+    static_assert((TEAM == kVirtWarps && STRIDE == kVirtWarps) || (TEAM == 1 && (STRIDE == kVirtWarps || (STRIDE == 1 && EVAL == 0))),
+                  "consecutive blocks carry no fused sums");
     extern __shared__ __align__(16) unsigned char pair_smem_raw[];
     PairSmem& S = *reinterpret_cast<PairSmem*>(pair_smem_raw);
+    constexpr uint32_t kStride = STRIDE;                           // distance of a warp's consecutive blocks
+    constexpr uint32_t kVPerWarp = TEAM == 1 && STRIDE == kVirtWarps ? kVirtWarps : 1;  // virtual warps a warp walks through
     constexpr uint64_t SG = MODE == 0 ? kGolden : 1ULL;            // stream distance of neighbouring genes
-    constexpr uint64_t STEP = SG * (uint64_t)(kVirtWarps * 64);    // ... of a lane's consecutive blocks
+    constexpr uint64_t STEP = SG * (uint64_t)(kStride * 64);       // ... of a lane's consecutive blocks
     constexpr uint32_t kOffList = offsetof(WarpSmem, list), kOffSide = offsetof(WarpSmem, side);
-    const uint32_t lane = opaque(threadIdx.x & 31), v = opaque(threadIdx.x >> 5);
-    WarpSmem& W = S.w[v];
+    const uint32_t lane = opaque(threadIdx.x & 31), warp = opaque(threadIdx.x >> 5);
+    WarpSmem& W = S.w[warp];
 
     pow_smem_load(S.pow);
     if (threadIdx.x < kPairSlots) {
@@ -630,7 +647,7 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
     if (threadIdx.x < kVirtWarps) S.progress[threadIdx.x] = 0;
     if (threadIdx.x == 0) {
         S.claiming = S.published = 0;
-        if (a.unit0 + blockIdx.x < a.unit_end) fill_pair_ctx<MODE>(S.ringctx[0], a, a.unit0 + blockIdx.x);  // the team's first pair
+        if (TEAM != 1 && a.unit0 + blockIdx.x < a.unit_end) fill_pair_ctx<MODE>(S.ringctx[0], a, a.unit0 + blockIdx.x);  // the team's first pair
     }
     __syncthreads();  // the only CTA barrier: from here on every warp is on its own
     const PowTables T = pow_tables(S.pow);
@@ -649,23 +666,27 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
     // A team's first pair is its block index; for every later turn the first warp to get there draws the next pair
     // from a global counter and publishes it to the team through a small ring (the warps of a team are never more
     // than kUnitRing turns apart).
-    for (uint64_t unit = a.unit0 + blockIdx.x; unit < a.unit_end; ++turn) {
-        PairSlot& slot = S.slot[turn % kPairSlots];
-        const PairCtx& C = S.ringctx[turn % kUnitRing];
-        if (EVAL != 0 && lane == 0)  // the slot is free once the pair that used it kPairSlots turns ago has been written out
+    for (uint64_t unit = a.unit0 + (TEAM == 1 ? blockIdx.x * kVirtWarps + warp : blockIdx.x); unit < a.unit_end; ++turn) {
+        PairSlot& slot = TEAM == 1 ? S.warpslot[warp] : S.slot[turn % kPairSlots];
+        const PairCtx& C = TEAM == 1 ? S.warpctx[warp] : S.ringctx[turn % kUnitRing];
+        if (TEAM == 1 && lane == 0) fill_pair_ctx<MODE>(S.warpctx[warp], a, unit);
+        if (EVAL != 0 && TEAM != 1 && lane == 0)  // the slot is free once the pair that used it kPairSlots turns ago has been written out
             while (*reinterpret_cast<volatile uint32_t*>(&slot.done) < turn / kPairSlots) __nanosleep(TEMO_PAIR_SLEEP);
         __syncwarp();  // also orders the reads of the pair's context behind lane 0's look at the hand-out ring
 
+#pragma unroll 1
+        for (uint32_t vv = 0; vv < kVPerWarp; ++vv) {
+        const uint32_t v = TEAM == 1 ? vv : warp;
         double acc_a = 0.0, acc_b = 0.0;
-        for (uint32_t blk0 = 0; blk0 < nblk; blk0 += kVirtWarps * kPairBlocks) {
+        for (uint32_t blk0 = 0; blk0 < nblk; blk0 += kStride * kPairBlocks) {
             // blocks v, v + 8, ... of this row tile (warp-uniform count)
-            const uint32_t left = nblk - blk0 > v ? (nblk - blk0 - v + kVirtWarps - 1) / kVirtWarps : 0u;
+            const uint32_t left = nblk - blk0 > v ? (nblk - blk0 - v + kStride - 1) / kStride : 0u;
             const uint32_t kmax = opaque(min(left, (uint32_t)kPairBlocks));
             if (kmax == 0) break;
             const uint32_t q_first = (blk0 + v) * 32 + lane;  // this lane's vector in the tile's first block
             const uint64_t pos = C.pos;
             {   // this warp's parent blocks of this tile into L2 (they are read in pass C)
-                const uint32_t kk = lane & 15, blk = blk0 + v + kk * kVirtWarps;
+                const uint32_t kk = lane & 15, blk = blk0 + v + kk * kStride;
                 if (kk < kmax && blk < nblk) {
                     const char* p = reinterpret_cast<const char*>(lane < 16 ? C.pa : C.pb) + (uint64_t)blk * 512;
 #pragma unroll
@@ -679,7 +700,7 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
                 const uint64_t first = pos + (uint64_t)(2 * q_first) * SG;
                 uint64_t p_r2 = first + a.dl_r2, p_ma = first + a.dl_mask_a, p_mb = first + a.dl_mask_b;
                 uint32_t q = q_first, e = lane * 2, sm_b = sm_lane;
-                for (uint32_t k = 0; k < kmax; ++k, p_r2 += STEP, p_ma += STEP, p_mb += STEP, q += kVirtWarps * 32, e += 64, sm_b += 512) {
+                for (uint32_t k = 0; k < kmax; ++k, p_r2 += STEP, p_ma += STEP, p_mb += STEP, q += kStride * 32, e += 64, sm_b += 512) {
                     const bool valid = q < nvec;
                     const bool vc = valid && cross;
                     // hr = H(r2 - 0.5) = 0 <=> top bit clear
@@ -712,7 +733,7 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
             __syncwarp();
             if (ncand > (uint32_t)a.cand_cap) {  // practically never: the literal formulation of this tile
                 double acc[2] = {acc_a, acc_b};
-                tile_plain<MODE, EVAL>(a, blk0, v, kmax, acc, &C, slot.pos);
+                tile_plain<MODE, EVAL>(a, blk0, v, kmax, acc, &C, slot.pos, kStride);
                 acc_a = acc[0], acc_b = acc[1];
                 __syncwarp();
                 continue;
@@ -729,7 +750,7 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
                     const bool two = t + 32 < total;
                     const uint32_t e0 = lds_u16(sm_w + kOffList + 2 * t), e1 = two ? lds_u16(sm_w + kOffList + 2 * t + 64) : e0;
                     // gene index relative to the tile's first gene
-                    const uint32_t j0 = e0 + (e0 >> 6) * (kVirtWarps * 64 - 64), j1 = e1 + (e1 >> 6) * (kVirtWarps * 64 - 64);
+                    const uint32_t j0 = e0 + (e0 >> 6) * (kStride * 64 - 64), j1 = e1 + (e1 >> 6) * (kStride * 64 - 64);
                     const uint64_t at0 = pos_tile + (uint64_t)j0 * SG, at1 = pos_tile + (uint64_t)j1 * SG;
                     const double mc0 = word_to_unit(draw_full<MODE>(seed, at0)), mc1 = word_to_unit(draw_full<MODE>(seed, at1));
                     const uint32_t r10 = draw_top<MODE>(seed, at0 + a.dl_r1), r11 = draw_top<MODE>(seed, at1 + a.dl_r1);
@@ -748,14 +769,14 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
                     sts_f64(sm_w + 8 * e0, q0);
                     if (two) sts_f64(sm_w + 8 * e1, q1);
                 }
-                if (__any_sync(0xffffffffu, redo)) pass_b_general<MODE>(a, pos_tile, total, sm_w, lane);
+                if (__any_sync(0xffffffffu, redo)) pass_b_general<MODE>(a, pos_tile, total, sm_w, lane, kStride);
             }
             __syncwarp();
             // ---- pass M: the mutation candidates of this tile (usually none)
 #pragma unroll 1
             for (uint32_t t = lane; t < ncand; t += 32) {
                 const uint32_t entry = W.cand[t], e = entry & 0x1fffu;
-                const uint32_t j = (blk0 + v) * 64 + e + (e >> 6) * (kVirtWarps * 64 - 64);
+                const uint32_t j = (blk0 + v) * 64 + e + (e >> 6) * (kStride * 64 - 64);
                 const uint64_t at = pos + (uint64_t)j * SG;
                 const double2 ch = mutated_children<MODE>(seed, at + a.dl_mask_a, at + a.dl_mask_b, a.dl_mut_a - a.dl_mask_a,
                                                           a.mask_thresh, a.xi, (entry & 0x2000u) != 0, (entry & 0x4000u) != 0,
@@ -773,7 +794,7 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
                 const double2* __restrict__ hi2 = reinterpret_cast<const double2*>(a.upper);
                 // piecewise-constant bounds from the launch constants (SEG): one side of the split for the whole tile,
                 // unless the tile's blocks straddle it
-                const uint32_t tile_g0 = (blk0 + v) * 64, tile_g1 = (blk0 + v + (kmax - 1) * kVirtWarps) * 64 + 64;
+                const uint32_t tile_g0 = (blk0 + v) * 64, tile_g1 = (blk0 + v + (kmax - 1) * kStride) * 64 + 64;
                 const bool seg_hi_side = tile_g0 >= a.seg_split, seg_mixed = SEG != 0 && !seg_hi_side && tile_g1 > a.seg_split;
                 const double seg_lo = a.seg_lo[seg_hi_side ? 1 : 0], seg_hi = a.seg_hi[seg_hi_side ? 1 : 0];
                 const double2* __restrict__ pa2 = reinterpret_cast<const double2*>(C.pa);
@@ -789,18 +810,18 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
                     const double2 zero2 = make_double2(0.0, 0.0);
                     double2 a0 = q < nvec ? __ldcs(pa2 + q) : zero2, b0 = q < nvec ? __ldcs(pb2 + q) : zero2;
                     double2 a1 = zero2, b1 = zero2;
-                    if (kmax > 1 && q + kVirtWarps * 32 < nvec) {
-                        a1 = __ldcs(pa2 + q + kVirtWarps * 32);
-                        b1 = __ldcs(pb2 + q + kVirtWarps * 32);
+                    if (kmax > 1 && q + kStride * 32 < nvec) {
+                        a1 = __ldcs(pa2 + q + kStride * 32);
+                        b1 = __ldcs(pb2 + q + kStride * 32);
                     }
                     // three sets (three blocks in flight) pay without the fused sums only: with them the larger loop body costs
                     // more in instruction fetch than the extra block in flight saves (3.32 vs 3.05 ms)
                     constexpr int kSets = (TEMO_PAIR_SETS == 3 && EVAL == 0) ? 3 : 2;
                     double2 a2 = zero2, b2 = zero2;
                     if constexpr (kSets == 3) {
-                        if (kmax > 2 && q + 2 * kVirtWarps * 32 < nvec) {
-                            a2 = __ldcs(pa2 + q + 2 * kVirtWarps * 32);
-                            b2 = __ldcs(pb2 + q + 2 * kVirtWarps * 32);
+                        if (kmax > 2 && q + 2 * kStride * 32 < nvec) {
+                            a2 = __ldcs(pa2 + q + 2 * kStride * 32);
+                            b2 = __ldcs(pb2 + q + 2 * kStride * 32);
                         }
                     }
                     auto block = [&](uint32_t k, double2& pa_v, double2& pb_v) {
@@ -820,7 +841,7 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
                         sbx_children(pa_v.x, pb_v.x, vbeta.x, lo_x, hi_x, ca0, cb0);
                         sbx_children(pa_v.y, pb_v.y, vbeta.y, lo_y, hi_y, ca1, cb1);
                         {   // the set is free: block k + kSets goes into it
-                            const uint32_t qf = q + kSets * kVirtWarps * 32;
+                            const uint32_t qf = q + kSets * kStride * 32;
                             if (k + kSets < kmax && qf < nvec) {
                                 pa_v = __ldcs(pa2 + qf);
                                 pb_v = __ldcs(pb2 + qf);
@@ -841,7 +862,7 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
                         accumulate_vector<EVAL>(2 * q, m1, ca0, cb0, ca1, cb1, acc_a, acc_b, slot.pos);
                         __stcs(oa2 + q, make_double2(ca0, ca1));
                         __stcs(ob2 + q, make_double2(cb0, cb1));
-                        q += kVirtWarps * 32;
+                        q += kStride * 32;
                         sm_b += 512;
                     };
                     for (uint32_t k = 0; k < kmax; k += kSets) {
@@ -870,10 +891,17 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
             if (lane == 0) {
                 slot.part[0][v] = acc_a;
                 slot.part[1][v] = acc_b;
-                __threadfence_block();
-                before = atomicAdd(&slot.arrived, 1u);
+                if (TEAM != 1) {
+                    __threadfence_block();
+                    before = atomicAdd(&slot.arrived, 1u);
+                }
             }
-            before = __shfl_sync(0xffffffffu, before, 0);
+            if (TEAM == 1) {
+                __syncwarp();
+                before = v;  // the last virtual warp writes the rows out
+            } else {
+                before = __shfl_sync(0xffffffffu, before, 0);
+            }
             if (before == kVirtWarps - 1) {
                 __threadfence_block();
                 const uint64_t f0 = a.f_row0 + (a.f_row0_dev ? (uint64_t)*a.f_row0_dev : 0);
@@ -891,19 +919,27 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
                     fb[i] = *reinterpret_cast<volatile double*>(&slot.pos[1][i - 1]);
                 }
                 __syncwarp();
-                if (lane == 0) {
+                if (TEAM != 1 && lane == 0) {
                     slot.arrived = 0;
                     __threadfence_block();
                     *reinterpret_cast<volatile uint32_t*>(&slot.done) = turn / kPairSlots + 1;
                 }
             }
         }
+        }  // virtual warps
         __syncwarp();
+        if constexpr (TEAM == 1) {  // this warp's next pair
+            uint32_t next = 0;
+            if (lane == 0) next = a.work_counter ? atomicAdd(a.work_counter, 1u) : turn * gridDim.x * kVirtWarps + blockIdx.x * kVirtWarps + warp;
+            next = __shfl_sync(0xffffffffu, next, 0);
+            unit = a.unit0 + (uint64_t)gridDim.x * kVirtWarps + next;
+            continue;
+        }
         // ---- the team's next pair (round-robin over the grid without a work counter)
         uint32_t next = 0;
         if (lane == 0) {
             const uint32_t T = turn + 1;
-            *reinterpret_cast<volatile uint32_t*>(&S.progress[v]) = T;
+            *reinterpret_cast<volatile uint32_t*>(&S.progress[warp]) = T;
             for (;;) {
                 if (*reinterpret_cast<volatile uint32_t*>(&S.published) >= T) {
                     next = *reinterpret_cast<volatile uint32_t*>(&S.ring[T % kUnitRing]);
@@ -931,6 +967,9 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
 struct K1Options {
     int generic, bound_arrays, cand_cap;
     int dynamic_pairs;  // pair kernel: pairs handed out through a global counter (1, default) or round-robin (0)
+    int single_warp;    // pair kernel, one warp per pair: -1 when the launch has a pair for every resident warp (default: consecutive
+                        // blocks without fused sums, the eight-virtual-warp walk with them), 0 never, 1 consecutive blocks whenever
+                        // that applies, 2 the walk always
 };
 inline int env_int(const char* name, int dflt) {
     const char* e = getenv(name);
@@ -939,7 +978,7 @@ inline int env_int(const char* name, int dflt) {
 inline K1Options& k1_options() {
     static K1Options o{env_int("TEMO_B200_GENERIC_K1", 0), env_int("TEMO_B200_K1_BOUND_ARRAYS", 0),
                        std::max(0, std::min(kPairCand, env_int("TEMO_B200_K1_CAND_CAP", kPairCand))),
-                       env_int("TEMO_B200_K1_DYNAMIC_PAIRS", 1)};
+                       env_int("TEMO_B200_K1_DYNAMIC_PAIRS", 1), env_int("TEMO_B200_K1_SINGLE_WARP", -1)};
     return o;
 }
 inline bool force_generic_kernel() { return k1_options().generic != 0; }
@@ -955,11 +994,11 @@ inline uint32_t* next_work_counter() {
     return counters + (next.fetch_add(1) % kCounters);
 }
 
-template <int MODE, int EVAL, int SEG>
+template <int MODE, int EVAL, int SEG, int TEAM = kVirtWarps, int STRIDE = kVirtWarps>
 void launch_pairs_seg(const ReproK& k, uint64_t units, cudaStream_t s) {
     static int grid = 0;  // per instantiation
     if (grid == 0) {
-        TEMO_CUDA(cudaFuncSetAttribute(reproduce_pairs_kernel<MODE, EVAL, SEG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        TEMO_CUDA(cudaFuncSetAttribute(reproduce_pairs_kernel<MODE, EVAL, SEG, TEAM, STRIDE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)sizeof(PairSmem)));
         int dev = 0, sms = 0;
         TEMO_CUDA(cudaGetDevice(&dev));
@@ -974,11 +1013,31 @@ void launch_pairs_seg(const ReproK& k, uint64_t units, cudaStream_t s) {
         kk.work_counter = next_work_counter();
         TEMO_CUDA(cudaMemsetAsync(kk.work_counter, 0, sizeof(uint32_t), s));
     }
-    reproduce_pairs_kernel<MODE, EVAL, SEG><<<(unsigned)std::min<uint64_t>(units, (uint64_t)grid), kVirtWarps * 32, sizeof(PairSmem), s>>>(kk);
+    const uint64_t teams_per_cta = TEAM == 1 ? kVirtWarps : 1;
+    reproduce_pairs_kernel<MODE, EVAL, SEG, TEAM, STRIDE>
+        <<<(unsigned)std::min<uint64_t>((units + teams_per_cta - 1) / teams_per_cta, (uint64_t)grid), kVirtWarps * 32, sizeof(PairSmem), s>>>(kk);
 }
 
 template <int MODE, int EVAL>
-void launch_pairs_eval(const ReproK& k, uint64_t units, int seg, cudaStream_t s) {
+void launch_pairs_eval(const ReproK& k, uint64_t units, int seg, int team, cudaStream_t s) {
+    if constexpr (EVAL == 0) {
+        if (team == 1) {  // one warp per pair, consecutive blocks
+            switch (seg) {
+            case 1: launch_pairs_seg<MODE, 0, 1, 1, 1>(k, units, s); break;
+            case 2: launch_pairs_seg<MODE, 0, 2, 1, 1>(k, units, s); break;
+            default: launch_pairs_seg<MODE, 0, 0, 1, 1>(k, units, s); break;
+            }
+            return;
+        }
+    }
+    if (team == -1) {  // one warp per pair, walking through the eight virtual warps of the canonical mapping
+        switch (seg) {
+        case 1: launch_pairs_seg<MODE, EVAL, 1, 1, kVirtWarps>(k, units, s); break;
+        case 2: launch_pairs_seg<MODE, EVAL, 2, 1, kVirtWarps>(k, units, s); break;
+        default: launch_pairs_seg<MODE, EVAL, 0, 1, kVirtWarps>(k, units, s); break;
+        }
+        return;
+    }
     switch (seg) {
     case 1: launch_pairs_seg<MODE, EVAL, 1>(k, units, s); break;
     case 2: launch_pairs_seg<MODE, EVAL, 2>(k, units, s); break;
@@ -987,13 +1046,13 @@ void launch_pairs_eval(const ReproK& k, uint64_t units, int seg, cudaStream_t s)
 }
 
 template <int MODE>
-void launch_pairs(const ReproK& k, uint64_t units, int eval, int seg, cudaStream_t s) {
+void launch_pairs(const ReproK& k, uint64_t units, int eval, int seg, int team, cudaStream_t s) {
     switch (eval) {
-    case 0: launch_pairs_eval<MODE, 0>(k, units, seg, s); break;
-    case kDtlz1: launch_pairs_eval<MODE, kDtlz1>(k, units, seg, s); break;
-    case kDtlz2: launch_pairs_eval<MODE, kDtlz2>(k, units, seg, s); break;
-    case kDtlz3: launch_pairs_eval<MODE, kDtlz3>(k, units, seg, s); break;
-    case kDtlz4: launch_pairs_eval<MODE, kDtlz4>(k, units, seg, s); break;
+    case 0: launch_pairs_eval<MODE, 0>(k, units, seg, team, s); break;
+    case kDtlz1: launch_pairs_eval<MODE, kDtlz1>(k, units, seg, team, s); break;
+    case kDtlz2: launch_pairs_eval<MODE, kDtlz2>(k, units, seg, team, s); break;
+    case kDtlz3: launch_pairs_eval<MODE, kDtlz3>(k, units, seg, team, s); break;
+    case kDtlz4: launch_pairs_eval<MODE, kDtlz4>(k, units, seg, team, s); break;
     default: fail(1, "reproduce: fused evaluation supports DTLZ1-4 only");
     }
 }
@@ -1064,6 +1123,9 @@ __global__ void pow_batch_kernel(const double* x, const double* y, uint64_t n, d
 //                       they are piecewise constant                       TEMO_B200_K1_BOUND_ARRAYS
 //   k1_cand_cap      mutation-candidate slots per warp tile of the pair
 //                    kernel, 0..kPairCand (0 forces its plain-tile path)  TEMO_B200_K1_CAND_CAP
+//   k1_single_warp   pair kernel with one warp per pair: -1 by shape,
+//                    0 never, 1 consecutive blocks (no fused sums),
+//                    2 the eight-virtual-warp walk                        TEMO_B200_K1_SINGLE_WARP
 inline unsigned stream_grid(uint64_t total, int block) {
     uint64_t g = (total + block - 1) / block;
     const uint64_t cap = (uint64_t)kSMs * 16;
@@ -1141,11 +1203,20 @@ void launch_reproduce(const ReproArgs& a, cudaStream_t s) {
     // Full pairs of wide even rows go through the phased pair kernel when mutation candidates are rare (expected
     // number per warp and tile <= 1); what is left (an odd last row) and every other shape through the generic one.
     const double cand_rate = k.mask_never ? 0.0 : ((double)k.mask_top + 1.0) * 0x1.0p-21;  // P(quick reject passes)
-    const double cand_per_warp = 2.0 * (double)std::min<uint64_t>(a.d / kVirtWarps, kTileGenes) * cand_rate;
+    // One warp per pair (narrow rows, no fused sums): when the launch has enough pairs to give every resident warp its own.
+    const uint64_t pairs_launched = std::min(unit_hi, k.half) > unit_lo ? std::min(unit_hi, k.half) - unit_lo : 0;
+    const bool enough_pairs = pairs_launched >= (uint64_t)kSMs * TEMO_PAIR_MIN_BLOCKS * kVirtWarps;
+    const int sw = k1_options().single_warp;
+    const bool single_warp = a.eval_problem == 0 && (sw == 1 || (sw < 0 && enough_pairs));
+    const int team = single_warp ? 1 : (sw == 2 || (sw < 0 && enough_pairs) ? -1 : kVirtWarps);  // -1: one warp per pair walking the eight virtual warps
+    // expected mutation candidates per warp tile (the tile's slots overflow into its literal formulation: P(more than 8) is
+    // 2e-4 at an expectation of 2, the most a single warp's tile of consecutive blocks can see at pm = 1)
+    const double cand_per_warp = 2.0 * (double)std::min<uint64_t>(single_warp ? a.d : a.d / kVirtWarps, kTileGenes) * cand_rate;
+    const double cand_limit = single_warp ? 2.1 : 1.0;
     k.cand_cap = pair_cand_cap();
     uint64_t next = unit_lo;  // first unit not yet launched
-    if (a.do_sbx && a.do_pm && vec == 2 && block == 256 && unit_lo < std::min(unit_hi, k.half) && a.d * 8 < (1ULL << 32) &&
-        cand_per_warp <= 1.0 && (a.src_ptr != nullptr || aligned16(a.pool)) && aligned16(a.out) && aligned16(a.lower) && aligned16(a.upper) &&
+    if (a.do_sbx && a.do_pm && vec == 2 && (block == 256 || single_warp) && unit_lo < std::min(unit_hi, k.half) && a.d * 8 < (1ULL << 32) &&
+        cand_per_warp <= cand_limit && (a.src_ptr != nullptr || aligned16(a.pool)) && aligned16(a.out) && aligned16(a.lower) && aligned16(a.upper) &&
         !force_generic_kernel()) {
         // bounds as launch constants: 0 arrays, 1 one constant segment (DTLZ), 2 two constant segments (LSMOP)
         int seg = 0;
@@ -1160,9 +1231,9 @@ void launch_reproduce(const ReproArgs& a, cudaStream_t s) {
         k.unit0 = unit_lo;
         k.unit_end = std::min(unit_hi, k.half);
         if (a.rng.mode == 0)
-            launch_pairs<0>(k, k.unit_end - k.unit0, a.eval_problem, seg, s);
+            launch_pairs<0>(k, k.unit_end - k.unit0, a.eval_problem, seg, team, s);
         else
-            launch_pairs<1>(k, k.unit_end - k.unit0, a.eval_problem, seg, s);
+            launch_pairs<1>(k, k.unit_end - k.unit0, a.eval_problem, seg, team, s);
         TEMO_CUDA(cudaGetLastError());
         next = k.unit_end;
     }
@@ -1199,6 +1270,7 @@ bool set_k1_option(const char* name, long value) {
     else if (key == "k1_bound_arrays") o.bound_arrays = value != 0;
     else if (key == "k1_cand_cap") o.cand_cap = (int)std::max(0L, std::min((long)kPairCand, value));
     else if (key == "k1_dynamic_pairs") o.dynamic_pairs = value != 0;
+    else if (key == "k1_single_warp") o.single_warp = value < 0 ? -1 : (int)std::min(2L, value);
     else return false;
     return true;
 }

@@ -26,6 +26,7 @@ with tb.RveaRun(cfg) as run:
         out["x"] = hashlib.sha256(np.ascontiguousarray(st["x"]).tobytes()).hexdigest()[:16]
         out["f"] = hashlib.sha256(np.ascontiguousarray(st["f"]).tobytes()).hexdigest()[:16]
     out["k1_ms"] = run.time_stage(1, a.reps)
+    out["eval_ms"] = run.time_stage(2, a.reps)
     if not a.no_fuse:
         try:
             out["k1_fused_ms"] = run.time_stage(3, a.reps)
