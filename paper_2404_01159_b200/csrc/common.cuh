@@ -116,6 +116,13 @@ __host__ __device__ __forceinline__ double clampd(double x, double lo, double hi
 }
 
 // ---- block reductions with a fixed (launch-shape independent of the GPU count) order -------
+// Canonical row mapping of every kernel that sums over a row (standalone and fused evaluation): the row is cut into
+// blocks of 32 vectors (one per lane), warp w of the row's nw warps owns the cblk = ceil(blocks / nw) consecutive blocks
+// [w * cblk, (w + 1) * cblk), and a lane adds the terms of its vectors in ascending order. (Consecutive blocks, not
+// interleaved ones: a warp then streams one contiguous piece of the row, which is what lets a single warp of the pair
+// kernel of reproduce.cu walk a whole row.) Then block_sum's tree: xor butterfly in the warp, warp totals ascending.
+__host__ __device__ __forceinline__ uint32_t canon_chunk_blocks(uint32_t blocks, uint32_t nw) { return (blocks + nw - 1) / nw; }
+
 // Sum over the block in a canonical tree: xor-shuffle butterfly inside each warp, then the
 // warp totals are added in ascending warp order by every thread (all threads get the result).
 template <int MAXW>

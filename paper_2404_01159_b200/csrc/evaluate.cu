@@ -5,10 +5,10 @@
 // Algorithmic traffic: 8*n*d bytes read + 8*n*m written.
 //
 // Two DTLZ paths with bit-identical results (same thread->gene mapping, same reduction tree
-// as the epilogue fused into reproduce.cu):
-//   eval_tma_kernel  persistent CTAs; an elected thread streams row chunks into a shared-
-//                    memory ring with cp.async.bulk (TMA, SASS UBLKCP) + mbarrier
-//                    complete_tx; needs 16-byte aligned rows (d even).
+// as the epilogue fused into reproduce.cu: common.cuh, canon_chunk_blocks):
+//   eval_tma_kernel  persistent CTAs; every warp streams its consecutive blocks of the CTA's rows
+//                    through its own shared-memory ring with cp.async.bulk (TMA, SASS UBLKCP) +
+//                    mbarrier complete_tx; needs 16-byte aligned rows (d even).
 //   eval_ldg_kernel  one CTA per row with plain (128-bit when d is even) loads; any shape.
 #include <map>
 #include <mutex>
@@ -27,7 +27,6 @@ struct EvalK {
     double* f;
     uint64_t f_row0;
     const uint32_t* f_row0_dev;
-    uint32_t chunk;  // genes per TMA stage: a multiple of 512 (canonical order), <= kChunkGenes, rows split evenly
 };
 
 template <int PID, int VEC>
@@ -38,9 +37,12 @@ __global__ void __launch_bounds__(256) eval_ldg_kernel(const EvalK a) {
     const uint64_t row = a.rows ? a.rows[i] : i;
     const double* p = a.x + row * a.d;
     double acc = 0.0;
-    const uint64_t nvec = a.d / VEC;
-    for (uint64_t q = threadIdx.x; q < nvec; q += blockDim.x) {
-        const uint64_t j0 = q * VEC;
+    const uint32_t nvec = (uint32_t)(a.d / VEC);
+    const uint32_t cblk = canon_chunk_blocks((nvec + 31) >> 5, blockDim.x >> 5), q_first = (threadIdx.x >> 5) * cblk * 32 + (threadIdx.x & 31);
+    for (uint32_t it = 0; it < cblk; ++it) {  // canonical mapping: this warp's consecutive blocks
+        const uint32_t q = q_first + it * 32;
+        if (q >= nvec) break;
+        const uint64_t j0 = (uint64_t)q * VEC;
         double xv[VEC];
         if (VEC == 2) {
             const double2 t = *reinterpret_cast<const double2*>(p + j0);
@@ -64,8 +66,15 @@ __global__ void __launch_bounds__(256) eval_ldg_kernel(const EvalK a) {
 }
 
 // ---- TMA path ---------------------------------------------------------------------------------
-constexpr int kChunkGenes = 4096;  // 32 KB per stage; multiple of B*VEC = 512 keeps the canonical order
-constexpr int kStages = 3;         // 96 KB ring -> two CTAs per SM
+constexpr int kWarpStageGenes = 640;  // 5 KB per warp and stage: ten 64-gene blocks, the tile of the pair kernel
+#ifndef TEMO_EVAL_STAGES
+#define TEMO_EVAL_STAGES 2
+#endif
+#ifndef TEMO_EVAL_CTAS
+#define TEMO_EVAL_CTAS 2
+#endif
+constexpr int kStages = TEMO_EVAL_STAGES;  // per warp; 8 warps x kStages x 5 KB per CTA
+constexpr int kEvalSlots = 4;              // rows a CTA's warps may be apart
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -100,68 +109,108 @@ __device__ __forceinline__ void tma_load_1d(void* dst_smem, const void* src_gmem
         : "memory");
 }
 
-// Persistent: CTA c handles rows c, c+grid, ... ; every row is ceil(d/kChunkGenes) chunks that
-// flow through a kStages-deep ring. Thread 0 is the producer (issues the next bulk copy as soon
-// as a stage has been drained), all 256 threads consume. d must be even (16-byte rows).
+struct EvalRowSlot {
+    double part[8];        // per-warp totals of the row
+    double pos[kMaxObj];   // its position genes
+    uint32_t arrived;      // warps that have delivered their total
+    uint32_t done;         // rows completed through this slot
+};
+struct EvalTmaSmem {
+    double tile[8][kStages][kWarpStageGenes];
+    uint64_t full_bar[8][kStages];
+    EvalRowSlot slot[kEvalSlots];
+};
+
+// Persistent: CTA c handles rows c, c + grid, ... Every warp streams ITS blocks of those rows (the canonical mapping:
+// warp w owns the consecutive blocks [w * cblk, (w + 1) * cblk) of a row) through its own ring of kStages bulk copies
+// with its own mbarriers - no CTA barrier anywhere: lane 0 issues the warp's next copy as soon as the warp has drained
+// a stage, the warps of a CTA drift apart, and the last of the eight to deliver a row's total adds the totals in
+// ascending warp order and leaves {sum, position genes} for eval_finish_kernel. d must be even (16-byte rows).
 template <int PID>
 __global__ void __launch_bounds__(256) eval_tma_kernel(const EvalK a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    double* ring = reinterpret_cast<double*>(smem_raw);  // kStages x kChunkGenes
-    __shared__ __align__(8) uint64_t full_bar[kStages];
-    __shared__ double s_red[8];
-    __shared__ double s_pos[kMaxObj];
+    EvalTmaSmem& S = *reinterpret_cast<EvalTmaSmem*>(smem_raw);
+    const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 
-    const uint64_t chunk = a.chunk;
-    const uint64_t chunks_per_row = (a.d + chunk - 1) / chunk;
+    if (threadIdx.x < 8 * kStages) mbar_init(&S.full_bar[threadIdx.x / kStages][threadIdx.x % kStages], 1);
+    if (threadIdx.x < kEvalSlots) S.slot[threadIdx.x].arrived = S.slot[threadIdx.x].done = 0;
+    if (threadIdx.x == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncthreads();  // the only one
+
+    const uint32_t nvec = (uint32_t)(a.d >> 1), nblk = (nvec + 31) >> 5, cblk = canon_chunk_blocks(nblk, 8);
+    const uint32_t g_begin = min(w * cblk * 64u, (uint32_t)a.d), g_end = min((w + 1) * cblk * 64u, (uint32_t)a.d);
+    const uint32_t nsub = (g_end - g_begin + kWarpStageGenes - 1) / kWarpStageGenes;  // copies per row (0: nothing of the row is ours)
     const uint64_t my_rows = a.n > blockIdx.x ? (a.n - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-    const uint64_t total = my_rows * chunks_per_row;  // chunks this CTA will consume
+    const uint64_t total = my_rows * nsub;
+    const uint32_t m1 = (uint32_t)a.m - 1;
+    double* const ring = &S.tile[w][0][0];
+    uint64_t* const bars = &S.full_bar[w][0];
 
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < kStages; ++s) mbar_init(&full_bar[s], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-
-    auto issue = [&](uint64_t c) {  // producer: start the copy of this CTA's c-th chunk
-        const uint64_t local_row = c / chunks_per_row, ch = c - local_row * chunks_per_row;
+    auto issue = [&](uint64_t c) {  // lane 0: start this warp's c-th copy
+        const uint64_t local_row = c / nsub;
+        const uint32_t sub = (uint32_t)(c - local_row * nsub);
         const uint64_t i = blockIdx.x + local_row * gridDim.x;
         const uint64_t row = a.rows ? a.rows[i] : i;
-        const uint64_t g0 = ch * chunk;
-        const uint32_t genes = (uint32_t)((a.d - g0) < chunk ? (a.d - g0) : chunk);
+        const uint32_t g0 = g_begin + sub * kWarpStageGenes;
+        const uint32_t genes = min((uint32_t)kWarpStageGenes, g_end - g0);
         const int st = (int)(c % kStages);
-        mbar_expect_tx(&full_bar[st], genes * 8u);
-        tma_load_1d(ring + (size_t)st * kChunkGenes, a.x + row * a.d + g0, genes * 8u, &full_bar[st]);
+        mbar_expect_tx(&bars[st], genes * 8u);
+        tma_load_1d(ring + (size_t)st * kWarpStageGenes, a.x + row * a.d + g0, genes * 8u, &bars[st]);
     };
-
-    if (threadIdx.x == 0)
+    if (lane == 0)
         for (uint64_t c = 0; c < total && c < (uint64_t)kStages; ++c) issue(c);
 
     const uint64_t f0 = a.f_row0 + (a.f_row0_dev ? (uint64_t)*a.f_row0_dev : 0);
-    double acc = 0.0;
-    for (uint64_t c = 0; c < total; ++c) {
-        const uint64_t local_row = c / chunks_per_row, ch = c - local_row * chunks_per_row;
-        const int st = (int)(c % kStages);
-        mbar_wait(&full_bar[st], (uint32_t)((c / kStages) & 1));
-        const uint64_t g0 = ch * chunk;
-        const uint32_t genes = (uint32_t)((a.d - g0) < chunk ? (a.d - g0) : chunk);
-        const double2* tile = reinterpret_cast<const double2*>(ring + (size_t)st * kChunkGenes);
-        // canonical order: global vector index q = g0/2 + t, t = tid, tid+256, ...
-        for (uint32_t t = threadIdx.x; t < genes / 2; t += 256) {
-            const double2 v = tile[t];
-            const uint64_t j = g0 + 2ull * t;
-            if (j + 1 >= a.m) acc += dtlz_term<PID>(v.x); else s_pos[j] = v.x;
-            if (j + 2 >= a.m) acc += dtlz_term<PID>(v.y); else s_pos[j + 1] = v.y;
+    uint64_t c = 0;
+    for (uint64_t r = 0; r < my_rows; ++r) {
+        EvalRowSlot& slot = S.slot[r % kEvalSlots];
+        if (lane == 0)  // the slot is free once the row that used it kEvalSlots rows ago has been written out
+            while (*reinterpret_cast<volatile uint32_t*>(&slot.done) < (uint32_t)(r / kEvalSlots)) __nanosleep(100);
+        __syncwarp();
+        double acc = 0.0;
+        for (uint32_t sub = 0; sub < nsub; ++sub, ++c) {
+            const int st = (int)(c % kStages);
+            mbar_wait(&bars[st], (uint32_t)((c / kStages) & 1));
+            const uint32_t g0 = g_begin + sub * kWarpStageGenes;
+            const uint32_t genes = min((uint32_t)kWarpStageGenes, g_end - g0);
+            const double2* tile = reinterpret_cast<const double2*>(ring + (size_t)st * kWarpStageGenes);
+            // canonical order: this lane's vectors of the warp's blocks in ascending order
+            for (uint32_t t = lane; t < genes / 2; t += 32) {
+                const double2 v = tile[t];
+                const uint32_t j = g0 + 2 * t;
+                if (j >= m1) acc += dtlz_term<PID>(v.x); else slot.pos[j] = v.x;
+                if (j + 1 >= m1) acc += dtlz_term<PID>(v.y); else slot.pos[j + 1] = v.y;
+            }
+            __syncwarp();  // stage drained by the warp
+            if (lane == 0 && c + kStages < total) issue(c + kStages);
         }
-        __syncthreads();  // stage drained by everyone
-        if (threadIdx.x == 0 && c + kStages < total) issue(c + kStages);
-        if (ch + 1 == chunks_per_row) {  // row complete: leave {sum, position genes} for eval_finish_kernel
-            const double sum = block_sum<8>(acc, s_red);
-            const uint64_t i = blockIdx.x + local_row * gridDim.x;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+        uint32_t before = 0;
+        if (lane == 0) {
+            slot.part[w] = acc;
+            __threadfence_block();
+            before = atomicAdd(&slot.arrived, 1u);
+        }
+        before = __shfl_sync(0xffffffffu, before, 0);
+        if (before == 7) {  // row complete: leave {sum, position genes} for eval_finish_kernel
+            __threadfence_block();
+            const uint64_t i = blockIdx.x + r * gridDim.x;
             double* frow = a.f + (f0 + i) * a.m;
-            if (threadIdx.x == 0) frow[0] = sum;
-            if (threadIdx.x >= 1 && threadIdx.x < a.m) frow[threadIdx.x] = s_pos[threadIdx.x - 1];
-            acc = 0.0;
-            __syncthreads();  // s_pos / s_red free for the next row
+            if (lane == 0) {
+                const volatile double* part = slot.part;
+                double sum = part[0];
+#pragma unroll
+                for (int k = 1; k < 8; ++k) sum += part[k];
+                frow[0] = sum;
+            }
+            for (uint32_t o = lane + 1; o < a.m; o += 32) frow[o] = *reinterpret_cast<volatile double*>(&slot.pos[o - 1]);
+            __syncwarp();
+            if (lane == 0) {
+                slot.arrived = 0;
+                __threadfence_block();
+                *reinterpret_cast<volatile uint32_t*>(&slot.done) = (uint32_t)(r / kEvalSlots) + 1;
+            }
         }
     }
 }
@@ -285,13 +334,13 @@ template <int PID>
 void launch_dtlz(const EvalK& k, bool tma, cudaStream_t s) {
     const int vec = row_vec(k.d), block = row_block(k.d);
     if (tma && eval_tma_enabled() && vec == 2 && block == 256) {
-        const size_t smem = (size_t)kStages * kChunkGenes * sizeof(double);
+        const size_t smem = sizeof(EvalTmaSmem);
         static bool configured = false;
         if (!configured) {
             TEMO_CUDA(cudaFuncSetAttribute(eval_tma_kernel<PID>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             configured = true;
         }
-        uint64_t grid = (uint64_t)kSMs * 2;
+        uint64_t grid = (uint64_t)kSMs * TEMO_EVAL_CTAS;
         if (grid > k.n) grid = k.n;
         eval_tma_kernel<PID><<<(unsigned)grid, 256, smem, s>>>(k);
         eval_finish_kernel<PID><<<(unsigned)((k.n + 127) / 128), 128, 0, s>>>(k.f, k.n, k.m, k.d, k.f_row0, k.f_row0_dev);
@@ -370,11 +419,7 @@ void launch_evaluate(const EvalArgs& a, cudaStream_t s) {
     require(a.d >= a.m, "dtlz_eval: d must be at least m");                              // problems.hpp:72
     require(a.m <= (uint64_t)kMaxObj, "evaluate: more than 32 objectives are not supported");
     if (a.n == 0) return;
-    // split a row into equal stages: ceil(d / 4096) chunks, each rounded up to a multiple of 512 genes
-    const uint64_t nchunks = (a.d + kChunkGenes - 1) / kChunkGenes;
-    uint64_t chunk = ((a.d + nchunks - 1) / nchunks + 511) / 512 * 512;
-    if (chunk > (uint64_t)kChunkGenes) chunk = kChunkGenes;
-    EvalK k{a.x, a.rows, a.n, a.d, a.m, a.f, a.f_row0, a.f_row0_dev, (uint32_t)chunk};
+    EvalK k{a.x, a.rows, a.n, a.d, a.m, a.f, a.f_row0, a.f_row0_dev};
     switch (a.problem) {
     case kDtlz1: launch_dtlz<kDtlz1>(k, a.allow_tma, s); break;
     case kDtlz2: launch_dtlz<kDtlz2>(k, a.allow_tma, s); break;

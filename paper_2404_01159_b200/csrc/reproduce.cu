@@ -164,9 +164,11 @@ __device__ __forceinline__ void reproduce_unit(const ReproK& a, const uint64_t u
 
     double acc_a = 0.0, acc_b = 0.0;
     const uint32_t nvec = (uint32_t)(a.d / VEC);
-    const uint32_t nvec_ceil = (nvec + blockDim.x - 1) / blockDim.x * blockDim.x;
+    // canonical row mapping (common.cuh): this warp's consecutive blocks
+    const uint32_t cblk = canon_chunk_blocks((nvec + 31) >> 5, blockDim.x >> 5), q_first = (uint32_t)warp * cblk * 32 + lane;
 
-    for (uint32_t q = threadIdx.x; q < nvec_ceil; q += blockDim.x) {  // whole warps stay in the loop
+    for (uint32_t it = 0; it < cblk; ++it) {  // whole warps stay in the loop
+        const uint32_t q = q_first + it * 32;
         const bool in_range = q < nvec;
         const uint32_t j0 = q * VEC;
         double xa[VEC], xb[VEC];
@@ -560,12 +562,12 @@ __device__ __forceinline__ void accumulate_vector(uint32_t j0, uint32_t m1, doub
 // Pass B of a tile with the general pow (base 0, or an exponent outside the narrow path's range): same list, same stores.
 template <int MODE>
 __device__ __noinline__ void pass_b_general(const ReproK& a, uint64_t pos_tile, uint32_t total, uint32_t sm_w, uint32_t lane,
-                                            uint32_t stride) {
+                                            uint32_t) {
     constexpr uint64_t SG = MODE == 0 ? kGolden : 1ULL;
     constexpr uint32_t kOffList = offsetof(WarpSmem, list);
     for (uint32_t t = lane; t < total; t += 32) {
         const uint32_t e = lds_u16(sm_w + kOffList + 2 * t);
-        const uint32_t j = e + (e >> 6) * (stride * 64 - 64);
+        const uint32_t j = e;
         const SpreadIn s = spread_inputs<MODE>(a.rng.seed, pos_tile + (uint64_t)j * SG, a.dl_r1, a.inv_exp);
         const double p = pow_spread_slow(s.base, s.yexp);
         sts_f64(sm_w + 8 * e, s.up ? p : -p);
@@ -597,7 +599,7 @@ __device__ __noinline__ void tile_plain(const ReproK& a, uint32_t blk0, uint32_t
     const PowTables T = pow_tables_global();
     double acc_a = acc[0], acc_b = acc[1];
     for (uint32_t k = 0; k < kmax; ++k) {
-        const uint32_t q = (blk0 + v + k * stride) * 32 + lane;
+        const uint32_t q = (blk0 + v + k) * 32 + lane;
         if (q >= nvec) break;
         double xa[2], xb[2], lo[2], hi[2], ca[2], cb[2];
         const double2 va = reinterpret_cast<const double2*>(c.pa)[q], vb = reinterpret_cast<const double2*>(c.pb)[q];
@@ -625,14 +627,13 @@ __device__ __noinline__ void tile_plain(const ReproK& a, uint32_t blk0, uint32_t
 // pairs on its own and walks the row's blocks consecutively (a row of d = 1000 is 16 blocks: two per warp of a team, and the
 // per-pair and per-tile work of eight warps for them; one warp makes a ten- and a six-block tile of it). Without the fused
 // sums only: their canonical order is that of the eight-warp mapping.
-template <int MODE, int EVAL, int SEG, int TEAM, int STRIDE>  // SEG: 0 bound arrays, 1 one constant segment, 2 two constant segments
+template <int MODE, int EVAL, int SEG, int TEAM>  // SEG: 0 bound arrays, 1 one constant segment, 2 two constant segments
 __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reproduce_pairs_kernel(const __grid_constant__ ReproK a) {
-    static_assert((TEAM == kVirtWarps && STRIDE == kVirtWarps) || (TEAM == 1 && (STRIDE == kVirtWarps || (STRIDE == 1 && EVAL == 0))),
-                  "consecutive blocks carry no fused sums");
+    static_assert(TEAM == kVirtWarps || TEAM == 1, "a pair belongs to a team of eight warps or to one warp");
     extern __shared__ __align__(16) unsigned char pair_smem_raw[];
     PairSmem& S = *reinterpret_cast<PairSmem*>(pair_smem_raw);
-    constexpr uint32_t kStride = STRIDE;                           // distance of a warp's consecutive blocks
-    constexpr uint32_t kVPerWarp = TEAM == 1 && STRIDE == kVirtWarps ? kVirtWarps : 1;  // virtual warps a warp walks through
+    constexpr uint32_t kStride = 1;                                // a warp's blocks are consecutive
+    constexpr uint32_t kVPerWarp = TEAM == 1 && EVAL != 0 ? kVirtWarps : 1;  // virtual warps a warp walks through
     constexpr uint64_t SG = MODE == 0 ? kGolden : 1ULL;            // stream distance of neighbouring genes
     constexpr uint64_t STEP = SG * (uint64_t)(kStride * 64);       // ... of a lane's consecutive blocks
     constexpr uint32_t kOffList = offsetof(WarpSmem, list), kOffSide = offsetof(WarpSmem, side);
@@ -655,6 +656,8 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
     const uint64_t seed = a.rng.seed;
     const uint32_t nvec = (uint32_t)(a.d >> 1);
     const uint32_t nblk = (nvec + 31) >> 5;  // 64-gene blocks in a row
+    // blocks per virtual warp of the canonical row mapping (internal.h); one warp without fused sums takes the row in one go
+    const uint32_t cblk = TEAM == 1 && EVAL == 0 ? nblk : canon_chunk_blocks(nblk, kVirtWarps);
     uint32_t lt;  // lanes below this one (kept in a register: an asm volatile result cannot be rematerialised in the loops)
     asm volatile("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
     const uint32_t top_thr = a.mask_never ? 0u : ((a.mask_top << 11) | 0x7ffu);  // (top >> 11) <= mask_top
@@ -678,15 +681,14 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
         for (uint32_t vv = 0; vv < kVPerWarp; ++vv) {
         const uint32_t v = TEAM == 1 ? vv : warp;
         double acc_a = 0.0, acc_b = 0.0;
-        for (uint32_t blk0 = 0; blk0 < nblk; blk0 += kStride * kPairBlocks) {
-            // blocks v, v + 8, ... of this row tile (warp-uniform count)
-            const uint32_t left = nblk - blk0 > v ? (nblk - blk0 - v + kStride - 1) / kStride : 0u;
-            const uint32_t kmax = opaque(min(left, (uint32_t)kPairBlocks));
-            if (kmax == 0) break;
-            const uint32_t q_first = (blk0 + v) * 32 + lane;  // this lane's vector in the tile's first block
+        // virtual warp v owns the blocks [v * cblk, (v + 1) * cblk) of the row: a tile is up to kPairBlocks of them
+        const uint32_t blk_end = min(nblk, (v + 1) * cblk);
+        for (uint32_t blk0 = v * cblk; blk0 < blk_end; blk0 += kPairBlocks) {
+            const uint32_t kmax = opaque(min(blk_end - blk0, (uint32_t)kPairBlocks));
+            const uint32_t q_first = blk0 * 32 + lane;  // this lane's vector in the tile's first block
             const uint64_t pos = C.pos;
             {   // this warp's parent blocks of this tile into L2 (they are read in pass C)
-                const uint32_t kk = lane & 15, blk = blk0 + v + kk * kStride;
+                const uint32_t kk = lane & 15, blk = blk0 + kk;
                 if (kk < kmax && blk < nblk) {
                     const char* p = reinterpret_cast<const char*>(lane < 16 ? C.pa : C.pb) + (uint64_t)blk * 512;
 #pragma unroll
@@ -733,14 +735,14 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
             __syncwarp();
             if (ncand > (uint32_t)a.cand_cap) {  // practically never: the literal formulation of this tile
                 double acc[2] = {acc_a, acc_b};
-                tile_plain<MODE, EVAL>(a, blk0, v, kmax, acc, &C, slot.pos, kStride);
+                tile_plain<MODE, EVAL>(a, blk0, 0, kmax, acc, &C, slot.pos, kStride);
                 acc_a = acc[0], acc_b = acc[1];
                 __syncwarp();
                 continue;
             }
             // ---- pass B: signed spread factor of the crossing genes, 64 at a time
             {
-                const uint64_t pos_tile = pos + (uint64_t)((blk0 + v) * 64) * SG;  // gene (blk0 + v) * 64
+                const uint64_t pos_tile = pos + (uint64_t)(blk0 * 64) * SG;  // gene blk0 * 64
                 // Anything off the common path (a base of exactly 0, a result within 2^-54 of 1, an exponent outside the narrow
                 // range) only raises `redo`: the general routine then recomputes the tile's list after the loop, so the loop
                 // itself carries no call, no fallback selects and no per-iteration look at the launch constants.
@@ -750,7 +752,7 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
                     const bool two = t + 32 < total;
                     const uint32_t e0 = lds_u16(sm_w + kOffList + 2 * t), e1 = two ? lds_u16(sm_w + kOffList + 2 * t + 64) : e0;
                     // gene index relative to the tile's first gene
-                    const uint32_t j0 = e0 + (e0 >> 6) * (kStride * 64 - 64), j1 = e1 + (e1 >> 6) * (kStride * 64 - 64);
+                    const uint32_t j0 = e0, j1 = e1;
                     const uint64_t at0 = pos_tile + (uint64_t)j0 * SG, at1 = pos_tile + (uint64_t)j1 * SG;
                     const double mc0 = word_to_unit(draw_full<MODE>(seed, at0)), mc1 = word_to_unit(draw_full<MODE>(seed, at1));
                     const uint32_t r10 = draw_top<MODE>(seed, at0 + a.dl_r1), r11 = draw_top<MODE>(seed, at1 + a.dl_r1);
@@ -776,7 +778,7 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
 #pragma unroll 1
             for (uint32_t t = lane; t < ncand; t += 32) {
                 const uint32_t entry = W.cand[t], e = entry & 0x1fffu;
-                const uint32_t j = (blk0 + v) * 64 + e + (e >> 6) * (kStride * 64 - 64);
+                const uint32_t j = blk0 * 64 + e;
                 const uint64_t at = pos + (uint64_t)j * SG;
                 const double2 ch = mutated_children<MODE>(seed, at + a.dl_mask_a, at + a.dl_mask_b, a.dl_mut_a - a.dl_mask_a,
                                                           a.mask_thresh, a.xi, (entry & 0x2000u) != 0, (entry & 0x4000u) != 0,
@@ -794,7 +796,7 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
                 const double2* __restrict__ hi2 = reinterpret_cast<const double2*>(a.upper);
                 // piecewise-constant bounds from the launch constants (SEG): one side of the split for the whole tile,
                 // unless the tile's blocks straddle it
-                const uint32_t tile_g0 = (blk0 + v) * 64, tile_g1 = (blk0 + v + (kmax - 1) * kStride) * 64 + 64;
+                const uint32_t tile_g0 = blk0 * 64, tile_g1 = (blk0 + kmax) * 64;
                 const bool seg_hi_side = tile_g0 >= a.seg_split, seg_mixed = SEG != 0 && !seg_hi_side && tile_g1 > a.seg_split;
                 const double seg_lo = a.seg_lo[seg_hi_side ? 1 : 0], seg_hi = a.seg_hi[seg_hi_side ? 1 : 0];
                 const double2* __restrict__ pa2 = reinterpret_cast<const double2*>(C.pa);
@@ -994,11 +996,11 @@ inline uint32_t* next_work_counter() {
     return counters + (next.fetch_add(1) % kCounters);
 }
 
-template <int MODE, int EVAL, int SEG, int TEAM = kVirtWarps, int STRIDE = kVirtWarps>
+template <int MODE, int EVAL, int SEG, int TEAM = kVirtWarps>
 void launch_pairs_seg(const ReproK& k, uint64_t units, cudaStream_t s) {
     static int grid = 0;  // per instantiation
     if (grid == 0) {
-        TEMO_CUDA(cudaFuncSetAttribute(reproduce_pairs_kernel<MODE, EVAL, SEG, TEAM, STRIDE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        TEMO_CUDA(cudaFuncSetAttribute(reproduce_pairs_kernel<MODE, EVAL, SEG, TEAM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)sizeof(PairSmem)));
         int dev = 0, sms = 0;
         TEMO_CUDA(cudaGetDevice(&dev));
@@ -1014,27 +1016,17 @@ void launch_pairs_seg(const ReproK& k, uint64_t units, cudaStream_t s) {
         TEMO_CUDA(cudaMemsetAsync(kk.work_counter, 0, sizeof(uint32_t), s));
     }
     const uint64_t teams_per_cta = TEAM == 1 ? kVirtWarps : 1;
-    reproduce_pairs_kernel<MODE, EVAL, SEG, TEAM, STRIDE>
+    reproduce_pairs_kernel<MODE, EVAL, SEG, TEAM>
         <<<(unsigned)std::min<uint64_t>((units + teams_per_cta - 1) / teams_per_cta, (uint64_t)grid), kVirtWarps * 32, sizeof(PairSmem), s>>>(kk);
 }
 
 template <int MODE, int EVAL>
 void launch_pairs_eval(const ReproK& k, uint64_t units, int seg, int team, cudaStream_t s) {
-    if constexpr (EVAL == 0) {
-        if (team == 1) {  // one warp per pair, consecutive blocks
-            switch (seg) {
-            case 1: launch_pairs_seg<MODE, 0, 1, 1, 1>(k, units, s); break;
-            case 2: launch_pairs_seg<MODE, 0, 2, 1, 1>(k, units, s); break;
-            default: launch_pairs_seg<MODE, 0, 0, 1, 1>(k, units, s); break;
-            }
-            return;
-        }
-    }
-    if (team == -1) {  // one warp per pair, walking through the eight virtual warps of the canonical mapping
+    if (team == 1) {  // one warp per pair
         switch (seg) {
-        case 1: launch_pairs_seg<MODE, EVAL, 1, 1, kVirtWarps>(k, units, s); break;
-        case 2: launch_pairs_seg<MODE, EVAL, 2, 1, kVirtWarps>(k, units, s); break;
-        default: launch_pairs_seg<MODE, EVAL, 0, 1, kVirtWarps>(k, units, s); break;
+        case 1: launch_pairs_seg<MODE, EVAL, 1, 1>(k, units, s); break;
+        case 2: launch_pairs_seg<MODE, EVAL, 2, 1>(k, units, s); break;
+        default: launch_pairs_seg<MODE, EVAL, 0, 1>(k, units, s); break;
         }
         return;
     }
@@ -1207,11 +1199,11 @@ void launch_reproduce(const ReproArgs& a, cudaStream_t s) {
     const uint64_t pairs_launched = std::min(unit_hi, k.half) > unit_lo ? std::min(unit_hi, k.half) - unit_lo : 0;
     const bool enough_pairs = pairs_launched >= (uint64_t)kSMs * TEMO_PAIR_MIN_BLOCKS * kVirtWarps;
     const int sw = k1_options().single_warp;
-    const bool single_warp = a.eval_problem == 0 && (sw == 1 || (sw < 0 && enough_pairs));
-    const int team = single_warp ? 1 : (sw == 2 || (sw < 0 && enough_pairs) ? -1 : kVirtWarps);  // -1: one warp per pair walking the eight virtual warps
+    const bool single_warp = sw > 0 || (sw < 0 && enough_pairs);
+    const int team = single_warp ? 1 : kVirtWarps;
     // expected mutation candidates per warp tile (the tile's slots overflow into its literal formulation: P(more than 8) is
     // 2e-4 at an expectation of 2, the most a single warp's tile of consecutive blocks can see at pm = 1)
-    const double cand_per_warp = 2.0 * (double)std::min<uint64_t>(single_warp ? a.d : a.d / kVirtWarps, kTileGenes) * cand_rate;
+    const double cand_per_warp = 2.0 * (double)std::min<uint64_t>(single_warp && a.eval_problem == 0 ? a.d : (a.d + kVirtWarps - 1) / kVirtWarps + 64, kTileGenes) * cand_rate;
     const double cand_limit = single_warp ? 2.1 : 1.0;
     k.cand_cap = pair_cand_cap();
     uint64_t next = unit_lo;  // first unit not yet launched
