@@ -219,8 +219,8 @@ __global__ void __launch_bounds__(256) eval_tma_kernel(const EvalK a) {
 // y_j = (1 + (j + 1) / d) x_j - 10 x_0 over the tail genes, g_i = mean of y^2 over group i (m consecutive groups of
 // nk * sublen_i tail genes), objectives like DTLZ1's linear front without the 0.5. The linkage coefficients come from
 // a table (lsmop1_coef: one correctly rounded division per gene, done once per d on the host). Reduction order = the
-// canonical one of this library, per group: thread t owns the vectors t, t + B, ... of the row and adds its genes of a
-// group in ascending order; xor butterfly inside a warp; warp totals in ascending order.
+// canonical one of this library (common.cuh), per group: a lane adds its genes of a group in ascending order; xor
+// butterfly inside a warp; warp totals in ascending order.
 // Measured at n = 2^17, d = 5000 (round 2): 1.19 ms = 4.4 TB/s (the round-1 kernel with scalar loads and a division per
 // gene: 1.66 ms). Two alternatives were built, verified bit-identical and dropped: the same sums through the
 // cp.async.bulk ring of eval_tma_kernel (2.9 ms: m block reductions and ten CTA barriers per 40 KB row), and the sums
@@ -245,7 +245,10 @@ __global__ void __launch_bounds__(256) eval_lsmop1_kernel(const EvalK a, const L
     uint32_t cur = 0;
     double acc = 0.0;
     const uint32_t nvec = (uint32_t)(a.d / VEC);
-    for (uint32_t q = threadIdx.x; q < nvec; q += B) {
+    const uint32_t cblk = canon_chunk_blocks((nvec + 31) >> 5, B >> 5), q_first = (threadIdx.x >> 5) * cblk * 32 + (threadIdx.x & 31);
+    for (uint32_t it = 0; it < cblk; ++it) {  // canonical mapping: this warp's consecutive blocks
+        const uint32_t q = q_first + it * 32;
+        if (q >= nvec) break;
         double xv[VEC], cv[VEC];
         if (VEC == 2) {
             const double2 t = *reinterpret_cast<const double2*>(p + 2 * (uint64_t)q);
@@ -284,6 +287,198 @@ __global__ void __launch_bounds__(256) eval_lsmop1_kernel(const EvalK a, const L
         if (o > 0) v *= 1.0 - p[a.m - 1 - o];
         frow[o] = v;
     }
+}
+
+// LSMOP1 through per-warp bulk-copy rings (the structure of eval_tma_kernel) for rows of up to 8 x 640 genes: a warp's
+// blocks of a row are the same genes in every row, so the group of each of a lane's twenty genes is decided once per
+// launch (one bit mask per group the warp touches: the inner loop is branch-free, one predicated add per candidate
+// group), and the lane's linkage coefficients stay in registers. x_0 of the next row (it scales the linkage term) is fetched a row ahead. The last warp to deliver
+// its group totals adds them in ascending warp order (warps that do not touch a group deliver 0.0, like the idle
+// threads of the plain kernel) and writes the objectives. Same bits as the plain kernel. Needs at most kLsmopTouch
+// groups per warp (lsmop_tma_touch); everything else goes through the plain kernel.
+constexpr int kLsmopTouch = 4;
+constexpr int kLsmopVecs = kWarpStageGenes / 64;  // vectors per lane and row
+struct LsmopRowSlot {
+    double part[kMaxObj][8];  // per-group, per-warp totals
+    double pos[kMaxObj];
+    uint32_t arrived, done;
+};
+struct LsmopTmaSmem {
+    double tile[8][kStages][kWarpStageGenes];
+    uint64_t full_bar[8][kStages];
+    LsmopRowSlot slot[kEvalSlots];
+    uint32_t end[kMaxObj + 1];
+};
+
+template <int TOUCH>  // accumulators per lane = groups a warp's genes may touch (2 or kLsmopTouch)
+__global__ void __launch_bounds__(256) eval_lsmop1_tma_kernel(const EvalK a, const LsmopLayout lay, const double* __restrict__ coef) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    LsmopTmaSmem& S = *reinterpret_cast<LsmopTmaSmem*>(smem_raw);
+    const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const uint32_t m = (uint32_t)a.m, m1 = m - 1;
+
+    if (threadIdx.x < 8 * kStages) mbar_init(&S.full_bar[threadIdx.x / kStages][threadIdx.x % kStages], 1);
+    if (threadIdx.x < kEvalSlots) S.slot[threadIdx.x].arrived = S.slot[threadIdx.x].done = 0;
+    if (threadIdx.x < m) S.end[threadIdx.x] = m1 + lay.start[threadIdx.x + 1];  // first gene after the group
+    if (threadIdx.x == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncthreads();  // the only one
+
+    const uint32_t nvec = (uint32_t)(a.d >> 1), nblk = (nvec + 31) >> 5, cblk = canon_chunk_blocks(nblk, 8);
+    const uint32_t g_begin = min(w * cblk * 64u, (uint32_t)a.d), g_end = min((w + 1) * cblk * 64u, (uint32_t)a.d);
+    const uint32_t genes = g_end - g_begin;  // <= kWarpStageGenes; 0: nothing of the row is ours
+    const uint64_t my_rows = a.n > blockIdx.x ? (a.n - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    const uint64_t total = genes ? my_rows : 0;
+    double* const ring = &S.tile[w][0][0];
+    uint64_t* const bars = &S.full_bar[w][0];
+    auto group_of = [&](uint32_t j) {  // first group whose end lies beyond gene j (m: beyond the last group)
+        uint32_t g = 0;
+        while (g < m && j >= S.end[g]) ++g;
+        return g;
+    };
+    const uint32_t grp_lo = group_of(max(g_begin, m1)), grp_hi = genes ? min(group_of(g_end - 1) + 1, m) : grp_lo;
+    // this lane's genes: coefficients, and for each accumulator (= group among the groups of this warp) the genes that go
+    // into it (bit 2k + v: gene v of the lane's k-th vector); position genes, genes beyond the last group and vectors
+    // beyond the row are in no mask
+    double2 cf[kLsmopVecs];
+    uint32_t in_group[TOUCH];
+#pragma unroll
+    for (int i = 0; i < TOUCH; ++i) in_group[i] = 0;
+    {
+        uint32_t cur = group_of(max(g_begin + 2 * lane, m1));
+#pragma unroll
+        for (int k = 0; k < kLsmopVecs; ++k) {
+            const uint32_t t = lane + 32 * k, j = g_begin + 2 * t;
+            const bool valid = t < genes / 2;
+            cf[k] = valid ? __ldg(reinterpret_cast<const double2*>(coef) + (j >> 1)) : make_double2(0.0, 0.0);
+#pragma unroll
+            for (int v = 0; v < 2; ++v) {
+                const uint32_t jj = j + v;
+                if (valid && jj >= m1) {
+                    while (cur < m && jj >= S.end[cur]) ++cur;
+#pragma unroll
+                    for (int i = 0; i < TOUCH; ++i)
+                        if (cur < m && cur - grp_lo == (uint32_t)i) in_group[i] |= 1u << (2 * k + v);
+                }
+            }
+        }
+    }
+    const uint32_t ntouch = grp_hi - grp_lo;  // <= TOUCH
+    const bool has_pos = g_begin == 0 && 2 * lane < m1;  // this lane's first vector holds position genes
+
+    auto row_of = [&](uint64_t r) {
+        const uint64_t i = blockIdx.x + r * gridDim.x;
+        return a.rows ? (uint64_t)a.rows[i] : i;
+    };
+    auto issue = [&](uint64_t c) {  // lane 0: start the copy of this warp's genes of its c-th row
+        const int st = (int)(c % kStages);
+        mbar_expect_tx(&bars[st], genes * 8u);
+        tma_load_1d(ring + (size_t)st * kWarpStageGenes, a.x + row_of(c) * a.d + g_begin, genes * 8u, &bars[st]);
+    };
+    if (lane == 0)
+        for (uint64_t c = 0; c < total && c < (uint64_t)kStages; ++c) issue(c);
+
+    const uint64_t f0 = a.f_row0 + (a.f_row0_dev ? (uint64_t)*a.f_row0_dev : 0);
+    double x0_next = my_rows ? a.x[row_of(0) * a.d] : 0.0;
+    for (uint64_t r = 0; r < my_rows; ++r) {
+        LsmopRowSlot& slot = S.slot[r % kEvalSlots];
+        const double t0 = 10.0 * x0_next;
+        if (r + 1 < my_rows) x0_next = a.x[row_of(r + 1) * a.d];
+        if (lane == 0)
+            while (*reinterpret_cast<volatile uint32_t*>(&slot.done) < (uint32_t)(r / kEvalSlots)) __nanosleep(100);
+        __syncwarp();
+        double acc[TOUCH];
+#pragma unroll
+        for (int i = 0; i < TOUCH; ++i) acc[i] = 0.0;
+        if (genes) {
+            const int st = (int)(r % kStages);
+            mbar_wait(&bars[st], (uint32_t)((r / kStages) & 1));
+            const double2* tile = reinterpret_cast<const double2*>(ring + (size_t)st * kWarpStageGenes);
+            if (has_pos) {
+                const double2 xv = tile[lane];
+                slot.pos[2 * lane] = xv.x;
+                if (2 * lane + 1 < m1) slot.pos[2 * lane + 1] = xv.y;
+            }
+            // branch-free: a predicated add per accumulator (a plain `if` becomes a jump table); a vector beyond the row reads
+            // stale shared memory and is in no mask
+#pragma unroll
+            for (int k = 0; k < kLsmopVecs; ++k) {
+                const double2 xv = tile[lane + 32 * k];
+#pragma unroll
+                for (int v = 0; v < 2; ++v) {
+                    const double y = (v ? cf[k].y : cf[k].x) * (v ? xv.y : xv.x) - t0;
+                    const double yy = y * y;
+#pragma unroll
+                    for (int i = 0; i < TOUCH; ++i)
+                        asm("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\tand.b32 t, %1, %2;\n\tsetp.ne.u32 p, t, 0;\n\t@p add.rn.f64 %0, %0, %3;\n\t}"
+                            : "+d"(acc[i])
+                            : "r"(in_group[i]), "r"(1u << (2 * k + v)), "d"(yy));
+                }
+            }
+            __syncwarp();  // stage drained by the warp
+            if (lane == 0 && r + kStages < total) issue(r + kStages);
+        }
+        // the warp's total of every group it touches (xor butterfly), 0.0 for the others
+        double mine = 0.0;  // lane g keeps the total of group g
+#pragma unroll
+        for (int i = 0; i < TOUCH; ++i) {
+            if ((uint32_t)i < ntouch) {  // warp-uniform
+                double v = acc[i];
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+                if (lane == grp_lo + i) mine = v;
+            }
+        }
+        if (lane < m) slot.part[lane][w] = mine;
+        __syncwarp();
+        uint32_t before = 0;
+        if (lane == 0) {
+            __threadfence_block();
+            before = atomicAdd(&slot.arrived, 1u);
+        }
+        before = __shfl_sync(0xffffffffu, before, 0);
+        if (before == 7) {  // row complete
+            __threadfence_block();
+            const uint64_t i = blockIdx.x + r * gridDim.x;
+            double* frow = a.f + (f0 + i) * a.m;
+            if (lane < m) {
+                const volatile double* part = slot.part[lane];
+                double sum = part[0];
+#pragma unroll
+                for (int k = 1; k < 8; ++k) sum += part[k];
+                const double gval = lay.sublen[lane] ? sum / (double)lay.sublen[lane] / (double)kLsmopNk : 0.0;
+                const volatile double* pos = slot.pos;
+                double v = 1.0 + gval;
+                for (uint32_t k = 0; k + lane + 1 < m; ++k) v *= pos[k];
+                if (lane > 0) v *= 1.0 - pos[m - 1 - lane];
+                frow[lane] = v;
+            }
+            __syncwarp();
+            if (lane == 0) {
+                slot.arrived = 0;
+                __threadfence_block();
+                *reinterpret_cast<volatile uint32_t*>(&slot.done) = (uint32_t)(r / kEvalSlots) + 1;
+            }
+        }
+    }
+}
+
+// the conditions of eval_lsmop1_tma_kernel: 0 if they do not hold, else the most groups a warp's genes touch
+int lsmop_tma_touch(const LsmopLayout& lay, uint64_t d, uint64_t m) {
+    const uint32_t nvec = (uint32_t)(d >> 1), nblk = (nvec + 31) >> 5, cblk = canon_chunk_blocks(nblk, 8), m1 = (uint32_t)m - 1;
+    if (cblk * 64u > (uint32_t)kWarpStageGenes) return 0;
+    uint32_t touch = 1;
+    for (uint32_t w = 0; w < 8; ++w) {
+        const uint32_t g_begin = std::min<uint32_t>(w * cblk * 64u, (uint32_t)d), g_end = std::min<uint32_t>((w + 1) * cblk * 64u, (uint32_t)d);
+        if (g_end <= g_begin) continue;
+        auto group_of = [&](uint32_t j) {
+            uint32_t g = 0;
+            while (g < m && j >= m1 + lay.start[g + 1]) ++g;
+            return g;
+        };
+        const uint32_t lo = group_of(std::max(g_begin, m1)), hi = std::min<uint32_t>(group_of(g_end - 1) + 1, (uint32_t)m);
+        if (hi > lo) touch = std::max(touch, hi - lo);
+    }
+    return touch <= (uint32_t)kLsmopTouch ? (int)touch : 0;
 }
 
 // Second half of the TMA path: the streaming kernel leaves {tail sum, position genes} in each objective
@@ -429,7 +624,31 @@ void launch_evaluate(const EvalArgs& a, cudaStream_t s) {
         const int block = row_block(a.d);
         const size_t smem = (size_t)a.m * block * sizeof(double);
         const double* coef = lsmop1_coef(a.d, s);
-        if (row_vec(a.d) == 2)
+        const LsmopLayout lay = lsmop1_layout(a.d, a.m);
+        const int touch = a.allow_tma && eval_tma_enabled() && row_vec(a.d) == 2 && block == 256 ? lsmop_tma_touch(lay, a.d, a.m) : 0;
+        if (touch) {
+            static bool configured = false;
+            if (!configured) {
+                TEMO_CUDA(cudaFuncSetAttribute(eval_lsmop1_tma_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LsmopTmaSmem)));
+                TEMO_CUDA(cudaFuncSetAttribute(eval_lsmop1_tma_kernel<kLsmopTouch>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LsmopTmaSmem)));
+                configured = true;
+            }
+            const uint64_t grid = std::min<uint64_t>((uint64_t)kSMs * TEMO_EVAL_CTAS, a.n);
+            if (touch <= 2)
+                eval_lsmop1_tma_kernel<2><<<(unsigned)grid, 256, sizeof(LsmopTmaSmem), s>>>(k, lay, coef);
+            else
+                eval_lsmop1_tma_kernel<kLsmopTouch><<<(unsigned)grid, 256, sizeof(LsmopTmaSmem), s>>>(k, lay, coef);
+        } else if (smem > 48 * 1024 && ([&] {  // m x block partials beyond the default dynamic shared memory (m > 24)
+                       static bool configured = false;
+                       if (!configured) {
+                           const int most = kMaxObj * 256 * (int)sizeof(double);
+                           TEMO_CUDA(cudaFuncSetAttribute(eval_lsmop1_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, most));
+                           TEMO_CUDA(cudaFuncSetAttribute(eval_lsmop1_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, most));
+                           configured = true;
+                       }
+                       return false;
+                   })()) {
+        } else if (row_vec(a.d) == 2)
             eval_lsmop1_kernel<2><<<(unsigned)a.n, block, smem, s>>>(k, lsmop1_layout(a.d, a.m), coef);
         else
             eval_lsmop1_kernel<1><<<(unsigned)a.n, block, smem, s>>>(k, lsmop1_layout(a.d, a.m), coef);
