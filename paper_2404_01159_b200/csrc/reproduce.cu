@@ -371,7 +371,6 @@ struct WarpSmem {
 };
 struct PairSlot {
     double part[2][kVirtWarps];  // per-warp totals of the two children
-    double pos[2][kMaxObj];      // position genes of the two children
     uint32_t arrived;            // warps that have delivered their partials
     uint32_t done;               // pairs completed through this slot
 };
@@ -537,25 +536,19 @@ __device__ __forceinline__ uint32_t lds_u16(uint32_t addr) {
 }
 __device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 
+// Fused evaluation terms of one vector (two genes of both children); the position genes (the first m - 1 of a row) carry
+// no term - they are read back from the children's rows when the objective rows are written.
 template <int EVAL>
 __device__ __forceinline__ void accumulate_vector(uint32_t j0, uint32_t m1, double ca0, double cb0, double ca1, double cb1,
-                                                  double& acc_a, double& acc_b, double (*pos)[kMaxObj]) {
+                                                  double& acc_a, double& acc_b) {
     if (EVAL == 0) return;
-    if (j0 >= m1) {
-        acc_a += dtlz_term<EVAL>(ca0);
-        acc_b += dtlz_term<EVAL>(cb0);
+    if (j0 + 1 >= m1) {
+        if (j0 >= m1) {
+            acc_a += dtlz_term<EVAL>(ca0);
+            acc_b += dtlz_term<EVAL>(cb0);
+        }
         acc_a += dtlz_term<EVAL>(ca1);
         acc_b += dtlz_term<EVAL>(cb1);
-    } else {  // the vector holds a position gene (first block of the row only)
-        pos[0][j0] = ca0;
-        pos[1][j0] = cb0;
-        if (j0 + 1 >= m1) {
-            acc_a += dtlz_term<EVAL>(ca1);
-            acc_b += dtlz_term<EVAL>(cb1);
-        } else {
-            pos[0][j0 + 1] = ca1;
-            pos[1][j0 + 1] = cb1;
-        }
     }
 }
 
@@ -589,8 +582,7 @@ __device__ __forceinline__ void fill_pair_ctx(PairCtx& c, const ReproK& a, uint6
 // The literal per-gene formulation of one warp tile (blocks v + 8k of the row tile starting at blk0): used when
 // the candidate slots of the phased passes overflow. Same bits, same accumulation order.
 template <int MODE, int EVAL>
-__device__ __noinline__ void tile_plain(const ReproK& a, uint32_t blk0, uint32_t v, uint32_t kmax, double* acc, const PairCtx* ctx,
-                                        double (*pos)[kMaxObj], uint32_t stride) {
+__device__ __noinline__ void tile_plain(const ReproK& a, uint32_t blk0, uint32_t v, uint32_t kmax, double* acc, const PairCtx* ctx) {
     const PairCtx c = *ctx;
     constexpr uint64_t SG = MODE == 0 ? kGolden : 1ULL;
     const uint32_t lane = threadIdx.x & 31;
@@ -616,7 +608,7 @@ __device__ __noinline__ void tile_plain(const ReproK& a, uint32_t blk0, uint32_t
                                                       a.mask_thresh, a.xi, hit_a, hit_b, xa[g], xb[g], beta, lo[g], hi[g]);
             ca[g] = ch.x, cb[g] = ch.y;
         }
-        accumulate_vector<EVAL>(2 * q, m1, ca[0], cb[0], ca[1], cb[1], acc_a, acc_b, pos);
+        accumulate_vector<EVAL>(2 * q, m1, ca[0], cb[0], ca[1], cb[1], acc_a, acc_b);
         reinterpret_cast<double2*>(c.oa)[q] = make_double2(ca[0], ca[1]);
         reinterpret_cast<double2*>(c.ob)[q] = make_double2(cb[0], cb[1]);
     }
@@ -735,7 +727,7 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
             __syncwarp();
             if (ncand > (uint32_t)a.cand_cap) {  // practically never: the literal formulation of this tile
                 double acc[2] = {acc_a, acc_b};
-                tile_plain<MODE, EVAL>(a, blk0, 0, kmax, acc, &C, slot.pos, kStride);
+                tile_plain<MODE, EVAL>(a, blk0, 0, kmax, acc, &C);
                 acc_a = acc[0], acc_b = acc[1];
                 __syncwarp();
                 continue;
@@ -818,7 +810,10 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
                     }
                     // three sets (three blocks in flight) pay without the fused sums only: with them the larger loop body costs
                     // more in instruction fetch than the extra block in flight saves (3.32 vs 3.05 ms)
-                    constexpr int kSets = (TEMO_PAIR_SETS == 3 && EVAL == 0) ? 3 : 2;
+                    #ifndef TEMO_PAIR_SETS_FUSED
+#define TEMO_PAIR_SETS_FUSED 2
+#endif
+                    constexpr int kSets = EVAL == 0 ? TEMO_PAIR_SETS : TEMO_PAIR_SETS_FUSED;
                     double2 a2 = zero2, b2 = zero2;
                     if constexpr (kSets == 3) {
                         if (kmax > 2 && q + 2 * kStride * 32 < nvec) {
@@ -861,7 +856,7 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
                                 cb1 = ch.y;
                             }
                         }
-                        accumulate_vector<EVAL>(2 * q, m1, ca0, cb0, ca1, cb1, acc_a, acc_b, slot.pos);
+                        accumulate_vector<EVAL>(2 * q, m1, ca0, cb0, ca1, cb1, acc_a, acc_b);
                         __stcs(oa2 + q, make_double2(ca0, ca1));
                         __stcs(ob2 + q, make_double2(cb0, cb1));
                         q += kStride * 32;
@@ -916,9 +911,9 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
                     for (int w = 1; w < kVirtWarps; ++w) g += part[w];
                     (lane == 0 ? fa : fb)[0] = g;
                 }
-                for (uint32_t i = lane + 1; i < a.m; i += 32) {
-                    fa[i] = *reinterpret_cast<volatile double*>(&slot.pos[0][i - 1]);
-                    fb[i] = *reinterpret_cast<volatile double*>(&slot.pos[1][i - 1]);
+                for (uint32_t i = lane + 1; i < a.m; i += 32) {  // the children's position genes, as written by pass C
+                    fa[i] = __ldcg(C.oa + (i - 1));
+                    fb[i] = __ldcg(C.ob + (i - 1));
                 }
                 __syncwarp();
                 if (TEAM != 1 && lane == 0) {
