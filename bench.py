@@ -305,7 +305,7 @@ def run_ours(args):
     K, W = args.steps, args.warmup
     gens_total = max(100, W + 2 * K + 2)
     cfg = tb.RunConfig(problem=args.problem, pop=args.pop, dim=args.dim, obj=args.obj, generations=gens_total,
-                       seed=args.seed, fuse_eval=not args.no_fuse)
+                       seed=args.seed, fuse_eval=False if args.no_fuse else None)
     t_init = time.time()
     run = tb.RveaRun(cfg)
     init_s = time.time() - t_init
@@ -342,7 +342,7 @@ def run_ours(args):
 
     # ---- per-kernel timings for the roofline (isolated launches, L2 flushed between them)
     peak, peak_src = measured_peaks()
-    fused_ok = args.problem.startswith("dtlz") and not args.no_fuse
+    fused_ok = args.problem.startswith("dtlz") and not args.no_fuse and d > 1024  # the library's rule (run.h, fuse_offspring_eval)
     k_ms = {
         "reproduce": run.time_stage(1, args.stage_reps),
         "evaluate": run.time_stage(2, args.stage_reps),
@@ -403,7 +403,7 @@ def run_ours(args):
                 if pair is not None:
                     gens2 = 100
                     cfg2 = tb.RunConfig(problem=args.problem, pop=args.same_config_pop, dim=args.dim, obj=args.obj,
-                                        generations=gens2, seed=args.seed, fuse_eval=not args.no_fuse)
+                                        generations=gens2, seed=args.seed, fuse_eval=False if args.no_fuse else None)
                     with tb.RveaRun(cfg2) as run2:
                         for _ in range(3):
                             run2.step()

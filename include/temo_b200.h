@@ -88,7 +88,7 @@ typedef struct temo_b200_run_config {
     double fr;            /* adaptation frequency: every ceil(fr * generations) generations */
     double time_budget_s; /* 0 -> run all generations */
     temo_b200_ga_params ga;
-    int32_t fuse_eval;    /* 1: evaluate offspring inside the reproduction kernel (default) */
+    int32_t fuse_eval;    /* evaluate offspring inside the reproduction kernel: 0 never, 1 whenever the problem allows, 2 by shape (default) */
     int32_t op;           /* TEMO_B200_OP_* (0 = ga); de / pso / cso / random: algorithms.hpp:253-268 */
     temo_b200_op_params opp;
     uint64_t horizon;     /* toy2 / toy3: episode length (RunConfig::horizon, algorithms.hpp:35; 0 -> 100) */

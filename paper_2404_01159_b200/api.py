@@ -477,7 +477,7 @@ class RunConfig:
     pso: tuple = (0.4, 1.5, 1.5)   # PsoParams {inertia, c1, c2}, operators.hpp:33-37
     cso: tuple = (0.1,)            # CsoParams {phi}, operators.hpp:39-41
     rng_mode: int = RNG_SPLITMIX64
-    fuse_eval: bool = True
+    fuse_eval: object = None       # None: by shape (rows wider than 1024 genes), True: whenever possible, False: never
     horizon: int = 100             # algorithms.hpp:35 (toy environments)
     track_archive: bool = False    # algorithms.hpp:31
     archive_cap: int = 0           # algorithms.hpp:32 (0: unbounded)
@@ -496,7 +496,7 @@ class RunConfig:
         cfg.dim, cfg.obj = self.dim, self.obj
         cfg.alpha, cfg.fr, cfg.time_budget_s = self.alpha, self.fr, self.time_budget_s
         cfg.ga = self.ga.c()
-        cfg.fuse_eval = 1 if self.fuse_eval else 0
+        cfg.fuse_eval = 2 if self.fuse_eval is None else (1 if self.fuse_eval else 0)
         cfg.op = OPERATOR_IDS[self.op]
         cfg.opp.de_f, cfg.opp.de_cr = self.de
         cfg.opp.pso_inertia, cfg.opp.pso_c1, cfg.opp.pso_c2 = self.pso

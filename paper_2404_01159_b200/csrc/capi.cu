@@ -188,7 +188,7 @@ void temo_b200_default_run_config(temo_b200_run_config* cfg) {
     cfg->fr = 0.1;
     cfg->time_budget_s = 0.0;
     temo_b200_default_ga_params(&cfg->ga);
-    cfg->fuse_eval = 1;
+    cfg->fuse_eval = 2;
     cfg->op = TEMO_B200_OP_GA;
     cfg->opp.de_f = 0.5;  // operators.hpp:28-41
     cfg->opp.de_cr = 0.9;

@@ -215,6 +215,73 @@ __global__ void __launch_bounds__(256) eval_tma_kernel(const EvalK a) {
     }
 }
 
+// Narrow rows (450 <= d <= kRowWarpGenes): with eight warps on a row of 8 KB every warp would spend its time on the
+// per-row hand-shake. Here a warp takes whole rows: one bulk copy per row into the warp's own ring, the lane walks the
+// eight virtual warps' blocks (same canonical order: eight per-lane accumulators, eight butterflies side by side, totals
+// added in ascending order), no slot, no atomic, no CTA barrier.
+constexpr int kRowWarpGenes = 1536;  // 12 KB rows: still eight warps' rings per SM
+constexpr int kRowWarps = 4;         // warps per CTA
+
+template <int PID>
+__global__ void __launch_bounds__(kRowWarps * 32) eval_tma_rows_kernel(const EvalK a, uint32_t stage_genes) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    double* const tiles = reinterpret_cast<double*>(smem_raw);  // kRowWarps x kStages x stage_genes
+    __shared__ __align__(8) uint64_t full_bar[kRowWarps][kStages];
+    const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (threadIdx.x < kRowWarps * kStages) mbar_init(&full_bar[threadIdx.x / kStages][threadIdx.x % kStages], 1);
+    if (threadIdx.x == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncthreads();  // the only one
+
+    const uint32_t d = (uint32_t)a.d, nvec = d >> 1, nblk = (nvec + 31) >> 5, cblk = canon_chunk_blocks(nblk, 8);
+    const uint32_t m1 = (uint32_t)a.m - 1;
+    const uint64_t gw = (uint64_t)blockIdx.x * kRowWarps + w, nw = (uint64_t)gridDim.x * kRowWarps;
+    const uint64_t my_rows = a.n > gw ? (a.n - gw + nw - 1) / nw : 0;
+    double* const ring = tiles + (size_t)w * kStages * stage_genes;
+    uint64_t* const bars = &full_bar[w][0];
+    auto issue = [&](uint64_t c) {  // lane 0: start the copy of this warp's c-th row
+        const uint64_t i = gw + c * nw;
+        const uint64_t row = a.rows ? a.rows[i] : i;
+        const int st = (int)(c % kStages);
+        mbar_expect_tx(&bars[st], d * 8u);
+        tma_load_1d(ring + (size_t)st * stage_genes, a.x + row * a.d, d * 8u, &bars[st]);
+    };
+    if (lane == 0)
+        for (uint64_t c = 0; c < my_rows && c < (uint64_t)kStages; ++c) issue(c);
+    const uint64_t f0 = a.f_row0 + (a.f_row0_dev ? (uint64_t)*a.f_row0_dev : 0);
+    for (uint64_t c = 0; c < my_rows; ++c) {
+        const int st = (int)(c % kStages);
+        mbar_wait(&bars[st], (uint32_t)((c / kStages) & 1));
+        const double* row = ring + (size_t)st * stage_genes;
+        const double2* tile = reinterpret_cast<const double2*>(row);
+        double acc[8];
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {  // virtual warp v: blocks [v * cblk, (v + 1) * cblk)
+            acc[v] = 0.0;
+            for (uint32_t k = 0; k < cblk; ++k) {
+                const uint32_t t = (v * cblk + k) * 32 + lane;
+                if (t < nvec) {
+                    const double2 x = tile[t];
+                    const uint32_t j = 2 * t;
+                    if (j >= m1) acc[v] += dtlz_term<PID>(x.x);
+                    if (j + 1 >= m1) acc[v] += dtlz_term<PID>(x.y);
+                }
+            }
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+            for (int v = 0; v < 8; ++v) acc[v] += __shfl_xor_sync(0xffffffffu, acc[v], off);
+        double sum = acc[0];
+#pragma unroll
+        for (int v = 1; v < 8; ++v) sum += acc[v];
+        double* frow = a.f + (f0 + gw + c * nw) * a.m;  // {sum, position genes} for eval_finish_kernel
+        if (lane == 0) frow[0] = sum;
+        for (uint32_t o = lane + 1; o < a.m; o += 32) frow[o] = row[o - 1];
+        __syncwarp();  // stage drained by the warp
+        if (lane == 0 && c + kStages < my_rows) issue(c + kStages);
+    }
+}
+
 // ---- LSMOP1 --------------------------------------------------------------------------------------
 // y_j = (1 + (j + 1) / d) x_j - 10 x_0 over the tail genes, g_i = mean of y^2 over group i (m consecutive groups of
 // nk * sublen_i tail genes), objectives like DTLZ1's linear front without the 0.5. The linkage coefficients come from
@@ -528,7 +595,20 @@ bool eval_tma_enabled() { return g_eval_tma != 0; }
 template <int PID>
 void launch_dtlz(const EvalK& k, bool tma, cudaStream_t s) {
     const int vec = row_vec(k.d), block = row_block(k.d);
-    if (tma && eval_tma_enabled() && vec == 2 && block == 256) {
+    if (tma && eval_tma_enabled() && vec == 2 && block == 256 && k.d <= (uint64_t)kRowWarpGenes) {  // one warp per row
+        const uint32_t stage_genes = (uint32_t)((k.d + 15) / 16 * 16);
+        const size_t smem = (size_t)kRowWarps * kStages * stage_genes * sizeof(double);
+        static bool configured = false;
+        if (!configured) {
+            TEMO_CUDA(cudaFuncSetAttribute(eval_tma_rows_kernel<PID>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)(kRowWarps * kStages * kRowWarpGenes * sizeof(double))));
+            configured = true;
+        }
+        const uint64_t ctas_per_sm = std::max<uint64_t>(1, std::min<uint64_t>(16, (200u * 1024u) / (smem + 1024)));
+        const uint64_t grid = std::min<uint64_t>((uint64_t)kSMs * ctas_per_sm, (k.n + kRowWarps - 1) / kRowWarps);
+        eval_tma_rows_kernel<PID><<<(unsigned)grid, kRowWarps * 32, smem, s>>>(k, stage_genes);
+        eval_finish_kernel<PID><<<(unsigned)((k.n + 127) / 128), 128, 0, s>>>(k.f, k.n, k.m, k.d, k.f_row0, k.f_row0_dev);
+    } else if (tma && eval_tma_enabled() && vec == 2 && block == 256) {
         const size_t smem = sizeof(EvalTmaSmem);
         static bool configured = false;
         if (!configured) {

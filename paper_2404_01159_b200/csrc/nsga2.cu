@@ -296,7 +296,7 @@ void Nsga2Run::step(const double* f_off_inject) {
     ra.lower = lower;
     ra.upper = upper;
     ra.seg = bound_seg;
-    const bool fused = cfg.fuse_eval && cfg.problem >= kDtlz1 && cfg.problem <= kDtlz4;
+    const bool fused = fuse_offspring_eval(cfg.fuse_eval, cfg.problem, d);
     if (fused) {
         ra.eval_problem = cfg.problem;
         ra.m = m;

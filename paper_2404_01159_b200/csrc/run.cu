@@ -378,7 +378,7 @@ uint64_t Run::step(double* survivors_f_host, const double* f_off_inject) {
     TEMO_CUDA(cudaEventRecord(ev[0], stream));
     if (uses_perm())
         TEMO_CUDA(cudaMemcpyAsync(perm_dev, h_perm[hp], n * sizeof(uint32_t), cudaMemcpyHostToDevice, stream));
-    const bool fused = fusable();
+    const bool fused = cfg.op == kOpGa && fuse_offspring_eval(cfg.fuse_eval, cfg.problem, d);
     launch_mating_table(p);
     TEMO_CUDA(cudaEventRecord(ev[1], stream));
     uint64_t launches = 1 + (fused ? 0 : 1) + 9 + 4;

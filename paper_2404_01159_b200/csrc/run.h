@@ -7,13 +7,20 @@
 
 namespace temo_b200 {
 
+// Offspring evaluation inside the reproduction kernel? DTLZ only; by shape (fuse_eval == 2): rows wider than 1024 genes -
+// narrower ones are cheaper as single-warp reproduction plus the one-warp-per-row evaluator (config #4, d = 1000:
+// 0.32 + 0.26 ms against 0.64 ms fused; d = 1536: 0.44 + 0.19 against 0.59).
+inline bool fuse_offspring_eval(int fuse_eval, int problem, uint64_t d) {
+    return fuse_eval != 0 && problem >= kDtlz1 && problem <= kDtlz4 && (fuse_eval == 1 || d > 1024);
+}
+
 struct RunConfig {  // reference: RunConfig, algorithms.hpp:21-41
     int problem = kDtlz2;
     int rng_mode = 0;
     uint64_t pop = 105, lattice_h = 0, generations = 100, seed = 42, dim = 0, obj = 3;
     double alpha = 2.0, fr = 0.1, time_budget_s = 0.0;
     GaParams ga;
-    int fuse_eval = 1;
+    int fuse_eval = 2;  // 0 never, 1 whenever the problem has a fused evaluation, 2 by shape (fuse_offspring_eval)
     // reproduction operator (algorithms.hpp:250-268): 0 ga, 1 de, 2 pso, 3 cso, 4 random; the swarm operators take
     // apd_scores of the parent pool as fitness and carry a SwarmState across generations
     int op = 0;

@@ -387,7 +387,7 @@ struct Shard {
         ra.seg = bound_seg;
         ra.global_n = n;
         ra.global_unit0 = (uint64_t)rank * h_loc;
-        const bool fused = cfg.fuse_eval && cfg.problem >= kDtlz1 && cfg.problem <= kDtlz4;
+        const bool fused = fuse_offspring_eval(cfg.fuse_eval, cfg.problem, d);
         if (fused) {
             ra.eval_problem = cfg.problem;
             ra.m = m;

@@ -387,7 +387,7 @@ def bench_main(args, metric, workload_config, measured_peaks, ClockSampler):
     pop = args.pop if strong else args.pop * world
     K, W = args.steps, args.warmup
     cfg = RunConfig(problem=args.problem, pop=pop, dim=args.dim, obj=args.obj, generations=max(100, W + K + 2), seed=args.seed,
-                    fuse_eval=not args.no_fuse)
+                    fuse_eval=False if args.no_fuse else None)
     shard = GpuShard(cfg, rank, world)
     run = ShardedRvea(cfg, comm, shard)
     for _ in range(W):
