@@ -175,6 +175,7 @@ def k1_options(tb):
     tb.set_option("k1_bound_arrays", 0)
     tb.set_option("k1_cand_cap", 8)
     tb.set_option("k1_dynamic_pairs", 1)
+    tb.set_option("k1_single_warp", -1)
 
 
 @pytest.mark.parametrize("shape", [(16, 512), (12, 5120), (6, 5122), (6, 10240), (5, 20000), (9, 2002)])
@@ -261,11 +262,85 @@ def test_pair_hand_out_is_invisible(tb, oracle, k1_options, problem):
         k1_options("k1_dynamic_pairs", dyn)
         got = tb.ga_reproduce(x, tb.RngStream(9, 100), tb.GaParams(), lo, hi)
         assert np.array_equal(got, exp), (dyn, ulp_diff(got, exp).max())
-        with tb.RveaRun(tb.RunConfig(problem=problem, pop=n, dim=d, obj=3, generations=3, seed=4)) as run:
+        with tb.RveaRun(tb.RunConfig(problem=problem, pop=n, dim=d, obj=3, generations=3, seed=4, fuse_eval=True)) as run:
             pops = [run.step() for _ in range(3)]
             out = run.download()
         outs.append((pops, out["x"], out["f"]))
     assert outs[0][0] == outs[1][0] and np.array_equal(outs[0][1], outs[1][1]) and np.array_equal(outs[0][2], outs[1][2])
+
+
+@pytest.mark.parametrize("shape", [(16, 512), (10, 5120), (6, 5122), (5, 20000), (9, 2002), (64, 100), (40, 66), (12, 1000)])
+@pytest.mark.parametrize("ga", [(1.0, 20.0, 1.0, 20.0), (0.6, 5.0, 3.0, 7.0), (1.0, 3000.0, 1.0, 20.0)])
+def test_single_warp_pairs_vs_oracle(tb, oracle, k1_options, shape, ga):
+    """One warp per pair (the path large populations take: consecutive blocks, no team hand-shake), forced here on small
+    populations, also on rows narrower than the eight-warp mapping needs (d = 100, 66) where up to two mutation
+    candidates per tile are expected: offspring against the oracle, with the global counter and round-robin."""
+    n, d = shape
+    lo, hi = np.zeros(d), np.ones(d)
+    x, _ = oracle.random_reproduce(n, d, 29, 0, lo, hi)
+    exp, c = oracle.ga_reproduce(x, 78, 4321, lo, hi, ga=ga)
+    k1_options("k1_single_warp", 1)
+    for dyn in (1, 0):
+        k1_options("k1_dynamic_pairs", dyn)
+        st = tb.RngStream(78, 4321)
+        got = tb.ga_reproduce(x, st, tb.GaParams(*ga), lo, hi)
+        assert st.counter == c
+        assert np.array_equal(got, exp), (dyn, ulp_diff(got, exp).max())
+
+
+@pytest.mark.parametrize("case", [("dtlz1", 600, 1400, 3), ("dtlz2", 2048, 640, 3), ("dtlz3", 300, 5000, 10), ("lsmop1", 400, 2000, 3),
+                                  ("dtlz4", 500, 452, 4)])
+def test_single_warp_runs_equal_team_runs(tb, k1_options, case):
+    """Whole generations with one warp per pair (fused sums flushed per virtual warp, position genes read back from the
+    children's rows) and with the eight-warp teams, fused and unfused, candidate slots exhausted or not: bit-identical
+    populations and objectives."""
+    problem, n, d, m = case
+    outs = []
+    for sw, fuse, cap in ((0, True, 8), (1, True, 8), (1, True, 0), (1, False, 8), (0, False, 8)):
+        k1_options("k1_single_warp", sw)
+        k1_options("k1_cand_cap", cap)
+        with tb.RveaRun(tb.RunConfig(problem=problem, pop=n, dim=d, obj=m, generations=4, seed=13, fuse_eval=fuse)) as run:
+            pops = [run.step() for _ in range(4)]
+            out = run.download()
+        outs.append((pops, out["x"], out["f"]))
+    for pops, x, f in outs[1:]:
+        assert pops == outs[0][0]
+        assert np.array_equal(x, outs[0][1]) and np.array_equal(f, outs[0][2])
+
+
+def test_fused_evaluation_by_shape_is_invisible(tb):
+    """fuse_eval = None picks the fused evaluation by row width (run.h, fuse_offspring_eval); either choice gives the
+    same run."""
+    for d in (640, 1400):
+        outs = []
+        for fuse in (None, True, False):
+            with tb.RveaRun(tb.RunConfig(problem="dtlz2", pop=512, dim=d, obj=3, generations=3, seed=21, fuse_eval=fuse)) as run:
+                pops = [run.step() for _ in range(3)]
+                out = run.download()
+            outs.append((pops, out["x"], out["f"]))
+        for pops, x, f in outs[1:]:
+            assert pops == outs[0][0] and np.array_equal(x, outs[0][1]) and np.array_equal(f, outs[0][2])
+
+
+@pytest.mark.parametrize("problem", ["dtlz1", "dtlz2", "dtlz3", "dtlz4", "lsmop1"])
+def test_tma_evaluators_equal_plain_kernels(tb, problem):
+    """The three bulk-copy evaluators (one warp per row up to 1536 genes, one ring per warp beyond, the LSMOP1 variant
+    with two or four groups per warp) against the one-CTA-per-row kernels: same canonical order, same bits - rows that
+    end inside a block, inside a warp's share, m up to 31, a single row, more rows than resident warps."""
+    rng = np.random.default_rng(3)
+    try:
+        for n, d, m in [(1000, 1000, 3), (777, 1534, 5), (300, 450, 3), (64, 1536, 10), (5, 500, 31), (1, 452, 2), (700, 5000, 3),
+                        (333, 4998, 5), (40, 5120, 10), (9, 20000, 3), (2500, 1538, 3), (200, 600, 12)]:
+            x = rng.random((n, d))
+            if problem == "lsmop1":
+                x[:, m - 1:] *= 10.0
+            tb.set_option("eval_tma", 1)
+            f1 = tb.evaluate(problem, x, m)
+            tb.set_option("eval_tma", 0)
+            f0 = tb.evaluate(problem, x, m)
+            assert np.array_equal(f0, f1), (n, d, m)
+    finally:
+        tb.set_option("eval_tma", 1)
 
 
 @pytest.mark.parametrize("shape", [(64, 640, 3), (48, 5000, 3), (32, 1402, 2), (40, 2050, 4), (24, 10240, 3), (16, 4998, 5), (9, 333, 3),
