@@ -798,7 +798,8 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
                 // always in flight and no value is ever moved between registers (the rotating three-set form of the earlier
                 // kernel spent ~30 of its ~135 instructions per block on moves). One instance of the loop only: a second
                 // copy for the tile that holds the bounds split cost more in instruction fetch than the moves it saved
-                // (no_instruction stalls 0.2 -> 1.1 per issue), so two-segment bounds (SEG == 2) are selected per gene.
+                // (no_instruction stalls 0.2 -> 1.1 per issue), so two-segment bounds (SEG == 2) are selected per gene, behind a
+                // warp-uniform branch, in the one tile of a row that holds the split.
                 {
                     uint32_t q = q_first, sm_b = sm_lane;
                     const double2 zero2 = make_double2(0.0, 0.0);
@@ -826,9 +827,12 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
                         if (SEG == 1) {
                             lo_x = lo_y = seg_lo, hi_x = hi_y = seg_hi;
                         } else if (SEG == 2) {
-                            const bool sx = 2 * q >= a.seg_split, sy = 2 * q + 1 >= a.seg_split;
-                            lo_x = sx ? a.seg_lo[1] : a.seg_lo[0], lo_y = sy ? a.seg_lo[1] : a.seg_lo[0];
-                            hi_x = sx ? a.seg_hi[1] : a.seg_hi[0], hi_y = sy ? a.seg_hi[1] : a.seg_hi[0];
+                            lo_x = lo_y = seg_lo, hi_x = hi_y = seg_hi;
+                            if (seg_mixed) {  // the one tile of a row that holds the split (warp-uniform)
+                                const bool sx = 2 * q >= a.seg_split, sy = 2 * q + 1 >= a.seg_split;
+                                lo_x = sx ? a.seg_lo[1] : a.seg_lo[0], lo_y = sy ? a.seg_lo[1] : a.seg_lo[0];
+                                hi_x = sx ? a.seg_hi[1] : a.seg_hi[0], hi_y = sy ? a.seg_hi[1] : a.seg_hi[0];
+                            }
                         } else {
                             const double2 vlo = __ldg(lo2 + q), vhi = __ldg(hi2 + q);
                             lo_x = vlo.x, lo_y = vlo.y, hi_x = vhi.x, hi_y = vhi.y;
