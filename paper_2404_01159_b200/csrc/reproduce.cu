@@ -304,13 +304,14 @@ __global__ void __launch_bounds__(256, TEMO_REPRO_MIN_BLOCKS) reproduce_kernel(c
 
 
 // ------------------------------------------------------------------------------------------------
-// Fast path: SBX + PM over full mating pairs of wide even rows — persistent teams of eight warps.
+// Fast path: SBX + PM over full mating pairs of even rows — persistent warps, a pair per warp (TEAM = 1: whenever the
+// launch has a pair for every resident warp) or per team of eight warps (TEAM = 8: small populations of wide rows).
 //
-// Same arithmetic, same draws, same thread->gene map (warp w owns the 64-gene blocks w, w+8, ... of the row,
-// lane l the vector l of a block) and the same reduction order as reproduce_unit above, reorganised so that
-// the expensive parts run dense and branch-free and no warp ever waits for another one:
-// a CTA (team) loops over pairs; inside a pair each warp works through its own blocks, one row tile of
-// 80 blocks (10 per warp) at a time, in four passes:
+// Same arithmetic, same draws, same thread->gene map (virtual warp w owns the consecutive 64-gene blocks
+// [w * cblk, (w + 1) * cblk) of the row, lane l the vector l of a block: common.cuh) and the same reduction order as
+// reproduce_unit above, reorganised so that the expensive parts run dense and branch-free and no warp ever waits for
+// another one: a warp works through its blocks in tiles of up to kPairBlocks (a single warp walks the eight virtual
+// warps of a pair one after the other), each tile in four passes:
 //   A  hashes only. hr = H(r2 - 0.5) for every gene (operators.hpp:90-91): the crossing genes (about half)
 //      are appended to the warp's list in shared memory and beta = 1 is planted for everybody. The quick
 //      reject of the mutation mask H(pm/d - r4) (operators.hpp:136) for both children: the few genes that
@@ -322,9 +323,10 @@ __global__ void __launch_bounds__(256, TEMO_REPRO_MIN_BLOCKS) reproduce_kernel(c
 //      replaced by a tagged NaN pointing at it.
 //   C  the streaming pass: 128-bit loads of both parents, blend + clamp (operators.hpp:92-95), a tagged beta
 //      swaps in the parked children, fused objective partial sums, 128-bit stores of both children.
-// There is no CTA barrier after start-up. A warp that finishes its share of a pair leaves its partial sums in
+// There is no CTA barrier after start-up. In a team a warp that finishes its share of a pair leaves its partial sums in
 // one of kPairSlots per-pair slots and moves on to the next pair; the last warp to arrive adds the eight
-// partials in ascending warp order (the order of block_sum) and writes the objective rows. The warps of an SM
+// partials in ascending warp order (the order of block_sum) and writes the objective rows. A single warp flushes the
+// sums of each virtual warp into its own slot and writes the rows after the eighth. The warps of an SM
 // therefore drift apart and their compute and memory passes overlap. At the start of a tile every warp asks for
 // its own parent blocks to be pulled into L2 (prefetch.global.L2; about half of those hints are honoured under
 // load), and pass C keeps the parents of the next two blocks in flight in registers.
@@ -554,8 +556,7 @@ __device__ __forceinline__ void accumulate_vector(uint32_t j0, uint32_t m1, doub
 
 // Pass B of a tile with the general pow (base 0, or an exponent outside the narrow path's range): same list, same stores.
 template <int MODE>
-__device__ __noinline__ void pass_b_general(const ReproK& a, uint64_t pos_tile, uint32_t total, uint32_t sm_w, uint32_t lane,
-                                            uint32_t) {
+__device__ __noinline__ void pass_b_general(const ReproK& a, uint64_t pos_tile, uint32_t total, uint32_t sm_w, uint32_t lane) {
     constexpr uint64_t SG = MODE == 0 ? kGolden : 1ULL;
     constexpr uint32_t kOffList = offsetof(WarpSmem, list);
     for (uint32_t t = lane; t < total; t += 32) {
@@ -624,10 +625,9 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
     static_assert(TEAM == kVirtWarps || TEAM == 1, "a pair belongs to a team of eight warps or to one warp");
     extern __shared__ __align__(16) unsigned char pair_smem_raw[];
     PairSmem& S = *reinterpret_cast<PairSmem*>(pair_smem_raw);
-    constexpr uint32_t kStride = 1;                                // a warp's blocks are consecutive
     constexpr uint32_t kVPerWarp = TEAM == 1 && EVAL != 0 ? kVirtWarps : 1;  // virtual warps a warp walks through
     constexpr uint64_t SG = MODE == 0 ? kGolden : 1ULL;            // stream distance of neighbouring genes
-    constexpr uint64_t STEP = SG * (uint64_t)(kStride * 64);       // ... of a lane's consecutive blocks
+    constexpr uint64_t STEP = SG * 64ULL;                           // ... of a lane's consecutive blocks
     constexpr uint32_t kOffList = offsetof(WarpSmem, list), kOffSide = offsetof(WarpSmem, side);
     const uint32_t lane = opaque(threadIdx.x & 31), warp = opaque(threadIdx.x >> 5);
     WarpSmem& W = S.w[warp];
@@ -694,7 +694,7 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
                 const uint64_t first = pos + (uint64_t)(2 * q_first) * SG;
                 uint64_t p_r2 = first + a.dl_r2, p_ma = first + a.dl_mask_a, p_mb = first + a.dl_mask_b;
                 uint32_t q = q_first, e = lane * 2, sm_b = sm_lane;
-                for (uint32_t k = 0; k < kmax; ++k, p_r2 += STEP, p_ma += STEP, p_mb += STEP, q += kStride * 32, e += 64, sm_b += 512) {
+                for (uint32_t k = 0; k < kmax; ++k, p_r2 += STEP, p_ma += STEP, p_mb += STEP, q += 32, e += 64, sm_b += 512) {
                     const bool valid = q < nvec;
                     const bool vc = valid && cross;
                     // hr = H(r2 - 0.5) = 0 <=> top bit clear
@@ -763,7 +763,7 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
                     sts_f64(sm_w + 8 * e0, q0);
                     if (two) sts_f64(sm_w + 8 * e1, q1);
                 }
-                if (__any_sync(0xffffffffu, redo)) pass_b_general<MODE>(a, pos_tile, total, sm_w, lane, kStride);
+                if (__any_sync(0xffffffffu, redo)) pass_b_general<MODE>(a, pos_tile, total, sm_w, lane);
             }
             __syncwarp();
             // ---- pass M: the mutation candidates of this tile (usually none)
@@ -805,9 +805,9 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
                     const double2 zero2 = make_double2(0.0, 0.0);
                     double2 a0 = q < nvec ? __ldcs(pa2 + q) : zero2, b0 = q < nvec ? __ldcs(pb2 + q) : zero2;
                     double2 a1 = zero2, b1 = zero2;
-                    if (kmax > 1 && q + kStride * 32 < nvec) {
-                        a1 = __ldcs(pa2 + q + kStride * 32);
-                        b1 = __ldcs(pb2 + q + kStride * 32);
+                    if (kmax > 1 && q + 32 < nvec) {
+                        a1 = __ldcs(pa2 + q + 32);
+                        b1 = __ldcs(pb2 + q + 32);
                     }
                     // three sets (three blocks in flight) pay without the fused sums only: with them the larger loop body costs
                     // more in instruction fetch than the extra block in flight saves (3.32 vs 3.05 ms)
@@ -817,9 +817,9 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
                     constexpr int kSets = EVAL == 0 ? TEMO_PAIR_SETS : TEMO_PAIR_SETS_FUSED;
                     double2 a2 = zero2, b2 = zero2;
                     if constexpr (kSets == 3) {
-                        if (kmax > 2 && q + 2 * kStride * 32 < nvec) {
-                            a2 = __ldcs(pa2 + q + 2 * kStride * 32);
-                            b2 = __ldcs(pb2 + q + 2 * kStride * 32);
+                        if (kmax > 2 && q + 2 * 32 < nvec) {
+                            a2 = __ldcs(pa2 + q + 2 * 32);
+                            b2 = __ldcs(pb2 + q + 2 * 32);
                         }
                     }
                     auto block = [&](uint32_t k, double2& pa_v, double2& pb_v) {
@@ -842,7 +842,7 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
                         sbx_children(pa_v.x, pb_v.x, vbeta.x, lo_x, hi_x, ca0, cb0);
                         sbx_children(pa_v.y, pb_v.y, vbeta.y, lo_y, hi_y, ca1, cb1);
                         {   // the set is free: block k + kSets goes into it
-                            const uint32_t qf = q + kSets * kStride * 32;
+                            const uint32_t qf = q + kSets * 32;
                             if (k + kSets < kmax && qf < nvec) {
                                 pa_v = __ldcs(pa2 + qf);
                                 pb_v = __ldcs(pb2 + qf);
@@ -863,7 +863,7 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
                         accumulate_vector<EVAL>(2 * q, m1, ca0, cb0, ca1, cb1, acc_a, acc_b);
                         __stcs(oa2 + q, make_double2(ca0, ca1));
                         __stcs(ob2 + q, make_double2(cb0, cb1));
-                        q += kStride * 32;
+                        q += 32;
                         sm_b += 512;
                     };
                     for (uint32_t k = 0; k < kmax; k += kSets) {
@@ -968,9 +968,8 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
 struct K1Options {
     int generic, bound_arrays, cand_cap;
     int dynamic_pairs;  // pair kernel: pairs handed out through a global counter (1, default) or round-robin (0)
-    int single_warp;    // pair kernel, one warp per pair: -1 when the launch has a pair for every resident warp (default: consecutive
-                        // blocks without fused sums, the eight-virtual-warp walk with them), 0 never, 1 consecutive blocks whenever
-                        // that applies, 2 the walk always
+    int single_warp;    // pair kernel, one warp per pair: -1 when the launch has a pair for every resident warp (default), 0 never
+                        // (teams of eight warps), 1 always
 };
 inline int env_int(const char* name, int dflt) {
     const char* e = getenv(name);
@@ -1114,9 +1113,8 @@ __global__ void pow_batch_kernel(const double* x, const double* y, uint64_t n, d
 //                       they are piecewise constant                       TEMO_B200_K1_BOUND_ARRAYS
 //   k1_cand_cap      mutation-candidate slots per warp tile of the pair
 //                    kernel, 0..kPairCand (0 forces its plain-tile path)  TEMO_B200_K1_CAND_CAP
-//   k1_single_warp   pair kernel with one warp per pair: -1 by shape,
-//                    0 never, 1 consecutive blocks (no fused sums),
-//                    2 the eight-virtual-warp walk                        TEMO_B200_K1_SINGLE_WARP
+//   k1_single_warp   pair kernel with one warp per pair: -1 when the launch
+//                    has a pair per resident warp, 0 never, 1 always      TEMO_B200_K1_SINGLE_WARP
 inline unsigned stream_grid(uint64_t total, int block) {
     uint64_t g = (total + block - 1) / block;
     const uint64_t cap = (uint64_t)kSMs * 16;
@@ -1261,7 +1259,7 @@ bool set_k1_option(const char* name, long value) {
     else if (key == "k1_bound_arrays") o.bound_arrays = value != 0;
     else if (key == "k1_cand_cap") o.cand_cap = (int)std::max(0L, std::min((long)kPairCand, value));
     else if (key == "k1_dynamic_pairs") o.dynamic_pairs = value != 0;
-    else if (key == "k1_single_warp") o.single_warp = value < 0 ? -1 : (int)std::min(2L, value);
+    else if (key == "k1_single_warp") o.single_warp = value < 0 ? -1 : (value != 0);
     else return false;
     return true;
 }
