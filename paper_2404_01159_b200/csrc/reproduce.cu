@@ -380,21 +380,32 @@ struct PairSlot {
 #define TEMO_PAIR_RING 4
 #endif
 constexpr int kUnitRing = TEMO_PAIR_RING;                    // pairs a team's warps may be apart
-struct PairSmem {
+// CTA geometry of the single-warp pairs (TEAM == 1): warps per CTA and CTAs per SM (the register budget follows)
+#ifndef TEMO_SOLO_WARPS
+#define TEMO_SOLO_WARPS 8
+#endif
+#ifndef TEMO_SOLO_CTAS
+#define TEMO_SOLO_CTAS 3
+#endif
+constexpr int kSoloWarps = TEMO_SOLO_WARPS, kSoloCtas = TEMO_SOLO_CTAS;
+template <int NW>
+struct PairSmemT {
     PowSmem pow;
-    WarpSmem w[kVirtWarps];
+    WarpSmem w[NW];
     PairSlot slot[kPairSlots];
     // pair hand-out: turn T of this team works on pair ring[T % kUnitRing], described by ringctx[T % kUnitRing] (filled once
     // per pair by the warp that fetched it)
     uint32_t ring[kUnitRing];
     PairCtx ringctx[kUnitRing];
-    PairCtx warpctx[kVirtWarps];    // single-warp pairs (TEAM == 1): every warp describes its own
-    PairSlot warpslot[kVirtWarps];  // ... and collects its own totals
-    uint32_t progress[kVirtWarps];  // turns every warp has finished
+    PairCtx warpctx[NW];    // single-warp pairs (TEAM == 1): every warp describes its own
+    PairSlot warpslot[NW];  // ... and collects its own totals
+    uint32_t progress[NW];  // turns every warp has finished
     uint32_t claiming, published;   // highest turn being fetched / already published
 };
 
+using PairSmem = PairSmemT<kVirtWarps>;
 static_assert(sizeof(PairSmem) + 1024 <= (228 * 1024) / TEMO_PAIR_MIN_BLOCKS, "the teams of an SM must fit its shared memory");
+static_assert(sizeof(PairSmemT<kSoloWarps>) + 1024 <= (228 * 1024) / kSoloCtas, "the single-warp CTAs of an SM must fit its shared memory");
 template <int N> struct ShowSize;
 #ifdef TEMO_SHOW_SMEM
 ShowSize<sizeof(PairSmem)> show_pair_smem;
@@ -621,10 +632,12 @@ __device__ __noinline__ void tile_plain(const ReproK& a, uint32_t blk0, uint32_t
 // per-pair and per-tile work of eight warps for them; one warp makes a ten- and a six-block tile of it). Without the fused
 // sums only: their canonical order is that of the eight-warp mapping.
 template <int MODE, int EVAL, int SEG, int TEAM>  // SEG: 0 bound arrays, 1 one constant segment, 2 two constant segments
-__global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reproduce_pairs_kernel(const __grid_constant__ ReproK a) {
+__global__ void __launch_bounds__((TEAM == 1 ? kSoloWarps : kVirtWarps) * 32, TEAM == 1 ? kSoloCtas : TEMO_PAIR_MIN_BLOCKS)
+    reproduce_pairs_kernel(const __grid_constant__ ReproK a) {
     static_assert(TEAM == kVirtWarps || TEAM == 1, "a pair belongs to a team of eight warps or to one warp");
+    constexpr int NW = TEAM == 1 ? kSoloWarps : kVirtWarps;  // warps of the CTA
     extern __shared__ __align__(16) unsigned char pair_smem_raw[];
-    PairSmem& S = *reinterpret_cast<PairSmem*>(pair_smem_raw);
+    PairSmemT<NW>& S = *reinterpret_cast<PairSmemT<NW>*>(pair_smem_raw);
     constexpr uint32_t kVPerWarp = TEAM == 1 && EVAL != 0 ? kVirtWarps : 1;  // virtual warps a warp walks through
     constexpr uint64_t SG = MODE == 0 ? kGolden : 1ULL;            // stream distance of neighbouring genes
     constexpr uint64_t STEP = SG * 64ULL;                           // ... of a lane's consecutive blocks
@@ -637,7 +650,7 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
         S.slot[threadIdx.x].arrived = 0;
         S.slot[threadIdx.x].done = 0;
     }
-    if (threadIdx.x < kVirtWarps) S.progress[threadIdx.x] = 0;
+    if (threadIdx.x < NW) S.progress[threadIdx.x] = 0;
     if (threadIdx.x == 0) {
         S.claiming = S.published = 0;
         if (TEAM != 1 && a.unit0 + blockIdx.x < a.unit_end) fill_pair_ctx<MODE>(S.ringctx[0], a, a.unit0 + blockIdx.x);  // the team's first pair
@@ -661,7 +674,7 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
     // A team's first pair is its block index; for every later turn the first warp to get there draws the next pair
     // from a global counter and publishes it to the team through a small ring (the warps of a team are never more
     // than kUnitRing turns apart).
-    for (uint64_t unit = a.unit0 + (TEAM == 1 ? blockIdx.x * kVirtWarps + warp : blockIdx.x); unit < a.unit_end; ++turn) {
+    for (uint64_t unit = a.unit0 + (TEAM == 1 ? blockIdx.x * NW + warp : blockIdx.x); unit < a.unit_end; ++turn) {
         PairSlot& slot = TEAM == 1 ? S.warpslot[warp] : S.slot[turn % kPairSlots];
         const PairCtx& C = TEAM == 1 ? S.warpctx[warp] : S.ringctx[turn % kUnitRing];
         if (TEAM == 1 && lane == 0) fill_pair_ctx<MODE>(S.warpctx[warp], a, unit);
@@ -931,9 +944,9 @@ __global__ void __launch_bounds__(kVirtWarps * 32, TEMO_PAIR_MIN_BLOCKS) reprodu
         __syncwarp();
         if constexpr (TEAM == 1) {  // this warp's next pair
             uint32_t next = 0;
-            if (lane == 0) next = a.work_counter ? atomicAdd(a.work_counter, 1u) : turn * gridDim.x * kVirtWarps + blockIdx.x * kVirtWarps + warp;
+            if (lane == 0) next = a.work_counter ? atomicAdd(a.work_counter, 1u) : turn * gridDim.x * NW + blockIdx.x * NW + warp;
             next = __shfl_sync(0xffffffffu, next, 0);
-            unit = a.unit0 + (uint64_t)gridDim.x * kVirtWarps + next;
+            unit = a.unit0 + (uint64_t)gridDim.x * NW + next;
             continue;
         }
         // ---- the team's next pair (round-robin over the grid without a work counter)
@@ -996,14 +1009,16 @@ inline uint32_t* next_work_counter() {
 
 template <int MODE, int EVAL, int SEG, int TEAM = kVirtWarps>
 void launch_pairs_seg(const ReproK& k, uint64_t units, cudaStream_t s) {
+    constexpr int NW = TEAM == 1 ? kSoloWarps : kVirtWarps;
+    constexpr int kCtas = TEAM == 1 ? kSoloCtas : TEMO_PAIR_MIN_BLOCKS;
     static int grid = 0;  // per instantiation
     if (grid == 0) {
         TEMO_CUDA(cudaFuncSetAttribute(reproduce_pairs_kernel<MODE, EVAL, SEG, TEAM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)sizeof(PairSmem)));
+                                       (int)sizeof(PairSmemT<NW>)));
         int dev = 0, sms = 0;
         TEMO_CUDA(cudaGetDevice(&dev));
         TEMO_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        grid = (sms > 0 ? sms : kSMs) * TEMO_PAIR_MIN_BLOCKS;
+        grid = (sms > 0 ? sms : kSMs) * kCtas;
     }
     ReproK kk = k;
     kk.work_counter = nullptr;
@@ -1013,9 +1028,9 @@ void launch_pairs_seg(const ReproK& k, uint64_t units, cudaStream_t s) {
         kk.work_counter = next_work_counter();
         TEMO_CUDA(cudaMemsetAsync(kk.work_counter, 0, sizeof(uint32_t), s));
     }
-    const uint64_t teams_per_cta = TEAM == 1 ? kVirtWarps : 1;
+    const uint64_t pairs_per_cta = TEAM == 1 ? NW : 1;
     reproduce_pairs_kernel<MODE, EVAL, SEG, TEAM>
-        <<<(unsigned)std::min<uint64_t>((units + teams_per_cta - 1) / teams_per_cta, (uint64_t)grid), kVirtWarps * 32, sizeof(PairSmem), s>>>(kk);
+        <<<(unsigned)std::min<uint64_t>((units + pairs_per_cta - 1) / pairs_per_cta, (uint64_t)grid), NW * 32, sizeof(PairSmemT<NW>), s>>>(kk);
 }
 
 template <int MODE, int EVAL>
@@ -1194,7 +1209,7 @@ void launch_reproduce(const ReproArgs& a, cudaStream_t s) {
     const double cand_rate = k.mask_never ? 0.0 : ((double)k.mask_top + 1.0) * 0x1.0p-21;  // P(quick reject passes)
     // One warp per pair (narrow rows, no fused sums): when the launch has enough pairs to give every resident warp its own.
     const uint64_t pairs_launched = std::min(unit_hi, k.half) > unit_lo ? std::min(unit_hi, k.half) - unit_lo : 0;
-    const bool enough_pairs = pairs_launched >= (uint64_t)kSMs * TEMO_PAIR_MIN_BLOCKS * kVirtWarps;
+    const bool enough_pairs = pairs_launched >= (uint64_t)kSMs * kSoloCtas * kSoloWarps;
     const int sw = k1_options().single_warp;
     const bool single_warp = sw > 0 || (sw < 0 && enough_pairs);
     const int team = single_warp ? 1 : kVirtWarps;
