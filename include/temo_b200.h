@@ -219,6 +219,12 @@ int temo_b200_run_last_generation(temo_b200_run* run, double* offspring, double*
  * [3] selection (+survivor commit), [4] adaptation, [5] host mating-permutation time (wall),
  * [6] number of kernels launched in the step, [7] permutation upload + mating table. */
 int temo_b200_run_timings(temo_b200_run* run, double* ms8);
+/* The same eight values for each of the last min(max_steps, 1024) steps since the last reset, oldest first (8 * steps
+ * doubles); *steps_out = steps written. The library reads a step's events while the NEXT step runs on the device, so a
+ * caller that wants per-step stage times of a timed loop asks once after the loop instead of once per step (no host
+ * work between the end of a step and the first launch of the next). reset != 0 empties the log afterwards.
+ * (Measurement support of the harness: no reference counterpart.) */
+int temo_b200_run_timing_history(temo_b200_run* run, double* ms8_per_step, uint64_t max_steps, int reset, uint64_t* steps_out);
 int temo_b200_run_destroy(temo_b200_run* run);
 
 /* rvea_run (algorithms.hpp:227-296), whole run, RunRecord fields flattened:

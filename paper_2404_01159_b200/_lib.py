@@ -110,6 +110,7 @@ SIGNATURES = {
     "temo_b200_run_download": (C.c_int, [_RUN, f64p, f64p, f64p, f64p]),
     "temo_b200_run_last_generation": (C.c_int, [_RUN, f64p, f64p, u64p]),
     "temo_b200_run_timings": (C.c_int, [_RUN, f64p]),
+    "temo_b200_run_timing_history": (C.c_int, [_RUN, f64p, C.c_uint64, C.c_int, C.POINTER(C.c_uint64)]),
     "temo_b200_run_destroy": (C.c_int, [_RUN]),
     "temo_b200_rvea_run": (C.c_int, [_CFG, f64p, f64p, u64p, u64p, u64p, f64p]),
     "temo_b200_dev_alloc": (C.c_void_p, [C.c_size_t]),

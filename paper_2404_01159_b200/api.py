@@ -719,6 +719,15 @@ class RveaRun:
         return dict(generation=ms[0], reproduce=ms[1], evaluate=ms[2], select=ms[3], adapt=ms[4], host_perm=ms[5],
                     launches=int(ms[6]), prep=ms[7])
 
+    def timing_history(self, max_steps: int = 1024, reset: bool = True) -> list:
+        """Stage timings (the dict of timings()) of each of the last steps since the last reset, oldest first; the library
+        reads a step's events while the next step runs, so a timed loop asks once after the loop."""
+        ms = np.zeros((max_steps, 8))
+        count = C.c_uint64(0)
+        _call(self._L.temo_b200_run_timing_history, self._h, _p(ms), u64(max_steps), C.c_int(1 if reset else 0), C.byref(count))
+        keys = ("generation", "reproduce", "evaluate", "select", "adapt", "host_perm", "launches", "prep")
+        return [{k: (int(row[i]) if k == "launches" else float(row[i])) for i, k in enumerate(keys)} for row in ms[:count.value]]
+
     def set_metrics(self, mc: MetricContext) -> None:
         """MetricContext of this run (algorithms.hpp:46-54): the references move to the device once."""
         pf = None if mc.pf_ref is None else _t(mc.pf_ref)

@@ -672,7 +672,15 @@ int temo_b200_run_last_generation(temo_b200_run* run, double* offspring, double*
 int temo_b200_run_timings(temo_b200_run* run, double* ms8) {
     return guarded([&] {
         require(run && run->impl && ms8, "run_timings: null argument");
+        run->impl->resolve_timings();
         std::memcpy(ms8, run->impl->timings, 8 * sizeof(double));
+    });
+}
+
+int temo_b200_run_timing_history(temo_b200_run* run, double* ms8_per_step, uint64_t max_steps, int reset, uint64_t* steps_out) {
+    return guarded([&] {
+        require(run && run->impl && steps_out && (ms8_per_step || max_steps == 0), "run_timing_history: null argument");
+        *steps_out = run->impl->timing_history(ms8_per_step, max_steps, reset != 0);
     });
 }
 

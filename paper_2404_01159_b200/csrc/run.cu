@@ -162,7 +162,8 @@ Run::Run(const RunConfig& c) : cfg(c) {
     skip_flag = dev_alloc<uint32_t>(1);
     TEMO_CUDA(cudaMallocHost(&h_status, 4 * sizeof(uint32_t)));
     ws.alloc(cap, r, m);
-    for (int e = 0; e < kNumEvents; ++e) TEMO_CUDA(cudaEventCreate(&ev[e]));
+    for (int s2 = 0; s2 < 2; ++s2)
+        for (int e = 0; e < kNumEvents; ++e) TEMO_CUDA(cudaEventCreate(&ev[s2][e]));
 
     // reference set (algorithms.hpp:236): lattice + unit vectors on the host (once), gamma on device
     const std::vector<double> unit = normalize_to_unit(simplex_lattice(m, H), r, m);
@@ -224,7 +225,8 @@ Run::~Run() {
     cudaFreeHost(h_status);
     ws.release();
     vindex.release();
-    for (int e = 0; e < kNumEvents; ++e) cudaEventDestroy(ev[e]);
+    for (int s2 = 0; s2 < 2; ++s2)
+        for (int e = 0; e < kNumEvents; ++e) cudaEventDestroy(ev[s2][e]);
 }
 
 // Reads n_elite / error flags back (one small D2H) and turns device-side contract violations
@@ -375,12 +377,13 @@ uint64_t Run::step(double* survivors_f_host, const double* f_off_inject) {
     ensure_permutation(p);
     const double host1 = now_ms();
 
-    TEMO_CUDA(cudaEventRecord(ev[0], stream));
+    cudaEvent_t* const evs = ev[evp];
+    TEMO_CUDA(cudaEventRecord(evs[0], stream));
     if (uses_perm())
         TEMO_CUDA(cudaMemcpyAsync(perm_dev, h_perm[hp], n * sizeof(uint32_t), cudaMemcpyHostToDevice, stream));
     const bool fused = cfg.op == kOpGa && fuse_offspring_eval(cfg.fuse_eval, cfg.problem, d);
     launch_mating_table(p);
-    TEMO_CUDA(cudaEventRecord(ev[1], stream));
+    TEMO_CUDA(cudaEventRecord(evs[1], stream));
     uint64_t launches = 1 + (fused ? 0 : 1) + 9 + 4;
     if (cfg.op == kOpGa) {
         launch_reproduction(p, fused);
@@ -388,9 +391,9 @@ uint64_t Run::step(double* survivors_f_host, const double* f_off_inject) {
     } else {
         launches += launch_other_operator(p);
     }
-    TEMO_CUDA(cudaEventRecord(ev[2], stream));
+    TEMO_CUDA(cudaEventRecord(evs[2], stream));
     if (!fused) launch_offspring_eval();
-    TEMO_CUDA(cudaEventRecord(ev[3], stream));
+    TEMO_CUDA(cudaEventRecord(evs[3], stream));
     if (f_off_inject) {  // lock-step testing: keep the device's objectives aside, select on the given ones
         if (!f_off_saved) f_off_saved = dev_alloc<double>(n * m);
         TEMO_CUDA(cudaMemcpyAsync(f_off_saved, fm[cur] + P * m, n * m * sizeof(double), cudaMemcpyDeviceToDevice, stream));
@@ -407,7 +410,7 @@ uint64_t Run::step(double* survivors_f_host, const double* f_off_inject) {
         ws.elite, ws.n_elite, P, m, parent_slot[cur], free_slot[cur], parent_slot[cur ^ 1], fm[cur], fm[cur ^ 1],
         used, d_P);
     launch_compact(cap, FreePred{used}, IdentityVal{}, free_scratch, n, free_slot[cur ^ 1], nullptr, stream);
-    TEMO_CUDA(cudaEventRecord(ev[4], stream));
+    TEMO_CUDA(cudaEventRecord(evs[4], stream));
 
     // reference-vector adaptation (algorithms.hpp:281)
     if ((t + 1) % adapt_every == 0) {
@@ -417,7 +420,7 @@ uint64_t Run::step(double* survivors_f_host, const double* f_off_inject) {
         launch_gamma_auto(v, r, m, ws, &vindex, gamma, ws.err_flag, skip_flag, stream);
         launches += 6 + vindex.levels;
     }
-    TEMO_CUDA(cudaEventRecord(ev[5], stream));
+    TEMO_CUDA(cudaEventRecord(evs[5], stream));
     TEMO_CUDA(cudaMemcpyAsync(h_status, ws.err_flag, sizeof(uint32_t), cudaMemcpyDeviceToHost, stream));
     TEMO_CUDA(cudaMemcpyAsync(h_status + 1, d_P, sizeof(uint32_t), cudaMemcpyDeviceToHost, stream));
     TEMO_CUDA(cudaGetLastError());
@@ -432,6 +435,7 @@ uint64_t Run::step(double* survivors_f_host, const double* f_off_inject) {
         ensure_permutation(next);
     }
     const double host3 = now_ms();
+    if (timings_pending) resolve_timings();  // the previous step's stage times, read while this one runs
 
     TEMO_CUDA(cudaStreamSynchronize(stream));
     if (h_status[0] & 1u) fail(1, "rv_select: gamma must be positive");
@@ -442,16 +446,38 @@ uint64_t Run::step(double* survivors_f_host, const double* f_off_inject) {
     if (survivors_f_host)
         TEMO_CUDA(cudaMemcpy(survivors_f_host, fm[cur], P * m * sizeof(double), cudaMemcpyDeviceToHost));
     if (track_archive) archive_insert();  // algorithms.hpp:282
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, ev[0], ev[5]); timings[0] = ms;
-    cudaEventElapsedTime(&ms, ev[1], ev[2]); timings[1] = ms;
-    cudaEventElapsedTime(&ms, ev[2], ev[3]); timings[2] = ms;
-    cudaEventElapsedTime(&ms, ev[3], ev[4]); timings[3] = ms;
-    cudaEventElapsedTime(&ms, ev[4], ev[5]); timings[4] = ms;
-    timings[5] = (host1 - host0) + (host3 - host2);
-    timings[6] = (double)launches;
-    cudaEventElapsedTime(&ms, ev[0], ev[1]); timings[7] = ms;
+    pending_host_ms = (host1 - host0) + (host3 - host2);
+    pending_launches = (double)launches;
+    timings_pending = true;
+    evp ^= 1;
     return P;
+}
+
+void Run::resolve_timings() {
+    if (!timings_pending) return;
+    cudaEvent_t* const e = ev[evp ^ 1];  // the last finished step's set
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e[0], e[5]); timings[0] = ms;
+    cudaEventElapsedTime(&ms, e[1], e[2]); timings[1] = ms;
+    cudaEventElapsedTime(&ms, e[2], e[3]); timings[2] = ms;
+    cudaEventElapsedTime(&ms, e[3], e[4]); timings[3] = ms;
+    cudaEventElapsedTime(&ms, e[4], e[5]); timings[4] = ms;
+    timings[5] = pending_host_ms;
+    timings[6] = pending_launches;
+    cudaEventElapsedTime(&ms, e[0], e[1]); timings[7] = ms;
+    timings_pending = false;
+    if (timing_log.empty()) timing_log.resize(kTimingLog * 8);
+    std::memcpy(&timing_log[(timing_steps % kTimingLog) * 8], timings, 8 * sizeof(double));
+    ++timing_steps;
+}
+
+uint64_t Run::timing_history(double* out, uint64_t max_steps, bool reset) {
+    resolve_timings();
+    const uint64_t have = std::min<uint64_t>(timing_steps, kTimingLog), count = std::min(have, max_steps);
+    for (uint64_t i = 0; i < count; ++i)
+        std::memcpy(out + i * 8, &timing_log[((timing_steps - count + i) % kTimingLog) * 8], 8 * sizeof(double));
+    if (reset) timing_steps = 0;
+    return count;
 }
 
 void Run::inject(uint64_t rows, const double* x, const double* f, const double* v_in, const double* gamma_in,

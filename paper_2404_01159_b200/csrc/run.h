@@ -120,8 +120,18 @@ struct Run {
     bool spec_valid = false;
     uint64_t spec_c_shuffle = 0;
     uint32_t* h_status = nullptr;  // pinned: [0] error flags, [1] survivor count
-    cudaEvent_t ev[kNumEvents]{};
+    // Stage events of a step, double-buffered: the elapsed times of step t are read while step t + 1 runs on the device
+    // (or when somebody asks for them), not between the end of step t and the first launch of step t + 1.
+    cudaEvent_t ev[2][kNumEvents]{};
+    int evp = 0;                   // event set of the step being enqueued
+    bool timings_pending = false;  // the last finished step's events (set evp ^ 1) have not been read yet
+    double pending_host_ms = 0.0, pending_launches = 0.0;
     double timings[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    static constexpr uint64_t kTimingLog = 1024;  // steps kept
+    std::vector<double> timing_log;               // 8 values per step, ring
+    uint64_t timing_steps = 0;                    // steps logged since the last reset
+    void resolve_timings();                       // reads the pending events into `timings` and the log
+    uint64_t timing_history(double* out, uint64_t max_steps, bool reset);  // oldest first; returns the number of steps written
 
 private:
     void check_status();
