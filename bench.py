@@ -340,7 +340,7 @@ def run_ours(args):
     t1 = time.perf_counter()
     for _ in range(K):
         p, f_host = run.step(want_f=True)
-        d2h.append(8 + p * m * 8)
+        d2h.append(8 + min(r, p + n) * m * 8)  # status words + the block the library copies (one row per reference vector at most)
     tb._lib.check(tb._lib.load().temo_b200_dev_sync())
     wall_e2e = time.perf_counter() - t1
     clocks = sampler.stop()

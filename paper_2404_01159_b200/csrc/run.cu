@@ -421,6 +421,11 @@ uint64_t Run::step(double* survivors_f_host, const double* f_off_inject) {
         launches += 6 + vindex.levels;
     }
     TEMO_CUDA(cudaEventRecord(evs[5], stream));
+    // the survivors' objectives for the caller: at most kmax rows survive (one per reference vector), and they sit at the
+    // head of the next generation's objective block; copied in the stream, so the step has ONE host round trip (the count
+    // is only known afterwards: the caller's buffer holds r x m doubles by contract)
+    if (survivors_f_host)
+        TEMO_CUDA(cudaMemcpyAsync(survivors_f_host, fm[cur ^ 1], kmax * m * sizeof(double), cudaMemcpyDeviceToHost, stream));
     TEMO_CUDA(cudaMemcpyAsync(h_status, ws.err_flag, sizeof(uint32_t), cudaMemcpyDeviceToHost, stream));
     TEMO_CUDA(cudaMemcpyAsync(h_status + 1, d_P, sizeof(uint32_t), cudaMemcpyDeviceToHost, stream));
     TEMO_CUDA(cudaGetLastError());
@@ -443,8 +448,6 @@ uint64_t Run::step(double* survivors_f_host, const double* f_off_inject) {
     P = h_status[1];
     cur ^= 1;
     ++t;
-    if (survivors_f_host)
-        TEMO_CUDA(cudaMemcpy(survivors_f_host, fm[cur], P * m * sizeof(double), cudaMemcpyDeviceToHost));
     if (track_archive) archive_insert();  // algorithms.hpp:282
     pending_host_ms = (host1 - host0) + (host3 - host2);
     pending_launches = (double)launches;
