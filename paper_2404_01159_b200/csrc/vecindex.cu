@@ -32,6 +32,17 @@ namespace temo_b200 {
 namespace {
 
 constexpr double kSlack = 1e-12;  // >> fp64 rounding of a cosine (~4e-16), << any decision it guards
+// The search divides only where the reference's exact expression is needed. Everywhere else (the centres of the tree's
+// nodes, and the leaf vectors that cannot reach the best cosine realised so far) a cosine is dot * rcp(nf * |v|) with the
+// hardware's approximate fp64 reciprocal (rcp.approx.ftz.f64: relative error <= 1.0e-6 measured over 2.7e8 arguments on
+// a B200, tools/rcp_check.cu; 2^-20 by the PTX manual). kApprox bounds the error of such a cosine (|cos| <= 1 up to
+// rounding) with a factor of four in hand; every decision taken on an approximate cosine is widened by it.
+constexpr double kApprox = 4e-6;
+__device__ __forceinline__ double rcp_approx(double x) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    return r;
+}
 
 __device__ __forceinline__ unsigned long long order_key(double x) {
     const unsigned long long b = (unsigned long long)__double_as_longlong(x);
@@ -248,22 +259,27 @@ struct Searcher {
     float Lf;
     float Lf_seen;  // the L for which (Lb, Sb) below were computed
     double Lb, Sb;  // L - slack and sqrt(1 - Lb^2)
+    bool exact_all;  // exhaustive scans (rows or vector sets with negative components): L says nothing about negative cosines
 
-    __device__ __forceinline__ double cosine(const double* rec) const {
+    __device__ __forceinline__ double dot_with(const double* rec) const {  // ascending k, multiply and add: the reference's dot
         double dot = 0.0;
 #pragma unroll
         for (int k = 0; k < MM; ++k)
             if (k < m) dot += row.u[k] * rec[k];
-        return dot / (row.nf * rec[m]);  // selection.hpp:178 / refvec.hpp:92
+        return dot;
+    }
+    __device__ __forceinline__ double cosine_approx(const double* rec) const {  // within kApprox of the exact expression
+        return dot_with(rec) * rcp_approx(row.nf * rec[m]);
     }
 
+    // q: approximate cosine to the node's centre
     __device__ __forceinline__ bool passes(double q, double cr, double sr) {
         if (Lf != Lf_seen) {  // warp-uniform: L is the same in every lane
             Lf_seen = Lf;
             Lb = (double)Lf - kSlack;
             Sb = sqrt(fmax(0.0, 1.0 - Lb * Lb));
         }
-        return q + kSlack >= Lb * cr - Sb * sr;
+        return q + (kSlack + kApprox) >= Lb * cr - Sb * sr;
     }
 
     __device__ __forceinline__ void leaf(uint64_t group) {
@@ -272,10 +288,16 @@ struct Searcher {
         if (p < ix.r) {
             const uint32_t j = ix.orig[p];
             if (j != row.self) {
-                c = cosine(ix.vp + p * (m + 1));
-                if (c > best_c || (c == best_c && j < best_j)) {
-                    best_c = c;
-                    best_j = j;
+                const double* rec = ix.vp + p * (m + 1);
+                const double dot = dot_with(rec), den = row.nf * rec[m];
+                // L is a lower bound of a cosine some vector has realised: a vector whose cosine cannot reach it is not
+                // the maximum (nor a tie for it) and is not divided for
+                if (exact_all || !(dot * rcp_approx(den) + kApprox < (double)Lf)) {
+                    c = dot / den;  // selection.hpp:178 / refvec.hpp:92
+                    if (c > best_c || (c == best_c && j < best_j)) {
+                        best_c = c;
+                        best_j = j;
+                    }
                 }
             }
         }
@@ -291,14 +313,14 @@ struct Searcher {
             double q = -1.0, cr = 1.0, sr = 0.0;
             if (valid) {
                 const double* rec = ix.node[LVL] + id * (m + 3);
-                q = cosine(rec);
+                q = cosine_approx(rec);
                 cr = rec[m + 1];
                 sr = rec[m + 2];
                 if (!(q == q)) q = 2.0;  // a NaN cosine never prunes
             }
-            // a centre is a realised cosine: it raises L unless it is the excluded vector itself
+            // a centre is a realised cosine: it raises L (by its lower bound) unless it is the excluded vector itself
             const bool is_self = valid && row.self != 0xffffffffu && ix.orig[ix.centre[LVL][id]] == row.self;
-            Lf = warp_max_lower((valid && !is_self && q <= 1.5) ? q : -1.0, Lf);
+            Lf = warp_max_lower((valid && !is_self && q <= 1.5) ? q - kApprox : -1.0, Lf);
             unsigned done = 0;
             // best-first: the passing child whose centre is closest to the row is opened first, which raises L to
             // (nearly) its final value at once and prunes most siblings; the order of visits does not change the
@@ -344,7 +366,7 @@ struct Searcher {
 template <int M>
 __device__ __forceinline__ void search_row(const IndexView& ix, const Row<M>& row, int m, bool prunable,
                                            double* best_c, uint32_t* best_j) {
-    Searcher<M> s{ix, row, m, (int)(threadIdx.x & 31), -INFINITY, 0xffffffffu, 0.0f, -1.0f, 0.0, 1.0};
+    Searcher<M> s{ix, row, m, (int)(threadIdx.x & 31), -INFINITY, 0xffffffffu, 0.0f, -1.0f, 0.0, 1.0, !prunable};
     if (!prunable) {
         s.exhaustive();
     } else {
