@@ -598,23 +598,21 @@ void launch_dtlz(const EvalK& k, bool tma, cudaStream_t s) {
     if (tma && eval_tma_enabled() && vec == 2 && block == 256 && k.d <= (uint64_t)kRowWarpGenes) {  // one warp per row
         const uint32_t stage_genes = (uint32_t)((k.d + 15) / 16 * 16);
         const size_t smem = (size_t)kRowWarps * kStages * stage_genes * sizeof(double);
-        static bool configured = false;
-        if (!configured) {
+        static std::once_flag configured;  // per instantiation; shards of one process may launch concurrently
+        std::call_once(configured, [] {
             TEMO_CUDA(cudaFuncSetAttribute(eval_tma_rows_kernel<PID>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)(kRowWarps * kStages * kRowWarpGenes * sizeof(double))));
-            configured = true;
-        }
+        });
         const uint64_t ctas_per_sm = std::max<uint64_t>(1, std::min<uint64_t>(16, (200u * 1024u) / (smem + 1024)));
         const uint64_t grid = std::min<uint64_t>((uint64_t)kSMs * ctas_per_sm, (k.n + kRowWarps - 1) / kRowWarps);
         eval_tma_rows_kernel<PID><<<(unsigned)grid, kRowWarps * 32, smem, s>>>(k, stage_genes);
         eval_finish_kernel<PID><<<(unsigned)((k.n + 127) / 128), 128, 0, s>>>(k.f, k.n, k.m, k.d, k.f_row0, k.f_row0_dev);
     } else if (tma && eval_tma_enabled() && vec == 2 && block == 256) {
         const size_t smem = sizeof(EvalTmaSmem);
-        static bool configured = false;
-        if (!configured) {
-            TEMO_CUDA(cudaFuncSetAttribute(eval_tma_kernel<PID>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            configured = true;
-        }
+        static std::once_flag configured;
+        std::call_once(configured, [] {
+            TEMO_CUDA(cudaFuncSetAttribute(eval_tma_kernel<PID>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(EvalTmaSmem)));
+        });
         uint64_t grid = (uint64_t)kSMs * TEMO_EVAL_CTAS;
         if (grid > k.n) grid = k.n;
         eval_tma_kernel<PID><<<(unsigned)grid, 256, smem, s>>>(k);
@@ -707,25 +705,23 @@ void launch_evaluate(const EvalArgs& a, cudaStream_t s) {
         const LsmopLayout lay = lsmop1_layout(a.d, a.m);
         const int touch = a.allow_tma && eval_tma_enabled() && row_vec(a.d) == 2 && block == 256 ? lsmop_tma_touch(lay, a.d, a.m) : 0;
         if (touch) {
-            static bool configured = false;
-            if (!configured) {
+            static std::once_flag configured;
+            std::call_once(configured, [] {
                 TEMO_CUDA(cudaFuncSetAttribute(eval_lsmop1_tma_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LsmopTmaSmem)));
                 TEMO_CUDA(cudaFuncSetAttribute(eval_lsmop1_tma_kernel<kLsmopTouch>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LsmopTmaSmem)));
-                configured = true;
-            }
+            });
             const uint64_t grid = std::min<uint64_t>((uint64_t)kSMs * TEMO_EVAL_CTAS, a.n);
             if (touch <= 2)
                 eval_lsmop1_tma_kernel<2><<<(unsigned)grid, 256, sizeof(LsmopTmaSmem), s>>>(k, lay, coef);
             else
                 eval_lsmop1_tma_kernel<kLsmopTouch><<<(unsigned)grid, 256, sizeof(LsmopTmaSmem), s>>>(k, lay, coef);
         } else if (smem > 48 * 1024 && ([&] {  // m x block partials beyond the default dynamic shared memory (m > 24)
-                       static bool configured = false;
-                       if (!configured) {
+                       static std::once_flag configured;
+                       std::call_once(configured, [] {
                            const int most = kMaxObj * 256 * (int)sizeof(double);
                            TEMO_CUDA(cudaFuncSetAttribute(eval_lsmop1_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, most));
                            TEMO_CUDA(cudaFuncSetAttribute(eval_lsmop1_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, most));
-                           configured = true;
-                       }
+                       });
                        return false;
                    })()) {
         } else if (row_vec(a.d) == 2)

@@ -1012,14 +1012,15 @@ void launch_pairs_seg(const ReproK& k, uint64_t units, cudaStream_t s) {
     constexpr int NW = TEAM == 1 ? kSoloWarps : kVirtWarps;
     constexpr int kCtas = TEAM == 1 ? kSoloCtas : TEMO_PAIR_MIN_BLOCKS;
     static int grid = 0;  // per instantiation
-    if (grid == 0) {
+    static std::once_flag configured;  // shards of one process may launch concurrently
+    std::call_once(configured, [] {
         TEMO_CUDA(cudaFuncSetAttribute(reproduce_pairs_kernel<MODE, EVAL, SEG, TEAM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)sizeof(PairSmemT<NW>)));
         int dev = 0, sms = 0;
         TEMO_CUDA(cudaGetDevice(&dev));
         TEMO_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
         grid = (sms > 0 ? sms : kSMs) * kCtas;
-    }
+    });
     ReproK kk = k;
     kk.work_counter = nullptr;
     if (k1_options().dynamic_pairs) {
