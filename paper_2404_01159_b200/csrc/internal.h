@@ -156,7 +156,11 @@ struct SelectWorkspace {
     uint32_t* v32_flags = nullptr;    // [1] bit0: a vector component is negative / non-finite
     double* part_c = nullptr;         // [chunks x rows_cap] per-chunk winners of the filtered association (m >= 5 only)
     uint32_t* part_j = nullptr;
-    unsigned char* row_flag = nullptr;  // [rows_cap] rows of the filtered scan that need the exact fallback
+    uint32_t* row_flag = nullptr;       // [rows_cap] rows of the filtered scan that need the fallback (1 near-ties, 2 exact only)
+    uint32_t* flag_list = nullptr;      // [rows_cap] those rows, compacted; flag_count [1]
+    uint32_t* flag_count = nullptr;
+    double* fb_c = nullptr;             // [rows_cap + kFallbackItems] partial winners of the fallback's (row, vector range) items
+    uint32_t* fb_j = nullptr;
     float* seed32 = nullptr;            // [rows_cap] starting value of a row's running fp32 maximum (subsample scan)
     void alloc(uint64_t rows_cap_, uint64_t r_, uint64_t m_);
     void release();

@@ -298,13 +298,14 @@ __global__ void __launch_bounds__(kFilterThreads) filter_seed_kernel(const doubl
 // to the end of the scan - the threshold only depends on the fp32 scores - when most of them have fallen below the final
 // threshold and are dropped: a few exact evaluations per row remain instead of one per running-maximum record.
 constexpr int kFilterCand = 6;  // candidate slots per row (pruned against the risen threshold when full)
+constexpr int kFallbackItems = 8192;  // (row, vector range) items the fallback spreads its rows over (when there are fewer rows)
 
 template <int M, bool SELF>
 __global__ void __launch_bounds__(kFilterThreads, 4) assoc_filter_kernel(
     const double* __restrict__ f, uint64_t n_rows, uint64_t m_rt, const double* __restrict__ z, const double* __restrict__ v,
     const double* __restrict__ vn, const float* __restrict__ v32, const uint32_t* __restrict__ vflags, uint64_t r, uint64_t chunk_vecs,
-    double* __restrict__ part_c, uint32_t* __restrict__ part_j, unsigned char* __restrict__ row_flag, const float* __restrict__ seed,
-    const uint32_t* skip_flag) {
+    double* __restrict__ part_c, uint32_t* __restrict__ part_j, uint32_t* __restrict__ row_flag, uint32_t* __restrict__ flag_list,
+    uint32_t* __restrict__ flag_count, const float* __restrict__ seed, const uint32_t* skip_flag) {
     // blockIdx.y = chunk of the vector range [y * chunk_vecs, (y + 1) * chunk_vecs): the per-row winners of the chunks are
     // merged in ascending chunk order afterwards (strict >: the first strict maximum overall)
     if (skip_flag && *skip_flag) return;
@@ -320,13 +321,13 @@ __global__ void __launch_bounds__(kFilterThreads, 4) assoc_filter_kernel(
     const bool v_ok = (*vflags & 1u) == 0;
     uint32_t row[R], cnt[R];
     float uf[R][MM], best32[R], thr[R];
-    bool overflow[R];
+    bool overflow[R], exact_only[R];
 #pragma unroll
     for (int t = 0; t < R; ++t) {
         row[t] = (uint32_t)(blockIdx.x * (uint64_t)(R * kFilterThreads) + t * kFilterThreads + threadIdx.x);
         const bool live = row[t] < n_rows;
         cnt[t] = 0;
-        overflow[t] = false;
+        overflow[t] = exact_only[t] = false;
         bool filter = v_ok && live;
         double fp[MM], nf = 0.0;
         if (live) {
@@ -353,7 +354,7 @@ __global__ void __launch_bounds__(kFilterThreads, 4) assoc_filter_kernel(
             thr[t] = INFINITY;  // nothing to do (selection.hpp:167-169: arg 0, theta 0)
         } else if (!filter) {   // the exact expression for every vector: filter_fallback_kernel
             thr[t] = INFINITY;
-            overflow[t] = true;
+            overflow[t] = exact_only[t] = true;
         }
     }
     const uint64_t j_begin = blockIdx.y * chunk_vecs, j_end = j_begin + chunk_vecs < r ? j_begin + chunk_vecs : r;
@@ -451,7 +452,9 @@ __global__ void __launch_bounds__(kFilterThreads, 4) assoc_filter_kernel(
         double best_c = -INFINITY;
         uint32_t arg = 0;
         if (overflow[t]) {
-            row_flag[row[t]] = 1;
+            // 2: a property of the row (every chunk says so); 1: more near-ties than slots. The first chunk to flag a row
+            // appends it to the fallback's list.
+            if (atomicExch(&row_flag[row[t]], exact_only[t] ? 2u : 1u) == 0u) flag_list[atomicAdd(flag_count, 1u)] = row[t];
         } else if (cnt[t]) {
             const double nf = SELF ? vn[row[t]] : [&] {
                 double s = 0.0;
@@ -477,51 +480,133 @@ __global__ void __launch_bounds__(kFilterThreads, 4) assoc_filter_kernel(
     }
 }
 
-// Rows the filter does not apply to (a negative / non-finite / fp32-unrepresentable component, a bad vector set, or more
-// near-ties than candidate slots): the reference's expression for every vector, one warp per flagged row, first strict
-// maximum (lexicographic max cosine / lowest j across the lanes). Result into chunk slot 0 (the scan left -inf everywhere).
-template <bool SELF>
-__global__ void filter_fallback_kernel(const double* __restrict__ f, uint64_t n_rows, uint64_t m, const double* __restrict__ z,
-                                       const double* __restrict__ v, const double* __restrict__ vn, uint64_t r,
-                                       const unsigned char* __restrict__ row_flag, double* __restrict__ part_c,
-                                       uint32_t* __restrict__ part_j, const uint32_t* skip_flag) {
+// Rows the scan gave up on (a handful per generation, but a single warp needs 0.8 ms for the 48620 vectors of config #4:
+// the latency of one serial scan used to be a fifth of the selection). The flagged rows are compacted by the scan; every
+// row is cut into S vector ranges (S = kFallbackItems / rows, at most 64) and a warp takes one (row, range) item at a time;
+// filter_fallback_merge_kernel then reduces the S partial winners of a row into chunk slot 0 (the chunk merge keeps the
+// first strict maximum).
+//   flag 1, more near-ties than candidate slots (rows with several near-zero components see many vectors of almost the
+//     same cosine): the same filter without slots - a lane walks its vectors in ascending j, scores them in fp32 and
+//     evaluates the reference's expression at once for every vector within kFilterTol of its running fp32 maximum (seeded
+//     like the scan's). The argument of the scan carries over: the vector that attains the exact maximum scores within
+//     2 * 2.1e-6 of the fp32 maximum, hence above every lane's running threshold.
+//   flag 2, rows the filter does not apply to (a negative / non-finite / fp32-unrepresentable component, a bad vector
+//     set): the reference's expression for every vector.
+// Lexicographic reduction (max cosine, lowest j) across lanes and ranges = the first strict maximum.
+__device__ __forceinline__ uint32_t fallback_split(uint32_t rows) {
+    const uint32_t s = rows ? (uint32_t)kFallbackItems / rows : 1u;
+    return s < 1u ? 1u : (s > 64u ? 64u : s);
+}
+
+template <int M, bool SELF>
+__global__ void __launch_bounds__(128) filter_fallback_kernel(
+    const double* __restrict__ f, uint64_t m_rt, const double* __restrict__ z, const double* __restrict__ v,
+    const double* __restrict__ vn, const float* __restrict__ v32, const float* __restrict__ seed, uint64_t r,
+    const uint32_t* __restrict__ row_flag, const uint32_t* __restrict__ flag_list, const uint32_t* __restrict__ flag_count,
+    double* __restrict__ fb_c, uint32_t* __restrict__ fb_j, const uint32_t* skip_flag) {
     if (skip_flag && *skip_flag) return;
-    const uint64_t row = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    constexpr int MM = M > 0 ? M : kMaxObj;
+    constexpr int SS = (MM + 3) / 4 * 4;
+    const int m = M > 0 ? M : (int)m_rt;
+    const int stride = M > 0 ? SS : (int)v32_stride(m);
     const uint32_t lane = threadIdx.x & 31;
-    if (row >= n_rows || !row_flag[row]) return;
-    double nf;
-    if (SELF) {
-        nf = vn[row];
-    } else {
-        double s = 0.0;
-        for (uint64_t k = 0; k < m; ++k) {
-            const double x = f[row * m + k] - z[k];
-            s += x * x;
+    const uint32_t count = *flag_count, S = fallback_split(count);
+    const uint64_t items = (uint64_t)count * S, warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint64_t len = (r + S - 1) / S;  // vectors per range
+    for (uint64_t item = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; item < items; item += warps) {
+        const uint64_t row = flag_list[item / S], j_begin = (item % S) * len, j_end = j_begin + len < r ? j_begin + len : r;
+        const unsigned flag = row_flag[row];
+        double nf;
+        if (SELF) {
+            nf = vn[row];
+        } else {
+            double s = 0.0;
+            for (int k = 0; k < m; ++k) {
+                const double x = f[row * m + k] - z[k];
+                s += x * x;
+            }
+            nf = sqrt(s);
         }
-        nf = sqrt(s);
-    }
-    double best_c = -INFINITY;
-    uint32_t arg = 0xffffffffu;
-    for (uint64_t j = lane; j < r; j += 32) {
-        if (SELF && j == row) continue;
-        double dot = 0.0;
-        for (uint64_t k = 0; k < m; ++k) dot += (SELF ? f[row * m + k] : f[row * m + k] - z[k]) * v[j * m + k];
-        const double c = dot / (nf * vn[j]);
-        if (c > best_c) {
-            best_c = c;
-            arg = (uint32_t)j;
-        }
-    }
+        double best_c = -INFINITY;
+        uint32_t arg = 0xffffffffu;
+        if (flag == 1) {
+            float uf[MM];
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-        const double oc = __shfl_xor_sync(0xffffffffu, best_c, off);
-        const uint32_t oj = __shfl_xor_sync(0xffffffffu, arg, off);
-        if (oc > best_c || (oc == best_c && oj < arg)) {
-            best_c = oc;
-            arg = oj;
+            for (int k = 0; k < MM; ++k) {
+                const double uk = (k < m && nf != 0.0) ? (SELF ? f[row * m + k] : f[row * m + k] - z[k]) / nf : 0.0;
+                uf[k] = (float)uk;  // the scan's conversion
+            }
+            float best32 = seed[row], thr = best32 * (1.0f - kFilterTol);
+            for (uint64_t j = j_begin + lane; j < j_end; j += 32) {
+                const float4* p4 = reinterpret_cast<const float4*>(v32 + j * stride);
+                float sc = 0.0f;
+#pragma unroll
+                for (int k4 = 0; k4 < SS / 4; ++k4)
+                    if (4 * k4 < m) {
+                        const float4 t4 = __ldg(p4 + k4);
+                        sc = fmaf(uf[4 * k4], t4.x, sc);
+                        if (4 * k4 + 1 < MM) sc = fmaf(uf[4 * k4 + 1 < MM ? 4 * k4 + 1 : 0], t4.y, sc);
+                        if (4 * k4 + 2 < MM) sc = fmaf(uf[4 * k4 + 2 < MM ? 4 * k4 + 2 : 0], t4.z, sc);
+                        if (4 * k4 + 3 < MM) sc = fmaf(uf[4 * k4 + 3 < MM ? 4 * k4 + 3 : 0], t4.w, sc);
+                    }
+                if (!(sc >= thr)) continue;
+                if (SELF && j == row) continue;  // refvec.hpp:91
+                if (sc > best32) {
+                    best32 = sc;
+                    thr = sc * (1.0f - kFilterTol);
+                }
+                const double c = exact_cosine(f + row * m, SELF ? nullptr : z, v + j * m, nf, vn[j], m);
+                if (c > best_c) {
+                    best_c = c;
+                    arg = (uint32_t)j;
+                }
+            }
+        } else {
+            for (uint64_t j = j_begin + lane; j < j_end; j += 32) {
+                if (SELF && j == row) continue;
+                double dot = 0.0;
+                for (int k = 0; k < m; ++k) dot += (SELF ? f[row * m + k] : f[row * m + k] - z[k]) * v[j * m + k];
+                const double c = dot / (nf * vn[j]);
+                if (c > best_c) {
+                    best_c = c;
+                    arg = (uint32_t)j;
+                }
+            }
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const double oc = __shfl_xor_sync(0xffffffffu, best_c, off);
+            const uint32_t oj = __shfl_xor_sync(0xffffffffu, arg, off);
+            if (oc > best_c || (oc == best_c && oj < arg)) {
+                best_c = oc;
+                arg = oj;
+            }
+        }
+        if (lane == 0) {
+            fb_c[item] = best_c;
+            fb_j[item] = arg;
         }
     }
-    if (lane == 0) {
+}
+
+// the S partial winners of every flagged row -> chunk slot 0 of the scan's scratch
+__global__ void filter_fallback_merge_kernel(const uint32_t* __restrict__ flag_list, const uint32_t* __restrict__ flag_count,
+                                             const double* __restrict__ fb_c, const uint32_t* __restrict__ fb_j,
+                                             double* __restrict__ part_c, uint32_t* __restrict__ part_j, const uint32_t* skip_flag) {
+    if (skip_flag && *skip_flag) return;
+    const uint32_t count = *flag_count, S = fallback_split(count);
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count; i += (uint64_t)gridDim.x * blockDim.x) {
+        double best_c = -INFINITY;
+        uint32_t arg = 0xffffffffu;
+        for (uint32_t k = 0; k < S; ++k) {
+            const double c = fb_c[i * S + k];
+            const uint32_t j = fb_j[i * S + k];
+            if (c > best_c || (c == best_c && j < arg)) {
+                best_c = c;
+                arg = j;
+            }
+        }
+        const uint32_t row = flag_list[i];
         part_c[row] = best_c;
         part_j[row] = arg == 0xffffffffu ? 0u : arg;
     }
@@ -667,7 +752,11 @@ void SelectWorkspace::alloc(uint64_t rows_cap_, uint64_t r_, uint64_t m_) {
     if (assoc_filter_preferred(m, r)) {
         part_c = dev_alloc<double>(rows_cap * kFilterMaxChunks);
         part_j = dev_alloc<uint32_t>(rows_cap * kFilterMaxChunks);
-        row_flag = dev_alloc<unsigned char>(rows_cap);
+        row_flag = dev_alloc<uint32_t>(rows_cap);
+        flag_list = dev_alloc<uint32_t>(rows_cap);
+        flag_count = dev_alloc<uint32_t>(1);
+        fb_c = dev_alloc<double>(rows_cap + kFallbackItems);
+        fb_j = dev_alloc<uint32_t>(rows_cap + kFallbackItems);
         seed32 = dev_alloc<float>(rows_cap);
     }
     TEMO_CUDA(cudaMemset(err_flag, 0, sizeof(uint32_t)));
@@ -677,6 +766,7 @@ void SelectWorkspace::release() {
     cudaFree(z); cudaFree(zkey); cudaFree(vn); cudaFree(assoc); cudaFree(theta); cudaFree(apd);
     cudaFree(best_key); cudaFree(best_row); cudaFree(first_row); cudaFree(elite); cudaFree(valid);
     cudaFree(n_elite); cudaFree(err_flag); cudaFree(tile_scratch); cudaFree(v32); cudaFree(v32_flags); cudaFree(part_c); cudaFree(part_j); cudaFree(row_flag); cudaFree(seed32);
+    cudaFree(flag_list); cudaFree(flag_count); cudaFree(fb_c); cudaFree(fb_j);
     *this = SelectWorkspace{};
 }
 
@@ -752,7 +842,8 @@ uint32_t launch_filter_scan(const double* rows, uint64_t n_rows, uint64_t m, con
     const size_t smem = (size_t)(kFilterTile + kFilterVecs) * v32_stride(m) * sizeof(float) +
                         (size_t)kFilterRows * kFilterCand * kFilterThreads * (sizeof(uint32_t) + sizeof(float));
     require(ws.row_flag != nullptr, "rv_select: workspace has no row flags");
-    TEMO_CUDA(cudaMemsetAsync(ws.row_flag, 0, n_rows, s));
+    TEMO_CUDA(cudaMemsetAsync(ws.row_flag, 0, n_rows * sizeof(uint32_t), s));
+    TEMO_CUDA(cudaMemsetAsync(ws.flag_count, 0, sizeof(uint32_t), s));
     float* seed = ws.seed32;
 #define CALL(MV)                                                                                                                  \
     {                                                                                                                             \
@@ -765,7 +856,10 @@ uint32_t launch_filter_scan(const double* rows, uint64_t n_rows, uint64_t m, con
                                        kFilterThreads, (size_t)kFilterTile * v32_stride(m) * sizeof(float), s>>>(                \
             rows, n_rows, m, z, ws.vn, ws.v32, r, seed, skip_flag);                                                               \
         assoc_filter_kernel<MV, SELF><<<grid, kFilterThreads, smem, s>>>(rows, n_rows, m, z, v, ws.vn, ws.v32, ws.v32_flags, r,    \
-                                                                         chunk_vecs, ws.part_c, ws.part_j, ws.row_flag, seed, skip_flag); \
+                                                                         chunk_vecs, ws.part_c, ws.part_j, ws.row_flag, ws.flag_list, ws.flag_count, seed, \
+                                                                         skip_flag);                                              \
+        filter_fallback_kernel<MV, SELF><<<kSMs * 8, 128, 0, s>>>(rows, m, z, v, ws.vn, ws.v32, seed, r, ws.row_flag, ws.flag_list, \
+                                                                  ws.flag_count, ws.fb_c, ws.fb_j, skip_flag);                      \
     }
     switch (m) {
     case 5: CALL(5); break;
@@ -773,8 +867,7 @@ uint32_t launch_filter_scan(const double* rows, uint64_t n_rows, uint64_t m, con
     default: CALL(0); break;
     }
 #undef CALL
-    filter_fallback_kernel<SELF><<<(unsigned)((n_rows + 3) / 4), 128, 0, s>>>(rows, n_rows, m, z, v, ws.vn, r, ws.row_flag, ws.part_c,
-                                                                            ws.part_j, skip_flag);
+    filter_fallback_merge_kernel<<<64, 256, 0, s>>>(ws.flag_list, ws.flag_count, ws.fb_c, ws.fb_j, ws.part_c, ws.part_j, skip_flag);
     TEMO_CUDA(cudaGetLastError());
     return (uint32_t)chunks;
 }
