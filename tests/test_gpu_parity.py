@@ -658,6 +658,42 @@ def test_rv_select_many_objectives_filter(tb, oracle, cfg):
         _check_selection(tb.rv_select(f, tb.RefVectorSet(v0, vbig, gamma), 10, 100, 2.0), oracle.rv_select(f, vbig, gamma, 10, 100, 2.0))
 
 
+def test_rv_select_many_objectives_near_ties_overflow(tb, oracle):
+    """Rows with more near-tied best vectors than the scan has candidate slots (six): directions with several equal or
+    near-zero components, for which whole orbits of lattice vectors have the same cosine up to rounding. They go to the
+    fallback (the filter without slots, a row spread over many warps): association, validity and survivors are still the
+    reference's first strict maximum."""
+    m, H = 10, 6
+    v0, gamma = oracle.make_ref_set(m, H)
+    n = 600
+    f = Stream(oracle, 9900).tensor(n, m) + 0.05
+    base = np.zeros(m)
+    f[0] = base  # the ideal point: every other row is a direction from here
+    rng = np.random.default_rng(5)
+    pat = []
+    for ones in (2, 3, 4, 5, 8, 10):  # `ones` equal components, zeros elsewhere: C(ones, k) tied vectors
+        u = np.zeros(m)
+        u[:ones] = 1.0
+        pat.append(u)
+    pat.append(np.array([1, 1, 1, 1, 1, 1, 1, 1, 1e-9, 1e-9]))
+    pat.append(np.array([3, 3, 3, 1e-12, 1e-12, 1e-12, 0, 0, 0, 0.0]))
+    k = 1
+    for u in pat:
+        for scale in (1.0, 7.5):
+            f[k] = base + scale * u
+            k += 1
+            f[k] = base + scale * u * (1.0 + 1e-9 * rng.standard_normal(m))  # near-ties instead of exact ones
+            f[k] = np.maximum(f[k], base)
+            k += 1
+            f[k] = base + scale * rng.permutation(u)
+            k += 1
+    for adapted in (False, True):
+        v, g = v0, gamma
+        if adapted:
+            v, g = oracle.adapt(v0, v0, gamma, base, base + np.linspace(0.5, 3.0, m))
+        _check_selection(tb.rv_select(f, tb.RefVectorSet(v0, v, g), 20, 100, 2.0), oracle.rv_select(f, v, g, 20, 100, 2.0))
+
+
 @pytest.mark.parametrize("mh", [(10, 5), (5, 10), (6, 6)])
 def test_gamma_many_objectives_filter(tb, oracle, mh):
     """min_vector_angles for m >= 5 and R >= 256 goes through the fp32-filtered exact scan (rows = the vectors themselves,
