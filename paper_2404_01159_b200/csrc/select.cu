@@ -217,6 +217,23 @@ __device__ __noinline__ double exact_cosine(const double* __restrict__ frow, con
     return dot / (nf * vnj);
 }
 
+// packed fp32 pairs (sm_100: FFMA2)
+__device__ __forceinline__ uint64_t pack2(float a, float b) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+    uint64_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ float sum2(uint64_t a) {
+    float x, y;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(x), "=f"(y) : "l"(a));
+    return x + y;
+}
+
 // Seed of the running threshold: the best fp32 score of a row over every kFilterSeedStep-th vector (6 % of the scan's
 // work). Any real score is a lower bound of the final maximum, so starting from it is as exact as starting from zero,
 // and with it only the handful of vectors that beat the subsample's best ever become candidates (a scan that starts
@@ -237,8 +254,10 @@ __global__ void __launch_bounds__(kFilterThreads) filter_seed_kernel(const doubl
     constexpr int SS = (MM + 3) / 4 * 4;
     const int stride = M > 0 ? SS : (int)v32_stride(m);
     extern __shared__ __align__(16) float s_v32[];  // kFilterTile subsampled unit vectors
+    constexpr int KP = (MM + 1) / 2;  // component pairs
     uint32_t row[R];
     float uf[R][MM], best[R];
+    uint64_t uf2[R][KP];
 #pragma unroll
     for (int t = 0; t < R; ++t) {
         row[t] = (uint32_t)(blockIdx.x * (uint64_t)(R * kFilterThreads) + t * kFilterThreads + threadIdx.x);
@@ -253,6 +272,8 @@ __global__ void __launch_bounds__(kFilterThreads) filter_seed_kernel(const doubl
         const double nf = !live ? 0.0 : (SELF ? vn[row[t]] : sqrt(s));
 #pragma unroll
         for (int k = 0; k < MM; ++k) uf[t][k] = (float)((k < m && nf != 0.0) ? fp[k] / nf : 0.0);  // the scan's own conversion
+#pragma unroll
+        for (int p = 0; p < KP; ++p) uf2[t][p] = pack2(uf[t][2 * p], 2 * p + 1 < MM ? uf[t][2 * p + 1 < MM ? 2 * p + 1 : 0] : 0.0f);
         best[t] = 0.0f;
     }
     const uint64_t n_sub = (r + kFilterSeedStep - 1) / kFilterSeedStep;  // vectors 0, 16, 32, ...
@@ -266,23 +287,28 @@ __global__ void __launch_bounds__(kFilterThreads) filter_seed_kernel(const doubl
         __syncthreads();
 #pragma unroll 2
         for (int jj = 0; jj < tile; ++jj) {
-            float vr[SS];
-            const float4* p4 = reinterpret_cast<const float4*>(s_v32 + jj * stride);
+            // packed multiply-adds, component pairs side by side (like the scan)
+            const ulonglong2* p2 = reinterpret_cast<const ulonglong2*>(s_v32 + jj * stride);
+            uint64_t vp[KP];
 #pragma unroll
             for (int k4 = 0; k4 < SS / 4; ++k4)
                 if (4 * k4 < m) {
-                    const float4 t4 = p4[k4];
-                    vr[4 * k4] = t4.x, vr[4 * k4 + 1] = t4.y, vr[4 * k4 + 2] = t4.z, vr[4 * k4 + 3] = t4.w;
+                    const ulonglong2 t2 = p2[k4];
+                    vp[2 * k4] = t2.x;
+                    if (2 * k4 + 1 < KP) vp[2 * k4 + 1 < KP ? 2 * k4 + 1 : 0] = t2.y;
+                }
+            uint64_t acc[R];
+#pragma unroll
+            for (int t = 0; t < R; ++t) acc[t] = 0ull;
+#pragma unroll
+            for (int p = 0; p < KP; ++p)
+                if (2 * p < m) {
+#pragma unroll
+                    for (int t = 0; t < R; ++t) acc[t] = ffma2(uf2[t][p], vp[p], acc[t]);
                 }
             float sc[R];
 #pragma unroll
-            for (int t = 0; t < R; ++t) sc[t] = 0.0f;
-#pragma unroll
-            for (int k = 0; k < MM; ++k)
-                if (k < m) {
-#pragma unroll
-                    for (int t = 0; t < R; ++t) sc[t] = fmaf(uf[t][k], vr[k], sc[t]);
-                }
+            for (int t = 0; t < R; ++t) sc[t] = sum2(acc[t]);
             const uint32_t j = (uint32_t)((q0 + jj) * kFilterSeedStep);
 #pragma unroll
             for (int t = 0; t < R; ++t)
@@ -297,23 +323,6 @@ __global__ void __launch_bounds__(kFilterThreads) filter_seed_kernel(const doubl
 // Candidates of a row: vectors whose fp32 score reached the row's running threshold. Their exact evaluation is deferred
 // to the end of the scan - the threshold only depends on the fp32 scores - when most of them have fallen below the final
 // threshold and are dropped: a few exact evaluations per row remain instead of one per running-maximum record.
-// packed fp32 pairs (sm_100: FFMA2)
-__device__ __forceinline__ uint64_t pack2(float a, float b) {
-    uint64_t r;
-    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
-    return r;
-}
-__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
-    uint64_t d;
-    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
-    return d;
-}
-__device__ __forceinline__ float sum2(uint64_t a) {
-    float x, y;
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(x), "=f"(y) : "l"(a));
-    return x + y;
-}
-
 constexpr int kFilterCand = 6;  // candidate slots per row (pruned against the risen threshold when full)
 constexpr int kFallbackItems = 8192;  // (row, vector range) items the fallback spreads its rows over (when there are fewer rows)
 
