@@ -386,10 +386,13 @@ __device__ __forceinline__ void search_row(const IndexView& ix, const Row<M>& ro
 #define TEMO_INDEX_WARPS 4
 #endif
 constexpr int kWarpsPerCta = TEMO_INDEX_WARPS;
+#ifndef TEMO_INDEX_MIN_CTAS
+#define TEMO_INDEX_MIN_CTAS 8
+#endif
 
 // Association + APD for the merged objective rows (selection.hpp:148-192), one warp per row.
 template <int M>
-__global__ void __launch_bounds__(kWarpsPerCta * 32) assoc_indexed_kernel(
+__global__ void __launch_bounds__(kWarpsPerCta * 32, TEMO_INDEX_MIN_CTAS) assoc_indexed_kernel(
     const double* __restrict__ f, uint64_t n_rows, const uint32_t* n_rows_dev, uint64_t m_rt,
     const double* __restrict__ z, const IndexView ix, const uint32_t* __restrict__ vflags, const double* __restrict__ gamma,
     double penalty, uint32_t* __restrict__ assoc, double* __restrict__ theta_out, double* __restrict__ apd_out,
@@ -437,7 +440,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) assoc_indexed_kernel(
 
 // gamma_i = acos(max_{j != i} cos(v_i, v_j)) (refvec.hpp:81-100), one warp per vector.
 template <int M>
-__global__ void __launch_bounds__(kWarpsPerCta * 32) gamma_indexed_kernel(
+__global__ void __launch_bounds__(kWarpsPerCta * 32, TEMO_INDEX_MIN_CTAS) gamma_indexed_kernel(
     const double* __restrict__ v, const double* __restrict__ vn, uint64_t r, uint64_t m_rt, const IndexView ix,
     const uint32_t* __restrict__ vflags, double* __restrict__ gamma, uint32_t* err_flag, const uint32_t* skip_flag) {
     if (skip_flag && *skip_flag) return;
