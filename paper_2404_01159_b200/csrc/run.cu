@@ -150,7 +150,7 @@ Run::Run(const RunConfig& c) : cfg(c) {
     }
     used = dev_alloc<unsigned char>(cap);
     d_P = dev_alloc<uint32_t>(1);
-    free_scratch = dev_alloc<uint32_t>((cap + kCompactTile - 1) / kCompactTile + 1);
+    free_scratch = compact_state_alloc(cap);
     v0 = dev_alloc<double>(r * m);
     v = dev_alloc<double>(r * m);
     gamma = dev_alloc<double>(r);
@@ -673,7 +673,7 @@ void Run::archive_reserve(uint64_t rows) {
     cudaFree(arch_keep); cudaFree(arch_list); cudaFree(arch_scratch);
     arch_keep = dev_alloc<unsigned char>(want);
     arch_list = dev_alloc<uint32_t>(want);
-    arch_scratch = dev_alloc<uint32_t>((want + kCompactTile - 1) / kCompactTile + 1);
+    arch_scratch = compact_state_alloc(want);
     if (!arch_count) arch_count = dev_alloc<uint32_t>(2);
     arch_capacity = want;
 }

@@ -779,7 +779,7 @@ void SelectWorkspace::alloc(uint64_t rows_cap_, uint64_t r_, uint64_t m_) {
     valid = dev_alloc<unsigned char>(r);
     n_elite = dev_alloc<uint32_t>(1);
     err_flag = dev_alloc<uint32_t>(1);
-    tile_scratch = dev_alloc<uint32_t>((r + kCompactTile - 1) / kCompactTile + 1);
+    tile_scratch = compact_state_alloc(r);
     v32 = dev_alloc<float>(r * v32_stride(m));
     v32_flags = dev_alloc<uint32_t>(1);
     if (assoc_filter_preferred(m, r)) {

@@ -209,7 +209,7 @@ struct Shard {
         free_slot = dev_alloc<uint32_t>(n_loc);
         free_all = dev_alloc<uint32_t>((uint64_t)world * n_loc);
         used = dev_alloc<unsigned char>(cap_loc);
-        free_scratch = dev_alloc<uint32_t>((cap_loc + kCompactTile - 1) / kCompactTile + 1);
+        free_scratch = compact_state_alloc(cap_loc);
         for (int b = 0; b < 2; ++b) {
             owner[b] = dev_alloc<uint32_t>(pcap);
             slot[b] = dev_alloc<uint32_t>(pcap);
