@@ -158,7 +158,7 @@ Run::Run(const RunConfig& c) : cfg(c) {
     upper = dev_alloc<double>(d);
     zmin = dev_alloc<double>(m);
     zmax = dev_alloc<double>(m);
-    zscratch = dev_alloc<unsigned long long>(2 * m);
+    zscratch = dev_alloc<unsigned long long>(2 * m + 1);
     skip_flag = dev_alloc<uint32_t>(1);
     TEMO_CUDA(cudaMallocHost(&h_status, 4 * sizeof(uint32_t)));
     ws.alloc(cap, r, m);

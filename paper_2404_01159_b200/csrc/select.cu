@@ -31,9 +31,12 @@ __device__ __forceinline__ double key_value(unsigned long long k) {
 constexpr unsigned long long kKeyMax = 0xffffffffffffffffULL;
 
 // ---- ideal point: column minima (tensor.hpp:211-219) --------------------------------------------
-// grid (blocks, m): block-strided rows of one column; NaNs never win (strict <).
+// grid (blocks, m): block-strided rows of one column; NaNs never win (strict <). The last CTA to finish decodes the keys
+// (a NaN in row 0 sticks: the reference seeds the scan with row 0 and a NaN never compares smaller / greater) and clears
+// the ticket. Scratch layout: m minimum keys, m maximum keys, one ticket word (col_minmax_scratch_words).
 __global__ void colmin_kernel(const double* f, uint64_t n_rows, const uint32_t* n_rows_dev, uint64_t m,
-                              unsigned long long* zkey_min, unsigned long long* zkey_max) {
+                              unsigned long long* zkey_min, unsigned long long* zkey_max, unsigned long long* ticket,
+                              bool want_max, double* zmin, double* zmax) {
     const uint64_t n = n_rows_dev ? (uint64_t)*n_rows_dev : n_rows;
     const uint64_t j = blockIdx.y;
     unsigned long long kmin = kKeyMax, kmax = 0ULL;
@@ -55,19 +58,41 @@ __global__ void colmin_kernel(const double* f, uint64_t n_rows, const uint32_t* 
     }
     if ((threadIdx.x & 31) == 0) {
         if (kmin != kKeyMax) atomicMin(&zkey_min[j], kmin);
-        if (zkey_max && kmax != 0ULL) atomicMax(&zkey_max[j], kmax);
+        if (want_max && kmax != 0ULL) atomicMax(&zkey_max[j], kmax);
     }
+    __shared__ bool s_last;
+    __syncthreads();  // this CTA's atomics are issued
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(ticket, 1ULL) == (unsigned long long)gridDim.x * gridDim.y - 1;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    if (threadIdx.x < m) {
+        const uint64_t c = threadIdx.x;
+        const double first = f[c];
+        if (zmin) zmin[c] = (first != first) ? first : key_value(*reinterpret_cast<volatile unsigned long long*>(&zkey_min[c]));
+        if (zmax) zmax[c] = (first != first) ? first : key_value(*reinterpret_cast<volatile unsigned long long*>(&zkey_max[c]));
+    }
+    if (threadIdx.x == 0) *ticket = 0ULL;
 }
 
-// Decodes the keys; a NaN in row 0 sticks (the reference seeds the scan with row 0 and a NaN
-// never compares smaller/greater).
-__global__ void colmin_finish_kernel(const double* f, uint64_t m, const unsigned long long* zkey_min,
-                                     const unsigned long long* zkey_max, double* zmin, double* zmax) {
-    const uint64_t j = threadIdx.x;
-    if (j >= m) return;
-    const double first = f[j];
-    if (zmin) zmin[j] = (first != first) ? first : key_value(zkey_min[j]);
-    if (zmax) zmax[j] = (first != first) ? first : key_value(zkey_max[j]);
+// Start of a selection in one launch: gamma > 0 (selection.hpp:152), the per-vector minima reset, the column-key scratch reset.
+__global__ void select_init_kernel(const double* gamma, uint64_t r, uint64_t m, uint32_t* err_flag, unsigned long long* best_key,
+                                   uint32_t* best_row, uint32_t* first_row, unsigned long long* zkey) {
+    const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (j < r) {
+        if (!(gamma[j] > 0.0)) atomicOr(err_flag, 1u);
+        best_key[j] = kKeyMax;
+        best_row[j] = 0xffffffffu;
+        first_row[j] = 0xffffffffu;
+    }
+    if (j < m) {
+        zkey[j] = kKeyMax;
+        zkey[m + j] = 0ULL;
+    }
+    if (j == 0) zkey[2 * m] = 0ULL;
 }
 
 __global__ void row_norms_kernel(const double* v, uint64_t r, uint64_t m, double* vn) {
@@ -78,10 +103,6 @@ __global__ void row_norms_kernel(const double* v, uint64_t r, uint64_t m, double
     vn[j] = sqrt(s);
 }
 
-__global__ void gamma_check_kernel(const double* gamma, uint64_t r, uint32_t* err_flag) {
-    const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    if (j < r && !(gamma[j] > 0.0)) atomicOr(err_flag, 1u);  // selection.hpp:152
-}
 
 // ---- association + APD ------------------------------------------------------------------------------
 constexpr int kAssocThreads = 128;
@@ -718,9 +739,14 @@ __global__ void elite_rows_kernel(uint64_t n_rows, const uint32_t* n_rows_dev, c
 }
 
 // validity + the elite of every valid vector (selection.hpp:209-217); compaction in ascending j follows
-struct ElitePred {
+struct ElitePred {  // also records the validity of the vector (the compaction asks once per element)
     const uint32_t* first_row;
-    __device__ bool operator()(uint64_t j) const { return first_row[j] != 0xffffffffu; }
+    unsigned char* valid;
+    __device__ bool operator()(uint64_t j) const {
+        const bool v = first_row[j] != 0xffffffffu;
+        valid[j] = v ? 1 : 0;
+        return v;
+    }
 };
 struct EliteValPlain {  // sharded runs: objectives are finite, the NaN rule cannot trigger
     const uint32_t* best_row;
@@ -737,10 +763,6 @@ struct EliteVal {
         return (a0 != a0) ? fr : best_row[j];
     }
 };
-__global__ void validity_kernel(const uint32_t* first_row, uint64_t r, unsigned char* valid) {
-    const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    if (j < r) valid[j] = first_row[j] != 0xffffffffu ? 1 : 0;
-}
 
 template <int M>
 void launch_assoc(const double* f, uint64_t n_rows, const uint32_t* n_rows_dev, uint64_t m,
@@ -767,7 +789,7 @@ void SelectWorkspace::alloc(uint64_t rows_cap_, uint64_t r_, uint64_t m_) {
     r = r_;
     m = m_;
     z = dev_alloc<double>(m);
-    zkey = dev_alloc<unsigned long long>(2 * m);
+    zkey = dev_alloc<unsigned long long>(2 * m + 1);
     vn = dev_alloc<double>(r);
     assoc = dev_alloc<uint32_t>(rows_cap);
     theta = dev_alloc<double>(rows_cap);
@@ -811,13 +833,12 @@ void launch_row_norms(const double* v, uint64_t r, uint64_t m, double* vn, cudaS
 void launch_col_minmax(const double* f, uint64_t n_rows, const uint32_t* n_rows_dev, uint64_t m,
                        double* zmin, double* zmax, unsigned long long* scratch2m, cudaStream_t s) {
     TEMO_CUDA(cudaMemsetAsync(scratch2m, 0xff, m * sizeof(unsigned long long), s));
-    TEMO_CUDA(cudaMemsetAsync(scratch2m + m, 0x00, m * sizeof(unsigned long long), s));
+    TEMO_CUDA(cudaMemsetAsync(scratch2m + m, 0x00, (m + 1) * sizeof(unsigned long long), s));  // maxima and the ticket
     uint64_t blocks = (n_rows + 255) / 256;
     if (blocks > (uint64_t)kSMs * 4) blocks = (uint64_t)kSMs * 4;
     if (blocks < 1) blocks = 1;
-    colmin_kernel<<<dim3((unsigned)blocks, (unsigned)m), 256, 0, s>>>(f, n_rows, n_rows_dev, m, scratch2m,
-                                                                     zmax ? scratch2m + m : nullptr);
-    colmin_finish_kernel<<<1, 32, 0, s>>>(f, m, scratch2m, scratch2m + m, zmin, zmax);
+    colmin_kernel<<<dim3((unsigned)blocks, (unsigned)m), 256, 0, s>>>(f, n_rows, n_rows_dev, m, scratch2m, scratch2m + m,
+                                                                     scratch2m + 2 * m, zmax != nullptr, zmin, zmax);
     TEMO_CUDA(cudaGetLastError());
 }
 
@@ -827,11 +848,14 @@ void launch_select_prepare(const double* f, uint64_t n_rows, uint64_t m, const d
     require(m >= 1 && m <= (uint64_t)kMaxObj, "rv_select: unsupported objective count");
     require(n_rows <= ws.rows_cap && r <= ws.r, "rv_select: workspace too small");
     require(n_rows < 0xffffffffULL && r < 0xffffffffULL, "rv_select: index range");
-    gamma_check_kernel<<<(unsigned)((r + 255) / 256), 256, 0, s>>>(gamma, r, ws.err_flag);
-    launch_col_minmax(f, n_rows, nullptr, m, ws.z, nullptr, ws.zkey, s);
-    TEMO_CUDA(cudaMemsetAsync(ws.best_key, 0xff, r * sizeof(unsigned long long), s));
-    TEMO_CUDA(cudaMemsetAsync(ws.best_row, 0xff, r * sizeof(uint32_t), s));
-    TEMO_CUDA(cudaMemsetAsync(ws.first_row, 0xff, r * sizeof(uint32_t), s));
+    // one launch for the resets (a small population's selection is a chain of few-microsecond operations), one for the ideal point
+    select_init_kernel<<<(unsigned)((std::max<uint64_t>(r, m) + 255) / 256), 256, 0, s>>>(gamma, r, m, ws.err_flag, ws.best_key,
+                                                                                       ws.best_row, ws.first_row, ws.zkey);
+    uint64_t blocks = (n_rows + 255) / 256;
+    if (blocks > (uint64_t)kSMs * 4) blocks = (uint64_t)kSMs * 4;
+    colmin_kernel<<<dim3((unsigned)blocks, (unsigned)m), 256, 0, s>>>(f, n_rows, nullptr, m, ws.zkey, ws.zkey + m, ws.zkey + 2 * m,
+                                                                     false, ws.z, nullptr);
+    TEMO_CUDA(cudaGetLastError());
 }
 
 void launch_elite_rows(uint64_t n_rows, const uint32_t* assoc, const double* apd, const unsigned long long* best_key,
@@ -841,12 +865,11 @@ void launch_elite_rows(uint64_t n_rows, const uint32_t* assoc, const double* apd
 }
 
 void launch_select_finish(uint64_t r, SelectWorkspace& ws, bool nan_rule, cudaStream_t s) {
-    validity_kernel<<<(unsigned)((r + 255) / 256), 256, 0, s>>>(ws.first_row, r, ws.valid);
     if (nan_rule)
-        launch_compact(r, ElitePred{ws.first_row}, EliteVal{ws.apd, ws.first_row, ws.best_row}, ws.tile_scratch, r, ws.elite,
+        launch_compact(r, ElitePred{ws.first_row, ws.valid}, EliteVal{ws.apd, ws.first_row, ws.best_row}, ws.tile_scratch, r, ws.elite,
                        ws.n_elite, s);
     else
-        launch_compact(r, ElitePred{ws.first_row}, EliteValPlain{ws.best_row}, ws.tile_scratch, r, ws.elite, ws.n_elite, s);
+        launch_compact(r, ElitePred{ws.first_row, ws.valid}, EliteValPlain{ws.best_row}, ws.tile_scratch, r, ws.elite, ws.n_elite, s);
     TEMO_CUDA(cudaGetLastError());
 }
 

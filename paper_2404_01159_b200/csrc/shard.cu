@@ -227,7 +227,7 @@ struct Shard {
         upper = dev_alloc<double>(d);
         zmin = dev_alloc<double>(m);
         zmax = dev_alloc<double>(m);
-        zscratch = dev_alloc<unsigned long long>(2 * m);
+        zscratch = dev_alloc<unsigned long long>(2 * m + 1);
         skip_flag = dev_alloc<uint32_t>(1);
         d_P = dev_alloc<uint32_t>(2);
         ws.alloc(pcap + n, r, m);
