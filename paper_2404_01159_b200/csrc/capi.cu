@@ -853,7 +853,12 @@ int temo_b200_hv_mc(const double* f, uint64_t n, uint64_t m, const double* ref, 
         require(m >= 1 && m <= (uint64_t)kMaxObj, "hv_mc: unsupported objective count");
         cudaStream_t s = ctx().stream;
         DevBuf<double> df(f, n * m, s), dl(m), dr(ref, m, s);
-        DevBuf<unsigned long long> hits(1), scratch(2 * m + 1);
+        DevBuf<unsigned long long> hits(1);
+        struct KeyScratch {
+            unsigned long long* p;
+            explicit KeyScratch(uint64_t mm) : p(col_minmax_scratch_alloc(mm)) {}
+            ~KeyScratch() { cudaFree(p); }
+        } scratch(m);
         launch_col_minmax(df.p, n, nullptr, m, dl.p, nullptr, scratch.p, s);
         double lo[kMaxObj];
         dl.to_host(lo, s);

@@ -197,9 +197,11 @@ void launch_gamma(const double* v, const double* vn, uint64_t r, uint64_t m, dou
                   uint32_t* err_flag, const uint32_t* skip_flag, cudaStream_t s);
 // zmin/zmax over rows [0, n_rows) of f (tensor.hpp:211-229).
 void launch_col_minmax(const double* f, uint64_t n_rows, const uint32_t* n_rows_dev, uint64_t m,
-                       double* zmin, double* zmax, unsigned long long* scratch2m /* 2 m + 1 words */, cudaStream_t s);
+                       double* zmin, double* zmax, unsigned long long* scratch2m /* col_minmax_scratch_alloc(m) */, cudaStream_t s);
+unsigned long long* col_minmax_scratch_alloc(uint64_t m);
 // adapt_vectors (refvec.hpp:119-131): v = unit(v0 * (zmax - zmin)); skip_flag[0] is set to 1
 // (and v left untouched) unless every range is > 0; err bit1 on a zero row.
+void preload_adapt_kernels();
 void launch_adapt_vectors(const double* v0, double* v, double* vn, uint64_t r, uint64_t m,
                           const double* zmin, const double* zmax, uint32_t* skip_flag,
                           uint32_t* err_flag, cudaStream_t s);

@@ -131,6 +131,13 @@ void launch_gamma(const double* v, const double* vn, uint64_t r, uint64_t m, dou
     TEMO_CUDA(cudaGetLastError());
 }
 
+// Loads the kernels a run first needs at its first adaptation (lazy module loading would do it there, see init_context).
+void preload_adapt_kernels() {
+    cudaFuncAttributes attr;
+    TEMO_CUDA(cudaFuncGetAttributes(&attr, adapt_gate_kernel));
+    TEMO_CUDA(cudaFuncGetAttributes(&attr, adapt_vectors_kernel));
+}
+
 void launch_adapt_vectors(const double* v0, double* v, double* vn, uint64_t r, uint64_t m,
                           const double* zmin, const double* zmax, uint32_t* skip_flag,
                           uint32_t* err_flag, cudaStream_t s) {

@@ -106,6 +106,7 @@ Run::Run(const RunConfig& c) : cfg(c) {
     require(cfg.obj >= 2 && cfg.obj <= (uint64_t)kMaxObj, "rvea_run: objective count out of range");
     require(cfg.op >= kOpGa && cfg.op <= kOpRandom, "rvea_run: unknown operator");  // algorithms.hpp:270
     if (cfg.op == kOpDe) require(cfg.pop >= 4, "de_reproduce: needs at least four rows");
+    preload_adapt_kernels();  // first used at the first adaptation: not in the middle of the loop
     n = cfg.pop;
     m = cfg.obj;
     if (cfg.problem == kToy2 || cfg.problem == kToy3) {  // problems.hpp:279-287: the environment fixes m and d
@@ -158,7 +159,7 @@ Run::Run(const RunConfig& c) : cfg(c) {
     upper = dev_alloc<double>(d);
     zmin = dev_alloc<double>(m);
     zmax = dev_alloc<double>(m);
-    zscratch = dev_alloc<unsigned long long>(2 * m + 1);
+    zscratch = col_minmax_scratch_alloc(m);
     skip_flag = dev_alloc<uint32_t>(1);
     TEMO_CUDA(cudaMallocHost(&h_status, 4 * sizeof(uint32_t)));
     ws.alloc(cap, r, m);

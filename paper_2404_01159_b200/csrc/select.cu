@@ -74,6 +74,8 @@ __global__ void colmin_kernel(const double* f, uint64_t n_rows, const uint32_t* 
         const double first = f[c];
         if (zmin) zmin[c] = (first != first) ? first : key_value(*reinterpret_cast<volatile unsigned long long*>(&zkey_min[c]));
         if (zmax) zmax[c] = (first != first) ? first : key_value(*reinterpret_cast<volatile unsigned long long*>(&zkey_max[c]));
+        zkey_min[c] = kKeyMax;  // the scratch is left as it was found: no reset launch (or memset) per call
+        zkey_max[c] = 0ULL;
     }
     if (threadIdx.x == 0) *ticket = 0ULL;
 }
@@ -789,7 +791,7 @@ void SelectWorkspace::alloc(uint64_t rows_cap_, uint64_t r_, uint64_t m_) {
     r = r_;
     m = m_;
     z = dev_alloc<double>(m);
-    zkey = dev_alloc<unsigned long long>(2 * m + 1);
+    zkey = col_minmax_scratch_alloc(m);
     vn = dev_alloc<double>(r);
     assoc = dev_alloc<uint32_t>(rows_cap);
     theta = dev_alloc<double>(rows_cap);
@@ -830,10 +832,16 @@ void launch_row_norms(const double* v, uint64_t r, uint64_t m, double* vn, cudaS
     TEMO_CUDA(cudaGetLastError());
 }
 
+// scratch of launch_col_minmax: m minimum keys (all ones), m maximum keys (zero), a ticket (zero); the kernel restores it
+unsigned long long* col_minmax_scratch_alloc(uint64_t m) {
+    unsigned long long* p = dev_alloc<unsigned long long>(2 * m + 1);
+    TEMO_CUDA(cudaMemset(p, 0xff, m * sizeof(unsigned long long)));
+    TEMO_CUDA(cudaMemset(p + m, 0x00, (m + 1) * sizeof(unsigned long long)));
+    return p;
+}
+
 void launch_col_minmax(const double* f, uint64_t n_rows, const uint32_t* n_rows_dev, uint64_t m,
                        double* zmin, double* zmax, unsigned long long* scratch2m, cudaStream_t s) {
-    TEMO_CUDA(cudaMemsetAsync(scratch2m, 0xff, m * sizeof(unsigned long long), s));
-    TEMO_CUDA(cudaMemsetAsync(scratch2m + m, 0x00, (m + 1) * sizeof(unsigned long long), s));  // maxima and the ticket
     uint64_t blocks = (n_rows + 255) / 256;
     if (blocks > (uint64_t)kSMs * 4) blocks = (uint64_t)kSMs * 4;
     if (blocks < 1) blocks = 1;

@@ -178,6 +178,7 @@ struct Shard {
     uint64_t launches = 0;                   // kernels + copies enqueued by this shard so far
 
     Shard(const RunConfig& c, int rank_, int world_) : cfg(c), rank(rank_), world(world_) {
+        preload_adapt_kernels();  // first used at the first adaptation: not in the middle of the loop
         require(world >= 1 && rank >= 0 && rank < world, "shard: bad rank");
         require(problem_known(cfg.problem), "make_problem: unknown problem");
         require(cfg.op == kOpGa, "shard: the sharded loop runs the ga operator");
@@ -227,7 +228,7 @@ struct Shard {
         upper = dev_alloc<double>(d);
         zmin = dev_alloc<double>(m);
         zmax = dev_alloc<double>(m);
-        zscratch = dev_alloc<unsigned long long>(2 * m + 1);
+        zscratch = col_minmax_scratch_alloc(m);
         skip_flag = dev_alloc<uint32_t>(1);
         d_P = dev_alloc<uint32_t>(2);
         ws.alloc(pcap + n, r, m);
