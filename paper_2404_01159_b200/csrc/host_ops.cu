@@ -127,9 +127,10 @@ void init_context(int device) {
     std::lock_guard<std::mutex> lock(g_ctx_mutex);
     if (g_ctx.device == device && g_ctx.stream) return;
     // Kernels that a run launches for the first time in the middle of its loop (the first adaptation of the reference
-    // vectors) would otherwise be loaded there: 0.4 ... 13 ms measured for two small kernels, inside somebody's timed
-    // region. Has an effect only if this is the process' first CUDA call (preload_adapt_kernels covers the other case).
-    setenv("CUDA_MODULE_LOADING", "EAGER", 0);
+    // vectors) would be loaded there under CUDA's lazy module loading: 0.4 ... 13 ms measured for two small kernels, inside
+    // somebody's timed region. A run loads them at creation (preload_adapt_kernels); TEMO_B200_EAGER_MODULES=1 asks for eager
+    // loading of everything instead (process-wide, and only if this is the process' first CUDA call).
+    if (getenv("TEMO_B200_EAGER_MODULES")) setenv("CUDA_MODULE_LOADING", "EAGER", 0);
     int count = 0;
     const cudaError_t e = cudaGetDeviceCount(&count);
     if (e != cudaSuccess || count == 0)
