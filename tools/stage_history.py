@@ -1,5 +1,8 @@
-import sys, os
-sys.path.insert(0, "/root/repo")
+"""Developer tool: per-step stage times of a short headline run (first-use hiccups, adaptation steps)."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2404_01159_b200 as tb
 tb.init(0)
 cfg = tb.RunConfig(problem="dtlz2", pop=1 << 17, dim=5000, obj=3, generations=100, seed=42)
