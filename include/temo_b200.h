@@ -369,6 +369,8 @@ int temo_b200_flush_l2(void);
  * "k1_dynamic_pairs" 1/0 hands the mating pairs to the persistent teams through a global counter (default) or
  * round-robin over the grid; "k1_single_warp" -1 gives a mating pair to one warp when the launch has a pair for every
  * resident warp and to a team of eight warps otherwise (default), 0 always teams, 1 always single warps;
+ * "k1_nested_bounds" 1/0 sends two nested bound segments (LSMOP) through the one-segment kernel plus a fix-up of the row's
+ * first genes (default) or selects the bounds per gene;
  * "eval_tma" 1/0 evaluates through the bulk-copy kernels (default) or the one-CTA-per-row kernels.
  * Returns TEMO_B200_EINVAL for an unknown name. */
 int temo_b200_set_option(const char* name, long value);

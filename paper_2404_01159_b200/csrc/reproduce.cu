@@ -59,6 +59,11 @@ struct ReproK {
     const double* upper;
     uint32_t seg_split;          // pair kernel, SEG variant: genes < seg_split have bounds [0], the others [1]
     double seg_lo[2], seg_hi[2];
+    // SEG == 1 standing in for two NESTED segments (LSMOP: [0, 1] for the first m - 1 genes inside [0, 10]): pass C clamps
+    // every gene to the outer box and the genes below fix_split (all in a row's first block) are clamped again to the inner
+    // one afterwards - clamp(clamp(x, outer), inner) = clamp(x, inner) bit for bit. 0: nothing to fix.
+    uint32_t fix_split;
+    double fix_lo, fix_hi;
     uint64_t m;
     double* f_out;
     uint64_t f_row0;
@@ -889,6 +894,14 @@ __global__ void __launch_bounds__((TEAM == 1 ? kSoloWarps : kVirtWarps) * 32, TE
                             block(k + 2, a2, b2);
                         }
                     }
+                    if (SEG == 1 && EVAL == 0 && a.fix_split && blk0 == 0 && 2 * lane < a.fix_split) {
+                        // the row's first genes belong to the inner box: this lane's own stores of block 0, clamped again
+                        double2 ca = oa2[lane], cb = ob2[lane];
+                        ca.x = clampd(ca.x, a.fix_lo, a.fix_hi), cb.x = clampd(cb.x, a.fix_lo, a.fix_hi);
+                        if (2 * lane + 1 < a.fix_split) ca.y = clampd(ca.y, a.fix_lo, a.fix_hi), cb.y = clampd(cb.y, a.fix_lo, a.fix_hi);
+                        oa2[lane] = ca;
+                        ob2[lane] = cb;
+                    }
                 }
             }
             __syncwarp();
@@ -983,6 +996,7 @@ struct K1Options {
     int dynamic_pairs;  // pair kernel: pairs handed out through a global counter (1, default) or round-robin (0)
     int single_warp;    // pair kernel, one warp per pair: -1 when the launch has a pair for every resident warp (default), 0 never
                         // (teams of eight warps), 1 always
+    int nested_bounds;  // two nested bound segments through the one-segment kernel + fix-up (1, default) or per-gene selects (0)
 };
 inline int env_int(const char* name, int dflt) {
     const char* e = getenv(name);
@@ -991,7 +1005,8 @@ inline int env_int(const char* name, int dflt) {
 inline K1Options& k1_options() {
     static K1Options o{env_int("TEMO_B200_GENERIC_K1", 0), env_int("TEMO_B200_K1_BOUND_ARRAYS", 0),
                        std::max(0, std::min(kPairCand, env_int("TEMO_B200_K1_CAND_CAP", kPairCand))),
-                       env_int("TEMO_B200_K1_DYNAMIC_PAIRS", 1), env_int("TEMO_B200_K1_SINGLE_WARP", -1)};
+                       env_int("TEMO_B200_K1_DYNAMIC_PAIRS", 1), env_int("TEMO_B200_K1_SINGLE_WARP", -1),
+                       env_int("TEMO_B200_K1_NESTED_BOUNDS", 1)};
     return o;
 }
 inline bool force_generic_kernel() { return k1_options().generic != 0; }
@@ -1131,6 +1146,8 @@ __global__ void pow_batch_kernel(const double* x, const double* y, uint64_t n, d
 //                    kernel, 0..kPairCand (0 forces its plain-tile path)  TEMO_B200_K1_CAND_CAP
 //   k1_single_warp   pair kernel with one warp per pair: -1 when the launch
 //                    has a pair per resident warp, 0 never, 1 always      TEMO_B200_K1_SINGLE_WARP
+//   k1_nested_bounds 1: two nested bound segments go through the
+//                    one-segment kernel + fix-up, 0: per-gene selects     TEMO_B200_K1_NESTED_BOUNDS
 inline unsigned stream_grid(uint64_t total, int block) {
     uint64_t g = (total + block - 1) / block;
     const uint64_t cap = (uint64_t)kSMs * 16;
@@ -1232,6 +1249,16 @@ void launch_reproduce(const ReproArgs& a, cudaStream_t s) {
                 const int from = seg == 1 ? (a.seg.split == 0 ? 1 : 0) : i;  // one segment: both entries hold it
                 k.seg_lo[i] = a.seg.lo[from], k.seg_hi[i] = a.seg.hi[from];
             }
+            // two nested segments whose split lies in the first block, no fused sums: the one-segment kernel + a fix-up
+            if (seg == 2 && a.eval_problem == 0 && a.seg.split <= 64 && a.seg.lo[0] >= a.seg.lo[1] && a.seg.hi[0] <= a.seg.hi[1] &&
+                k1_options().nested_bounds) {
+                seg = 1;
+                k.fix_split = (uint32_t)a.seg.split;
+                k.fix_lo = a.seg.lo[0], k.fix_hi = a.seg.hi[0];
+                k.seg_lo[0] = k.seg_lo[1] = a.seg.lo[1];
+                k.seg_hi[0] = k.seg_hi[1] = a.seg.hi[1];
+                k.seg_split = 0;
+            }
         }
         k.unit0 = unit_lo;
         k.unit_end = std::min(unit_hi, k.half);
@@ -1276,6 +1303,7 @@ bool set_k1_option(const char* name, long value) {
     else if (key == "k1_cand_cap") o.cand_cap = (int)std::max(0L, std::min((long)kPairCand, value));
     else if (key == "k1_dynamic_pairs") o.dynamic_pairs = value != 0;
     else if (key == "k1_single_warp") o.single_warp = value < 0 ? -1 : (value != 0);
+    else if (key == "k1_nested_bounds") o.nested_bounds = value != 0;
     else return false;
     return true;
 }

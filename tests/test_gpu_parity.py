@@ -176,6 +176,7 @@ def k1_options(tb):
     tb.set_option("k1_cand_cap", 8)
     tb.set_option("k1_dynamic_pairs", 1)
     tb.set_option("k1_single_warp", -1)
+    tb.set_option("k1_nested_bounds", 1)
 
 
 @pytest.mark.parametrize("shape", [(16, 512), (12, 5120), (6, 5122), (6, 10240), (5, 20000), (9, 2002)])
@@ -205,10 +206,16 @@ def test_pair_kernel_bound_segments(tb, oracle, k1_options, split):
     x, _ = oracle.random_reproduce(n, d, 5, 0, lo, hi)
     exp, _ = oracle.ga_reproduce(x, 9, 0, lo, hi)
     got = {}
-    for arrays in (0, 1):
+    # bound arrays; launch constants with per-gene selects; nested segments (the first inside the second, split in the first
+    # block) through the one-segment kernel with the fix-up of the row's first genes; the same with one warp per pair
+    for arrays, nested, solo in ((0, 1, -1), (0, 0, -1), (1, 1, -1), (0, 1, 1), (0, 0, 1)):
         k1_options("k1_bound_arrays", arrays)
+        k1_options("k1_nested_bounds", nested)
+        k1_options("k1_single_warp", solo)
         got[arrays] = tb.ga_reproduce(x, tb.RngStream(9, 0), tb.GaParams(), lo, hi)
-        assert np.array_equal(got[arrays], exp), (arrays, ulp_diff(got[arrays], exp).max())
+        assert np.array_equal(got[arrays], exp), (arrays, nested, solo, ulp_diff(got[arrays], exp).max())
+    k1_options("k1_single_warp", -1)
+    k1_options("k1_nested_bounds", 1)
     # three segments: not representable, must silently stay on the arrays
     lo[d // 3:d // 2] = -5.0
     x3, _ = oracle.random_reproduce(n, d, 6, 0, lo, hi)
